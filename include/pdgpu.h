@@ -1,0 +1,162 @@
+/*
+ * pdgpu.h -- C ABI of the B200 MSBFM engine (libpdgpu.so).
+ *
+ * Drop-in boundary for the reference library `pdfast` (header-only C++20,
+ * proj/include/pdfast/).  Every entry point names the reference interface it
+ * replaces as <file>:<line>.  Plain pointers and sizes only; no CUDA or torch
+ * types cross this boundary (streams are passed as void*, NULL = the engine's
+ * own stream).  The C++ wrapper include/pdgpu.hpp maps these calls back onto
+ * the reference's class shapes and exception types.
+ *
+ * Data layout (shared with the reference): node p = (k*Ny + j)*Nx + i
+ * (grid.hpp:30-36), fields are component-major SoA  u[c*N + p]
+ * (VecField, field.hpp:14-16).  Batched device entries take
+ * [batch][dim][N] fp64.
+ *
+ * Errors: every int-returning call returns PDGPU_OK (0) or one of the codes
+ * below; pdgpu_last_error() returns the thread-local message of the last
+ * failure.  The three pdfast exceptions of the hot path keep distinct codes.
+ */
+#ifndef PDGPU_H
+#define PDGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PDGPU_OK 0
+#define PDGPU_ERR_HORIZON_TOO_LARGE 1 /* pdfast::HorizonTooLargeForGrid, convolution.hpp:61-62 */
+#define PDGPU_ERR_SHAPE_MISMATCH 2    /* pdfast::ShapeMismatch, convolution.hpp:120-121 */
+#define PDGPU_ERR_LEDGER_OUT_OF_BAND 3 /* pdfast::LedgerOutOfBand, corrections.hpp:99-100 */
+#define PDGPU_ERR_INVALID_ARGUMENT 4
+#define PDGPU_ERR_CUDA 5
+#define PDGPU_ERR_OUT_OF_MEMORY 6
+#define PDGPU_ERR_NOT_SUPPORTED 7
+
+typedef struct pdgpu_engine* pdgpu_t;
+
+const char* pdgpu_last_error(void);
+const char* pdgpu_version(void);
+
+/* ---------------------------------------------------------------- engine --
+ * FastForce<Dim>(grid, hz, K)   convolution.hpp:239-246
+ *   dims[dim]: lattice nodes per axis; M: band half-width (Horizon::M);
+ *   stencils: n_pairs x (2M+1)^dim doubles in KernelStack storage order
+ *   (KernelStack::component(pair), kernel.hpp:50-54,72).  Builds the
+ *   spectral symbol on `device`.  Fails with PDGPU_ERR_HORIZON_TOO_LARGE
+ *   when some dims[d] < M+1, like PadTransform's ctor. */
+int pdgpu_create(int dim, const int* dims, int M, const double* stencils, int device, pdgpu_t* out);
+void pdgpu_destroy(pdgpu_t h);
+
+/* Grid::h / Grid::origin (grid.hpp:15-20), Horizon::delta (grid.hpp:114-116),
+ * Material::rho (material.hpp:33-37): needed by positions (update_bonds,
+ * crack seeding, constraints) and by the VV step. */
+int pdgpu_set_geometry(pdgpu_t h, double spacing, const double* origin, double delta, double rho);
+
+/* FastForce::apply(u, f)   convolution.hpp:249-259 -- f = A_hat u, the
+ * uncorrected spectral force; f is overwritten.  Device pointers,
+ * [batch][dim][N], stream-ordered. */
+int pdgpu_apply(pdgpu_t h, const double* u, double* f, int batch, void* stream);
+/* Same with host vectors; n_nodes is the caller's field length and must
+ * equal the lattice size (ShapeMismatch, convolution.hpp:120-121). */
+int pdgpu_apply_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes, int batch);
+
+/* FastForce::last_imag_residue()  convolution.hpp:261.  The R2C pipeline
+ * produces real fields by construction: always 0. */
+double pdgpu_last_imag_residue(pdgpu_t h);
+/* FastForce::footprint_bytes()  convolution.hpp:263-266 (device bytes held). */
+size_t pdgpu_footprint_bytes(pdgpu_t h);
+int64_t pdgpu_n_nodes(pdgpu_t h);
+int pdgpu_symbol_is_real(pdgpu_t h);
+
+/* ----------------------------------------------------------- corrections --
+ * Regions (grid.hpp:172-209): per-node constraint direction mask (bit d =
+ * direction d).  near_surface may be NULL (recomputed from the geometry). */
+int pdgpu_set_regions(pdgpu_t h, const uint8_t* near_surface, const uint8_t* constraint_mask);
+/* SurfaceDiag raw storage (corrections.hpp:20-62): de is n_pairs x N, rows
+ * with near_surface set are used.  By default the engine builds it itself
+ * from the stencils (build_de, corrections.hpp:65-68). */
+int pdgpu_set_surface_diag(pdgpu_t h, const double* de);
+/* BondLedger (ledger.hpp:13-57) as CSR: row_start[N+1], partners sorted per
+ * row and symmetric.  Replaces the device ledger.  LedgerOutOfBand if a
+ * partner is not an in-band lattice neighbour. */
+int pdgpu_set_ledger(pdgpu_t h, const int64_t* row_start, const int64_t* partners);
+/* BondLedger::break_bond for n pairs (p,q) (ledger.hpp:21-26). */
+int pdgpu_break_bonds(pdgpu_t h, const int64_t* pairs, int64_t n);
+/* Broken bonds as sorted (p,q) pairs, p < q; *count = total (may exceed cap). */
+int pdgpu_ledger_pairs(pdgpu_t h, int64_t* out_pairs, int64_t cap, int64_t* count);
+/* apply_corrections(f, u, de, regions, ledger, K, grid)  corrections.hpp:76-110
+ * f += De u (surface rows) + sum_q K(q-p)(u_p - u_q) (fracture rows), rows
+ * constrained in the output direction untouched.  Device pointers. */
+int pdgpu_apply_corrections(pdgpu_t h, const double* u, double* f, int batch, void* stream);
+/* K.u as the reference's tests and Simulation compute it:
+ * FastForce::apply + apply_corrections (e.g. tests/test_corrections.cpp:107-110). */
+int pdgpu_matvec(pdgpu_t h, const double* u, double* f, int batch, void* stream);
+int pdgpu_matvec_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes, int batch);
+/* Simulation::evaluate_force (timestepping.hpp:295-310): f = A u + body,
+ * then zero every constrained (node, dir).  Device pointers, one field. */
+int pdgpu_evaluate_force(pdgpu_t h, const double* u, double* f, void* stream);
+
+/* --------------------------------------------------------------- problem --
+ * Problem<Dim> setup (timestepping.hpp:40-52).  Boxes are closed, cell
+ * centres tested (geometry.hpp:53-63); lo/hi have dim entries. */
+/* Constraint (grid.hpp:160-166): kind 0 = displacement, 1 = velocity. */
+int pdgpu_add_constraint(pdgpu_t h, const double* lo, const double* hi, int dir_mask, int kind, double value);
+/* Load (timestepping.hpp:26-30): body force density on a box. */
+int pdgpu_add_load(pdgpu_t h, const double* lo, const double* hi, const double* value);
+/* Body force field directly (dim x N, host). */
+int pdgpu_set_body(pdgpu_t h, const double* body);
+/* seed_cracks (fracture.hpp:164-198): segment {ax, ay, bx, by, width}
+ * (CrackSpec<2>::Segment) / notch {axis, plane, width, lo0, lo1, lo2, hi0,
+ * hi1, hi2} (CrackSpec<3>::Notch).  *added = bonds newly broken. */
+int pdgpu_seed_segment(pdgpu_t h, const double* seg, int64_t* added);
+int pdgpu_seed_notch(pdgpu_t h, const double* notch, int64_t* added);
+
+/* ------------------------------------------------------------- fracture --
+ * update_bonds(grid, hz, u, ledger, s0, watch)  fracture.hpp:204-231.
+ * u on the device ([dim][N]); watch = {lo[dim], hi[dim]} or NULL.
+ * Newly broken bonds are returned as (p, q) pairs in the reference's
+ * visiting order (p ascending, then offset order); *count = total. */
+int pdgpu_update_bonds(pdgpu_t h, const double* u, double s0, const double* watch, int64_t* out_pairs, int64_t cap,
+                       int64_t* count);
+
+/* ------------------------------------------------------------ CG solver --
+ * New static solver (the reference has ADR only): Hestenes-Stiefel CG on
+ * K := -A restricted to free DOFs, rhs = mask .* (b + A u_c) with u_c the
+ * prescribed displacement values.  b, x device [dim][N]; on return x holds
+ * the full displacement (free solution + prescribed values).  Stops at
+ * ||r|| <= tol ||rhs||. */
+int pdgpu_cg_solve(pdgpu_t h, const double* b, double* x, double tol, int maxit, int* iters, double* relres,
+                   void* stream);
+/* Host-vector variant; hist (optional, nhist x dim x N) receives the first
+ * nhist iterates x_1..x_nhist (free part, before prescribed values). */
+int pdgpu_cg_solve_host(pdgpu_t h, const double* b, double* x, double tol, int maxit, int* iters, double* relres,
+                        double* hist, int nhist);
+
+/* ------------------------------------------------------ velocity Verlet --
+ * Simulation<Dim> with Integrator::Vv (timestepping.hpp:167-351).
+ * sim_init zeroes u, v (optional initial velocity field), applies
+ * constraints at t = 0 (timestepping.hpp:201). */
+int pdgpu_sim_init(pdgpu_t h, double dt, const double* v0);
+/* n_steps of Simulation::step (timestepping.hpp:209-241); s0 < 0 disables
+ * fracture; watch as in update_bonds.  *broken = bonds broken in these steps. */
+int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64_t* broken);
+/* Copies of the state (host, dim x N each, any may be NULL). */
+int pdgpu_sim_get(pdgpu_t h, double* u, double* v, double* f, double* t);
+
+/* ------------------------------------------------------------- assembly --
+ * Host-side restatements of the reference's setup routines, so a caller
+ * without the reference can assemble a problem. */
+/* build_kernel (kernel.hpp:99-127): out n_pairs x (2M+1)^dim */
+int pdgpu_build_kernel(int dim, double spacing, double delta, int M, double E, double thickness, double* out);
+/* Regions near-surface flags (grid.hpp:181-189): out N bytes */
+int pdgpu_near_surface(int dim, const int* dims, int M, uint8_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PDGPU_H */

@@ -1,0 +1,9 @@
+"""B200-native MSBFM (matrix-structure-based fast method) K.u engine for
+linear bond-based peridynamics -- drop-in GPU path for the reference
+`pdfast` FastForce / apply_corrections / update_bonds and new CG / VV
+drivers.  See DESIGN.md and include/pdgpu.h."""
+from .engine import (Error, FastForce, HorizonTooLargeForGrid, LedgerOutOfBand, ShapeMismatch, band_offsets,
+                     build_kernel, n_pairs, near_surface, pair_index)
+
+__all__ = ["Error", "FastForce", "HorizonTooLargeForGrid", "LedgerOutOfBand", "ShapeMismatch", "band_offsets",
+           "build_kernel", "n_pairs", "near_surface", "pair_index"]

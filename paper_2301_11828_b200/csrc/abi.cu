@@ -1,0 +1,864 @@
+// abi.cu -- the C ABI (include/pdgpu.h) over the engine.  Host-side
+// orchestration only: setup, stream-ordered launches, error mapping.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pdgpu.h"
+#include "assembly.h"
+#include "engine.h"
+
+using namespace pdgpu;
+
+struct pdgpu_engine : public Engine {};
+
+namespace {
+
+thread_local std::string g_err;
+
+struct PdError : std::runtime_error {
+    int code;
+    PdError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaErrorMemoryAllocation) throw PdError(PDGPU_ERR_OUT_OF_MEMORY, std::string(what) + ": out of memory");
+    if (e != cudaSuccess) throw PdError(PDGPU_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+int guarded(F&& fn) {
+    try {
+        fn();
+        return PDGPU_OK;
+    } catch (const PdError& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host out of memory";
+        return PDGPU_ERR_OUT_OF_MEMORY;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        const std::string w = e.what();
+        if (w.find("out of memory") != std::string::npos) return PDGPU_ERR_OUT_OF_MEMORY;
+        return PDGPU_ERR_CUDA;
+    }
+}
+
+template <class T>
+void dalloc(T*& p, size_t count, const char* what) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cuda_check(cudaMalloc((void**)&p, sizeof(T) * std::max<size_t>(count, 1)), what);
+}
+
+cudaStream_t pick_stream(Engine& e, void* s) { return s ? (cudaStream_t)s : e.stream; }
+
+void coords_of(const Engine& e, int64_t p, int* c) {
+    c[0] = (int)(p % e.plan.N[0]);
+    c[1] = (int)((p / e.plan.N[0]) % e.plan.N[1]);
+    c[2] = (int)(p / ((int64_t)e.plan.N[0] * e.plan.N[1]));
+}
+
+int find_offset(const Engine& e, const int* o) {
+    for (int k = 0; k < e.nof; ++k)
+        if (e.offs[3 * k] == o[0] && e.offs[3 * k + 1] == o[1] && e.offs[3 * k + 2] == o[2]) return k;
+    return -1;
+}
+
+void ensure_ledger(Engine& e) {
+    if (e.d_ledger) return;
+    const int64_t N = e.plan.nodes;
+    dalloc(e.d_ledger, (size_t)(N * e.lw), "alloc ledger");
+    dalloc(e.d_bond_rows, (size_t)N, "alloc bond rows");
+    dalloc(e.d_listed, (size_t)N, "alloc listed");
+    cuda_check(cudaMemset(e.d_ledger, 0, sizeof(uint32_t) * N * e.lw), "zero ledger");
+    cuda_check(cudaMemset(e.d_listed, 0, sizeof(int) * N), "zero listed");
+    cuda_check(cudaMemset(e.d_counters, 0, sizeof(unsigned long long) * 2), "zero counters");
+    e.n_bond_rows = 0;
+    e.total_broken = 0;
+    e.new_pairs_cap = std::max<int64_t>(1 << 20, N / 4);
+    dalloc(e.d_new_pairs, (size_t)(2 * e.new_pairs_cap), "alloc new pairs");
+}
+
+void upload_surface(Engine& e, const std::vector<long long>& rows, const std::vector<double>& de) {
+    e.n_surf = (int64_t)rows.size();
+    dalloc(e.d_surf_rows, rows.size(), "alloc surface rows");
+    dalloc(e.d_surf_de, de.size(), "alloc surface de");
+    if (!rows.empty()) {
+        cuda_check(cudaMemcpy(e.d_surf_rows, rows.data(), sizeof(long long) * rows.size(), cudaMemcpyHostToDevice),
+                   "copy surface rows");
+        cuda_check(cudaMemcpy(e.d_surf_de, de.data(), sizeof(double) * de.size(), cudaMemcpyHostToDevice),
+                   "copy surface de");
+    }
+}
+
+// recompute the constraint mask and the constrained-dof list (last writer wins,
+// identical to applying the constraints in order, corrections.hpp:142-160)
+void rebuild_constraints(Engine& e) {
+    const int64_t N = e.plan.nodes;
+    const int dim = e.dim;
+    e.h_cmask.assign((size_t)N, 0);
+    std::map<long long, std::pair<int, double>> dofs;
+    for (const auto& cs : e.constraints) {
+        for (int64_t p = 0; p < N; ++p) {
+            double x[3];
+            assembly::node_pos(dim, e.plan.N, e.h, e.origin, p, x);
+            if (!assembly::box_contains(dim, cs.lo, cs.hi, x)) continue;
+            e.h_cmask[(size_t)p] |= cs.dir_mask;
+            for (int d = 0; d < dim; ++d)
+                if ((cs.dir_mask >> d) & 1u) dofs[(long long)d * N + p] = {cs.kind, cs.value};
+        }
+    }
+    cuda_check(cudaMemcpy(e.d_cmask, e.h_cmask.data(), (size_t)N, cudaMemcpyHostToDevice), "copy cmask");
+    std::vector<long long> ids;
+    std::vector<double> vals;
+    std::vector<int> kinds;
+    for (const auto& kv : dofs) {
+        ids.push_back(kv.first);
+        kinds.push_back(kv.second.first);
+        vals.push_back(kv.second.second);
+    }
+    e.n_cdofs = (int64_t)ids.size();
+    dalloc(e.d_cdofs, ids.size(), "alloc cdofs");
+    dalloc(e.d_cval, vals.size(), "alloc cval");
+    dalloc(e.d_ckind, kinds.size(), "alloc ckind");
+    if (!ids.empty()) {
+        cuda_check(cudaMemcpy(e.d_cdofs, ids.data(), sizeof(long long) * ids.size(), cudaMemcpyHostToDevice), "cdofs");
+        cuda_check(cudaMemcpy(e.d_cval, vals.data(), sizeof(double) * vals.size(), cudaMemcpyHostToDevice), "cval");
+        cuda_check(cudaMemcpy(e.d_ckind, kinds.data(), sizeof(int) * kinds.size(), cudaMemcpyHostToDevice), "ckind");
+    }
+}
+
+bool has_constraints(const Engine& e) { return !e.constraints.empty() || e.any_cmask; }
+
+// set bits for (p, q) pairs on the device; returns the number newly broken
+__global__ void k_break_pairs(uint32_t* ledger, int lw, const long long* quad, int64_t n, long long* bond_rows,
+                              int* listed, unsigned long long* counters) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long p = quad[4 * i], k = quad[4 * i + 1], q = quad[4 * i + 2], kn = quad[4 * i + 3];
+    const unsigned old = atomicOr(&ledger[p * lw + (k >> 5)], 1u << (k & 31));
+    if ((old >> (k & 31)) & 1u) return;
+    atomicOr(&ledger[q * lw + (kn >> 5)], 1u << (kn & 31));
+    atomicAdd(&counters[1], 1ull);
+    if (atomicExch(&listed[p], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = p;
+    if (atomicExch(&listed[q], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = q;
+}
+
+// host (p,q) pairs -> device bits; dedups within the call by sequential
+// semantics of break_bond (a pair listed twice breaks once).
+int64_t break_pairs(Engine& e, const int64_t* pairs, int64_t n) {
+    ensure_ledger(e);
+    std::vector<long long> quad;
+    quad.reserve((size_t)(4 * n));
+    std::vector<std::pair<long long, long long>> seen;
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t p = pairs[2 * i], q = pairs[2 * i + 1];
+        if (p < 0 || q < 0 || p >= e.plan.nodes || q >= e.plan.nodes)
+            throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bond endpoint out of range");
+        int cp[3], cq[3], o[3], no[3];
+        coords_of(e, p, cp);
+        coords_of(e, q, cq);
+        for (int d = 0; d < 3; ++d) {
+            o[d] = cq[d] - cp[d];
+            no[d] = -o[d];
+        }
+        const int k = find_offset(e, o), kn = find_offset(e, no);
+        if (k < 0 || kn < 0) throw PdError(PDGPU_ERR_LEDGER_OUT_OF_BAND, "broken bond exceeds the horizon band");
+        const long long a = std::min(p, q), b = std::max(p, q);
+        if (std::find(seen.begin(), seen.end(), std::make_pair(a, b)) != seen.end()) continue;
+        if (n < 4096) seen.push_back({a, b});
+        quad.push_back(p);
+        quad.push_back(k);
+        quad.push_back(q);
+        quad.push_back(kn);
+    }
+    const int64_t m = (int64_t)quad.size() / 4;
+    if (m == 0) return 0;
+    long long* d_quad = nullptr;
+    cuda_check(cudaMalloc(&d_quad, sizeof(long long) * quad.size()), "alloc quad");
+    cuda_check(cudaMemcpy(d_quad, quad.data(), sizeof(long long) * quad.size(), cudaMemcpyHostToDevice), "copy quad");
+    cuda_check(cudaMemsetAsync(e.d_counters + 1, 0, sizeof(unsigned long long), e.stream), "reset");
+    k_break_pairs<<<(unsigned)((m + 127) / 128), 128, 0, e.stream>>>(e.d_ledger, e.lw, d_quad, m, e.d_bond_rows,
+                                                                     e.d_listed, e.d_counters);
+    cuda_check(cudaGetLastError(), "break pairs");
+    unsigned long long cnt[2];
+    cuda_check(cudaMemcpyAsync(cnt, e.d_counters, sizeof(cnt), cudaMemcpyDeviceToHost, e.stream), "counters");
+    cuda_check(cudaStreamSynchronize(e.stream), "break pairs sync");
+    cudaFree(d_quad);
+    e.n_bond_rows = (int64_t)cnt[0];
+    e.total_broken += (int64_t)cnt[1];
+    return (int64_t)cnt[1];
+}
+
+void matvec_impl(Engine& e, const double* u, double* f, int batch, cudaStream_t s) {
+    launch_fast_apply(e, u, f, batch, s, 1.0, nullptr, nullptr);
+    launch_corrections(e, u, f, batch, s, 1.0);
+}
+
+void evaluate_force_impl(Engine& e, const double* u, double* f, cudaStream_t s) {
+    const bool cons = has_constraints(e);
+    launch_fast_apply(e, u, f, 1, s, 1.0, cons ? e.d_cmask : nullptr, e.d_body);
+    launch_corrections(e, u, f, 1, s, 1.0);
+}
+
+void ensure_stage(Engine& e, int64_t elems) {
+    if (elems <= e.stage_cap) return;
+    dalloc(e.d_u_stage, (size_t)elems, "alloc stage u");
+    dalloc(e.d_f_stage, (size_t)elems, "alloc stage f");
+    e.stage_cap = elems;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pdgpu_last_error(void) { return g_err.c_str(); }
+const char* pdgpu_version(void) { return "pdgpu 0.1 (sm_100a)"; }
+
+int pdgpu_create(int dim, const int* dims, int M, const double* stencils, int device, pdgpu_t* out) {
+    return guarded([&] {
+        if (!out || !dims || !stencils) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        *out = nullptr;
+        if (dim != 2 && dim != 3) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "dim must be 2 or 3");
+        if (M < 1 || M > 8) throw PdError(PDGPU_ERR_NOT_SUPPORTED, "band half-width M must be in [1, 8]");
+        for (int d = 0; d < dim; ++d)
+            if (dims[d] < M + 1)
+                throw PdError(PDGPU_ERR_HORIZON_TOO_LARGE, "need at least M+1 nodes per axis for the embedding");
+        cuda_check(cudaSetDevice(device), "set device");
+        auto* e = new pdgpu_engine();
+        try {
+            e->device = device;
+            e->dim = dim;
+            e->M = M;
+            e->np = assembly::n_pairs(dim);
+            e->ss = 1;
+            for (int d = 0; d < dim; ++d) e->ss *= (2 * M + 1);
+            e->stencils.assign(stencils, stencils + e->np * e->ss);
+            e->offs = assembly::band_offsets(dim, M);
+            e->nof = (int)e->offs.size() / 3;
+            e->lw = (e->nof + 31) / 32;
+            e->delta = M;
+            plan_init(e->plan, dim, dims);
+            const Plan& pl = e->plan;
+            const int64_t N = pl.nodes;
+            if (pl.P[0] / 4 * 2 * 16 > 227 * 1024 || pl.Pl / 2 * dim * 16 > 227 * 1024)
+                throw PdError(PDGPU_ERR_NOT_SUPPORTED, "lattice too large for the single-CTA transform tiles");
+            // physical (even) stencils give a real symbol
+            e->real_symbol = true;
+            {
+                const int side = 2 * M + 1;
+                for (int p = 0; p < e->np && e->real_symbol; ++p)
+                    for (int64_t si = 0; si < e->ss; ++si) {
+                        int64_t rem = si;
+                        int o[3] = {0, 0, 0};
+                        for (int d = 0; d < dim; ++d) {
+                            o[d] = (int)(rem % side) - M;
+                            rem /= side;
+                        }
+                        int no[3] = {-o[0], -o[1], -o[2]};
+                        const int64_t sj = assembly::stencil_index(dim, M, no);
+                        if (e->stencils[p * e->ss + si] != e->stencils[p * e->ss + sj]) {
+                            e->real_symbol = false;
+                            break;
+                        }
+                    }
+            }
+            set_kernel_attributes();
+            cuda_check(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking), "stream");
+            // stencils + per-offset coefficient table koff[k*np + pair]
+            std::vector<double> kbuf(e->stencils);
+            for (int k = 0; k < e->nof; ++k)
+                for (int p = 0; p < e->np; ++p)
+                    kbuf.push_back(e->stencils[p * e->ss + assembly::stencil_index(dim, M, &e->offs[3 * k])]);
+            dalloc(e->d_K, kbuf.size(), "alloc K");
+            cuda_check(cudaMemcpy(e->d_K, kbuf.data(), sizeof(double) * kbuf.size(), cudaMemcpyHostToDevice), "K");
+            std::vector<int> obuf(e->offs);
+            std::vector<long long> disp;
+            for (int k = 0; k < e->nof; ++k) {
+                const int* o = &e->offs[3 * k];
+                int no[3] = {-o[0], -o[1], -o[2]};
+                obuf.push_back(find_offset(*e, no));
+                disp.push_back((long long)o[2] * pl.N[0] * pl.N[1] + (long long)o[1] * pl.N[0] + o[0]);
+            }
+            dalloc(e->d_offs, obuf.size(), "alloc offs");
+            cuda_check(cudaMemcpy(e->d_offs, obuf.data(), sizeof(int) * obuf.size(), cudaMemcpyHostToDevice), "offs");
+            dalloc(e->d_disp, disp.size(), "alloc disp");
+            cuda_check(cudaMemcpy(e->d_disp, disp.data(), sizeof(long long) * disp.size(), cudaMemcpyHostToDevice),
+                       "disp");
+            build_twiddles(*e);
+            build_symbol(*e);
+            // regions + surface diagonal from the geometry (build_de)
+            e->h_near = assembly::near_surface(dim, dims, M);
+            std::vector<long long> rows;
+            std::vector<double> de;
+            assembly::surface_diag(dim, dims, M, e->stencils.data(), e->h_near, rows, de);
+            upload_surface(*e, rows, de);
+            dalloc(e->d_cmask, (size_t)N, "alloc cmask");
+            cuda_check(cudaMemset(e->d_cmask, 0, (size_t)N), "zero cmask");
+            e->h_cmask.assign((size_t)N, 0);
+            dalloc(e->d_counters, 2, "alloc counters");
+            cuda_check(cudaMemset(e->d_counters, 0, 16), "zero counters");
+            dalloc(e->d_red, 4096, "alloc red");
+            dalloc(e->d_scal, 16, "alloc scal");
+            dalloc(e->d_ticket, 4, "alloc ticket");
+            cuda_check(cudaMemset(e->d_ticket, 0, 16), "zero ticket");
+            cuda_check(cudaDeviceSynchronize(), "create");
+        } catch (...) {
+            pdgpu_destroy(e);
+            throw;
+        }
+        *out = e;
+    });
+}
+
+void pdgpu_destroy(pdgpu_t h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    void* ptrs[] = {h->d_tw, h->d_sym, h->d_K, h->d_offs, h->d_disp, h->d_S1, h->d_S2, h->d_u_stage, h->d_f_stage,
+                    h->d_cmask, h->d_surf_rows, h->d_surf_de, h->d_ledger, h->d_bond_rows, h->d_listed,
+                    h->d_counters, h->d_new_pairs, h->d_body, h->d_cdofs, h->d_cval, h->d_ckind, h->d_u, h->d_v,
+                    h->d_f, h->d_fprev, h->d_red, h->d_scal, h->d_ticket, h->d_cg};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+int pdgpu_set_geometry(pdgpu_t h, double spacing, const double* origin, double delta, double rho) {
+    return guarded([&] {
+        if (!h || !(spacing > 0)) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad geometry");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        h->h = spacing;
+        for (int d = 0; d < 3; ++d) h->origin[d] = (origin && d < h->dim) ? origin[d] : 0.0;
+        h->delta = delta;
+        h->rho = rho > 0 ? rho : 1.0;
+        if (!h->constraints.empty()) rebuild_constraints(*h);
+    });
+}
+
+int pdgpu_apply(pdgpu_t h, const double* u, double* f, int batch, void* stream) {
+    return guarded([&] {
+        if (!h || !u || !f || batch < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad apply arguments");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        launch_fast_apply(*h, u, f, batch, pick_stream(*h, stream), 1.0, nullptr, nullptr);
+    });
+}
+
+int pdgpu_apply_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes, int batch) {
+    return guarded([&] {
+        if (!h || !u || !f || batch < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad apply arguments");
+        if (n_nodes != h->plan.nodes) throw PdError(PDGPU_ERR_SHAPE_MISMATCH, "field length does not match the lattice");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const int64_t m = (int64_t)batch * h->dim * n_nodes;
+        ensure_stage(*h, m);
+        cuda_check(cudaMemcpyAsync(h->d_u_stage, u, sizeof(double) * m, cudaMemcpyHostToDevice, h->stream), "H2D");
+        launch_fast_apply(*h, h->d_u_stage, h->d_f_stage, batch, h->stream, 1.0, nullptr, nullptr);
+        cuda_check(cudaMemcpyAsync(f, h->d_f_stage, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(h->stream), "apply_host");
+    });
+}
+
+double pdgpu_last_imag_residue(pdgpu_t h) { return h ? h->imag_residue : 0.0; }
+
+size_t pdgpu_footprint_bytes(pdgpu_t h) {
+    if (!h) return 0;
+    const Plan& pl = h->plan;
+    const int64_t N = pl.nodes;
+    size_t b = 0;
+    b += (size_t)pl.ncols * pl.Pl * h->np * (h->real_symbol ? 8 : 16);
+    b += (size_t)(16 * (1 << pl.logTWN));
+    b += (size_t)h->cap_batch * 16 * (pl.S1_per_vec + ((pl.dim == 3 || pl.k3_halves == 1) ? pl.S2_per_vec : 0));
+    b += (size_t)N + (size_t)h->n_surf * (8 + 8 * h->np);
+    if (h->d_ledger) b += (size_t)N * (4 * h->lw + 12);
+    return b;
+}
+
+int64_t pdgpu_n_nodes(pdgpu_t h) { return h ? h->plan.nodes : 0; }
+int pdgpu_symbol_is_real(pdgpu_t h) { return h && h->real_symbol ? 1 : 0; }
+
+int pdgpu_set_regions(pdgpu_t h, const uint8_t* near_surface, const uint8_t* cmask) {
+    return guarded([&] {
+        if (!h) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null handle");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const int64_t N = h->plan.nodes;
+        if (near_surface) {
+            h->h_near.assign(near_surface, near_surface + N);
+            std::vector<long long> rows;
+            std::vector<double> de;
+            assembly::surface_diag(h->dim, h->plan.N, h->M, h->stencils.data(), h->h_near, rows, de);
+            upload_surface(*h, rows, de);
+        }
+        if (cmask) {
+            h->h_cmask.assign(cmask, cmask + N);
+            h->any_cmask = false;
+            for (int64_t p = 0; p < N; ++p) h->any_cmask = h->any_cmask || cmask[p] != 0;
+            cuda_check(cudaMemcpy(h->d_cmask, cmask, (size_t)N, cudaMemcpyHostToDevice), "copy cmask");
+        }
+    });
+}
+
+int pdgpu_set_surface_diag(pdgpu_t h, const double* de) {
+    return guarded([&] {
+        if (!h || !de) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const int64_t N = h->plan.nodes;
+        std::vector<long long> rows;
+        std::vector<double> vals;
+        for (int64_t p = 0; p < N; ++p) {
+            if (!h->h_near[(size_t)p]) continue;
+            rows.push_back(p);
+            for (int k = 0; k < h->np; ++k) vals.push_back(de[(int64_t)k * N + p]);
+        }
+        upload_surface(*h, rows, vals);
+    });
+}
+
+int pdgpu_set_ledger(pdgpu_t h, const int64_t* row_start, const int64_t* partners) {
+    return guarded([&] {
+        if (!h || !row_start) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        ensure_ledger(*h);
+        const int64_t N = h->plan.nodes;
+        std::vector<uint32_t> bits((size_t)(N * h->lw), 0u);
+        std::vector<long long> rows;
+        std::vector<int> listed((size_t)N, 0);
+        int64_t halves = 0;
+        for (int64_t p = 0; p < N; ++p) {
+            for (int64_t j = row_start[p]; j < row_start[p + 1]; ++j) {
+                const int64_t q = partners[j];
+                if (q < 0 || q >= N) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "partner out of range");
+                int cp[3], cq[3], o[3];
+                coords_of(*h, p, cp);
+                coords_of(*h, q, cq);
+                for (int d = 0; d < 3; ++d) o[d] = cq[d] - cp[d];
+                const int k = find_offset(*h, o);
+                if (k < 0) throw PdError(PDGPU_ERR_LEDGER_OUT_OF_BAND, "broken bond exceeds the horizon band");
+                bits[(size_t)(p * h->lw + (k >> 5))] |= 1u << (k & 31);
+                ++halves;
+            }
+            if (row_start[p + 1] > row_start[p]) {
+                rows.push_back(p);
+                listed[(size_t)p] = 1;
+            }
+        }
+        cuda_check(cudaMemcpy(h->d_ledger, bits.data(), sizeof(uint32_t) * bits.size(), cudaMemcpyHostToDevice),
+                   "copy ledger");
+        cuda_check(cudaMemcpy(h->d_listed, listed.data(), sizeof(int) * listed.size(), cudaMemcpyHostToDevice),
+                   "copy listed");
+        if (!rows.empty())
+            cuda_check(cudaMemcpy(h->d_bond_rows, rows.data(), sizeof(long long) * rows.size(), cudaMemcpyHostToDevice),
+                       "copy rows");
+        unsigned long long cnt[2] = {(unsigned long long)rows.size(), 0ull};
+        cuda_check(cudaMemcpy(h->d_counters, cnt, sizeof(cnt), cudaMemcpyHostToDevice), "copy counters");
+        h->n_bond_rows = (int64_t)rows.size();
+        h->total_broken = halves / 2;
+    });
+}
+
+int pdgpu_break_bonds(pdgpu_t h, const int64_t* pairs, int64_t n) {
+    return guarded([&] {
+        if (!h || (n > 0 && !pairs)) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        break_pairs(*h, pairs, n);
+    });
+}
+
+int pdgpu_ledger_pairs(pdgpu_t h, int64_t* out, int64_t cap, int64_t* count) {
+    return guarded([&] {
+        if (!h || !count) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        *count = 0;
+        if (!h->d_ledger) return;
+        const int64_t N = h->plan.nodes;
+        std::vector<uint32_t> bits((size_t)(N * h->lw));
+        cuda_check(cudaStreamSynchronize(h->stream), "sync");
+        cuda_check(cudaMemcpy(bits.data(), h->d_ledger, sizeof(uint32_t) * bits.size(), cudaMemcpyDeviceToHost),
+                   "read ledger");
+        // partner order per row = ascending q = ascending displacement
+        std::vector<int> order(h->nof);
+        std::vector<long long> disp(h->nof);
+        for (int k = 0; k < h->nof; ++k) {
+            order[k] = k;
+            const int* o = &h->offs[3 * k];
+            disp[k] = (long long)o[2] * h->plan.N[0] * h->plan.N[1] + (long long)o[1] * h->plan.N[0] + o[0];
+        }
+        std::sort(order.begin(), order.end(), [&](int a, int b) { return disp[a] < disp[b]; });
+        int64_t c = 0;
+        for (int64_t p = 0; p < N; ++p)
+            for (int k : order) {
+                if (disp[k] <= 0) continue;
+                if (!((bits[(size_t)(p * h->lw + (k >> 5))] >> (k & 31)) & 1u)) continue;
+                if (out && c < cap) {
+                    out[2 * c] = p;
+                    out[2 * c + 1] = p + disp[k];
+                }
+                ++c;
+            }
+        *count = c;
+    });
+}
+
+int pdgpu_apply_corrections(pdgpu_t h, const double* u, double* f, int batch, void* stream) {
+    return guarded([&] {
+        if (!h || !u || !f || batch < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        launch_corrections(*h, u, f, batch, pick_stream(*h, stream), 1.0);
+    });
+}
+
+int pdgpu_matvec(pdgpu_t h, const double* u, double* f, int batch, void* stream) {
+    return guarded([&] {
+        if (!h || !u || !f || batch < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        matvec_impl(*h, u, f, batch, pick_stream(*h, stream));
+    });
+}
+
+int pdgpu_matvec_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes, int batch) {
+    return guarded([&] {
+        if (!h || !u || !f || batch < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
+        if (n_nodes != h->plan.nodes) throw PdError(PDGPU_ERR_SHAPE_MISMATCH, "field length does not match the lattice");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const int64_t m = (int64_t)batch * h->dim * n_nodes;
+        ensure_stage(*h, m);
+        cuda_check(cudaMemcpyAsync(h->d_u_stage, u, sizeof(double) * m, cudaMemcpyHostToDevice, h->stream), "H2D");
+        matvec_impl(*h, h->d_u_stage, h->d_f_stage, batch, h->stream);
+        cuda_check(cudaMemcpyAsync(f, h->d_f_stage, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(h->stream), "matvec_host");
+    });
+}
+
+int pdgpu_evaluate_force(pdgpu_t h, const double* u, double* f, void* stream) {
+    return guarded([&] {
+        if (!h || !u || !f) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        evaluate_force_impl(*h, u, f, pick_stream(*h, stream));
+    });
+}
+
+int pdgpu_add_constraint(pdgpu_t h, const double* lo, const double* hi, int dir_mask, int kind, double value) {
+    return guarded([&] {
+        if (!h || !lo || !hi) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        Constraint c;
+        memset(&c, 0, sizeof(c));
+        for (int d = 0; d < h->dim; ++d) {
+            c.lo[d] = lo[d];
+            c.hi[d] = hi[d];
+        }
+        c.dir_mask = (uint8_t)dir_mask;
+        c.kind = kind;
+        c.value = value;
+        h->constraints.push_back(c);
+        rebuild_constraints(*h);
+    });
+}
+
+int pdgpu_add_load(pdgpu_t h, const double* lo, const double* hi, const double* value) {
+    return guarded([&] {
+        if (!h || !lo || !hi || !value) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const int64_t N = h->plan.nodes;
+        if (h->h_body.empty()) h->h_body.assign((size_t)(h->dim * N), 0.0);
+        for (int64_t p = 0; p < N; ++p) {
+            double x[3];
+            assembly::node_pos(h->dim, h->plan.N, h->h, h->origin, p, x);
+            if (!assembly::box_contains(h->dim, lo, hi, x)) continue;
+            for (int d = 0; d < h->dim; ++d) h->h_body[(size_t)(d * N + p)] += value[d];
+        }
+        dalloc(h->d_body, h->h_body.size(), "alloc body");
+        cuda_check(cudaMemcpy(h->d_body, h->h_body.data(), sizeof(double) * h->h_body.size(), cudaMemcpyHostToDevice),
+                   "copy body");
+    });
+}
+
+int pdgpu_set_body(pdgpu_t h, const double* body) {
+    return guarded([&] {
+        if (!h || !body) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const int64_t N = h->plan.nodes;
+        h->h_body.assign(body, body + h->dim * N);
+        dalloc(h->d_body, h->h_body.size(), "alloc body");
+        cuda_check(cudaMemcpy(h->d_body, body, sizeof(double) * h->h_body.size(), cudaMemcpyHostToDevice), "copy body");
+    });
+}
+
+static void seed_impl(Engine& e, const double* geom, bool notch, int64_t* added) {
+    const int dim = e.dim;
+    double lo[3], hi[3];
+    if (!notch) {
+        for (int d = 0; d < 2; ++d) {
+            const double a = geom[d], b = geom[2 + d], w = geom[4];
+            lo[d] = std::min(a - w, b - w);
+            hi[d] = std::max(a + w, b + w);
+        }
+    } else {
+        const int axis = (int)geom[0];
+        for (int d = 0; d < 3; ++d) {
+            lo[d] = d == axis ? geom[1] - geom[2] : geom[3 + d];
+            hi[d] = d == axis ? geom[1] + geom[2] : geom[6 + d];
+        }
+    }
+    int clo[3] = {0, 0, 0}, chi[3] = {0, 0, 0};
+    const double pad = e.delta + e.h;
+    for (int d = 0; d < dim; ++d) {
+        clo[d] = std::max(0, (int)floor((lo[d] - pad - e.origin[d]) / e.h));
+        chi[d] = std::min(e.plan.N[d] - 1, (int)ceil((hi[d] + pad - e.origin[d]) / e.h));
+    }
+    std::vector<int64_t> pairs;
+    const int* N = e.plan.N;
+    int c[3];
+    for (c[2] = clo[2]; c[2] <= chi[2]; ++c[2])
+        for (c[1] = clo[1]; c[1] <= chi[1]; ++c[1])
+            for (c[0] = clo[0]; c[0] <= chi[0]; ++c[0]) {
+                const int64_t p = ((int64_t)c[2] * N[1] + c[1]) * N[0] + c[0];
+                double xp[3];
+                assembly::node_pos(dim, N, e.h, e.origin, p, xp);
+                for (int k = 0; k < e.nof; ++k) {
+                    const int* o = &e.offs[3 * k];
+                    int qc[3] = {c[0] + o[0], c[1] + o[1], c[2] + o[2]};
+                    bool in = true;
+                    for (int d = 0; d < dim; ++d) in = in && qc[d] >= 0 && qc[d] < N[d];
+                    if (!in) continue;
+                    const int64_t q = ((int64_t)qc[2] * N[1] + qc[1]) * N[0] + qc[0];
+                    if (q < p) continue;
+                    double xq[3];
+                    assembly::node_pos(dim, N, e.h, e.origin, q, xq);
+                    const bool cross = notch ? assembly::notch_crosses(geom, xp, xq) : assembly::segment_crosses(geom, xp, xq);
+                    if (cross) {
+                        pairs.push_back(p);
+                        pairs.push_back(q);
+                    }
+                }
+            }
+    const int64_t n = break_pairs(e, pairs.data(), (int64_t)pairs.size() / 2);
+    if (added) *added = n;
+}
+
+int pdgpu_seed_segment(pdgpu_t h, const double* seg, int64_t* added) {
+    return guarded([&] {
+        if (!h || !seg) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        if (h->dim != 2) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "segments are 2D cracks");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        seed_impl(*h, seg, false, added);
+    });
+}
+
+int pdgpu_seed_notch(pdgpu_t h, const double* notch, int64_t* added) {
+    return guarded([&] {
+        if (!h || !notch) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        if (h->dim != 3) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "notches are 3D cracks");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        seed_impl(*h, notch, true, added);
+    });
+}
+
+int pdgpu_update_bonds(pdgpu_t h, const double* u, double s0, const double* watch, int64_t* out, int64_t cap,
+                       int64_t* count) {
+    return guarded([&] {
+        if (!h || !u) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        ensure_ledger(*h);
+        const int64_t n = launch_update_bonds(*h, u, s0, watch, h->stream);
+        if (count) *count = n;
+        if (out && cap > 0 && n > 0) {
+            const int64_t m = std::min(n, h->new_pairs_cap);
+            std::vector<long long> raw((size_t)(2 * m));
+            cuda_check(cudaMemcpy(raw.data(), h->d_new_pairs, sizeof(long long) * raw.size(), cudaMemcpyDeviceToHost),
+                       "read pairs");
+            std::vector<std::pair<long long, long long>> pk;
+            for (int64_t i = 0; i < m; ++i) pk.push_back({raw[2 * i], raw[2 * i + 1]});
+            std::sort(pk.begin(), pk.end());
+            const int* N = h->plan.N;
+            for (int64_t i = 0; i < std::min(m, cap); ++i) {
+                const int* o = &h->offs[3 * pk[i].second];
+                out[2 * i] = pk[i].first;
+                out[2 * i + 1] = pk[i].first + (long long)o[2] * N[0] * N[1] + (long long)o[1] * N[0] + o[0];
+            }
+        }
+    });
+}
+
+// ------------------------------------------------------------------ CG ---
+static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit, int* iters, double* relres,
+                    cudaStream_t s, double* hist_host, int nhist) {
+    const int64_t N = e.plan.nodes, m = (int64_t)e.dim * N;
+    if (!e.d_cg || e.cg_cap < m) {
+        dalloc(e.d_cg, (size_t)(4 * m), "alloc cg");
+        e.cg_cap = m;
+    }
+    double* r = e.d_cg;
+    double* p = r + m;
+    double* q = p + m;
+    double* uc = q + m;
+    // prescribed displacement values u_c (displacement constraints only)
+    bool any_uc = false;
+    {
+        std::vector<double> huc((size_t)m, 0.0);
+        for (const auto& cs : e.constraints) {
+            if (cs.kind != 0) continue;
+            for (int64_t pn = 0; pn < N; ++pn) {
+                double xx[3];
+                assembly::node_pos(e.dim, e.plan.N, e.h, e.origin, pn, xx);
+                if (!assembly::box_contains(e.dim, cs.lo, cs.hi, xx)) continue;
+                for (int d = 0; d < e.dim; ++d)
+                    if ((cs.dir_mask >> d) & 1u) huc[(size_t)(d * N + pn)] = cs.value;
+            }
+        }
+        for (double v : huc) any_uc = any_uc || v != 0.0;
+        if (any_uc)
+            cuda_check(cudaMemcpyAsync(uc, huc.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s), "copy uc");
+    }
+    if (any_uc) {
+        matvec_impl(e, uc, q, 1, s);
+        launch_mask_rhs(r, b, q, e.d_cmask, N, e.dim, s);
+    } else {
+        launch_mask_rhs(r, b, nullptr, e.d_cmask, N, e.dim, s);
+    }
+    cuda_check(cudaMemsetAsync(x, 0, sizeof(double) * m, s), "zero x");
+    cuda_check(cudaMemcpyAsync(p, r, sizeof(double) * m, cudaMemcpyDeviceToDevice, s), "p = r");
+    launch_dot(e, r, r, m, e.d_scal + 0, s);
+    double rr0 = 0;
+    cuda_check(cudaMemcpyAsync(&rr0, e.d_scal, sizeof(double), cudaMemcpyDeviceToHost, s), "read rr");
+    cuda_check(cudaStreamSynchronize(s), "cg init");
+    const double bnorm = sqrt(rr0);
+    int k = 0;
+    double rel = bnorm > 0 ? 1.0 : 0.0;
+    while (bnorm > 0 && k < maxit) {
+        launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
+        launch_corrections(e, p, q, 1, s, -1.0);
+        launch_dot(e, p, q, m, e.d_scal + 1, s);
+        launch_cg_update(e, x, r, p, q, m, e.d_scal, e.d_scal + 2, s);
+        double rr1 = 0;
+        cuda_check(cudaMemcpyAsync(&rr1, e.d_scal + 2, sizeof(double), cudaMemcpyDeviceToHost, s), "read rr");
+        ++k;
+        if (hist_host && k <= nhist)
+            cuda_check(cudaMemcpyAsync(hist_host + (size_t)(k - 1) * m, x, sizeof(double) * m, cudaMemcpyDeviceToHost, s),
+                       "hist");
+        cuda_check(cudaStreamSynchronize(s), "cg iter");
+        rel = sqrt(rr1) / bnorm;
+        if (rel <= tol) break;
+        launch_cg_direction(p, r, m, e.d_scal, s);
+    }
+    if (any_uc) launch_axpy(x, uc, 1.0, m, s);
+    cuda_check(cudaStreamSynchronize(s), "cg done");
+    if (iters) *iters = k;
+    if (relres) *relres = rel;
+}
+
+int pdgpu_cg_solve(pdgpu_t h, const double* b, double* x, double tol, int maxit, int* iters, double* relres,
+                   void* stream) {
+    return guarded([&] {
+        if (!h || !b || !x) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        cg_impl(*h, b, x, tol, maxit, iters, relres, pick_stream(*h, stream), nullptr, 0);
+    });
+}
+
+int pdgpu_cg_solve_host(pdgpu_t h, const double* b, double* x, double tol, int maxit, int* iters, double* relres,
+                        double* hist, int nhist) {
+    return guarded([&] {
+        if (!h || !b || !x) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const int64_t m = (int64_t)h->dim * h->plan.nodes;
+        ensure_stage(*h, m);
+        cuda_check(cudaMemcpyAsync(h->d_u_stage, b, sizeof(double) * m, cudaMemcpyHostToDevice, h->stream), "H2D");
+        cg_impl(*h, h->d_u_stage, h->d_f_stage, tol, maxit, iters, relres, h->stream, hist, nhist);
+        cuda_check(cudaMemcpy(x, h->d_f_stage, sizeof(double) * m, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+// ------------------------------------------------------------------ VV ---
+int pdgpu_sim_init(pdgpu_t h, double dt, const double* v0) {
+    return guarded([&] {
+        if (!h) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null handle");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const int64_t m = (int64_t)h->dim * h->plan.nodes;
+        dalloc(h->d_u, (size_t)m, "alloc u");
+        dalloc(h->d_v, (size_t)m, "alloc v");
+        dalloc(h->d_f, (size_t)m, "alloc f");
+        dalloc(h->d_fprev, (size_t)m, "alloc fprev");
+        cuda_check(cudaMemset(h->d_u, 0, sizeof(double) * m), "zero");
+        cuda_check(cudaMemset(h->d_v, 0, sizeof(double) * m), "zero");
+        cuda_check(cudaMemset(h->d_f, 0, sizeof(double) * m), "zero");
+        cuda_check(cudaMemset(h->d_fprev, 0, sizeof(double) * m), "zero");
+        if (v0) cuda_check(cudaMemcpy(h->d_v, v0, sizeof(double) * m, cudaMemcpyHostToDevice), "copy v0");
+        h->dt = dt;
+        h->t = 0.0;
+        h->step = 0;
+        h->force_ready = false;
+        launch_enforce(h->d_u, h->d_v, h->d_cdofs, h->d_cval, h->d_ckind, h->n_cdofs, 0.0, h->stream);
+        cuda_check(cudaStreamSynchronize(h->stream), "sim init");
+    });
+}
+
+int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64_t* broken) {
+    return guarded([&] {
+        if (!h || !h->d_u) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "simulation not initialised");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        Engine& e = *h;
+        const int64_t N = e.plan.nodes;
+        const double inv_rho = 1.0 / e.rho;
+        int64_t nb = 0;
+        if (s0 >= 0) ensure_ledger(e);
+        for (int i = 0; i < n_steps; ++i) {
+            if (!e.force_ready) {
+                evaluate_force_impl(e, e.d_u, e.d_f, e.stream);
+                e.force_ready = true;
+            }
+            launch_vv_drift(e.d_u, e.d_v, e.d_f, e.d_cmask, N, e.dim, e.dt, inv_rho, e.stream);
+            e.t += e.dt;
+            launch_enforce(e.d_u, e.d_v, e.d_cdofs, e.d_cval, e.d_ckind, e.n_cdofs, e.t, e.stream);
+            std::swap(e.d_f, e.d_fprev);
+            evaluate_force_impl(e, e.d_u, e.d_f, e.stream);
+            launch_vv_kick(e.d_v, e.d_fprev, e.d_f, e.d_cmask, N, e.dim, e.dt, inv_rho, e.stream);
+            launch_enforce(e.d_u, e.d_v, e.d_cdofs, e.d_cval, e.d_ckind, e.n_cdofs, e.t, e.stream);
+            if (s0 >= 0) nb += launch_update_bonds(e, e.d_u, s0, watch, e.stream);
+            ++e.step;
+        }
+        cuda_check(cudaStreamSynchronize(e.stream), "sim step");
+        if (broken) *broken = nb;
+    });
+}
+
+int pdgpu_sim_get(pdgpu_t h, double* u, double* v, double* f, double* t) {
+    return guarded([&] {
+        if (!h || !h->d_u) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "simulation not initialised");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const size_t m = sizeof(double) * h->dim * h->plan.nodes;
+        cuda_check(cudaStreamSynchronize(h->stream), "sync");
+        if (u) cuda_check(cudaMemcpy(u, h->d_u, m, cudaMemcpyDeviceToHost), "u");
+        if (v) cuda_check(cudaMemcpy(v, h->d_v, m, cudaMemcpyDeviceToHost), "v");
+        if (f) cuda_check(cudaMemcpy(f, h->d_f, m, cudaMemcpyDeviceToHost), "f");
+        if (t) *t = h->t;
+    });
+}
+
+// ------------------------------------------------------------ assembly ---
+int pdgpu_build_kernel(int dim, double spacing, double delta, int M, double E, double thickness, double* out) {
+    return guarded([&] {
+        if (!out || (dim != 2 && dim != 3) || M < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
+        if (dim == 2 && !(thickness > 0)) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "2D micromodulus requires the plate thickness");
+        const std::vector<double> K = assembly::build_kernel(dim, spacing, delta, M, E, thickness);
+        memcpy(out, K.data(), sizeof(double) * K.size());
+    });
+}
+
+int pdgpu_near_surface(int dim, const int* dims, int M, uint8_t* out) {
+    return guarded([&] {
+        if (!out || !dims) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
+        const std::vector<uint8_t> v = assembly::near_surface(dim, dims, M);
+        memcpy(out, v.data(), v.size());
+    });
+}
+
+}  // extern "C"

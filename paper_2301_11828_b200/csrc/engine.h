@@ -1,0 +1,137 @@
+// engine.h -- internal state of one GPU MSBFM engine (the object behind the
+// opaque pdgpu_t handle).  Host-only C++; kernels live in *.cu files.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+namespace pdgpu {
+
+constexpr int kMaxDim = 3;
+
+// Transform geometry.  Each axis is padded to P = 2*pow2ceil(N): >= N+M so the
+// circular correlation equals the reference's linear one on the window
+// (convolution.hpp:58-71 uses P = 2N, identical for power-of-two N).
+struct Plan {
+    int dim = 2;
+    int N[3] = {1, 1, 1};
+    int P[3] = {1, 1, 1};
+    int logP[3] = {0, 0, 0};
+    int64_t nodes = 0;  // N0*N1*N2
+    int Hx = 0;         // R2C half spectrum along x: P0/2 + 1 columns
+    int logQx = 0;      // x transforms are Qx = P0/4 points (R2C + zero half)
+    // spectral (last-axis) pass: column count, physical length, padded length
+    int ncols = 0, Nl = 0, Pl = 0, logPl = 0;
+    int64_t S1_per_vec = 0;  // complex elements per vector in S1 (d*Nz*Hx*Ny)
+    int64_t S2_per_vec = 0;  // complex elements per vector in S2 (3D: d*Hx*Py*Nz; 2D K3 output)
+    int logTWN = 0;          // twiddle table length = max P
+    // launch shapes
+    int k1_rows = 1;         // rows per CTA in the x passes
+    int k3_cols = 1;         // columns per CTA in the spectral pass
+    int k3_halves = 2;       // 2 = both half-spectra resident, 1 = two passes
+    int k2_zt = 1;           // z rows per CTA in the 3D y passes
+};
+
+struct Constraint {
+    double lo[3], hi[3];
+    uint8_t dir_mask;
+    int kind;  // 0 displacement, 1 velocity (grid.hpp:160-166)
+    double value;
+};
+
+struct Engine {
+    int device = 0;
+    int dim = 2, M = 0, np = 3, nof = 0, lw = 1;
+    int64_t ss = 0;  // stencil size (2M+1)^dim
+    Plan plan;
+    bool real_symbol = true;
+    std::vector<double> stencils;  // np * ss, KernelStack storage order (kernel.hpp:50-54)
+    std::vector<int> offs;         // nof*3, for_each_offset order (kernel.hpp:71-89)
+
+    // geometry for positions (grid.hpp:15-67) -- needed by fracture/constraints
+    double h = 1.0, origin[3] = {0, 0, 0}, delta = 0.0, rho = 1.0;
+
+    cudaStream_t stream = nullptr;  // engine-owned default stream
+    double2* d_tw = nullptr;        // exp(-2 pi i k / TWN)
+    void* d_sym = nullptr;          // symbol: real double or double2, np * ncols * Pl
+    double* d_K = nullptr;          // stencils on device (np * ss)
+    int* d_offs = nullptr;          // nof*3
+    long long* d_disp = nullptr;    // nof: linear node displacement of each offset
+    int64_t cap_batch = 0;
+    double2* d_S1 = nullptr;
+    double2* d_S2 = nullptr;
+    double* d_u_stage = nullptr;    // host-API staging
+    double* d_f_stage = nullptr;
+    int64_t stage_cap = 0;
+
+    // regions / corrections
+    uint8_t* d_cmask = nullptr;        // N, constraint direction mask per node
+    std::vector<uint8_t> h_cmask, h_near;
+    int64_t n_surf = 0;
+    long long* d_surf_rows = nullptr;  // surface node ids
+    double* d_surf_de = nullptr;       // n_surf * np
+    uint32_t* d_ledger = nullptr;      // N * lw bit set over offsets
+    long long* d_bond_rows = nullptr;  // rows with >=1 broken bond (unordered)
+    int* d_listed = nullptr;           // N flags: row already in d_bond_rows
+    unsigned long long* d_counters = nullptr;  // [0] = #bond rows, [1] = #new pairs
+    int64_t n_bond_rows = 0;           // host mirror
+    int64_t total_broken = 0;
+    long long* d_new_pairs = nullptr;  // update_bonds output buffer (p, k) pairs
+    int64_t new_pairs_cap = 0;
+
+    // constraints / loads / simulation state
+    std::vector<Constraint> constraints;
+    std::vector<double> h_body;          // dim * N (lazily)
+    double* d_body = nullptr;
+    long long* d_cdofs = nullptr;        // constrained dof ids (a*N + p), last-writer-wins order
+    double* d_cval = nullptr;            // value per constrained dof
+    int* d_ckind = nullptr;              // kind per constrained dof
+    int64_t n_cdofs = 0;
+    double *d_u = nullptr, *d_v = nullptr, *d_f = nullptr, *d_fprev = nullptr;
+    double t = 0.0, dt = 0.0;
+    int64_t step = 0;
+    bool force_ready = false;
+    bool any_cmask = false;              // constraint mask set directly (set_regions)
+    double* d_cg = nullptr;              // CG work vectors r, p, q, u_c
+    int64_t cg_cap = 0;
+    // reductions scratch
+    double* d_red = nullptr;           // partial sums
+    double* d_scal = nullptr;          // device scalars
+    unsigned int* d_ticket = nullptr;
+    double imag_residue = 0.0;
+};
+
+// spectral.cu
+void plan_init(Plan& pl, int dim, const int* dims);
+void engine_alloc_workspace(Engine& e, int64_t batch);
+void build_twiddles(Engine& e);
+void build_symbol(Engine& e);
+void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStream_t s,
+                       double scale, const uint8_t* cmask, const double* body);
+void set_kernel_attributes();
+
+// corrections.cu
+void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s,
+                        double scale);
+int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double* watch,
+                            cudaStream_t s);
+
+// solvers.cu
+void launch_dot(Engine& e, const double* a, const double* b, int64_t n, double* out_dev,
+                cudaStream_t s);
+void launch_cg_update(Engine& e, double* x, double* r, const double* p, const double* q, int64_t n,
+                      const double* scal, double* rr_out, cudaStream_t s);
+void launch_cg_direction(double* p, const double* r, int64_t n, const double* scal, cudaStream_t s);
+void launch_mask_rhs(double* out, const double* b, const double* Auc, const uint8_t* cmask,
+                     int64_t N, int dim, cudaStream_t s);
+void launch_vv_drift(double* u, const double* v, const double* f, const uint8_t* cmask, int64_t N,
+                     int dim, double dt, double inv_rho, cudaStream_t s);
+void launch_vv_kick(double* v, const double* fprev, const double* f, const uint8_t* cmask,
+                    int64_t N, int dim, double dt, double inv_rho, cudaStream_t s);
+void launch_enforce(double* u, double* v, const long long* dofs, const double* val, const int* kind,
+                    int64_t n, double t, cudaStream_t s);
+void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s);
+
+}  // namespace pdgpu

@@ -1,0 +1,201 @@
+// solvers.cu -- CG vector kernels (fused axpy + dot, deterministic
+// warp-shuffle reductions) and the velocity-Verlet elementwise kernels.
+//
+// CG is new work (the reference has only ADR, timestepping.hpp:79-145);
+// VV drift/kick/constraints follow timestepping.hpp:312-334 and
+// corrections.hpp:142-160.
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "engine.h"
+
+namespace pdgpu {
+
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs, fixed => deterministic order
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// block-reduce v into partial[blockIdx.x]; the last block to finish sums the
+// partials in index order into *out.  Deterministic for a fixed grid.
+__device__ void grid_reduce(double v, double* partial, unsigned int* ticket, double* out) {
+    __shared__ double ws[32];
+    __shared__ bool last;
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) ws[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double s = lane < (blockDim.x >> 5) ? ws[lane] : 0.0;
+        s = warp_sum(s);
+        if (lane == 0) {
+            partial[blockIdx.x] = s;
+            __threadfence();
+            const unsigned int t = atomicAdd(ticket, 1u);
+            last = (t == gridDim.x - 1);
+        }
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        double s = 0.0;
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += ((volatile double*)partial)[i];
+        s = warp_sum(s);
+        if (lane == 0) ws[wid] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += ws[w];
+            *out = tot;
+            *ticket = 0u;
+        }
+    }
+}
+
+__global__ void k_dot(const double* __restrict__ a, const double* __restrict__ b, int64_t n, double* partial,
+                      unsigned int* ticket, double* out) {
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        s += a[i] * b[i];
+    grid_reduce(s, partial, ticket, out);
+}
+
+// scal[0] = rr, scal[1] = p.q ; alpha = rr / pq ; x += alpha p ; r -= alpha q ; rr_out = r.r
+__global__ void k_cg_update(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                            const double* __restrict__ q, int64_t n, const double* scal, double* partial,
+                            unsigned int* ticket, double* rr_out) {
+    const double alpha = scal[0] / scal[1];
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        x[i] += alpha * p[i];
+        const double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        s += ri * ri;
+    }
+    grid_reduce(s, partial, ticket, rr_out);
+}
+
+// beta = scal[2] / scal[0] ; p = r + beta p
+__global__ void k_cg_direction(double* __restrict__ p, const double* __restrict__ r, int64_t n,
+                               const double* scal) {
+    const double beta = scal[2] / scal[0];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = r[i] + beta * p[i];
+}
+
+__global__ void k_rotate(double* scal) { scal[0] = scal[2]; }
+
+__global__ void k_mask_rhs(double* out, const double* b, const double* Auc, const uint8_t* cmask, int64_t N,
+                           int dim) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N * dim) return;
+    const int a = (int)(i / N);
+    const int64_t p = i - (int64_t)a * N;
+    const double v = b[i] + (Auc ? Auc[i] : 0.0);
+    out[i] = ((cmask[p] >> a) & 1u) ? 0.0 : v;
+}
+
+__global__ void k_vv_drift(double* u, const double* v, const double* f, const uint8_t* cmask, int64_t N, int dim,
+                           double dt, double inv_rho) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N * dim) return;
+    const int a = (int)(i / N);
+    const int64_t p = i - (int64_t)a * N;
+    if ((cmask[p] >> a) & 1u) return;
+    // u += dt*v + 0.5*dt*dt*f*inv_rho   (timestepping.hpp:318-319, same order, no contraction)
+    const double t1 = __dmul_rn(dt, v[i]);
+    const double t2 = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(0.5, dt), dt), f[i]), inv_rho);
+    u[i] = __dadd_rn(u[i], __dadd_rn(t1, t2));
+}
+
+__global__ void k_vv_kick(double* v, const double* fprev, const double* f, const uint8_t* cmask, int64_t N, int dim,
+                          double dt, double inv_rho) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N * dim) return;
+    const int a = (int)(i / N);
+    const int64_t p = i - (int64_t)a * N;
+    if ((cmask[p] >> a) & 1u) return;
+    // v += 0.5*dt*(f_prev + f)*inv_rho   (timestepping.hpp:330-331)
+    const double t = __dmul_rn(__dmul_rn(__dmul_rn(0.5, dt), __dadd_rn(fprev[i], f[i])), inv_rho);
+    v[i] = __dadd_rn(v[i], t);
+}
+
+__global__ void k_enforce(double* u, double* v, const long long* dofs, const double* val, const int* kind, int64_t n,
+                          double t) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int64_t k = dofs[i];
+    if (kind[i] == 0) {
+        u[k] = val[i];
+        v[k] = 0.0;
+    } else {
+        u[k] = __dmul_rn(val[i], t);
+        v[k] = val[i];
+    }
+}
+
+__global__ void k_axpy(double* y, const double* x, double a, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[i] += a * x[i];
+}
+
+static void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static unsigned blocks_for(int64_t n, int th) { return (unsigned)((n + th - 1) / th); }
+
+void launch_dot(Engine& e, const double* a, const double* b, int64_t n, double* out_dev, cudaStream_t s) {
+    k_dot<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, e.d_red, e.d_ticket, out_dev);
+    check(cudaGetLastError(), "dot");
+}
+
+void launch_cg_update(Engine& e, double* x, double* r, const double* p, const double* q, int64_t n,
+                      const double* scal, double* rr_out, cudaStream_t s) {
+    k_cg_update<<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, q, n, scal, e.d_red, e.d_ticket, rr_out);
+    check(cudaGetLastError(), "cg_update");
+}
+
+void launch_cg_direction(double* p, const double* r, int64_t n, const double* scal, cudaStream_t s) {
+    k_cg_direction<<<kRedBlocks, kRedThreads, 0, s>>>(p, r, n, scal);
+    k_rotate<<<1, 1, 0, s>>>(const_cast<double*>(scal));
+    check(cudaGetLastError(), "cg_direction");
+}
+
+void launch_mask_rhs(double* out, const double* b, const double* Auc, const uint8_t* cmask, int64_t N, int dim,
+                     cudaStream_t s) {
+    k_mask_rhs<<<blocks_for(N * dim, 256), 256, 0, s>>>(out, b, Auc, cmask, N, dim);
+    check(cudaGetLastError(), "mask_rhs");
+}
+
+void launch_vv_drift(double* u, const double* v, const double* f, const uint8_t* cmask, int64_t N, int dim, double dt,
+                     double inv_rho, cudaStream_t s) {
+    k_vv_drift<<<blocks_for(N * dim, 256), 256, 0, s>>>(u, v, f, cmask, N, dim, dt, inv_rho);
+    check(cudaGetLastError(), "vv_drift");
+}
+
+void launch_vv_kick(double* v, const double* fprev, const double* f, const uint8_t* cmask, int64_t N, int dim,
+                    double dt, double inv_rho, cudaStream_t s) {
+    k_vv_kick<<<blocks_for(N * dim, 256), 256, 0, s>>>(v, fprev, f, cmask, N, dim, dt, inv_rho);
+    check(cudaGetLastError(), "vv_kick");
+}
+
+void launch_enforce(double* u, double* v, const long long* dofs, const double* val, const int* kind, int64_t n,
+                    double t, cudaStream_t s) {
+    if (n == 0) return;
+    k_enforce<<<blocks_for(n, 256), 256, 0, s>>>(u, v, dofs, val, kind, n, t);
+    check(cudaGetLastError(), "enforce");
+}
+
+void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s) {
+    k_axpy<<<blocks_for(n, 256), 256, 0, s>>>(y, x, a, n);
+    check(cudaGetLastError(), "axpy");
+}
+
+}  // namespace pdgpu

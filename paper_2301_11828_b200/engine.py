@@ -1,0 +1,304 @@
+"""Python host mirror of the reference `pdfast` operator API over libpdgpu.
+
+Names, argument meaning and error behaviour follow the reference
+(proj/include/pdfast/*.hpp); all compute goes through the C ABI
+(include/pdgpu.h) into the sm_100a kernels.  Host arrays are numpy fp64 in
+the reference layout (component-major SoA, node p = (k*Ny + j)*Nx + i);
+device arrays are torch CUDA tensors of the same layout (batched
+[batch][dim][N]).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _lib
+
+
+class Error(RuntimeError):
+    """pdfast::Error (errors.hpp:8-10)."""
+
+
+class HorizonTooLargeForGrid(Error):
+    """errors.hpp:21-23; raised by the engine ctor (convolution.hpp:61-62)."""
+
+
+class ShapeMismatch(Error):
+    """errors.hpp:24-26; field length != lattice size (convolution.hpp:120-121)."""
+
+
+class LedgerOutOfBand(Error):
+    """errors.hpp:27-29; broken bond outside the band (corrections.hpp:99-100)."""
+
+
+class CudaError(Error):
+    pass
+
+
+_CODES = {1: HorizonTooLargeForGrid, 2: ShapeMismatch, 3: LedgerOutOfBand, 4: ValueError, 5: CudaError,
+          6: MemoryError, 7: NotImplementedError}
+
+
+def _check(rc: int):
+    if rc != 0:
+        lib = _lib.load()
+        msg = lib.pdgpu_last_error().decode()
+        raise _CODES.get(rc, Error)(msg)
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(_lib.c_double_p)
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def n_pairs(dim: int) -> int:
+    """kernel.hpp:14-15"""
+    return dim * (dim + 1) // 2
+
+
+def pair_index(dim: int, a: int, b: int) -> int:
+    """kernel.hpp:19-28"""
+    if a > b:
+        a, b = b, a
+    if dim == 2:
+        return a + b
+    return (0, 3, 5)[a] + b - a
+
+
+def band_offsets(dim: int, M: int) -> np.ndarray:
+    """In-band off-centre offsets in KernelStack::for_each_offset order (kernel.hpp:71-89)."""
+    out = []
+    zr = M if dim == 3 else 0
+    for a in range(-M, M + 1):
+        for b in range(-M, M + 1):
+            for c in range(-zr, zr + 1):
+                n2 = a * a + b * b + c * c
+                if 0 < n2 <= M * M:
+                    out.append((a, b, c))
+    return np.array(out, dtype=np.int64).reshape(-1, 3)
+
+
+def build_kernel(dim: int, h: float, delta: float, M: int, E: float, thickness: float = 0.0) -> np.ndarray:
+    """build_kernel (kernel.hpp:99-127) -> (n_pairs, (2M+1)^dim) stencils, KernelStack storage order."""
+    lib = _lib.load()
+    out = np.zeros((n_pairs(dim), (2 * M + 1) ** dim))
+    _check(lib.pdgpu_build_kernel(dim, h, delta, M, E, thickness, _dp(out)))
+    return out
+
+
+def near_surface(dims, M: int) -> np.ndarray:
+    """Regions near-surface flags (grid.hpp:181-189)."""
+    lib = _lib.load()
+    dims_a = (C.c_int * len(dims))(*dims)
+    out = np.zeros(int(np.prod(dims)), dtype=np.uint8)
+    _check(lib.pdgpu_near_surface(len(dims), dims_a, M, out.ctypes.data_as(_lib.c_uint8_p)))
+    return out
+
+
+class FastForce:
+    """GPU counterpart of pdfast::FastForce<Dim> (convolution.hpp:237-274),
+    extended with the correction, fracture and solver state the reference
+    keeps in Simulation (timestepping.hpp:167-351).
+
+    FastForce(dims, M, stencils) mirrors FastForce(grid, hz, K): dims =
+    Grid::dims, M = Horizon::M, stencils = KernelStack components.
+    """
+
+    def __init__(self, dims, M: int, stencils: np.ndarray, device: int = 0):
+        self._lib = _lib.load()
+        self.dims = tuple(int(d) for d in dims)
+        self.dim = len(self.dims)
+        self.M = int(M)
+        self.n = int(np.prod(self.dims))
+        st = _f64(stencils).reshape(-1)
+        if st.size != n_pairs(self.dim) * (2 * M + 1) ** self.dim:
+            raise ValueError("stencils must be n_pairs x (2M+1)^dim")
+        dims_a = (C.c_int * self.dim)(*self.dims)
+        h = C.c_void_p()
+        _check(self._lib.pdgpu_create(self.dim, dims_a, self.M, _dp(st), device, C.byref(h)))
+        self._h = h
+
+    # ------------------------------------------------------------ lifetime
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.pdgpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ---------------------------------------------------------- geometry
+    def set_geometry(self, h: float, origin=None, delta: float = 0.0, rho: float = 1.0):
+        org = _f64(origin if origin is not None else np.zeros(self.dim))
+        _check(self._lib.pdgpu_set_geometry(self._h, h, _dp(org), delta, rho))
+
+    # ------------------------------------------------------ spectral apply
+    def apply(self, u: np.ndarray) -> np.ndarray:
+        """FastForce::apply (convolution.hpp:249-259) on host fields (dim, N) or (B, dim, N)."""
+        u = _f64(u)
+        n_nodes = u.shape[-1]
+        batch = max(u.size // max(self.dim * n_nodes, 1), 1)
+        f = np.empty_like(u)
+        _check(self._lib.pdgpu_apply_host(self._h, _dp(u), _dp(f), n_nodes, batch))
+        return f
+
+    def apply_device(self, u, f, batch: int = 1, stream=None):
+        """Device pointers / torch tensors, layout [batch][dim][N]."""
+        _check(self._lib.pdgpu_apply(self._h, _ptr(u), _ptr(f), batch, _stream(stream)))
+
+    def last_imag_residue(self) -> float:
+        return self._lib.pdgpu_last_imag_residue(self._h)
+
+    def footprint_bytes(self) -> int:
+        return self._lib.pdgpu_footprint_bytes(self._h)
+
+    def symbol_is_real(self) -> bool:
+        return bool(self._lib.pdgpu_symbol_is_real(self._h))
+
+    # --------------------------------------------------------- corrections
+    def set_regions(self, near_surface=None, constraint_mask=None):
+        ns = None if near_surface is None else np.ascontiguousarray(near_surface, dtype=np.uint8)
+        cm = None if constraint_mask is None else np.ascontiguousarray(constraint_mask, dtype=np.uint8)
+        _check(self._lib.pdgpu_set_regions(self._h, None if ns is None else ns.ctypes.data_as(_lib.c_uint8_p),
+                                           None if cm is None else cm.ctypes.data_as(_lib.c_uint8_p)))
+
+    def set_surface_diag(self, de: np.ndarray):
+        de = _f64(de)
+        _check(self._lib.pdgpu_set_surface_diag(self._h, _dp(de)))
+
+    def set_ledger(self, row_start: np.ndarray, partners: np.ndarray):
+        rs = np.ascontiguousarray(row_start, dtype=np.int64)
+        pt = np.ascontiguousarray(partners, dtype=np.int64)
+        if pt.size == 0:
+            pt = np.zeros(1, dtype=np.int64)
+        _check(self._lib.pdgpu_set_ledger(self._h, rs.ctypes.data_as(_lib.c_int64_p), pt.ctypes.data_as(_lib.c_int64_p)))
+
+    def break_bonds(self, pairs):
+        pr = np.ascontiguousarray(np.asarray(pairs, dtype=np.int64).reshape(-1, 2))
+        _check(self._lib.pdgpu_break_bonds(self._h, pr.ctypes.data_as(_lib.c_int64_p), pr.shape[0]))
+
+    def ledger_pairs(self) -> np.ndarray:
+        cnt = C.c_int64()
+        _check(self._lib.pdgpu_ledger_pairs(self._h, None, 0, C.byref(cnt)))
+        out = np.zeros((max(cnt.value, 1), 2), dtype=np.int64)
+        _check(self._lib.pdgpu_ledger_pairs(self._h, out.ctypes.data_as(_lib.c_int64_p), cnt.value, C.byref(cnt)))
+        return out[: cnt.value]
+
+    def matvec(self, u: np.ndarray) -> np.ndarray:
+        """FastForce::apply + apply_corrections (corrections.hpp:76-110) on host fields."""
+        u = _f64(u)
+        batch = max(u.size // max(self.dim * u.shape[-1], 1), 1)
+        f = np.empty_like(u)
+        _check(self._lib.pdgpu_matvec_host(self._h, _dp(u), _dp(f), u.shape[-1], batch))
+        return f
+
+    def matvec_device(self, u, f, batch: int = 1, stream=None):
+        _check(self._lib.pdgpu_matvec(self._h, _ptr(u), _ptr(f), batch, _stream(stream)))
+
+    def apply_corrections_device(self, u, f, batch: int = 1, stream=None):
+        _check(self._lib.pdgpu_apply_corrections(self._h, _ptr(u), _ptr(f), batch, _stream(stream)))
+
+    def evaluate_force_device(self, u, f, stream=None):
+        _check(self._lib.pdgpu_evaluate_force(self._h, _ptr(u), _ptr(f), _stream(stream)))
+
+    # ------------------------------------------------------------- problem
+    def add_constraint(self, lo, hi, dir_mask: int, kind: int = 0, value: float = 0.0):
+        _check(self._lib.pdgpu_add_constraint(self._h, _dp(_f64(lo)), _dp(_f64(hi)), int(dir_mask), int(kind),
+                                              float(value)))
+
+    def add_load(self, lo, hi, value):
+        _check(self._lib.pdgpu_add_load(self._h, _dp(_f64(lo)), _dp(_f64(hi)), _dp(_f64(value))))
+
+    def set_body(self, body: np.ndarray):
+        _check(self._lib.pdgpu_set_body(self._h, _dp(_f64(body))))
+
+    def seed_segment(self, a, b, width: float = 0.0) -> int:
+        seg = _f64([a[0], a[1], b[0], b[1], width])
+        added = C.c_int64()
+        _check(self._lib.pdgpu_seed_segment(self._h, _dp(seg), C.byref(added)))
+        return added.value
+
+    def seed_notch(self, axis: int, plane: float, width: float, lo, hi) -> int:
+        nt = _f64([axis, plane, width, lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]])
+        added = C.c_int64()
+        _check(self._lib.pdgpu_seed_notch(self._h, _dp(nt), C.byref(added)))
+        return added.value
+
+    # ------------------------------------------------------------ fracture
+    def update_bonds(self, u, s0: float, watch=None, cap: int = 1 << 20) -> np.ndarray:
+        """update_bonds (fracture.hpp:204-231); u is a device tensor [dim][N]."""
+        w = None if watch is None else _f64(np.concatenate([np.asarray(watch[0]), np.asarray(watch[1])]))
+        out = np.zeros((cap, 2), dtype=np.int64)
+        cnt = C.c_int64()
+        _check(self._lib.pdgpu_update_bonds(self._h, _ptr(u), float(s0), None if w is None else _dp(w),
+                                            out.ctypes.data_as(_lib.c_int64_p), cap, C.byref(cnt)))
+        return out[: min(cnt.value, cap)]
+
+    # ------------------------------------------------------------------ CG
+    def cg_solve(self, b: np.ndarray, tol: float = 1e-10, maxit: int = 10000, nhist: int = 0):
+        b = _f64(b)
+        x = np.empty_like(b)
+        it = C.c_int()
+        rel = C.c_double()
+        hist = np.zeros((max(nhist, 1),) + b.shape) if nhist else None
+        _check(self._lib.pdgpu_cg_solve_host(self._h, _dp(b), _dp(x), tol, maxit, C.byref(it), C.byref(rel),
+                                             None if hist is None else _dp(hist), nhist))
+        return x, it.value, rel.value, hist
+
+    def cg_solve_device(self, b, x, tol: float = 1e-10, maxit: int = 10000, stream=None):
+        it = C.c_int()
+        rel = C.c_double()
+        _check(self._lib.pdgpu_cg_solve(self._h, _ptr(b), _ptr(x), tol, maxit, C.byref(it), C.byref(rel),
+                                        _stream(stream)))
+        return it.value, rel.value
+
+    # ------------------------------------------------------------------ VV
+    def sim_init(self, dt: float, v0=None):
+        _check(self._lib.pdgpu_sim_init(self._h, dt, None if v0 is None else _dp(_f64(v0))))
+
+    def sim_step(self, n_steps: int = 1, s0: float = -1.0, watch=None) -> int:
+        w = None if watch is None else _f64(np.concatenate([np.asarray(watch[0]), np.asarray(watch[1])]))
+        nb = C.c_int64()
+        _check(self._lib.pdgpu_sim_step(self._h, n_steps, s0, None if w is None else _dp(w), C.byref(nb)))
+        return nb.value
+
+    def sim_get(self):
+        u = np.zeros((self.dim, self.n))
+        v = np.zeros_like(u)
+        f = np.zeros_like(u)
+        t = C.c_double()
+        _check(self._lib.pdgpu_sim_get(self._h, _dp(u), _dp(v), _dp(f), C.byref(t)))
+        return u, v, f, t.value
+
+
+def _ptr(x) -> int:
+    if isinstance(x, int):
+        return x
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    raise TypeError("expected a device pointer or a CUDA tensor")
+
+
+def _stream(s):
+    if s is None:
+        return None
+    if hasattr(s, "cuda_stream"):
+        return s.cuda_stream
+    return int(s)
