@@ -1,0 +1,355 @@
+#!/usr/bin/env python
+"""bench.py -- MSBFM K.u throughput on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], largest single-GPU rung): 2D linear
+bond-based PD, 4096 x 4096 nodes (2 DOF/node), delta = 3.015 h (M = 3),
+micromodulus 9E/(pi t delta^3) with E = t = 1, no constraints, no cracks
+(near-surface diagonal correction on 12N-36 rows), fp64, batch of 16 seeded
+uniform[-1,1] displacement vectors per step.  One step = one batched
+K.u = FastForce::apply + apply_corrections over the 16 vectors.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+value  : DOF-matvecs/s over the timed steps, inputs resident in HBM
+         (inputs 4.3 GB per step >> 126 MB L2: no flush needed).
+e2e    : the same metric through the public host API pdgpu_matvec_host
+         (pinned host u in, host f out, copies inside the timed region).
+roofline: the dominant kernel (K3, fused y-FFT + symbol + inverse y-FFT),
+         algorithmic bytes per launch / its mean CUDA-event duration.
+cpu_baseline: the reference's own FastForce::apply + apply_corrections
+         (oracle/_ref, headers compiled unmodified) on the host cores,
+         bounded sample.  --impl reference prints that arm alone.
+N > 1 (torchrun): every rank runs its own 16-vector batch (independent
+replicas over vectors, no data-path collective) -> weak scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_SIDE = 4096
+BATCH = 16
+DIM = 2
+M = 3
+METRIC = "DOF-matvecs/sec of MSBFM K·u (fp64)"
+UNIT = "DOF-matvecs/s"
+
+
+def workload_config(n_gpus: int):
+    return {"workload": f"2D MSBFM K·u, {N_SIDE}x{N_SIDE} nodes, batch {BATCH} (BASELINE configs[1] top rung)",
+            "grid": [N_SIDE, N_SIDE], "dof_per_node": DIM, "batch": BATCH, "delta_over_h": 3.015, "M": M,
+            "E": 1.0, "thickness": 1.0, "corrections": "surface diagonal (12N-36 rows), no cracks",
+            "padding": "2N per axis (R2C half spectrum)", "l2": "inputs 4.3 GB per step > L2, no flush",
+            "parallelism": f"replicas{n_gpus} (batch per rank)" if n_gpus > 1 else "single GPU"}
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                vals = [v.strip() for v in out.stdout.strip().split(",")]
+                if len(vals) >= 6:
+                    self.samples.append(vals)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def start(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------- peaks / bytes --
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def k3_algorithmic_bytes(n_side: int, batch: int):
+    """K3 per launch: read + write the half spectrum (Hx x Ny complex per
+    component per vector) + the real symbol once per launch (n_pairs x Hx x Py)."""
+    hx = n_side + 1          # Px/2 + 1 with Px = 2N
+    ny, py = n_side, 2 * n_side
+    data = batch * DIM * hx * ny * 16 * 2
+    sym = 3 * hx * py * 8
+    return data + sym
+
+
+def matvec_algorithmic_bytes(n_side: int, batch: int):
+    """SURVEY.md 8(d) pass model: 80 B/DOF per vector + 48N B symbol per call."""
+    n = n_side * n_side
+    return batch * 80 * DIM * n + 48 * n
+
+
+# ------------------------------------------------------------------ CPU leg --
+def _mem_available_bytes():
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except Exception:
+        pass
+    return 16 << 30
+
+
+def reference_problem(n_side):
+    from oracle.oracle import RefProblem
+    h = 1.0 / n_side
+    r = RefProblem((n_side, n_side), h=h, delta=3.015 * h, M=M, E=1.0, thickness=1.0)
+    r.finalize()
+    return r
+
+
+def cpu_threads_for(n_side):
+    # one reference FastForce instance holds (n_pairs + d + 2) padded complex grids
+    footprint = (3 + DIM + 2) * (2 * n_side) ** 2 * 16 + 4 * DIM * n_side * n_side * 8
+    cores = os.cpu_count() or 1
+    return max(1, min(cores, int(0.6 * _mem_available_bytes() // footprint))), cores
+
+
+def cpu_reference_sample(n_side, steps=1, budget_s=150.0):
+    """Time the reference path (oracle/_ref) on host cores: each step one
+    vector per thread, independent FastForce instances (convolution.hpp:53-54)."""
+    import numpy as np
+    from oracle import oracle as orc
+    if not orc.ref_available():
+        return None
+    threads, cores = cpu_threads_for(n_side)
+    r = reference_problem(n_side)
+    rng = np.random.default_rng(1234)
+    u = rng.uniform(-1.0, 1.0, size=(threads, DIM, n_side * n_side))
+    times = []
+    t_start = time.time()
+    for _ in range(steps):
+        times.append(r.bench(u, threads))
+        if time.time() - t_start > budget_s:
+            break
+    per_step = statistics.median(times)
+    value = threads * DIM * n_side * n_side / per_step
+    return {"value": value, "unit": UNIT, "cores": threads, "host_cores": cores, "kind": "reference",
+            "sample": f"{threads} of the {BATCH} vectors per step ({threads} threads x 1 vector, one FastForce each), "
+                      f"{len(times)} step(s), median {per_step:.2f} s; reference headers + oracle/fftw_cpu (FFTW3 "
+                      f"absent), g++ -O2", "steps_timed": len(times), "s_per_step": per_step}
+
+
+# -------------------------------------------------------------------- main --
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    res = cpu_reference_sample(N_SIDE, steps=max(args.steps, 1), budget_s=args.ref_budget)
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpdref.so not built"}))
+        return 0
+    line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": res["steps_timed"],
+            "warmup": 0, "ms_per_step": res["s_per_step"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": workload_config(1),
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "reference arm: the reference's own CPU path; warm-up steps skipped (no caches/JIT to warm), "
+                    "timed steps capped by a wall budget"}
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=N_SIDE)
+    ap.add_argument("--batch", type=int, default=BATCH)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-budget", type=float, default=150.0)
+    args = ap.parse_args()
+    globals()["N_SIDE"] = args.n
+    globals()["BATCH"] = args.batch
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2301_11828_b200 import FastForce, build_kernel
+
+    n = N_SIDE * N_SIDE
+    h = 1.0 / N_SIDE
+    K = build_kernel(DIM, h, 3.015 * h, M, 1.0, 1.0)
+    ff = FastForce((N_SIDE, N_SIDE), M, K, device=local)
+    ff.set_geometry(h, [0.0, 0.0], 3.015 * h, 1.0)
+
+    stream = torch.cuda.Stream()
+    gen = torch.Generator(device="cuda").manual_seed(1000 * 2 + rank)
+    u = torch.empty((BATCH, DIM, n), dtype=torch.float64, device="cuda")
+    u.uniform_(-1.0, 1.0, generator=gen)
+    f = torch.empty_like(u)
+    torch.cuda.synchronize()
+
+    def step():
+        ff.matvec_device(u, f, BATCH, stream)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize()
+    ff.timing_read()  # discard warm-up marks
+    ff.timing(True)
+    launches0 = ff.launch_count()
+    clk = ClockSampler(local)
+    clk.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    launches = ff.launch_count() - launches0
+    passes = ff.timing_read()
+    ff.timing(False)
+    if world > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    value = world * BATCH * DIM * n / (ms_step * 1e-3)
+
+    # sanity: finite output
+    assert torch.isfinite(f).all().item(), "non-finite K.u"
+
+    # roofline of the dominant kernel (K3) from the live CUDA events
+    peak, peak_src = measured_peaks()
+    k3_ms, k3_n = passes.get("K3_spectral", (0.0, 0))
+    k3_bytes = k3_algorithmic_bytes(N_SIDE, BATCH)
+    k3_avg_s = (k3_ms / max(k3_n, 1)) * 1e-3
+    k3_gbs = k3_bytes / k3_avg_s / 1e9 if k3_avg_s > 0 else None
+    mv_bytes = matvec_algorithmic_bytes(N_SIDE, BATCH)
+    mv_gbs = mv_bytes / (ms_step * 1e-3) / 1e9
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "k3_dram_bytes.json")
+    if os.path.exists(tr_path):
+        try:
+            with open(tr_path) as fh:
+                tj = json.load(fh)
+            if tj.get("n") == N_SIDE and tj.get("batch") == BATCH:
+                traffic = tj.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    roofline = {"bound": "hbm", "kernel": "k_spectral (K3: y-FFT + symbol + inverse y-FFT)", "achieved": k3_gbs,
+                "peak": peak, "unit": "GB/s", "frac": (k3_gbs / peak) if k3_gbs else None, "traffic": traffic,
+                "algorithmic_bytes_per_launch": k3_bytes, "mean_launch_ms": k3_avg_s * 1e3, "peak_source": peak_src,
+                "matvec": {"algorithmic_bytes_per_step": mv_bytes, "achieved_gbs": mv_gbs, "frac": mv_gbs / peak,
+                           "model": "SURVEY 8(d): 80 B/DOF/vector + 48N B symbol"},
+                "passes_ms_per_step": {k: v[0] / args.steps for k, v in passes.items()}}
+
+    # end to end through the public host API (pinned host buffers)
+    e2e = None
+    if not args.no_e2e:
+        uh = torch.empty((BATCH, DIM, n), dtype=torch.float64, pin_memory=True)
+        uh.copy_(u)
+        fh = torch.empty_like(uh, pin_memory=True)
+        uh_np, fh_np = uh.numpy(), fh.numpy()
+        ff.matvec(uh_np, out=fh_np)  # warm the staging buffers (not timed)
+        e2e_steps = max(1, min(args.steps, 3))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            ff.matvec(uh_np, out=fh_np)
+        torch.cuda.synchronize()
+        e2e_s = (time.perf_counter() - t0) / e2e_steps
+        if world > 1:
+            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        nbytes = BATCH * DIM * n * 8
+        e2e = {"value": world * BATCH * DIM * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "steps": e2e_steps, "ms_per_step": e2e_s * 1e3,
+               "api": "pdgpu_matvec_host (pinned host u -> host f)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_reference_sample(N_SIDE, steps=1, budget_s=60.0)
+            if cpu:
+                cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as exc:  # the CPU leg must not kill the GPU number
+            cpu = {"error": str(exc)[:200]}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1], torch Philox)",
+                "config": workload_config(world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clocks}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    ff.close()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -147,6 +147,17 @@ int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64
 /* Copies of the state (host, dim x N each, any may be NULL). */
 int pdgpu_sim_get(pdgpu_t h, double* u, double* v, double* f, double* t);
 
+/* ---------------------------------------------------------- diagnostics --
+ * Per-pass device timing with CUDA events on the launching stream (pass ids:
+ * 0 K1 x-forward, 1 K2 y-forward (3D), 2 K3 spectral, 3 K4 y-inverse (3D),
+ * 4 K5 x-inverse, 5 surface correction, 6 fracture correction, 7 vector
+ * ops).  timing_read synchronises, returns the summed milliseconds and
+ * launch counts per pass since the last read, and resets them. */
+int pdgpu_timing_enable(pdgpu_t h, int on);
+int pdgpu_timing_read(pdgpu_t h, double* ms_per_pass, int64_t* count_per_pass, int npass);
+/* Number of kernels this engine has launched (all entry points). */
+int64_t pdgpu_launch_count(pdgpu_t h);
+
 /* ------------------------------------------------------------- assembly --
  * Host-side restatements of the reference's setup routines, so a caller
  * without the reference can assemble a problem. */

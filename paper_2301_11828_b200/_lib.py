@@ -54,6 +54,9 @@ SIGNATURES = {
     "pdgpu_sim_init": (C.c_int, [C.c_void_p, C.c_double, c_double_p]),
     "pdgpu_sim_step": (C.c_int, [C.c_void_p, C.c_int, C.c_double, c_double_p, c_int64_p]),
     "pdgpu_sim_get": (C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p, c_double_p]),
+    "pdgpu_timing_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "pdgpu_timing_read": (C.c_int, [C.c_void_p, c_double_p, c_int64_p, C.c_int]),
+    "pdgpu_launch_count": (C.c_int64, [C.c_void_p]),
     "pdgpu_build_kernel": (C.c_int, [C.c_int, C.c_double, C.c_double, C.c_int, C.c_double, C.c_double, c_double_p]),
     "pdgpu_near_surface": (C.c_int, [C.c_int, c_int_p, C.c_int, c_uint8_p]),
 }

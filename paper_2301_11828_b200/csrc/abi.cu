@@ -330,6 +330,9 @@ void pdgpu_destroy(pdgpu_t h) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
+    if (h->copy_in) cudaStreamDestroy(h->copy_in);
+    if (h->copy_out) cudaStreamDestroy(h->copy_out);
+    for (cudaEvent_t ev : h->ev_pool) cudaEventDestroy(ev);
     delete h;
 }
 
@@ -528,12 +531,36 @@ int pdgpu_matvec_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes, in
         if (!h || !u || !f || batch < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
         if (n_nodes != h->plan.nodes) throw PdError(PDGPU_ERR_SHAPE_MISMATCH, "field length does not match the lattice");
         cuda_check(cudaSetDevice(h->device), "set device");
-        const int64_t m = (int64_t)batch * h->dim * n_nodes;
-        ensure_stage(*h, m);
-        cuda_check(cudaMemcpyAsync(h->d_u_stage, u, sizeof(double) * m, cudaMemcpyHostToDevice, h->stream), "H2D");
-        matvec_impl(*h, h->d_u_stage, h->d_f_stage, batch, h->stream);
-        cuda_check(cudaMemcpyAsync(f, h->d_f_stage, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream), "D2H");
-        cuda_check(cudaStreamSynchronize(h->stream), "matvec_host");
+        const int64_t mv = (int64_t)h->dim * n_nodes;
+        ensure_stage(*h, (int64_t)batch * mv);
+        if (!h->copy_in) {
+            cuda_check(cudaStreamCreateWithFlags(&h->copy_in, cudaStreamNonBlocking), "stream");
+            cuda_check(cudaStreamCreateWithFlags(&h->copy_out, cudaStreamNonBlocking), "stream");
+        }
+        // pipeline: H2D of chunk c+1 and D2H of chunk c-1 overlap the mat-vec of chunk c
+        const int chunk = batch >= 8 ? 2 : 1;
+        const int nch = (batch + chunk - 1) / chunk;
+        std::vector<cudaEvent_t> evh(nch), evc(nch);
+        for (int c = 0; c < nch; ++c) {
+            cuda_check(cudaEventCreateWithFlags(&evh[c], cudaEventDisableTiming), "event");
+            cuda_check(cudaEventCreateWithFlags(&evc[c], cudaEventDisableTiming), "event");
+        }
+        for (int c = 0; c < nch; ++c) {
+            const int b0 = c * chunk, nb = std::min(chunk, batch - b0);
+            const size_t off = (size_t)b0 * mv, bytes = sizeof(double) * (size_t)nb * mv;
+            cuda_check(cudaMemcpyAsync(h->d_u_stage + off, u + off, bytes, cudaMemcpyHostToDevice, h->copy_in), "H2D");
+            cuda_check(cudaEventRecord(evh[c], h->copy_in), "record");
+            cuda_check(cudaStreamWaitEvent(h->stream, evh[c], 0), "wait");
+            matvec_impl(*h, h->d_u_stage + off, h->d_f_stage + off, nb, h->stream);
+            cuda_check(cudaEventRecord(evc[c], h->stream), "record");
+            cuda_check(cudaStreamWaitEvent(h->copy_out, evc[c], 0), "wait");
+            cuda_check(cudaMemcpyAsync(f + off, h->d_f_stage + off, bytes, cudaMemcpyDeviceToHost, h->copy_out), "D2H");
+        }
+        cuda_check(cudaStreamSynchronize(h->copy_out), "matvec_host");
+        for (int c = 0; c < nch; ++c) {
+            cudaEventDestroy(evh[c]);
+            cudaEventDestroy(evc[c]);
+        }
     });
 }
 
@@ -842,6 +869,40 @@ int pdgpu_sim_get(pdgpu_t h, double* u, double* v, double* f, double* t) {
         if (t) *t = h->t;
     });
 }
+
+// --------------------------------------------------------- diagnostics ---
+int pdgpu_timing_enable(pdgpu_t h, int on) {
+    return guarded([&] {
+        if (!h) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null handle");
+        h->timing = on != 0;
+    });
+}
+
+int pdgpu_timing_read(pdgpu_t h, double* ms, int64_t* cnt, int npass) {
+    return guarded([&] {
+        if (!h) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null handle");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        cuda_check(cudaDeviceSynchronize(), "timing sync");
+        for (int i = 0; i < npass; ++i) {
+            if (ms) ms[i] = 0.0;
+            if (cnt) cnt[i] = 0;
+        }
+        for (size_t k = 0; k < h->mark_pass.size(); ++k) {
+            const int id = h->mark_pass[k];
+            if (id >= npass) continue;
+            float t = 0.f;
+            cuda_check(cudaEventElapsedTime(&t, h->mark_a[k], h->mark_b[k]), "elapsed");
+            if (ms) ms[id] += t;
+            if (cnt) cnt[id] += 1;
+        }
+        h->mark_pass.clear();
+        h->mark_a.clear();
+        h->mark_b.clear();
+        h->ev_used = 0;
+    });
+}
+
+int64_t pdgpu_launch_count(pdgpu_t h) { return h ? h->launches : 0; }
 
 // ------------------------------------------------------------ assembly ---
 int pdgpu_build_kernel(int dim, double spacing, double delta, int M, double E, double thickness, double* out) {

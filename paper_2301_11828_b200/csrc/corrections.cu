@@ -106,6 +106,7 @@ static void check(cudaError_t e, const char* what) {
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale) {
     const int64_t N = e.plan.nodes;
     if (e.n_surf > 0) {
+        PassTimer pt(e, kPassCorr, s);
         const int64_t tot = e.n_surf * batch;
         const int th = 256;
         if (e.dim == 2)
@@ -116,6 +117,7 @@ void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaSt
                                                                        e.n_surf, N, batch, scale);
     }
     if (e.n_bond_rows > 0) {
+        PassTimer pt(e, kPassBonds, s);
         const int64_t warps = e.n_bond_rows * batch;
         const int th = 256;
         const int64_t blocks = (warps * 32 + th - 1) / th;
@@ -232,6 +234,7 @@ int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double*
     const int th = 128;
     const int64_t N = pl.nodes;
     const int* negk = (const int*)(e.d_offs + 3 * e.nof);
+    e.launches += 1;
     k_update_bonds<<<(unsigned)((N + th - 1) / th), th, 0, s>>>(u, e.d_ledger, e.d_offs, e.d_disp, negk, A, N,
                                                                e.d_new_pairs, e.new_pairs_cap, e.d_counters,
                                                                e.d_bond_rows, e.d_listed);

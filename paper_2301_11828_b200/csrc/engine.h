@@ -54,6 +54,7 @@ struct Engine {
     double h = 1.0, origin[3] = {0, 0, 0}, delta = 0.0, rho = 1.0;
 
     cudaStream_t stream = nullptr;  // engine-owned default stream
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host-API copy pipeline
     double2* d_tw = nullptr;        // exp(-2 pi i k / TWN)
     void* d_sym = nullptr;          // symbol: real double or double2, np * ncols * Pl
     double* d_K = nullptr;          // stencils on device (np * ss)
@@ -101,6 +102,50 @@ struct Engine {
     double* d_scal = nullptr;          // device scalars
     unsigned int* d_ticket = nullptr;
     double imag_residue = 0.0;
+
+    // per-pass device timing (CUDA events on the launching stream) and the
+    // number of kernels launched -- read by bench.py for the roofline
+    bool timing = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<int> mark_pass;
+    std::vector<cudaEvent_t> mark_a, mark_b;
+    int64_t launches = 0;
+    cudaEvent_t next_event() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t ev;
+            cudaEventCreate(&ev);
+            ev_pool.push_back(ev);
+        }
+        return ev_pool[ev_used++];
+    }
+};
+
+enum PassId { kPassK1 = 0, kPassK2 = 1, kPassK3 = 2, kPassK4 = 3, kPassK5 = 4, kPassCorr = 5, kPassBonds = 6,
+              kPassVec = 7, kNumPass = 8 };
+
+// RAII bracket of one pass with events when e.timing is on
+struct PassTimer {
+    Engine& e;
+    int id;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    PassTimer(Engine& e_, int id_, cudaStream_t s_, int nlaunch = 1) : e(e_), id(id_), s(s_) {
+        e.launches += nlaunch;
+        if (e.timing) {
+            a = e.next_event();
+            cudaEventRecord(a, s);
+        }
+    }
+    ~PassTimer() {
+        if (e.timing) {
+            cudaEvent_t b = e.next_event();
+            cudaEventRecord(b, s);
+            e.mark_pass.push_back(id);
+            e.mark_a.push_back(a);
+            e.mark_b.push_back(b);
+        }
+    }
 };
 
 // spectral.cu

@@ -1,17 +1,21 @@
-// fft.cuh -- CTA-cooperative fp64 FFTs in shared memory for sm_100a.
+// fft.cuh -- register-resident fp64 FFTs for sm_100a.
 //
 // Replaces the FFTW3 C2C executions of the reference (convolution.hpp:114,127,
 // 159).  Transforms are unnormalised, forward = exp(-2*pi*i*k*n/Q) like
-// FFTW_FORWARD.  Every transform length here is a power of two: the GPU pads
-// each axis to P = 2*pow2ceil(N) (>= N+M, so the linear correlation on the
-// window is exact).  The zero half of each padded
-// input is never transformed: a P-point DFT of data with support < P/2 is two
-// P/2-point DFTs (even and odd outputs), which is what the callers do.
+// FFTW_FORWARD.  Every transform length is a power of two: the GPU pads each
+// axis to P = 2*pow2ceil(N) (>= N+M, exact linear correlation on the window,
+// DESIGN.md "Padding"), and the zero half of each padded input is never
+// transformed (a P-point DFT of data supported on [0, P/2) is two P/2-point
+// DFTs -- even and odd outputs -- which the callers run).
 //
-// Algorithm: Stockham autosort, radix-4 stages (one radix-8 or radix-2 stage
-// first when log2 Q is odd), operands staged in shared memory, butterflies in
-// registers.  Each stage loads all of its items into registers, barriers,
-// then stores, so a single buffer is reused in place.
+// Algorithm: Stockham autosort.  A transform of Q = 2^LOGQ points is owned
+// by T = Q/R threads, each holding R points in registers in the "natural"
+// layout  v[j] <-> x[t + j*T].  Passes: one remainder pass of radix
+// 2^(LOGQ mod LOGR) first (no twiddles), then radix-R passes; between passes
+// the data is exchanged once through shared memory (padded one slot every
+// 16 so the 16-byte accesses of every quarter-warp hit distinct banks).  The
+// last pass lands in the natural layout again, so a forward transform, a
+// pointwise product and an inverse transform chain without extra exchanges.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -25,7 +29,7 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 }
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
-// a * (s*i), s = +-1
+// a * (S*i), S = +-1
 template <int S>
 __device__ __forceinline__ double2 cmul_si(double2 a) { return make_double2(-S * a.y, S * a.x); }
 
@@ -37,120 +41,199 @@ __device__ __forceinline__ double2 twiddle(const double2* __restrict__ tw, int i
     return w;
 }
 
-// S = -1 forward, +1 inverse
+// padded shared-memory slot
+__device__ __forceinline__ int spad(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int spad_size(int q) { return q + (q >> 4) + 1; }
+
+// ------------------------------------------------------------ butterflies --
+// multiply by exp(S*2*pi*i*E/16) with compile-time E
+template <int E, int S>
+__device__ __forceinline__ double2 tw16(double2 a) {
+    constexpr int e = E & 15;
+    if constexpr (e == 0) return a;
+    else if constexpr (e == 4) return cmul_si<S>(a);
+    else if constexpr (e == 8) return make_double2(-a.x, -a.y);
+    else if constexpr (e == 12) return cmul_si<-S>(a);
+    else {
+        constexpr double C[16] = {1.0,
+                                  0.92387953251128675613,
+                                  0.70710678118654752440,
+                                  0.38268343236508977173,
+                                  0.0,
+                                  -0.38268343236508977173,
+                                  -0.70710678118654752440,
+                                  -0.92387953251128675613,
+                                  -1.0,
+                                  -0.92387953251128675613,
+                                  -0.70710678118654752440,
+                                  -0.38268343236508977173,
+                                  0.0,
+                                  0.38268343236508977173,
+                                  0.70710678118654752440,
+                                  0.92387953251128675613};
+        constexpr double c = C[e];
+        constexpr double s = S * C[(e + 12) & 15];  // sin(2 pi e/16) = cos(2 pi (e-4)/16)
+        return make_double2(a.x * c - a.y * s, a.x * s + a.y * c);
+    }
+}
+
 template <int S>
 __device__ __forceinline__ void dft2(double2& a, double2& b) {
-    double2 t = a;
+    const double2 t = a;
     a = cadd(t, b);
     b = csub(t, b);
 }
 
 template <int S>
 __device__ __forceinline__ void dft4(double2& x0, double2& x1, double2& x2, double2& x3) {
-    double2 a = cadd(x0, x2), c = csub(x0, x2);
-    double2 b = cadd(x1, x3), d = cmul_si<S>(csub(x1, x3));
+    const double2 a = cadd(x0, x2), c = csub(x0, x2);
+    const double2 b = cadd(x1, x3), d = cmul_si<S>(csub(x1, x3));
     x0 = cadd(a, b);
     x2 = csub(a, b);
     x1 = cadd(c, d);
     x3 = csub(c, d);
 }
 
-template <int S>
-__device__ __forceinline__ void dft8(double2* v) {
-    const double r = 0.70710678118654752440084436210484904;
-    double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
-    double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
-    dft4<S>(e0, e1, e2, e3);
-    dft4<S>(o0, o1, o2, o3);
-    // W8^1 = (1 + S i)/sqrt2, W8^2 = S i, W8^3 = (-1 + S i)/sqrt2
-    double2 t1 = make_double2(r * (o1.x - S * o1.y), r * (o1.y + S * o1.x));
-    double2 t2 = cmul_si<S>(o2);
-    double2 t3 = make_double2(r * (-o3.x - S * o3.y), r * (-o3.y + S * o3.x));
-    v[0] = cadd(e0, o0);
-    v[4] = csub(e0, o0);
-    v[1] = cadd(e1, t1);
-    v[5] = csub(e1, t1);
-    v[2] = cadd(e2, t2);
-    v[6] = csub(e2, t2);
-    v[3] = cadd(e3, t3);
-    v[7] = csub(e3, t3);
-}
-
-template <int R, int S>
-__device__ __forceinline__ void dftR(double2* v) {
-    if constexpr (R == 2) dft2<S>(v[0], v[1]);
-    else if constexpr (R == 4) dft4<S>(v[0], v[1], v[2], v[3]);
-    else dft8<S>(v);
-}
-
-// One Stockham stage of radix R over nb transforms of length Q = 2^logQ held
-// contiguously in buf.  IPT bounds the items per thread: nb*Q/R <= IPT*nthreads.
-template <int R, int S, int IPT>
-__device__ __forceinline__ void stockham_stage(double2* buf, int nb, int logQ, int Ns, int logNsR,
-                                               const double2* __restrict__ tw, int logTWN) {
-    const int Q = 1 << logQ;
-    const int logR = R == 2 ? 1 : (R == 4 ? 2 : 3);
-    const int QR = Q >> logR;
-    const int total = nb * QR;
-    const int nth = blockDim.x;
-    double2 v[IPT][R];
-    int dst[IPT];
-#pragma unroll
-    for (int it = 0; it < IPT; ++it) {
-        const int item = threadIdx.x + it * nth;
-        if (item < total) {
-            const int t = item >> (logQ - logR);
-            const int j = item & (QR - 1);
-            const double2* src = buf + (t << logQ) + j;
-            const int k = j & (Ns - 1);
-#pragma unroll
-            for (int r = 0; r < R; ++r) v[it][r] = src[r * QR];
-            if (Ns > 1) {
-                const int step = k << (logTWN - logNsR);  // k * TWN / (Ns*R)
-#pragma unroll
-                for (int r = 1; r < R; ++r) v[it][r] = cmul(v[it][r], twiddle<S>(tw, step * r));
-            }
-            dftR<R, S>(v[it]);
-            dst[it] = (t << logQ) + ((j - k) << logR) + k;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int it = 0; it < IPT; ++it) {
-        const int item = threadIdx.x + it * nth;
-        if (item < total) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) buf[dst[it] + r * Ns] = v[it][r];
-        }
-    }
-    __syncthreads();
-}
-
-// Full in-place FFT of nb transforms of length 2^logQ in shared memory.
-// Caller must __syncthreads() before (data staged) -- this routine ends with
-// a barrier so results are visible to all threads.
-// IPT must satisfy nb*Q/4 <= IPT*blockDim (radix-4) and nb*Q/8 for radix-8;
-// the radix-2 case only occurs for Q == 2.
-template <int S, int IPT>
-__device__ void block_fft(double2* buf, int nb, int logQ, const double2* __restrict__ tw, int logTWN) {
-    if (logQ == 0) return;
-    int Ns = 1, logNs = 0, l = logQ;
-    if (l == 1) {
-        stockham_stage<2, S, IPT>(buf, nb, logQ, 1, 1, tw, logTWN);
+// in-place DFT of 2^LR points, natural order in and out
+template <int LR, int S>
+__device__ __forceinline__ void dft(double2* v) {
+    if constexpr (LR == 0) {
         return;
-    }
-    if (l & 1) {
-        stockham_stage<8, S, IPT>(buf, nb, logQ, 1, 3, tw, logTWN);
-        Ns = 8;
-        logNs = 3;
-        l -= 3;
-    }
-    while (l >= 2) {
-        stockham_stage<4, S, IPT>(buf, nb, logQ, Ns, logNs + 2, tw, logTWN);
-        Ns <<= 2;
-        logNs += 2;
-        l -= 2;
+    } else if constexpr (LR == 1) {
+        dft2<S>(v[0], v[1]);
+    } else if constexpr (LR == 2) {
+        dft4<S>(v[0], v[1], v[2], v[3]);
+    } else if constexpr (LR == 3) {
+        // 8 = 2 x 4 (DIT): even/odd inputs
+        double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+        double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+        dft4<S>(e0, e1, e2, e3);
+        dft4<S>(o0, o1, o2, o3);
+        o1 = tw16<2, S>(o1);
+        o2 = tw16<4, S>(o2);
+        o3 = tw16<6, S>(o3);
+        v[0] = cadd(e0, o0);
+        v[4] = csub(e0, o0);
+        v[1] = cadd(e1, o1);
+        v[5] = csub(e1, o1);
+        v[2] = cadd(e2, o2);
+        v[6] = csub(e2, o2);
+        v[3] = cadd(e3, o3);
+        v[7] = csub(e3, o3);
+    } else {
+        // 16 = 4 x 4 in place: input m = 4*m1 + m2, output k = k1 + 4*k2.
+        // Column DFT4s over m1 leave A[m2][k1] in v[4*k1 + m2]; after the
+        // twiddles, row DFT4s over m2 leave X[k1 + 4*k2] in v[4*k1 + k2];
+        // the final index permutation is a compile-time register renaming.
+#pragma unroll
+        for (int m2 = 0; m2 < 4; ++m2) dft4<S>(v[m2], v[4 + m2], v[8 + m2], v[12 + m2]);
+        v[5] = tw16<1, S>(v[5]);
+        v[9] = tw16<2, S>(v[9]);
+        v[13] = tw16<3, S>(v[13]);
+        v[6] = tw16<2, S>(v[6]);
+        v[10] = tw16<4, S>(v[10]);
+        v[14] = tw16<6, S>(v[14]);
+        v[7] = tw16<3, S>(v[7]);
+        v[11] = tw16<6, S>(v[11]);
+        v[15] = tw16<9, S>(v[15]);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) dft4<S>(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
+        // transpose 4x4: X[k1 + 4*k2] = v[4*k1 + k2]
+        double2 t;
+        t = v[1]; v[1] = v[4]; v[4] = t;
+        t = v[2]; v[2] = v[8]; v[8] = t;
+        t = v[3]; v[3] = v[12]; v[12] = t;
+        t = v[6]; v[6] = v[9]; v[9] = t;
+        t = v[7]; v[7] = v[13]; v[13] = t;
+        t = v[11]; v[11] = v[14]; v[14] = t;
     }
 }
+
+// --------------------------------------------------------------- plans ----
+// Threads-per-transform and points-per-thread for a length-2^LOGQ transform
+// with at most 2^LOGRMAX points per thread.
+template <int LOGQ, int LOGRMAX>
+struct FftShape {
+    static constexpr int LOGR = LOGQ < LOGRMAX ? LOGQ : LOGRMAX;
+    static constexpr int R = 1 << LOGR;
+    static constexpr int Q = 1 << LOGQ;
+    static constexpr int T = Q / R;
+    static constexpr int LOGT = LOGQ - LOGR;
+    static constexpr int LOGREM = LOGR == 0 ? 0 : LOGQ % LOGR;
+    static constexpr int NFULL = LOGR == 0 ? 0 : LOGQ / LOGR;
+    static constexpr int NPASS = NFULL + (LOGREM ? 1 : 0);
+    static constexpr int XBUF = spad_size(Q);  // exchange slots per transform
+};
+
+// One Stockham pass of radix 2^LR on the R registers of thread t, Ns = 2^LOGNS.
+template <int LOGQ, int LOGR, int LR, int LOGNS, int S>
+__device__ __forceinline__ void fft_pass(double2 (&v)[1 << LOGR], int t, const double2* __restrict__ tw,
+                                         int logTWN) {
+    constexpr int R = 1 << LOGR, r = 1 << LR, nb = R / r;
+    constexpr int T = (1 << LOGQ) / R;
+#pragma unroll
+    for (int i = 0; i < nb; ++i) {
+        double2 w[r];
+#pragma unroll
+        for (int m = 0; m < r; ++m) w[m] = v[i + m * nb];
+        if constexpr (LOGNS > 0) {
+            const int b = t + i * T;
+            const int k = b & ((1 << LOGNS) - 1);
+            const int sh = logTWN - LOGNS - LR;
+#pragma unroll
+            for (int m = 1; m < r; ++m) w[m] = cmul(w[m], twiddle<S>(tw, (k * m) << sh));
+        }
+        dft<LR, S>(w);
+#pragma unroll
+        for (int m = 0; m < r; ++m) v[i + m * nb] = w[m];
+    }
+}
+
+// store after a pass (Stockham destination), barrier, reload natural layout
+template <int LOGQ, int LOGR, int LR, int LOGNS, class Bar>
+__device__ __forceinline__ void fft_exchange(double2 (&v)[1 << LOGR], int t, double2* xb, Bar bar) {
+    constexpr int R = 1 << LOGR, r = 1 << LR, nb = R / r;
+    constexpr int T = (1 << LOGQ) / R;
+#pragma unroll
+    for (int i = 0; i < nb; ++i) {
+        const int b = t + i * T;
+        const int base = ((b >> LOGNS) << (LOGNS + LR)) + (b & ((1 << LOGNS) - 1));
+#pragma unroll
+        for (int m = 0; m < r; ++m) xb[spad(base + (m << LOGNS))] = v[i + m * nb];
+    }
+    bar();
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = xb[spad(t + j * T)];
+    bar();
+}
+
+template <int LOGQ, int LOGR, int S, int P, int LOGNS, class Bar>
+__device__ __forceinline__ void fft_passes(double2 (&v)[1 << LOGR], int t, double2* xb,
+                                           const double2* __restrict__ tw, int logTWN, Bar bar) {
+    using Sh = FftShape<LOGQ, LOGR>;
+    if constexpr (P < Sh::NPASS) {
+        constexpr int LR = (P == 0 && Sh::LOGREM) ? Sh::LOGREM : LOGR;
+        fft_pass<LOGQ, LOGR, LR, LOGNS, S>(v, t, tw, logTWN);
+        if constexpr (P + 1 < Sh::NPASS) {
+            fft_exchange<LOGQ, LOGR, LR, LOGNS>(v, t, xb, bar);
+            fft_passes<LOGQ, LOGR, S, P + 1, LOGNS + LR>(v, t, xb, tw, logTWN, bar);
+        }
+    }
+}
+
+// Full transform: v[j] holds x[t + j*T] on entry and X[t + j*T] on exit.
+// xb: this transform's exchange buffer (FftShape::XBUF slots); bar(): a
+// barrier covering every thread of the transform (all groups of a CTA in
+// lockstep use __syncthreads).
+template <int LOGQ, int LOGRMAX, int S, class Bar>
+__device__ __forceinline__ void reg_fft(double2 (&v)[1 << FftShape<LOGQ, LOGRMAX>::LOGR], int t, double2* xb,
+                                        const double2* __restrict__ tw, int logTWN, Bar bar) {
+    using Sh = FftShape<LOGQ, LOGRMAX>;
+    fft_passes<LOGQ, Sh::LOGR, S, 0, 0>(v, t, xb, tw, logTWN, bar);
+}
+
+struct BlockBar {
+    __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
 
 }  // namespace pdgpu

@@ -6,23 +6,29 @@
 // extraction (inverse_extract :158-172).
 //
 // Pass structure (one vector; B vectors batch into the grid):
-//   K1 rfft_rows   : real rows along x -> half spectrum (Hx = Px/2+1), written
-//                    transposed [kx][row] so the next pass reads contiguously.
+//   K1 rfft_rows   : real rows along x -> half spectrum (Hx = Px/2+1 columns),
+//                    written transposed [kx][row] so K3 reads contiguously.
 //   K2 cfft_y_fwd  : (3D) padded y FFT, written transposed [kx][ky][z].
 //   K3 spectral    : padded FFT along the last axis, d x d symbol multiply,
-//                    inverse FFT, truncation to the window -- fused, one CTA
-//                    per column group, all d components resident in SMEM.
+//                    inverse FFT, truncation to the window -- one fused pass,
+//                    spectra never leave registers between the transforms;
+//                    in place.
 //   K4 cfft_y_inv  : (3D) inverse y FFT + truncation, transposed back.
 //   K5 irfft_rows  : C2R along x + truncation + epilogue (scale, constraint
 //                    mask, body force), written in the reference's node order.
-// The symbol (K9, build_symbol) is conj(G_hat)/prod(P) evaluated once by a
-// direct DFT of the (2M+1)^d stencil: real for the physical (even) stencils,
-// complex for arbitrary ones (the reference's random-stencil tests).
+// All transforms are register-resident Stockham FFTs (fft.cuh).  The symbol
+// (K9) is conj(G_hat)/prod(P) by a direct DFT of the (2M+1)^d stencil: real
+// for the physical (even) stencils, complex for arbitrary ones (the
+// reference's random-stencil tests).  Layout [col][half][k][pair] so each
+// thread reads its n_pairs coefficients contiguously.
 #include <cuda_runtime.h>
 #include <math.h>
 
 #include <algorithm>
 #include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
 
 #include "engine.h"
 #include "fft.cuh"
@@ -34,6 +40,11 @@ static inline int ilog2(int64_t v) {
     while ((int64_t(1) << l) < v) ++l;
     return l;
 }
+
+constexpr int kSmemBudget = 210 * 1024;
+
+static int xbuf_slots(int logq) { return (1 << logq) + ((1 << logq) >> 4) + 1; }
+static int threads_per_transform(int logq, int logrmax) { return 1 << std::max(0, logq - logrmax); }
 
 void plan_init(Plan& pl, int dim, const int* dims) {
     pl.dim = dim;
@@ -57,7 +68,7 @@ void plan_init(Plan& pl, int dim, const int* dims) {
         pl.Pl = pl.P[1];
         pl.logPl = pl.logP[1];
         pl.S1_per_vec = (int64_t)dim * pl.Hx * pl.N[1];
-        pl.S2_per_vec = pl.S1_per_vec;
+        pl.S2_per_vec = pl.S1_per_vec;  // K3 output (out of place, z^0 parked in it)
     } else {
         pl.ncols = pl.Hx * pl.P[1];
         pl.Nl = pl.N[2];
@@ -67,275 +78,389 @@ void plan_init(Plan& pl, int dim, const int* dims) {
         pl.S2_per_vec = (int64_t)dim * pl.Hx * pl.P[1] * pl.N[2];
     }
     pl.logTWN = std::max(pl.logP[0], std::max(pl.logP[1], pl.logP[2]));
-    const int64_t row_bytes = (int64_t)(pl.P[0] / 2) * 16;
-    pl.k1_rows = (int)std::max<int64_t>(1, std::min<int64_t>(8, 131072 / row_bytes));
-    const int64_t col_bytes_both = (int64_t)dim * pl.Pl * 16;
-    if (col_bytes_both <= 200 * 1024) {
-        pl.k3_halves = 2;
-        pl.k3_cols = (int)std::max<int64_t>(1, std::min<int64_t>(8, 98304 / col_bytes_both));
-    } else {
-        pl.k3_halves = 1;
-        pl.k3_cols = 1;
+    // K1/K5: two transforms (even/odd outputs) of Qx points per row
+    {
+        const int T = threads_per_transform(pl.logQx, 4);
+        const int per_row = 2 * xbuf_slots(pl.logQx) * 16;
+        int tr = 1;
+        while (tr < 8 && 2 * (tr * 2) * T <= 512 && (tr * 2) * per_row <= kSmemBudget) tr *= 2;
+        pl.k1_rows = std::min(tr, pl.N[1]);
+    }
+    // K3: columns per CTA
+    {
+        const int logq = pl.logPl - 1;
+        const int logr = dim == 3 ? 3 : 4;
+        const int T = threads_per_transform(logq, logr);
+        const bool zsmem = dim == 3;  // 2D columns are too long to park z^0 on chip
+        const int per_col = (xbuf_slots(logq) + (zsmem ? 2 * dim - 1 : dim - 1) * (1 << logq)) * 16;
+        int nc = 1;
+        while ((nc * 2) * T <= 256 && (nc * 2) * per_col <= kSmemBudget) nc *= 2;
+        pl.k3_cols = nc;
+        pl.k3_halves = zsmem ? 2 : 1;
     }
     if (dim == 3) {
-        const int64_t yrow = (int64_t)pl.P[1] * 16;
-        pl.k2_zt = (int)std::max<int64_t>(1, std::min<int64_t>(8, 65536 / yrow));
-        pl.k2_zt = std::min(pl.k2_zt, pl.N[2]);
+        const int logq = pl.logP[1] - 1;
+        const int T = threads_per_transform(logq, 4);
+        const int per_z = 2 * xbuf_slots(logq) * 16;
+        int zt = 1;
+        while (zt < 8 && 2 * (zt * 2) * T <= 512 && (zt * 2) * per_z <= kSmemBudget) zt *= 2;
+        pl.k2_zt = std::min(zt, pl.N[2]);
     }
 }
 
 // ------------------------------------------------------------------ K1 ---
-template <int IPT>
-__global__ void __launch_bounds__(1024) k_rfft_rows(const double* __restrict__ u, double2* __restrict__ S,
-                                                    int Nx, int Nrow, int Hx, int logQx, int TR,
-                                                    const double2* __restrict__ tw, int logTWN) {
+// Row transform of Nx reals zero-padded to Px = 4*Qx: z[n] = x[2n] + i x[2n+1]
+// (n < Qx carries all data); Z = FFT_{2Qx}(z) via even (E) and odd (O)
+// outputs, each a Qx-point FFT; X[k] = Fe + e^{-2 pi i k/Px} Fo.
+template <int LOGQ>
+__global__ void __launch_bounds__(512) k_rfft_rows(const double* __restrict__ u, double2* __restrict__ S, int Nx,
+                                                   int Nrow, int Hx, int TR, const double2* __restrict__ tw,
+                                                   int logTWN) {
+    using Sh = FftShape<LOGQ, 4>;
+    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
     extern __shared__ double2 sm[];
-    const int Qx = 1 << logQx;
+    const int gi = threadIdx.x >> Sh::LOGT;
+    const int t = threadIdx.x & (T - 1);
+    const int r = gi >> 1, eo = gi & 1;
     const int slab = blockIdx.y;
     const int row0 = blockIdx.x * TR;
     const int nr = min(TR, Nrow - row0);
-    const double* src = u + ((int64_t)slab * Nrow + row0) * Nx;
-    const int shE = logTWN - (logQx + 1);  // exp(-2 pi i n / (2Qx))
-    for (int idx = threadIdx.x; idx < nr * Qx; idx += blockDim.x) {
-        const int r = idx >> logQx, n = idx & (Qx - 1);
+    const bool valid = r < nr;
+    const double* src = u + ((int64_t)slab * Nrow + row0 + r) * Nx;
+    double2* xb = sm + gi * XB;
+    double2 v[R];
+    const int shE = logTWN - (LOGQ + 1);
+    const bool vec = (Nx & 1) == 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int n = t + j * T;
         const int i0 = 2 * n;
-        const double a = i0 < Nx ? src[(int64_t)r * Nx + i0] : 0.0;
-        const double b = i0 + 1 < Nx ? src[(int64_t)r * Nx + i0 + 1] : 0.0;
-        const double2 z = make_double2(a, b);
-        sm[(r << (logQx + 1)) + n] = z;
-        sm[(r << (logQx + 1)) + Qx + n] = cmul(z, __ldg(tw + (n << shE)));
+        double2 z = make_double2(0.0, 0.0);
+        if (valid && i0 < Nx) {
+            if (vec) z = __ldg(reinterpret_cast<const double2*>(src + i0));
+            else z = make_double2(src[i0], i0 + 1 < Nx ? src[i0 + 1] : 0.0);
+        }
+        v[j] = eo ? cmul(z, __ldg(tw + (n << shE))) : z;
     }
+    reg_fft<LOGQ, 4, -1>(v, t, xb, tw, logTWN, BlockBar{});
+#pragma unroll
+    for (int j = 0; j < R; ++j) xb[spad(t + j * T)] = v[j];
     __syncthreads();
-    block_fft<-1, IPT>(sm, 2 * nr, logQx, tw, logTWN);
-    const int halfP = 2 * Qx;
-    const int shX = logTWN - (logQx + 2);  // exp(-2 pi i k / Px)
+    constexpr int halfP = 2 * Q;
+    const int shX = logTWN - (LOGQ + 2);
     for (int idx = threadIdx.x; idx < nr * Hx; idx += blockDim.x) {
-        const int kx = idx / nr, r = idx - kx * nr;
+        const int kx = idx / nr, rr = idx - kx * nr;
         const int k = kx & (halfP - 1);
         const int k2 = (halfP - kx) & (halfP - 1);
-        const double2* Z = sm + (r << (logQx + 1));
-        const double2 A = Z[(k & 1) * Qx + (k >> 1)];
-        const double2 B = cconj(Z[(k2 & 1) * Qx + (k2 >> 1)]);
+        const double2* Z = sm + 2 * rr * XB;
+        const double2 A = Z[(k & 1) * XB + spad(k >> 1)];
+        const double2 B = cconj(Z[(k2 & 1) * XB + spad(k2 >> 1)]);
         const double2 Fe = cscale(cadd(A, B), 0.5);
         const double2 D = csub(A, B);
         const double2 Fo = make_double2(0.5 * D.y, -0.5 * D.x);
         const double2 W = __ldg(tw + (kx << shX));
-        S[((int64_t)slab * Hx + kx) * Nrow + row0 + r] = cadd(Fe, cmul(W, Fo));
+        S[((int64_t)slab * Hx + kx) * Nrow + row0 + rr] = cadd(Fe, cmul(W, Fo));
     }
 }
 
 // ------------------------------------------------------------------ K5 ---
-template <int IPT, bool MASK, bool BODY>
-__global__ void __launch_bounds__(1024) k_irfft_rows(const double2* __restrict__ S, double* __restrict__ f,
-                                                     int Nx, int Nrow, int Nz, int dim, int Hx, int logQx,
-                                                     int TR, const double2* __restrict__ tw, int logTWN,
-                                                     double scale, const uint8_t* __restrict__ cmask,
-                                                     const double* __restrict__ body, int64_t nodes) {
+// C2R: Z[k] = (X[k] + conj X[h-k]) + i e^{+2 pi i k/Px} (X[k] - conj X[h-k]),
+// h = Px/2; z = IFFT_{2Qx}(Z) on its first Qx outputs = E'[n] + e^{+2 pi i n/(2Qx)} O'[n];
+// x[2n] = Re z, x[2n+1] = Im z.
+template <int LOGQ>
+__global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ S, double* __restrict__ f, int Nx,
+                                                    int Nrow, int Nz, int dim, int Hx, int TR,
+                                                    const double2* __restrict__ tw, int logTWN, double scale,
+                                                    const uint8_t* __restrict__ cmask,
+                                                    const double* __restrict__ body, int64_t nodes) {
+    using Sh = FftShape<LOGQ, 4>;
+    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
     extern __shared__ double2 sm[];
-    const int Qx = 1 << logQx;
-    const int halfP = 2 * Qx;
+    const int gi = threadIdx.x >> Sh::LOGT;
+    const int t = threadIdx.x & (T - 1);
+    const int eo = gi & 1;
     const int slab = blockIdx.y;
     const int row0 = blockIdx.x * TR;
     const int nr = min(TR, Nrow - row0);
-    const int shX = logTWN - (logQx + 2);  // exp(+2 pi i k / Px)
+    constexpr int halfP = 2 * Q;
+    const int shX = logTWN - (LOGQ + 2);
     const double2* src = S + (int64_t)slab * Hx * Nrow + row0;
-    // Z[k] = (X[k] + conj X[h-k]) + i e^{+2 pi i k/Px} (X[k] - conj X[h-k]),  h = Px/2
-    for (int idx = threadIdx.x; idx < nr * (Qx + 1); idx += blockDim.x) {
-        const int k = idx / nr, r = idx - k * nr;
+    for (int idx = threadIdx.x; idx < nr * (Q + 1); idx += blockDim.x) {
+        const int k = idx / nr, rr = idx - k * nr;
         const int k2 = halfP - k;
-        const double2 Xa = src[(int64_t)k * Nrow + r];
-        const double2 Xb = src[(int64_t)k2 * Nrow + r];
-        double2* Z = sm + (r << (logQx + 1));
+        const double2 Xa = src[(int64_t)k * Nrow + rr];
+        const double2 Xb = src[(int64_t)k2 * Nrow + rr];
+        double2* Z = sm + 2 * rr * XB;
         {
             const double2 s = cadd(Xa, cconj(Xb));
-            const double2 dd = csub(Xa, cconj(Xb));
-            const double2 W = twiddle<1>(tw, k << shX);
-            const double2 t = cmul(W, dd);
-            const double2 z = make_double2(s.x - t.y, s.y + t.x);
-            Z[(k & 1) * Qx + (k >> 1)] = z;
+            const double2 t2 = cmul(twiddle<1>(tw, k << shX), csub(Xa, cconj(Xb)));
+            Z[(k & 1) * XB + spad(k >> 1)] = make_double2(s.x - t2.y, s.y + t2.x);
         }
-        if (k != 0 && k != Qx) {
+        if (k != 0 && k != Q) {
             const double2 s = cadd(Xb, cconj(Xa));
-            const double2 dd = csub(Xb, cconj(Xa));
-            const double2 W = twiddle<1>(tw, k2 << shX);
-            const double2 t = cmul(W, dd);
-            const double2 z = make_double2(s.x - t.y, s.y + t.x);
-            Z[(k2 & 1) * Qx + (k2 >> 1)] = z;
+            const double2 t2 = cmul(twiddle<1>(tw, k2 << shX), csub(Xb, cconj(Xa)));
+            Z[(k2 & 1) * XB + spad(k2 >> 1)] = make_double2(s.x - t2.y, s.y + t2.x);
         }
     }
     __syncthreads();
-    block_fft<1, IPT>(sm, 2 * nr, logQx, tw, logTWN);
-    const int shE = logTWN - (logQx + 1);  // exp(+2 pi i n / (2Qx))
+    double2* xb = sm + gi * XB;
+    double2 v[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = xb[spad(t + j * T)];
+    __syncthreads();
+    reg_fft<LOGQ, 4, 1>(v, t, xb, tw, logTWN, BlockBar{});
+    const int shE = logTWN - (LOGQ + 1);
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int n = t + j * T;
+        xb[spad(n)] = eo ? cmul(twiddle<1>(tw, n << shE), v[j]) : v[j];
+    }
+    __syncthreads();
     const int a = (slab / Nz) % dim;
     const int z = slab % Nz;
     double* dst = f + ((int64_t)slab * Nrow + row0) * Nx;
-    for (int idx = threadIdx.x; idx < nr * Qx; idx += blockDim.x) {
-        const int r = idx >> logQx, n = idx & (Qx - 1);
+    const bool vec = (Nx & 1) == 0;
+    for (int idx = threadIdx.x; idx < nr * Q; idx += blockDim.x) {
+        const int rr = idx >> LOGQ, n = idx & (Q - 1);
         const int i0 = 2 * n;
         if (i0 >= Nx) continue;
-        const double2* Z = sm + (r << (logQx + 1));
-        const double2 zz = cadd(Z[n], cmul(twiddle<1>(tw, n << shE), Z[Qx + n]));
-        const int64_t node = ((int64_t)z * Nrow + row0 + r) * Nx + i0;
+        const double2 zz = cadd(sm[2 * rr * XB + spad(n)], sm[(2 * rr + 1) * XB + spad(n)]);
         double v0 = zz.x * scale, v1 = zz.y * scale;
-        if (BODY) {
+        const int64_t node = ((int64_t)z * Nrow + row0 + rr) * Nx + i0;
+        const bool two = i0 + 1 < Nx;
+        if (body) {
             v0 += body[(int64_t)a * nodes + node];
-            if (i0 + 1 < Nx) v1 += body[(int64_t)a * nodes + node + 1];
+            if (two) v1 += body[(int64_t)a * nodes + node + 1];
         }
-        if (MASK) {
+        if (cmask) {
             if ((cmask[node] >> a) & 1u) v0 = 0.0;
-            if (i0 + 1 < Nx && ((cmask[node + 1] >> a) & 1u)) v1 = 0.0;
+            if (two && ((cmask[node + 1] >> a) & 1u)) v1 = 0.0;
         }
-        dst[(int64_t)r * Nx + i0] = v0;
-        if (i0 + 1 < Nx) dst[(int64_t)r * Nx + i0 + 1] = v1;
+        double* o = dst + (int64_t)rr * Nx + i0;
+        if (vec) {
+            *reinterpret_cast<double2*>(o) = make_double2(v0, v1);
+        } else {
+            o[0] = v0;
+            if (two) o[1] = v1;
+        }
     }
 }
 
 // ------------------------------------------------------------------ K3 ---
-// Columns: in[((b*D + c)*ncols + col)*Nl + n], n < Nl.  Symbol H[(pair*ncols + col)*Pl + k].
-// SMEM layout [cc][c][hh][Ql].  NH = 2: both half spectra resident (in-place
-// allowed).  NH = 1: the two halves run back to back, the second accumulates
-// into `out` (out must not alias in).
+// Columns in[((b*D + c)*ncols + col)*Nl + n], n < Nl, zero-padded to Pl = 2Ql.
+// Half h (ky = 2k + h): U_c = FFT_Ql(x_c[n] e^{-2 pi i h n/Pl}); F_a = sum_c
+// H[col][h][k][pair(a,c)] U_c; z_a^h = IFFT_Ql(F_a);  y_a[n] = z_a^0[n] +
+// e^{+2 pi i n/Pl} z_a^1[n].  z^0 is parked in SMEM (thread-private slots).
 template <int D>
 __device__ __forceinline__ int pair_of(int a, int b) {
-    if (a > b) { const int t = a; a = b; b = t; }
+    if (a > b) {
+        const int t = a;
+        a = b;
+        b = t;
+    }
     if (D == 2) return a + b;
     return (a == 0 ? 0 : (a == 1 ? 3 : 5)) + b - a;
 }
 
-template <int IPT, int D, bool REAL>
-__global__ void __launch_bounds__(1024) k_spectral(const double2* in, double2* out, const void* __restrict__ sym,
-                                                   int ncols, int Nl, int logPl, int NC, int NH,
-                                                   const double2* __restrict__ tw, int logTWN) {
+// Only one component's spectrum is live in registers at a time; the other
+// d-1 wait in thread-private SMEM slots (`cpark`).  The half-0 result z^0 is
+// parked either in SMEM (ZSMEM, small columns; in place allowed) or in `out`
+// itself (large 2D columns; `out` must not alias `in`, the second half
+// re-reads `in` and read-modify-writes `out`).
+template <int D, bool REAL>
+__device__ __forceinline__ void symbol_product(double2* F, const double2* U, const void* __restrict__ sym,
+                                               int64_t fidx) {
+    constexpr int NP = D * (D + 1) / 2;
+    if (REAL) {
+        const double* H = (const double*)sym + fidx * NP;
+        double g[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) g[p] = __ldg(H + p);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+                const double gg = g[pair_of<D>(a, c)];
+                acc.x += gg * U[c].x;
+                acc.y += gg * U[c].y;
+            }
+            F[a] = acc;
+        }
+    } else {
+        const double2* H = (const double2*)sym + fidx * NP;
+        double2 g[NP];
+#pragma unroll
+        for (int p = 0; p < NP; ++p) g[p] = __ldg(H + p);
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc = cadd(acc, cmul(g[pair_of<D>(a, c)], U[c]));
+            F[a] = acc;
+        }
+    }
+}
+
+template <int LOGQ, int D, bool REAL, int LOGR, bool ZSMEM>
+__global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2* out, const void* __restrict__ sym,
+                                                     int ncols, int Nl, int NC, const double2* __restrict__ tw,
+                                                     int logTWN) {
+    using Sh = FftShape<LOGQ, LOGR>;
+    constexpr int Q = Sh::Q, T = Sh::T, XB = Sh::XBUF;
+    constexpr int RR = Sh::R;
     extern __shared__ double2 sm[];
-    const int logQl = logPl - 1;
-    const int Ql = 1 << logQl;
-    const int Pl = 1 << logPl;
-    const int col0 = blockIdx.x * NC;
-    const int nc = min(NC, ncols - col0);
+    const int gi = threadIdx.x >> Sh::LOGT;
+    const int t = threadIdx.x & (T - 1);
+    const int col = blockIdx.x * NC + gi;
     const int b = blockIdx.y;
-    const int shP = logTWN - logPl;  // exp(-+2 pi i n / Pl)
-    const int npass = NH == 2 ? 1 : 2;
-    for (int pass = 0; pass < npass; ++pass) {
-        // load (+ odd-half pre-twiddle)
-        for (int idx = threadIdx.x; idx < nc * D * Ql; idx += blockDim.x) {
-            const int n = idx & (Ql - 1);
-            const int t = idx >> logQl;  // cc*D + c
-            const int cc = t / D, c = t - cc * D;
-            double2 v = make_double2(0.0, 0.0);
-            if (n < Nl) v = in[((int64_t)(b * D + c) * ncols + col0 + cc) * Nl + n];
-            if (NH == 2) {
-                sm[((t * 2) << logQl) + n] = v;
-                sm[((t * 2 + 1) << logQl) + n] = cmul(v, __ldg(tw + (n << shP)));
-            } else {
-                sm[(t << logQl) + n] = pass ? cmul(v, __ldg(tw + (n << shP))) : v;
+    const bool valid = col < ncols;
+    double2* xb = sm + gi * XB;
+    // per column: (D-1)*Q component park, then (ZSMEM) D*Q half-0 park
+    double2* cpark = sm + NC * XB + (int64_t)gi * (ZSMEM ? 2 * D - 1 : D - 1) * Q;
+    double2* zpark = cpark + (D - 1) * Q;
+    const int shP = logTWN - (LOGQ + 1);
+    double2 v[RR];
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll 1
+        for (int c = 0; c < D; ++c) {
+            const double2* src = in + ((int64_t)(b * D + c) * ncols + col) * Nl;
+#pragma unroll
+            for (int j = 0; j < RR; ++j) {
+                const int n = t + j * T;
+                double2 x = make_double2(0.0, 0.0);
+                if (valid && n < Nl) x = src[n];
+                v[j] = h ? cmul(x, __ldg(tw + (n << shP))) : x;
+            }
+            reg_fft<LOGQ, LOGR, -1>(v, t, xb, tw, logTWN, BlockBar{});
+            if (c < D - 1) {
+#pragma unroll
+                for (int j = 0; j < RR; ++j) cpark[c * Q + j * T + t] = v[j];
             }
         }
-        __syncthreads();
-        block_fft<-1, IPT>(sm, nc * D * NH, logQl, tw, logTWN);
-        // per-frequency d x d product with the symbol
-        for (int idx = threadIdx.x; idx < nc * NH * Ql; idx += blockDim.x) {
-            const int m = idx & (Ql - 1);
-            const int rest = idx >> logQl;  // cc*NH + hh
-            const int cc = rest / NH, hh = rest - cc * NH;
-            const int h = NH == 2 ? hh : pass;
-            const int ky = 2 * m + h;
-            const int col = col0 + cc;
-            double2 U[D];
+        // per-frequency d x d product (ky = 2k + h); last component in v
+        const int64_t sbase = ((int64_t)(valid ? col : 0) * 2 + h) * Q;
 #pragma unroll
-            for (int c = 0; c < D; ++c) U[c] = sm[(((cc * D + c) * NH + hh) << logQl) + m];
+        for (int j = 0; j < RR; ++j) {
+            const int k = t + j * T;
+            double2 U[D], F[D];
 #pragma unroll
-            for (int a = 0; a < D; ++a) {
-                double2 acc = make_double2(0.0, 0.0);
+            for (int c = 0; c < D - 1; ++c) U[c] = cpark[c * Q + j * T + t];
+            U[D - 1] = v[j];
+            symbol_product<D, REAL>(F, U, sym, sbase + k);
 #pragma unroll
-                for (int c = 0; c < D; ++c) {
-                    const int64_t si = ((int64_t)pair_of<D>(a, c) * ncols + col) * Pl + ky;
-                    if (REAL) {
-                        const double g = __ldg((const double*)sym + si);
-                        acc.x += g * U[c].x;
-                        acc.y += g * U[c].y;
-                    } else {
-                        acc = cadd(acc, cmul(__ldg((const double2*)sym + si), U[c]));
-                    }
+            for (int a = 0; a < D - 1; ++a) cpark[a * Q + j * T + t] = F[a];
+            v[j] = F[D - 1];
+        }
+#pragma unroll 1
+        for (int ai = 0; ai < D; ++ai) {
+            const int a = D - 1 - ai;  // the component already in registers first
+            if (ai > 0) {
+#pragma unroll
+                for (int j = 0; j < RR; ++j) v[j] = cpark[a * Q + j * T + t];
+            }
+            reg_fft<LOGQ, LOGR, 1>(v, t, xb, tw, logTWN, BlockBar{});
+            double2* dst = out + ((int64_t)(b * D + a) * ncols + col) * Nl;
+#pragma unroll
+            for (int j = 0; j < RR; ++j) {
+                const int n = t + j * T;
+                if (ZSMEM) {
+                    double2* zp = zpark + a * Q + j * T + t;
+                    if (h == 0) *zp = v[j];
+                    else if (valid && n < Nl) dst[n] = cadd(*zp, cmul(twiddle<1>(tw, n << shP), v[j]));
+                } else if (valid && n < Nl) {
+                    if (h == 0) dst[n] = v[j];
+                    else dst[n] = cadd(dst[n], cmul(twiddle<1>(tw, n << shP), v[j]));
                 }
-                sm[(((cc * D + a) * NH + hh) << logQl) + m] = acc;
             }
         }
-        __syncthreads();
-        block_fft<1, IPT>(sm, nc * D * NH, logQl, tw, logTWN);
-        // combine halves, truncate to the window, store
-        for (int idx = threadIdx.x; idx < nc * D * Nl; idx += blockDim.x) {
-            const int t = idx / Nl, n = idx - t * Nl;
-            const int cc = t / D, a = t - cc * D;
-            const int64_t o = ((int64_t)(b * D + a) * ncols + col0 + cc) * Nl + n;
-            double2 y;
-            if (NH == 2) {
-                y = cadd(sm[((t * 2) << logQl) + n],
-                         cmul(twiddle<1>(tw, n << shP), sm[((t * 2 + 1) << logQl) + n]));
-            } else {
-                y = sm[(t << logQl) + n];
-                if (pass) y = cadd(out[o], cmul(twiddle<1>(tw, n << shP), y));
-            }
-            out[o] = y;
-        }
-        __syncthreads();
     }
 }
 
 // ------------------------------------------------------- K2 / K4 (3D) ---
-template <int IPT>
-__global__ void __launch_bounds__(1024) k_cfft_y_fwd(const double2* __restrict__ S1, double2* __restrict__ S2,
-                                                     int Ny, int Nz, int Hx, int logPy, int ZT,
-                                                     const double2* __restrict__ tw, int logTWN) {
+template <int LOGQ>
+__global__ void __launch_bounds__(512) k_cfft_y_fwd(const double2* __restrict__ S1, double2* __restrict__ S2, int Ny,
+                                                    int Nz, int Hx, int ZT, const double2* __restrict__ tw,
+                                                    int logTWN) {
+    using Sh = FftShape<LOGQ, 4>;
+    constexpr int T = Sh::T, R = Sh::R, XB = Sh::XBUF;
+    constexpr int Py = 2 * Sh::Q;
     extern __shared__ double2 sm[];
-    const int logQ = logPy - 1, Q = 1 << logQ, Py = 1 << logPy;
+    const int gi = threadIdx.x >> Sh::LOGT;
+    const int t = threadIdx.x & (T - 1);
+    const int zz = gi >> 1, eo = gi & 1;
     const int z0 = blockIdx.x * ZT;
     const int nz = min(ZT, Nz - z0);
     const int kx = blockIdx.y;
     const int bd = blockIdx.z;
-    const int shP = logTWN - logPy;
-    for (int idx = threadIdx.x; idx < nz * Q; idx += blockDim.x) {
-        const int zz = idx >> logQ, n = idx & (Q - 1);
-        double2 v = make_double2(0.0, 0.0);
-        if (n < Ny) v = S1[(((int64_t)bd * Nz + z0 + zz) * Hx + kx) * Ny + n];
-        sm[((zz * 2) << logQ) + n] = v;
-        sm[((zz * 2 + 1) << logQ) + n] = cmul(v, __ldg(tw + (n << shP)));
+    const bool valid = zz < nz;
+    const int shP = logTWN - (LOGQ + 1);
+    const double2* src = S1 + (((int64_t)bd * Nz + z0 + zz) * Hx + kx) * Ny;
+    double2* xb = sm + gi * XB;
+    double2 v[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int n = t + j * T;
+        double2 x = make_double2(0.0, 0.0);
+        if (valid && n < Ny) x = src[n];
+        v[j] = eo ? cmul(x, __ldg(tw + (n << shP))) : x;
     }
+    reg_fft<LOGQ, 4, -1>(v, t, xb, tw, logTWN, BlockBar{});
+#pragma unroll
+    for (int j = 0; j < R; ++j) xb[spad(t + j * T)] = v[j];
     __syncthreads();
-    block_fft<-1, IPT>(sm, 2 * nz, logQ, tw, logTWN);
     for (int idx = threadIdx.x; idx < Py * nz; idx += blockDim.x) {
-        const int ky = idx / nz, zz = idx - ky * nz;
-        S2[(((int64_t)bd * Hx + kx) * Py + ky) * Nz + z0 + zz] = sm[((zz * 2 + (ky & 1)) << logQ) + (ky >> 1)];
+        const int ky = idx / nz, z = idx - ky * nz;
+        S2[(((int64_t)bd * Hx + kx) * Py + ky) * Nz + z0 + z] = sm[(2 * z + (ky & 1)) * XB + spad(ky >> 1)];
     }
 }
 
-template <int IPT>
-__global__ void __launch_bounds__(1024) k_cfft_y_inv(const double2* __restrict__ S2, double2* __restrict__ S1,
-                                                     int Ny, int Nz, int Hx, int logPy, int ZT,
-                                                     const double2* __restrict__ tw, int logTWN) {
+template <int LOGQ>
+__global__ void __launch_bounds__(512) k_cfft_y_inv(const double2* __restrict__ S2, double2* __restrict__ S1, int Ny,
+                                                    int Nz, int Hx, int ZT, const double2* __restrict__ tw,
+                                                    int logTWN) {
+    using Sh = FftShape<LOGQ, 4>;
+    constexpr int T = Sh::T, R = Sh::R, XB = Sh::XBUF;
+    constexpr int Py = 2 * Sh::Q;
     extern __shared__ double2 sm[];
-    const int logQ = logPy - 1, Py = 1 << logPy;
+    const int gi = threadIdx.x >> Sh::LOGT;
+    const int t = threadIdx.x & (T - 1);
+    const int eo = gi & 1;
     const int z0 = blockIdx.x * ZT;
     const int nz = min(ZT, Nz - z0);
     const int kx = blockIdx.y;
     const int bd = blockIdx.z;
-    const int shP = logTWN - logPy;
+    const int shP = logTWN - (LOGQ + 1);
     for (int idx = threadIdx.x; idx < Py * nz; idx += blockDim.x) {
-        const int ky = idx / nz, zz = idx - ky * nz;
-        sm[((zz * 2 + (ky & 1)) << logQ) + (ky >> 1)] = S2[(((int64_t)bd * Hx + kx) * Py + ky) * Nz + z0 + zz];
+        const int ky = idx / nz, z = idx - ky * nz;
+        sm[(2 * z + (ky & 1)) * XB + spad(ky >> 1)] = S2[(((int64_t)bd * Hx + kx) * Py + ky) * Nz + z0 + z];
     }
     __syncthreads();
-    block_fft<1, IPT>(sm, 2 * nz, logQ, tw, logTWN);
+    double2* xb = sm + gi * XB;
+    double2 v[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) v[j] = xb[spad(t + j * T)];
+    __syncthreads();
+    reg_fft<LOGQ, 4, 1>(v, t, xb, tw, logTWN, BlockBar{});
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int n = t + j * T;
+        xb[spad(n)] = eo ? cmul(twiddle<1>(tw, n << shP), v[j]) : v[j];
+    }
+    __syncthreads();
     for (int idx = threadIdx.x; idx < nz * Ny; idx += blockDim.x) {
-        const int zz = idx / Ny, n = idx - zz * Ny;
-        const double2 y = cadd(sm[((zz * 2) << logQ) + n], cmul(twiddle<1>(tw, n << shP), sm[((zz * 2 + 1) << logQ) + n]));
-        S1[(((int64_t)bd * Nz + z0 + zz) * Hx + kx) * Ny + n] = y;
+        const int z = idx / Ny, n = idx - z * Ny;
+        S1[(((int64_t)bd * Nz + z0 + z) * Hx + kx) * Ny + n] =
+            cadd(sm[2 * z * XB + spad(n)], sm[(2 * z + 1) * XB + spad(n)]);
     }
 }
 
 // ------------------------------------------------------------ symbol K9 --
 // H(k) = scale * sum_o K(o) exp(+2 pi i k.o / P) = conj(G_hat(k)) / prod(P)
 // (convolution.hpp:107-116 embeds K at wrapped offsets and FFTs; the product
-// at :140-153 uses conj(G_hat)).  Direct DFT over the stencil, phases exact.
+// at :140-153 uses conj(G_hat)).  Exact rational phases via sincospi.
+// Output layout [col][h][k][pair], ky = 2k + h.
 __global__ void k_build_symbol(void* sym, const double* __restrict__ K, int dim, int M, int np, int64_t ss,
                                int ncols, int Pl, int P0, int P1, int P2, int real, double scale) {
     const int64_t nfreq = (int64_t)ncols * Pl;
@@ -343,20 +468,27 @@ __global__ void k_build_symbol(void* sym, const double* __restrict__ K, int dim,
     if (idx >= nfreq) return;
     const int col = (int)(idx / Pl), kl = (int)(idx % Pl);
     int k0, k1, k2;
-    if (dim == 2) { k0 = col; k1 = kl; k2 = 0; }
-    else { k0 = col / P1; k1 = col % P1; k2 = kl; }
+    if (dim == 2) {
+        k0 = col;
+        k1 = kl;
+        k2 = 0;
+    } else {
+        k0 = col / P1;
+        k1 = col % P1;
+        k2 = kl;
+    }
     const int side = 2 * M + 1;
     double2 ex[17], ey[17], ez[17];
     for (int o = -M; o <= M; ++o) {
         double s, c;
-        int m0 = (int)(((int64_t)k0 * (o + P0)) % P0);
+        const int m0 = (int)(((int64_t)k0 * (o + P0)) % P0);
         sincospi(2.0 * (double)m0 / (double)P0, &s, &c);
         ex[o + M] = make_double2(c, s);
-        int m1 = (int)(((int64_t)k1 * (o + P1)) % P1);
+        const int m1 = (int)(((int64_t)k1 * (o + P1)) % P1);
         sincospi(2.0 * (double)m1 / (double)P1, &s, &c);
         ey[o + M] = make_double2(c, s);
         if (dim == 3) {
-            int m2 = (int)(((int64_t)k2 * (o + P2)) % P2);
+            const int m2 = (int)(((int64_t)k2 * (o + P2)) % P2);
             sincospi(2.0 * (double)m2 / (double)P2, &s, &c);
             ez[o + M] = make_double2(c, s);
         } else {
@@ -381,10 +513,11 @@ __global__ void k_build_symbol(void* sym, const double* __restrict__ K, int dim,
                 }
             }
         }
+    const int Ql = Pl / 2;
+    const int64_t o = (((int64_t)col * 2 + (kl & 1)) * Ql + (kl >> 1)) * np;
     for (int p = 0; p < np; ++p) {
-        const int64_t o = (int64_t)p * nfreq + idx;
-        if (real) ((double*)sym)[o] = acc[p].x * scale;
-        else ((double2*)sym)[o] = make_double2(acc[p].x * scale, acc[p].y * scale);
+        if (real) ((double*)sym)[o + p] = acc[p].x * scale;
+        else ((double2*)sym)[o + p] = make_double2(acc[p].x * scale, acc[p].y * scale);
     }
 }
 
@@ -393,57 +526,65 @@ static void check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-#define PDGPU_SMEM_ATTR(...) \
-    check(cudaFuncSetAttribute(__VA_ARGS__, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448), "smem attr")
+static void smem_attr(const void* fn) {
+    check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448), "smem attr");
+}
 
-template <int IPT>
-static void set_attrs_ipt() {
-    PDGPU_SMEM_ATTR(k_rfft_rows<IPT>);
-    PDGPU_SMEM_ATTR(k_irfft_rows<IPT, false, false>);
-    PDGPU_SMEM_ATTR(k_irfft_rows<IPT, true, false>);
-    PDGPU_SMEM_ATTR(k_irfft_rows<IPT, true, true>);
-    PDGPU_SMEM_ATTR(k_irfft_rows<IPT, false, true>);
-    PDGPU_SMEM_ATTR(k_spectral<IPT, 2, true>);
-    PDGPU_SMEM_ATTR(k_spectral<IPT, 2, false>);
-    PDGPU_SMEM_ATTR(k_spectral<IPT, 3, true>);
-    PDGPU_SMEM_ATTR(k_spectral<IPT, 3, false>);
-    PDGPU_SMEM_ATTR(k_cfft_y_fwd<IPT>);
-    PDGPU_SMEM_ATTR(k_cfft_y_inv<IPT>);
+template <int L>
+static void set_attrs_l() {
+    smem_attr((const void*)k_rfft_rows<L>);
+    smem_attr((const void*)k_irfft_rows<L>);
+    smem_attr((const void*)k_spectral<L, 2, true, 4, false>);
+    smem_attr((const void*)k_spectral<L, 2, false, 4, false>);
+    if constexpr (L <= 9) {
+        smem_attr((const void*)k_spectral<L, 3, true, 3, true>);
+        smem_attr((const void*)k_spectral<L, 3, false, 3, true>);
+        smem_attr((const void*)k_cfft_y_fwd<L>);
+        smem_attr((const void*)k_cfft_y_inv<L>);
+    }
+}
+
+template <int... Ls>
+static void set_attrs_all(std::integer_sequence<int, Ls...>) {
+    (set_attrs_l<Ls + 1>(), ...);
 }
 
 void set_kernel_attributes() {
-    set_attrs_ipt<1>();
-    set_attrs_ipt<2>();
-    set_attrs_ipt<4>();
-    set_attrs_ipt<8>();
+    static bool done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && done[dev]) return;
+    set_attrs_all(std::make_integer_sequence<int, 12>{});
+    if (dev < 64) done[dev] = true;
 }
 
-// threads and items-per-thread for a block FFT with `items` radix-4 work items
-static void pick_threads(int64_t items, int& nth, int& ipt) {
-    nth = 64;
-    while (nth < 1024 && (items + nth - 1) / nth > 4) nth <<= 1;
-    int64_t need = (items + nth - 1) / nth;
-    ipt = need <= 1 ? 1 : need <= 2 ? 2 : need <= 4 ? 4 : 8;
-    if (need > 8) throw std::runtime_error("FFT tile too large for one CTA");
-}
-
-#define DISPATCH_IPT(ipt, KCALL)                     \
-    switch (ipt) {                                   \
-        case 1: { constexpr int I = 1; KCALL; } break; \
-        case 2: { constexpr int I = 2; KCALL; } break; \
-        case 4: { constexpr int I = 4; KCALL; } break; \
-        default: { constexpr int I = 8; KCALL; } break; \
+// runtime log2 -> compile-time template dispatch over [1, 12]
+#define PDGPU_CASE(L, CALL) \
+    case L: {               \
+        constexpr int LQ = L; \
+        CALL;               \
+    } break;
+#define PDGPU_DISPATCH_LOGQ(lq, CALL)                                                                       \
+    switch (lq) {                                                                                           \
+        PDGPU_CASE(1, CALL) PDGPU_CASE(2, CALL) PDGPU_CASE(3, CALL) PDGPU_CASE(4, CALL) PDGPU_CASE(5, CALL) \
+        PDGPU_CASE(6, CALL) PDGPU_CASE(7, CALL) PDGPU_CASE(8, CALL) PDGPU_CASE(9, CALL)                     \
+        PDGPU_CASE(10, CALL) PDGPU_CASE(11, CALL) PDGPU_CASE(12, CALL)                                      \
+        default: throw std::runtime_error("transform length out of range");                                 \
+    }
+#define PDGPU_DISPATCH_LOGQ9(lq, CALL)                                                                      \
+    switch (lq) {                                                                                           \
+        PDGPU_CASE(1, CALL) PDGPU_CASE(2, CALL) PDGPU_CASE(3, CALL) PDGPU_CASE(4, CALL) PDGPU_CASE(5, CALL) \
+        PDGPU_CASE(6, CALL) PDGPU_CASE(7, CALL) PDGPU_CASE(8, CALL) PDGPU_CASE(9, CALL)                     \
+        default: throw std::runtime_error("3D transform length out of range");                              \
     }
 
 void build_twiddles(Engine& e) {
     const int n = 1 << e.plan.logTWN;
     std::vector<double2> tw(n);
     for (int k = 0; k < n; ++k) {
-        // exact-argument evaluation in long double
         const long double ang = -2.0L * 3.141592653589793238462643383279502884L * (long double)k / (long double)n;
         tw[k] = make_double2((double)cosl(ang), (double)sinl(ang));
     }
-    // enforce exact symmetric values at the quarter points
     tw[0] = make_double2(1.0, 0.0);
     if (n >= 4) {
         tw[n / 4] = make_double2(0.0, -1.0);
@@ -477,8 +618,7 @@ void engine_alloc_workspace(Engine& e, int64_t batch) {
     e.d_S1 = e.d_S2 = nullptr;
     const Plan& pl = e.plan;
     check(cudaMalloc(&e.d_S1, sizeof(double2) * pl.S1_per_vec * batch), "alloc S1");
-    const bool need_s2 = pl.dim == 3 || pl.k3_halves == 1;
-    if (need_s2) check(cudaMalloc(&e.d_S2, sizeof(double2) * pl.S2_per_vec * batch), "alloc S2");
+    if (pl.S2_per_vec) check(cudaMalloc(&e.d_S2, sizeof(double2) * pl.S2_per_vec * batch), "alloc S2");
     e.cap_batch = batch;
 }
 
@@ -488,84 +628,79 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
     engine_alloc_workspace(e, batch);
     const int d = pl.dim;
     const int Nx = pl.N[0], Ny = pl.N[1], Nz = pl.N[2];
-    const int Qx = 1 << pl.logQx;
     const int nslab = batch * d * Nz;
+    const int lqx = pl.logQx;
     // K1
     {
+        PassTimer pt(e, kPassK1, s);
         const int TR = pl.k1_rows;
-        int nth, ipt;
-        pick_threads((int64_t)2 * TR * Qx / 4 + 1, nth, ipt);
+        const int T = threads_per_transform(lqx, 4);
         dim3 grid((Ny + TR - 1) / TR, nslab);
-        const size_t smem = sizeof(double2) * (size_t)TR * 2 * Qx;
-        DISPATCH_IPT(ipt, (k_rfft_rows<I><<<grid, nth, smem, s>>>(u, e.d_S1, Nx, Ny, pl.Hx, pl.logQx, TR, e.d_tw,
-                                                                   pl.logTWN)));
+        const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_slots(lqx);
+        PDGPU_DISPATCH_LOGQ(lqx, (k_rfft_rows<LQ><<<grid, 2 * TR * T, smem, s>>>(u, e.d_S1, Nx, Ny, pl.Hx, TR, e.d_tw,
+                                                                                pl.logTWN)));
     }
-    double2* specIn = e.d_S1;
-    double2* specOut = e.d_S1;
+    double2* spec = e.d_S1;
     if (d == 3) {
+        PassTimer pt(e, kPassK2, s);
         const int ZT = pl.k2_zt;
-        int nth, ipt;
-        pick_threads((int64_t)2 * ZT * (pl.P[1] / 2) / 4 + 1, nth, ipt);
+        const int lq = pl.logP[1] - 1;
+        const int T = threads_per_transform(lq, 4);
         dim3 grid((Nz + ZT - 1) / ZT, pl.Hx, batch * d);
-        const size_t smem = sizeof(double2) * (size_t)ZT * pl.P[1];
-        DISPATCH_IPT(ipt, (k_cfft_y_fwd<I><<<grid, nth, smem, s>>>(e.d_S1, e.d_S2, Ny, Nz, pl.Hx, pl.logP[1], ZT,
-                                                                    e.d_tw, pl.logTWN)));
-        specIn = specOut = e.d_S2;
-    } else if (pl.k3_halves == 1) {
-        specOut = e.d_S2;
+        const size_t smem = sizeof(double2) * (size_t)2 * ZT * xbuf_slots(lq);
+        PDGPU_DISPATCH_LOGQ9(lq, (k_cfft_y_fwd<LQ><<<grid, 2 * ZT * T, smem, s>>>(e.d_S1, e.d_S2, Ny, Nz, pl.Hx, ZT,
+                                                                                 e.d_tw, pl.logTWN)));
+        spec = e.d_S2;
     }
-    // K3
+    // K3: 2D out of place S1 -> S2 (z^0 parked in S2), 3D in place on S2
+    double2* xin = e.d_S1;
     {
-        const int NC = pl.k3_cols, NH = pl.k3_halves;
-        const int Ql = pl.Pl / 2;
-        int nth, ipt;
-        pick_threads((int64_t)NC * d * NH * Ql / 4 + 1, nth, ipt);
+        PassTimer pt(e, kPassK3, s);
+        const int NC = pl.k3_cols;
+        const int lq = pl.logPl - 1;
+        const int logr = d == 3 ? 3 : 4;
+        const int T = threads_per_transform(lq, logr);
         dim3 grid((pl.ncols + NC - 1) / NC, batch);
-        const size_t smem = sizeof(double2) * (size_t)NC * d * NH * Ql;
+        const bool zsmem = pl.k3_halves == 2;
+        const size_t smem =
+            sizeof(double2) * (size_t)NC * (xbuf_slots(lq) + (zsmem ? 2 * d - 1 : d - 1) * (1 << lq));
         if (d == 2) {
             if (e.real_symbol)
-                DISPATCH_IPT(ipt, (k_spectral<I, 2, true><<<grid, nth, smem, s>>>(specIn, specOut, e.d_sym, pl.ncols,
-                                                                                 pl.Nl, pl.logPl, NC, NH, e.d_tw,
-                                                                                 pl.logTWN)))
+                PDGPU_DISPATCH_LOGQ(lq, (k_spectral<LQ, 2, true, 4, false><<<grid, NC * T, smem, s>>>(
+                                            spec, e.d_S2, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
             else
-                DISPATCH_IPT(ipt, (k_spectral<I, 2, false><<<grid, nth, smem, s>>>(specIn, specOut, e.d_sym, pl.ncols,
-                                                                                  pl.Nl, pl.logPl, NC, NH, e.d_tw,
-                                                                                  pl.logTWN)))
+                PDGPU_DISPATCH_LOGQ(lq, (k_spectral<LQ, 2, false, 4, false><<<grid, NC * T, smem, s>>>(
+                                            spec, e.d_S2, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
+            xin = e.d_S2;
         } else {
             if (e.real_symbol)
-                DISPATCH_IPT(ipt, (k_spectral<I, 3, true><<<grid, nth, smem, s>>>(specIn, specOut, e.d_sym, pl.ncols,
-                                                                                 pl.Nl, pl.logPl, NC, NH, e.d_tw,
-                                                                                 pl.logTWN)))
+                PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, true, 3, true><<<grid, NC * T, smem, s>>>(
+                                             spec, spec, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
             else
-                DISPATCH_IPT(ipt, (k_spectral<I, 3, false><<<grid, nth, smem, s>>>(specIn, specOut, e.d_sym, pl.ncols,
-                                                                                  pl.Nl, pl.logPl, NC, NH, e.d_tw,
-                                                                                  pl.logTWN)))
+                PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, false, 3, true><<<grid, NC * T, smem, s>>>(
+                                             spec, spec, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
         }
     }
-    double2* xIn = specOut;
     if (d == 3) {
+        PassTimer pt(e, kPassK4, s);
         const int ZT = pl.k2_zt;
-        int nth, ipt;
-        pick_threads((int64_t)2 * ZT * (pl.P[1] / 2) / 4 + 1, nth, ipt);
+        const int lq = pl.logP[1] - 1;
+        const int T = threads_per_transform(lq, 4);
         dim3 grid((Nz + ZT - 1) / ZT, pl.Hx, batch * d);
-        const size_t smem = sizeof(double2) * (size_t)ZT * pl.P[1];
-        DISPATCH_IPT(ipt, (k_cfft_y_inv<I><<<grid, nth, smem, s>>>(e.d_S2, e.d_S1, Ny, Nz, pl.Hx, pl.logP[1], ZT,
-                                                                    e.d_tw, pl.logTWN)));
-        xIn = e.d_S1;
+        const size_t smem = sizeof(double2) * (size_t)2 * ZT * xbuf_slots(lq);
+        PDGPU_DISPATCH_LOGQ9(lq, (k_cfft_y_inv<LQ><<<grid, 2 * ZT * T, smem, s>>>(e.d_S2, e.d_S1, Ny, Nz, pl.Hx, ZT,
+                                                                                 e.d_tw, pl.logTWN)));
     }
     // K5
     {
+        PassTimer pt(e, kPassK5, s);
         const int TR = pl.k1_rows;
-        int nth, ipt;
-        pick_threads((int64_t)2 * TR * Qx / 4 + 1, nth, ipt);
+        const int T = threads_per_transform(lqx, 4);
         dim3 grid((Ny + TR - 1) / TR, nslab);
-        const size_t smem = sizeof(double2) * (size_t)TR * 2 * Qx;
-#define K5_ARGS xIn, f, Nx, Ny, Nz, d, pl.Hx, pl.logQx, TR, e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes
-        if (cmask && body) DISPATCH_IPT(ipt, (k_irfft_rows<I, true, true><<<grid, nth, smem, s>>>(K5_ARGS)))
-        else if (cmask) DISPATCH_IPT(ipt, (k_irfft_rows<I, true, false><<<grid, nth, smem, s>>>(K5_ARGS)))
-        else if (body) DISPATCH_IPT(ipt, (k_irfft_rows<I, false, true><<<grid, nth, smem, s>>>(K5_ARGS)))
-        else DISPATCH_IPT(ipt, (k_irfft_rows<I, false, false><<<grid, nth, smem, s>>>(K5_ARGS)))
-#undef K5_ARGS
+        const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_slots(lqx);
+        PDGPU_DISPATCH_LOGQ(lqx, (k_irfft_rows<LQ><<<grid, 2 * TR * T, smem, s>>>(
+                                     xin, f, Nx, Ny, Nz, d, pl.Hx, TR, e.d_tw, pl.logTWN, scale, cmask, body,
+                                     pl.nodes)));
     }
     check(cudaGetLastError(), "fast_apply launch");
 }

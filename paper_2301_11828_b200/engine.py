@@ -169,6 +169,21 @@ class FastForce:
     def footprint_bytes(self) -> int:
         return self._lib.pdgpu_footprint_bytes(self._h)
 
+    PASSES = ("K1_rfft_x", "K2_fft_y", "K3_spectral", "K4_ifft_y", "K5_irfft_x", "K6_surface", "K6_bonds", "vec")
+
+    def timing(self, on: bool = True):
+        _check(self._lib.pdgpu_timing_enable(self._h, 1 if on else 0))
+
+    def timing_read(self):
+        """{pass name: (total ms, launches)} since the last read (CUDA events on the launching stream)."""
+        ms = np.zeros(8)
+        cnt = np.zeros(8, dtype=np.int64)
+        _check(self._lib.pdgpu_timing_read(self._h, _dp(ms), cnt.ctypes.data_as(_lib.c_int64_p), 8))
+        return {n: (float(ms[i]), int(cnt[i])) for i, n in enumerate(self.PASSES) if cnt[i]}
+
+    def launch_count(self) -> int:
+        return int(self._lib.pdgpu_launch_count(self._h))
+
     def symbol_is_real(self) -> bool:
         return bool(self._lib.pdgpu_symbol_is_real(self._h))
 
@@ -201,11 +216,13 @@ class FastForce:
         _check(self._lib.pdgpu_ledger_pairs(self._h, out.ctypes.data_as(_lib.c_int64_p), cnt.value, C.byref(cnt)))
         return out[: cnt.value]
 
-    def matvec(self, u: np.ndarray) -> np.ndarray:
+    def matvec(self, u: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
         """FastForce::apply + apply_corrections (corrections.hpp:76-110) on host fields."""
         u = _f64(u)
         batch = max(u.size // max(self.dim * u.shape[-1], 1), 1)
-        f = np.empty_like(u)
+        f = np.empty_like(u) if out is None else out
+        if f.dtype != np.float64 or not f.flags.c_contiguous or f.shape != u.shape:
+            raise ValueError("out must be a C-contiguous float64 array shaped like u")
         _check(self._lib.pdgpu_matvec_host(self._h, _dp(u), _dp(f), u.shape[-1], batch))
         return f
 
