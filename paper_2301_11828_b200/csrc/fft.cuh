@@ -165,23 +165,56 @@ struct FftShape {
     static constexpr int XBUF = spad_size(Q);  // exchange slots per transform
 };
 
+// Per-thread twiddle bases: pass P >= 1 multiplies input m of its (single)
+// butterfly by w_P^m, w_P = exp(-2 pi i k / (Ns R)), k = t mod Ns.  Only the
+// bases are read from the table (once per kernel); the powers are formed in
+// registers (depth <= 4 products, a few ulp), keeping the L1 path free for
+// the data exchanges.
+struct FftTw {
+    double2 w[3];
+};
+
+template <int LOGQ, int LOGRMAX>
+__device__ __forceinline__ FftTw make_fft_tw(int t, const double2* __restrict__ tw, int logTWN) {
+    using Sh = FftShape<LOGQ, LOGRMAX>;
+    FftTw r;
+#pragma unroll
+    for (int p = 1; p < 4; ++p) {
+        r.w[p - 1] = make_double2(1.0, 0.0);
+        if (p < Sh::NPASS) {
+            const int logns = Sh::LOGREM ? Sh::LOGREM + (p - 1) * Sh::LOGR : p * Sh::LOGR;
+            const int k = t & ((1 << logns) - 1);
+            r.w[p - 1] = __ldg(tw + (k << (logTWN - logns - Sh::LOGR)));
+        }
+    }
+    return r;
+}
+
+__device__ __forceinline__ double2 csqr(double2 a) {
+    return make_double2(a.x * a.x - a.y * a.y, 2.0 * a.x * a.y);
+}
+
 // One Stockham pass of radix 2^LR on the R registers of thread t, Ns = 2^LOGNS.
+// Passes with LOGNS > 0 are full radix-R passes (one butterfly per thread).
 template <int LOGQ, int LOGR, int LR, int LOGNS, int S>
-__device__ __forceinline__ void fft_pass(double2 (&v)[1 << LOGR], int t, const double2* __restrict__ tw,
-                                         int logTWN) {
+__device__ __forceinline__ void fft_pass(double2 (&v)[1 << LOGR], double2 base) {
     constexpr int R = 1 << LOGR, r = 1 << LR, nb = R / r;
-    constexpr int T = (1 << LOGQ) / R;
 #pragma unroll
     for (int i = 0; i < nb; ++i) {
         double2 w[r];
 #pragma unroll
         for (int m = 0; m < r; ++m) w[m] = v[i + m * nb];
         if constexpr (LOGNS > 0) {
-            const int b = t + i * T;
-            const int k = b & ((1 << LOGNS) - 1);
-            const int sh = logTWN - LOGNS - LR;
+            static_assert(nb == 1, "twiddled passes are full radix");
+            double2 pw[r];
+            pw[1] = S > 0 ? cconj(base) : base;
 #pragma unroll
-            for (int m = 1; m < r; ++m) w[m] = cmul(w[m], twiddle<S>(tw, (k * m) << sh));
+            for (int m = 2; m < r; ++m) {
+                const int hb = m >= 8 ? 8 : (m >= 4 ? 4 : 2);  // highest power of two <= m
+                pw[m] = (hb == m) ? csqr(pw[m >> 1]) : cmul(pw[hb], pw[m - hb]);
+            }
+#pragma unroll
+            for (int m = 1; m < r; ++m) w[m] = cmul(w[m], pw[m]);
         }
         dft<LR, S>(w);
 #pragma unroll
@@ -208,28 +241,29 @@ __device__ __forceinline__ void fft_exchange(double2 (&v)[1 << LOGR], int t, dou
 }
 
 template <int LOGQ, int LOGR, int S, int P, int LOGNS, class Bar>
-__device__ __forceinline__ void fft_passes(double2 (&v)[1 << LOGR], int t, double2* xb,
-                                           const double2* __restrict__ tw, int logTWN, Bar bar) {
+__device__ __forceinline__ void fft_passes(double2 (&v)[1 << LOGR], int t, double2* xb, const FftTw& tws, Bar bar) {
     using Sh = FftShape<LOGQ, LOGR>;
     if constexpr (P < Sh::NPASS) {
         constexpr int LR = (P == 0 && Sh::LOGREM) ? Sh::LOGREM : LOGR;
-        fft_pass<LOGQ, LOGR, LR, LOGNS, S>(v, t, tw, logTWN);
+        fft_pass<LOGQ, LOGR, LR, LOGNS, S>(v, P > 0 ? tws.w[P > 0 ? P - 1 : 0] : make_double2(1.0, 0.0));
         if constexpr (P + 1 < Sh::NPASS) {
             fft_exchange<LOGQ, LOGR, LR, LOGNS>(v, t, xb, bar);
-            fft_passes<LOGQ, LOGR, S, P + 1, LOGNS + LR>(v, t, xb, tw, logTWN, bar);
+            fft_passes<LOGQ, LOGR, S, P + 1, LOGNS + LR>(v, t, xb, tws, bar);
         }
     }
 }
 
 // Full transform: v[j] holds x[t + j*T] on entry and X[t + j*T] on exit.
-// xb: this transform's exchange buffer (FftShape::XBUF slots); bar(): a
-// barrier covering every thread of the transform (all groups of a CTA in
+// xb: this transform's exchange buffer (FftShape::XBUF slots); tws: the
+// thread's twiddle bases (make_fft_tw, same for forward and inverse); bar():
+// a barrier covering every thread of the transform (all groups of a CTA in
 // lockstep use __syncthreads).
 template <int LOGQ, int LOGRMAX, int S, class Bar>
 __device__ __forceinline__ void reg_fft(double2 (&v)[1 << FftShape<LOGQ, LOGRMAX>::LOGR], int t, double2* xb,
-                                        const double2* __restrict__ tw, int logTWN, Bar bar) {
+                                        const FftTw& tws, Bar bar) {
     using Sh = FftShape<LOGQ, LOGRMAX>;
-    fft_passes<LOGQ, Sh::LOGR, S, 0, 0>(v, t, xb, tw, logTWN, bar);
+    static_assert(Sh::NPASS <= 4, "at most three twiddled passes");
+    fft_passes<LOGQ, Sh::LOGR, S, 0, 0>(v, t, xb, tws, bar);
 }
 
 struct BlockBar {

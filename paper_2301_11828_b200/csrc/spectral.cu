@@ -142,7 +142,7 @@ __global__ void __launch_bounds__(512) k_rfft_rows(const double* __restrict__ u,
         }
         v[j] = eo ? cmul(z, __ldg(tw + (n << shE))) : z;
     }
-    reg_fft<LOGQ, 4, -1>(v, t, xb, tw, logTWN, BlockBar{});
+    reg_fft<LOGQ, 4, -1>(v, t, xb, make_fft_tw<LOGQ, 4>(t, tw, logTWN), BlockBar{});
 #pragma unroll
     for (int j = 0; j < R; ++j) xb[spad(t + j * T)] = v[j];
     __syncthreads();
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
 #pragma unroll
     for (int j = 0; j < R; ++j) v[j] = xb[spad(t + j * T)];
     __syncthreads();
-    reg_fft<LOGQ, 4, 1>(v, t, xb, tw, logTWN, BlockBar{});
+    reg_fft<LOGQ, 4, 1>(v, t, xb, make_fft_tw<LOGQ, 4>(t, tw, logTWN), BlockBar{});
     const int shE = logTWN - (LOGQ + 1);
 #pragma unroll
     for (int j = 0; j < R; ++j) {
@@ -321,6 +321,7 @@ __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2*
     double2* zpark = cpark + (D - 1) * Q;
     const int shP = logTWN - (LOGQ + 1);
     double2 v[RR];
+    const FftTw tws = make_fft_tw<LOGQ, LOGR>(t, tw, logTWN);
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
 #pragma unroll 1
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2*
                 if (valid && n < Nl) x = src[n];
                 v[j] = h ? cmul(x, __ldg(tw + (n << shP))) : x;
             }
-            reg_fft<LOGQ, LOGR, -1>(v, t, xb, tw, logTWN, BlockBar{});
+            reg_fft<LOGQ, LOGR, -1>(v, t, xb, tws, BlockBar{});
             if (c < D - 1) {
 #pragma unroll
                 for (int j = 0; j < RR; ++j) cpark[c * Q + j * T + t] = v[j];
@@ -360,7 +361,7 @@ __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2*
 #pragma unroll
                 for (int j = 0; j < RR; ++j) v[j] = cpark[a * Q + j * T + t];
             }
-            reg_fft<LOGQ, LOGR, 1>(v, t, xb, tw, logTWN, BlockBar{});
+            reg_fft<LOGQ, LOGR, 1>(v, t, xb, tws, BlockBar{});
             double2* dst = out + ((int64_t)(b * D + a) * ncols + col) * Nl;
 #pragma unroll
             for (int j = 0; j < RR; ++j) {
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(512) k_cfft_y_fwd(const double2* __restrict__ 
         if (valid && n < Ny) x = src[n];
         v[j] = eo ? cmul(x, __ldg(tw + (n << shP))) : x;
     }
-    reg_fft<LOGQ, 4, -1>(v, t, xb, tw, logTWN, BlockBar{});
+    reg_fft<LOGQ, 4, -1>(v, t, xb, make_fft_tw<LOGQ, 4>(t, tw, logTWN), BlockBar{});
 #pragma unroll
     for (int j = 0; j < R; ++j) xb[spad(t + j * T)] = v[j];
     __syncthreads();
@@ -442,7 +443,7 @@ __global__ void __launch_bounds__(512) k_cfft_y_inv(const double2* __restrict__ 
 #pragma unroll
     for (int j = 0; j < R; ++j) v[j] = xb[spad(t + j * T)];
     __syncthreads();
-    reg_fft<LOGQ, 4, 1>(v, t, xb, tw, logTWN, BlockBar{});
+    reg_fft<LOGQ, 4, 1>(v, t, xb, make_fft_tw<LOGQ, 4>(t, tw, logTWN), BlockBar{});
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const int n = t + j * T;
