@@ -236,6 +236,7 @@ int pdgpu_create(int dim, const int* dims, int M, const double* stencils, int de
         auto* e = new pdgpu_engine();
         try {
             e->device = device;
+            cuda_check(cudaDeviceGetAttribute(&e->num_sms, cudaDevAttrMultiProcessorCount, device), "sm count");
             e->dim = dim;
             e->M = M;
             e->np = assembly::n_pairs(dim);

@@ -43,6 +43,7 @@ struct Constraint {
 
 struct Engine {
     int device = 0;
+    int num_sms = 148;
     int dim = 2, M = 0, np = 3, nof = 0, lw = 1;
     int64_t ss = 0;  // stencil size (2M+1)^dim
     Plan plan;

@@ -23,6 +23,7 @@
 // thread reads its n_pairs coefficients contiguously.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <stdexcept>
@@ -85,6 +86,7 @@ void plan_init(Plan& pl, int dim, const int* dims) {
         int tr = 1;
         while (tr < 8 && 2 * (tr * 2) * T <= 512 && (tr * 2) * per_row <= kSmemBudget) tr *= 2;
         pl.k1_rows = std::min(tr, pl.N[1]);
+        if (const char* env = getenv("PDGPU_K1_ROWS")) pl.k1_rows = std::max(1, std::min(pl.k1_rows, atoi(env)));
     }
     // K3: columns per CTA
     {
@@ -312,8 +314,10 @@ __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2*
     extern __shared__ double2 sm[];
     const int gi = threadIdx.x >> Sh::LOGT;
     const int t = threadIdx.x & (T - 1);
-    const int col = blockIdx.x * NC + gi;
-    const int b = blockIdx.y;
+    // batch index fastest in launch order: the CTAs resident together share
+    // a column's symbol in L2 instead of re-reading it per vector
+    const int col = blockIdx.y * NC + gi;
+    const int b = blockIdx.x;
     const bool valid = col < ncols;
     double2* xb = sm + gi * XB;
     // per column: (D-1)*Q component park, then (ZSMEM) D*Q half-0 park
@@ -377,6 +381,148 @@ __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2*
             }
         }
     }
+}
+
+// ------------------------------------------------------ K3, pipelined ---
+// 2D spectral pass as a persistent kernel: each CTA walks (vector, column)
+// items in vector-fastest order, one column group of NC columns per item
+// (NC*T = 256 threads).  Every global operand of the six FFTs of an item
+// (x_0, x_1 for both halves, then z^0_1, z^0_0 for the read-modify-write of
+// the second half) is fetched with cp.async into a staging buffer one FFT
+// ahead of its use, so HBM/L2 latency hides behind the previous transform.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int n = pred ? 16 : 0;  // zero-fill outside the window
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <int LOGQ, bool REAL>
+__global__ void __launch_bounds__(256, 1) k_spectral2d_pipe(const double2* __restrict__ in, double2* out,
+                                                            const void* __restrict__ sym, int ncols, int Nl, int NC,
+                                                            int batch, const double2* __restrict__ tw, int logTWN) {
+    using Sh = FftShape<LOGQ, 4>;
+    constexpr int Q = Sh::Q, T = Sh::T, XB = Sh::XBUF, RR = Sh::R;
+    extern __shared__ double2 sm[];
+    const int gi = threadIdx.x >> Sh::LOGT;
+    const int t = threadIdx.x & (T - 1);
+    double2* xb = sm + gi * XB;
+    double2* cpark = sm + NC * XB + gi * Q;        // component 0 park
+    double2* stage = sm + NC * XB + NC * Q + gi * Q;  // staging, natural order [j*T + t]
+    const int shP = logTWN - (LOGQ + 1);
+    const FftTw tws = make_fft_tw<LOGQ, 4>(t, tw, logTWN);
+    const int ngroups = (ncols + NC - 1) / NC;
+    const int64_t nitems = (int64_t)ngroups * batch;
+    const int64_t cstride = (int64_t)ncols * Nl;  // component stride
+
+    // stage operand: src column (already offset), n < Nl valid
+    auto fetch = [&](const double2* src, bool ok) {
+#pragma unroll
+        for (int j = 0; j < RR; ++j) {
+            const int n = t + j * T;
+            const bool p = ok && n < Nl;
+            cp_async16(stage + j * T + t, p ? src + n : src, p);
+        }
+        cp_async_commit();
+    };
+    auto item_ptrs = [&](int64_t it, int& b, int& col, bool& valid) {
+        b = (int)(it % batch);
+        col = (int)(it / batch) * NC + gi;
+        valid = col < ncols;
+    };
+
+    int64_t it = blockIdx.x;
+    if (it < nitems) {
+        int b, col;
+        bool valid;
+        item_ptrs(it, b, col, valid);
+        fetch(in + ((int64_t)(b * 2 + 0) * ncols + (valid ? col : 0)) * Nl, valid);
+    }
+    for (; it < nitems; it += gridDim.x) {
+        int b, col;
+        bool valid;
+        item_ptrs(it, b, col, valid);
+        const int cc = valid ? col : 0;
+        const double2* x0 = in + ((int64_t)(b * 2 + 0) * ncols + cc) * Nl;
+        const double2* x1 = x0 + cstride;
+        double2* z0 = out + ((int64_t)(b * 2 + 0) * ncols + cc) * Nl;
+        double2* z1 = z0 + cstride;
+        double2 v[RR];
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+                cp_async_wait_all();
+                __syncthreads();
+#pragma unroll
+                for (int j = 0; j < RR; ++j) {
+                    const double2 x = stage[j * T + t];
+                    v[j] = h ? cmul(x, __ldg(tw + ((t + j * T) << shP))) : x;
+                }
+                __syncthreads();
+                // next operand: x1 after x0; after x1 of half 0 -> x0 of half 1;
+                // after x1 of half 1 -> z^0_1 for the read-modify-write
+                if (c == 0) fetch(x1, valid);
+                else if (h == 0) fetch(x0, valid);
+                else fetch(z1, valid);
+                reg_fft<LOGQ, 4, -1>(v, t, xb, tws, BlockBar{});
+                if (c == 0) {
+#pragma unroll
+                    for (int j = 0; j < RR; ++j) cpark[j * T + t] = v[j];
+                }
+            }
+            // 2 x 2 product; component 1 stays in registers
+            const int64_t sbase = ((int64_t)cc * 2 + h) * Q;
+#pragma unroll
+            for (int j = 0; j < RR; ++j) {
+                const int k = t + j * T;
+                double2 U[2], F[2];
+                U[0] = cpark[j * T + t];
+                U[1] = v[j];
+                symbol_product<2, REAL>(F, U, sym, sbase + k);
+                cpark[j * T + t] = F[0];
+                v[j] = F[1];
+            }
+#pragma unroll 1
+            for (int ai = 0; ai < 2; ++ai) {
+                const int a = 1 - ai;
+                if (ai == 1) {
+#pragma unroll
+                    for (int j = 0; j < RR; ++j) v[j] = cpark[j * T + t];
+                }
+                reg_fft<LOGQ, 4, 1>(v, t, xb, tws, BlockBar{});
+                double2* dst = a ? z1 : z0;
+                if (h == 0) {
+#pragma unroll
+                    for (int j = 0; j < RR; ++j) {
+                        const int n = t + j * T;
+                        if (valid && n < Nl) dst[n] = v[j];
+                    }
+                } else {
+                    cp_async_wait_all();
+                    __syncthreads();
+#pragma unroll
+                    for (int j = 0; j < RR; ++j) {
+                        const int n = t + j * T;
+                        const double2 y = cadd(stage[j * T + t], cmul(twiddle<1>(tw, n << shP), v[j]));
+                        if (valid && n < Nl) dst[n] = y;
+                    }
+                    __syncthreads();
+                    if (a == 1) {
+                        fetch(z0, valid);
+                    } else if (it + gridDim.x < nitems) {
+                        int b2, col2;
+                        bool valid2;
+                        item_ptrs(it + gridDim.x, b2, col2, valid2);
+                        fetch(in + ((int64_t)(b2 * 2 + 0) * ncols + (valid2 ? col2 : 0)) * Nl, valid2);
+                    }
+                }
+            }
+            if (h == 0) __syncthreads();  // z^0 stores visible before the half-1 re-read
+        }
+    }
+    cp_async_wait_all();
 }
 
 // ------------------------------------------------------- K2 / K4 (3D) ---
@@ -537,6 +683,8 @@ static void set_attrs_l() {
     smem_attr((const void*)k_irfft_rows<L>);
     smem_attr((const void*)k_spectral<L, 2, true, 4, false>);
     smem_attr((const void*)k_spectral<L, 2, false, 4, false>);
+    smem_attr((const void*)k_spectral2d_pipe<L, true>);
+    smem_attr((const void*)k_spectral2d_pipe<L, false>);
     if constexpr (L <= 9) {
         smem_attr((const void*)k_spectral<L, 3, true, 3, true>);
         smem_attr((const void*)k_spectral<L, 3, false, 3, true>);
@@ -661,17 +809,21 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
         const int lq = pl.logPl - 1;
         const int logr = d == 3 ? 3 : 4;
         const int T = threads_per_transform(lq, logr);
-        dim3 grid((pl.ncols + NC - 1) / NC, batch);
+        dim3 grid(batch, (pl.ncols + NC - 1) / NC);
         const bool zsmem = pl.k3_halves == 2;
         const size_t smem =
             sizeof(double2) * (size_t)NC * (xbuf_slots(lq) + (zsmem ? 2 * d - 1 : d - 1) * (1 << lq));
         if (d == 2) {
+            // persistent, cp.async-pipelined variant: NC*(XB + 2Q) slots
+            const size_t psmem = sizeof(double2) * (size_t)NC * (xbuf_slots(lq) + 2 * (1 << lq));
+            const int64_t nitems = (int64_t)((pl.ncols + NC - 1) / NC) * batch;
+            const unsigned pgrid = (unsigned)std::min<int64_t>(nitems, e.num_sms);
             if (e.real_symbol)
-                PDGPU_DISPATCH_LOGQ(lq, (k_spectral<LQ, 2, true, 4, false><<<grid, NC * T, smem, s>>>(
-                                            spec, e.d_S2, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
+                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, true><<<pgrid, NC * T, psmem, s>>>(
+                                            spec, e.d_S2, e.d_sym, pl.ncols, pl.Nl, NC, batch, e.d_tw, pl.logTWN)))
             else
-                PDGPU_DISPATCH_LOGQ(lq, (k_spectral<LQ, 2, false, 4, false><<<grid, NC * T, smem, s>>>(
-                                            spec, e.d_S2, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
+                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, false><<<pgrid, NC * T, psmem, s>>>(
+                                            spec, e.d_S2, e.d_sym, pl.ncols, pl.Nl, NC, batch, e.d_tw, pl.logTWN)))
             xin = e.d_S2;
         } else {
             if (e.real_symbol)
