@@ -301,7 +301,8 @@ def main():
                 "algorithmic_bytes_per_launch": k3_bytes, "mean_launch_ms": k3_avg_s * 1e3, "peak_source": peak_src,
                 "matvec": {"algorithmic_bytes_per_step": mv_bytes, "achieved_gbs": mv_gbs, "frac": mv_gbs / peak,
                            "model": "SURVEY 8(d): 80 B/DOF/vector + 48N B symbol"},
-                "passes_ms_per_step": {k: v[0] / args.steps for k, v in passes.items()}}
+                "passes_ms_per_step": {k: v[0] / args.steps for k, v in passes.items()},
+                "symbol_mode": ff.symbol_mode()}
 
     # end to end through the public host API (pinned host buffers)
     e2e = None

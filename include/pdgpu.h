@@ -71,6 +71,9 @@ double pdgpu_last_imag_residue(pdgpu_t h);
 size_t pdgpu_footprint_bytes(pdgpu_t h);
 int64_t pdgpu_n_nodes(pdgpu_t h);
 int pdgpu_symbol_is_real(pdgpu_t h);
+/* 0 complex symbol table, 1 real symbol table, 2 separable per-column
+ * symbol (physical stencils of definite parity per axis). */
+int pdgpu_symbol_mode(pdgpu_t h);
 
 /* ----------------------------------------------------------- corrections --
  * Regions (grid.hpp:172-209): per-node constraint direction mask (bit d =

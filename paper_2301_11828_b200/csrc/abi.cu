@@ -2,6 +2,7 @@
 // orchestration only: setup, stream-ordered launches, error mapping.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -198,6 +199,74 @@ int64_t break_pairs(Engine& e, const int64_t* pairs, int64_t n) {
     return (int64_t)cnt[1];
 }
 
+// Separable symbol (2D): if every stencil component has a definite parity
+// in each axis (true for build_kernel output, kernel.hpp:109-116: K^xx, K^yy
+// even/even, K^xy odd/odd), H_p(kx, ky) = sum_m D_p[kx][m] * (cos|sin)(2 pi ky m/Py)
+// with D_p[kx][0] = C_p[0] for pairs even in y, D_p[kx][m] = 2 C_p[m], and
+// C_p[m] = sign_p / (Px Py) sum_ox K_p(ox, m) (cos|sin)(2 pi kx ox / Px),
+// sign_p = -1 for odd/odd pairs (i*i).  Exact rewrite of the direct DFT of
+// the stencil; the kernel evaluates H per frequency instead of streaming an
+// O(N) table.  Enabled by PDGPU_SYMBOL=separable.
+void build_coltab(Engine& e) {
+    if (e.d_coltab) {
+        cudaFree(e.d_coltab);
+        e.d_coltab = nullptr;
+    }
+    if (e.dim != 2 || !e.real_symbol) return;
+    // opt-in: measured slower than the streamed real table on B200 (the
+    // spectral pass is FP64-issue bound, not HBM bound; profiles/README.md)
+    const char* env = getenv("PDGPU_SYMBOL");
+    if (!env || std::string(env) != "separable") return;
+    const int M = e.M, side = 2 * M + 1;
+    auto Kat = [&](int p, int ox, int oy) { return e.stencils[(size_t)(p * e.ss + (oy + M) * side + (ox + M))]; };
+    // parity per pair and axis: +1 even, -1 odd, 0 neither
+    int par[3][2];
+    for (int p = 0; p < 3; ++p)
+        for (int ax = 0; ax < 2; ++ax) {
+            bool even = true, odd = true;
+            for (int oy = -M; oy <= M; ++oy)
+                for (int ox = -M; ox <= M; ++ox) {
+                    // the centre (-row sum, kernel.hpp:119-125) is a constant
+                    // term of the symbol; an odd pair's centre is round-off
+                    if (ox == 0 && oy == 0) continue;
+                    const double a = Kat(p, ox, oy);
+                    const double b = ax == 0 ? Kat(p, -ox, oy) : Kat(p, ox, -oy);
+                    even = even && a == b;
+                    odd = odd && a == -b;
+                }
+            par[p][ax] = even ? 1 : (odd ? -1 : 0);
+        }
+    // the kernel hard-wires xx, yy even and xy odd along y, equal parity in x
+    const bool ok = par[0][1] == 1 && par[2][1] == 1 && par[1][1] == -1 && par[0][0] == 1 && par[2][0] == 1 &&
+                    par[1][0] == -1;
+    if (!ok) return;
+    const Plan& pl = e.plan;
+    const int ND = 3 * (M + 1);
+    std::vector<double> tab((size_t)pl.ncols * ND, 0.0);
+    const long double pi2 = 2.0L * 3.141592653589793238462643383279502884L;
+    const long double scale = 1.0L / ((long double)pl.P[0] * (long double)pl.P[1]);
+    for (int kx = 0; kx < pl.ncols; ++kx) {
+        for (int p = 0; p < 3; ++p) {
+            const bool oddx = par[p][0] == -1;
+            const long double sign = (oddx ? -1.0L : 1.0L);
+            for (int m = 0; m <= M; ++m) {
+                long double c = 0.0L;
+                for (int ox = -M; ox <= M; ++ox) {
+                    if (ox == 0 && m == 0) continue;  // centre added below
+                    const long double ang = pi2 * (long double)(((int64_t)kx * (ox + pl.P[0])) % pl.P[0]) / pl.P[0];
+                    c += (long double)Kat(p, ox, m) * (oddx ? sinl(ang) : cosl(ang));
+                }
+                c *= sign * scale;
+                const bool evy = par[p][1] == 1;
+                const long double centre = (long double)Kat(p, 0, 0) * scale;
+                tab[(size_t)kx * ND + p * (M + 1) + m] = (double)(m == 0 ? (evy ? c : 0.0L) + centre : 2.0L * c);
+            }
+        }
+    }
+    cuda_check(cudaMalloc(&e.d_coltab, sizeof(double) * tab.size()), "alloc coltab");
+    cuda_check(cudaMemcpy(e.d_coltab, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice), "coltab");
+}
+
 void matvec_impl(Engine& e, const double* u, double* f, int batch, cudaStream_t s) {
     launch_fast_apply(e, u, f, batch, s, 1.0, nullptr, nullptr);
     launch_corrections(e, u, f, batch, s, 1.0);
@@ -296,6 +365,7 @@ int pdgpu_create(int dim, const int* dims, int M, const double* stencils, int de
                        "disp");
             build_twiddles(*e);
             build_symbol(*e);
+            build_coltab(*e);
             // regions + surface diagonal from the geometry (build_de)
             e->h_near = assembly::near_surface(dim, dims, M);
             std::vector<long long> rows;
@@ -327,7 +397,7 @@ void pdgpu_destroy(pdgpu_t h) {
     void* ptrs[] = {h->d_tw, h->d_sym, h->d_K, h->d_offs, h->d_disp, h->d_S1, h->d_S2, h->d_u_stage, h->d_f_stage,
                     h->d_cmask, h->d_surf_rows, h->d_surf_de, h->d_ledger, h->d_bond_rows, h->d_listed,
                     h->d_counters, h->d_new_pairs, h->d_body, h->d_cdofs, h->d_cval, h->d_ckind, h->d_u, h->d_v,
-                    h->d_f, h->d_fprev, h->d_red, h->d_scal, h->d_ticket, h->d_cg};
+                    h->d_f, h->d_fprev, h->d_red, h->d_scal, h->d_ticket, h->d_cg, h->d_coltab};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->stream) cudaStreamDestroy(h->stream);
@@ -388,6 +458,7 @@ size_t pdgpu_footprint_bytes(pdgpu_t h) {
 
 int64_t pdgpu_n_nodes(pdgpu_t h) { return h ? h->plan.nodes : 0; }
 int pdgpu_symbol_is_real(pdgpu_t h) { return h && h->real_symbol ? 1 : 0; }
+int pdgpu_symbol_mode(pdgpu_t h) { return !h ? -1 : (h->d_coltab ? 2 : (h->real_symbol ? 1 : 0)); }
 
 int pdgpu_set_regions(pdgpu_t h, const uint8_t* near_surface, const uint8_t* cmask) {
     return guarded([&] {

@@ -59,6 +59,7 @@ struct Engine {
     double2* d_tw = nullptr;        // exp(-2 pi i k / TWN)
     void* d_sym = nullptr;          // symbol: real double or double2, np * ncols * Pl
     double* d_K = nullptr;          // stencils on device (np * ss)
+    double* d_coltab = nullptr;     // separable symbol: per column n_pairs x (M+1) coefficients (2D)
     int* d_offs = nullptr;          // nof*3
     long long* d_disp = nullptr;    // nof: linear node displacement of each offset
     int64_t cap_batch = 0;

@@ -77,6 +77,71 @@ __device__ __forceinline__ double2 tw16(double2 a) {
     }
 }
 
+// multiply by exp(S*2*pi*i*E/32) with compile-time E
+template <int E, int S>
+__device__ __forceinline__ double2 tw32(double2 a) {
+    constexpr int e = E & 31;
+    if constexpr ((e & 1) == 0) {
+        return tw16<e / 2, S>(a);
+    } else {
+        constexpr double C[32] = {1.0,
+                                  0.98078528040323044913,
+                                  0.92387953251128675613,
+                                  0.83146961230254523708,
+                                  0.70710678118654752440,
+                                  0.55557023301960222474,
+                                  0.38268343236508977173,
+                                  0.19509032201612826785,
+                                  0.0,
+                                  -0.19509032201612826785,
+                                  -0.38268343236508977173,
+                                  -0.55557023301960222474,
+                                  -0.70710678118654752440,
+                                  -0.83146961230254523708,
+                                  -0.92387953251128675613,
+                                  -0.98078528040323044913,
+                                  -1.0,
+                                  -0.98078528040323044913,
+                                  -0.92387953251128675613,
+                                  -0.83146961230254523708,
+                                  -0.70710678118654752440,
+                                  -0.55557023301960222474,
+                                  -0.38268343236508977173,
+                                  -0.19509032201612826785,
+                                  0.0,
+                                  0.19509032201612826785,
+                                  0.38268343236508977173,
+                                  0.55557023301960222474,
+                                  0.70710678118654752440,
+                                  0.83146961230254523708,
+                                  0.92387953251128675613,
+                                  0.98078528040323044913};
+        constexpr double c = C[e];
+        constexpr double s = S * C[(e + 24) & 31];  // sin(2 pi e/32) = cos(2 pi (e-8)/32)
+        return make_double2(a.x * c - a.y * s, a.x * s + a.y * c);
+    }
+}
+
+// run-time exponent variant of tw32 (folds to constants inside unrolled loops)
+template <int S>
+__device__ __forceinline__ double2 tw32r(int e, double2 a) {
+    switch (e & 31) {
+#define PDGPU_TW32_CASE(E) \
+    case E:                \
+        return tw32<E, S>(a);
+        PDGPU_TW32_CASE(0) PDGPU_TW32_CASE(1) PDGPU_TW32_CASE(2) PDGPU_TW32_CASE(3) PDGPU_TW32_CASE(4)
+        PDGPU_TW32_CASE(5) PDGPU_TW32_CASE(6) PDGPU_TW32_CASE(7) PDGPU_TW32_CASE(8) PDGPU_TW32_CASE(9)
+        PDGPU_TW32_CASE(10) PDGPU_TW32_CASE(11) PDGPU_TW32_CASE(12) PDGPU_TW32_CASE(13) PDGPU_TW32_CASE(14)
+        PDGPU_TW32_CASE(15) PDGPU_TW32_CASE(16) PDGPU_TW32_CASE(17) PDGPU_TW32_CASE(18) PDGPU_TW32_CASE(19)
+        PDGPU_TW32_CASE(20) PDGPU_TW32_CASE(21) PDGPU_TW32_CASE(22) PDGPU_TW32_CASE(23) PDGPU_TW32_CASE(24)
+        PDGPU_TW32_CASE(25) PDGPU_TW32_CASE(26) PDGPU_TW32_CASE(27) PDGPU_TW32_CASE(28) PDGPU_TW32_CASE(29)
+        PDGPU_TW32_CASE(30)
+#undef PDGPU_TW32_CASE
+        default:
+            return tw32<31, S>(a);
+    }
+}
+
 template <int S>
 __device__ __forceinline__ void dft2(double2& a, double2& b) {
     const double2 t = a;

@@ -398,11 +398,21 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-template <int LOGQ, bool REAL>
-__global__ void __launch_bounds__(256, 1) k_spectral2d_pipe(const double2* __restrict__ in, double2* out,
-                                                            const void* __restrict__ sym, int ncols, int Nl, int NC,
-                                                            int batch, const double2* __restrict__ tw, int logTWN) {
-    using Sh = FftShape<LOGQ, 4>;
+constexpr int kPipeLogR = 4;  // 16 points per thread: 256 threads per 4096-point column
+constexpr int kPipeThreads = 256;
+
+// Symbol modes: 0 complex table, 1 real table (both [col][h][k][pair]),
+// 2 separable: for stencils of definite parity per axis (the physical
+// kernels, kernel.hpp:109-116) the symbol along the column axis is
+// H(ky) = D[0] + sum_{m=1..M} D[m] * (cos|sin)(2 pi ky m / Pl) with per-column
+// coefficients D (coltab, O(Hx*M) doubles) -- no O(N) symbol stream.
+template <int LOGQ, int SYM>
+__global__ void __launch_bounds__(kPipeThreads, 1) k_spectral2d_pipe(const double2* __restrict__ in, double2* out,
+                                                            const void* __restrict__ sym,
+                                                            const double* __restrict__ coltab, int M, int ncols,
+                                                            int Nl, int NC, int batch, const double2* __restrict__ tw,
+                                                            int logTWN) {
+    using Sh = FftShape<LOGQ, kPipeLogR>;
     constexpr int Q = Sh::Q, T = Sh::T, XB = Sh::XBUF, RR = Sh::R;
     extern __shared__ double2 sm[];
     const int gi = threadIdx.x >> Sh::LOGT;
@@ -411,7 +421,15 @@ __global__ void __launch_bounds__(256, 1) k_spectral2d_pipe(const double2* __res
     double2* cpark = sm + NC * XB + gi * Q;        // component 0 park
     double2* stage = sm + NC * XB + NC * Q + gi * Q;  // staging, natural order [j*T + t]
     const int shP = logTWN - (LOGQ + 1);
-    const FftTw tws = make_fft_tw<LOGQ, 4>(t, tw, logTWN);
+    const FftTw tws = make_fft_tw<LOGQ, kPipeLogR>(t, tw, logTWN);
+    // exp(-2 pi i t/Pl): the half-1 pre-twiddle of n = t + j*T is this times
+    // exp(-2 pi i j/(2R)) (compile time); exp(+2 pi i (2t+h)/Pl) seeds the
+    // symbol phases of ky = 2(t + j*T) + h.
+    const double2 wt = __ldg(tw + (t << shP));
+    const double2 eh0 = cconj(__ldg(tw + ((2 * t) << shP)));
+    const double2 eh1 = cconj(__ldg(tw + ((2 * t + 1) << shP)));
+    const int ND = 3 * (M + 1);
+    double* dsm = reinterpret_cast<double*>(sm + NC * XB + 2 * NC * Q) + gi * ND;
     const int ngroups = (ncols + NC - 1) / NC;
     const int64_t nitems = (int64_t)ngroups * batch;
     const int64_t cstride = (int64_t)ncols * Nl;  // component stride
@@ -455,18 +473,22 @@ __global__ void __launch_bounds__(256, 1) k_spectral2d_pipe(const double2* __res
             for (int c = 0; c < 2; ++c) {
                 cp_async_wait_all();
                 __syncthreads();
+                if (h == 0) {
 #pragma unroll
-                for (int j = 0; j < RR; ++j) {
-                    const double2 x = stage[j * T + t];
-                    v[j] = h ? cmul(x, __ldg(tw + ((t + j * T) << shP))) : x;
+                    for (int j = 0; j < RR; ++j) v[j] = stage[j * T + t];
+                } else {
+#pragma unroll
+                    for (int j = 0; j < RR; ++j) v[j] = cmul(stage[j * T + t], tw32r<-1>(j * (16 / RR), wt));
                 }
                 __syncthreads();
+                if (SYM == 2 && h == 0 && c == 0)
+                    for (int i = t; i < ND; i += T) dsm[i] = valid ? __ldg(coltab + (int64_t)cc * ND + i) : 0.0;
                 // next operand: x1 after x0; after x1 of half 0 -> x0 of half 1;
                 // after x1 of half 1 -> z^0_1 for the read-modify-write
                 if (c == 0) fetch(x1, valid);
                 else if (h == 0) fetch(x0, valid);
                 else fetch(z1, valid);
-                reg_fft<LOGQ, 4, -1>(v, t, xb, tws, BlockBar{});
+                reg_fft<LOGQ, kPipeLogR, -1>(v, t, xb, tws, BlockBar{});
                 if (c == 0) {
 #pragma unroll
                     for (int j = 0; j < RR; ++j) cpark[j * T + t] = v[j];
@@ -474,13 +496,29 @@ __global__ void __launch_bounds__(256, 1) k_spectral2d_pipe(const double2* __res
             }
             // 2 x 2 product; component 1 stays in registers
             const int64_t sbase = ((int64_t)cc * 2 + h) * Q;
+            const double2 eh = h ? eh1 : eh0;
 #pragma unroll
             for (int j = 0; j < RR; ++j) {
                 const int k = t + j * T;
                 double2 U[2], F[2];
                 U[0] = cpark[j * T + t];
                 U[1] = v[j];
-                symbol_product<2, REAL>(F, U, sym, sbase + k);
+                if (SYM == 2) {
+                    // e = exp(+2 pi i ky / Pl), ky = 2k + h
+                    const double2 e = tw32r<1>(j * (32 / RR), eh);
+                    double gxx = dsm[0], gyy = dsm[2 * (M + 1)], gxy = dsm[M + 1];
+                    double2 em = e;
+                    for (int m = 1; m <= M; ++m) {
+                        gxx += dsm[m] * em.x;
+                        gxy += dsm[(M + 1) + m] * em.y;
+                        gyy += dsm[2 * (M + 1) + m] * em.x;
+                        em = cmul(em, e);
+                    }
+                    F[0] = make_double2(gxx * U[0].x + gxy * U[1].x, gxx * U[0].y + gxy * U[1].y);
+                    F[1] = make_double2(gxy * U[0].x + gyy * U[1].x, gxy * U[0].y + gyy * U[1].y);
+                } else {
+                    symbol_product<2, SYM == 1>(F, U, sym, sbase + k);
+                }
                 cpark[j * T + t] = F[0];
                 v[j] = F[1];
             }
@@ -491,7 +529,7 @@ __global__ void __launch_bounds__(256, 1) k_spectral2d_pipe(const double2* __res
 #pragma unroll
                     for (int j = 0; j < RR; ++j) v[j] = cpark[j * T + t];
                 }
-                reg_fft<LOGQ, 4, 1>(v, t, xb, tws, BlockBar{});
+                reg_fft<LOGQ, kPipeLogR, 1>(v, t, xb, tws, BlockBar{});
                 double2* dst = a ? z1 : z0;
                 if (h == 0) {
 #pragma unroll
@@ -505,7 +543,7 @@ __global__ void __launch_bounds__(256, 1) k_spectral2d_pipe(const double2* __res
 #pragma unroll
                     for (int j = 0; j < RR; ++j) {
                         const int n = t + j * T;
-                        const double2 y = cadd(stage[j * T + t], cmul(twiddle<1>(tw, n << shP), v[j]));
+                        const double2 y = cadd(stage[j * T + t], cmul(tw32r<1>(j * (16 / RR), cconj(wt)), v[j]));
                         if (valid && n < Nl) dst[n] = y;
                     }
                     __syncthreads();
@@ -683,8 +721,9 @@ static void set_attrs_l() {
     smem_attr((const void*)k_irfft_rows<L>);
     smem_attr((const void*)k_spectral<L, 2, true, 4, false>);
     smem_attr((const void*)k_spectral<L, 2, false, 4, false>);
-    smem_attr((const void*)k_spectral2d_pipe<L, true>);
-    smem_attr((const void*)k_spectral2d_pipe<L, false>);
+    smem_attr((const void*)k_spectral2d_pipe<L, 0>);
+    smem_attr((const void*)k_spectral2d_pipe<L, 1>);
+    smem_attr((const void*)k_spectral2d_pipe<L, 2>);
     if constexpr (L <= 9) {
         smem_attr((const void*)k_spectral<L, 3, true, 3, true>);
         smem_attr((const void*)k_spectral<L, 3, false, 3, true>);
@@ -815,15 +854,22 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
             sizeof(double2) * (size_t)NC * (xbuf_slots(lq) + (zsmem ? 2 * d - 1 : d - 1) * (1 << lq));
         if (d == 2) {
             // persistent, cp.async-pipelined variant: NC*(XB + 2Q) slots
-            const size_t psmem = sizeof(double2) * (size_t)NC * (xbuf_slots(lq) + 2 * (1 << lq));
-            const int64_t nitems = (int64_t)((pl.ncols + NC - 1) / NC) * batch;
+            const int Tp = threads_per_transform(lq, kPipeLogR);
+            const int NCp = std::max(1, kPipeThreads / Tp);
+            const int ND = 3 * (e.M + 1);
+            const size_t psmem = sizeof(double2) * (size_t)NCp * (xbuf_slots(lq) + 2 * (1 << lq)) +
+                                 sizeof(double) * (size_t)NCp * ND;
+            const int64_t nitems = (int64_t)((pl.ncols + NCp - 1) / NCp) * batch;
             const unsigned pgrid = (unsigned)std::min<int64_t>(nitems, e.num_sms);
-            if (e.real_symbol)
-                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, true><<<pgrid, NC * T, psmem, s>>>(
-                                            spec, e.d_S2, e.d_sym, pl.ncols, pl.Nl, NC, batch, e.d_tw, pl.logTWN)))
+            const int mode = e.d_coltab ? 2 : (e.real_symbol ? 1 : 0);
+#define PIPE_ARGS spec, e.d_S2, e.d_sym, e.d_coltab, e.M, pl.ncols, pl.Nl, NCp, batch, e.d_tw, pl.logTWN
+            if (mode == 2)
+                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, 2><<<pgrid, NCp * Tp, psmem, s>>>(PIPE_ARGS)))
+            else if (mode == 1)
+                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, 1><<<pgrid, NCp * Tp, psmem, s>>>(PIPE_ARGS)))
             else
-                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, false><<<pgrid, NC * T, psmem, s>>>(
-                                            spec, e.d_S2, e.d_sym, pl.ncols, pl.Nl, NC, batch, e.d_tw, pl.logTWN)))
+                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, 0><<<pgrid, NCp * Tp, psmem, s>>>(PIPE_ARGS)))
+#undef PIPE_ARGS
             xin = e.d_S2;
         } else {
             if (e.real_symbol)

@@ -187,6 +187,10 @@ class FastForce:
     def symbol_is_real(self) -> bool:
         return bool(self._lib.pdgpu_symbol_is_real(self._h))
 
+    def symbol_mode(self) -> str:
+        """'complex-table' | 'real-table' | 'separable' (per-column coefficients)."""
+        return ("complex-table", "real-table", "separable")[self._lib.pdgpu_symbol_mode(self._h)]
+
     # --------------------------------------------------------- corrections
     def set_regions(self, near_surface=None, constraint_mask=None):
         ns = None if near_surface is None else np.ascontiguousarray(near_surface, dtype=np.uint8)
