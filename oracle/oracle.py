@@ -136,6 +136,10 @@ def rlib():
             "ref_sim_step": (C.c_int64, [C.c_void_p, C.c_int]),
             "ref_sim_get": (None, [C.c_void_p, dp, dp, dp, dp]),
             "ref_bench": (C.c_double, [C.c_void_p, dp, C.c_int64, C.c_int]),
+            "ref_random_kernel": (None, [C.c_void_p, C.c_int, C.c_int, C.c_double, dp]),
+            "ref_random_field": (None, [C.c_void_p, C.c_int, C.c_int64, C.c_double, dp]),
+            "ref_random_ledger": (C.c_int64, [C.c_void_p, C.c_int, ip, C.c_int, C.c_int, i64p, C.c_int64]),
+            "ref_tbt_apply_all": (None, [C.c_void_p, dp, dp]),
         }
         for n, (r, a) in sig.items():
             f = getattr(L, n)

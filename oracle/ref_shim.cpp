@@ -20,6 +20,7 @@
 #include "pdfast/fracture.hpp"
 #include "pdfast/reference.hpp"
 #include "pdfast/timestepping.hpp"
+#include "support/oracles.hpp"
 
 using namespace pdfast;
 
@@ -511,6 +512,56 @@ double ref_bench(void* vp, const double* u, int64_t n_vec, int threads) {
     };
     if (P->dim == 2) return run(get<2>(P), std::integral_constant<int, 2>{});
     return run(get<3>(P), std::integral_constant<int, 3>{});
+}
+
+}  // extern "C"
+
+// ------------------------------------------- reference test-suite oracles --
+// tests/support/oracles.hpp (compiled in place): random_kernel :99-110,
+// random_field :113-119, random_ledger :123-137, tbt_apply_all :72-96.
+extern "C" {
+
+void ref_random_kernel(void* rng, int dim, int M, double h, double* out) {
+    auto& r = *static_cast<std::mt19937*>(rng);
+    auto copy = [&](const auto& K, int np) {
+        const size_t ss = K.stencil_size();
+        for (int p = 0; p < np; ++p) std::memcpy(out + p * ss, K.component(p).data(), sizeof(double) * ss);
+    };
+    if (dim == 2) copy(oracle::random_kernel<2>(M, h, r), 3);
+    else copy(oracle::random_kernel<3>(M, h, r), 6);
+}
+
+void ref_random_field(void* rng, int dim, int64_t n, double amp, double* out) {
+    auto& r = *static_cast<std::mt19937*>(rng);
+    if (dim == 2) from_field<2>(oracle::random_field<2>(n, r, amp), out, n);
+    else from_field<3>(oracle::random_field<3>(n, r, amp), out, n);
+}
+
+int64_t ref_random_ledger(void* rng, int dim, const int* dims, int M, int tries, int64_t* out, int64_t cap) {
+    auto& r = *static_cast<std::mt19937*>(rng);
+    if (dim == 2) {
+        Grid<2> g;
+        g.dims = {dims[0], dims[1]};
+        g.h = 1.0;
+        return pairs_t<2>(oracle::random_ledger<2>(g, M, tries, r), out, cap);
+    }
+    Grid<3> g;
+    g.dims = {dims[0], dims[1], dims[2]};
+    g.h = 1.0;
+    return pairs_t<3>(oracle::random_ledger<3>(g, M, tries, r), out, cap);
+}
+
+void ref_tbt_apply_all(void* vp, const double* u, double* f) {
+    auto* P = static_cast<RefProblem*>(vp);
+    auto run = [&](auto* B, auto dimc) {
+        constexpr int Dim = decltype(dimc)::value;
+        const index_t n = B->grid.n_nodes();
+        VecField<Dim> U;
+        to_field<Dim>(u, U, n);
+        from_field<Dim>(oracle::tbt_apply_all<Dim>(B->grid, B->K, U), f, n);
+    };
+    if (P->dim == 2) run(get<2>(P), std::integral_constant<int, 2>{});
+    else run(get<3>(P), std::integral_constant<int, 3>{});
 }
 
 }  // extern "C"
