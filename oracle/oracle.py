@@ -282,7 +282,7 @@ class Oracle:
         return self.L.orc_static_residual(self.h, _d(_f64(b)), _d(_f64(x)))
 
     def update_bonds(self, u, s0, watch=None, cap=1 << 20):
-        w = None if watch is None else _f64(np.concatenate([watch[0], watch[1]]))
+        w = None if watch is None else _box6(watch, self.dim)
         out = np.zeros((cap, 2), dtype=np.int64)
         n = self.L.orc_update_bonds(self.h, _d(_f64(u)), s0, None if w is None else _d(w),
                                     out.ctypes.data_as(i64p), cap)
@@ -294,7 +294,7 @@ class Oracle:
             self.L.orc_sim_set_velocity(self.h, _d(_f64(v0)))
 
     def sim_step(self, n=1, s0=-1.0, watch=None):
-        w = None if watch is None else _f64(np.concatenate([watch[0], watch[1]]))
+        w = None if watch is None else _box6(watch, self.dim)
         tot = 0
         for _ in range(n):
             tot += self.L.orc_sim_step(self.h, s0, None if w is None else _d(w))
@@ -435,3 +435,11 @@ class RefProblem:
         u = _f64(u_batch)
         nvec = u.shape[0]
         return self.L.ref_bench(self.h, _d(u), nvec, threads)
+
+
+def _box6(watch, dim):
+    """oracle.c boxes are {lo[0..3), hi[0..3)} regardless of dim."""
+    b = np.zeros(6)
+    b[:dim] = np.asarray(watch[0], dtype=np.float64)[:dim]
+    b[3:3 + dim] = np.asarray(watch[1], dtype=np.float64)[:dim]
+    return b

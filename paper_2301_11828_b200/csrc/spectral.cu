@@ -855,13 +855,14 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
         if (d == 2) {
             // persistent, cp.async-pipelined variant: NC*(XB + 2Q) slots
             const int Tp = threads_per_transform(lq, kPipeLogR);
-            const int NCp = std::max(1, kPipeThreads / Tp);
+            const int mode = e.d_coltab ? 2 : (e.real_symbol ? 1 : 0);
             const int ND = 3 * (e.M + 1);
-            const size_t psmem = sizeof(double2) * (size_t)NCp * (xbuf_slots(lq) + 2 * (1 << lq)) +
-                                 sizeof(double) * (size_t)NCp * ND;
+            const size_t per_col = sizeof(double2) * (size_t)(xbuf_slots(lq) + 2 * (1 << lq)) +
+                                   (mode == 2 ? sizeof(double) * (size_t)ND : 0);
+            const int NCp = (int)std::max<size_t>(1, std::min<size_t>(kPipeThreads / Tp, 225 * 1024 / per_col));
+            const size_t psmem = per_col * NCp;
             const int64_t nitems = (int64_t)((pl.ncols + NCp - 1) / NCp) * batch;
             const unsigned pgrid = (unsigned)std::min<int64_t>(nitems, e.num_sms);
-            const int mode = e.d_coltab ? 2 : (e.real_symbol ? 1 : 0);
 #define PIPE_ARGS spec, e.d_S2, e.d_sym, e.d_coltab, e.M, pl.ncols, pl.Nl, NCp, batch, e.d_tw, pl.logTWN
             if (mode == 2)
                 PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, 2><<<pgrid, NCp * Tp, psmem, s>>>(PIPE_ARGS)))
