@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(512) k_rfft_rows(const double* __restrict__ u,
     double2 v[R];
     const int shE = logTWN - (LOGQ + 1);
     const bool vec = (Nx & 1) == 0;
+    const double2 wbase = __ldg(tw + (t << shE));  // e^{-2 pi i t/(2Qx)}
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const int n = t + j * T;
@@ -142,7 +143,7 @@ __global__ void __launch_bounds__(512) k_rfft_rows(const double* __restrict__ u,
             if (vec) z = __ldg(reinterpret_cast<const double2*>(src + i0));
             else z = make_double2(src[i0], i0 + 1 < Nx ? src[i0 + 1] : 0.0);
         }
-        v[j] = eo ? cmul(z, __ldg(tw + (n << shE))) : z;
+        v[j] = eo ? cmul(z, tw32r<-1>(j * (16 / R), wbase)) : z;
     }
     reg_fft<LOGQ, 4, -1>(v, t, xb, make_fft_tw<LOGQ, 4>(t, tw, logTWN), BlockBar{});
 #pragma unroll
@@ -150,6 +151,11 @@ __global__ void __launch_bounds__(512) k_rfft_rows(const double* __restrict__ u,
     __syncthreads();
     constexpr int halfP = 2 * Q;
     const int shX = logTWN - (LOGQ + 2);
+    // e^{-2 pi i kx/Px} by recurrence along the thread's kx sequence
+    const bool rec = (blockDim.x % nr) == 0;
+    const int kstep = rec ? (int)blockDim.x / nr : 0;
+    double2 Wk = __ldg(tw + ((threadIdx.x / nr) << shX));
+    const double2 Wstep = __ldg(tw + ((kstep & (2 * halfP - 1)) << shX));
     for (int idx = threadIdx.x; idx < nr * Hx; idx += blockDim.x) {
         const int kx = idx / nr, rr = idx - kx * nr;
         const int k = kx & (halfP - 1);
@@ -160,7 +166,8 @@ __global__ void __launch_bounds__(512) k_rfft_rows(const double* __restrict__ u,
         const double2 Fe = cscale(cadd(A, B), 0.5);
         const double2 D = csub(A, B);
         const double2 Fo = make_double2(0.5 * D.y, -0.5 * D.x);
-        const double2 W = __ldg(tw + (kx << shX));
+        const double2 W = rec ? Wk : __ldg(tw + (kx << shX));
+        Wk = cmul(Wk, Wstep);
         S[((int64_t)slab * Hx + kx) * Nrow + row0 + rr] = cadd(Fe, cmul(W, Fo));
     }
 }
@@ -187,20 +194,30 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
     constexpr int halfP = 2 * Q;
     const int shX = logTWN - (LOGQ + 2);
     const double2* src = S + (int64_t)slab * Hx * Nrow + row0;
+    // twiddle e^{+2 pi i k/Px} by recurrence along the thread's k sequence
+    // (k advances by blockDim/nr per iteration); one table read for the base
+    // and one for the step; e^{+2 pi i (h-k)/Px} = -conj(e^{+2 pi i k/Px}).
+    const bool rec = (blockDim.x % nr) == 0;
+    const int kstep = rec ? (int)blockDim.x / nr : 0;
+    double2 Wk = twiddle<1>(tw, (threadIdx.x / nr) << shX);
+    const double2 Wstep = twiddle<1>(tw, (kstep & (halfP * 2 - 1)) << shX);
     for (int idx = threadIdx.x; idx < nr * (Q + 1); idx += blockDim.x) {
         const int k = idx / nr, rr = idx - k * nr;
         const int k2 = halfP - k;
+        const double2 W = rec ? Wk : twiddle<1>(tw, k << shX);
+        Wk = cmul(Wk, Wstep);
         const double2 Xa = src[(int64_t)k * Nrow + rr];
         const double2 Xb = src[(int64_t)k2 * Nrow + rr];
         double2* Z = sm + 2 * rr * XB;
         {
             const double2 s = cadd(Xa, cconj(Xb));
-            const double2 t2 = cmul(twiddle<1>(tw, k << shX), csub(Xa, cconj(Xb)));
+            const double2 t2 = cmul(W, csub(Xa, cconj(Xb)));
             Z[(k & 1) * XB + spad(k >> 1)] = make_double2(s.x - t2.y, s.y + t2.x);
         }
         if (k != 0 && k != Q) {
+            const double2 W2 = make_double2(-W.x, W.y);
             const double2 s = cadd(Xb, cconj(Xa));
-            const double2 t2 = cmul(twiddle<1>(tw, k2 << shX), csub(Xb, cconj(Xa)));
+            const double2 t2 = cmul(W2, csub(Xb, cconj(Xa)));
             Z[(k2 & 1) * XB + spad(k2 >> 1)] = make_double2(s.x - t2.y, s.y + t2.x);
         }
     }
@@ -212,10 +229,11 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
     __syncthreads();
     reg_fft<LOGQ, 4, 1>(v, t, xb, make_fft_tw<LOGQ, 4>(t, tw, logTWN), BlockBar{});
     const int shE = logTWN - (LOGQ + 1);
+    const double2 wbase = twiddle<1>(tw, t << shE);  // e^{+2 pi i t/(2Qx)}
 #pragma unroll
     for (int j = 0; j < R; ++j) {
         const int n = t + j * T;
-        xb[spad(n)] = eo ? cmul(twiddle<1>(tw, n << shE), v[j]) : v[j];
+        xb[spad(n)] = eo ? cmul(tw32r<1>(j * (16 / R), wbase), v[j]) : v[j];
     }
     __syncthreads();
     const int a = (slab / Nz) % dim;
@@ -397,6 +415,178 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// ------------------------------------------------------ K1, pipelined ---
+// Persistent x-forward pass: each CTA walks (slab, row-group) tiles; the next
+// tile's TR rows of reals land in a staging buffer via cp.async while the
+// current tile is transformed and written, so HBM latency overlaps compute.
+// Requires even Nx (16-byte row alignment); the plain kernel covers the rest.
+template <int LOGQ>
+__global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restrict__ u, double2* __restrict__ S,
+                                                           int Nx, int Nrow, int nslab, int Hx, int TR,
+                                                           const double2* __restrict__ tw, int logTWN) {
+    using Sh = FftShape<LOGQ, 4>;
+    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
+    extern __shared__ double2 sm[];
+    double* stage = reinterpret_cast<double*>(sm + 2 * TR * XB);  // TR rows x (4Q reals max)
+    const int gi = threadIdx.x >> Sh::LOGT;
+    const int t = threadIdx.x & (T - 1);
+    const int r = gi >> 1, eo = gi & 1;
+    const int shE = logTWN - (LOGQ + 1);
+    const int shX = logTWN - (LOGQ + 2);
+    constexpr int halfP = 2 * Q;
+    const double2 wbase = __ldg(tw + (t << shE));
+    const FftTw tws = make_fft_tw<LOGQ, 4>(t, tw, logTWN);
+    const int groups = (Nrow + TR - 1) / TR;
+    const int64_t ntiles = (int64_t)groups * nslab;
+    const int rowlen = 2 * Q;  // staged doubles per row (>= Nx)
+    auto fetch = [&](int64_t tile) {
+        const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
+        const int nr = min(TR, Nrow - row0);
+        const double* src = u + ((int64_t)slab * Nrow + row0) * Nx;
+        const int chunks_per_row = rowlen / 2;
+        for (int c = threadIdx.x; c < TR * chunks_per_row; c += blockDim.x) {
+            const int rr = c / chunks_per_row, i0 = 2 * (c - rr * chunks_per_row);
+            const bool p = rr < nr && i0 < Nx;
+            cp_async16(stage + rr * rowlen + i0, p ? src + (int64_t)rr * Nx + i0 : src, p);
+        }
+        cp_async_commit();
+    };
+    int64_t tile = blockIdx.x;
+    if (tile < ntiles) fetch(tile);
+    for (; tile < ntiles; tile += gridDim.x) {
+        const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
+        const int nr = min(TR, Nrow - row0);
+        double2* xb = sm + gi * XB;
+        double2 v[R];
+        cp_async_wait_all();
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const int n = t + j * T;
+            const double2 z = *reinterpret_cast<const double2*>(stage + r * rowlen + 2 * n);
+            v[j] = eo ? cmul(z, tw32r<-1>(j * (16 / R), wbase)) : z;
+        }
+        __syncthreads();
+        if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);
+        reg_fft<LOGQ, 4, -1>(v, t, xb, tws, BlockBar{});
+#pragma unroll
+        for (int j = 0; j < R; ++j) xb[spad(t + j * T)] = v[j];
+        __syncthreads();
+        const bool rec = (blockDim.x % nr) == 0;
+        const int kstep = rec ? (int)blockDim.x / nr : 0;
+        double2 Wk = __ldg(tw + ((threadIdx.x / nr) << shX));
+        const double2 Wstep = __ldg(tw + ((kstep & (2 * halfP - 1)) << shX));
+        for (int idx = threadIdx.x; idx < nr * Hx; idx += blockDim.x) {
+            const int kx = idx / nr, rr = idx - kx * nr;
+            const int k = kx & (halfP - 1);
+            const int k2 = (halfP - kx) & (halfP - 1);
+            const double2* Z = sm + 2 * rr * XB;
+            const double2 A = Z[(k & 1) * XB + spad(k >> 1)];
+            const double2 B = cconj(Z[(k2 & 1) * XB + spad(k2 >> 1)]);
+            const double2 Fe = cscale(cadd(A, B), 0.5);
+            const double2 D = csub(A, B);
+            const double2 Fo = make_double2(0.5 * D.y, -0.5 * D.x);
+            const double2 W = rec ? Wk : __ldg(tw + (kx << shX));
+            Wk = cmul(Wk, Wstep);
+            S[((int64_t)slab * Hx + kx) * Nrow + row0 + rr] = cadd(Fe, cmul(W, Fo));
+        }
+        __syncthreads();  // xb reused by the next tile's exchanges
+    }
+    cp_async_wait_all();
+}
+
+// ------------------------------------------------------ K5, pipelined ---
+// Persistent x-inverse pass, one row per tile, double-buffered: cp.async
+// drops the next row's half spectrum X[k] straight into the slot where
+// Z[k] lives (E/O split, padded) of the idle buffer, so the C2R pre-pass runs
+// in place and the gather latency of the transposed read overlaps the
+// current row's transform.
+template <int LOGQ>
+__global__ void __launch_bounds__(2 * FftShape<LOGQ, 4>::T, 1)
+    k_irfft_rows_pipe(const double2* __restrict__ S, double* __restrict__ f, int Nx, int Nrow, int nslab, int Nz,
+                      int dim, int Hx, const double2* __restrict__ tw, int logTWN, double scale,
+                      const uint8_t* __restrict__ cmask, const double* __restrict__ body, int64_t nodes) {
+    using Sh = FftShape<LOGQ, 4>;
+    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
+    constexpr int halfP = 2 * Q;
+    extern __shared__ double2 sm[];
+    const int eo = threadIdx.x >> Sh::LOGT;
+    const int t = threadIdx.x & (T - 1);
+    const int shX = logTWN - (LOGQ + 2);
+    const int shE = logTWN - (LOGQ + 1);
+    const double2 wbase = twiddle<1>(tw, t << shE);
+    const FftTw tws = make_fft_tw<LOGQ, 4>(t, tw, logTWN);
+    const int64_t ntiles = (int64_t)Nrow * nslab;
+    // slot of X[k] / Z[k] inside a buffer of 2*XB slots; X[halfP] in the spare slot
+    auto pos = [&](int k) { return k == halfP ? 2 * XB - 1 : (k & 1) * XB + spad(k >> 1); };
+    auto fetch = [&](int64_t tile, double2* buf) {
+        const int slab = (int)(tile / Nrow), row = (int)(tile % Nrow);
+        const double2* src = S + (int64_t)slab * Hx * Nrow + row;
+        for (int k = threadIdx.x; k < Hx; k += blockDim.x) cp_async16(buf + pos(k), src + (int64_t)k * Nrow, true);
+        cp_async_commit();
+    };
+    int cur = 0;
+    int64_t tile = blockIdx.x;
+    if (tile < ntiles) fetch(tile, sm);
+    const int kstep = blockDim.x;
+    const double2 Wstep = twiddle<1>(tw, (kstep & (2 * halfP - 1)) << shX);
+    for (; tile < ntiles; tile += gridDim.x) {
+        double2* buf = sm + cur * 2 * XB;
+        cp_async_wait_all();
+        __syncthreads();
+        if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x, sm + (cur ^ 1) * 2 * XB);
+        // Z[k] = (X[k] + conj X[h-k]) + i e^{+2 pi i k/Px} (X[k] - conj X[h-k]) in place, pairs (k, h-k)
+        double2 Wk = twiddle<1>(tw, threadIdx.x << shX);
+        for (int k = threadIdx.x; k <= Q; k += kstep) {
+            const double2 W = Wk;
+            Wk = cmul(Wk, Wstep);
+            const int k2 = halfP - k;
+            const double2 Xa = buf[pos(k)], Xb = buf[pos(k2)];
+            const double2 s1 = cadd(Xa, cconj(Xb));
+            const double2 t1 = cmul(W, csub(Xa, cconj(Xb)));
+            buf[pos(k)] = make_double2(s1.x - t1.y, s1.y + t1.x);
+            if (k != 0 && k != Q) {
+                const double2 W2 = make_double2(-W.x, W.y);
+                const double2 s2 = cadd(Xb, cconj(Xa));
+                const double2 t2 = cmul(W2, csub(Xb, cconj(Xa)));
+                buf[pos(k2)] = make_double2(s2.x - t2.y, s2.y + t2.x);
+            }
+        }
+        __syncthreads();
+        double2* xb = buf + eo * XB;
+        double2 v[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) v[j] = xb[spad(t + j * T)];
+        __syncthreads();
+        reg_fft<LOGQ, 4, 1>(v, t, xb, tws, BlockBar{});
+#pragma unroll
+        for (int j = 0; j < R; ++j) xb[spad(t + j * T)] = eo ? cmul(tw32r<1>(j * (16 / R), wbase), v[j]) : v[j];
+        __syncthreads();
+        const int slab = (int)(tile / Nrow), row = (int)(tile % Nrow);
+        const int a = (slab / Nz) % dim;
+        const int z = slab % Nz;
+        double* dst = f + ((int64_t)slab * Nrow + row) * Nx;
+        for (int n = threadIdx.x; n < Q; n += blockDim.x) {
+            const int i0 = 2 * n;
+            if (i0 >= Nx) break;
+            const double2 zz = cadd(buf[spad(n)], buf[XB + spad(n)]);
+            double v0 = zz.x * scale, v1 = zz.y * scale;
+            const int64_t node = ((int64_t)z * Nrow + row) * Nx + i0;
+            if (body) {
+                v0 += body[(int64_t)a * nodes + node];
+                v1 += body[(int64_t)a * nodes + node + 1];
+            }
+            if (cmask) {
+                if ((cmask[node] >> a) & 1u) v0 = 0.0;
+                if ((cmask[node + 1] >> a) & 1u) v1 = 0.0;
+            }
+            *reinterpret_cast<double2*>(dst + i0) = make_double2(v0, v1);
+        }
+        cur ^= 1;
+    }
+    cp_async_wait_all();
+}
 
 constexpr int kPipeLogR = 4;  // 16 points per thread: 256 threads per 4096-point column
 constexpr int kPipeThreads = 256;
@@ -718,6 +908,8 @@ static void smem_attr(const void* fn) {
 template <int L>
 static void set_attrs_l() {
     smem_attr((const void*)k_rfft_rows<L>);
+    smem_attr((const void*)k_rfft_rows_pipe<L>);
+    smem_attr((const void*)k_irfft_rows_pipe<L>);
     smem_attr((const void*)k_irfft_rows<L>);
     smem_attr((const void*)k_spectral<L, 2, true, 4, false>);
     smem_attr((const void*)k_spectral<L, 2, false, 4, false>);
@@ -825,8 +1017,16 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
         const int T = threads_per_transform(lqx, 4);
         dim3 grid((Ny + TR - 1) / TR, nslab);
         const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_slots(lqx);
-        PDGPU_DISPATCH_LOGQ(lqx, (k_rfft_rows<LQ><<<grid, 2 * TR * T, smem, s>>>(u, e.d_S1, Nx, Ny, pl.Hx, TR, e.d_tw,
-                                                                                pl.logTWN)));
+        const size_t psmem = smem + sizeof(double) * (size_t)TR * (2 << lqx);
+        if ((Nx & 1) == 0 && psmem <= 227 * 1024 && !getenv("PDGPU_NO_K1_PIPE")) {
+            const int64_t ntiles = (int64_t)((Ny + TR - 1) / TR) * nslab;
+            const unsigned pgrid = (unsigned)std::min<int64_t>(ntiles, e.num_sms);
+            PDGPU_DISPATCH_LOGQ(lqx, (k_rfft_rows_pipe<LQ><<<pgrid, 2 * TR * T, psmem, s>>>(
+                                         u, e.d_S1, Nx, Ny, nslab, pl.Hx, TR, e.d_tw, pl.logTWN)));
+        } else {
+            PDGPU_DISPATCH_LOGQ(lqx, (k_rfft_rows<LQ><<<grid, 2 * TR * T, smem, s>>>(u, e.d_S1, Nx, Ny, pl.Hx, TR,
+                                                                                    e.d_tw, pl.logTWN)));
+        }
     }
     double2* spec = e.d_S1;
     if (d == 3) {
@@ -898,9 +1098,19 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
         const int T = threads_per_transform(lqx, 4);
         dim3 grid((Ny + TR - 1) / TR, nslab);
         const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_slots(lqx);
-        PDGPU_DISPATCH_LOGQ(lqx, (k_irfft_rows<LQ><<<grid, 2 * TR * T, smem, s>>>(
-                                     xin, f, Nx, Ny, Nz, d, pl.Hx, TR, e.d_tw, pl.logTWN, scale, cmask, body,
-                                     pl.nodes)));
+        const size_t psmem = sizeof(double2) * (size_t)4 * xbuf_slots(lqx);
+        if ((Nx & 1) == 0 && psmem <= 227 * 1024 && T >= 16 && !getenv("PDGPU_NO_K5_PIPE")) {
+            const int64_t ntiles = (int64_t)Ny * nslab;
+            const int per_sm = std::max<int>(1, (int)(227 * 1024 / psmem));
+            const unsigned pgrid = (unsigned)std::min<int64_t>(ntiles, (int64_t)e.num_sms * per_sm);
+            PDGPU_DISPATCH_LOGQ(lqx, (k_irfft_rows_pipe<LQ><<<pgrid, 2 * T, psmem, s>>>(
+                                         xin, f, Nx, Ny, nslab, Nz, d, pl.Hx, e.d_tw, pl.logTWN, scale, cmask, body,
+                                         pl.nodes)));
+        } else {
+            PDGPU_DISPATCH_LOGQ(lqx, (k_irfft_rows<LQ><<<grid, 2 * TR * T, smem, s>>>(
+                                         xin, f, Nx, Ny, Nz, d, pl.Hx, TR, e.d_tw, pl.logTWN, scale, cmask, body,
+                                         pl.nodes)));
+        }
     }
     check(cudaGetLastError(), "fast_apply launch");
 }
