@@ -95,6 +95,8 @@ int pdgpu_ledger_pairs(pdgpu_t h, int64_t* out_pairs, int64_t cap, int64_t* coun
  * f += De u (surface rows) + sum_q K(q-p)(u_p - u_q) (fracture rows), rows
  * constrained in the output direction untouched.  Device pointers. */
 int pdgpu_apply_corrections(pdgpu_t h, const double* u, double* f, int batch, void* stream);
+/* Same on host fields ([batch][dim][N]); f is updated in place. */
+int pdgpu_apply_corrections_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes, int batch);
 /* K.u as the reference's tests and Simulation compute it:
  * FastForce::apply + apply_corrections (e.g. tests/test_corrections.cpp:107-110). */
 int pdgpu_matvec(pdgpu_t h, const double* u, double* f, int batch, void* stream);

@@ -39,6 +39,7 @@ SIGNATURES = {
     "pdgpu_break_bonds": (C.c_int, [C.c_void_p, c_int64_p, C.c_int64]),
     "pdgpu_ledger_pairs": (C.c_int, [C.c_void_p, c_int64_p, C.c_int64, c_int64_p]),
     "pdgpu_apply_corrections": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "pdgpu_apply_corrections_host": (C.c_int, [C.c_void_p, c_double_p, c_double_p, C.c_int64, C.c_int]),
     "pdgpu_matvec": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "pdgpu_matvec_host": (C.c_int, [C.c_void_p, c_double_p, c_double_p, C.c_int64, C.c_int]),
     "pdgpu_evaluate_force": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -590,6 +590,21 @@ int pdgpu_apply_corrections(pdgpu_t h, const double* u, double* f, int batch, vo
     });
 }
 
+int pdgpu_apply_corrections_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes, int batch) {
+    return guarded([&] {
+        if (!h || !u || !f || batch < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
+        if (n_nodes != h->plan.nodes) throw PdError(PDGPU_ERR_SHAPE_MISMATCH, "field length does not match the lattice");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const int64_t m = (int64_t)batch * h->dim * n_nodes;
+        ensure_stage(*h, m);
+        cuda_check(cudaMemcpyAsync(h->d_u_stage, u, sizeof(double) * m, cudaMemcpyHostToDevice, h->stream), "H2D");
+        cuda_check(cudaMemcpyAsync(h->d_f_stage, f, sizeof(double) * m, cudaMemcpyHostToDevice, h->stream), "H2D");
+        launch_corrections(*h, h->d_u_stage, h->d_f_stage, batch, h->stream, 1.0);
+        cuda_check(cudaMemcpyAsync(f, h->d_f_stage, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(h->stream), "apply_corrections_host");
+    });
+}
+
 int pdgpu_matvec(pdgpu_t h, const double* u, double* f, int batch, void* stream) {
     return guarded([&] {
         if (!h || !u || !f || batch < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
