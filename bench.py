@@ -10,17 +10,19 @@ K.u = FastForce::apply + apply_corrections over the 16 vectors.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-value  : DOF-matvecs/s over the timed steps, inputs resident in HBM
-         (inputs 4.3 GB per step >> 126 MB L2: no flush needed).
-e2e    : the same metric through the public host API pdgpu_matvec_host
-         (pinned host u in, host f out, copies inside the timed region).
-roofline: the dominant kernel (K3, fused y-FFT + symbol + inverse y-FFT),
-         algorithmic bytes per launch / its mean CUDA-event duration.
+value   : DOF-matvecs/s over the timed steps, inputs resident in HBM
+          (4.3 GB per step >> 126 MB L2: no flush needed).
+e2e     : the same metric through the public host API pdgpu_matvec_host
+          (pinned host u in, host f out, copies inside the timed region).
+roofline: the dominant kernel (K3: y-FFT + symbol + inverse y-FFT),
+          algorithmic bytes per launch / its mean CUDA-event duration.
+configs : secondary BASELINE numbers -- CG solve times (configs 1, 3, 4) and
+          the 3D K.u rate (config 4, 128^3) -- skipped with --no-extra.
 cpu_baseline: the reference's own FastForce::apply + apply_corrections
-         (oracle/_ref, headers compiled unmodified) on the host cores,
-         bounded sample.  --impl reference prints that arm alone.
+          (oracle/_ref, headers compiled unmodified) on the host cores,
+          bounded sample.  --impl reference prints that arm alone.
 N > 1 (torchrun): every rank runs its own 16-vector batch (independent
-replicas over vectors, no data-path collective) -> weak scaling.
+vectors, no data-path collective) -> weak scaling; time = max over ranks.
 """
 from __future__ import annotations
 
@@ -49,43 +51,62 @@ def workload_config(n_gpus: int):
             "grid": [N_SIDE, N_SIDE], "dof_per_node": DIM, "batch": BATCH, "delta_over_h": 3.015, "M": M,
             "E": 1.0, "thickness": 1.0, "corrections": "surface diagonal (12N-36 rows), no cracks",
             "padding": "2N per axis (R2C half spectrum)", "l2": "inputs 4.3 GB per step > L2, no flush",
-            "parallelism": f"replicas{n_gpus} (batch per rank)" if n_gpus > 1 else "single GPU"}
+            "parallelism": f"{n_gpus} ranks x own batch (replicas, no data-path collective)" if n_gpus > 1
+            else "single GPU"}
 
 
 # ----------------------------------------------------------------- clocks --
 class ClockSampler:
+    """nvidia-smi -lms 100 streamed during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
         self.samples = []
-        self._stop = threading.Event()
-        self._t = None
-
-    def _run(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
-                vals = [v.strip() for v in out.stdout.strip().split(",")]
-                if len(vals) >= 6:
-                    self.samples.append(vals)
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self.proc = None
+        self.thread = None
 
     def start(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        time.sleep(0.3)  # first sample lands before the timed region
+
+    def _read(self):
+        for line in self.proc.stdout:
+            vals = [v.strip() for v in line.strip().split(",")]
+            if len(vals) >= 6:
+                self.samples.append(vals)
 
     def stop(self):
-        self._stop.set()
-        if self._t:
-            self._t.join(timeout=10)
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=5)
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+
+        sm = [v for v in (num(s[0]) for s in self.samples) if v is not None]
+        mx = [v for v in (num(s[1]) for s in self.samples) if v is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
@@ -108,9 +129,7 @@ def k3_algorithmic_bytes(n_side: int, batch: int):
     component per vector) + the real symbol once per launch (n_pairs x Hx x Py)."""
     hx = n_side + 1          # Px/2 + 1 with Px = 2N
     ny, py = n_side, 2 * n_side
-    data = batch * DIM * hx * ny * 16 * 2
-    sym = 3 * hx * py * 8
-    return data + sym
+    return batch * DIM * hx * ny * 16 * 2 + 3 * hx * py * 8
 
 
 def matvec_algorithmic_bytes(n_side: int, batch: int):
@@ -131,16 +150,8 @@ def _mem_available_bytes():
     return 16 << 30
 
 
-def reference_problem(n_side):
-    from oracle.oracle import RefProblem
-    h = 1.0 / n_side
-    r = RefProblem((n_side, n_side), h=h, delta=3.015 * h, M=M, E=1.0, thickness=1.0)
-    r.finalize()
-    return r
-
-
 def cpu_threads_for(n_side):
-    # one reference FastForce instance holds (n_pairs + d + 2) padded complex grids
+    # one reference FastForce holds (n_pairs + d + 2) padded complex grids (convolution.hpp:263-266)
     footprint = (3 + DIM + 2) * (2 * n_side) ** 2 * 16 + 4 * DIM * n_side * n_side * 8
     cores = os.cpu_count() or 1
     return max(1, min(cores, int(0.6 * _mem_available_bytes() // footprint))), cores
@@ -154,7 +165,9 @@ def cpu_reference_sample(n_side, steps=1, budget_s=150.0):
     if not orc.ref_available():
         return None
     threads, cores = cpu_threads_for(n_side)
-    r = reference_problem(n_side)
+    h = 1.0 / n_side
+    r = orc.RefProblem((n_side, n_side), h=h, delta=3.015 * h, M=M, E=1.0, thickness=1.0)
+    r.finalize()
     rng = np.random.default_rng(1234)
     u = rng.uniform(-1.0, 1.0, size=(threads, DIM, n_side * n_side))
     times = []
@@ -171,16 +184,9 @@ def cpu_reference_sample(n_side, steps=1, budget_s=150.0):
                       f"absent), g++ -O2", "steps_timed": len(times), "s_per_step": per_step}
 
 
-# -------------------------------------------------------------------- main --
-def dist_env():
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
-
-
 def run_reference_arm(args):
-    rank, world, _ = dist_env()
+    from paper_2301_11828_b200 import dist as D
+    rank, world, _ = D.env()
     if rank != 0:
         return 0
     res = cpu_reference_sample(N_SIDE, steps=max(args.steps, 1), budget_s=args.ref_budget)
@@ -199,16 +205,98 @@ def run_reference_arm(args):
     return 0
 
 
+# -------------------------------------------------------- secondary configs --
+def clamp_boxes(dim, dl):
+    out = []
+    for ax in range(dim):
+        lo0, hi0 = [0.0] * dim, [1.0] * dim
+        hi0[ax] = dl
+        lo1, hi1 = [0.0] * dim, [1.0] * dim
+        lo1[ax] = 1.0 - dl
+        out += [(lo0, hi0), (lo1, hi1)]
+    return out
+
+
+def extra_configs(device, stream):
+    """CG solve times (configs 1, 3, 4) and the 3D K.u rate (config 4), device-resident."""
+    import torch
+    from paper_2301_11828_b200 import FastForce, build_kernel
+    out = {}
+
+    def engine(dims, constraints):
+        dim = len(dims)
+        h = 1.0 / dims[0]
+        ff = FastForce(dims, M, build_kernel(dim, h, 3.015 * h, M, 1.0, 1.0), device=device)
+        ff.set_geometry(h, [0.0] * dim, 3.015 * h, 1.0)
+        for lo, hi, mask, value in constraints:
+            ff.add_constraint(lo, hi, mask, 0, value)
+        return ff
+
+    def timed(fn):
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        r = fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        return ev0.elapsed_time(ev1), r
+
+    g = torch.Generator(device="cuda")
+    # config 1: 128^2, clamped delta layers, CG to 1e-10
+    dims = (128, 128)
+    dl = 3.015 / 128
+    ff = engine(dims, [(lo, hi, 3, 0.0) for lo, hi in clamp_boxes(2, dl)])
+    b = torch.empty((2, 128 * 128), dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=g.manual_seed(1001))
+    x = torch.empty_like(b)
+    ff.cg_solve_device(b, x, tol=1e-10, maxit=20000, stream=stream)  # warm
+    ms, (it, rel) = timed(lambda: ff.cg_solve_device(b, x, tol=1e-10, maxit=20000, stream=stream))
+    out["config1_cg"] = {"grid": [128, 128], "tol": 1e-10, "iterations": it, "relres": rel, "solve_ms": ms}
+    ff.close()
+    # config 3: 1024^2, centre crack L/2, +-1e-3 on top/bottom layers (u_y), CG to 1e-10
+    n = 1024
+    dl = 3.015 / n
+    cons = [((0.0, 1.0 - dl), (1.0, 1.0), 0b01, 0.0), ((0.0, 1.0 - dl), (1.0, 1.0), 0b10, 1e-3),
+            ((0.0, 0.0), (1.0, dl), 0b01, 0.0), ((0.0, 0.0), (1.0, dl), 0b10, -1e-3)]
+    ff = engine((n, n), cons)
+    bonds = ff.seed_segment((0.25, 0.5), (0.75, 0.5))
+    b = torch.zeros((2, n * n), dtype=torch.float64, device="cuda")
+    x = torch.empty_like(b)
+    ms, (it, rel) = timed(lambda: ff.cg_solve_device(b, x, tol=1e-10, maxit=50000, stream=stream))
+    out["config3_cg"] = {"grid": [n, n], "crack_bonds": bonds, "tol": 1e-10, "iterations": it, "relres": rel,
+                         "solve_ms": ms}
+    ff.close()
+    # config 4: 128^3 clamped cube; K.u rate and CG to 1e-9
+    n = 128
+    dl = 3.015 / n
+    ff = engine((n, n, n), [(lo, hi, 7, 0.0) for lo, hi in clamp_boxes(3, dl)])
+    u = torch.empty((3, n ** 3), dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=g.manual_seed(4000))
+    f = torch.empty_like(u)
+    for _ in range(3):
+        ff.matvec_device(u, f, 1, stream)
+    reps = 20
+    ms, _ = timed(lambda: [ff.matvec_device(u, f, 1, stream) for _ in range(reps)])
+    out["config4_matvec"] = {"grid": [n, n, n], "value": 3 * n ** 3 / (ms / reps * 1e-3), "unit": UNIT,
+                             "ms_per_matvec": ms / reps}
+    b = torch.empty((3, n ** 3), dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=g.manual_seed(4001))
+    x = torch.empty_like(b)
+    ms, (it, rel) = timed(lambda: ff.cg_solve_device(b, x, tol=1e-9, maxit=20000, stream=stream))
+    out["config4_cg"] = {"grid": [n, n, n], "tol": 1e-9, "iterations": it, "relres": rel, "solve_ms": ms}
+    ff.close()
+    return out
+
+
+# -------------------------------------------------------------------- main --
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=N_SIDE)
     ap.add_argument("--batch", type=int, default=BATCH)
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the secondary configs")
     ap.add_argument("--ref-budget", type=float, default=150.0)
     args = ap.parse_args()
     globals()["N_SIDE"] = args.n
@@ -216,15 +304,13 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args)
 
-    import numpy as np
     import torch
-    import torch.distributed as dist
-
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_2301_11828_b200 import FastForce, build_kernel
+    from paper_2301_11828_b200 import dist as D
+
+    rank, world, local = D.env()
+    torch.cuda.set_device(local)
+    D.init("nccl", torch.device("cuda", local))
 
     n = N_SIDE * N_SIDE
     h = 1.0 / N_SIDE
@@ -233,7 +319,8 @@ def main():
     ff.set_geometry(h, [0.0, 0.0], 3.015 * h, 1.0)
 
     stream = torch.cuda.Stream()
-    gen = torch.Generator(device="cuda").manual_seed(1000 * 2 + rank)
+    lo, _ = D.vector_range(BATCH, rank, world)
+    gen = torch.Generator(device="cuda").manual_seed(D.vector_seed(2000, lo))
     u = torch.empty((BATCH, DIM, n), dtype=torch.float64, device="cuda")
     u.uniform_(-1.0, 1.0, generator=gen)
     f = torch.empty_like(u)
@@ -251,8 +338,7 @@ def main():
     launches0 = ff.launch_count()
     clk = ClockSampler(local)
     clk.start()
-    if world > 1:
-        dist.barrier()
+    D.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -261,24 +347,16 @@ def main():
         step()
     ev1.record(stream)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    D.barrier()
     clocks = clk.stop()
-    ms_total = ev0.elapsed_time(ev1)
+    ms_total = D.max_over_ranks(ev0.elapsed_time(ev1), "cuda")
     launches = ff.launch_count() - launches0
     passes = ff.timing_read()
     ff.timing(False)
-    if world > 1:
-        t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total = float(t.item())
     ms_step = ms_total / args.steps
     value = world * BATCH * DIM * n / (ms_step * 1e-3)
-
-    # sanity: finite output
     assert torch.isfinite(f).all().item(), "non-finite K.u"
 
-    # roofline of the dominant kernel (K3) from the live CUDA events
     peak, peak_src = measured_peaks()
     k3_ms, k3_n = passes.get("K3_spectral", (0.0, 0))
     k3_bytes = k3_algorithmic_bytes(N_SIDE, BATCH)
@@ -296,13 +374,15 @@ def main():
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             pass
-    roofline = {"bound": "hbm", "kernel": "k_spectral (K3: y-FFT + symbol + inverse y-FFT)", "achieved": k3_gbs,
-                "peak": peak, "unit": "GB/s", "frac": (k3_gbs / peak) if k3_gbs else None, "traffic": traffic,
-                "algorithmic_bytes_per_launch": k3_bytes, "mean_launch_ms": k3_avg_s * 1e3, "peak_source": peak_src,
+    roofline = {"bound": "hbm", "kernel": "k_spectral2d_pipe (K3: y-FFT + symbol + inverse y-FFT)",
+                "achieved": k3_gbs, "peak": peak, "unit": "GB/s", "frac": (k3_gbs / peak) if k3_gbs else None,
+                "traffic": traffic, "algorithmic_bytes_per_launch": k3_bytes, "mean_launch_ms": k3_avg_s * 1e3,
+                "peak_source": peak_src,
                 "matvec": {"algorithmic_bytes_per_step": mv_bytes, "achieved_gbs": mv_gbs, "frac": mv_gbs / peak,
                            "model": "SURVEY 8(d): 80 B/DOF/vector + 48N B symbol"},
                 "passes_ms_per_step": {k: v[0] / args.steps for k, v in passes.items()},
-                "symbol_mode": ff.symbol_mode()}
+                "symbol_mode": ff.symbol_mode(),
+                "note": "path is fp64-pipe bound on B200 (DESIGN.md sec.3); HBM fraction per the contract"}
 
     # end to end through the public host API (pinned host buffers)
     e2e = None
@@ -313,22 +393,28 @@ def main():
         uh_np, fh_np = uh.numpy(), fh.numpy()
         ff.matvec(uh_np, out=fh_np)  # warm the staging buffers (not timed)
         e2e_steps = max(1, min(args.steps, 3))
-        if world > 1:
-            dist.barrier()
+        D.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(e2e_steps):
             ff.matvec(uh_np, out=fh_np)
         torch.cuda.synchronize()
-        e2e_s = (time.perf_counter() - t0) / e2e_steps
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_s = float(t.item())
+        e2e_s = D.max_over_ranks((time.perf_counter() - t0) / e2e_steps, "cuda")
         nbytes = BATCH * DIM * n * 8
         e2e = {"value": world * BATCH * DIM * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "steps": e2e_steps, "ms_per_step": e2e_s * 1e3,
-               "api": "pdgpu_matvec_host (pinned host u -> host f)"}
+               "api": "pdgpu_matvec_host (pinned host u -> host f; H2D/compute/D2H pipelined in 2-vector chunks)"}
+        del uh, fh
+    ff.close()
+    del u, f
+    torch.cuda.empty_cache()
+
+    extra = None
+    if not args.no_extra and world == 1:
+        try:
+            extra = extra_configs(local, stream)
+        except Exception as exc:
+            extra = {"error": str(exc)[:300]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -344,11 +430,9 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1], torch Philox)",
                 "config": workload_config(world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clocks}
+                "gpu_launches": launches, "clocks": clocks, "configs": extra}
         print(json.dumps(line))
-    if world > 1:
-        dist.destroy_process_group()
-    ff.close()
+    D.finalize()
     return 0
 
 

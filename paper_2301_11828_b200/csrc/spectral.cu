@@ -588,6 +588,76 @@ __global__ void __launch_bounds__(2 * FftShape<LOGQ, 4>::T, 1)
     cp_async_wait_all();
 }
 
+// ------------------------------------------- K3, component-grouped (2D) ---
+// Two warp groups per column: group c owns component c end to end (forward
+// FFT, its row of the 2x2 symbol product, inverse FFT), so each thread keeps
+// one 16-point spectrum and a CTA runs twice the warps of the single-group
+// kernel.  The only cross-group traffic is the product's operand swap through
+// the groups' exchange buffers.  Half 0 parks z^0 in `out`, half 1
+// read-modify-writes it (out must not alias in).
+template <int LOGQ, bool REAL>
+__global__ void __launch_bounds__(512, 1) k_spectral2d_cg(const double2* __restrict__ in, double2* out,
+                                                          const void* __restrict__ sym, int ncols, int Nl, int NC,
+                                                          int batch, const double2* __restrict__ tw, int logTWN) {
+    using Sh = FftShape<LOGQ, 4>;
+    constexpr int Q = Sh::Q, T = Sh::T, XB = Sh::XBUF, RR = Sh::R;
+    extern __shared__ double2 sm[];
+    const int g = threadIdx.x >> Sh::LOGT;  // c * NC + ci
+    const int c = g / NC, ci = g - c * NC;
+    const int t = threadIdx.x & (T - 1);
+    double2* xb = sm + g * XB;
+    const double2* xo = sm + ((1 - c) * NC + ci) * XB;  // partner component's buffer
+    const int shP = logTWN - (LOGQ + 1);
+    const FftTw tws = make_fft_tw<LOGQ, 4>(t, tw, logTWN);
+    const double2 wt = __ldg(tw + (t << shP));
+    const int b = blockIdx.x;
+    const int col = blockIdx.y * NC + ci;
+    const bool valid = col < ncols;
+    const int cc = valid ? col : 0;
+    const double2* x = in + ((int64_t)(b * 2 + c) * ncols + cc) * Nl;
+    double2* z = out + ((int64_t)(b * 2 + c) * ncols + cc) * Nl;
+    const int pself = 2 * c;  // xx (c=0) or yy (c=1); cross term xy = 1
+    double2 v[RR];
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int j = 0; j < RR; ++j) {
+            const int n = t + j * T;
+            double2 xv = make_double2(0.0, 0.0);
+            if (valid && n < Nl) xv = x[n];
+            v[j] = h ? cmul(xv, tw32r<-1>(j * (16 / RR), wt)) : xv;
+        }
+        reg_fft<LOGQ, 4, -1>(v, t, xb, tws, BlockBar{});
+#pragma unroll
+        for (int j = 0; j < RR; ++j) xb[spad(t + j * T)] = v[j];
+        __syncthreads();
+        const int64_t sbase = ((int64_t)cc * 2 + h) * Q;
+#pragma unroll
+        for (int j = 0; j < RR; ++j) {
+            const int k = t + j * T;
+            const double2 uo = xo[spad(k)];
+            if (REAL) {
+                const double* H = (const double*)sym + (sbase + k) * 3;
+                const double gs = __ldg(H + pself), gx = __ldg(H + 1);
+                v[j] = make_double2(gs * v[j].x + gx * uo.x, gs * v[j].y + gx * uo.y);
+            } else {
+                const double2* H = (const double2*)sym + (sbase + k) * 3;
+                v[j] = cadd(cmul(__ldg(H + pself), v[j]), cmul(__ldg(H + 1), uo));
+            }
+        }
+        __syncthreads();
+        reg_fft<LOGQ, 4, 1>(v, t, xb, tws, BlockBar{});
+#pragma unroll
+        for (int j = 0; j < RR; ++j) {
+            const int n = t + j * T;
+            if (valid && n < Nl) {
+                if (h == 0) z[n] = v[j];
+                else z[n] = cadd(z[n], cmul(tw32r<1>(j * (16 / RR), cconj(wt)), v[j]));
+            }
+        }
+    }
+}
+
 constexpr int kPipeLogR = 4;  // 16 points per thread: 256 threads per 4096-point column
 constexpr int kPipeThreads = 256;
 
@@ -910,6 +980,8 @@ static void set_attrs_l() {
     smem_attr((const void*)k_rfft_rows<L>);
     smem_attr((const void*)k_rfft_rows_pipe<L>);
     smem_attr((const void*)k_irfft_rows_pipe<L>);
+    smem_attr((const void*)k_spectral2d_cg<L, true>);
+    smem_attr((const void*)k_spectral2d_cg<L, false>);
     smem_attr((const void*)k_irfft_rows<L>);
     smem_attr((const void*)k_spectral<L, 2, true, 4, false>);
     smem_attr((const void*)k_spectral<L, 2, false, 4, false>);
@@ -1052,7 +1124,20 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
         const bool zsmem = pl.k3_halves == 2;
         const size_t smem =
             sizeof(double2) * (size_t)NC * (xbuf_slots(lq) + (zsmem ? 2 * d - 1 : d - 1) * (1 << lq));
-        if (d == 2) {
+        const char* k3env = getenv("PDGPU_K3");
+        if (d == 2 && k3env && std::string(k3env) == "cg" && e.d_coltab == nullptr) {
+            const int Tc = threads_per_transform(lq, 4);
+            const int NCc = std::max(1, 256 / Tc);
+            const size_t csmem = sizeof(double2) * (size_t)2 * NCc * xbuf_slots(lq);
+            dim3 cgrid(batch, (pl.ncols + NCc - 1) / NCc);
+            if (e.real_symbol)
+                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_cg<LQ, true><<<cgrid, 2 * NCc * Tc, csmem, s>>>(
+                                            spec, e.d_S2, e.d_sym, pl.ncols, pl.Nl, NCc, batch, e.d_tw, pl.logTWN)))
+            else
+                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_cg<LQ, false><<<cgrid, 2 * NCc * Tc, csmem, s>>>(
+                                            spec, e.d_S2, e.d_sym, pl.ncols, pl.Nl, NCc, batch, e.d_tw, pl.logTWN)))
+            xin = e.d_S2;
+        } else if (d == 2) {
             // persistent, cp.async-pipelined variant: NC*(XB + 2Q) slots
             const int Tp = threads_per_transform(lq, kPipeLogR);
             const int mode = e.d_coltab ? 2 : (e.real_symbol ? 1 : 0);

@@ -1,0 +1,73 @@
+"""Multi-GPU plumbing for the batched mat-vec (one process per GPU).
+
+Round 1 shards the work unit BASELINE.json batches -- independent
+displacement vectors -- across ranks: every rank owns whole vectors, there is
+no data-path collective (SURVEY.md sec.8e "replicas"), and the only
+communication is the timing reduction (max over ranks) and the result
+checksums.  The slab-decomposed FFT (all-to-all transposes) is the next
+multi-GPU item.
+"""
+from __future__ import annotations
+
+import os
+
+import torch
+import torch.distributed as dist
+
+
+def env():
+    """(rank, world, local_rank) from the torchrun environment."""
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def init(backend: str = "nccl", device=None):
+    rank, world, local = env()
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if backend == "nccl":
+            dist.init_process_group(backend, device_id=device)
+        else:
+            dist.init_process_group(backend)
+    return rank, world, local
+
+
+def vector_range(total: int, rank: int, world: int, weak: bool = True):
+    """Vectors [lo, hi) owned by `rank`.  weak: every rank owns `total`
+    vectors of its own (global ids rank*total + i); strong: `total` split."""
+    if weak:
+        return rank * total, (rank + 1) * total
+    per = (total + world - 1) // world
+    return min(rank * per, total), min((rank + 1) * per, total)
+
+
+def vector_seed(base: int, gid: int) -> int:
+    """Seed of global vector gid (seed = 1000*config + index)."""
+    return base + gid
+
+
+def max_over_ranks(value: float, device="cpu") -> float:
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def gather_checksums(local, device="cpu"):
+    """All ranks' per-vector checksums, rank-major (list of lists)."""
+    t = torch.tensor(list(local), dtype=torch.float64, device=device)
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [t.tolist()]
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [o.tolist() for o in out]
+
+
+def barrier():
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+def finalize():
+    if dist.is_available() and dist.is_initialized():
+        dist.destroy_process_group()
