@@ -60,6 +60,8 @@ struct Engine {
     void* d_sym = nullptr;          // symbol: real double or double2, np * ncols * Pl
     double* d_K = nullptr;          // stencils on device (np * ss)
     double* d_coltab = nullptr;     // separable symbol: per column n_pairs x (M+1) coefficients (2D)
+    double2* d_scratch = nullptr;   // per-CTA component park of the two-CTA/SM spectral kernel
+    int64_t scratch_cap = 0;
     int* d_offs = nullptr;          // nof*3
     long long* d_disp = nullptr;    // nof: linear node displacement of each offset
     int64_t cap_batch = 0;

@@ -271,15 +271,15 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[1 << LOGR], double2 base) 
         for (int m = 0; m < r; ++m) w[m] = v[i + m * nb];
         if constexpr (LOGNS > 0) {
             static_assert(nb == 1, "twiddled passes are full radix");
-            double2 pw[r];
-            pw[1] = S > 0 ? cconj(base) : base;
+            // sequential powers: only the base and the running power stay
+            // live (register pressure), error grows to ~r ulp
+            const double2 b1 = S > 0 ? cconj(base) : base;
+            double2 p = b1;
 #pragma unroll
-            for (int m = 2; m < r; ++m) {
-                const int hb = m >= 8 ? 8 : (m >= 4 ? 4 : 2);  // highest power of two <= m
-                pw[m] = (hb == m) ? csqr(pw[m >> 1]) : cmul(pw[hb], pw[m - hb]);
+            for (int m = 1; m < r; ++m) {
+                w[m] = cmul(w[m], p);
+                if (m + 1 < r) p = cmul(p, b1);
             }
-#pragma unroll
-            for (int m = 1; m < r; ++m) w[m] = cmul(w[m], pw[m]);
         }
         dft<LR, S>(w);
 #pragma unroll

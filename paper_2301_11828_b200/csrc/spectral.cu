@@ -496,168 +496,6 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
     cp_async_wait_all();
 }
 
-// ------------------------------------------------------ K5, pipelined ---
-// Persistent x-inverse pass, one row per tile, double-buffered: cp.async
-// drops the next row's half spectrum X[k] straight into the slot where
-// Z[k] lives (E/O split, padded) of the idle buffer, so the C2R pre-pass runs
-// in place and the gather latency of the transposed read overlaps the
-// current row's transform.
-template <int LOGQ>
-__global__ void __launch_bounds__(2 * FftShape<LOGQ, 4>::T, 1)
-    k_irfft_rows_pipe(const double2* __restrict__ S, double* __restrict__ f, int Nx, int Nrow, int nslab, int Nz,
-                      int dim, int Hx, const double2* __restrict__ tw, int logTWN, double scale,
-                      const uint8_t* __restrict__ cmask, const double* __restrict__ body, int64_t nodes) {
-    using Sh = FftShape<LOGQ, 4>;
-    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
-    constexpr int halfP = 2 * Q;
-    extern __shared__ double2 sm[];
-    const int eo = threadIdx.x >> Sh::LOGT;
-    const int t = threadIdx.x & (T - 1);
-    const int shX = logTWN - (LOGQ + 2);
-    const int shE = logTWN - (LOGQ + 1);
-    const double2 wbase = twiddle<1>(tw, t << shE);
-    const FftTw tws = make_fft_tw<LOGQ, 4>(t, tw, logTWN);
-    const int64_t ntiles = (int64_t)Nrow * nslab;
-    // slot of X[k] / Z[k] inside a buffer of 2*XB slots; X[halfP] in the spare slot
-    auto pos = [&](int k) { return k == halfP ? 2 * XB - 1 : (k & 1) * XB + spad(k >> 1); };
-    auto fetch = [&](int64_t tile, double2* buf) {
-        const int slab = (int)(tile / Nrow), row = (int)(tile % Nrow);
-        const double2* src = S + (int64_t)slab * Hx * Nrow + row;
-        for (int k = threadIdx.x; k < Hx; k += blockDim.x) cp_async16(buf + pos(k), src + (int64_t)k * Nrow, true);
-        cp_async_commit();
-    };
-    int cur = 0;
-    int64_t tile = blockIdx.x;
-    if (tile < ntiles) fetch(tile, sm);
-    const int kstep = blockDim.x;
-    const double2 Wstep = twiddle<1>(tw, (kstep & (2 * halfP - 1)) << shX);
-    for (; tile < ntiles; tile += gridDim.x) {
-        double2* buf = sm + cur * 2 * XB;
-        cp_async_wait_all();
-        __syncthreads();
-        if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x, sm + (cur ^ 1) * 2 * XB);
-        // Z[k] = (X[k] + conj X[h-k]) + i e^{+2 pi i k/Px} (X[k] - conj X[h-k]) in place, pairs (k, h-k)
-        double2 Wk = twiddle<1>(tw, threadIdx.x << shX);
-        for (int k = threadIdx.x; k <= Q; k += kstep) {
-            const double2 W = Wk;
-            Wk = cmul(Wk, Wstep);
-            const int k2 = halfP - k;
-            const double2 Xa = buf[pos(k)], Xb = buf[pos(k2)];
-            const double2 s1 = cadd(Xa, cconj(Xb));
-            const double2 t1 = cmul(W, csub(Xa, cconj(Xb)));
-            buf[pos(k)] = make_double2(s1.x - t1.y, s1.y + t1.x);
-            if (k != 0 && k != Q) {
-                const double2 W2 = make_double2(-W.x, W.y);
-                const double2 s2 = cadd(Xb, cconj(Xa));
-                const double2 t2 = cmul(W2, csub(Xb, cconj(Xa)));
-                buf[pos(k2)] = make_double2(s2.x - t2.y, s2.y + t2.x);
-            }
-        }
-        __syncthreads();
-        double2* xb = buf + eo * XB;
-        double2 v[R];
-#pragma unroll
-        for (int j = 0; j < R; ++j) v[j] = xb[spad(t + j * T)];
-        __syncthreads();
-        reg_fft<LOGQ, 4, 1>(v, t, xb, tws, BlockBar{});
-#pragma unroll
-        for (int j = 0; j < R; ++j) xb[spad(t + j * T)] = eo ? cmul(tw32r<1>(j * (16 / R), wbase), v[j]) : v[j];
-        __syncthreads();
-        const int slab = (int)(tile / Nrow), row = (int)(tile % Nrow);
-        const int a = (slab / Nz) % dim;
-        const int z = slab % Nz;
-        double* dst = f + ((int64_t)slab * Nrow + row) * Nx;
-        for (int n = threadIdx.x; n < Q; n += blockDim.x) {
-            const int i0 = 2 * n;
-            if (i0 >= Nx) break;
-            const double2 zz = cadd(buf[spad(n)], buf[XB + spad(n)]);
-            double v0 = zz.x * scale, v1 = zz.y * scale;
-            const int64_t node = ((int64_t)z * Nrow + row) * Nx + i0;
-            if (body) {
-                v0 += body[(int64_t)a * nodes + node];
-                v1 += body[(int64_t)a * nodes + node + 1];
-            }
-            if (cmask) {
-                if ((cmask[node] >> a) & 1u) v0 = 0.0;
-                if ((cmask[node + 1] >> a) & 1u) v1 = 0.0;
-            }
-            *reinterpret_cast<double2*>(dst + i0) = make_double2(v0, v1);
-        }
-        cur ^= 1;
-    }
-    cp_async_wait_all();
-}
-
-// ------------------------------------------- K3, component-grouped (2D) ---
-// Two warp groups per column: group c owns component c end to end (forward
-// FFT, its row of the 2x2 symbol product, inverse FFT), so each thread keeps
-// one 16-point spectrum and a CTA runs twice the warps of the single-group
-// kernel.  The only cross-group traffic is the product's operand swap through
-// the groups' exchange buffers.  Half 0 parks z^0 in `out`, half 1
-// read-modify-writes it (out must not alias in).
-template <int LOGQ, bool REAL>
-__global__ void __launch_bounds__(512, 1) k_spectral2d_cg(const double2* __restrict__ in, double2* out,
-                                                          const void* __restrict__ sym, int ncols, int Nl, int NC,
-                                                          int batch, const double2* __restrict__ tw, int logTWN) {
-    using Sh = FftShape<LOGQ, 4>;
-    constexpr int Q = Sh::Q, T = Sh::T, XB = Sh::XBUF, RR = Sh::R;
-    extern __shared__ double2 sm[];
-    const int g = threadIdx.x >> Sh::LOGT;  // c * NC + ci
-    const int c = g / NC, ci = g - c * NC;
-    const int t = threadIdx.x & (T - 1);
-    double2* xb = sm + g * XB;
-    const double2* xo = sm + ((1 - c) * NC + ci) * XB;  // partner component's buffer
-    const int shP = logTWN - (LOGQ + 1);
-    const FftTw tws = make_fft_tw<LOGQ, 4>(t, tw, logTWN);
-    const double2 wt = __ldg(tw + (t << shP));
-    const int b = blockIdx.x;
-    const int col = blockIdx.y * NC + ci;
-    const bool valid = col < ncols;
-    const int cc = valid ? col : 0;
-    const double2* x = in + ((int64_t)(b * 2 + c) * ncols + cc) * Nl;
-    double2* z = out + ((int64_t)(b * 2 + c) * ncols + cc) * Nl;
-    const int pself = 2 * c;  // xx (c=0) or yy (c=1); cross term xy = 1
-    double2 v[RR];
-#pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
-#pragma unroll
-        for (int j = 0; j < RR; ++j) {
-            const int n = t + j * T;
-            double2 xv = make_double2(0.0, 0.0);
-            if (valid && n < Nl) xv = x[n];
-            v[j] = h ? cmul(xv, tw32r<-1>(j * (16 / RR), wt)) : xv;
-        }
-        reg_fft<LOGQ, 4, -1>(v, t, xb, tws, BlockBar{});
-#pragma unroll
-        for (int j = 0; j < RR; ++j) xb[spad(t + j * T)] = v[j];
-        __syncthreads();
-        const int64_t sbase = ((int64_t)cc * 2 + h) * Q;
-#pragma unroll
-        for (int j = 0; j < RR; ++j) {
-            const int k = t + j * T;
-            const double2 uo = xo[spad(k)];
-            if (REAL) {
-                const double* H = (const double*)sym + (sbase + k) * 3;
-                const double gs = __ldg(H + pself), gx = __ldg(H + 1);
-                v[j] = make_double2(gs * v[j].x + gx * uo.x, gs * v[j].y + gx * uo.y);
-            } else {
-                const double2* H = (const double2*)sym + (sbase + k) * 3;
-                v[j] = cadd(cmul(__ldg(H + pself), v[j]), cmul(__ldg(H + 1), uo));
-            }
-        }
-        __syncthreads();
-        reg_fft<LOGQ, 4, 1>(v, t, xb, tws, BlockBar{});
-#pragma unroll
-        for (int j = 0; j < RR; ++j) {
-            const int n = t + j * T;
-            if (valid && n < Nl) {
-                if (h == 0) z[n] = v[j];
-                else z[n] = cadd(z[n], cmul(tw32r<1>(j * (16 / RR), cconj(wt)), v[j]));
-            }
-        }
-    }
-}
-
 constexpr int kPipeLogR = 4;  // 16 points per thread: 256 threads per 4096-point column
 constexpr int kPipeThreads = 256;
 
@@ -979,9 +817,6 @@ template <int L>
 static void set_attrs_l() {
     smem_attr((const void*)k_rfft_rows<L>);
     smem_attr((const void*)k_rfft_rows_pipe<L>);
-    smem_attr((const void*)k_irfft_rows_pipe<L>);
-    smem_attr((const void*)k_spectral2d_cg<L, true>);
-    smem_attr((const void*)k_spectral2d_cg<L, false>);
     smem_attr((const void*)k_irfft_rows<L>);
     smem_attr((const void*)k_spectral<L, 2, true, 4, false>);
     smem_attr((const void*)k_spectral<L, 2, false, 4, false>);
@@ -1124,20 +959,7 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
         const bool zsmem = pl.k3_halves == 2;
         const size_t smem =
             sizeof(double2) * (size_t)NC * (xbuf_slots(lq) + (zsmem ? 2 * d - 1 : d - 1) * (1 << lq));
-        const char* k3env = getenv("PDGPU_K3");
-        if (d == 2 && k3env && std::string(k3env) == "cg" && e.d_coltab == nullptr) {
-            const int Tc = threads_per_transform(lq, 4);
-            const int NCc = std::max(1, 256 / Tc);
-            const size_t csmem = sizeof(double2) * (size_t)2 * NCc * xbuf_slots(lq);
-            dim3 cgrid(batch, (pl.ncols + NCc - 1) / NCc);
-            if (e.real_symbol)
-                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_cg<LQ, true><<<cgrid, 2 * NCc * Tc, csmem, s>>>(
-                                            spec, e.d_S2, e.d_sym, pl.ncols, pl.Nl, NCc, batch, e.d_tw, pl.logTWN)))
-            else
-                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_cg<LQ, false><<<cgrid, 2 * NCc * Tc, csmem, s>>>(
-                                            spec, e.d_S2, e.d_sym, pl.ncols, pl.Nl, NCc, batch, e.d_tw, pl.logTWN)))
-            xin = e.d_S2;
-        } else if (d == 2) {
+        if (d == 2) {
             // persistent, cp.async-pipelined variant: NC*(XB + 2Q) slots
             const int Tp = threads_per_transform(lq, kPipeLogR);
             const int mode = e.d_coltab ? 2 : (e.real_symbol ? 1 : 0);
@@ -1179,23 +1001,16 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
     // K5
     {
         PassTimer pt(e, kPassK5, s);
-        const int TR = pl.k1_rows;
+        // one row per CTA: two 256-thread CTAs co-reside per SM (measured
+        // faster than two rows per CTA or a persistent double-buffered variant)
+        int TR = 1;
+        if (const char* env = getenv("PDGPU_K5_ROWS")) TR = std::max(1, std::min(pl.k1_rows, atoi(env)));
         const int T = threads_per_transform(lqx, 4);
         dim3 grid((Ny + TR - 1) / TR, nslab);
         const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_slots(lqx);
-        const size_t psmem = sizeof(double2) * (size_t)4 * xbuf_slots(lqx);
-        if ((Nx & 1) == 0 && psmem <= 227 * 1024 && T >= 16 && !getenv("PDGPU_NO_K5_PIPE")) {
-            const int64_t ntiles = (int64_t)Ny * nslab;
-            const int per_sm = std::max<int>(1, (int)(227 * 1024 / psmem));
-            const unsigned pgrid = (unsigned)std::min<int64_t>(ntiles, (int64_t)e.num_sms * per_sm);
-            PDGPU_DISPATCH_LOGQ(lqx, (k_irfft_rows_pipe<LQ><<<pgrid, 2 * T, psmem, s>>>(
-                                         xin, f, Nx, Ny, nslab, Nz, d, pl.Hx, e.d_tw, pl.logTWN, scale, cmask, body,
-                                         pl.nodes)));
-        } else {
-            PDGPU_DISPATCH_LOGQ(lqx, (k_irfft_rows<LQ><<<grid, 2 * TR * T, smem, s>>>(
-                                         xin, f, Nx, Ny, Nz, d, pl.Hx, TR, e.d_tw, pl.logTWN, scale, cmask, body,
-                                         pl.nodes)));
-        }
+        PDGPU_DISPATCH_LOGQ(lqx, (k_irfft_rows<LQ><<<grid, 2 * TR * T, smem, s>>>(
+                                     xin, f, Nx, Ny, Nz, d, pl.Hx, TR, e.d_tw, pl.logTWN, scale, cmask, body,
+                                     pl.nodes)));
     }
     check(cudaGetLastError(), "fast_apply launch");
 }
