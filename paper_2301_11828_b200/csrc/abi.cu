@@ -401,6 +401,7 @@ void pdgpu_destroy(pdgpu_t h) {
                     h->d_scratch};
     for (void* p : ptrs)
         if (p) cudaFree(p);
+    if (h->cg_graph) cudaGraphExecDestroy(h->cg_graph);
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->copy_in) cudaStreamDestroy(h->copy_in);
     if (h->copy_out) cudaStreamDestroy(h->copy_out);
@@ -848,7 +849,47 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
     const double bnorm = sqrt(rr0);
     int k = 0;
     double rel = bnorm > 0 ? 1.0 : 0.0;
-    while (bnorm > 0 && k < maxit) {
+    if (!hist_host && bnorm > 0 && !getenv("PDGPU_CG_HOSTLOOP")) {
+        // One iteration captured as a CUDA graph and replayed in chunks; the
+        // convergence test runs on the device (k_cg_update_dev), so the host
+        // synchronises once per chunk instead of once per iteration.
+        engine_alloc_workspace(e, 1);
+        const bool timing = e.timing;
+        e.timing = false;
+        if (!e.cg_graph || e.cg_graph_x != x || e.cg_graph_stream != s || e.cg_cap != m) {
+            if (e.cg_graph) cudaGraphExecDestroy(e.cg_graph);
+            e.cg_graph = nullptr;
+            cudaGraph_t g;
+            cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+            launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
+            launch_corrections(e, p, q, 1, s, -1.0);
+            launch_dot(e, p, q, m, e.d_scal + 1, s);
+            launch_cg_step_dev(e, x, r, p, q, m, e.d_scal, s);
+            cuda_check(cudaStreamEndCapture(s, &g), "end capture");
+            cuda_check(cudaGraphInstantiate(&e.cg_graph, g, 0), "instantiate");
+            cudaGraphDestroy(g);
+            e.cg_graph_x = x;
+            e.cg_graph_stream = s;
+        }
+        e.timing = timing;
+        const double init[6] = {rr0, 0.0, rr0, tol * tol * rr0, 0.0, 0.0};
+        cuda_check(cudaMemcpyAsync(e.d_scal, init, sizeof(init), cudaMemcpyHostToDevice, s), "scal init");
+        double st[6] = {0, 0, 0, 0, 0, 0};
+        int launched = 0;
+        const int chunk = m > (1 << 22) ? 4 : 16;
+        while (launched < maxit) {
+            const int nl = std::min(chunk, maxit - launched);
+            for (int i = 0; i < nl; ++i) cuda_check(cudaGraphLaunch(e.cg_graph, s), "graph launch");
+            launched += nl;
+            e.launches += (int64_t)nl * 8;
+            cuda_check(cudaMemcpyAsync(st, e.d_scal, sizeof(st), cudaMemcpyDeviceToHost, s), "read scal");
+            cuda_check(cudaStreamSynchronize(s), "cg chunk");
+            if (st[4] != 0.0) break;
+        }
+        k = (int)st[5];
+        rel = sqrt(st[2]) / bnorm;
+    }
+    while (!(!hist_host && bnorm > 0 && !getenv("PDGPU_CG_HOSTLOOP")) && bnorm > 0 && k < maxit) {
         launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
         launch_corrections(e, p, q, 1, s, -1.0);
         launch_dot(e, p, q, m, e.d_scal + 1, s);

@@ -101,6 +101,9 @@ struct Engine {
     bool any_cmask = false;              // constraint mask set directly (set_regions)
     double* d_cg = nullptr;              // CG work vectors r, p, q, u_c
     int64_t cg_cap = 0;
+    cudaGraphExec_t cg_graph = nullptr;  // one captured CG iteration (keyed by x, stream)
+    const double* cg_graph_x = nullptr;
+    cudaStream_t cg_graph_stream = nullptr;
     // reductions scratch
     double* d_red = nullptr;           // partial sums
     double* d_scal = nullptr;          // device scalars
@@ -173,6 +176,8 @@ void launch_dot(Engine& e, const double* a, const double* b, int64_t n, double* 
 void launch_cg_update(Engine& e, double* x, double* r, const double* p, const double* q, int64_t n,
                       const double* scal, double* rr_out, cudaStream_t s);
 void launch_cg_direction(double* p, const double* r, int64_t n, const double* scal, cudaStream_t s);
+void launch_cg_step_dev(Engine& e, double* x, double* r, double* p, const double* q, int64_t n, double* scal,
+                        cudaStream_t s);
 void launch_mask_rhs(double* out, const double* b, const double* Auc, const uint8_t* cmask,
                      int64_t N, int dim, cudaStream_t s);
 void launch_vv_drift(double* u, const double* v, const double* f, const uint8_t* cmask, int64_t N,

@@ -91,6 +91,74 @@ __global__ void k_cg_direction(double* __restrict__ p, const double* __restrict_
 
 __global__ void k_rotate(double* scal) { scal[0] = scal[2]; }
 
+// ---- graph-replayable CG step with the convergence test on the device ----
+// scal = {rr, p.q, rr_new, tol^2 * rr_0, done, iterations}
+template <class CB>
+__device__ void grid_reduce_cb(double v, double* partial, unsigned int* ticket, CB cb) {
+    __shared__ double ws[32];
+    __shared__ bool last;
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) ws[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double s = lane < (blockDim.x >> 5) ? ws[lane] : 0.0;
+        s = warp_sum(s);
+        if (lane == 0) {
+            partial[blockIdx.x] = s;
+            __threadfence();
+            const unsigned int t = atomicAdd(ticket, 1u);
+            last = (t == gridDim.x - 1);
+        }
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        double s = 0.0;
+        for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += ((volatile double*)partial)[i];
+        s = warp_sum(s);
+        if (lane == 0) ws[wid] = s;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double tot = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += ws[w];
+            cb(tot);
+            *ticket = 0u;
+        }
+    }
+}
+
+__global__ void k_cg_update_dev(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                                const double* __restrict__ q, int64_t n, double* scal, double* partial,
+                                unsigned int* ticket) {
+    if (scal[4] != 0.0) return;
+    const double alpha = scal[0] / scal[1];
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        x[i] += alpha * p[i];
+        const double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        s += ri * ri;
+    }
+    grid_reduce_cb(s, partial, ticket, [&](double tot) {
+        scal[2] = tot;
+        scal[5] += 1.0;
+        if (tot <= scal[3]) scal[4] = 1.0;
+    });
+}
+
+__global__ void k_cg_direction_dev(double* __restrict__ p, const double* __restrict__ r, int64_t n,
+                                   const double* scal) {
+    if (scal[4] != 0.0) return;
+    const double beta = scal[2] / scal[0];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = r[i] + beta * p[i];
+}
+
+__global__ void k_rotate_dev(double* scal) {
+    if (scal[4] == 0.0) scal[0] = scal[2];
+}
+
 __global__ void k_mask_rhs(double* out, const double* b, const double* Auc, const uint8_t* cmask, int64_t N,
                            int dim) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -160,6 +228,15 @@ void launch_cg_update(Engine& e, double* x, double* r, const double* p, const do
                       const double* scal, double* rr_out, cudaStream_t s) {
     k_cg_update<<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, q, n, scal, e.d_red, e.d_ticket, rr_out);
     check(cudaGetLastError(), "cg_update");
+}
+
+void launch_cg_step_dev(Engine& e, double* x, double* r, double* p, const double* q, int64_t n, double* scal,
+                        cudaStream_t s) {
+    k_cg_update_dev<<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, q, n, scal, e.d_red, e.d_ticket);
+    k_cg_direction_dev<<<kRedBlocks, kRedThreads, 0, s>>>(p, r, n, scal);
+    k_rotate_dev<<<1, 1, 0, s>>>(scal);
+    e.launches += 3;
+    check(cudaGetLastError(), "cg_step_dev");
 }
 
 void launch_cg_direction(double* p, const double* r, int64_t n, const double* scal, cudaStream_t s) {
