@@ -207,64 +207,119 @@ int64_t break_pairs(Engine& e, const int64_t* pairs, int64_t n) {
 // sign_p = -1 for odd/odd pairs (i*i).  Exact rewrite of the direct DFT of
 // the stencil; the kernel evaluates H per frequency instead of streaming an
 // O(N) table.  Enabled by PDGPU_SYMBOL=separable.
+// 3D: the column axis is z, columns are (kx, ky), and the per-column
+// coefficients fold the x and y phases; pairs odd in z (xz, yz) use sin.
+// Opt-in (PDGPU_SYMBOL=separable): it removes the O(N) symbol stream (half of
+// the 3D spectral pass's HBM bytes at batch 1) but measured slower in 2D and
+// 3D, both fp64-issue bound; it remains a memory-footprint option.
 void build_coltab(Engine& e) {
     if (e.d_coltab) {
         cudaFree(e.d_coltab);
         e.d_coltab = nullptr;
     }
-    if (e.dim != 2 || !e.real_symbol) return;
-    // opt-in: measured slower than the streamed real table on B200 (the
-    // spectral pass is FP64-issue bound, not HBM bound; profiles/README.md)
-    const char* env = getenv("PDGPU_SYMBOL");
-    if (!env || std::string(env) != "separable") return;
-    const int M = e.M, side = 2 * M + 1;
-    auto Kat = [&](int p, int ox, int oy) { return e.stencils[(size_t)(p * e.ss + (oy + M) * side + (ox + M))]; };
-    // parity per pair and axis: +1 even, -1 odd, 0 neither
-    int par[3][2];
-    for (int p = 0; p < 3; ++p)
-        for (int ax = 0; ax < 2; ++ax) {
+    e.coltab_oddmask = 0;
+    if (!e.real_symbol) return;
+    // off by default: measured slower in both 2D and 3D on B200 (the spectral
+    // pass is fp64-issue bound); it saves the O(N) symbol memory (3.2 GB at 256^3)
+    bool want = false;
+    if (const char* env = getenv("PDGPU_SYMBOL")) {
+        if (std::string(env) == "separable") want = true;
+        if (std::string(env) == "table") want = false;
+    }
+    if (!want) return;
+    const int dim = e.dim, M = e.M, side = 2 * M + 1, np = e.np, l = dim - 1;
+    auto Kat = [&](int p, const int* o) {
+        int64_t idx = 0;
+        for (int d = dim - 1; d >= 0; --d) idx = idx * side + (o[d] + M);
+        return e.stencils[(size_t)(p * e.ss + idx)];
+    };
+    // parity per pair and axis: +1 even, -1 odd, 0 neither.  The centre
+    // (-row sum, kernel.hpp:119-125) is a constant term of the symbol and is
+    // excluded: an odd pair's centre is round-off of the row sum.
+    std::vector<int> par((size_t)np * dim, 0);
+    for (int p = 0; p < np; ++p)
+        for (int ax = 0; ax < dim; ++ax) {
             bool even = true, odd = true;
-            for (int oy = -M; oy <= M; ++oy)
-                for (int ox = -M; ox <= M; ++ox) {
-                    // the centre (-row sum, kernel.hpp:119-125) is a constant
-                    // term of the symbol; an odd pair's centre is round-off
-                    if (ox == 0 && oy == 0) continue;
-                    const double a = Kat(p, ox, oy);
-                    const double b = ax == 0 ? Kat(p, -ox, oy) : Kat(p, ox, -oy);
-                    even = even && a == b;
-                    odd = odd && a == -b;
+            for (int64_t si = 0; si < e.ss; ++si) {
+                int o[3] = {0, 0, 0};
+                int64_t rem = si;
+                for (int d = 0; d < dim; ++d) {
+                    o[d] = (int)(rem % side) - M;
+                    rem /= side;
                 }
-            par[p][ax] = even ? 1 : (odd ? -1 : 0);
+                if (o[0] == 0 && o[1] == 0 && o[2] == 0) continue;
+                int r[3] = {o[0], o[1], o[2]};
+                r[ax] = -r[ax];
+                const double a = Kat(p, o), b = Kat(p, r);
+                even = even && a == b;
+                odd = odd && a == -b;
+            }
+            par[(size_t)(p * dim + ax)] = even ? 1 : (odd ? -1 : 0);
         }
-    // the kernel hard-wires xx, yy even and xy odd along y, equal parity in x
-    const bool ok = par[0][1] == 1 && par[2][1] == 1 && par[1][1] == -1 && par[0][0] == 1 && par[2][0] == 1 &&
-                    par[1][0] == -1;
-    if (!ok) return;
+    int oddmask = 0;
+    for (int p = 0; p < np; ++p) {
+        int nodd = 0;
+        for (int ax = 0; ax < dim; ++ax) {
+            if (par[(size_t)(p * dim + ax)] == 0) return;
+            nodd += par[(size_t)(p * dim + ax)] == -1;
+        }
+        if (nodd & 1) return;  // imaginary symbol
+        if (par[(size_t)(p * dim + l)] == -1) oddmask |= 1 << p;
+    }
+    if (dim == 2 && oddmask != 0b010) return;  // the 2D kernel hard-wires xx, yy even and xy odd along y
     const Plan& pl = e.plan;
-    const int ND = 3 * (M + 1);
-    std::vector<double> tab((size_t)pl.ncols * ND, 0.0);
+    const int ND = np * (M + 1);
     const long double pi2 = 2.0L * 3.141592653589793238462643383279502884L;
-    const long double scale = 1.0L / ((long double)pl.P[0] * (long double)pl.P[1]);
-    for (int kx = 0; kx < pl.ncols; ++kx) {
-        for (int p = 0; p < 3; ++p) {
-            const bool oddx = par[p][0] == -1;
-            const long double sign = (oddx ? -1.0L : 1.0L);
+    const long double scale = 1.0L / ((long double)pl.P[0] * (long double)pl.P[1] * (long double)pl.P[2]);
+    // per-axis trig tables cos/sin(2 pi k o / P_d), o = -M..M
+    std::vector<std::vector<double>> cs(2), sn(2);
+    for (int d = 0; d < dim - 1; ++d) {
+        const int P = pl.P[d], n = d == 0 ? pl.Hx : pl.P[1];
+        cs[d].resize((size_t)n * side);
+        sn[d].resize((size_t)n * side);
+        for (int k = 0; k < n; ++k)
+            for (int o = -M; o <= M; ++o) {
+                const long double ang = pi2 * (long double)(((int64_t)k * (o + P)) % P) / P;
+                cs[d][(size_t)k * side + o + M] = (double)cosl(ang);
+                sn[d][(size_t)k * side + o + M] = (double)sinl(ang);
+            }
+    }
+    std::vector<double> tab((size_t)pl.ncols * ND, 0.0);
+    for (int col = 0; col < pl.ncols; ++col) {
+        const int kx = dim == 2 ? col : col / pl.P[1], ky = dim == 2 ? 0 : col % pl.P[1];
+        for (int p = 0; p < np; ++p) {
+            int nodd = 0;
+            for (int ax = 0; ax < dim; ++ax) nodd += par[(size_t)(p * dim + ax)] == -1;
+            const double sign = nodd == 2 ? -1.0 : 1.0;  // i * i
+            const bool oddx = par[(size_t)(p * dim)] == -1, oddy = dim == 3 && par[(size_t)(p * dim + 1)] == -1;
             for (int m = 0; m <= M; ++m) {
-                long double c = 0.0L;
-                for (int ox = -M; ox <= M; ++ox) {
-                    if (ox == 0 && m == 0) continue;  // centre added below
-                    const long double ang = pi2 * (long double)(((int64_t)kx * (ox + pl.P[0])) % pl.P[0]) / pl.P[0];
-                    c += (long double)Kat(p, ox, m) * (oddx ? sinl(ang) : cosl(ang));
-                }
-                c *= sign * scale;
-                const bool evy = par[p][1] == 1;
-                const long double centre = (long double)Kat(p, 0, 0) * scale;
-                tab[(size_t)kx * ND + p * (M + 1) + m] = (double)(m == 0 ? (evy ? c : 0.0L) + centre : 2.0L * c);
+                double c = 0.0;
+                const int oy_lo = dim == 3 ? -M : 0, oy_hi = dim == 3 ? M : 0;
+                for (int oy = oy_lo; oy <= oy_hi; ++oy)
+                    for (int ox = -M; ox <= M; ++ox) {
+                        int o[3] = {ox, dim == 3 ? oy : m, dim == 3 ? m : 0};
+                        if (ox == 0 && oy == 0 && m == 0) continue;  // centre added below
+                        const double kv = Kat(p, o);
+                        if (kv == 0.0) continue;
+                        double fx = oddx ? sn[0][(size_t)kx * side + ox + M] : cs[0][(size_t)kx * side + ox + M];
+                        double fy = 1.0;
+                        if (dim == 3) fy = oddy ? sn[1][(size_t)ky * side + oy + M] : cs[1][(size_t)ky * side + oy + M];
+                        c += kv * fx * fy;
+                    }
+                c *= sign * (double)scale;
+                const bool evl = par[(size_t)(p * dim + l)] == 1;
+                int zero[3] = {0, 0, 0};
+                const double centre = Kat(p, zero) * (double)scale;
+                tab[(size_t)col * ND + p * (M + 1) + m] = m == 0 ? (evl ? c : 0.0) + centre : 2.0 * c;
             }
         }
     }
     cuda_check(cudaMalloc(&e.d_coltab, sizeof(double) * tab.size()), "alloc coltab");
     cuda_check(cudaMemcpy(e.d_coltab, tab.data(), sizeof(double) * tab.size(), cudaMemcpyHostToDevice), "coltab");
+    e.coltab_oddmask = oddmask;
+    // the O(N) table is no longer read
+    if (e.d_sym) cudaFree(e.d_sym);
+    e.d_sym = nullptr;
 }
 
 void matvec_impl(Engine& e, const double* u, double* f, int batch, cudaStream_t s) {
@@ -450,7 +505,8 @@ size_t pdgpu_footprint_bytes(pdgpu_t h) {
     const Plan& pl = h->plan;
     const int64_t N = pl.nodes;
     size_t b = 0;
-    b += (size_t)pl.ncols * pl.Pl * h->np * (h->real_symbol ? 8 : 16);
+    if (h->d_sym) b += (size_t)pl.ncols * pl.Pl * h->np * (h->real_symbol ? 8 : 16);
+    if (h->d_coltab) b += (size_t)pl.ncols * h->np * (h->M + 1) * 8;
     b += (size_t)(16 * (1 << pl.logTWN));
     b += (size_t)h->cap_batch * 16 * (pl.S1_per_vec + ((pl.dim == 3 || pl.k3_halves == 1) ? pl.S2_per_vec : 0));
     b += (size_t)N + (size_t)h->n_surf * (8 + 8 * h->np);

@@ -60,6 +60,7 @@ struct Engine {
     void* d_sym = nullptr;          // symbol: real double or double2, np * ncols * Pl
     double* d_K = nullptr;          // stencils on device (np * ss)
     double* d_coltab = nullptr;     // separable symbol: per column n_pairs x (M+1) coefficients (2D)
+    int coltab_oddmask = 0;         // bit p: pair p odd along the column axis (sin terms)
     double2* d_scratch = nullptr;   // per-CTA component park of the two-CTA/SM spectral kernel
     int64_t scratch_cap = 0;
     int* d_offs = nullptr;          // nof*3

@@ -322,13 +322,15 @@ __device__ __forceinline__ void symbol_product(double2* F, const double2* U, con
     }
 }
 
-template <int LOGQ, int D, bool REAL, int LOGR, bool ZSMEM>
+template <int LOGQ, int D, bool REAL, int LOGR, bool ZSMEM, bool SEP = false>
 __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2* out, const void* __restrict__ sym,
                                                      int ncols, int Nl, int NC, const double2* __restrict__ tw,
-                                                     int logTWN) {
+                                                     int logTWN, const double* __restrict__ coltab = nullptr,
+                                                     int M = 0, int oddmask = 0) {
     using Sh = FftShape<LOGQ, LOGR>;
     constexpr int Q = Sh::Q, T = Sh::T, XB = Sh::XBUF;
     constexpr int RR = Sh::R;
+    constexpr int NP = D * (D + 1) / 2;
     extern __shared__ double2 sm[];
     const int gi = threadIdx.x >> Sh::LOGT;
     const int t = threadIdx.x & (T - 1);
@@ -344,6 +346,11 @@ __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2*
     const int shP = logTWN - (LOGQ + 1);
     double2 v[RR];
     const FftTw tws = make_fft_tw<LOGQ, LOGR>(t, tw, logTWN);
+    // separable symbol: this column's n_pairs x (M+1) coefficients in SMEM
+    const int ND = NP * (M + 1);
+    double* dsm = reinterpret_cast<double*>(sm + NC * XB + (int64_t)NC * (ZSMEM ? 2 * D - 1 : D - 1) * Q) + gi * ND;
+    if (SEP)
+        for (int i = t; i < ND; i += T) dsm[i] = valid ? __ldg(coltab + (int64_t)col * ND + i) : 0.0;
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
 #pragma unroll 1
@@ -364,6 +371,8 @@ __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2*
         }
         // per-frequency d x d product (ky = 2k + h); last component in v
         const int64_t sbase = ((int64_t)(valid ? col : 0) * 2 + h) * Q;
+        // e^{+2 pi i kz/Pl} for kz = 2(t + jT) + h: base(t, h) * e^{2 pi i j/RR}
+        const double2 eh = SEP ? cconj(__ldg(tw + ((2 * t + h) << shP))) : make_double2(1.0, 0.0);
 #pragma unroll
         for (int j = 0; j < RR; ++j) {
             const int k = t + j * T;
@@ -371,7 +380,31 @@ __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2*
 #pragma unroll
             for (int c = 0; c < D - 1; ++c) U[c] = cpark[c * Q + j * T + t];
             U[D - 1] = v[j];
-            symbol_product<D, REAL>(F, U, sym, sbase + k);
+            if (SEP) {
+                const double2 e = tw32r<1>(j * (32 / RR), eh);
+                double g[NP];
+#pragma unroll
+                for (int p = 0; p < NP; ++p) g[p] = dsm[p * (M + 1)];
+                double2 em = e;
+                for (int m = 1; m <= M; ++m) {
+#pragma unroll
+                    for (int p = 0; p < NP; ++p) g[p] += dsm[p * (M + 1) + m] * (((oddmask >> p) & 1) ? em.y : em.x);
+                    em = cmul(em, e);
+                }
+#pragma unroll
+                for (int a = 0; a < D; ++a) {
+                    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int c = 0; c < D; ++c) {
+                        const double gg = g[pair_of<D>(a, c)];
+                        acc.x += gg * U[c].x;
+                        acc.y += gg * U[c].y;
+                    }
+                    F[a] = acc;
+                }
+            } else {
+                symbol_product<D, REAL>(F, U, sym, sbase + k);
+            }
 #pragma unroll
             for (int a = 0; a < D - 1; ++a) cpark[a * Q + j * T + t] = F[a];
             v[j] = F[D - 1];
@@ -818,14 +851,13 @@ static void set_attrs_l() {
     smem_attr((const void*)k_rfft_rows<L>);
     smem_attr((const void*)k_rfft_rows_pipe<L>);
     smem_attr((const void*)k_irfft_rows<L>);
-    smem_attr((const void*)k_spectral<L, 2, true, 4, false>);
-    smem_attr((const void*)k_spectral<L, 2, false, 4, false>);
     smem_attr((const void*)k_spectral2d_pipe<L, 0>);
     smem_attr((const void*)k_spectral2d_pipe<L, 1>);
     smem_attr((const void*)k_spectral2d_pipe<L, 2>);
     if constexpr (L <= 9) {
         smem_attr((const void*)k_spectral<L, 3, true, 3, true>);
         smem_attr((const void*)k_spectral<L, 3, false, 3, true>);
+        smem_attr((const void*)k_spectral<L, 3, true, 3, true, true>);
         smem_attr((const void*)k_cfft_y_fwd<L>);
         smem_attr((const void*)k_cfft_y_inv<L>);
     }
@@ -980,7 +1012,16 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
 #undef PIPE_ARGS
             xin = e.d_S2;
         } else {
-            if (e.real_symbol)
+            if (e.d_coltab) {
+                // per-column coefficient block in SMEM: shrink the column group to fit
+                const size_t per_col = smem / NC + sizeof(double) * 6 * (e.M + 1);
+                int NCs = NC;
+                while (NCs > 1 && per_col * NCs > 225 * 1024) NCs >>= 1;
+                dim3 sgrid(batch, (pl.ncols + NCs - 1) / NCs);
+                PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, true, 3, true, true><<<sgrid, NCs * T, per_col * NCs, s>>>(
+                                             spec, spec, e.d_sym, pl.ncols, pl.Nl, NCs, e.d_tw, pl.logTWN, e.d_coltab,
+                                             e.M, e.coltab_oddmask)))
+            } else if (e.real_symbol)
                 PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, true, 3, true><<<grid, NC * T, smem, s>>>(
                                              spec, spec, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
             else

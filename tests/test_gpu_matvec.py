@@ -71,3 +71,16 @@ def test_batched_apply_matches_single():
     fb = ff.matvec(u)
     for i in range(3):
         assert rel(fb[i], o.matvec(u[i])) <= TOL
+
+
+@pytest.mark.parametrize("dims", [(96, 80), (24, 20, 16)])
+def test_separable_symbol_mode(dims, monkeypatch):
+    """PDGPU_SYMBOL=separable: per-column symbol coefficients instead of the
+    O(N) table -- same K.u to 1e-11."""
+    monkeypatch.setenv("PDGPU_SYMBOL", "separable")
+    h = 1.0 / dims[0]
+    o = Oracle(dims, h=h, delta=3.015 * h, M=3, E=1.0, thickness=1.0)
+    ff = engine_for(o)
+    assert ff.symbol_mode() == "separable"
+    u = random_field(Rng(31), len(dims), o.n)
+    assert rel(ff.matvec(u), o.matvec(u)) <= TOL
