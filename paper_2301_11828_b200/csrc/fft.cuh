@@ -10,8 +10,9 @@
 //
 // Algorithm: Stockham autosort.  A transform of Q = 2^LOGQ points is owned
 // by T = Q/R threads, each holding R points in registers in the "natural"
-// layout  v[j] <-> x[t + j*T].  Passes: one remainder pass of radix
-// 2^(LOGQ mod LOGR) first (no twiddles), then radix-R passes; between passes
+// layout  v[j] <-> x[t + j*T].  Passes: radix-R passes, the first without
+// twiddles, then (when LOGR does not divide LOGQ) one remainder pass of radix
+// 2^(LOGQ mod LOGR) with R/r butterflies per thread; between passes
 // the data is exchanged once through shared memory (padded one slot every
 // 16 so the 16-byte accesses of every quarter-warp hit distinct banks).  The
 // last pass lands in the natural layout again, so a forward transform, a
@@ -230,8 +231,10 @@ struct FftShape {
     static constexpr int XBUF = spad_size(Q);  // exchange slots per transform
 };
 
-// Per-thread twiddle bases: pass P >= 1 multiplies input m of its (single)
-// butterfly by w_P^m, w_P = exp(-2 pi i k / (Ns R)), k = t mod Ns.  Only the
+// Per-thread twiddle bases: pass P >= 1 multiplies input m of butterfly b
+// by w^m, w = exp(-2 pi i k / (Ns r)), k = b mod Ns.  In full-radix passes
+// b = t; in the remainder pass (last, radix r < R) b = t + i*T, i < R/r, all
+// below Ns, and w_i = w_t * exp(-2 pi i i/R) (compile-time factor).  Only the
 // bases are read from the table (once per kernel); the powers are formed in
 // registers (depth <= 4 products, a few ulp), keeping the L1 path free for
 // the data exchanges.
@@ -247,9 +250,10 @@ __device__ __forceinline__ FftTw make_fft_tw(int t, const double2* __restrict__ 
     for (int p = 1; p < 4; ++p) {
         r.w[p - 1] = make_double2(1.0, 0.0);
         if (p < Sh::NPASS) {
-            const int logns = Sh::LOGREM ? Sh::LOGREM + (p - 1) * Sh::LOGR : p * Sh::LOGR;
+            const int logns = p * Sh::LOGR;
+            const int lr = (p == Sh::NPASS - 1 && Sh::LOGREM) ? Sh::LOGREM : Sh::LOGR;
             const int k = t & ((1 << logns) - 1);
-            r.w[p - 1] = __ldg(tw + (k << (logTWN - logns - Sh::LOGR)));
+            r.w[p - 1] = __ldg(tw + (k << (logTWN - logns - lr)));
         }
     }
     return r;
@@ -270,10 +274,11 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[1 << LOGR], double2 base) 
 #pragma unroll
         for (int m = 0; m < r; ++m) w[m] = v[i + m * nb];
         if constexpr (LOGNS > 0) {
-            static_assert(nb == 1, "twiddled passes are full radix");
             // sequential powers: only the base and the running power stay
-            // live (register pressure), error grows to ~r ulp
-            const double2 b1 = S > 0 ? cconj(base) : base;
+            // live (register pressure), error grows to ~r ulp.  Butterfly i
+            // of a remainder pass: base * exp(S 2 pi i i/R).
+            const double2 b0 = S > 0 ? cconj(base) : base;
+            const double2 b1 = tw32r<S>(i * (32 / R), b0);
             double2 p = b1;
 #pragma unroll
             for (int m = 1; m < r; ++m) {
@@ -296,20 +301,46 @@ __device__ __forceinline__ void fft_exchange(double2 (&v)[1 << LOGR], int t, dou
     for (int i = 0; i < nb; ++i) {
         const int b = t + i * T;
         const int base = ((b >> LOGNS) << (LOGNS + LR)) + (b & ((1 << LOGNS) - 1));
+        // padded slot of base + m*Ns with compile-time strides where the
+        // padding is separable (Ns == 1 and r <= 16, or Ns a multiple of 16)
+        if constexpr (LOGNS == 0 && LR <= 4) {
+            double2* p = xb + spad(base);
 #pragma unroll
-        for (int m = 0; m < r; ++m) xb[spad(base + (m << LOGNS))] = v[i + m * nb];
+            for (int m = 0; m < r; ++m) p[m] = v[i + m * nb];
+        } else if constexpr (LOGNS >= 4) {
+            constexpr int NS = 1 << LOGNS;
+            double2* p = xb + spad(base);
+#pragma unroll
+            for (int m = 0; m < r; ++m) p[m * (NS + NS / 16)] = v[i + m * nb];
+        } else {
+#pragma unroll
+            for (int m = 0; m < r; ++m) xb[spad(base + (m << LOGNS))] = v[i + m * nb];
+        }
     }
     bar();
+    if constexpr (T % 16 == 0) {
+        const double2* p = xb + spad(t);
 #pragma unroll
-    for (int j = 0; j < R; ++j) v[j] = xb[spad(t + j * T)];
+        for (int j = 0; j < R; ++j) v[j] = p[j * (T + T / 16)];
+    } else {
+#pragma unroll
+        for (int j = 0; j < R; ++j) v[j] = xb[spad(t + j * T)];
+    }
     bar();
+}
+
+// natural-layout slot of element t + j*T (compile-time stride when T % 16 == 0)
+template <int T>
+__device__ __forceinline__ int nat_slot(int t, int j) {
+    if constexpr (T % 16 == 0) return spad(t) + j * (T + T / 16);
+    else return spad(t + j * T);
 }
 
 template <int LOGQ, int LOGR, int S, int P, int LOGNS, class Bar>
 __device__ __forceinline__ void fft_passes(double2 (&v)[1 << LOGR], int t, double2* xb, const FftTw& tws, Bar bar) {
     using Sh = FftShape<LOGQ, LOGR>;
     if constexpr (P < Sh::NPASS) {
-        constexpr int LR = (P == 0 && Sh::LOGREM) ? Sh::LOGREM : LOGR;
+        constexpr int LR = (P == Sh::NPASS - 1 && Sh::LOGREM) ? Sh::LOGREM : LOGR;
         fft_pass<LOGQ, LOGR, LR, LOGNS, S>(v, P > 0 ? tws.w[P > 0 ? P - 1 : 0] : make_double2(1.0, 0.0));
         if constexpr (P + 1 < Sh::NPASS) {
             fft_exchange<LOGQ, LOGR, LR, LOGNS>(v, t, xb, bar);

@@ -85,8 +85,9 @@ void plan_init(Plan& pl, int dim, const int* dims) {
         const int per_row = 2 * xbuf_slots(pl.logQx) * 16;
         int tr = 1;
         while (tr < 8 && 2 * (tr * 2) * T <= 512 && (tr * 2) * per_row <= kSmemBudget) tr *= 2;
-        pl.k1_rows = std::min(tr, pl.N[1]);
-        if (const char* env = getenv("PDGPU_K1_ROWS")) pl.k1_rows = std::max(1, std::min(pl.k1_rows, atoi(env)));
+        if (const char* env = getenv("PDGPU_K1_ROWS")) tr = std::max(1, std::min(tr, atoi(env)));
+        while (tr > 1 && tr > pl.N[1]) tr /= 2;  // power of two (K1 pipe template)
+        pl.k1_rows = tr;
     }
     // K3: columns per CTA
     {
@@ -176,14 +177,15 @@ __global__ void __launch_bounds__(512) k_rfft_rows(const double* __restrict__ u,
 // C2R: Z[k] = (X[k] + conj X[h-k]) + i e^{+2 pi i k/Px} (X[k] - conj X[h-k]),
 // h = Px/2; z = IFFT_{2Qx}(Z) on its first Qx outputs = E'[n] + e^{+2 pi i n/(2Qx)} O'[n];
 // x[2n] = Re z, x[2n+1] = Im z.
-template <int LOGQ>
+template <int LOGQ, int LOGTR>
 __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ S, double* __restrict__ f, int Nx,
-                                                    int Nrow, int Nz, int dim, int Hx, int TR,
+                                                    int Nrow, int Nz, int dim, int Hx,
                                                     const double2* __restrict__ tw, int logTWN, double scale,
                                                     const uint8_t* __restrict__ cmask,
                                                     const double* __restrict__ body, int64_t nodes) {
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
+    constexpr int TR = 1 << LOGTR;
     extern __shared__ double2 sm[];
     const int gi = threadIdx.x >> Sh::LOGT;
     const int t = threadIdx.x & (T - 1);
@@ -194,31 +196,63 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
     constexpr int halfP = 2 * Q;
     const int shX = logTWN - (LOGQ + 2);
     const double2* src = S + (int64_t)slab * Hx * Nrow + row0;
-    // twiddle e^{+2 pi i k/Px} by recurrence along the thread's k sequence
-    // (k advances by blockDim/nr per iteration); one table read for the base
-    // and one for the step; e^{+2 pi i (h-k)/Px} = -conj(e^{+2 pi i k/Px}).
-    const bool rec = (blockDim.x % nr) == 0;
-    const int kstep = rec ? (int)blockDim.x / nr : 0;
-    double2 Wk = twiddle<1>(tw, (threadIdx.x / nr) << shX);
-    const double2 Wstep = twiddle<1>(tw, (kstep & (halfP * 2 - 1)) << shX);
-    for (int idx = threadIdx.x; idx < nr * (Q + 1); idx += blockDim.x) {
-        const int k = idx / nr, rr = idx - k * nr;
-        const int k2 = halfP - k;
-        const double2 W = rec ? Wk : twiddle<1>(tw, k << shX);
-        Wk = cmul(Wk, Wstep);
-        const double2 Xa = src[(int64_t)k * Nrow + rr];
-        const double2 Xb = src[(int64_t)k2 * Nrow + rr];
-        double2* Z = sm + 2 * rr * XB;
-        {
-            const double2 s = cadd(Xa, cconj(Xb));
-            const double2 t2 = cmul(W, csub(Xa, cconj(Xb)));
-            Z[(k & 1) * XB + spad(k >> 1)] = make_double2(s.x - t2.y, s.y + t2.x);
+    // Z[k] and Z[halfP-k] from X[k], X[halfP-k] for k < Q; thread item u has
+    // j = j0 + 2T*u, k = 2j (j < Q/2) or 2(j - Q/2) + 1, so Z lands in E[j],
+    // E[Q-j] or O[j'], O[Q-1-j'] -- consecutive slots of one buffer per
+    // quarter-warp.  Thread i -> j0 = 8*(i >> (3+LOGTR)) + (i & 7), row
+    // rr = (i >> 3) & (TR-1) (rows adjacent in S fill whole sectors).  The U
+    // item loads are issued together (the gather is latency bound).
+    // e^{+2 pi i k/Px} = e^{2 pi i 2 j0/Px} e^{2 pi i u/R} (x e^{2 pi i/Px} e^{-i pi/2} for odd k).
+    {
+        constexpr int LA = (2 * T >= 8) ? 3 : 0;
+        constexpr int U = R / 2;
+        const int rr = (threadIdx.x >> LA) & (TR - 1);
+        const int j0 = ((threadIdx.x >> (LA + LOGTR)) << LA) + (threadIdx.x & ((1 << LA) - 1));
+        const bool live = rr < nr;
+        const double2 W0 = twiddle<1>(tw, (2 * j0) << shX);
+        const double2 W1 = cmul(W0, twiddle<1>(tw, 1 << shX));
+        double2 Xa[U], Xb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = j0 + 2 * T * u;
+            const int k = j < Q / 2 ? 2 * j : 2 * (j - Q / 2) + 1;
+            Xa[u] = live ? src[(int64_t)k * Nrow + rr] : make_double2(0.0, 0.0);
+            Xb[u] = live ? src[(int64_t)(halfP - k) * Nrow + rr] : make_double2(0.0, 0.0);
         }
-        if (k != 0 && k != Q) {
-            const double2 W2 = make_double2(-W.x, W.y);
-            const double2 s = cadd(Xb, cconj(Xa));
-            const double2 t2 = cmul(W2, csub(Xb, cconj(Xa)));
-            Z[(k2 & 1) * XB + spad(k2 >> 1)] = make_double2(s.x - t2.y, s.y + t2.x);
+        double2* E = sm + 2 * rr * XB;
+        double2* O = E + XB;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int j = j0 + 2 * T * u;
+            const bool even = j < Q / 2;
+            const double2 W = R >= 4 ? (2 * T * u < Q / 2 ? tw32r<1>(u * (32 / R), W0)
+                                                            : tw32r<1>(u * (32 / R) - 8, W1))
+                                     : twiddle<1>(tw, (even ? 2 * j : 2 * (j - Q / 2) + 1) << shX);
+            const double2 a = Xa[u], bb = Xb[u];
+            const double2 s1 = cadd(a, cconj(bb));
+            const double2 t1 = cmul(W, csub(a, cconj(bb)));
+            const double2 W2 = make_double2(-W.x, W.y);  // e^{+2 pi i (halfP-k)/Px}
+            const double2 s2 = cadd(bb, cconj(a));
+            const double2 t2 = cmul(W2, csub(bb, cconj(a)));
+            const double2 Zk = make_double2(s1.x - t1.y, s1.y + t1.x);
+            const double2 Zm = make_double2(s2.x - t2.y, s2.y + t2.x);
+            if (live) {
+                if (even) {
+                    E[spad(j)] = Zk;
+                    if (j != 0) E[spad(Q - j)] = Zm;
+                } else {
+                    const int jo = j - Q / 2;
+                    O[spad(jo)] = Zk;
+                    O[spad(Q - 1 - jo)] = Zm;
+                }
+            }
+        }
+        // Nyquist k = Q (self-paired, W = e^{i pi/2} = i) -> E[Q/2]
+        if (threadIdx.x < nr) {
+            const double2 xq = src[(int64_t)Q * Nrow + threadIdx.x];
+            const double2 s1 = cadd(xq, cconj(xq));
+            const double2 t1 = cmul(make_double2(0.0, 1.0), csub(xq, cconj(xq)));
+            sm[2 * threadIdx.x * XB + (Q & 1) * XB + spad(Q >> 1)] = make_double2(s1.x - t1.y, s1.y + t1.x);
         }
     }
     __syncthreads();
@@ -240,10 +274,12 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
     const int z = slab % Nz;
     double* dst = f + ((int64_t)slab * Nrow + row0) * Nx;
     const bool vec = (Nx & 1) == 0;
-    for (int idx = threadIdx.x; idx < nr * Q; idx += blockDim.x) {
+#pragma unroll 4
+    for (int u = 0; u < R / 2; ++u) {  // nr*Q <= 2*TR*T * R/2 items
+        const int idx = threadIdx.x + u * 2 * TR * T;
         const int rr = idx >> LOGQ, n = idx & (Q - 1);
         const int i0 = 2 * n;
-        if (i0 >= Nx) continue;
+        if (rr >= nr || i0 >= Nx) continue;
         const double2 zz = cadd(sm[2 * rr * XB + spad(n)], sm[(2 * rr + 1) * XB + spad(n)]);
         double v0 = zz.x * scale, v1 = zz.y * scale;
         const int64_t node = ((int64_t)z * Nrow + row0 + rr) * Nx + i0;
@@ -454,12 +490,13 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // tile's TR rows of reals land in a staging buffer via cp.async while the
 // current tile is transformed and written, so HBM latency overlaps compute.
 // Requires even Nx (16-byte row alignment); the plain kernel covers the rest.
-template <int LOGQ>
+template <int LOGQ, int LOGTR>
 __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restrict__ u, double2* __restrict__ S,
-                                                           int Nx, int Nrow, int nslab, int Hx, int TR,
+                                                           int Nx, int Nrow, int nslab, int Hx,
                                                            const double2* __restrict__ tw, int logTWN) {
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
+    constexpr int TR = 1 << LOGTR;
     extern __shared__ double2 sm[];
     double* stage = reinterpret_cast<double*>(sm + 2 * TR * XB);  // TR rows x (4Q reals max)
     const int gi = threadIdx.x >> Sh::LOGT;
@@ -485,6 +522,18 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
         }
         cp_async_commit();
     };
+    // Post-processing items (a, rr): one thread makes X[2a] (from E[a], E[Q-a])
+    // and X[2a+1] (from O[a], O[Q-1-a]), a = a0 + 2T*u, plus X[halfP] for
+    // a0 == 0.  Thread i -> a0 = 8*(i >> (3+LOGTR)) + (i & 7), rr = (i >> 3) &
+    // (TR-1): each quarter-warp reads 8 consecutive slots of one buffer
+    // (distinct banks for the 16-byte loads) and each warp store still fills
+    // whole 32-byte sectors along rr.  W(2a) = e^{-2 pi i 2a/Px} =
+    // W(2a0) e^{-2 pi i u/R}: two table reads per thread, hoisted.
+    constexpr int LA = (2 * T >= 8) ? 3 : 0;  // tiny transforms: rr fastest
+    const int rr = (threadIdx.x >> LA) & (TR - 1);
+    const int a0 = ((threadIdx.x >> (LA + LOGTR)) << LA) + (threadIdx.x & ((1 << LA) - 1));
+    const double2 W0 = __ldg(tw + ((2 * a0) << shX));
+    const double2 W1 = cmul(W0, __ldg(tw + (1 << shX)));  // W(2a0 + 1)
     int64_t tile = blockIdx.x;
     if (tile < ntiles) fetch(tile);
     for (; tile < ntiles; tile += gridDim.x) {
@@ -504,25 +553,38 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
         if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);
         reg_fft<LOGQ, 4, -1>(v, t, xb, tws, BlockBar{});
 #pragma unroll
-        for (int j = 0; j < R; ++j) xb[spad(t + j * T)] = v[j];
+        for (int j = 0; j < R; ++j) xb[nat_slot<T>(t, j)] = v[j];
         __syncthreads();
-        const bool rec = (blockDim.x % nr) == 0;
-        const int kstep = rec ? (int)blockDim.x / nr : 0;
-        double2 Wk = __ldg(tw + ((threadIdx.x / nr) << shX));
-        const double2 Wstep = __ldg(tw + ((kstep & (2 * halfP - 1)) << shX));
-        for (int idx = threadIdx.x; idx < nr * Hx; idx += blockDim.x) {
-            const int kx = idx / nr, rr = idx - kx * nr;
-            const int k = kx & (halfP - 1);
-            const int k2 = (halfP - kx) & (halfP - 1);
-            const double2* Z = sm + 2 * rr * XB;
-            const double2 A = Z[(k & 1) * XB + spad(k >> 1)];
-            const double2 B = cconj(Z[(k2 & 1) * XB + spad(k2 >> 1)]);
-            const double2 Fe = cscale(cadd(A, B), 0.5);
-            const double2 D = csub(A, B);
-            const double2 Fo = make_double2(0.5 * D.y, -0.5 * D.x);
-            const double2 W = rec ? Wk : __ldg(tw + (kx << shX));
-            Wk = cmul(Wk, Wstep);
-            S[((int64_t)slab * Hx + kx) * Nrow + row0 + rr] = cadd(Fe, cmul(W, Fo));
+        // X[kx] = Fe + e^{-2 pi i kx/Px} Fo, Fe/Fo from Z[k], conj Z[halfP-k] (items: see top)
+        const double2* E = sm + 2 * rr * XB;
+        const double2* O = E + XB;
+        double2* dst = S + (int64_t)slab * Hx * Nrow + row0 + rr;
+        const bool live = rr < nr;
+#pragma unroll 4
+        for (int u = 0; u < R / 2; ++u) {
+            const int a = a0 + 2 * T * u;
+            // kx = 2a: A = E[a], B = conj Z[halfP - 2a] = conj E[(Q - a) mod Q]
+            // kx = 2a+1: A = O[a], B = conj Z[halfP - 2a - 1] = conj O[Q - 1 - a]
+            const double2 Ae = E[spad(a)];
+            const double2 Be = cconj(E[spad((Q - a) & (Q - 1))]);
+            const double2 Ao = O[spad(a)];
+            const double2 Bo = cconj(O[spad(Q - 1 - a)]);
+            {
+                const double2 Fe = cscale(cadd(Ae, Be), 0.5);
+                const double2 D = csub(Ae, Be);
+                const double2 Fo = make_double2(0.5 * D.y, -0.5 * D.x);
+                if (live) dst[(int64_t)(2 * a) * Nrow] = cadd(Fe, cmul(tw32r<-1>(u * (32 / R), W0), Fo));
+            }
+            {
+                const double2 Fe = cscale(cadd(Ao, Bo), 0.5);
+                const double2 D = csub(Ao, Bo);
+                const double2 Fo = make_double2(0.5 * D.y, -0.5 * D.x);
+                if (live) dst[(int64_t)(2 * a + 1) * Nrow] = cadd(Fe, cmul(tw32r<-1>(u * (32 / R), W1), Fo));
+            }
+        }
+        if (a0 == 0 && live) {  // Nyquist: X[halfP] = Re Z0 - Im Z0 (k = k2 = 0)
+            const double2 A = E[0];
+            dst[(int64_t)halfP * Nrow] = make_double2(A.x - A.y, 0.0);
         }
         __syncthreads();  // xb reused by the next tile's exchanges
     }
@@ -849,8 +911,14 @@ static void smem_attr(const void* fn) {
 template <int L>
 static void set_attrs_l() {
     smem_attr((const void*)k_rfft_rows<L>);
-    smem_attr((const void*)k_rfft_rows_pipe<L>);
-    smem_attr((const void*)k_irfft_rows<L>);
+    smem_attr((const void*)k_rfft_rows_pipe<L, 0>);
+    smem_attr((const void*)k_rfft_rows_pipe<L, 1>);
+    smem_attr((const void*)k_rfft_rows_pipe<L, 2>);
+    smem_attr((const void*)k_rfft_rows_pipe<L, 3>);
+    smem_attr((const void*)k_irfft_rows<L, 0>);
+    smem_attr((const void*)k_irfft_rows<L, 1>);
+    smem_attr((const void*)k_irfft_rows<L, 2>);
+    smem_attr((const void*)k_irfft_rows<L, 3>);
     smem_attr((const void*)k_spectral2d_pipe<L, 0>);
     smem_attr((const void*)k_spectral2d_pipe<L, 1>);
     smem_attr((const void*)k_spectral2d_pipe<L, 2>);
@@ -959,9 +1027,15 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
         const size_t psmem = smem + sizeof(double) * (size_t)TR * (2 << lqx);
         if ((Nx & 1) == 0 && psmem <= 227 * 1024 && !getenv("PDGPU_NO_K1_PIPE")) {
             const int64_t ntiles = (int64_t)((Ny + TR - 1) / TR) * nslab;
-            const unsigned pgrid = (unsigned)std::min<int64_t>(ntiles, e.num_sms);
-            PDGPU_DISPATCH_LOGQ(lqx, (k_rfft_rows_pipe<LQ><<<pgrid, 2 * TR * T, psmem, s>>>(
-                                         u, e.d_S1, Nx, Ny, nslab, pl.Hx, TR, e.d_tw, pl.logTWN)));
+            // CTAs resident per SM (128 registers/thread under the 512-thread bound)
+            const int per_sm = std::max(1, std::min((int)(228 * 1024 / (psmem + 1024)), 65536 / (2 * TR * T * 128)));
+            const unsigned pgrid = (unsigned)std::min<int64_t>(ntiles, (int64_t)e.num_sms * per_sm);
+            const int ltr = TR == 8 ? 3 : TR == 4 ? 2 : TR == 2 ? 1 : 0;
+#define PDGPU_K1P(LT) k_rfft_rows_pipe<LQ, LT><<<pgrid, 2 * TR * T, psmem, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, \
+                                                                               e.d_tw, pl.logTWN)
+            PDGPU_DISPATCH_LOGQ(lqx, (ltr == 3 ? PDGPU_K1P(3) : ltr == 2 ? PDGPU_K1P(2) : ltr == 1 ? PDGPU_K1P(1)
+                                                                                                   : PDGPU_K1P(0)));
+#undef PDGPU_K1P
         } else {
             PDGPU_DISPATCH_LOGQ(lqx, (k_rfft_rows<LQ><<<grid, 2 * TR * T, smem, s>>>(u, e.d_S1, Nx, Ny, pl.Hx, TR,
                                                                                     e.d_tw, pl.logTWN)));
@@ -1046,12 +1120,16 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
         // faster than two rows per CTA or a persistent double-buffered variant)
         int TR = 1;
         if (const char* env = getenv("PDGPU_K5_ROWS")) TR = std::max(1, std::min(pl.k1_rows, atoi(env)));
+        while (TR & (TR - 1)) TR &= TR - 1;  // power of two (template)
+        const int ltr = TR == 8 ? 3 : TR == 4 ? 2 : TR == 2 ? 1 : 0;
         const int T = threads_per_transform(lqx, 4);
         dim3 grid((Ny + TR - 1) / TR, nslab);
         const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_slots(lqx);
-        PDGPU_DISPATCH_LOGQ(lqx, (k_irfft_rows<LQ><<<grid, 2 * TR * T, smem, s>>>(
-                                     xin, f, Nx, Ny, Nz, d, pl.Hx, TR, e.d_tw, pl.logTWN, scale, cmask, body,
-                                     pl.nodes)));
+#define PDGPU_K5(LT) k_irfft_rows<LQ, LT><<<grid, 2 * TR * T, smem, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx, e.d_tw, \
+                                                                        pl.logTWN, scale, cmask, body, pl.nodes)
+        PDGPU_DISPATCH_LOGQ(lqx, (ltr == 3 ? PDGPU_K5(3) : ltr == 2 ? PDGPU_K5(2) : ltr == 1 ? PDGPU_K5(1)
+                                                                                          : PDGPU_K5(0)));
+#undef PDGPU_K5
     }
     check(cudaGetLastError(), "fast_apply launch");
 }
