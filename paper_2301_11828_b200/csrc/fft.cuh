@@ -42,6 +42,18 @@ __device__ __forceinline__ double2 twiddle(const double2* __restrict__ tw, int i
     return w;
 }
 
+// hide a value from loop-invariant code motion (persistent kernels would
+// otherwise precompute per-j twiddle products once and spill them)
+__device__ __forceinline__ double2 opaque(double2 a) {
+    asm volatile("" : "+d"(a.x), "+d"(a.y));
+    return a;
+}
+
+__device__ __forceinline__ int opaque(int a) {
+    asm volatile("" : "+r"(a));
+    return a;
+}
+
 // padded shared-memory slot
 __device__ __forceinline__ int spad(int i) { return i + (i >> 4); }
 __host__ __device__ constexpr int spad_size(int q) { return q + (q >> 4) + 1; }
@@ -277,7 +289,9 @@ __device__ __forceinline__ void fft_pass(double2 (&v)[1 << LOGR], double2 base) 
             // sequential powers: only the base and the running power stay
             // live (register pressure), error grows to ~r ulp.  Butterfly i
             // of a remainder pass: base * exp(S 2 pi i i/R).
-            const double2 b0 = S > 0 ? cconj(base) : base;
+            // opaque: inside persistent loops the optimiser would otherwise
+            // hoist all the powers out of the loop and spill them
+            const double2 b0 = opaque(S > 0 ? cconj(base) : base);
             const double2 b1 = tw32r<S>(i * (32 / R), b0);
             double2 p = b1;
 #pragma unroll
@@ -329,6 +343,45 @@ __device__ __forceinline__ void fft_exchange(double2 (&v)[1 << LOGR], int t, dou
     bar();
 }
 
+// Split exchange: the same permutation through a buffer of 8-byte slots,
+// real parts first, then imaginary parts (half the shared memory of
+// fft_exchange -- lets two CTAs share an SM -- for twice the barriers).
+// Padding one slot per 16 keeps every half-warp on distinct banks.
+template <int LOGQ, int LOGR, int LR, int LOGNS, class Bar>
+__device__ __forceinline__ void fft_exchange_split(double2 (&v)[1 << LOGR], int t, double* xd, Bar bar) {
+    constexpr int R = 1 << LOGR, r = 1 << LR, nb = R / r;
+    constexpr int T = (1 << LOGQ) / R;
+#pragma unroll
+    for (int part = 0; part < 2; ++part) {
+#pragma unroll
+        for (int i = 0; i < nb; ++i) {
+            const int b = t + i * T;
+            const int base = ((b >> LOGNS) << (LOGNS + LR)) + (b & ((1 << LOGNS) - 1));
+#pragma unroll
+            for (int m = 0; m < r; ++m) {
+                const double2 x = v[i + m * nb];
+                xd[spad(base + (m << LOGNS))] = part ? x.y : x.x;
+            }
+        }
+        bar();
+        if constexpr (T % 16 == 0) {
+            const double* p = xd + spad(t);
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                if (part) v[j].y = p[j * (T + T / 16)];
+                else v[j].x = p[j * (T + T / 16)];
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                if (part) v[j].y = xd[spad(t + j * T)];
+                else v[j].x = xd[spad(t + j * T)];
+            }
+        }
+        bar();
+    }
+}
+
 // natural-layout slot of element t + j*T (compile-time stride when T % 16 == 0)
 template <int T>
 __device__ __forceinline__ int nat_slot(int t, int j) {
@@ -336,15 +389,16 @@ __device__ __forceinline__ int nat_slot(int t, int j) {
     else return spad(t + j * T);
 }
 
-template <int LOGQ, int LOGR, int S, int P, int LOGNS, class Bar>
+template <int LOGQ, int LOGR, int S, int P, int LOGNS, bool SPLIT, class Bar>
 __device__ __forceinline__ void fft_passes(double2 (&v)[1 << LOGR], int t, double2* xb, const FftTw& tws, Bar bar) {
     using Sh = FftShape<LOGQ, LOGR>;
     if constexpr (P < Sh::NPASS) {
         constexpr int LR = (P == Sh::NPASS - 1 && Sh::LOGREM) ? Sh::LOGREM : LOGR;
         fft_pass<LOGQ, LOGR, LR, LOGNS, S>(v, P > 0 ? tws.w[P > 0 ? P - 1 : 0] : make_double2(1.0, 0.0));
         if constexpr (P + 1 < Sh::NPASS) {
-            fft_exchange<LOGQ, LOGR, LR, LOGNS>(v, t, xb, bar);
-            fft_passes<LOGQ, LOGR, S, P + 1, LOGNS + LR>(v, t, xb, tws, bar);
+            if constexpr (SPLIT) fft_exchange_split<LOGQ, LOGR, LR, LOGNS>(v, t, reinterpret_cast<double*>(xb), bar);
+            else fft_exchange<LOGQ, LOGR, LR, LOGNS>(v, t, xb, bar);
+            fft_passes<LOGQ, LOGR, S, P + 1, LOGNS + LR, SPLIT>(v, t, xb, tws, bar);
         }
     }
 }
@@ -353,13 +407,14 @@ __device__ __forceinline__ void fft_passes(double2 (&v)[1 << LOGR], int t, doubl
 // xb: this transform's exchange buffer (FftShape::XBUF slots); tws: the
 // thread's twiddle bases (make_fft_tw, same for forward and inverse); bar():
 // a barrier covering every thread of the transform (all groups of a CTA in
-// lockstep use __syncthreads).
-template <int LOGQ, int LOGRMAX, int S, class Bar>
+// lockstep use __syncthreads).  SPLIT: xb holds XBUF 8-byte slots instead
+// (fft_exchange_split).
+template <int LOGQ, int LOGRMAX, int S, class Bar, bool SPLIT = false>
 __device__ __forceinline__ void reg_fft(double2 (&v)[1 << FftShape<LOGQ, LOGRMAX>::LOGR], int t, double2* xb,
                                         const FftTw& tws, Bar bar) {
     using Sh = FftShape<LOGQ, LOGRMAX>;
     static_assert(Sh::NPASS <= 4, "at most three twiddled passes");
-    fft_passes<LOGQ, Sh::LOGR, S, 0, 0>(v, t, xb, tws, bar);
+    fft_passes<LOGQ, Sh::LOGR, S, 0, 0, SPLIT>(v, t, xb, tws, bar);
 }
 
 struct BlockBar {

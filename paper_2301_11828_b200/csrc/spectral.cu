@@ -756,6 +756,123 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_spectral2d_pipe(const doubl
     cp_async_wait_all();
 }
 
+// Two-CTA-per-SM variant of the 2D spectral pass: the exchange buffer holds
+// 8-byte slots (split real/imaginary exchange) and operands come straight from
+// global memory, so a CTA needs NC*(Q*16 + XBUF*8) bytes (~99 KB at Q = 4096)
+// and 128 registers per thread.  Two co-resident CTAs overlap each other's
+// load / symbol / store phases with FFT work (one CTA per SM leaves them
+// exposed).  Same data flow and numerics as k_spectral2d_pipe.
+template <int LOGQ, int SYM>
+__global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double2* __restrict__ in, double2* out,
+                                                                   const void* __restrict__ sym,
+                                                                   const double* __restrict__ coltab, int M,
+                                                                   int ncols, int Nl, int NC, int batch,
+                                                                   const double2* __restrict__ tw, int logTWN) {
+    using Sh = FftShape<LOGQ, kPipeLogR>;
+    constexpr int Q = Sh::Q, T = Sh::T, XB = Sh::XBUF, RR = Sh::R;
+    extern __shared__ double2 sm[];
+    const int gi = threadIdx.x >> Sh::LOGT;
+    const int t = threadIdx.x & (T - 1);
+    double2* park = sm + gi * Q;  // thread-private slots [j*T + t]
+    double* xd = reinterpret_cast<double*>(sm + NC * Q);
+    double2* xb = reinterpret_cast<double2*>(xd + gi * XB);
+    const int ND = 3 * (M + 1);
+    double* dsm = xd + NC * XB + gi * ND;
+    const int shP = logTWN - (LOGQ + 1);
+    // register budget (128): twiddle bases are re-read from the (L1-resident)
+    // table where they are used, behind opaque indices so they stay there
+    const int ngroups = (ncols + NC - 1) / NC;
+    const int64_t nitems = (int64_t)ngroups * batch;
+    const int64_t cstride = (int64_t)ncols * Nl;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        const int b = (int)(it % batch);
+        const int col = (int)(it / batch) * NC + gi;
+        const bool valid = col < ncols;
+        const int cc = valid ? col : 0;
+        const double2* x0 = in + ((int64_t)(b * 2 + 0) * ncols + cc) * Nl;
+        double2* z0 = out + ((int64_t)(b * 2 + 0) * ncols + cc) * Nl;
+        if (SYM == 2)
+            for (int i = t; i < ND; i += T) dsm[i] = valid ? __ldg(coltab + (int64_t)cc * ND + i) : 0.0;
+        double2 v[RR];
+#pragma unroll 1
+        for (int h = 0; h < 2; ++h) {
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+                const double2* src = x0 + c * cstride;
+#pragma unroll
+                for (int j = 0; j < RR; ++j) {
+                    const int n = t + j * T;
+                    v[j] = (valid && n < Nl) ? src[n] : make_double2(0.0, 0.0);
+                }
+                if (h) {
+                    const double2 w = __ldg(tw + (opaque(t) << shP));  // exp(-2 pi i t/Pl)
+#pragma unroll
+                    for (int j = 0; j < RR; ++j) v[j] = cmul(v[j], tw32r<-1>(j * (16 / RR), w));
+                }
+                reg_fft<LOGQ, kPipeLogR, -1, BlockBar, true>(v, t, xb, make_fft_tw<LOGQ, kPipeLogR>(opaque(t), tw, logTWN),
+                                                             BlockBar{});
+                if (c == 0) {
+#pragma unroll
+                    for (int j = 0; j < RR; ++j) park[j * T + t] = v[j];
+                }
+            }
+            // 2 x 2 product; component 1 stays in registers
+            const int64_t sbase = ((int64_t)cc * 2 + h) * Q;
+            const double2 eh = cconj(__ldg(tw + ((2 * opaque(t) + h) << shP)));  // exp(+2 pi i (2t+h)/Pl)
+#pragma unroll
+            for (int j = 0; j < RR; ++j) {
+                const int k = t + j * T;
+                double2 U[2], F[2];
+                U[0] = park[j * T + t];
+                U[1] = v[j];
+                if (SYM == 2) {
+                    const double2 e = tw32r<1>(j * (32 / RR), eh);  // exp(+2 pi i (2k+h)/Pl)
+                    double gxx = dsm[0], gyy = dsm[2 * (M + 1)], gxy = dsm[M + 1];
+                    double2 em = e;
+                    for (int m = 1; m <= M; ++m) {
+                        gxx += dsm[m] * em.x;
+                        gxy += dsm[(M + 1) + m] * em.y;
+                        gyy += dsm[2 * (M + 1) + m] * em.x;
+                        em = cmul(em, e);
+                    }
+                    F[0] = make_double2(gxx * U[0].x + gxy * U[1].x, gxx * U[0].y + gxy * U[1].y);
+                    F[1] = make_double2(gxy * U[0].x + gyy * U[1].x, gxy * U[0].y + gyy * U[1].y);
+                } else {
+                    symbol_product<2, SYM == 1>(F, U, sym, sbase + k);
+                }
+                park[j * T + t] = F[0];
+                v[j] = F[1];
+            }
+#pragma unroll 1
+            for (int ai = 0; ai < 2; ++ai) {
+                const int a = 1 - ai;
+                if (ai == 1) {
+#pragma unroll
+                    for (int j = 0; j < RR; ++j) v[j] = park[j * T + t];
+                }
+                reg_fft<LOGQ, kPipeLogR, 1, BlockBar, true>(v, t, xb, make_fft_tw<LOGQ, kPipeLogR>(opaque(t), tw, logTWN),
+                                                            BlockBar{});
+                double2* dst = z0 + a * cstride;
+                if (h == 0) {
+#pragma unroll
+                    for (int j = 0; j < RR; ++j) {
+                        const int n = t + j * T;
+                        if (valid && n < Nl) dst[n] = v[j];
+                    }
+                } else {
+                    // y = z^0 + exp(+2 pi i n/Pl) z^1; z^0 was stored by this thread
+                    const double2 w = cconj(__ldg(tw + (opaque(t) << shP)));
+#pragma unroll
+                    for (int j = 0; j < RR; ++j) {
+                        const int n = t + j * T;
+                        if (valid && n < Nl) dst[n] = cadd(dst[n], cmul(tw32r<1>(j * (16 / RR), w), v[j]));
+                    }
+                }
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------- K2 / K4 (3D) ---
 template <int LOGQ>
 __global__ void __launch_bounds__(512) k_cfft_y_fwd(const double2* __restrict__ S1, double2* __restrict__ S2, int Ny,
@@ -922,6 +1039,9 @@ static void set_attrs_l() {
     smem_attr((const void*)k_spectral2d_pipe<L, 0>);
     smem_attr((const void*)k_spectral2d_pipe<L, 1>);
     smem_attr((const void*)k_spectral2d_pipe<L, 2>);
+    smem_attr((const void*)k_spectral2d_duo<L, 0>);
+    smem_attr((const void*)k_spectral2d_duo<L, 1>);
+    smem_attr((const void*)k_spectral2d_duo<L, 2>);
     if constexpr (L <= 9) {
         smem_attr((const void*)k_spectral<L, 3, true, 3, true>);
         smem_attr((const void*)k_spectral<L, 3, false, 3, true>);
@@ -1072,6 +1192,25 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
             const int ND = 3 * (e.M + 1);
             const size_t per_col = sizeof(double2) * (size_t)(xbuf_slots(lq) + 2 * (1 << lq)) +
                                    (mode == 2 ? sizeof(double) * (size_t)ND : 0);
+            // two-CTA/SM split-exchange kernel (default) unless PDGPU_K3=pipe
+            const char* k3env = getenv("PDGPU_K3");
+            if (!(k3env && std::string(k3env) == "pipe") && lq >= 4) {
+                const int NCd = kPipeThreads / Tp;
+                const size_t dsmem = (size_t)NCd * (sizeof(double2) * (1 << lq) + sizeof(double) * xbuf_slots(lq) +
+                                                    (mode == 2 ? sizeof(double) * ND : 0));
+                const int per_sm = std::max(1, std::min(2, (int)(228 * 1024 / (dsmem + 1024))));
+                const int64_t nitems = (int64_t)((pl.ncols + NCd - 1) / NCd) * batch;
+                const unsigned dgrid = (unsigned)std::min<int64_t>(nitems, (int64_t)e.num_sms * per_sm);
+#define DUO_ARGS spec, e.d_S2, e.d_sym, e.d_coltab, e.M, pl.ncols, pl.Nl, NCd, batch, e.d_tw, pl.logTWN
+                if (mode == 2)
+                    PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_duo<LQ, 2><<<dgrid, NCd * Tp, dsmem, s>>>(DUO_ARGS)))
+                else if (mode == 1)
+                    PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_duo<LQ, 1><<<dgrid, NCd * Tp, dsmem, s>>>(DUO_ARGS)))
+                else
+                    PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_duo<LQ, 0><<<dgrid, NCd * Tp, dsmem, s>>>(DUO_ARGS)))
+#undef DUO_ARGS
+                xin = e.d_S2;
+            } else {
             const int NCp = (int)std::max<size_t>(1, std::min<size_t>(kPipeThreads / Tp, 225 * 1024 / per_col));
             const size_t psmem = per_col * NCp;
             const int64_t nitems = (int64_t)((pl.ncols + NCp - 1) / NCp) * batch;
@@ -1085,6 +1224,7 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
                 PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, 0><<<pgrid, NCp * Tp, psmem, s>>>(PIPE_ARGS)))
 #undef PIPE_ARGS
             xin = e.d_S2;
+            }
         } else {
             if (e.d_coltab) {
                 // per-column coefficient block in SMEM: shrink the column group to fit

@@ -6,7 +6,7 @@
 #include "../../paper_2301_11828_b200/csrc/fft.cuh"
 using namespace pdgpu;
 
-template <int LOGQ, int MINB>
+template <int LOGQ, int MINB, bool SPLIT>
 __global__ void __launch_bounds__(FftShape<LOGQ, 4>::T * 1, MINB) bench(const double2* tw, int logTWN, int iters,
                                                                          double2* out) {
     using Sh = FftShape<LOGQ, 4>;
@@ -17,8 +17,8 @@ __global__ void __launch_bounds__(FftShape<LOGQ, 4>::T * 1, MINB) bench(const do
     for (int j = 0; j < Sh::R; ++j) v[j] = make_double2(t * 1e-3 + j, j * 1e-2);
     const FftTw tws = make_fft_tw<LOGQ, 4>(t, tw, logTWN);
     for (int i = 0; i < iters; ++i) {
-        reg_fft<LOGQ, 4, -1>(v, t, sm, tws, BlockBar{});
-        reg_fft<LOGQ, 4, 1>(v, t, sm, tws, BlockBar{});
+        reg_fft<LOGQ, 4, -1, BlockBar, SPLIT>(v, t, sm, tws, BlockBar{});
+        reg_fft<LOGQ, 4, 1, BlockBar, SPLIT>(v, t, sm, tws, BlockBar{});
 #pragma unroll
         for (int j = 0; j < Sh::R; ++j) v[j] = cscale(v[j], 1.0 / (1 << LOGQ));
     }
@@ -28,28 +28,28 @@ __global__ void __launch_bounds__(FftShape<LOGQ, 4>::T * 1, MINB) bench(const do
     out[blockIdx.x * blockDim.x + t] = acc;
 }
 
-template <int LOGQ, int MINB>
+template <int LOGQ, int MINB, bool SPLIT = false>
 void run(const double2* tw, int logTWN, int ctas_per_sm) {
     using Sh = FftShape<LOGQ, 4>;
     const int iters = 200;
     const int grid = 148 * ctas_per_sm;
-    const size_t smem = sizeof(double2) * Sh::XBUF;
-    cudaFuncSetAttribute(bench<LOGQ, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    const size_t smem = (SPLIT ? sizeof(double) : sizeof(double2)) * Sh::XBUF;
+    cudaFuncSetAttribute(bench<LOGQ, MINB, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     double2* out;
     cudaMalloc(&out, sizeof(double2) * grid * Sh::T);
-    bench<LOGQ, MINB><<<grid, Sh::T, smem>>>(tw, logTWN, 2, out);
+    bench<LOGQ, MINB, SPLIT><<<grid, Sh::T, smem>>>(tw, logTWN, 2, out);
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
-    bench<LOGQ, MINB><<<grid, Sh::T, smem>>>(tw, logTWN, iters, out);
+    bench<LOGQ, MINB, SPLIT><<<grid, Sh::T, smem>>>(tw, logTWN, iters, out);
     cudaEventRecord(b);
     cudaEventSynchronize(b);
     float ms;
     cudaEventElapsedTime(&ms, a, b);
     const double ffts = 2.0 * iters * grid;
     const double per_sm_us = ms * 1e3 / (ffts / 148);
-    printf("LOGQ=%d T=%d ctas/SM=%d: %.3f ms, %.3f us per transform per SM (%.0f clk @1.965GHz)  err=%s\n", LOGQ,
+    printf("split=%d LOGQ=%d T=%d ctas/SM=%d: %.3f ms, %.3f us per transform per SM (%.0f clk @1.965GHz)  err=%s\n", (int)SPLIT, LOGQ,
            Sh::T, ctas_per_sm, ms, per_sm_us, per_sm_us * 1965, cudaGetErrorString(cudaGetLastError()));
     cudaFree(out);
 }
@@ -70,5 +70,8 @@ int main() {
     run<11, 1>(tw, logTWN, 2);
     run<11, 2>(tw, logTWN, 4);
     run<8, 1>(tw, logTWN, 8);
+    run<12, 1, true>(tw, logTWN, 1);
+    run<12, 2, true>(tw, logTWN, 2);
+    run<11, 2, true>(tw, logTWN, 4);
     return 0;
 }
