@@ -286,6 +286,60 @@ def extra_configs(device, stream):
 
 
 # -------------------------------------------------------------------- main --
+def run_slab(args):
+    """Strong scaling of one BATCH x N^2 problem over the ranks: row slabs with
+    M ghost rows per interior face, ghost rows exchanged by NCCL send/recv
+    before every mat-vec (paper_2301_11828_b200/slab.py).  Timed like the
+    default arm: barrier + synchronize on both sides, max over ranks."""
+    import torch
+    from paper_2301_11828_b200 import build_kernel
+    from paper_2301_11828_b200 import dist as D
+    from paper_2301_11828_b200.slab import SlabForce
+
+    rank, world, local = D.env()
+    torch.cuda.set_device(local)
+    D.init("nccl", torch.device("cuda", local))
+    n = N_SIDE * N_SIDE
+    h = 1.0 / N_SIDE
+    K = build_kernel(DIM, h, 3.015 * h, M, 1.0, 1.0)
+    sf = SlabForce((N_SIDE, N_SIDE), M, K, rank=rank, world=world, device=torch.device("cuda", local))
+    sf.set_geometry(h, None, 3.015 * h, 1.0)
+    gen = torch.Generator(device="cuda").manual_seed(D.vector_seed(2000, 0) + rank)
+    u = torch.empty((BATCH, DIM, sf.n_owned), dtype=torch.float64, device="cuda")
+    u.uniform_(-1.0, 1.0, generator=gen)
+    f = torch.empty_like(u)
+    for _ in range(args.warmup):
+        sf.matvec(u, f)
+    torch.cuda.synchronize()
+    clk = ClockSampler(local)
+    clk.start()
+    D.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        sf.matvec(u, f)
+    ev1.record()
+    torch.cuda.synchronize()
+    D.barrier()
+    clocks = clk.stop()
+    ms_step = D.max_over_ranks(ev0.elapsed_time(ev1), "cuda") / args.steps
+    halo = 2 * M * N_SIDE * DIM * 8 * BATCH if world > 1 else 0
+    if rank == 0:
+        line = {"metric": METRIC, "value": BATCH * DIM * n / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded uniform[-1,1], torch Philox)",
+                "config": {"workload": f"2D MSBFM K.u, {N_SIDE}x{N_SIDE} nodes, batch {BATCH}, row slabs",
+                           "parallelism": f"{world} row slabs + {M}-row halo (NCCL send/recv)",
+                           "halo_bytes_per_rank_per_step": halo},
+                "clocks": clocks, "gpu_launches": None, "roofline": None, "cpu_baseline": None, "e2e": None}
+        print(json.dumps(line))
+    D.finalize()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -298,11 +352,16 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary configs")
     ap.add_argument("--ref-budget", type=float, default=150.0)
+    ap.add_argument("--shard", default="vectors", choices=["vectors", "slab"],
+                    help="N>1: vectors = every rank its own batch (weak, default); slab = one lattice split "
+                         "into row slabs with M-row halo exchange (strong, SURVEY 8e)")
     args = ap.parse_args()
     globals()["N_SIDE"] = args.n
     globals()["BATCH"] = args.batch
     if args.impl == "reference":
         return run_reference_arm(args)
+    if args.shard == "slab":
+        return run_slab(args)
 
     import torch
     from paper_2301_11828_b200 import FastForce, build_kernel
@@ -374,7 +433,7 @@ def main():
                 traffic = tj.get("dram_bytes_per_launch")
         except Exception:
             pass
-    roofline = {"bound": "hbm", "kernel": "k_spectral2d_pipe (K3: y-FFT + symbol + inverse y-FFT)",
+    roofline = {"bound": "hbm", "kernel": "k_spectral2d_duo (K3: y-FFT + symbol + inverse y-FFT)",
                 "achieved": k3_gbs, "peak": peak, "unit": "GB/s", "frac": (k3_gbs / peak) if k3_gbs else None,
                 "traffic": traffic, "algorithmic_bytes_per_launch": k3_bytes, "mean_launch_ms": k3_avg_s * 1e3,
                 "peak_source": peak_src,

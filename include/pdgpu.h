@@ -79,6 +79,20 @@ int pdgpu_symbol_mode(pdgpu_t h);
  * Regions (grid.hpp:172-209): per-node constraint direction mask (bit d =
  * direction d).  near_surface may be NULL (recomputed from the geometry). */
 int pdgpu_set_regions(pdgpu_t h, const uint8_t* near_surface, const uint8_t* constraint_mask);
+/* Slab (halo) decomposition: this engine's lattice is rows
+ * [row_offset, row_offset + dims[dim-1]) of a lattice with global_rows rows
+ * along the slowest axis (rows j in 2D, planes k in 3D; grid.hpp:30-36).
+ * Rebuilds the near-surface flags and D^e (grid.hpp:181-189,
+ * corrections.hpp:24-42) against the global faces: slab faces interior to
+ * the global lattice are not surfaces.  The caller supplies M ghost rows on
+ * each interior face and keeps only the owned rows of K.u. */
+int pdgpu_set_slab(pdgpu_t h, int global_rows, int row_offset);
+/* Constraint state as the CG driver uses it (timestepping.hpp:306-309,
+ * corrections.hpp:142-160): mask[N] = constrained direction bits per node,
+ * uc[dim*N] = prescribed displacement values (0 where free or velocity-driven).
+ * Either pointer may be NULL.  Used by multi-rank drivers that run CG over
+ * slabs. */
+int pdgpu_constraint_values(pdgpu_t h, uint8_t* mask, double* uc);
 /* SurfaceDiag raw storage (corrections.hpp:20-62): de is n_pairs x N, rows
  * with near_surface set are used.  By default the engine builds it itself
  * from the stencils (build_de, corrections.hpp:65-68). */

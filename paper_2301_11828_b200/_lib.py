@@ -35,6 +35,8 @@ SIGNATURES = {
     "pdgpu_symbol_mode": (C.c_int, [C.c_void_p]),
     "pdgpu_set_regions": (C.c_int, [C.c_void_p, c_uint8_p, c_uint8_p]),
     "pdgpu_set_surface_diag": (C.c_int, [C.c_void_p, c_double_p]),
+    "pdgpu_set_slab": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "pdgpu_constraint_values": (C.c_int, [C.c_void_p, c_uint8_p, c_double_p]),
     "pdgpu_set_ledger": (C.c_int, [C.c_void_p, c_int64_p, c_int64_p]),
     "pdgpu_break_bonds": (C.c_int, [C.c_void_p, c_int64_p, C.c_int64]),
     "pdgpu_ledger_pairs": (C.c_int, [C.c_void_p, c_int64_p, C.c_int64, c_int64_p]),

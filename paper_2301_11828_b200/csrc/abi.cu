@@ -527,7 +527,7 @@ int pdgpu_set_regions(pdgpu_t h, const uint8_t* near_surface, const uint8_t* cma
             h->h_near.assign(near_surface, near_surface + N);
             std::vector<long long> rows;
             std::vector<double> de;
-            assembly::surface_diag(h->dim, h->plan.N, h->M, h->stencils.data(), h->h_near, rows, de);
+            assembly::surface_diag(h->dim, h->plan.N, h->M, h->stencils.data(), h->h_near, rows, de, h->slab);
             upload_surface(*h, rows, de);
         }
         if (cmask) {
@@ -536,6 +536,23 @@ int pdgpu_set_regions(pdgpu_t h, const uint8_t* near_surface, const uint8_t* cma
             for (int64_t p = 0; p < N; ++p) h->any_cmask = h->any_cmask || cmask[p] != 0;
             cuda_check(cudaMemcpy(h->d_cmask, cmask, (size_t)N, cudaMemcpyHostToDevice), "copy cmask");
         }
+    });
+}
+
+int pdgpu_set_slab(pdgpu_t h, int global_rows, int row_offset) {
+    return guarded([&] {
+        if (!h) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null handle");
+        const int n_last = h->plan.N[h->dim - 1];
+        if (global_rows < n_last || row_offset < 0 || row_offset + n_last > global_rows)
+            throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "slab outside the global lattice");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        h->slab.off = row_offset;
+        h->slab.global = global_rows;
+        h->h_near = assembly::near_surface(h->dim, h->plan.N, h->M, h->slab);
+        std::vector<long long> rows;
+        std::vector<double> de;
+        assembly::surface_diag(h->dim, h->plan.N, h->M, h->stencils.data(), h->h_near, rows, de, h->slab);
+        upload_surface(*h, rows, de);
     });
 }
 
@@ -860,6 +877,42 @@ int pdgpu_update_bonds(pdgpu_t h, const double* u, double s0, const double* watc
     });
 }
 
+// prescribed displacement values u_c over all DOFs (displacement constraints,
+// later boxes win -- corrections.hpp:142-160 applied in order); true if any != 0
+static bool prescribed_values(const Engine& e, std::vector<double>& huc) {
+    const int64_t N = e.plan.nodes, m = (int64_t)e.dim * N;
+    huc.assign((size_t)m, 0.0);
+    for (const auto& cs : e.constraints) {
+        if (cs.kind != 0) continue;
+        for (int64_t pn = 0; pn < N; ++pn) {
+            double xx[3];
+            assembly::node_pos(e.dim, e.plan.N, e.h, e.origin, pn, xx);
+            if (!assembly::box_contains(e.dim, cs.lo, cs.hi, xx)) continue;
+            for (int d = 0; d < e.dim; ++d)
+                if ((cs.dir_mask >> d) & 1u) huc[(size_t)(d * N + pn)] = cs.value;
+        }
+    }
+    bool any = false;
+    for (double v : huc) any = any || v != 0.0;
+    return any;
+}
+
+int pdgpu_constraint_values(pdgpu_t h, uint8_t* mask, double* uc) {
+    return guarded([&] {
+        if (!h) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null handle");
+        const int64_t N = h->plan.nodes;
+        if (mask) {
+            if ((int64_t)h->h_cmask.size() == N) std::copy(h->h_cmask.begin(), h->h_cmask.end(), mask);
+            else std::fill(mask, mask + N, (uint8_t)0);
+        }
+        if (uc) {
+            std::vector<double> huc;
+            prescribed_values(*h, huc);
+            std::copy(huc.begin(), huc.end(), uc);
+        }
+    });
+}
+
 // ------------------------------------------------------------------ CG ---
 static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit, int* iters, double* relres,
                     cudaStream_t s, double* hist_host, int nhist) {
@@ -873,23 +926,9 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
     double* q = p + m;
     double* uc = q + m;
     // prescribed displacement values u_c (displacement constraints only)
-    bool any_uc = false;
-    {
-        std::vector<double> huc((size_t)m, 0.0);
-        for (const auto& cs : e.constraints) {
-            if (cs.kind != 0) continue;
-            for (int64_t pn = 0; pn < N; ++pn) {
-                double xx[3];
-                assembly::node_pos(e.dim, e.plan.N, e.h, e.origin, pn, xx);
-                if (!assembly::box_contains(e.dim, cs.lo, cs.hi, xx)) continue;
-                for (int d = 0; d < e.dim; ++d)
-                    if ((cs.dir_mask >> d) & 1u) huc[(size_t)(d * N + pn)] = cs.value;
-            }
-        }
-        for (double v : huc) any_uc = any_uc || v != 0.0;
-        if (any_uc)
-            cuda_check(cudaMemcpyAsync(uc, huc.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s), "copy uc");
-    }
+    std::vector<double> huc;
+    const bool any_uc = prescribed_values(e, huc);
+    if (any_uc) cuda_check(cudaMemcpyAsync(uc, huc.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s), "copy uc");
     if (any_uc) {
         matvec_impl(e, uc, q, 1, s);
         launch_mask_rhs(r, b, q, e.d_cmask, N, e.dim, s);
@@ -972,7 +1011,14 @@ int pdgpu_cg_solve(pdgpu_t h, const double* b, double* x, double tol, int maxit,
     return guarded([&] {
         if (!h || !b || !x) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
         cuda_check(cudaSetDevice(h->device), "set device");
-        cg_impl(*h, b, x, tol, maxit, iters, relres, pick_stream(*h, stream), nullptr, 0);
+        cudaStream_t s = pick_stream(*h, stream);
+        if (s == cudaStreamLegacy || s == cudaStreamPerThread) {
+            // default streams cannot be captured into the CG graph: run on the
+            // engine stream, ordered after the caller's work (cg_impl syncs at exit)
+            cuda_check(cudaStreamSynchronize(s), "sync caller stream");
+            s = h->stream;
+        }
+        cg_impl(*h, b, x, tol, maxit, iters, relres, s, nullptr, 0);
     });
 }
 

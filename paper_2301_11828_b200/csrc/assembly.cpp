@@ -86,7 +86,13 @@ std::vector<double> build_kernel(int dim, double h, double delta, int M, double 
     return K;
 }
 
-std::vector<uint8_t> near_surface(int dim, const int* dims, int M) {
+// global extent / coordinate of axis d under the slab frame
+static inline int frame_lim(int dim, const int* dims, int d, const SlabFrame& s) {
+    return (d == dim - 1 && s.global >= 0) ? s.global : dims[d];
+}
+static inline int frame_off(int dim, int d, const SlabFrame& s) { return d == dim - 1 ? s.off : 0; }
+
+std::vector<uint8_t> near_surface(int dim, const int* dims, int M, SlabFrame slab) {
     const int nz = dim == 3 ? dims[2] : 1;
     const int64_t n = (int64_t)dims[0] * dims[1] * nz;
     std::vector<uint8_t> out((size_t)n, 0);
@@ -96,7 +102,8 @@ std::vector<uint8_t> near_surface(int dim, const int* dims, int M) {
         c[1] = (int)((p / dims[0]) % dims[1]);
         c[2] = (int)(p / ((int64_t)dims[0] * dims[1]));
         for (int d = 0; d < dim; ++d)
-            if (c[d] < M || c[d] >= dims[d] - M) {
+            if (c[d] + frame_off(dim, d, slab) < M ||
+                c[d] + frame_off(dim, d, slab) >= frame_lim(dim, dims, d, slab) - M) {
                 out[(size_t)p] = 1;
                 break;
             }
@@ -105,7 +112,7 @@ std::vector<uint8_t> near_surface(int dim, const int* dims, int M) {
 }
 
 void surface_diag(int dim, const int* dims, int M, const double* K, const std::vector<uint8_t>& near,
-                  std::vector<long long>& rows, std::vector<double>& de) {
+                  std::vector<long long>& rows, std::vector<double>& de, SlabFrame slab) {
     const int np = n_pairs(dim);
     int64_t ss = 1;
     for (int d = 0; d < dim; ++d) ss *= (2 * M + 1);
@@ -125,10 +132,9 @@ void surface_diag(int dim, const int* dims, int M, const double* K, const std::v
         for (size_t k = 0; k < nof; ++k) {
             const int* o = &offs[3 * k];
             bool inside = true;
-            const int lim[3] = {dims[0], dims[1], nz};
             for (int d = 0; d < dim; ++d) {
-                const int q = c[d] + o[d];
-                inside = inside && q >= 0 && q < lim[d];
+                const int q = c[d] + frame_off(dim, d, slab) + o[d];
+                inside = inside && q >= 0 && q < frame_lim(dim, dims, d, slab);
             }
             if (inside) continue;
             const int64_t si = stencil_index(dim, M, o);

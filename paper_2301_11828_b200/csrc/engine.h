@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 
+#include "assembly.h"
+
 namespace pdgpu {
 
 constexpr int kMaxDim = 3;
@@ -75,6 +77,7 @@ struct Engine {
     // regions / corrections
     uint8_t* d_cmask = nullptr;        // N, constraint direction mask per node
     std::vector<uint8_t> h_cmask, h_near;
+    assembly::SlabFrame slab;          // rows of a larger lattice (pdgpu_set_slab)
     int64_t n_surf = 0;
     long long* d_surf_rows = nullptr;  // surface node ids
     double* d_surf_de = nullptr;       // n_surf * np

@@ -482,6 +482,34 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pr
     const int n = pred ? 16 : 0;  // zero-fill outside the window
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(n) : "memory");
 }
+// L2 eviction-priority hints (createpolicy, sm_80+): data re-read within the
+// same CTA a few microseconds later is loaded/stored evict_last, its last use
+// evict_first, so the streaming traffic of the other CTAs does not push it out.
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ld_hint(const double2* a, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double2 ld_hint_rw(const double2* a, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_hint(double2* a, double2 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y), "l"(pol)
+                 : "memory");
+}
+
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
@@ -799,10 +827,12 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
                 const double2* src = x0 + c * cstride;
+                // x is read again for half 1: keep it in L2 until then
+                const uint64_t pol = h ? l2_policy_evict_first() : l2_policy_evict_last();
 #pragma unroll
                 for (int j = 0; j < RR; ++j) {
                     const int n = t + j * T;
-                    v[j] = (valid && n < Nl) ? src[n] : make_double2(0.0, 0.0);
+                    v[j] = (valid && n < Nl) ? ld_hint(src + n, pol) : make_double2(0.0, 0.0);
                 }
                 if (h) {
                     const double2 w = __ldg(tw + (opaque(t) << shP));  // exp(-2 pi i t/Pl)
@@ -854,18 +884,21 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
                                                             BlockBar{});
                 double2* dst = z0 + a * cstride;
                 if (h == 0) {
+                    const uint64_t pol = l2_policy_evict_last();  // z^0: re-read by this thread in half 1
 #pragma unroll
                     for (int j = 0; j < RR; ++j) {
                         const int n = t + j * T;
-                        if (valid && n < Nl) dst[n] = v[j];
+                        if (valid && n < Nl) st_hint(dst + n, v[j], pol);
                     }
                 } else {
+                    const uint64_t pol = l2_policy_evict_first();
                     // y = z^0 + exp(+2 pi i n/Pl) z^1; z^0 was stored by this thread
                     const double2 w = cconj(__ldg(tw + (opaque(t) << shP)));
 #pragma unroll
                     for (int j = 0; j < RR; ++j) {
                         const int n = t + j * T;
-                        if (valid && n < Nl) dst[n] = cadd(dst[n], cmul(tw32r<1>(j * (16 / RR), w), v[j]));
+                        if (valid && n < Nl)
+                            st_hint(dst + n, cadd(ld_hint_rw(dst + n, pol), cmul(tw32r<1>(j * (16 / RR), w), v[j])), pol);
                     }
                 }
             }

@@ -198,6 +198,20 @@ class FastForce:
         _check(self._lib.pdgpu_set_regions(self._h, None if ns is None else ns.ctypes.data_as(_lib.c_uint8_p),
                                            None if cm is None else cm.ctypes.data_as(_lib.c_uint8_p)))
 
+    def set_slab(self, global_rows: int, row_offset: int):
+        """This lattice is rows [row_offset, row_offset + dims[-1]) of one with
+        `global_rows` rows along the slowest axis (halo slab decomposition):
+        near-surface flags and D^e follow the global faces."""
+        _check(self._lib.pdgpu_set_slab(self._h, int(global_rows), int(row_offset)))
+
+    def constraint_values(self):
+        """(mask[N] uint8 constrained-direction bits, uc[dim, N] prescribed
+        displacements) -- what cg_solve masks with and shifts by."""
+        mask = np.zeros(self.n, dtype=np.uint8)
+        uc = np.zeros((self.dim, self.n))
+        _check(self._lib.pdgpu_constraint_values(self._h, mask.ctypes.data_as(_lib.c_uint8_p), _dp(uc)))
+        return mask, uc
+
     def set_surface_diag(self, de: np.ndarray):
         de = _f64(de)
         _check(self._lib.pdgpu_set_surface_diag(self._h, _dp(de)))
@@ -317,9 +331,15 @@ def _ptr(x) -> int:
     raise TypeError("expected a device pointer or a CUDA tensor")
 
 
+_CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy default stream's explicit handle
+
+
 def _stream(s):
+    """None -> the engine's own stream; a torch stream (or raw handle) -> that
+    stream.  Torch's default stream has handle 0, which the C ABI reads as
+    "engine stream", so it is passed as cudaStreamLegacy to stay ordered with
+    the caller's torch work."""
     if s is None:
         return None
-    if hasattr(s, "cuda_stream"):
-        return s.cuda_stream
-    return int(s)
+    h = s.cuda_stream if hasattr(s, "cuda_stream") else int(s)
+    return h if h else _CUDA_STREAM_LEGACY

@@ -1,0 +1,197 @@
+"""Halo (overlap-save) slab decomposition of the MSBFM operator over ranks.
+
+SURVEY.md sec.8e.  The FFT convolution couples every node, but the stencil
+reaches only M rows, so the operator on a block of rows needs the rows
+themselves plus M rows on either side.  Rank r owns rows [r0, r1) of the
+slowest axis (rows j in 2D, planes k in 3D; node p = (k*Ny + j)*Nx + i,
+grid.hpp:30-36) and runs its own zero-padded FFT convolution (one libpdgpu
+engine) over those rows plus M ghost rows on each interior face.  Before every
+mat-vec each rank sends its first / last M owned rows to its neighbours
+(torch.distributed point-to-point: NCCL between GPUs, gloo in the CPU tests):
+2*M*plane*dim*8 bytes per rank per vector -- 393 KB at 4096^2 -- against the
+two full all-to-all transposes of a distributed FFT.
+
+Exactness: for an owned row every in-band neighbour lies in the owned or ghost
+rows, the engine's zero padding only replaces rows outside the global lattice
+(where the reference pads with zeros too, convolution.hpp:183-195), and
+pdgpu_set_slab rebuilds D^e / near-surface flags against the global faces
+(grid.hpp:181-189, corrections.hpp:24-42).  Ghost-row outputs are discarded.
+
+CG over slabs restates the engine's Hestenes-Stiefel loop (abi.cu cg_impl;
+K := -M_f A M_f, rhs = M_f (b + A u_c)) with the two dot products per
+iteration all-reduced.  Fracture / VV across slabs (cross-face bond ledgers)
+is not built: SlabForce covers K.u, corrections on a fixed ledger, and CG.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+
+def slab_rows(n_rows: int, rank: int, world: int):
+    """Owned rows [r0, r1) of `rank` (balanced contiguous split)."""
+    return n_rows * rank // world, n_rows * (rank + 1) // world
+
+
+class SlabForce:
+    """One rank's share of K.u on a row slab with M ghost rows per interior face.
+
+    dims/M/stencils as FastForce.  engine(ext_dims) -> engine object (default:
+    FastForce on `device`); it must offer set_slab, set_geometry,
+    add_constraint, constraint_values and matvec_device(u, f, batch, stream).
+    Fields are torch tensors (batch, dim, R*plane) of the owned rows.
+    """
+
+    def __init__(self, dims, M: int, stencils, rank: int = 0, world: int = 1, device=None, engine=None,
+                 group=None):
+        self.dims = tuple(int(d) for d in dims)
+        self.dim = len(self.dims)
+        self.M = int(M)
+        self.rank, self.world, self.group = int(rank), int(world), group
+        self.plane = int(np.prod(self.dims[:-1]))
+        self.rows = self.dims[-1]
+        self.r0, self.r1 = slab_rows(self.rows, self.rank, self.world)
+        self.R = self.r1 - self.r0
+        if self.world > 1 and self.R < self.M:
+            raise ValueError(f"slab of {self.R} rows is thinner than the horizon M = {self.M}")
+        self.gl = self.M if self.r0 > 0 else 0
+        self.gh = self.M if self.r1 < self.rows else 0
+        self.L = self.R + self.gl + self.gh
+        self.ext_dims = self.dims[:-1] + (self.L,)
+        self.device = torch.device(device) if device is not None else torch.device("cpu")
+        if engine is None:
+            from .engine import FastForce
+
+            if self.device.type != "cuda":
+                raise RuntimeError("SlabForce needs a CUDA device (libpdgpu engine)")
+            engine = lambda ext: FastForce(ext, self.M, stencils, device=self.device.index or 0)  # noqa: E731
+        self.eng = engine(self.ext_dims)
+        self.eng.set_slab(self.rows, self.r0 - self.gl)
+        self._bufs = {}
+
+    # ------------------------------------------------------------ set-up
+    def set_geometry(self, h: float, origin=None, delta: float = 0.0, rho: float = 1.0):
+        """Global geometry; the engine's origin moves to its first (ghost) row
+        so node positions stay global (grid.hpp:53-57)."""
+        org = np.zeros(self.dim) if origin is None else np.array(origin, dtype=np.float64)
+        org[-1] += (self.r0 - self.gl) * h
+        self.eng.set_geometry(h, org, delta, rho)
+
+    def add_constraint(self, lo, hi, dir_mask: int, kind: int = 0, value: float = 0.0):
+        self.eng.add_constraint(lo, hi, dir_mask, kind, value)
+
+    @property
+    def n_owned(self) -> int:
+        return self.R * self.plane
+
+    def owned(self, x):
+        """Owned rows of a global field (..., N) -> (..., R*plane)."""
+        return x[..., self.r0 * self.plane:self.r1 * self.plane]
+
+    # ------------------------------------------------------------ halo
+    def _buf(self, batch: int):
+        if batch not in self._bufs:
+            z = lambda: torch.zeros((batch, self.dim, self.L * self.plane), dtype=torch.float64,  # noqa: E731
+                                    device=self.device)
+            self._bufs[batch] = (z(), z())
+        return self._bufs[batch]
+
+    def exchange(self, ext):
+        """Fill the ghost rows of ext (batch, dim, L*plane) from the neighbours."""
+        if self.world == 1:
+            return
+        b = ext.shape[0]
+        e = ext.view(b, self.dim, self.L, self.plane)
+        M, gl, R = self.M, self.gl, self.R
+        ops, recvs = [], []
+        if self.gl:
+            peer = self.rank - 1
+            ops.append(dist.P2POp(dist.isend, e[:, :, gl:gl + M].contiguous(), peer, self.group))
+            buf = torch.empty((b, self.dim, M, self.plane), dtype=ext.dtype, device=ext.device)
+            ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
+            recvs.append((buf, 0))
+        if self.gh:
+            peer = self.rank + 1
+            ops.append(dist.P2POp(dist.isend, e[:, :, gl + R - M:gl + R].contiguous(), peer, self.group))
+            buf = torch.empty((b, self.dim, M, self.plane), dtype=ext.dtype, device=ext.device)
+            ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
+            recvs.append((buf, gl + R))
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        for buf, row in recvs:
+            e[:, :, row:row + M].copy_(buf)
+
+    def _stream(self):
+        return torch.cuda.current_stream(self.device) if self.device.type == "cuda" else None
+
+    # ------------------------------------------------------------ K.u
+    def matvec(self, u, f=None):
+        """f = A u (FastForce::apply + apply_corrections) on the owned rows;
+        u, f: (batch, dim, R*plane) or (dim, R*plane)."""
+        squeeze = u.dim() == 2
+        u3 = u.unsqueeze(0) if squeeze else u
+        b = u3.shape[0]
+        ext, fext = self._buf(b)
+        own = slice(self.gl * self.plane, (self.gl + self.R) * self.plane)
+        ext[:, :, own].copy_(u3)
+        self.exchange(ext)
+        self.eng.matvec_device(ext, fext, b, stream=self._stream())
+        out = fext[:, :, own]
+        if f is None:
+            f = out.clone()
+        else:
+            (f.unsqueeze(0) if squeeze else f).copy_(out)
+            return f
+        return f[0] if squeeze else f
+
+    # ------------------------------------------------------------ CG
+    def _allsum(self, t):
+        if self.world > 1:
+            dist.all_reduce(t, group=self.group)
+        return t
+
+    def dot(self, a, b):
+        return self._allsum(torch.sum(a * b).reshape(1))
+
+    def constraint_values(self):
+        """(free[dim, R*plane] fp64 0/1 mask, uc[dim, R*plane]) on the owned rows."""
+        mask, uc = self.eng.constraint_values()
+        own = slice(self.gl * self.plane, (self.gl + self.R) * self.plane)
+        mask = np.asarray(mask)[own]
+        free = np.stack([((mask >> a) & 1) == 0 for a in range(self.dim)]).astype(np.float64)
+        uc = np.asarray(uc).reshape(self.dim, -1)[:, own]
+        to = lambda x: torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float64, device=self.device)  # noqa: E731
+        return to(free), to(uc)
+
+    def cg_solve(self, b, tol: float = 1e-10, maxit: int = 10000):
+        """Solve K_ff x_f = b_f over all ranks (K := -A on free DOFs, x = u_c on
+        constrained ones); b, x: (dim, R*plane) owned rows.  Returns
+        (x, iterations, relative residual)."""
+        free, uc = self.constraint_values()
+        any_uc = bool(self._allsum(torch.tensor([float(torch.count_nonzero(uc))], dtype=torch.float64,
+                                                device=self.device)).item() > 0)
+        if any_uc:
+            r = free * (b + self.matvec(uc))
+        else:
+            r = free * b
+        x = torch.zeros_like(r)
+        p = r.clone()
+        rr = self.dot(r, r)
+        bnorm = float(rr.sqrt().item())
+        k, rel = 0, (1.0 if bnorm > 0 else 0.0)
+        while bnorm > 0 and k < maxit:
+            q = -free * self.matvec(p)
+            alpha = rr / self.dot(p, q)
+            x.add_(alpha * p)
+            r.sub_(alpha * q)
+            rr_new = self.dot(r, r)
+            k += 1
+            rel = float(rr_new.sqrt().item()) / bnorm
+            if rel <= tol:
+                break
+            p.mul_(rr_new / rr).add_(r)
+            rr = rr_new
+        if any_uc:
+            x.add_(uc)
+        return x, k, rel

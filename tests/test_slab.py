@@ -1,0 +1,229 @@
+"""Halo slab decomposition (paper_2301_11828_b200/slab.py).
+
+CPU (gloo, world size 2 and 3): SlabForce's ghost-row exchange, slab origin
+and D^e bookkeeping and its all-reduced CG, with a test double for the
+per-rank engine built on the C oracle (the oracle's FFT convolution on the
+extended slab + the global lattice's D^e rows) -- the gathered owned rows must
+equal the oracle's single-lattice K.u and CG solution.
+
+GPU: the libpdgpu engine behind the same class -- several slabs of one
+lattice on one device (ghost rows filled from the global field instead of by
+P2P, since gpurun has one GPU) must reproduce the single-engine K.u.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+N = 32
+M = 3
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _geom(n):
+    h = 1.0 / n
+    return h, 3.015 * h
+
+
+def _clamp(add, n, dim=2):
+    """Config-1 style clamp: the four delta-deep face layers, all directions."""
+    h, delta = _geom(n)
+    big = 10.0
+    for ax in range(dim):
+        lo = [-big] * dim
+        hi = [big] * dim
+        hi[ax] = delta
+        add(lo, hi, (1 << dim) - 1, 0, 0.0)
+        lo = [-big] * dim
+        hi = [big] * dim
+        lo[ax] = 1.0 - delta
+        add(lo, hi, (1 << dim) - 1, 0, 0.0)
+
+
+class OracleSlabEngine:
+    """Test double of the per-rank engine: C-oracle FFT convolution on the
+    extended slab (zero outside it) plus D^e taken from the global lattice."""
+
+    def __init__(self, ext_dims, global_dims, K, de_global):
+        self.ext, self.gdims, self.K, self.de_g = tuple(ext_dims), tuple(global_dims), K, de_global
+        self.dim = len(ext_dims)
+        self.plane = int(np.prod(ext_dims[:-1]))
+        self.n = int(np.prod(ext_dims))
+        self.cons = []
+        self.h, self.origin = 1.0, np.zeros(self.dim)
+        self._o = None
+
+    def _oracle(self):
+        from oracle.oracle import Oracle
+        if self._o is None:
+            self._o = Oracle(self.ext, h=self.h, delta=3.015 * self.h, M=M, origin=self.origin)
+            self._o.set_kernel(self.K)
+            for c in self.cons:
+                self._o.add_constraint(*c)
+        return self._o
+
+    def set_slab(self, rows, off):
+        self.de = self.de_g[:, off * self.plane:off * self.plane + self.n]
+
+    def set_geometry(self, h, origin, delta, rho):
+        self.h, self.origin, self._o = h, np.array(origin, dtype=np.float64), None
+
+    def add_constraint(self, lo, hi, mask, kind=0, value=0.0):
+        self.cons.append((lo, hi, mask, kind, value))
+        self._o = None
+
+    def constraint_values(self):
+        o = self._oracle()
+        _, cm = o.regions()
+        uc = np.zeros((self.dim, self.n))  # only zero-valued displacement constraints here
+        return cm, uc
+
+    def matvec_device(self, u, f, batch, stream=None):
+        from paper_2301_11828_b200.engine import pair_index
+        o = self._oracle()
+        for b in range(batch):
+            ub = u[b].numpy()
+            fb = o.apply(ub)
+            for a in range(self.dim):
+                for c in range(self.dim):
+                    fb[a] += self.de[pair_index(self.dim, a, c)] * ub[c]
+            f[b].copy_(torch.from_numpy(fb))
+
+
+def _global_oracle(n, clamp):
+    from oracle.oracle import Oracle
+    h, delta = _geom(n)
+    o = Oracle((n, n), h=h, delta=delta, M=M)
+    if clamp:
+        _clamp(o.add_constraint, n)
+    return o
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
+                      MASTER_PORT=str(port))
+    from oracle.oracle import Rng, random_field
+    from paper_2301_11828_b200 import dist as D
+    from paper_2301_11828_b200.slab import SlabForce
+    r, w, _ = D.init("gloo")
+    g = _global_oracle(N, clamp=False)
+    K, de = g.kernel(), g.de()
+    h, delta = _geom(N)
+    sf = SlabForce((N, N), M, K, rank=r, world=w,
+                   engine=lambda ext: OracleSlabEngine(ext, (N, N), K, de))
+    sf.set_geometry(h, None, delta, 1.0)
+    u = random_field(Rng(4100), 2, N * N)
+    ub = torch.from_numpy(np.stack([sf.owned(u), sf.owned(-0.5 * u)]))
+    f = sf.matvec(ub)
+    # CG on the clamped problem
+    sfc = SlabForce((N, N), M, K, rank=r, world=w,
+                    engine=lambda ext: OracleSlabEngine(ext, (N, N), K, de))
+    sfc.set_geometry(h, None, delta, 1.0)
+    _clamp(sfc.add_constraint, N)
+    b = random_field(Rng(4101), 2, N * N)
+    x, it, rel = sfc.cg_solve(torch.from_numpy(np.ascontiguousarray(sfc.owned(b))), tol=1e-10, maxit=2000)
+    parts = [None] * w
+    import torch.distributed as dist
+    dist.all_gather_object(parts, (sf.r0, sf.r1, f.numpy(), x.numpy(), it, rel))
+    if r == 0:
+        q.put(parts)
+    D.finalize()
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_halo_gloo(world):
+    from oracle.oracle import Rng, random_field
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = q.get(timeout=500)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = _global_oracle(N, clamp=False)
+    u = random_field(Rng(4100), 2, N * N)
+    f_ref = np.stack([g.matvec(u), g.matvec(-0.5 * u)])
+    f = np.zeros_like(f_ref)
+    x = np.zeros((2, N * N))
+    for r0, r1, fr, xr, it, rel in parts:
+        f[:, :, r0 * N:r1 * N] = fr
+        x[:, r0 * N:r1 * N] = xr
+        assert rel <= 1e-10
+    err = np.linalg.norm(f - f_ref) / np.linalg.norm(f_ref)
+    assert err <= 1e-12, err
+    gc = _global_oracle(N, clamp=True)
+    b = random_field(Rng(4101), 2, N * N)
+    x_ref, it_ref, rel_ref, _ = gc.cg(b, tol=1e-10, maxit=2000)
+    assert abs(parts[0][4] - it_ref) <= 2
+    assert np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref) <= 1e-7
+    # the GPU-free CG answer satisfies the oracle's own static residual
+    assert gc.static_residual(b, x) <= 1e-10 * (1 + 1e-3)
+
+
+def test_slab_rows_partition():
+    from paper_2301_11828_b200.slab import slab_rows
+    for n, w in [(4096, 8), (100, 3), (7, 7)]:
+        spans = [slab_rows(n, r, w) for r in range(w)]
+        assert spans[0][0] == 0 and spans[-1][1] == n
+        assert all(spans[i][1] == spans[i + 1][0] for i in range(w - 1))
+
+
+def _emulated_slabs(dims, K, world, u, dev, constraints=()):
+    """All slabs of one lattice on one GPU; ghost rows copied from the global
+    field (what the P2P exchange delivers)."""
+    from paper_2301_11828_b200.slab import SlabForce
+    plane = int(np.prod(dims[:-1]))
+    h = 1.0 / dims[0]
+    out = torch.zeros_like(u)
+    for r in range(world):
+        sf = SlabForce(dims, M, K, rank=r, world=world, device=dev)
+        sf.set_geometry(h, None, 3.015 * h, 1.0)
+        for c in constraints:
+            sf.add_constraint(*c)
+        lo = (sf.r0 - sf.gl) * plane
+        hi = (sf.r1 + sf.gh) * plane
+
+        def fill(ext, lo=lo, hi=hi):
+            ext.copy_(u[:, :, lo:hi])
+
+        sf.exchange = fill
+        out[:, :, sf.r0 * plane:sf.r1 * plane] = sf.matvec(sf.owned(u).contiguous())
+        sf.eng.close()
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims,world", [((256, 256), 4), ((96, 80), 3), ((24, 20, 32), 4)])
+def test_slab_engine_gpu(dims, world):
+    from oracle.oracle import Rng, random_field
+    from paper_2301_11828_b200.engine import FastForce, build_kernel
+    dev = torch.device("cuda:0")
+    dim = len(dims)
+    n = int(np.prod(dims))
+    h = 1.0 / dims[0]
+    K = build_kernel(dim, h, 3.015 * h, M, 1.0, 1.0 if dim == 2 else 0.0)
+    u = torch.from_numpy(np.stack([random_field(Rng(4200 + i), dim, n) for i in range(2)])).to(dev)
+    full = FastForce(dims, M, K)
+    full.set_geometry(h, None, 3.015 * h, 1.0)
+    f_ref = torch.zeros_like(u)
+    full.matvec_device(u, f_ref, 2, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    f = _emulated_slabs(dims, K, world, u, dev)
+    torch.cuda.synchronize()
+    err = float(torch.linalg.norm(f - f_ref) / torch.linalg.norm(f_ref))
+    assert err <= 1e-12, err
+    full.close()
