@@ -443,6 +443,32 @@ def main():
                 "symbol_mode": ff.symbol_mode(),
                 "note": "path is fp64-pipe bound on B200 (DESIGN.md sec.3); HBM fraction per the contract"}
 
+    # comparison point: the same apply by direct stencil summation
+    direct = None
+    if not args.no_extra:
+        try:
+            fd = torch.empty_like(u)
+            with torch.cuda.stream(stream):
+                ff.apply_direct_device(u, fd, BATCH, stream)
+                ff.apply_device(u, f, BATCH, stream)
+            torch.cuda.synchronize()
+            rel = float(torch.linalg.norm(fd - f) / torch.linalg.norm(f))
+            d0 = torch.cuda.Event(enable_timing=True)
+            d1 = torch.cuda.Event(enable_timing=True)
+            d0.record(stream)
+            for _ in range(args.steps):
+                ff.apply_direct_device(u, fd, BATCH, stream)
+            d1.record(stream)
+            torch.cuda.synchronize()
+            dms = d0.elapsed_time(d1) / args.steps
+            direct = {"what": "FastForce::apply by direct stencil summation (csrc/direct.cu): SURVEY 8f comparison "
+                              "point and on-device cross-check, not the MSBFM metric",
+                      "ms_per_step": dms, "value": BATCH * DIM * n / (dms * 1e-3), "unit": UNIT,
+                      "rel_diff_vs_fft_apply": rel, "bytes_per_dof_model": 16}
+            del fd
+        except Exception as exc:
+            direct = {"error": str(exc)[:200]}
+
     # end to end through the public host API (pinned host buffers)
     e2e = None
     if not args.no_e2e:
@@ -474,6 +500,8 @@ def main():
             extra = extra_configs(local, stream)
         except Exception as exc:
             extra = {"error": str(exc)[:300]}
+    if direct is not None:
+        extra = dict(extra or {}, direct_stencil_4096_b16=direct)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

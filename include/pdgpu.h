@@ -66,6 +66,12 @@ int pdgpu_apply_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes, int
 
 /* FastForce::last_imag_residue()  convolution.hpp:261.  The R2C pipeline
  * produces real fields by construction: always 0. */
+/* FastForce::apply (no corrections) by direct stencil summation on the
+ * device -- the reference's independent oracle tbt_apply_all
+ * (tests/support/oracles.hpp:72-96) -- as a cross-check of pdgpu_apply and
+ * its comparison point.  Same layout and contract as
+ * pdgpu_apply. */
+int pdgpu_apply_direct(pdgpu_t h, const double* u, double* f, int batch, void* stream);
 double pdgpu_last_imag_residue(pdgpu_t h);
 /* FastForce::footprint_bytes()  convolution.hpp:263-266 (device bytes held). */
 size_t pdgpu_footprint_bytes(pdgpu_t h);

@@ -27,6 +27,7 @@ SIGNATURES = {
     "pdgpu_destroy": (None, [C.c_void_p]),
     "pdgpu_set_geometry": (C.c_int, [C.c_void_p, C.c_double, c_double_p, C.c_double, C.c_double]),
     "pdgpu_apply": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
+    "pdgpu_apply_direct": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]),
     "pdgpu_apply_host": (C.c_int, [C.c_void_p, c_double_p, c_double_p, C.c_int64, C.c_int]),
     "pdgpu_last_imag_residue": (C.c_double, [C.c_void_p]),
     "pdgpu_footprint_bytes": (C.c_size_t, [C.c_void_p]),

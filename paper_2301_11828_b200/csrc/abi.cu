@@ -453,7 +453,7 @@ void pdgpu_destroy(pdgpu_t h) {
                     h->d_cmask, h->d_surf_rows, h->d_surf_de, h->d_ledger, h->d_bond_rows, h->d_listed,
                     h->d_counters, h->d_new_pairs, h->d_body, h->d_cdofs, h->d_cval, h->d_ckind, h->d_u, h->d_v,
                     h->d_f, h->d_fprev, h->d_red, h->d_scal, h->d_ticket, h->d_cg, h->d_coltab,
-                    h->d_scratch};
+                    h->d_scratch, h->d_kc};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->cg_graph) cudaGraphExecDestroy(h->cg_graph);
@@ -481,6 +481,14 @@ int pdgpu_apply(pdgpu_t h, const double* u, double* f, int batch, void* stream) 
         if (!h || !u || !f || batch < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad apply arguments");
         cuda_check(cudaSetDevice(h->device), "set device");
         launch_fast_apply(*h, u, f, batch, pick_stream(*h, stream), 1.0, nullptr, nullptr);
+    });
+}
+
+int pdgpu_apply_direct(pdgpu_t h, const double* u, double* f, int batch, void* stream) {
+    return guarded([&] {
+        if (!h || !u || !f || batch < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad apply arguments");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        launch_direct_apply(*h, u, f, batch, pick_stream(*h, stream), 1.0);
     });
 }
 

@@ -60,7 +60,8 @@ struct Engine {
     cudaStream_t copy_in = nullptr, copy_out = nullptr;  // host-API copy pipeline
     double2* d_tw = nullptr;        // exp(-2 pi i k / TWN)
     void* d_sym = nullptr;          // symbol: real double or double2, np * ncols * Pl
-    double* d_K = nullptr;          // stencils on device (np * ss)
+    double* d_K = nullptr;          // stencils on device (np * ss), then koff[nof][np]
+    double* d_kc = nullptr;         // centre coefficients (3D direct stencil)
     double* d_coltab = nullptr;     // separable symbol: per column n_pairs x (M+1) coefficients (2D)
     int coltab_oddmask = 0;         // bit p: pair p odd along the column axis (sin terms)
     double2* d_scratch = nullptr;   // per-CTA component park of the two-CTA/SM spectral kernel
@@ -167,6 +168,9 @@ void build_symbol(Engine& e);
 void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStream_t s,
                        double scale, const uint8_t* cmask, const double* body);
 void set_kernel_attributes();
+
+// direct.cu
+void launch_direct_apply(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale);
 
 // corrections.cu
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s,

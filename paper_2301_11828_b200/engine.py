@@ -163,6 +163,11 @@ class FastForce:
         """Device pointers / torch tensors, layout [batch][dim][N]."""
         _check(self._lib.pdgpu_apply(self._h, _ptr(u), _ptr(f), batch, _stream(stream)))
 
+    def apply_direct_device(self, u, f, batch: int = 1, stream=None):
+        """FastForce::apply by direct stencil summation on the device (cross-check
+        of apply_device; the reference oracle's tbt_apply_all)."""
+        _check(self._lib.pdgpu_apply_direct(self._h, _ptr(u), _ptr(f), batch, _stream(stream)))
+
     def last_imag_residue(self) -> float:
         return self._lib.pdgpu_last_imag_residue(self._h)
 
