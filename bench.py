@@ -282,6 +282,28 @@ def extra_configs(device, stream):
     ms, (it, rel) = timed(lambda: ff.cg_solve_device(b, x, tol=1e-9, maxit=20000, stream=stream))
     out["config4_cg"] = {"grid": [n, n, n], "tol": 1e-9, "iterations": it, "relres": rel, "solve_ms": ms}
     ff.close()
+    # config 5: 2048^2 notch, velocity-driven top/bottom layers, VV with bond breaking (s0 = 1e-3)
+    import numpy as np
+    n = 2048
+    h = 1.0 / n
+    dl = 3.015 * h
+    K = build_kernel(2, h, dl, M, 1.0, 1.0)
+    lam = max(sum(2.0 * np.abs(K[0 if (a, b) == (0, 0) else (1 if a != b else 2)]).sum() for b in range(2))
+              for a in range(2))
+    dt = 0.8 * 2.0 * (1.0 / lam) ** 0.5  # Gershgorin bound of adr_mass, rho = 1
+    ff = FastForce((n, n), M, K, device=device)
+    ff.set_geometry(h, [0.0, 0.0], dl, 1.0)
+    ff.add_constraint((0.0, 1.0 - dl), (1.0, 1.0), 0b10, 1, 1e-4)
+    ff.add_constraint((0.0, 0.0), (1.0, dl), 0b10, 1, -1e-4)
+    bonds = ff.seed_segment((0.0, 0.5), (0.25, 0.5))
+    ff.sim_init(dt)
+    ff.sim_step(10, 1e-3)
+    steps = 200
+    ms, broken = timed(lambda: ff.sim_step(steps, 1e-3))
+    out["config5_vv"] = {"grid": [n, n], "notch_bonds": bonds, "dt": dt, "s0": 1e-3, "steps": steps,
+                         "ms_per_step": ms / steps, "bonds_broken_in_timed_steps": broken,
+                         "note": "velocity BC +-1e-4 (SURVEY 8d reading); stretch test every step"}
+    ff.close()
     return out
 
 

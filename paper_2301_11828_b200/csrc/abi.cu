@@ -81,8 +81,9 @@ void ensure_ledger(Engine& e) {
     dalloc(e.d_listed, (size_t)N, "alloc listed");
     cuda_check(cudaMemset(e.d_ledger, 0, sizeof(uint32_t) * N * e.lw), "zero ledger");
     cuda_check(cudaMemset(e.d_listed, 0, sizeof(int) * N), "zero listed");
-    cuda_check(cudaMemset(e.d_counters, 0, sizeof(unsigned long long) * 2), "zero counters");
+    cuda_check(cudaMemset(e.d_counters, 0, sizeof(unsigned long long) * 4), "zero counters");
     e.n_bond_rows = 0;
+    e.bond_rows_on_device = false;
     e.total_broken = 0;
     e.new_pairs_cap = std::max<int64_t>(1 << 20, N / 4);
     dalloc(e.d_new_pairs, (size_t)(2 * e.new_pairs_cap), "alloc new pairs");
@@ -430,8 +431,8 @@ int pdgpu_create(int dim, const int* dims, int M, const double* stencils, int de
             dalloc(e->d_cmask, (size_t)N, "alloc cmask");
             cuda_check(cudaMemset(e->d_cmask, 0, (size_t)N), "zero cmask");
             e->h_cmask.assign((size_t)N, 0);
-            dalloc(e->d_counters, 2, "alloc counters");
-            cuda_check(cudaMemset(e->d_counters, 0, 16), "zero counters");
+            dalloc(e->d_counters, 4, "alloc counters");
+            cuda_check(cudaMemset(e->d_counters, 0, 32), "zero counters");
             dalloc(e->d_red, 4096, "alloc red");
             dalloc(e->d_scal, 16, "alloc scal");
             dalloc(e->d_ticket, 4, "alloc ticket");
@@ -1075,7 +1076,10 @@ int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64
         const int64_t N = e.plan.nodes;
         const double inv_rho = 1.0 / e.rho;
         int64_t nb = 0;
-        if (s0 >= 0) ensure_ledger(e);
+        if (s0 >= 0) {
+            ensure_ledger(e);
+            cuda_check(cudaMemsetAsync(e.d_counters + 2, 0, sizeof(unsigned long long), e.stream), "reset breaks");
+        }
         for (int i = 0; i < n_steps; ++i) {
             if (!e.force_ready) {
                 evaluate_force_impl(e, e.d_u, e.d_f, e.stream);
@@ -1088,8 +1092,18 @@ int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64
             evaluate_force_impl(e, e.d_u, e.d_f, e.stream);
             launch_vv_kick(e.d_v, e.d_fprev, e.d_f, e.d_cmask, N, e.dim, e.dt, inv_rho, e.stream);
             launch_enforce(e.d_u, e.d_v, e.d_cdofs, e.d_cval, e.d_ckind, e.n_cdofs, e.t, e.stream);
-            if (s0 >= 0) nb += launch_update_bonds(e, e.d_u, s0, watch, e.stream);
+            if (s0 >= 0) launch_update_bonds(e, e.d_u, s0, watch, e.stream, /*sync=*/false);
             ++e.step;
+        }
+        if (s0 >= 0) {
+            // one read-back per call: row count and breaks of all steps
+            unsigned long long cnt[3];
+            cuda_check(cudaMemcpyAsync(cnt, e.d_counters, sizeof(cnt), cudaMemcpyDeviceToHost, e.stream), "counters");
+            cuda_check(cudaStreamSynchronize(e.stream), "sim step");
+            e.n_bond_rows = (int64_t)cnt[0];
+            e.bond_rows_on_device = false;
+            nb = (int64_t)cnt[2];
+            e.total_broken += nb;
         }
         cuda_check(cudaStreamSynchronize(e.stream), "sim step");
         if (broken) *broken = nb;

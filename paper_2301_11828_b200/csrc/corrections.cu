@@ -10,6 +10,7 @@
 //     contraction) so the break decision matches the reference's
 //     bond_stretch bit for bit (fracture.hpp:17-29, 204-231).
 #include <cuda_runtime.h>
+#include <stdlib.h>
 
 #include <stdexcept>
 #include <string>
@@ -53,49 +54,54 @@ __global__ void k_surface(const double* __restrict__ u, double* __restrict__ f, 
 
 template <int D>
 __global__ void k_bonds(const double* __restrict__ u, double* __restrict__ f, const long long* __restrict__ rows,
-                        int64_t nrows, const uint32_t* __restrict__ ledger, int lw, const long long* __restrict__ disp,
+                        int64_t nrows, const unsigned long long* __restrict__ nrows_dev,
+                        const uint32_t* __restrict__ ledger, int lw, const long long* __restrict__ disp,
                         const double* __restrict__ koff, int nof, const uint8_t* __restrict__ cmask, int64_t nodes,
                         int batch, double scale) {
     constexpr int NP = D * (D + 1) / 2;
-    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    // row count from the device when bonds broke since the host last looked
+    // (sim_step does not synchronise per step); grid-stride over warps
+    const int64_t nr = nrows_dev ? (int64_t)*nrows_dev : nrows;
     const int lane = threadIdx.x & 31;
-    if (warp >= nrows * batch) return;
-    const int b = (int)(warp / nrows);
-    const int64_t r = warp - (int64_t)b * nrows;
-    const int64_t p = rows[r];
-    const double* ub = u + (int64_t)b * D * nodes;
-    double up[D];
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; warp < nr * batch; warp += nwarps) {
+        const int b = (int)(warp / nr);
+        const int64_t r = warp - (int64_t)b * nr;
+        const int64_t p = rows[r];
+        const double* ub = u + (int64_t)b * D * nodes;
+        double up[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) up[c] = ub[(int64_t)c * nodes + p];
-    double acc[D];
+        for (int c = 0; c < D; ++c) up[c] = ub[(int64_t)c * nodes + p];
+        double acc[D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) acc[a] = 0.0;
-    for (int w = 0; w < lw; ++w) {
-        const uint32_t word = ledger[p * lw + w];
-        const int k = w * 32 + lane;
-        if (k < nof && ((word >> lane) & 1u)) {
-            const int64_t q = p + disp[k];
-            double du[D];
+        for (int a = 0; a < D; ++a) acc[a] = 0.0;
+        for (int w = 0; w < lw; ++w) {
+            const uint32_t word = ledger[p * lw + w];
+            const int k = w * 32 + lane;
+            if (k < nof && ((word >> lane) & 1u)) {
+                const int64_t q = p + disp[k];
+                double du[D];
 #pragma unroll
-            for (int c = 0; c < D; ++c) du[c] = up[c] - ub[(int64_t)c * nodes + q];
+                for (int c = 0; c < D; ++c) du[c] = up[c] - ub[(int64_t)c * nodes + q];
 #pragma unroll
-            for (int a = 0; a < D; ++a) {
-                double s = 0.0;
+                for (int a = 0; a < D; ++a) {
+                    double sacc = 0.0;
 #pragma unroll
-                for (int c = 0; c < D; ++c) s += koff[k * NP + pair_idx<D>(a, c)] * du[c];
-                acc[a] += s;
+                    for (int c = 0; c < D; ++c) sacc += koff[k * NP + pair_idx<D>(a, c)] * du[c];
+                    acc[a] += sacc;
+                }
             }
         }
-    }
-#pragma unroll
-    for (int a = 0; a < D; ++a)
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], o);
-    if (lane == 0) {
-        const uint8_t cm = cmask[p];
 #pragma unroll
         for (int a = 0; a < D; ++a)
-            if (!((cm >> a) & 1u)) f[((int64_t)b * D + a) * nodes + p] += scale * acc[a];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc[a] += __shfl_xor_sync(0xffffffffu, acc[a], o);
+        if (lane == 0) {
+            const uint8_t cm = cmask[p];
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+                if (!((cm >> a) & 1u)) f[((int64_t)b * D + a) * nodes + p] += scale * acc[a];
+        }
     }
 }
 
@@ -116,19 +122,21 @@ void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaSt
             k_surface<3><<<(unsigned)((tot + th - 1) / th), th, 0, s>>>(u, f, e.d_surf_rows, e.d_surf_de, e.d_cmask,
                                                                        e.n_surf, N, batch, scale);
     }
-    if (e.n_bond_rows > 0) {
+    if (e.n_bond_rows > 0 || e.bond_rows_on_device) {
         PassTimer pt(e, kPassBonds, s);
-        const int64_t warps = e.n_bond_rows * batch;
         const int th = 256;
-        const int64_t blocks = (warps * 32 + th - 1) / th;
+        // host count known: exact grid; otherwise a resident grid reading the count
+        const int64_t blocks = e.bond_rows_on_device ? (int64_t)e.num_sms * 8
+                                                     : (e.n_bond_rows * batch * 32 + th - 1) / th;
+        const unsigned long long* nd = e.bond_rows_on_device ? e.d_counters : nullptr;
         // koff is stored right after the stencils in d_K (see abi.cu)
         const double* koff = e.d_K + e.np * e.ss;
         if (e.dim == 2)
-            k_bonds<2><<<(unsigned)blocks, th, 0, s>>>(u, f, e.d_bond_rows, e.n_bond_rows, e.d_ledger, e.lw, e.d_disp,
-                                                      koff, e.nof, e.d_cmask, N, batch, scale);
+            k_bonds<2><<<(unsigned)blocks, th, 0, s>>>(u, f, e.d_bond_rows, e.n_bond_rows, nd, e.d_ledger, e.lw,
+                                                      e.d_disp, koff, e.nof, e.d_cmask, N, batch, scale);
         else
-            k_bonds<3><<<(unsigned)blocks, th, 0, s>>>(u, f, e.d_bond_rows, e.n_bond_rows, e.d_ledger, e.lw, e.d_disp,
-                                                      koff, e.nof, e.d_cmask, N, batch, scale);
+            k_bonds<3><<<(unsigned)blocks, th, 0, s>>>(u, f, e.d_bond_rows, e.n_bond_rows, nd, e.d_ledger, e.lw,
+                                                      e.d_disp, koff, e.nof, e.d_cmask, N, batch, scale);
     }
     check(cudaGetLastError(), "corrections launch");
 }
@@ -138,9 +146,14 @@ struct BondArgs {
     int dim, Nx, Ny, Nz, nof, lw;
     double h, o0, o1, o2;
     double s0;
+    double s1sq;  // (1 + s0)^2
+    int fast;     // squared-length pre-test enabled (s0 > -1)
     int has_watch;
     double wlo[3], whi[3];
 };
+
+// counters[2] += counters[1] (breaks of this sweep, for a later host read)
+__global__ void k_accumulate(unsigned long long* counters) { counters[2] += counters[1]; }
 
 __device__ __forceinline__ double pos_rn(double origin, int c, double h) {
     return __dadd_rn(origin, __dmul_rn((double)c + 0.5, h));
@@ -190,10 +203,24 @@ __global__ void k_update_bonds(const double* __restrict__ u, uint32_t* ledger, c
             len0 = __dadd_rn(len0, __dmul_rn(r, r));
             len1 = __dadd_rn(len1, __dmul_rn(ev, ev));
         }
-        len0 = __dsqrt_rn(len0);
-        len1 = __dsqrt_rn(len1);
-        const double s = __ddiv_rn(__dsub_rn(len1, len0), len0);
-        if (s >= A.s0) {
+        // Decide on squared lengths when the answer is unambiguous (s >= s0
+        // <=> |xi+eta|^2 >= (1+s0)^2 |xi|^2); the margin (1e-12 relative) is
+        // far above the few-ulp error of either side, so only bonds within
+        // it take the reference's exact sqrt/div sequence below and every
+        // decision stays the reference's (fracture.hpp:17-29, 224).
+        bool brk;
+        const double thr = A.s1sq * len0;
+        if (A.fast && len1 < thr * (1.0 - 1e-12)) {
+            brk = false;
+        } else if (A.fast && len1 > thr * (1.0 + 1e-12)) {
+            brk = true;
+        } else {
+            len0 = __dsqrt_rn(len0);
+            len1 = __dsqrt_rn(len1);
+            const double s = __ddiv_rn(__dsub_rn(len1, len0), len0);
+            brk = s >= A.s0;
+        }
+        if (brk) {
             atomicOr(&ledger[p * A.lw + (k >> 5)], 1u << (k & 31));
             const int kn = negk[k];
             atomicOr(&ledger[q * A.lw + (kn >> 5)], 1u << (kn & 31));
@@ -208,9 +235,94 @@ __global__ void k_update_bonds(const double* __restrict__ u, uint32_t* ledger, c
     }
 }
 
-// Returns the number of newly broken bonds; new pairs are left in
-// e.d_new_pairs as (p, offset index) and bond rows are appended.
-int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double* watch, cudaStream_t s) {
+// 2D tiled variant of k_update_bonds (no watch box): 32 x 8 nodes per CTA,
+// u of the tile plus its forward halo (x +-M, y +M) in SMEM, compile-time
+// forward offsets (q > p: oy > 0, or oy == 0 and ox > 0), one ledger word per
+// node.  Same arithmetic and decision rule as k_update_bonds.
+constexpr int band_index2d(int M, int ox, int oy) {
+    int idx = 0;
+    for (int a = -M; a <= M; ++a)
+        for (int b = -M; b <= M; ++b) {
+            if (a == ox && b == oy) return idx;
+            if (a * a + b * b > 0 && a * a + b * b <= M * M) ++idx;
+        }
+    return -1;
+}
+
+template <int M>
+__global__ void __launch_bounds__(256) k_update_bonds_tile2d(const double* __restrict__ u, uint32_t* ledger, BondArgs A,
+                                                             int64_t nodes, long long* new_pairs, int64_t cap,
+                                                             unsigned long long* counters, long long* bond_rows,
+                                                             int* listed) {
+    constexpr int TX = 32, TY = 8, W = TX + 2 * M, H = TY + M;
+    __shared__ double su[2][H][W + 1];
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    for (int i = threadIdx.x; i < H * W; i += 256) {
+        const int yy = i / W, xx = i - yy * W;
+        const int gx = x0 + xx - M, gy = y0 + yy;
+        const bool in = gx >= 0 && gx < A.Nx && gy < A.Ny;
+        const int64_t q = (int64_t)gy * A.Nx + gx;
+        su[0][yy][xx] = in ? u[q] : 0.0;
+        su[1][yy][xx] = in ? u[nodes + q] : 0.0;
+    }
+    __syncthreads();
+    const int tx = threadIdx.x & (TX - 1), ty = threadIdx.x / TX;
+    const int cx = x0 + tx, cy = y0 + ty;
+    if (cx >= A.Nx || cy >= A.Ny) return;
+    const int64_t p = (int64_t)cy * A.Nx + cx;
+    const double xp0 = pos_rn(A.o0, cx, A.h), xp1 = pos_rn(A.o1, cy, A.h);
+    const double up0 = su[0][ty][tx + M], up1 = su[1][ty][tx + M];
+    const uint32_t word = ledger[p];  // lw == 1 (<= 32 in-band offsets)
+    uint32_t newbits = 0;
+#pragma unroll
+    for (int oy = 0; oy <= M; ++oy) {
+#pragma unroll
+        for (int ox = -M; ox <= M; ++ox) {
+            if (ox * ox + oy * oy > M * M || (oy == 0 && ox <= 0)) continue;
+            const int k = band_index2d(M, ox, oy);
+            const int qx = cx + ox, qy = cy + oy;
+            if (qx < 0 || qx >= A.Nx || qy >= A.Ny) continue;
+            if ((word >> k) & 1u) continue;
+            const double r0 = __dsub_rn(pos_rn(A.o0, qx, A.h), xp0);
+            const double r1 = __dsub_rn(pos_rn(A.o1, qy, A.h), xp1);
+            const double e0 = __dsub_rn(__dadd_rn(r0, su[0][ty + oy][tx + M + ox]), up0);
+            const double e1 = __dsub_rn(__dadd_rn(r1, su[1][ty + oy][tx + M + ox]), up1);
+            double len0 = __dadd_rn(__dadd_rn(0.0, __dmul_rn(r0, r0)), __dmul_rn(r1, r1));
+            double len1 = __dadd_rn(__dadd_rn(0.0, __dmul_rn(e0, e0)), __dmul_rn(e1, e1));
+            bool brk;
+            const double thr = A.s1sq * len0;
+            if (A.fast && len1 < thr * (1.0 - 1e-12)) {
+                brk = false;
+            } else if (A.fast && len1 > thr * (1.0 + 1e-12)) {
+                brk = true;
+            } else {
+                len0 = __dsqrt_rn(len0);
+                len1 = __dsqrt_rn(len1);
+                brk = __ddiv_rn(__dsub_rn(len1, len0), len0) >= A.s0;
+            }
+            if (!brk) continue;
+            newbits |= 1u << k;
+            const int64_t q = p + (int64_t)oy * A.Nx + ox;
+            atomicOr(&ledger[q], 1u << band_index2d(M, -ox, -oy));
+            const unsigned long long slot = atomicAdd(&counters[1], 1ull);
+            if ((int64_t)slot < cap) {
+                new_pairs[2 * slot] = p;
+                new_pairs[2 * slot + 1] = k;
+            }
+            if (atomicExch(&listed[q], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = q;
+        }
+    }
+    if (newbits) {
+        atomicOr(&ledger[p], newbits);
+        if (atomicExch(&listed[p], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = p;
+    }
+}
+
+// Returns the number of newly broken bonds (sync = true); new pairs are left
+// in e.d_new_pairs as (p, offset index) and bond rows are appended.  With
+// sync = false nothing is read back: the row count stays on the device
+// (k_bonds reads it) and counters[2] accumulates the breaks for the caller.
+int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double* watch, cudaStream_t s, bool sync) {
     const Plan& pl = e.plan;
     BondArgs A;
     A.dim = e.dim;
@@ -224,6 +336,8 @@ int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double*
     A.o1 = e.origin[1];
     A.o2 = e.origin[2];
     A.s0 = s0;
+    A.s1sq = (1.0 + s0) * (1.0 + s0);
+    A.fast = s0 > -1.0 + 1e-6 && !getenv("PDGPU_EXACT_STRETCH");
     A.has_watch = watch != nullptr;
     for (int d = 0; d < 3; ++d) {
         A.wlo[d] = watch && d < e.dim ? watch[d] : 0.0;
@@ -235,14 +349,31 @@ int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double*
     const int64_t N = pl.nodes;
     const int* negk = (const int*)(e.d_offs + 3 * e.nof);
     e.launches += 1;
-    k_update_bonds<<<(unsigned)((N + th - 1) / th), th, 0, s>>>(u, e.d_ledger, e.d_offs, e.d_disp, negk, A, N,
-                                                               e.d_new_pairs, e.new_pairs_cap, e.d_counters,
-                                                               e.d_bond_rows, e.d_listed);
+    if (e.dim == 2 && e.lw == 1 && !watch && e.M >= 1 && e.M <= 3 && !getenv("PDGPU_BONDS_GENERIC")) {
+        dim3 grid((pl.N[0] + 31) / 32, (pl.N[1] + 7) / 8);
+#define PDGPU_UB(MM)                                                                                      \
+    k_update_bonds_tile2d<MM><<<grid, 256, 0, s>>>(u, e.d_ledger, A, N, e.d_new_pairs, e.new_pairs_cap, \
+                                                  e.d_counters, e.d_bond_rows, e.d_listed)
+        if (e.M == 1) PDGPU_UB(1);
+        else if (e.M == 2) PDGPU_UB(2);
+        else PDGPU_UB(3);
+#undef PDGPU_UB
+    } else {
+        k_update_bonds<<<(unsigned)((N + th - 1) / th), th, 0, s>>>(u, e.d_ledger, e.d_offs, e.d_disp, negk, A, N,
+                                                                   e.d_new_pairs, e.new_pairs_cap, e.d_counters,
+                                                                   e.d_bond_rows, e.d_listed);
+    }
     check(cudaGetLastError(), "update_bonds launch");
+    if (!sync) {
+        e.bond_rows_on_device = true;
+        k_accumulate<<<1, 1, 0, s>>>(e.d_counters);
+        return 0;
+    }
     unsigned long long cnt[2];
     check(cudaMemcpyAsync(cnt, e.d_counters, sizeof(cnt), cudaMemcpyDeviceToHost, s), "read counters");
     check(cudaStreamSynchronize(s), "update_bonds");
     e.n_bond_rows = (int64_t)cnt[0];
+    e.bond_rows_on_device = false;
     e.total_broken += (int64_t)cnt[1];
     return (int64_t)cnt[1];
 }

@@ -85,8 +85,9 @@ struct Engine {
     uint32_t* d_ledger = nullptr;      // N * lw bit set over offsets
     long long* d_bond_rows = nullptr;  // rows with >=1 broken bond (unordered)
     int* d_listed = nullptr;           // N flags: row already in d_bond_rows
-    unsigned long long* d_counters = nullptr;  // [0] = #bond rows, [1] = #new pairs
+    unsigned long long* d_counters = nullptr;  // [0] = #bond rows, [1] = #new pairs, [2] = breaks since read
     int64_t n_bond_rows = 0;           // host mirror
+    bool bond_rows_on_device = false;  // [0] may be ahead of n_bond_rows (unsynchronised sim_step)
     int64_t total_broken = 0;
     long long* d_new_pairs = nullptr;  // update_bonds output buffer (p, k) pairs
     int64_t new_pairs_cap = 0;
@@ -176,7 +177,7 @@ void launch_direct_apply(Engine& e, const double* u, double* f, int batch, cudaS
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s,
                         double scale);
 int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double* watch,
-                            cudaStream_t s);
+                            cudaStream_t s, bool sync = true);
 
 // solvers.cu
 void launch_dot(Engine& e, const double* a, const double* b, int64_t n, double* out_dev,
