@@ -38,6 +38,30 @@
 namespace pdgpu {
 
 // ------------------------------------------------ async copies / L2 hints ---
+// mbarrier + 1D bulk copy (cp.async.bulk, TMA engine) helpers
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=: mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}" ::"r"(
+            smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     const int n = pred ? 16 : 0;  // zero-fill outside the window
@@ -809,12 +833,38 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
     double2* xb = reinterpret_cast<double2*>(xd + gi * XB);
     const int ND = 3 * (M + 1);
     double* dsm = xd + NC * XB + gi * ND;
+    // x_0 of the next half arrives in the park by a bulk copy (TMA engine)
+    // issued while the previous half's last inverse transform runs
+    uint64_t* bars = reinterpret_cast<uint64_t*>(xd + NC * XB + (SYM == 2 ? NC * ND : 0));
+    const unsigned xbytes = (unsigned)Nl * 16u;
     const int shP = logTWN - (LOGQ + 1);
     // register budget (128): twiddle bases are re-read from the (L1-resident)
     // table where they are used, behind opaque indices so they stay there
     const int ngroups = (ncols + NC - 1) / NC;
     const int64_t nitems = (int64_t)ngroups * batch;
     const int64_t cstride = (int64_t)ncols * Nl;
+    auto item_x0 = [&](int64_t item, bool& ok) {
+        const int bb = (int)(item % batch);
+        const int cl = (int)(item / batch) * NC + gi;
+        ok = cl < ncols;
+        return in + ((int64_t)(bb * 2 + 0) * ncols + (ok ? cl : 0)) * Nl;
+    };
+    // all threads call this after a CTA barrier (park no longer read)
+    auto prefetch = [&](const double2* src, bool ok) {
+        if (t == 0 && ok) {
+            fence_proxy_async();
+            mbar_expect_tx(&bars[gi], xbytes);
+            bulk_load(park, src, xbytes, &bars[gi]);
+        }
+    };
+    if (t == 0) mbar_init(&bars[gi], 1);
+    __syncthreads();
+    unsigned ph = 0;
+    if (blockIdx.x < nitems) {
+        bool ok;
+        const double2* x = item_x0(blockIdx.x, ok);
+        prefetch(x, ok);
+    }
     for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
         const int b = (int)(it % batch);
         const int col = (int)(it / batch) * NC + gi;
@@ -829,13 +879,25 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
         for (int h = 0; h < 2; ++h) {
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
-                const double2* src = x0 + c * cstride;
-                // x is read again for half 1: keep it in L2 until then
-                const uint64_t pol = h ? l2_policy_evict_first() : l2_policy_evict_last();
+                if (c == 0) {
+                    if (valid) {
+                        mbar_wait(&bars[gi], ph);
+                        ph ^= 1;
+                    }
 #pragma unroll
-                for (int j = 0; j < RR; ++j) {
-                    const int n = t + j * T;
-                    v[j] = (valid && n < Nl) ? ld_hint(src + n, pol) : make_double2(0.0, 0.0);
+                    for (int j = 0; j < RR; ++j) {
+                        const int n = t + j * T;
+                        v[j] = (valid && n < Nl) ? park[j * T + t] : make_double2(0.0, 0.0);
+                    }
+                } else {
+                    const double2* src = x0 + cstride;
+                    // x_1 is read again for half 1: keep it in L2 until then
+                    const uint64_t pol = h ? l2_policy_evict_first() : l2_policy_evict_last();
+#pragma unroll
+                    for (int j = 0; j < RR; ++j) {
+                        const int n = t + j * T;
+                        v[j] = (valid && n < Nl) ? ld_hint(src + n, pol) : make_double2(0.0, 0.0);
+                    }
                 }
                 if (h) {
                     const double2 w = __ldg(tw + (opaque(t) << shP));  // exp(-2 pi i t/Pl)
@@ -882,6 +944,14 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
                 if (ai == 1) {
 #pragma unroll
                     for (int j = 0; j < RR; ++j) v[j] = park[j * T + t];
+                    __syncthreads();  // park free: fetch the next half's x_0 behind this transform
+                    if (h == 0) {
+                        prefetch(x0, valid);
+                    } else if (it + gridDim.x < nitems) {
+                        bool ok;
+                        const double2* x = item_x0(it + gridDim.x, ok);
+                        prefetch(x, ok);
+                    }
                 }
                 reg_fft<LOGQ, kPipeLogR, 1, BlockBar, true>(v, t, xb, make_fft_tw<LOGQ, kPipeLogR>(opaque(t), tw, logTWN),
                                                             BlockBar{});
@@ -1233,7 +1303,7 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
             if (!(k3env && std::string(k3env) == "pipe") && lq >= 4) {
                 const int NCd = kPipeThreads / Tp;
                 const size_t dsmem = (size_t)NCd * (sizeof(double2) * (1 << lq) + sizeof(double) * xbuf_slots(lq) +
-                                                    (mode == 2 ? sizeof(double) * ND : 0));
+                                                    (mode == 2 ? sizeof(double) * ND : 0) + sizeof(uint64_t));
                 const int per_sm = std::max(1, std::min(2, (int)(228 * 1024 / (dsmem + 1024))));
                 const int64_t nitems = (int64_t)((pl.ncols + NCd - 1) / NCd) * batch;
                 const unsigned dgrid = (unsigned)std::min<int64_t>(nitems, (int64_t)e.num_sms * per_sm);
