@@ -60,6 +60,10 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
+// bulk prefetch of [src, src+bytes) into L2 (TMA engine, no SMEM, no registers)
+__device__ __forceinline__ void l2_prefetch(const void* src, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
@@ -880,6 +884,18 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
                 if (c == 0) {
+                    if (valid && t == 0) {
+                        // operands of the rest of this half, pulled into L2 behind FFT(x_0):
+                        // x_1, this half's symbol rows, and z^0 for the half-1 update
+                        l2_prefetch(x0 + cstride, xbytes);
+                        if (SYM != 2)
+                            l2_prefetch((const char*)sym + (((int64_t)cc * 2 + h) * Q) * 3 * (SYM == 1 ? 8 : 16),
+                                        (unsigned)Q * 3 * (SYM == 1 ? 8 : 16));
+                        if (h) {
+                            l2_prefetch(z0, xbytes);
+                            l2_prefetch(z0 + cstride, xbytes);
+                        }
+                    }
                     if (valid) {
                         mbar_wait(&bars[gi], ph);
                         ph ^= 1;
