@@ -510,7 +510,7 @@ def main():
         nbytes = BATCH * DIM * n * 8
         e2e = {"value": world * BATCH * DIM * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nbytes,
                "d2h_bytes_per_step": nbytes, "steps": e2e_steps, "ms_per_step": e2e_s * 1e3,
-               "api": "pdgpu_matvec_host (pinned host u -> host f; H2D/compute/D2H pipelined in 2-vector chunks)"}
+               "api": "pdgpu_matvec_host (pinned host u -> host f; H2D/compute/D2H pipelined in 1-vector chunks)"}
         del uh, fh
     ff.close()
     del u, f

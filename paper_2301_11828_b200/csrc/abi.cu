@@ -708,8 +708,10 @@ int pdgpu_matvec_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes, in
             cuda_check(cudaStreamCreateWithFlags(&h->copy_in, cudaStreamNonBlocking), "stream");
             cuda_check(cudaStreamCreateWithFlags(&h->copy_out, cudaStreamNonBlocking), "stream");
         }
-        // pipeline: H2D of chunk c+1 and D2H of chunk c-1 overlap the mat-vec of chunk c
-        const int chunk = batch >= 8 ? 2 : 1;
+        // pipeline: H2D of chunk c+1 and D2H of chunk c-1 overlap the mat-vec of
+        // chunk c.  PCIe-bound (the copies take ~4x the mat-vec), so one-vector
+        // chunks: the exposed first H2D and last D2H are as short as possible
+        const int chunk = 1;
         const int nch = (batch + chunk - 1) / chunk;
         std::vector<cudaEvent_t> evh(nch), evc(nch);
         for (int c = 0; c < nch; ++c) {
