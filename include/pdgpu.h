@@ -191,6 +191,18 @@ int pdgpu_build_kernel(int dim, double spacing, double delta, int M, double E, d
 /* Regions near-surface flags (grid.hpp:181-189): out N bytes */
 int pdgpu_near_surface(int dim, const int* dims, int M, uint8_t* out);
 
+/* ------------------------------------------------------------ snapshots --
+ * write_snapshot_dat / read_snapshot_dat (output.hpp:74-154): the
+ * reference's plain-text, bit-exact trajectory format ("dir/snap_%07d.dat",
+ * %.17g values, node ids from 1).  u is dim x N host SoA; damage may be NULL
+ * (written as 0).  Host-only (no handle, no device).  The reader fills the
+ * header fields; pass u = NULL first to learn dims, then buffers of dim*N
+ * (and N for damage). */
+int pdgpu_write_snapshot(int dim, const int* dims, double spacing, const double* origin, const double* u,
+                         const double* damage, int64_t step, double t, const char* dir, char* path_out, int path_cap);
+int pdgpu_read_snapshot(const char* path, int dim, int* dims, double* spacing, double* origin, int64_t* step,
+                        double* t, double* u, double* damage);
+
 #ifdef __cplusplus
 }
 #endif

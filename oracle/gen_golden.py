@@ -249,9 +249,39 @@ def gen_vv():
     np.savez_compressed(os.path.join(OUT, "vv_precracked.npz"), **out)
 
 
+def snapshot_case(dim):
+    """Fields of the snapshot goldens: mt19937 values (seed 6000 + dim) scaled
+    over many decades, plus exact edge values (0, -0, 1/3, tiny, huge)."""
+    dims = (7, 5) if dim == 2 else (4, 3, 2)
+    n = int(np.prod(dims))
+    rng = Rng(6000 + dim, ref=True)
+    u = rng.uniform(dim * n).reshape(dim, n) * 10.0 ** np.linspace(-300, 300, dim * n).reshape(dim, n)
+    u[0, :5] = [0.0, -0.0, 1.0 / 3.0, 5e-324, 1.7976931348623157e308]
+    damage = rng.uniform(n) * 0.5 + 0.5
+    origin = np.array([0.125, -2.0 / 3.0, 1e-17][:dim])
+    return dims, 1.0 / 1024.0 if dim == 2 else 0.1, origin, u, damage, 42 if dim == 2 else 1234567, 0.1 * 3
+
+
+def gen_snapshots():
+    """Snapshot files written by the reference's write_snapshot_dat (output.hpp:76-102),
+    run through oracle/_ref/snap_writer on raw fp64 inputs."""
+    import subprocess
+    import tempfile
+    exe = os.path.join(HERE, "_ref", "snap_writer")
+    for dim in (2, 3):
+        dims, h, origin, u, damage, step, t = snapshot_case(dim)
+        d = os.path.join(OUT, f"snap{dim}d")
+        with tempfile.TemporaryDirectory() as tmp:
+            fu, fd = os.path.join(tmp, "u.raw"), os.path.join(tmp, "d.raw")
+            np.ascontiguousarray(u).tofile(fu)
+            np.ascontiguousarray(damage).tofile(fd)
+            args = [exe, str(dim), *map(str, dims), repr(h), *map(repr, origin.tolist()), str(step), repr(t), d, fu, fd]
+            subprocess.run(args, check=True, capture_output=True)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
-    for fn in (gen_conv, gen_corrections, gen_acceptance, gen_configs, gen_seeds, gen_vv):
+    for fn in (gen_conv, gen_corrections, gen_acceptance, gen_configs, gen_seeds, gen_vv, gen_snapshots):
         fn()
         print("wrote", fn.__name__)
 

@@ -564,4 +564,6 @@ void ref_tbt_apply_all(void* vp, const double* u, double* f) {
     else run(get<3>(P), std::integral_constant<int, 3>{});
 }
 
+
+
 }  // extern "C"

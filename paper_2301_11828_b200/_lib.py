@@ -37,6 +37,10 @@ SIGNATURES = {
     "pdgpu_set_regions": (C.c_int, [C.c_void_p, c_uint8_p, c_uint8_p]),
     "pdgpu_set_surface_diag": (C.c_int, [C.c_void_p, c_double_p]),
     "pdgpu_set_slab": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "pdgpu_write_snapshot": (C.c_int, [C.c_int, C.POINTER(C.c_int), C.c_double, c_double_p, c_double_p, c_double_p,
+                                       C.c_int64, C.c_double, C.c_char_p, C.c_char_p, C.c_int]),
+    "pdgpu_read_snapshot": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_int), c_double_p, c_double_p,
+                                      C.POINTER(C.c_int64), c_double_p, c_double_p, c_double_p]),
     "pdgpu_constraint_values": (C.c_int, [C.c_void_p, c_uint8_p, c_double_p]),
     "pdgpu_set_ledger": (C.c_int, [C.c_void_p, c_int64_p, c_int64_p]),
     "pdgpu_break_bonds": (C.c_int, [C.c_void_p, c_int64_p, C.c_int64]),

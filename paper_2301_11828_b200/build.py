@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpdgpu.so")
-SOURCES = ["spectral.cu", "corrections.cu", "direct.cu", "solvers.cu", "abi.cu", "assembly.cpp"]
+SOURCES = ["spectral.cu", "corrections.cu", "direct.cu", "solvers.cu", "abi.cu", "assembly.cpp", "snapshot.cpp"]
 HEADERS = ["engine.h", "fft.cuh", "assembly.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -15,6 +15,15 @@
 #include "assembly.h"
 #include "engine.h"
 
+namespace pdgpu {
+namespace snapshot {
+std::string write(const std::string& dir, int dim, const int* dims, double h, const double* origin,
+                  const double* u, const double* damage, int64_t step, double t);
+bool read(const std::string& path, int dim, int* dims, double* h, double* origin, int64_t* step, double* t,
+          double* u, double* damage, std::string& err);
+}  // namespace snapshot
+}  // namespace pdgpu
+
 using namespace pdgpu;
 
 struct pdgpu_engine : public Engine {};
@@ -1178,3 +1187,28 @@ int pdgpu_near_surface(int dim, const int* dims, int M, uint8_t* out) {
 }
 
 }  // extern "C"
+
+/* ------------------------------------------------------------ snapshots -- */
+int pdgpu_write_snapshot(int dim, const int* dims, double spacing, const double* origin, const double* u,
+                         const double* damage, int64_t step, double t, const char* dir, char* path_out, int path_cap) {
+    return guarded([&] {
+        if (!dims || !origin || !dir || !u || dim < 1 || dim > 3) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
+        const std::string path = pdgpu::snapshot::write(dir, dim, dims, spacing, origin, u, damage, step, t);
+        if (path.empty()) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, std::string("cannot write snapshot in ") + dir);
+        if (path_out && path_cap > 0) {
+            strncpy(path_out, path.c_str(), (size_t)path_cap - 1);
+            path_out[path_cap - 1] = 0;
+        }
+    });
+}
+
+int pdgpu_read_snapshot(const char* path, int dim, int* dims, double* spacing, double* origin, int64_t* step,
+                        double* t, double* u, double* damage) {
+    return guarded([&] {
+        if (!path || !dims || !spacing || !origin || !step || !t || dim < 1 || dim > 3)
+            throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
+        std::string err;
+        if (!pdgpu::snapshot::read(path, dim, dims, spacing, origin, step, t, u, damage, err))
+            throw PdError(PDGPU_ERR_INVALID_ARGUMENT, err);
+    });
+}

@@ -121,6 +121,7 @@ class FastForce:
         h = C.c_void_p()
         _check(self._lib.pdgpu_create(self.dim, dims_a, self.M, _dp(st), device, C.byref(h)))
         self._h = h
+        self._geom = (1.0, np.zeros(self.dim))
 
     # ------------------------------------------------------------ lifetime
     def close(self):
@@ -147,6 +148,7 @@ class FastForce:
     # ---------------------------------------------------------- geometry
     def set_geometry(self, h: float, origin=None, delta: float = 0.0, rho: float = 1.0):
         org = _f64(origin if origin is not None else np.zeros(self.dim))
+        self._geom = (float(h), org.copy())
         _check(self._lib.pdgpu_set_geometry(self._h, h, _dp(org), delta, rho))
 
     # ------------------------------------------------------ spectral apply
@@ -319,6 +321,10 @@ class FastForce:
         _check(self._lib.pdgpu_sim_step(self._h, n_steps, s0, None if w is None else _dp(w), C.byref(nb)))
         return nb.value
 
+    def write_snapshot(self, directory: str, u: np.ndarray, step: int, t: float, damage=None) -> str:
+        """write_snapshot_dat (output.hpp:76-102) of host field u (dim, N) on this lattice/geometry."""
+        return write_snapshot(directory, self.dims, self._geom[0], self._geom[1], u, step, t, damage)
+
     def sim_get(self):
         u = np.zeros((self.dim, self.n))
         v = np.zeros_like(u)
@@ -326,6 +332,38 @@ class FastForce:
         t = C.c_double()
         _check(self._lib.pdgpu_sim_get(self._h, _dp(u), _dp(v), _dp(f), C.byref(t)))
         return u, v, f, t.value
+
+
+def write_snapshot(directory: str, dims, h: float, origin, u: np.ndarray, step: int, t: float, damage=None) -> str:
+    """write_snapshot_dat (output.hpp:76-102): directory/snap_%07d.dat, %.17g values; returns the path."""
+    lib = _lib.load()
+    dim = len(dims)
+    n = int(np.prod(dims))
+    u = _f64(u).reshape(dim, n)
+    org = _f64(origin if origin is not None else np.zeros(dim))
+    d = None if damage is None else _f64(damage)
+    buf = C.create_string_buffer(4096)
+    _check(lib.pdgpu_write_snapshot(dim, (C.c_int * dim)(*dims), float(h), _dp(org), _dp(u),
+                                    None if d is None else _dp(d), int(step), float(t), directory.encode(), buf, 4096))
+    return buf.value.decode()
+
+
+def read_snapshot(path: str, dim: int):
+    """read_snapshot_dat (output.hpp:116-154) -> dict(dims, h, origin, step, t, u[dim, N], damage[N])."""
+    lib = _lib.load()
+    dims = (C.c_int * 3)()
+    h = C.c_double()
+    org = np.zeros(3)
+    step = C.c_int64()
+    t = C.c_double()
+    p = path.encode()
+    _check(lib.pdgpu_read_snapshot(p, dim, dims, C.byref(h), _dp(org), C.byref(step), C.byref(t), None, None))
+    n = int(np.prod([dims[d] for d in range(dim)]))
+    u = np.zeros((dim, n))
+    dmg = np.zeros(n)
+    _check(lib.pdgpu_read_snapshot(p, dim, dims, C.byref(h), _dp(org), C.byref(step), C.byref(t), _dp(u), _dp(dmg)))
+    return {"dims": tuple(dims[d] for d in range(dim)), "h": h.value, "origin": org[:dim].copy(),
+            "step": step.value, "t": t.value, "u": u, "damage": dmg}
 
 
 def _ptr(x) -> int:
