@@ -117,6 +117,7 @@ void rebuild_constraints(Engine& e) {
     const int dim = e.dim;
     e.h_cmask.assign((size_t)N, 0);
     std::map<long long, std::pair<int, double>> dofs;
+    std::map<long long, double> ucv;  // prescribed displacements (kind 0 only, later boxes win)
     for (const auto& cs : e.constraints) {
         for (int64_t p = 0; p < N; ++p) {
             double x[3];
@@ -124,7 +125,27 @@ void rebuild_constraints(Engine& e) {
             if (!assembly::box_contains(dim, cs.lo, cs.hi, x)) continue;
             e.h_cmask[(size_t)p] |= cs.dir_mask;
             for (int d = 0; d < dim; ++d)
-                if ((cs.dir_mask >> d) & 1u) dofs[(long long)d * N + p] = {cs.kind, cs.value};
+                if ((cs.dir_mask >> d) & 1u) {
+                    dofs[(long long)d * N + p] = {cs.kind, cs.value};
+                    if (cs.kind == 0) ucv[(long long)d * N + p] = cs.value;
+                }
+        }
+    }
+    // u_c for CG as a sparse list (the solve scatters it on the device)
+    {
+        std::vector<long long> uid;
+        std::vector<double> uval;
+        for (const auto& kv : ucv)
+            if (kv.second != 0.0) {
+                uid.push_back(kv.first);
+                uval.push_back(kv.second);
+            }
+        e.n_uc = (int64_t)uid.size();
+        dalloc(e.d_uc_ids, std::max<size_t>(uid.size(), 1), "alloc uc ids");
+        dalloc(e.d_uc_val, std::max<size_t>(uval.size(), 1), "alloc uc val");
+        if (!uid.empty()) {
+            cuda_check(cudaMemcpy(e.d_uc_ids, uid.data(), sizeof(long long) * uid.size(), cudaMemcpyHostToDevice), "uc");
+            cuda_check(cudaMemcpy(e.d_uc_val, uval.data(), sizeof(double) * uval.size(), cudaMemcpyHostToDevice), "uc");
         }
     }
     cuda_check(cudaMemcpy(e.d_cmask, e.h_cmask.data(), (size_t)N, cudaMemcpyHostToDevice), "copy cmask");
@@ -463,7 +484,7 @@ void pdgpu_destroy(pdgpu_t h) {
                     h->d_cmask, h->d_surf_rows, h->d_surf_de, h->d_ledger, h->d_bond_rows, h->d_listed,
                     h->d_counters, h->d_new_pairs, h->d_body, h->d_cdofs, h->d_cval, h->d_ckind, h->d_u, h->d_v,
                     h->d_f, h->d_fprev, h->d_red, h->d_scal, h->d_ticket, h->d_cg, h->d_coltab,
-                    h->d_scratch, h->d_kc};
+                    h->d_scratch, h->d_kc, h->d_uc_ids, h->d_uc_val};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->cg_graph) cudaGraphExecDestroy(h->cg_graph);
@@ -945,10 +966,13 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
     double* p = r + m;
     double* q = p + m;
     double* uc = q + m;
-    // prescribed displacement values u_c (displacement constraints only)
-    std::vector<double> huc;
-    const bool any_uc = prescribed_values(e, huc);
-    if (any_uc) cuda_check(cudaMemcpyAsync(uc, huc.data(), sizeof(double) * m, cudaMemcpyHostToDevice, s), "copy uc");
+    // prescribed displacement values u_c (displacement constraints only), scattered
+    // on the device from the list rebuild_constraints keeps (no host O(N) pass per solve)
+    const bool any_uc = e.n_uc > 0;
+    if (any_uc) {
+        cuda_check(cudaMemsetAsync(uc, 0, sizeof(double) * m, s), "zero uc");
+        launch_scatter(uc, e.d_uc_ids, e.d_uc_val, e.n_uc, s);
+    }
     if (any_uc) {
         matvec_impl(e, uc, q, 1, s);
         launch_mask_rhs(r, b, q, e.d_cmask, N, e.dim, s);

@@ -99,6 +99,9 @@ struct Engine {
     long long* d_cdofs = nullptr;        // constrained dof ids (a*N + p), last-writer-wins order
     double* d_cval = nullptr;            // value per constrained dof
     int* d_ckind = nullptr;              // kind per constrained dof
+    long long* d_uc_ids = nullptr;       // CG: dofs with a nonzero prescribed displacement
+    double* d_uc_val = nullptr;
+    int64_t n_uc = 0;
     int64_t n_cdofs = 0;
     double *d_u = nullptr, *d_v = nullptr, *d_f = nullptr, *d_fprev = nullptr;
     double t = 0.0, dt = 0.0;
@@ -196,5 +199,6 @@ void launch_vv_kick(double* v, const double* fprev, const double* f, const uint8
 void launch_enforce(double* u, double* v, const long long* dofs, const double* val, const int* kind,
                     int64_t n, double t, cudaStream_t s);
 void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s);
+void launch_scatter(double* y, const long long* ids, const double* val, int64_t n, cudaStream_t s);
 
 }  // namespace pdgpu

@@ -208,6 +208,11 @@ __global__ void k_enforce(double* u, double* v, const long long* dofs, const dou
     }
 }
 
+__global__ void k_scatter(double* y, const long long* ids, const double* val, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) y[ids[i]] = val[i];
+}
+
 __global__ void k_axpy(double* y, const double* x, double a, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) y[i] += a * x[i];
@@ -268,6 +273,12 @@ void launch_enforce(double* u, double* v, const long long* dofs, const double* v
     if (n == 0) return;
     k_enforce<<<blocks_for(n, 256), 256, 0, s>>>(u, v, dofs, val, kind, n, t);
     check(cudaGetLastError(), "enforce");
+}
+
+void launch_scatter(double* y, const long long* ids, const double* val, int64_t n, cudaStream_t s) {
+    if (n == 0) return;
+    k_scatter<<<blocks_for(n, 256), 256, 0, s>>>(y, ids, val, n);
+    check(cudaGetLastError(), "scatter");
 }
 
 void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s) {
