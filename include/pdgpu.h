@@ -80,6 +80,12 @@ int pdgpu_symbol_is_real(pdgpu_t h);
 /* 0 complex symbol table, 1 real symbol table, 2 separable per-column
  * symbol (physical stencils of definite parity per axis). */
 int pdgpu_symbol_mode(pdgpu_t h);
+/* Transform embedding per axis, bit d set = periodic (P_d = N_d, aliased
+ * boundary terms removed by the wrap correction), clear = zero-padded to
+ * P_d = 2 pow2ceil(N_d) like PadTransform (convolution.hpp:58-71).  Both give
+ * the reference's linear correlation; PDGPU_EMBED=padded at create time forces
+ * padding on every axis. */
+int pdgpu_embedding(pdgpu_t h);
 
 /* ----------------------------------------------------------- corrections --
  * Regions (grid.hpp:172-209): per-node constraint direction mask (bit d =

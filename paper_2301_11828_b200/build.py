@@ -14,6 +14,9 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpdgpu.so")
+# spectral.cu is compiled once per part (-DPDGPU_PART=k): each object
+# instantiates only its own kernel templates, and the parts build in parallel
+SPECTRAL_PARTS = 5
 SOURCES = ["spectral.cu", "corrections.cu", "direct.cu", "solvers.cu", "abi.cu", "assembly.cpp", "snapshot.cpp"]
 HEADERS = ["engine.h", "fft.cuh", "assembly.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -42,12 +45,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []
+    units = []
     for s in SOURCES:
+        if s == "spectral.cu":
+            units += [(s, f"{s}.part{k}.o", [f"-DPDGPU_PART={k}"]) for k in range(SPECTRAL_PARTS)]
+        elif s == "corrections.cu":
+            units.append((s, s + ".o", ["--fmad=false"]))  # bond stretch must round like the reference
+        else:
+            units.append((s, s + ".o", []))
+    for s, oname, extra in units:
         src = os.path.join(CSRC, s)
-        obj = os.path.join(objdir, s + ".o")
-        extra = []
-        if s == "corrections.cu":
-            extra = ["--fmad=false"]  # bond stretch must round like the reference
+        obj = os.path.join(objdir, oname)
         cmd = [NVCC, *ARCH, *FLAGS, *extra, "-Xptxas", "-v" if verbose else "-O3", "-c", src, "-o", obj]
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
         objs.append(obj)

@@ -402,7 +402,7 @@ int pdgpu_create(int dim, const int* dims, int M, const double* stencils, int de
             e->nof = (int)e->offs.size() / 3;
             e->lw = (e->nof + 31) / 32;
             e->delta = M;
-            plan_init(e->plan, dim, dims);
+            plan_init(e->plan, dim, dims, M);
             const Plan& pl = e->plan;
             const int64_t N = pl.nodes;
             if (pl.P[0] / 4 * 2 * 16 > 227 * 1024 || pl.Pl / 2 * dim * 16 > 227 * 1024)
@@ -556,6 +556,7 @@ size_t pdgpu_footprint_bytes(pdgpu_t h) {
 int64_t pdgpu_n_nodes(pdgpu_t h) { return h ? h->plan.nodes : 0; }
 int pdgpu_symbol_is_real(pdgpu_t h) { return h && h->real_symbol ? 1 : 0; }
 int pdgpu_symbol_mode(pdgpu_t h) { return !h ? -1 : (h->d_coltab ? 2 : (h->real_symbol ? 1 : 0)); }
+int pdgpu_embedding(pdgpu_t h) { return !h ? -1 : h->plan.circ_mask; }
 
 int pdgpu_set_regions(pdgpu_t h, const uint8_t* near_surface, const uint8_t* cmask) {
     return guarded([&] {

@@ -109,6 +109,122 @@ static void check(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// K6w wrap correction of the periodic embedding (engine.h, Plan).  Along a
+// periodic axis the FFT product evaluates sum_o K(o) u[(p+o) mod P]; the
+// reference's padded transform (convolution.hpp:58-71,183-195) sees zeros
+// outside the lattice.  The two differ exactly by the aliased terms: offsets
+// o with p+o outside the lattice along some axis, every such axis periodic
+// (P = N, so the wrapped coordinate lands back inside).  Only nodes within M
+// layers of a periodic face have any; thread per such node, enumerated face
+// by face (a node in the bands of several periodic axes is handled by the
+// first), the full (2M+1)^d box of every stencil component (the same
+// entries the symbol is built from, so arbitrary stencils stay exact).
+// f_a[p] -= scale * sum_o sum_b K_ab(o) u_b[wrap(p+o)] on rows not
+// constrained in a (K5 has zeroed those).
+template <int D>
+__global__ void k_wrap(const double* __restrict__ u, double* __restrict__ f, const double* __restrict__ K,
+                       int M, int64_t ss, int N0, int N1, int N2, int circ_mask, const uint8_t* __restrict__ cmask,
+                       int64_t nodes, int batch, double scale, int64_t band0, int64_t band1, int64_t band2) {
+    constexpr int NP = D * (D + 1) / 2;
+    const int64_t per_vec = band0 + band1 + band2;
+    const int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gidx >= per_vec * batch) return;
+    const int b = (int)(gidx / per_vec);
+    int64_t r = gidx - (int64_t)b * per_vec;
+    const int N[3] = {N0, N1, N2};
+    int ax = 0;
+    if (r >= band0) {
+        r -= band0;
+        ax = 1;
+        if (r >= band1) {
+            r -= band1;
+            ax = 2;
+        }
+    }
+    // mixed radix (x fastest), the band axis taking 2M values
+    int c[3];
+    for (int d = 0; d < 3; ++d) {
+        const int n = d == ax ? 2 * M : N[d];
+        c[d] = (int)(r % n);
+        r /= n;
+    }
+    c[ax] = c[ax] < M ? c[ax] : N[ax] - 2 * M + c[ax];
+    for (int d = 0; d < ax; ++d)  // already covered by an earlier periodic axis
+        if (((circ_mask >> d) & 1) && (c[d] < M || c[d] >= N[d] - M)) return;
+    const int64_t p = ((int64_t)c[2] * N1 + c[1]) * N0 + c[0];
+    const uint8_t cm = cmask ? cmask[p] : 0;
+    const double* ub = u + (int64_t)b * D * nodes;
+    double acc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) acc[a] = 0.0;
+    const int side = 2 * M + 1;
+    const int m2 = D == 3 ? M : 0;
+    for (int o2 = -m2; o2 <= m2; ++o2) {
+        int w2 = c[2] + o2, out2 = 0;
+        if (D == 3 && (w2 < 0 || w2 >= N2)) {
+            if (!((circ_mask >> 2) & 1)) continue;
+            w2 = w2 < 0 ? w2 + N2 : w2 - N2;
+            out2 = 1;
+        }
+        for (int o1 = -M; o1 <= M; ++o1) {
+            int w1 = c[1] + o1, out1 = out2;
+            if (w1 < 0 || w1 >= N1) {
+                if (!((circ_mask >> 1) & 1)) continue;
+                w1 = w1 < 0 ? w1 + N1 : w1 - N1;
+                out1 = 1;
+            }
+            const int64_t srow = ((int64_t)(o2 + m2) * side + (o1 + M)) * side + M;
+            const int64_t qrow = ((int64_t)w2 * N1 + w1) * N0;
+            for (int o0 = -M; o0 <= M; ++o0) {
+                int w0 = c[0] + o0, out = out1;
+                if (w0 < 0 || w0 >= N0) {
+                    if (!(circ_mask & 1)) continue;
+                    w0 = w0 < 0 ? w0 + N0 : w0 - N0;
+                    out = 1;
+                }
+                if (!out) continue;
+                const int64_t si = srow + o0;
+                const int64_t q = qrow + w0;
+                double uq[D];
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) uq[bb] = ub[(int64_t)bb * nodes + q];
+#pragma unroll
+                for (int a = 0; a < D; ++a)
+#pragma unroll
+                    for (int bb = 0; bb < D; ++bb) acc[a] += __ldg(K + pair_idx<D>(a, bb) * ss + si) * uq[bb];
+            }
+        }
+    }
+    (void)NP;
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        if ((cm >> a) & 1u) continue;
+        f[((int64_t)b * D + a) * nodes + p] -= scale * acc[a];
+    }
+}
+
+void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
+                            const uint8_t* cmask) {
+    const Plan& pl = e.plan;
+    int64_t band[3] = {0, 0, 0};
+    for (int d = 0; d < pl.dim; ++d) {
+        if (!pl.circ[d]) continue;
+        band[d] = 2 * e.M;
+        for (int k = 0; k < 3; ++k)
+            if (k != d) band[d] *= pl.N[k];
+    }
+    const int64_t tot = (band[0] + band[1] + band[2]) * batch;
+    if (tot == 0) return;
+    const int th = 128;
+    const unsigned blocks = (unsigned)((tot + th - 1) / th);
+    if (pl.dim == 2)
+        k_wrap<2><<<blocks, th, 0, s>>>(u, f, e.d_K, e.M, e.ss, pl.N[0], pl.N[1], pl.N[2], pl.circ_mask, cmask,
+                                        pl.nodes, batch, scale, band[0], band[1], band[2]);
+    else
+        k_wrap<3><<<blocks, th, 0, s>>>(u, f, e.d_K, e.M, e.ss, pl.N[0], pl.N[1], pl.N[2], pl.circ_mask, cmask,
+                                        pl.nodes, batch, scale, band[0], band[1], band[2]);
+}
+
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale) {
     const int64_t N = e.plan.nodes;
     if (e.n_surf > 0) {

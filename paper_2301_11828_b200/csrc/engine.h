@@ -13,14 +13,27 @@ namespace pdgpu {
 
 constexpr int kMaxDim = 3;
 
-// Transform geometry.  Each axis is padded to P = 2*pow2ceil(N): >= N+M so the
-// circular correlation equals the reference's linear one on the window
-// (convolution.hpp:58-71 uses P = 2N, identical for power-of-two N).
+// Transform geometry.  Two embeddings per axis:
+//  - padded:   P = 2*pow2ceil(N) >= N+M, so the circular correlation equals
+//              the reference's linear one on the window (convolution.hpp:58-71
+//              uses P = 2N, identical for power-of-two N);
+//  - periodic: P = N (power of two, N >= max(2M+1, 16)).  The circular
+//              correlation then differs from the linear one only on the M
+//              node layers at each face of the axis, where stencil offsets
+//              leaving the lattice wrap onto the opposite face; those aliased
+//              terms are subtracted by the wrap correction (K6w,
+//              corrections.cu) -- the same "circulant + sparse boundary
+//              correction" split MSBFM already uses for D^e.  A quarter of
+//              the padded FFT volume in 2D, an eighth in 3D.
+// Default: periodic on every eligible axis; PDGPU_EMBED=padded forces padding.
 struct Plan {
     int dim = 2;
     int N[3] = {1, 1, 1};
     int P[3] = {1, 1, 1};
     int logP[3] = {0, 0, 0};
+    int circ[3] = {0, 0, 0};  // 1 = periodic embedding along this axis
+    int circ_mask = 0;        // bit d = circ[d]
+    int nh = 2;               // half-spectra of the last-axis pass: 2 padded, 1 periodic
     int64_t nodes = 0;  // N0*N1*N2
     int Hx = 0;         // R2C half spectrum along x: P0/2 + 1 columns
     int logQx = 0;      // x transforms are Qx = P0/4 points (R2C + zero half)
@@ -165,7 +178,7 @@ struct PassTimer {
 };
 
 // spectral.cu
-void plan_init(Plan& pl, int dim, const int* dims);
+void plan_init(Plan& pl, int dim, const int* dims, int M);
 void engine_alloc_workspace(Engine& e, int64_t batch);
 void build_twiddles(Engine& e);
 void build_symbol(Engine& e);
@@ -177,6 +190,8 @@ void set_kernel_attributes();
 void launch_direct_apply(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale);
 
 // corrections.cu
+void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
+                            const uint8_t* cmask);
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s,
                         double scale);
 int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double* watch,

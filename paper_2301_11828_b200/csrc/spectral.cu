@@ -35,6 +35,10 @@
 #include "engine.h"
 #include "fft.cuh"
 
+#ifndef PDGPU_PART
+#define PDGPU_ALL_PARTS 1  // see "The host side is compiled in parts" below
+#endif
+
 namespace pdgpu {
 
 // ------------------------------------------------ async copies / L2 hints ---
@@ -113,14 +117,25 @@ constexpr int kSmemBudget = 210 * 1024;
 static int xbuf_slots(int logq) { return (1 << logq) + ((1 << logq) >> 4) + 1; }
 static int threads_per_transform(int logq, int logrmax) { return 1 << std::max(0, logq - logrmax); }
 
-void plan_init(Plan& pl, int dim, const int* dims) {
+#if defined(PDGPU_ALL_PARTS) || PDGPU_PART == 0
+void plan_init(Plan& pl, int dim, const int* dims, int M) {
     pl.dim = dim;
+    bool periodic_ok = true;
+    if (const char* env = getenv("PDGPU_EMBED")) periodic_ok = std::string(env) != "padded";
+    pl.circ_mask = 0;
     for (int d = 0; d < 3; ++d) {
         pl.N[d] = d < dim ? dims[d] : 1;
+        pl.circ[d] = 0;
         if (d < dim) {
             const int lp = ilog2(pl.N[d]);
-            pl.logP[d] = lp + 1;
-            pl.P[d] = 1 << (lp + 1);
+            const bool pow2 = (1 << lp) == pl.N[d];
+            // periodic needs a power of two with room for the whole stencil
+            // (no self-overlap of the wrapped band) and the transform minimum
+            // sizes (duo/3D spectral kernels: >= 16 points)
+            pl.circ[d] = periodic_ok && pow2 && pl.N[d] >= 2 * M + 1 && pl.N[d] >= 16;
+            pl.logP[d] = pl.circ[d] ? lp : lp + 1;
+            pl.P[d] = 1 << pl.logP[d];
+            pl.circ_mask |= pl.circ[d] << d;
         } else {
             pl.logP[d] = 0;
             pl.P[d] = 1;
@@ -134,6 +149,7 @@ void plan_init(Plan& pl, int dim, const int* dims) {
         pl.Nl = pl.N[1];
         pl.Pl = pl.P[1];
         pl.logPl = pl.logP[1];
+        pl.nh = pl.circ[1] ? 1 : 2;
         pl.S1_per_vec = (int64_t)dim * pl.Hx * pl.N[1];
         pl.S2_per_vec = pl.S1_per_vec;  // K3 output (out of place, z^0 parked in it)
     } else {
@@ -141,6 +157,7 @@ void plan_init(Plan& pl, int dim, const int* dims) {
         pl.Nl = pl.N[2];
         pl.Pl = pl.P[2];
         pl.logPl = pl.logP[2];
+        pl.nh = pl.circ[2] ? 1 : 2;
         pl.S1_per_vec = (int64_t)dim * pl.N[2] * pl.Hx * pl.N[1];
         pl.S2_per_vec = (int64_t)dim * pl.Hx * pl.P[1] * pl.N[2];
     }
@@ -157,15 +174,16 @@ void plan_init(Plan& pl, int dim, const int* dims) {
     }
     // K3: columns per CTA
     {
-        const int logq = pl.logPl - 1;
+        const int logq = pl.logPl - (pl.nh == 2 ? 1 : 0);
         const int logr = dim == 3 ? 3 : 4;
         const int T = threads_per_transform(logq, logr);
-        const bool zsmem = dim == 3;  // 2D columns are too long to park z^0 on chip
+        // 2D columns are too long to park z^0 on chip; periodic: no z^0 at all
+        const bool zsmem = dim == 3 && pl.nh == 2;
         const int per_col = (xbuf_slots(logq) + (zsmem ? 2 * dim - 1 : dim - 1) * (1 << logq)) * 16;
         int nc = 1;
         while ((nc * 2) * T <= 256 && (nc * 2) * per_col <= kSmemBudget) nc *= 2;
         pl.k3_cols = nc;
-        pl.k3_halves = zsmem ? 2 : 1;
+        pl.k3_halves = dim == 3 ? 2 : 1;  // 3D: in place on S2; 2D: out of place S1 -> S2
     }
     if (dim == 3) {
         const int logq = pl.logP[1] - 1;
@@ -176,12 +194,16 @@ void plan_init(Plan& pl, int dim, const int* dims) {
         pl.k2_zt = std::min(zt, pl.N[2]);
     }
 }
+#endif
 
 // ------------------------------------------------------------------ K1 ---
 // Row transform of Nx reals zero-padded to Px = 4*Qx: z[n] = x[2n] + i x[2n+1]
 // (n < Qx carries all data); Z = FFT_{2Qx}(z) via even (E) and odd (O)
 // outputs, each a Qx-point FFT; X[k] = Fe + e^{-2 pi i k/Px} Fo.
-template <int LOGQ>
+// CIRC (periodic embedding, Px = Nx): z fills all 2Qx points and the even /
+// odd split is a decimation-in-frequency stage, E <- z[n] + z[n+Qx],
+// O <- (z[n] - z[n+Qx]) e^{-2 pi i n/(2Qx)}.
+template <int LOGQ, bool CIRC>
 __global__ void __launch_bounds__(512) k_rfft_rows(const double* __restrict__ u, double2* __restrict__ S, int Nx,
                                                    int Nrow, int Hx, int TR, const double2* __restrict__ tw,
                                                    int logTWN) {
@@ -209,6 +231,10 @@ __global__ void __launch_bounds__(512) k_rfft_rows(const double* __restrict__ u,
         if (valid && i0 < Nx) {
             if (vec) z = __ldg(reinterpret_cast<const double2*>(src + i0));
             else z = make_double2(src[i0], i0 + 1 < Nx ? src[i0 + 1] : 0.0);
+        }
+        if (CIRC) {  // Nx = 4Q, even
+            const double2 z2 = valid ? __ldg(reinterpret_cast<const double2*>(src + i0 + 2 * Q)) : make_double2(0.0, 0.0);
+            z = eo ? csub(z, z2) : cadd(z, z2);
         }
         v[j] = eo ? cmul(z, tw32r<-1>(j * (16 / R), wbase)) : z;
     }
@@ -242,8 +268,9 @@ __global__ void __launch_bounds__(512) k_rfft_rows(const double* __restrict__ u,
 // ------------------------------------------------------------------ K5 ---
 // C2R: Z[k] = (X[k] + conj X[h-k]) + i e^{+2 pi i k/Px} (X[k] - conj X[h-k]),
 // h = Px/2; z = IFFT_{2Qx}(Z) on its first Qx outputs = E'[n] + e^{+2 pi i n/(2Qx)} O'[n];
-// x[2n] = Re z, x[2n+1] = Im z.
-template <int LOGQ, int LOGTR>
+// x[2n] = Re z, x[2n+1] = Im z.  CIRC (Px = Nx): all 2Qx outputs are kept,
+// z[n + Qx] = E'[n] - e^{+2 pi i n/(2Qx)} O'[n].
+template <int LOGQ, int LOGTR, bool CIRC>
 __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ S, double* __restrict__ f, int Nx,
                                                     int Nrow, int Nz, int dim, int Hx,
                                                     const double2* __restrict__ tw, int logTWN, double scale,
@@ -340,13 +367,17 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
     const int z = slab % Nz;
     double* dst = f + ((int64_t)slab * Nrow + row0) * Nx;
     const bool vec = (Nx & 1) == 0;
+    constexpr int NOUT = CIRC ? 2 * Q : Q;  // complex outputs kept per row
+    constexpr int LOGNOUT = CIRC ? LOGQ + 1 : LOGQ;
 #pragma unroll 4
-    for (int u = 0; u < R / 2; ++u) {  // nr*Q <= 2*TR*T * R/2 items
+    for (int u = 0; u < (CIRC ? R : R / 2); ++u) {  // nr*NOUT <= 2*TR*T * R/2 (x2) items
         const int idx = threadIdx.x + u * 2 * TR * T;
-        const int rr = idx >> LOGQ, n = idx & (Q - 1);
+        const int rr = idx >> LOGNOUT, n = idx & (NOUT - 1);
         const int i0 = 2 * n;
         if (rr >= nr || i0 >= Nx) continue;
-        const double2 zz = cadd(sm[2 * rr * XB + spad(n)], sm[(2 * rr + 1) * XB + spad(n)]);
+        const int m = n & (Q - 1);
+        const double2 zo = sm[(2 * rr + 1) * XB + spad(m)];
+        const double2 zz = (CIRC && n >= Q) ? csub(sm[2 * rr * XB + spad(m)], zo) : cadd(sm[2 * rr * XB + spad(m)], zo);
         double v0 = zz.x * scale, v1 = zz.y * scale;
         const int64_t node = ((int64_t)z * Nrow + row0 + rr) * Nx + i0;
         const bool two = i0 + 1 < Nx;
@@ -373,6 +404,7 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
 // Half h (ky = 2k + h): U_c = FFT_Ql(x_c[n] e^{-2 pi i h n/Pl}); F_a = sum_c
 // H[col][h][k][pair(a,c)] U_c; z_a^h = IFFT_Ql(F_a);  y_a[n] = z_a^0[n] +
 // e^{+2 pi i n/Pl} z_a^1[n].  z^0 is parked in SMEM (thread-private slots).
+// NH = 1 (periodic column, Pl = Ql = Nl): one pass, no pre-twiddle, no park.
 template <int D>
 __device__ __forceinline__ int pair_of(int a, int b) {
     if (a > b) {
@@ -424,7 +456,7 @@ __device__ __forceinline__ void symbol_product(double2* F, const double2* U, con
     }
 }
 
-template <int LOGQ, int D, bool REAL, int LOGR, bool ZSMEM, bool SEP = false>
+template <int LOGQ, int D, bool REAL, int LOGR, bool ZSMEM, bool SEP = false, int NH = 2>
 __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2* out, const void* __restrict__ sym,
                                                      int ncols, int Nl, int NC, const double2* __restrict__ tw,
                                                      int logTWN, const double* __restrict__ coltab = nullptr,
@@ -445,7 +477,7 @@ __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2*
     // per column: (D-1)*Q component park, then (ZSMEM) D*Q half-0 park
     double2* cpark = sm + NC * XB + (int64_t)gi * (ZSMEM ? 2 * D - 1 : D - 1) * Q;
     double2* zpark = cpark + (D - 1) * Q;
-    const int shP = logTWN - (LOGQ + 1);
+    const int shP = logTWN - (LOGQ + NH - 1);  // Pl = NH * Q
     double2 v[RR];
     const FftTw tws = make_fft_tw<LOGQ, LOGR>(t, tw, logTWN);
     // separable symbol: this column's n_pairs x (M+1) coefficients in SMEM
@@ -454,7 +486,7 @@ __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2*
     if (SEP)
         for (int i = t; i < ND; i += T) dsm[i] = valid ? __ldg(coltab + (int64_t)col * ND + i) : 0.0;
 #pragma unroll 1
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < NH; ++h) {
 #pragma unroll 1
         for (int c = 0; c < D; ++c) {
             const double2* src = in + ((int64_t)(b * D + c) * ncols + col) * Nl;
@@ -472,9 +504,9 @@ __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2*
             }
         }
         // per-frequency d x d product (ky = 2k + h); last component in v
-        const int64_t sbase = ((int64_t)(valid ? col : 0) * 2 + h) * Q;
+        const int64_t sbase = ((int64_t)(valid ? col : 0) * NH + h) * Q;
         // e^{+2 pi i kz/Pl} for kz = 2(t + jT) + h: base(t, h) * e^{2 pi i j/RR}
-        const double2 eh = SEP ? cconj(__ldg(tw + ((2 * t + h) << shP))) : make_double2(1.0, 0.0);
+        const double2 eh = SEP ? cconj(__ldg(tw + ((NH * t + h) << shP))) : make_double2(1.0, 0.0);
 #pragma unroll
         for (int j = 0; j < RR; ++j) {
             const int k = t + j * T;
@@ -549,7 +581,7 @@ __global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2*
 // tile's TR rows of reals land in a staging buffer via cp.async while the
 // current tile is transformed and written, so HBM latency overlaps compute.
 // Requires even Nx (16-byte row alignment); the plain kernel covers the rest.
-template <int LOGQ, int LOGTR>
+template <int LOGQ, int LOGTR, bool CIRC>
 __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restrict__ u, double2* __restrict__ S,
                                                            int Nx, int Nrow, int nslab, int Hx,
                                                            const double2* __restrict__ tw, int logTWN) {
@@ -557,7 +589,7 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
     constexpr int TR = 1 << LOGTR;
     extern __shared__ double2 sm[];
-    double* stage = reinterpret_cast<double*>(sm + 2 * TR * XB);  // TR rows x (4Q reals max)
+    double* stage = reinterpret_cast<double*>(sm + 2 * TR * XB);  // TR rows x rowlen reals
     const int gi = threadIdx.x >> Sh::LOGT;
     const int t = threadIdx.x & (T - 1);
     const int r = gi >> 1, eo = gi & 1;
@@ -568,7 +600,7 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
     const FftTw tws = make_fft_tw<LOGQ, 4>(t, tw, logTWN);
     const int groups = (Nrow + TR - 1) / TR;
     const int64_t ntiles = (int64_t)groups * nslab;
-    const int rowlen = 2 * Q;  // staged doubles per row (>= Nx)
+    const int rowlen = CIRC ? 4 * Q : 2 * Q;  // staged doubles per row (>= Nx)
     auto fetch = [&](int64_t tile) {
         const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
         const int nr = min(TR, Nrow - row0);
@@ -605,7 +637,11 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
 #pragma unroll
         for (int j = 0; j < R; ++j) {
             const int n = t + j * T;
-            const double2 z = *reinterpret_cast<const double2*>(stage + r * rowlen + 2 * n);
+            double2 z = *reinterpret_cast<const double2*>(stage + r * rowlen + 2 * n);
+            if (CIRC) {  // decimation in frequency (see k_rfft_rows)
+                const double2 z2 = *reinterpret_cast<const double2*>(stage + r * rowlen + 2 * (n + Q));
+                z = eo ? csub(z, z2) : cadd(z, z2);
+            }
             v[j] = eo ? cmul(z, tw32r<-1>(j * (16 / R), wbase)) : z;
         }
         __syncthreads();
@@ -815,13 +851,16 @@ __global__ void __launch_bounds__(kPipeThreads, 1) k_spectral2d_pipe(const doubl
     cp_async_wait_all();
 }
 
+// NH = 2: padded column (Pl = 2Q, data on [0, Q)), two half-spectra as above.
+// NH = 1: periodic column (Pl = Q = Nl): one forward FFT per component, the
+// product, one inverse FFT, stored directly (no z^0 read-modify-write).
 // Two-CTA-per-SM variant of the 2D spectral pass: the exchange buffer holds
 // 8-byte slots (split real/imaginary exchange) and operands come straight from
 // global memory, so a CTA needs NC*(Q*16 + XBUF*8) bytes (~99 KB at Q = 4096)
 // and 128 registers per thread.  Two co-resident CTAs overlap each other's
 // load / symbol / store phases with FFT work (one CTA per SM leaves them
 // exposed).  Same data flow and numerics as k_spectral2d_pipe.
-template <int LOGQ, int SYM>
+template <int LOGQ, int SYM, int NH>
 __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double2* __restrict__ in, double2* out,
                                                                    const void* __restrict__ sym,
                                                                    const double* __restrict__ coltab, int M,
@@ -841,7 +880,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
     // issued while the previous half's last inverse transform runs
     uint64_t* bars = reinterpret_cast<uint64_t*>(xd + NC * XB + (SYM == 2 ? NC * ND : 0));
     const unsigned xbytes = (unsigned)Nl * 16u;
-    const int shP = logTWN - (LOGQ + 1);
+    const int shP = logTWN - (LOGQ + NH - 1);  // Pl = NH * Q
     // register budget (128): twiddle bases are re-read from the (L1-resident)
     // table where they are used, behind opaque indices so they stay there
     const int ngroups = (ncols + NC - 1) / NC;
@@ -880,7 +919,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
             for (int i = t; i < ND; i += T) dsm[i] = valid ? __ldg(coltab + (int64_t)cc * ND + i) : 0.0;
         double2 v[RR];
 #pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < NH; ++h) {
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
                 if (c == 0) {
@@ -889,9 +928,9 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
                         // x_1, this half's symbol rows, and z^0 for the half-1 update
                         l2_prefetch(x0 + cstride, xbytes);
                         if (SYM != 2)
-                            l2_prefetch((const char*)sym + (((int64_t)cc * 2 + h) * Q) * 3 * (SYM == 1 ? 8 : 16),
+                            l2_prefetch((const char*)sym + (((int64_t)cc * NH + h) * Q) * 3 * (SYM == 1 ? 8 : 16),
                                         (unsigned)Q * 3 * (SYM == 1 ? 8 : 16));
-                        if (h) {
+                        if (NH == 2 && h) {
                             l2_prefetch(z0, xbytes);
                             l2_prefetch(z0 + cstride, xbytes);
                         }
@@ -908,7 +947,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
                 } else {
                     const double2* src = x0 + cstride;
                     // x_1 is read again for half 1: keep it in L2 until then
-                    const uint64_t pol = h ? l2_policy_evict_first() : l2_policy_evict_last();
+                    const uint64_t pol = h == NH - 1 ? l2_policy_evict_first() : l2_policy_evict_last();
 #pragma unroll
                     for (int j = 0; j < RR; ++j) {
                         const int n = t + j * T;
@@ -928,8 +967,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
                 }
             }
             // 2 x 2 product; component 1 stays in registers
-            const int64_t sbase = ((int64_t)cc * 2 + h) * Q;
-            const double2 eh = cconj(__ldg(tw + ((2 * opaque(t) + h) << shP)));  // exp(+2 pi i (2t+h)/Pl)
+            const int64_t sbase = ((int64_t)cc * NH + h) * Q;
+            const double2 eh = cconj(__ldg(tw + ((NH * opaque(t) + h) << shP)));  // exp(+2 pi i (NH t+h)/Pl)
 #pragma unroll
             for (int j = 0; j < RR; ++j) {
                 const int k = t + j * T;
@@ -937,7 +976,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
                 U[0] = park[j * T + t];
                 U[1] = v[j];
                 if (SYM == 2) {
-                    const double2 e = tw32r<1>(j * (32 / RR), eh);  // exp(+2 pi i (2k+h)/Pl)
+                    const double2 e = tw32r<1>(j * (32 / RR), eh);  // exp(+2 pi i (NH k+h)/Pl)
                     double gxx = dsm[0], gyy = dsm[2 * (M + 1)], gxy = dsm[M + 1];
                     double2 em = e;
                     for (int m = 1; m <= M; ++m) {
@@ -961,7 +1000,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
 #pragma unroll
                     for (int j = 0; j < RR; ++j) v[j] = park[j * T + t];
                     __syncthreads();  // park free: fetch the next half's x_0 behind this transform
-                    if (h == 0) {
+                    if (h + 1 < NH) {
                         prefetch(x0, valid);
                     } else if (it + gridDim.x < nitems) {
                         bool ok;
@@ -972,7 +1011,14 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
                 reg_fft<LOGQ, kPipeLogR, 1, BlockBar, true>(v, t, xb, make_fft_tw<LOGQ, kPipeLogR>(opaque(t), tw, logTWN),
                                                             BlockBar{});
                 double2* dst = z0 + a * cstride;
-                if (h == 0) {
+                if (NH == 1) {
+                    const uint64_t pol = l2_policy_evict_first();
+#pragma unroll
+                    for (int j = 0; j < RR; ++j) {
+                        const int n = t + j * T;
+                        if (valid && n < Nl) st_hint(dst + n, v[j], pol);
+                    }
+                } else if (h == 0) {
                     const uint64_t pol = l2_policy_evict_last();  // z^0: re-read by this thread in half 1
 #pragma unroll
                     for (int j = 0; j < RR; ++j) {
@@ -996,7 +1042,9 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
 }
 
 // ------------------------------------------------------- K2 / K4 (3D) ---
-template <int LOGQ>
+// CIRC (periodic y, Py = Ny = 2Q): even/odd outputs by a decimation-in-
+// frequency stage (as in k_rfft_rows); K4 keeps all 2Q outputs.
+template <int LOGQ, bool CIRC>
 __global__ void __launch_bounds__(512) k_cfft_y_fwd(const double2* __restrict__ S1, double2* __restrict__ S2, int Ny,
                                                     int Nz, int Hx, int ZT, const double2* __restrict__ tw,
                                                     int logTWN) {
@@ -1021,6 +1069,10 @@ __global__ void __launch_bounds__(512) k_cfft_y_fwd(const double2* __restrict__ 
         const int n = t + j * T;
         double2 x = make_double2(0.0, 0.0);
         if (valid && n < Ny) x = src[n];
+        if (CIRC) {
+            const double2 x2 = valid ? src[n + Sh::Q] : make_double2(0.0, 0.0);
+            x = eo ? csub(x, x2) : cadd(x, x2);
+        }
         v[j] = eo ? cmul(x, __ldg(tw + (n << shP))) : x;
     }
     reg_fft<LOGQ, 4, -1>(v, t, xb, make_fft_tw<LOGQ, 4>(t, tw, logTWN), BlockBar{});
@@ -1033,7 +1085,7 @@ __global__ void __launch_bounds__(512) k_cfft_y_fwd(const double2* __restrict__ 
     }
 }
 
-template <int LOGQ>
+template <int LOGQ, bool CIRC>
 __global__ void __launch_bounds__(512) k_cfft_y_inv(const double2* __restrict__ S2, double2* __restrict__ S1, int Ny,
                                                     int Nz, int Hx, int ZT, const double2* __restrict__ tw,
                                                     int logTWN) {
@@ -1068,8 +1120,9 @@ __global__ void __launch_bounds__(512) k_cfft_y_inv(const double2* __restrict__ 
     __syncthreads();
     for (int idx = threadIdx.x; idx < nz * Ny; idx += blockDim.x) {
         const int z = idx / Ny, n = idx - z * Ny;
-        S1[(((int64_t)bd * Nz + z0 + z) * Hx + kx) * Ny + n] =
-            cadd(sm[2 * z * XB + spad(n)], sm[(2 * z + 1) * XB + spad(n)]);
+        const int m = n & (Sh::Q - 1);
+        const double2 e0 = sm[2 * z * XB + spad(m)], o1 = sm[(2 * z + 1) * XB + spad(m)];
+        S1[(((int64_t)bd * Nz + z0 + z) * Hx + kx) * Ny + n] = (CIRC && n >= Sh::Q) ? csub(e0, o1) : cadd(e0, o1);
     }
 }
 
@@ -1078,8 +1131,9 @@ __global__ void __launch_bounds__(512) k_cfft_y_inv(const double2* __restrict__ 
 // (convolution.hpp:107-116 embeds K at wrapped offsets and FFTs; the product
 // at :140-153 uses conj(G_hat)).  Exact rational phases via sincospi.
 // Output layout [col][h][k][pair], ky = 2k + h.
+#if defined(PDGPU_ALL_PARTS) || PDGPU_PART == 0
 __global__ void k_build_symbol(void* sym, const double* __restrict__ K, int dim, int M, int np, int64_t ss,
-                               int ncols, int Pl, int P0, int P1, int P2, int real, double scale) {
+                               int ncols, int Pl, int P0, int P1, int P2, int real, double scale, int NH) {
     const int64_t nfreq = (int64_t)ncols * Pl;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= nfreq) return;
@@ -1130,13 +1184,14 @@ __global__ void k_build_symbol(void* sym, const double* __restrict__ K, int dim,
                 }
             }
         }
-    const int Ql = Pl / 2;
-    const int64_t o = (((int64_t)col * 2 + (kl & 1)) * Ql + (kl >> 1)) * np;
+    const int Ql = Pl / NH;
+    const int64_t o = (((int64_t)col * NH + (kl % NH)) * Ql + kl / NH) * np;
     for (int p = 0; p < np; ++p) {
         if (real) ((double*)sym)[o + p] = acc[p].x * scale;
         else ((double2*)sym)[o + p] = make_double2(acc[p].x * scale, acc[p].y * scale);
     }
 }
+#endif
 
 // ------------------------------------------------------------------ host --
 static void check(cudaError_t e, const char* what) {
@@ -1147,45 +1202,22 @@ static void smem_attr(const void* fn) {
     check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448), "smem attr");
 }
 
-template <int L>
-static void set_attrs_l() {
-    smem_attr((const void*)k_rfft_rows<L>);
-    smem_attr((const void*)k_rfft_rows_pipe<L, 0>);
-    smem_attr((const void*)k_rfft_rows_pipe<L, 1>);
-    smem_attr((const void*)k_rfft_rows_pipe<L, 2>);
-    smem_attr((const void*)k_rfft_rows_pipe<L, 3>);
-    smem_attr((const void*)k_irfft_rows<L, 0>);
-    smem_attr((const void*)k_irfft_rows<L, 1>);
-    smem_attr((const void*)k_irfft_rows<L, 2>);
-    smem_attr((const void*)k_irfft_rows<L, 3>);
-    smem_attr((const void*)k_spectral2d_pipe<L, 0>);
-    smem_attr((const void*)k_spectral2d_pipe<L, 1>);
-    smem_attr((const void*)k_spectral2d_pipe<L, 2>);
-    smem_attr((const void*)k_spectral2d_duo<L, 0>);
-    smem_attr((const void*)k_spectral2d_duo<L, 1>);
-    smem_attr((const void*)k_spectral2d_duo<L, 2>);
-    if constexpr (L <= 9) {
-        smem_attr((const void*)k_spectral<L, 3, true, 3, true>);
-        smem_attr((const void*)k_spectral<L, 3, false, 3, true>);
-        smem_attr((const void*)k_spectral<L, 3, true, 3, true, true>);
-        smem_attr((const void*)k_cfft_y_fwd<L>);
-        smem_attr((const void*)k_cfft_y_inv<L>);
-    }
-}
 
-template <int... Ls>
-static void set_attrs_all(std::integer_sequence<int, Ls...>) {
-    (set_attrs_l<Ls + 1>(), ...);
-}
+// The host side is compiled in parts (PDGPU_PART = 0..4, one object file
+// each, built in parallel) so every translation unit instantiates only its
+// own kernel templates; without PDGPU_PART everything is compiled at once.
 
-void set_kernel_attributes() {
-    static bool done[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev < 64 && done[dev]) return;
-    set_attrs_all(std::make_integer_sequence<int, 12>{});
-    if (dev < 64) done[dev] = true;
-}
+void set_attrs_k1();
+void set_attrs_k5();
+void set_attrs_k3_2d();
+void set_attrs_3d();
+void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s);
+void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t s, double scale,
+               const uint8_t* cmask, const double* body);
+void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s);
+void launch_k2_3d(Engine& e, int batch, cudaStream_t s);
+void launch_k3_3d(Engine& e, double2* spec, int batch, cudaStream_t s);
+void launch_k4_3d(Engine& e, int batch, cudaStream_t s);
 
 // runtime log2 -> compile-time template dispatch over [1, 12]
 #define PDGPU_CASE(L, CALL) \
@@ -1206,6 +1238,297 @@ void set_kernel_attributes() {
         PDGPU_CASE(6, CALL) PDGPU_CASE(7, CALL) PDGPU_CASE(8, CALL) PDGPU_CASE(9, CALL)                     \
         default: throw std::runtime_error("3D transform length out of range");                              \
     }
+
+
+#if defined(PDGPU_ALL_PARTS) || PDGPU_PART == 1
+template <int L, bool C>
+static void set_attrs_k1_l() {
+    smem_attr((const void*)k_rfft_rows<L, C>);
+    smem_attr((const void*)k_rfft_rows_pipe<L, 0, C>);
+    smem_attr((const void*)k_rfft_rows_pipe<L, 1, C>);
+    smem_attr((const void*)k_rfft_rows_pipe<L, 2, C>);
+    smem_attr((const void*)k_rfft_rows_pipe<L, 3, C>);
+}
+template <int... Ls>
+static void set_attrs_k1_all(std::integer_sequence<int, Ls...>) {
+    (set_attrs_k1_l<Ls + 1, false>(), ...);
+    (set_attrs_k1_l<Ls + 1, true>(), ...);
+}
+void set_attrs_k1() { set_attrs_k1_all(std::make_integer_sequence<int, 12>{}); }
+
+void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
+    const Plan& pl = e.plan;
+    const int Nx = pl.N[0], Ny = pl.N[1], Nz = pl.N[2];
+    const int nslab = batch * pl.dim * Nz;
+    const int lqx = pl.logQx;
+    const bool cx = pl.circ[0] != 0;
+    int TR = pl.k1_rows;
+    const int T = threads_per_transform(lqx, 4);
+    const size_t rowlen = (size_t)(cx ? 4 : 2) << lqx;  // staged reals per row
+    auto smem_of = [&](int tr) { return sizeof(double2) * (size_t)2 * tr * xbuf_slots(lqx); };
+    auto psmem_of = [&](int tr) { return smem_of(tr) + sizeof(double) * (size_t)tr * rowlen; };
+    int PTR = TR;  // pipelined kernel: shrink the tile until the staging buffer fits
+    while (PTR > 1 && psmem_of(PTR) > 227 * 1024) PTR /= 2;
+    if ((Nx & 1) == 0 && psmem_of(PTR) <= 227 * 1024 && !getenv("PDGPU_NO_K1_PIPE")) {
+        const size_t psmem = psmem_of(PTR);
+        const int64_t ntiles = (int64_t)((Ny + PTR - 1) / PTR) * nslab;
+        // CTAs resident per SM (128 registers/thread under the 512-thread bound)
+        const int per_sm = std::max(1, std::min((int)(228 * 1024 / (psmem + 1024)), 65536 / (2 * PTR * T * 128)));
+        const unsigned pgrid = (unsigned)std::min<int64_t>(ntiles, (int64_t)e.num_sms * per_sm);
+        const int ltr = PTR == 8 ? 3 : PTR == 4 ? 2 : PTR == 2 ? 1 : 0;
+#define PDGPU_K1P(LT, C) k_rfft_rows_pipe<LQ, LT, C><<<pgrid, 2 * PTR * T, psmem, s>>>(u, e.d_S1, Nx, Ny, nslab, \
+                                                                                pl.Hx, e.d_tw, pl.logTWN)
+#define PDGPU_K1PC(C) (ltr == 3 ? PDGPU_K1P(3, C) : ltr == 2 ? PDGPU_K1P(2, C) : ltr == 1 ? PDGPU_K1P(1, C) \
+                                                                                 : PDGPU_K1P(0, C))
+        if (cx) PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K1PC(true))
+        else PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K1PC(false))
+#undef PDGPU_K1PC
+#undef PDGPU_K1P
+    } else {
+        dim3 grid((Ny + TR - 1) / TR, nslab);
+        const size_t smem = smem_of(TR);
+        if (cx)
+            PDGPU_DISPATCH_LOGQ(lqx, (k_rfft_rows<LQ, true><<<grid, 2 * TR * T, smem, s>>>(u, e.d_S1, Nx, Ny, pl.Hx, TR,
+                                                                                      e.d_tw, pl.logTWN)))
+        else
+            PDGPU_DISPATCH_LOGQ(lqx, (k_rfft_rows<LQ, false><<<grid, 2 * TR * T, smem, s>>>(u, e.d_S1, Nx, Ny, pl.Hx,
+                                                                                       TR, e.d_tw, pl.logTWN)))
+    }
+}
+#endif
+
+#if defined(PDGPU_ALL_PARTS) || PDGPU_PART == 2
+template <int L, bool C>
+static void set_attrs_k5_l() {
+    smem_attr((const void*)k_irfft_rows<L, 0, C>);
+    smem_attr((const void*)k_irfft_rows<L, 1, C>);
+    smem_attr((const void*)k_irfft_rows<L, 2, C>);
+    smem_attr((const void*)k_irfft_rows<L, 3, C>);
+}
+template <int... Ls>
+static void set_attrs_k5_all(std::integer_sequence<int, Ls...>) {
+    (set_attrs_k5_l<Ls + 1, false>(), ...);
+    (set_attrs_k5_l<Ls + 1, true>(), ...);
+}
+void set_attrs_k5() { set_attrs_k5_all(std::make_integer_sequence<int, 12>{}); }
+
+void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t s, double scale,
+               const uint8_t* cmask, const double* body) {
+    const Plan& pl = e.plan;
+    const int Nx = pl.N[0], Ny = pl.N[1], Nz = pl.N[2], d = pl.dim;
+    const int nslab = batch * d * Nz;
+    const int lqx = pl.logQx;
+    const bool cx = pl.circ[0] != 0;
+    // one row per CTA: two 256-thread CTAs co-reside per SM (measured
+    // faster than two rows per CTA or a persistent double-buffered variant)
+    int TR = 1;
+    if (const char* env = getenv("PDGPU_K5_ROWS")) TR = std::max(1, std::min(pl.k1_rows, atoi(env)));
+    while (TR & (TR - 1)) TR &= TR - 1;  // power of two (template)
+    const int ltr = TR == 8 ? 3 : TR == 4 ? 2 : TR == 2 ? 1 : 0;
+    const int T = threads_per_transform(lqx, 4);
+    dim3 grid((Ny + TR - 1) / TR, nslab);
+    const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_slots(lqx);
+#define PDGPU_K5(LT, C) k_irfft_rows<LQ, LT, C><<<grid, 2 * TR * T, smem, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx, e.d_tw, \
+                                                                          pl.logTWN, scale, cmask, body, pl.nodes)
+#define PDGPU_K5C(C) (ltr == 3 ? PDGPU_K5(3, C) : ltr == 2 ? PDGPU_K5(2, C) : ltr == 1 ? PDGPU_K5(1, C) : PDGPU_K5(0, C))
+    if (cx) PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(true))
+    else PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(false))
+#undef PDGPU_K5C
+#undef PDGPU_K5
+}
+#endif
+
+#if defined(PDGPU_ALL_PARTS) || PDGPU_PART == 3
+template <int L>
+static void set_attrs_k3_l() {
+    if constexpr (L >= 4) {
+        smem_attr((const void*)k_spectral2d_duo<L, 0, 1>);
+        smem_attr((const void*)k_spectral2d_duo<L, 1, 1>);
+        smem_attr((const void*)k_spectral2d_duo<L, 2, 1>);
+        smem_attr((const void*)k_spectral2d_duo<L, 0, 2>);
+        smem_attr((const void*)k_spectral2d_duo<L, 1, 2>);
+        smem_attr((const void*)k_spectral2d_duo<L, 2, 2>);
+    }
+    smem_attr((const void*)k_spectral2d_pipe<L, 0>);
+    smem_attr((const void*)k_spectral2d_pipe<L, 1>);
+    smem_attr((const void*)k_spectral2d_pipe<L, 2>);
+}
+template <int... Ls>
+static void set_attrs_k3_all(std::integer_sequence<int, Ls...>) {
+    (set_attrs_k3_l<Ls + 1>(), ...);
+}
+void set_attrs_k3_2d() { set_attrs_k3_all(std::make_integer_sequence<int, 12>{}); }
+
+#define PDGPU_DISPATCH_LOGQ_4_12(lq, CALL)                                                                  \
+    switch (lq) {                                                                                           \
+        PDGPU_CASE(4, CALL) PDGPU_CASE(5, CALL) PDGPU_CASE(6, CALL) PDGPU_CASE(7, CALL) PDGPU_CASE(8, CALL) \
+        PDGPU_CASE(9, CALL) PDGPU_CASE(10, CALL) PDGPU_CASE(11, CALL) PDGPU_CASE(12, CALL)                  \
+        default: throw std::runtime_error("transform length out of range");                                 \
+    }
+
+// 2D K3: out of place S1 -> S2 (padded: z^0 parked in S2)
+void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s) {
+    const Plan& pl = e.plan;
+    const int nh = pl.nh;
+    const int lq = pl.logPl - (nh == 2 ? 1 : 0);
+    // persistent, cp.async-pipelined variant: NC*(XB + 2Q) slots
+    const int Tp = threads_per_transform(lq, kPipeLogR);
+    const int mode = e.d_coltab ? 2 : (e.real_symbol ? 1 : 0);
+    const int ND = 3 * (e.M + 1);
+    const size_t per_col = sizeof(double2) * (size_t)(xbuf_slots(lq) + 2 * (1 << lq)) +
+                           (mode == 2 ? sizeof(double) * (size_t)ND : 0);
+    // two-CTA/SM split-exchange kernel (default) unless PDGPU_K3=pipe
+    // (the pipe variant handles padded columns only)
+    const char* k3env = getenv("PDGPU_K3");
+    if ((nh == 1 || !(k3env && std::string(k3env) == "pipe")) && lq >= 4) {
+        const int NCd = kPipeThreads / Tp;
+        const size_t dsmem = (size_t)NCd * (sizeof(double2) * (1 << lq) + sizeof(double) * xbuf_slots(lq) +
+                                            (mode == 2 ? sizeof(double) * ND : 0) + sizeof(uint64_t));
+        const int per_sm = std::max(1, std::min(2, (int)(228 * 1024 / (dsmem + 1024))));
+        const int64_t nitems = (int64_t)((pl.ncols + NCd - 1) / NCd) * batch;
+        const unsigned dgrid = (unsigned)std::min<int64_t>(nitems, (int64_t)e.num_sms * per_sm);
+#define DUO_ARGS spec, e.d_S2, e.d_sym, e.d_coltab, e.M, pl.ncols, pl.Nl, NCd, batch, e.d_tw, pl.logTWN
+#define DUO_NH(NHV)                                                                                           \
+    if (mode == 2)                                                                                            \
+        PDGPU_DISPATCH_LOGQ_4_12(lq, (k_spectral2d_duo<LQ, 2, NHV><<<dgrid, NCd * Tp, dsmem, s>>>(DUO_ARGS))) \
+    else if (mode == 1)                                                                                       \
+        PDGPU_DISPATCH_LOGQ_4_12(lq, (k_spectral2d_duo<LQ, 1, NHV><<<dgrid, NCd * Tp, dsmem, s>>>(DUO_ARGS))) \
+    else                                                                                                      \
+        PDGPU_DISPATCH_LOGQ_4_12(lq, (k_spectral2d_duo<LQ, 0, NHV><<<dgrid, NCd * Tp, dsmem, s>>>(DUO_ARGS)))
+        if (nh == 1) {
+            DUO_NH(1)
+        } else {
+            DUO_NH(2)
+        }
+#undef DUO_NH
+#undef DUO_ARGS
+    } else {
+        if (nh != 2) throw std::runtime_error("periodic column too short for the spectral kernel");
+        const int NCp = (int)std::max<size_t>(1, std::min<size_t>(kPipeThreads / Tp, 225 * 1024 / per_col));
+        const size_t psmem = per_col * NCp;
+        const int64_t nitems = (int64_t)((pl.ncols + NCp - 1) / NCp) * batch;
+        const unsigned pgrid = (unsigned)std::min<int64_t>(nitems, e.num_sms);
+#define PIPE_ARGS spec, e.d_S2, e.d_sym, e.d_coltab, e.M, pl.ncols, pl.Nl, NCp, batch, e.d_tw, pl.logTWN
+        if (mode == 2)
+            PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, 2><<<pgrid, NCp * Tp, psmem, s>>>(PIPE_ARGS)))
+        else if (mode == 1)
+            PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, 1><<<pgrid, NCp * Tp, psmem, s>>>(PIPE_ARGS)))
+        else
+            PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, 0><<<pgrid, NCp * Tp, psmem, s>>>(PIPE_ARGS)))
+#undef PIPE_ARGS
+    }
+}
+#endif
+
+#if defined(PDGPU_ALL_PARTS) || PDGPU_PART == 4
+template <int L, bool C>
+static void set_attrs_3d_l() {
+    smem_attr((const void*)k_cfft_y_fwd<L, C>);
+    smem_attr((const void*)k_cfft_y_inv<L, C>);
+    if constexpr (!C) {
+        smem_attr((const void*)k_spectral<L, 3, true, 3, true>);
+        smem_attr((const void*)k_spectral<L, 3, false, 3, true>);
+        smem_attr((const void*)k_spectral<L, 3, true, 3, true, true>);
+    } else {
+        smem_attr((const void*)k_spectral<L, 3, true, 3, false, false, 1>);
+        smem_attr((const void*)k_spectral<L, 3, false, 3, false, false, 1>);
+        smem_attr((const void*)k_spectral<L, 3, true, 3, false, true, 1>);
+    }
+}
+template <int... Ls>
+static void set_attrs_3d_all(std::integer_sequence<int, Ls...>) {
+    (set_attrs_3d_l<Ls + 1, false>(), ...);
+    (set_attrs_3d_l<Ls + 1, true>(), ...);
+}
+void set_attrs_3d() { set_attrs_3d_all(std::make_integer_sequence<int, 9>{}); }
+
+void launch_k2_3d(Engine& e, int batch, cudaStream_t s) {
+    const Plan& pl = e.plan;
+    const int Ny = pl.N[1], Nz = pl.N[2];
+    const int ZT = pl.k2_zt;
+    const int lq = pl.logP[1] - 1;
+    const int T = threads_per_transform(lq, 4);
+    dim3 grid((Nz + ZT - 1) / ZT, pl.Hx, batch * pl.dim);
+    const size_t smem = sizeof(double2) * (size_t)2 * ZT * xbuf_slots(lq);
+    if (pl.circ[1])
+        PDGPU_DISPATCH_LOGQ9(lq, (k_cfft_y_fwd<LQ, true><<<grid, 2 * ZT * T, smem, s>>>(e.d_S1, e.d_S2, Ny, Nz, pl.Hx,
+                                                                                    ZT, e.d_tw, pl.logTWN)))
+    else
+        PDGPU_DISPATCH_LOGQ9(lq, (k_cfft_y_fwd<LQ, false><<<grid, 2 * ZT * T, smem, s>>>(e.d_S1, e.d_S2, Ny, Nz, pl.Hx,
+                                                                                     ZT, e.d_tw, pl.logTWN)))
+}
+
+void launch_k4_3d(Engine& e, int batch, cudaStream_t s) {
+    const Plan& pl = e.plan;
+    const int Ny = pl.N[1], Nz = pl.N[2];
+    const int ZT = pl.k2_zt;
+    const int lq = pl.logP[1] - 1;
+    const int T = threads_per_transform(lq, 4);
+    dim3 grid((Nz + ZT - 1) / ZT, pl.Hx, batch * pl.dim);
+    const size_t smem = sizeof(double2) * (size_t)2 * ZT * xbuf_slots(lq);
+    if (pl.circ[1])
+        PDGPU_DISPATCH_LOGQ9(lq, (k_cfft_y_inv<LQ, true><<<grid, 2 * ZT * T, smem, s>>>(e.d_S2, e.d_S1, Ny, Nz, pl.Hx,
+                                                                                    ZT, e.d_tw, pl.logTWN)))
+    else
+        PDGPU_DISPATCH_LOGQ9(lq, (k_cfft_y_inv<LQ, false><<<grid, 2 * ZT * T, smem, s>>>(e.d_S2, e.d_S1, Ny, Nz, pl.Hx,
+                                                                                     ZT, e.d_tw, pl.logTWN)))
+}
+
+// 3D K3 in place on S2
+void launch_k3_3d(Engine& e, double2* spec, int batch, cudaStream_t s) {
+    const Plan& pl = e.plan;
+    const int d = pl.dim;
+    const int NC = pl.k3_cols;
+    const int nh = pl.nh;
+    const int lq = pl.logPl - (nh == 2 ? 1 : 0);
+    const int T = threads_per_transform(lq, 3);
+    dim3 grid(batch, (pl.ncols + NC - 1) / NC);
+    const bool zsmem = nh == 2;
+    const size_t smem = sizeof(double2) * (size_t)NC * (xbuf_slots(lq) + (zsmem ? 2 * d - 1 : d - 1) * (1 << lq));
+    const double* ct = e.d_coltab;
+    const int M = e.M, om = e.coltab_oddmask;
+    if (e.d_coltab) {
+        // per-column coefficient block in SMEM: shrink the column group to fit
+        const size_t per_col = smem / NC + sizeof(double) * 6 * (e.M + 1);
+        int NCs = NC;
+        while (NCs > 1 && per_col * NCs > 225 * 1024) NCs >>= 1;
+        dim3 sgrid(batch, (pl.ncols + NCs - 1) / NCs);
+        if (nh == 1)
+            PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, true, 3, false, true, 1><<<sgrid, NCs * T, per_col * NCs, s>>>(
+                                         spec, spec, e.d_sym, pl.ncols, pl.Nl, NCs, e.d_tw, pl.logTWN, ct, M, om)))
+        else
+            PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, true, 3, true, true><<<sgrid, NCs * T, per_col * NCs, s>>>(
+                                         spec, spec, e.d_sym, pl.ncols, pl.Nl, NCs, e.d_tw, pl.logTWN, ct, M, om)))
+    } else if (e.real_symbol) {
+        if (nh == 1)
+            PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, true, 3, false, false, 1><<<grid, NC * T, smem, s>>>(
+                                         spec, spec, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
+        else
+            PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, true, 3, true><<<grid, NC * T, smem, s>>>(
+                                         spec, spec, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
+    } else {
+        if (nh == 1)
+            PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, false, 3, false, false, 1><<<grid, NC * T, smem, s>>>(
+                                         spec, spec, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
+        else
+            PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, false, 3, true><<<grid, NC * T, smem, s>>>(
+                                         spec, spec, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
+    }
+}
+#endif
+
+#if defined(PDGPU_ALL_PARTS) || PDGPU_PART == 0
+void set_kernel_attributes() {
+    static bool done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && done[dev]) return;
+    set_attrs_k1();
+    set_attrs_k5();
+    set_attrs_k3_2d();
+    set_attrs_3d();
+    if (dev < 64) done[dev] = true;
+}
 
 void build_twiddles(Engine& e) {
     const int n = 1 << e.plan.logTWN;
@@ -1235,7 +1558,7 @@ void build_symbol(Engine& e) {
     const int th = 128;
     const int64_t blocks = (nfreq + th - 1) / th;
     k_build_symbol<<<(unsigned)blocks, th, 0, e.stream>>>(e.d_sym, e.d_K, e.dim, e.M, e.np, e.ss, pl.ncols, pl.Pl,
-                                                         pl.P[0], pl.P[1], pl.P[2], e.real_symbol ? 1 : 0, scale);
+                                                         pl.P[0], pl.P[1], pl.P[2], e.real_symbol ? 1 : 0, scale, pl.nh);
     check(cudaGetLastError(), "build_symbol launch");
     check(cudaStreamSynchronize(e.stream), "build_symbol");
 }
@@ -1256,144 +1579,38 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
     const Plan& pl = e.plan;
     engine_alloc_workspace(e, batch);
     const int d = pl.dim;
-    const int Nx = pl.N[0], Ny = pl.N[1], Nz = pl.N[2];
-    const int nslab = batch * d * Nz;
-    const int lqx = pl.logQx;
-    // K1
     {
         PassTimer pt(e, kPassK1, s);
-        const int TR = pl.k1_rows;
-        const int T = threads_per_transform(lqx, 4);
-        dim3 grid((Ny + TR - 1) / TR, nslab);
-        const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_slots(lqx);
-        const size_t psmem = smem + sizeof(double) * (size_t)TR * (2 << lqx);
-        if ((Nx & 1) == 0 && psmem <= 227 * 1024 && !getenv("PDGPU_NO_K1_PIPE")) {
-            const int64_t ntiles = (int64_t)((Ny + TR - 1) / TR) * nslab;
-            // CTAs resident per SM (128 registers/thread under the 512-thread bound)
-            const int per_sm = std::max(1, std::min((int)(228 * 1024 / (psmem + 1024)), 65536 / (2 * TR * T * 128)));
-            const unsigned pgrid = (unsigned)std::min<int64_t>(ntiles, (int64_t)e.num_sms * per_sm);
-            const int ltr = TR == 8 ? 3 : TR == 4 ? 2 : TR == 2 ? 1 : 0;
-#define PDGPU_K1P(LT) k_rfft_rows_pipe<LQ, LT><<<pgrid, 2 * TR * T, psmem, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, \
-                                                                               e.d_tw, pl.logTWN)
-            PDGPU_DISPATCH_LOGQ(lqx, (ltr == 3 ? PDGPU_K1P(3) : ltr == 2 ? PDGPU_K1P(2) : ltr == 1 ? PDGPU_K1P(1)
-                                                                                                   : PDGPU_K1P(0)));
-#undef PDGPU_K1P
-        } else {
-            PDGPU_DISPATCH_LOGQ(lqx, (k_rfft_rows<LQ><<<grid, 2 * TR * T, smem, s>>>(u, e.d_S1, Nx, Ny, pl.Hx, TR,
-                                                                                    e.d_tw, pl.logTWN)));
-        }
+        launch_k1(e, u, batch, s);
     }
     double2* spec = e.d_S1;
     if (d == 3) {
         PassTimer pt(e, kPassK2, s);
-        const int ZT = pl.k2_zt;
-        const int lq = pl.logP[1] - 1;
-        const int T = threads_per_transform(lq, 4);
-        dim3 grid((Nz + ZT - 1) / ZT, pl.Hx, batch * d);
-        const size_t smem = sizeof(double2) * (size_t)2 * ZT * xbuf_slots(lq);
-        PDGPU_DISPATCH_LOGQ9(lq, (k_cfft_y_fwd<LQ><<<grid, 2 * ZT * T, smem, s>>>(e.d_S1, e.d_S2, Ny, Nz, pl.Hx, ZT,
-                                                                                 e.d_tw, pl.logTWN)));
+        launch_k2_3d(e, batch, s);
         spec = e.d_S2;
     }
-    // K3: 2D out of place S1 -> S2 (z^0 parked in S2), 3D in place on S2
     double2* xin = e.d_S1;
     {
         PassTimer pt(e, kPassK3, s);
-        const int NC = pl.k3_cols;
-        const int lq = pl.logPl - 1;
-        const int logr = d == 3 ? 3 : 4;
-        const int T = threads_per_transform(lq, logr);
-        dim3 grid(batch, (pl.ncols + NC - 1) / NC);
-        const bool zsmem = pl.k3_halves == 2;
-        const size_t smem =
-            sizeof(double2) * (size_t)NC * (xbuf_slots(lq) + (zsmem ? 2 * d - 1 : d - 1) * (1 << lq));
         if (d == 2) {
-            // persistent, cp.async-pipelined variant: NC*(XB + 2Q) slots
-            const int Tp = threads_per_transform(lq, kPipeLogR);
-            const int mode = e.d_coltab ? 2 : (e.real_symbol ? 1 : 0);
-            const int ND = 3 * (e.M + 1);
-            const size_t per_col = sizeof(double2) * (size_t)(xbuf_slots(lq) + 2 * (1 << lq)) +
-                                   (mode == 2 ? sizeof(double) * (size_t)ND : 0);
-            // two-CTA/SM split-exchange kernel (default) unless PDGPU_K3=pipe
-            const char* k3env = getenv("PDGPU_K3");
-            if (!(k3env && std::string(k3env) == "pipe") && lq >= 4) {
-                const int NCd = kPipeThreads / Tp;
-                const size_t dsmem = (size_t)NCd * (sizeof(double2) * (1 << lq) + sizeof(double) * xbuf_slots(lq) +
-                                                    (mode == 2 ? sizeof(double) * ND : 0) + sizeof(uint64_t));
-                const int per_sm = std::max(1, std::min(2, (int)(228 * 1024 / (dsmem + 1024))));
-                const int64_t nitems = (int64_t)((pl.ncols + NCd - 1) / NCd) * batch;
-                const unsigned dgrid = (unsigned)std::min<int64_t>(nitems, (int64_t)e.num_sms * per_sm);
-#define DUO_ARGS spec, e.d_S2, e.d_sym, e.d_coltab, e.M, pl.ncols, pl.Nl, NCd, batch, e.d_tw, pl.logTWN
-                if (mode == 2)
-                    PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_duo<LQ, 2><<<dgrid, NCd * Tp, dsmem, s>>>(DUO_ARGS)))
-                else if (mode == 1)
-                    PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_duo<LQ, 1><<<dgrid, NCd * Tp, dsmem, s>>>(DUO_ARGS)))
-                else
-                    PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_duo<LQ, 0><<<dgrid, NCd * Tp, dsmem, s>>>(DUO_ARGS)))
-#undef DUO_ARGS
-                xin = e.d_S2;
-            } else {
-            const int NCp = (int)std::max<size_t>(1, std::min<size_t>(kPipeThreads / Tp, 225 * 1024 / per_col));
-            const size_t psmem = per_col * NCp;
-            const int64_t nitems = (int64_t)((pl.ncols + NCp - 1) / NCp) * batch;
-            const unsigned pgrid = (unsigned)std::min<int64_t>(nitems, e.num_sms);
-#define PIPE_ARGS spec, e.d_S2, e.d_sym, e.d_coltab, e.M, pl.ncols, pl.Nl, NCp, batch, e.d_tw, pl.logTWN
-            if (mode == 2)
-                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, 2><<<pgrid, NCp * Tp, psmem, s>>>(PIPE_ARGS)))
-            else if (mode == 1)
-                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, 1><<<pgrid, NCp * Tp, psmem, s>>>(PIPE_ARGS)))
-            else
-                PDGPU_DISPATCH_LOGQ(lq, (k_spectral2d_pipe<LQ, 0><<<pgrid, NCp * Tp, psmem, s>>>(PIPE_ARGS)))
-#undef PIPE_ARGS
+            launch_k3_2d(e, spec, batch, s);
             xin = e.d_S2;
-            }
         } else {
-            if (e.d_coltab) {
-                // per-column coefficient block in SMEM: shrink the column group to fit
-                const size_t per_col = smem / NC + sizeof(double) * 6 * (e.M + 1);
-                int NCs = NC;
-                while (NCs > 1 && per_col * NCs > 225 * 1024) NCs >>= 1;
-                dim3 sgrid(batch, (pl.ncols + NCs - 1) / NCs);
-                PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, true, 3, true, true><<<sgrid, NCs * T, per_col * NCs, s>>>(
-                                             spec, spec, e.d_sym, pl.ncols, pl.Nl, NCs, e.d_tw, pl.logTWN, e.d_coltab,
-                                             e.M, e.coltab_oddmask)))
-            } else if (e.real_symbol)
-                PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, true, 3, true><<<grid, NC * T, smem, s>>>(
-                                             spec, spec, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
-            else
-                PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, false, 3, true><<<grid, NC * T, smem, s>>>(
-                                             spec, spec, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
+            launch_k3_3d(e, spec, batch, s);
         }
     }
     if (d == 3) {
         PassTimer pt(e, kPassK4, s);
-        const int ZT = pl.k2_zt;
-        const int lq = pl.logP[1] - 1;
-        const int T = threads_per_transform(lq, 4);
-        dim3 grid((Nz + ZT - 1) / ZT, pl.Hx, batch * d);
-        const size_t smem = sizeof(double2) * (size_t)2 * ZT * xbuf_slots(lq);
-        PDGPU_DISPATCH_LOGQ9(lq, (k_cfft_y_inv<LQ><<<grid, 2 * ZT * T, smem, s>>>(e.d_S2, e.d_S1, Ny, Nz, pl.Hx, ZT,
-                                                                                 e.d_tw, pl.logTWN)));
+        launch_k4_3d(e, batch, s);
     }
-    // K5
+    // K5 (+ K6w, the periodic embedding's wrap correction)
     {
-        PassTimer pt(e, kPassK5, s);
-        // one row per CTA: two 256-thread CTAs co-reside per SM (measured
-        // faster than two rows per CTA or a persistent double-buffered variant)
-        int TR = 1;
-        if (const char* env = getenv("PDGPU_K5_ROWS")) TR = std::max(1, std::min(pl.k1_rows, atoi(env)));
-        while (TR & (TR - 1)) TR &= TR - 1;  // power of two (template)
-        const int ltr = TR == 8 ? 3 : TR == 4 ? 2 : TR == 2 ? 1 : 0;
-        const int T = threads_per_transform(lqx, 4);
-        dim3 grid((Ny + TR - 1) / TR, nslab);
-        const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_slots(lqx);
-#define PDGPU_K5(LT) k_irfft_rows<LQ, LT><<<grid, 2 * TR * T, smem, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx, e.d_tw, \
-                                                                        pl.logTWN, scale, cmask, body, pl.nodes)
-        PDGPU_DISPATCH_LOGQ(lqx, (ltr == 3 ? PDGPU_K5(3) : ltr == 2 ? PDGPU_K5(2) : ltr == 1 ? PDGPU_K5(1)
-                                                                                          : PDGPU_K5(0)));
-#undef PDGPU_K5
+        PassTimer pt(e, kPassK5, s, pl.circ_mask ? 2 : 1);
+        launch_k5(e, xin, f, batch, s, scale, cmask, body);
+        if (pl.circ_mask) launch_wrap_correction(e, u, f, batch, s, scale, cmask);
     }
     check(cudaGetLastError(), "fast_apply launch");
 }
+#endif
 
 }  // namespace pdgpu

@@ -194,6 +194,10 @@ class FastForce:
     def symbol_is_real(self) -> bool:
         return bool(self._lib.pdgpu_symbol_is_real(self._h))
 
+    def embedding(self) -> int:
+        """Bit d set: axis d uses the periodic embedding (P = N + wrap correction)."""
+        return int(self._lib.pdgpu_embedding(self._h))
+
     def symbol_mode(self) -> str:
         """'complex-table' | 'real-table' | 'separable' (per-column coefficients)."""
         return ("complex-table", "real-table", "separable")[self._lib.pdgpu_symbol_mode(self._h)]

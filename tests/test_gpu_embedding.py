@@ -1,0 +1,120 @@
+"""Periodic embedding (P = N + wrap correction, engine.h Plan) against the
+padded one (P = 2N, the reference's PadTransform, convolution.hpp:58-71) and
+against the CPU oracle.  Both must give the reference's linear correlation:
+relative L2 <= 1e-11 on every row, constrained ones included, for arbitrary
+(complex-symbol) stencils, the physical ones, mixed periodic/padded axes,
+the constraint-mask / body-force epilogue and CG."""
+import numpy as np
+import pytest
+
+from oracle.oracle import Oracle, Rng, random_field
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-11
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def make(o, embed, monkeypatch):
+    from paper_2301_11828_b200 import FastForce
+    if embed == "padded":
+        monkeypatch.setenv("PDGPU_EMBED", "padded")
+    else:
+        monkeypatch.delenv("PDGPU_EMBED", raising=False)
+    return FastForce(o.dims, o.M, o.kernel())
+
+
+@pytest.mark.parametrize("dims,M,bits", [((64, 64), 3, 3), ((64, 48), 3, 1), ((48, 64), 3, 2), ((16, 16), 3, 3),
+                                         ((32, 32, 32), 3, 7), ((32, 24, 16), 3, 5), ((24, 20, 12), 3, 0),
+                                         ((16, 16), 8, 0), ((32, 16), 8, 1)])
+def test_embedding_choice(dims, M, bits, monkeypatch):
+    o = Oracle(dims, h=1.0 / dims[0], delta=3.015 / dims[0], M=M)
+    assert make(o, "periodic", monkeypatch).embedding() == bits
+    assert make(o, "padded", monkeypatch).embedding() == 0
+
+
+@pytest.mark.parametrize("dims,M", [((64, 64), 3), ((32, 128), 2), ((128, 40), 4), ((40, 64), 3), ((16, 16), 7),
+                                    ((16, 16, 16), 3), ((32, 16, 16), 2), ((16, 24, 32), 3), ((32, 32, 12), 2)])
+def test_random_stencil_both_embeddings(dims, M, monkeypatch):
+    rng = Rng(91 + M)
+    o = Oracle(dims, h=0.5, M=M)
+    o.random_kernel(rng)
+    u = np.stack([random_field(rng, len(dims), o.n) for _ in range(2)])
+    want = np.stack([o.apply(u[i]) for i in range(2)])
+    fp = make(o, "periodic", monkeypatch)
+    assert fp.embedding() != 0
+    got_p = fp.apply(u)
+    got_z = make(o, "padded", monkeypatch).apply(u)
+    assert rel(got_p, want) <= TOL
+    assert rel(got_z, want) <= TOL
+    assert rel(got_p, got_z) <= TOL
+
+
+@pytest.mark.parametrize("dims", [(128, 128), (256, 64), (32, 32, 32)])
+def test_physical_corrected_matvec_with_bonds(dims, monkeypatch):
+    d = len(dims)
+    h = 1.0 / dims[0]
+    o = Oracle(dims, h=h, delta=3.015 * h, M=3)
+    ff = make(o, "periodic", monkeypatch)
+    assert ff.embedding() == (1 << d) - 1
+    o.random_ledger(Rng(5), 40)
+    ff.break_bonds(o.ledger_pairs())
+    u = random_field(Rng(1000 + d), d, o.n)
+    assert rel(ff.matvec(u), o.matvec(u)) <= TOL
+
+
+@pytest.mark.parametrize("dims", [(128, 128), (64, 32, 32)])
+def test_constrained_epilogue_and_cg(dims, monkeypatch):
+    """Constraint mask + body force in the K5 epilogue, then the wrap
+    correction must leave constrained rows at zero (timestepping.hpp:306-309);
+    CG (scale -1, masked operand) must meet the oracle's residual."""
+    torch = pytest.importorskip("torch")
+    d = len(dims)
+    h = 1.0 / dims[0]
+    dl = 3.015 * h
+    o = Oracle(dims, h=h, delta=dl, M=3)
+    ff = make(o, "periodic", monkeypatch)
+    ff.set_geometry(h, [0.0] * d, dl, 1.0)
+    ext = [dims[a] * h for a in range(d)]
+    for ax in range(d):
+        for side in (0, 1):
+            lo = [0.0] * d
+            hi = list(ext)
+            if side == 0:
+                hi[ax] = dl
+            else:
+                lo[ax] = ext[ax] - dl
+            o.add_constraint(lo, hi, (1 << d) - 1)
+            ff.add_constraint(lo, hi, (1 << d) - 1)
+    body = random_field(Rng(77), d, o.n)
+    o.set_body(body)
+    ff.set_body(body)
+    u = random_field(Rng(78), d, o.n)
+    ud = torch.tensor(u, device="cuda")
+    fd = torch.empty_like(ud)
+    ff.evaluate_force_device(ud, fd)
+    torch.cuda.synchronize()
+    f = fd.cpu().numpy()
+    want = o.evaluate_force(u)
+    assert rel(f, want) <= TOL
+    cm = o.regions()[1] if isinstance(o.regions(), tuple) else None
+    if cm is not None:
+        for a in range(d):
+            assert np.all(f[a][(cm >> a) & 1 == 1] == 0.0)
+    b = random_field(Rng(79), d, o.n)
+    x, it, relres, _ = ff.cg_solve(b, tol=1e-10, maxit=20000)
+    assert relres <= 1e-10
+    assert o.static_residual(b, x) <= 1.001e-10
+
+
+@pytest.mark.parametrize("dims", [(64, 64), (32, 32, 32)])
+def test_separable_symbol_periodic(dims, monkeypatch):
+    monkeypatch.setenv("PDGPU_SYMBOL", "separable")
+    h = 1.0 / dims[0]
+    o = Oracle(dims, h=h, delta=3.015 * h, M=3)
+    ff = make(o, "periodic", monkeypatch)
+    assert ff.symbol_mode() == "separable" and ff.embedding() == (1 << len(dims)) - 1
+    u = random_field(Rng(31), len(dims), o.n)
+    assert rel(ff.matvec(u), o.matvec(u)) <= TOL
