@@ -14,7 +14,7 @@ value   : DOF-matvecs/s over the timed steps, inputs resident in HBM
           (4.3 GB per step >> 126 MB L2: no flush needed).
 e2e     : the same metric through the public host API pdgpu_matvec_host
           (pinned host u in, host f out, copies inside the timed region).
-roofline: the dominant kernel (K3: y-FFT + symbol + inverse y-FFT),
+roofline: the dominant pass (largest share of the step; all three in per_pass),
           algorithmic bytes per launch / its mean CUDA-event duration.
 configs : secondary BASELINE numbers -- CG solve times (configs 1, 3, 4) and
           the 3D K.u rate (config 4, 128^3) -- skipped with --no-extra.
@@ -50,7 +50,7 @@ def workload_config(n_gpus: int):
     return {"workload": f"2D MSBFM K·u, {N_SIDE}x{N_SIDE} nodes, batch {BATCH} (BASELINE configs[1] top rung)",
             "grid": [N_SIDE, N_SIDE], "dof_per_node": DIM, "batch": BATCH, "delta_over_h": 3.015, "M": M,
             "E": 1.0, "thickness": 1.0, "corrections": "surface diagonal (12N-36 rows), no cracks",
-            "padding": "2N per axis (R2C half spectrum)", "l2": "inputs 4.3 GB per step > L2, no flush",
+            "embedding": "periodic P = N per axis + wrap correction (PDGPU_EMBED=padded: P = 2N)", "l2": "inputs 4.3 GB per step > L2, no flush",
             "parallelism": f"{n_gpus} ranks x own batch (replicas, no data-path collective)" if n_gpus > 1
             else "single GPU"}
 
@@ -124,18 +124,24 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def k3_algorithmic_bytes(n_side: int, batch: int):
-    """K3 per launch: read + write the half spectrum (Hx x Ny complex per
-    component per vector) + the real symbol once per launch (n_pairs x Hx x Py)."""
-    hx = n_side + 1          # Px/2 + 1 with Px = 2N
-    ny, py = n_side, 2 * n_side
-    return batch * DIM * hx * ny * 16 * 2 + 3 * hx * py * 8
-
-
-def matvec_algorithmic_bytes(n_side: int, batch: int):
-    """SURVEY.md 8(d) pass model: 80 B/DOF per vector + 48N B symbol per call."""
+def pass_algorithmic_bytes(n_side: int, batch: int, periodic: bool):
+    """Algorithmic HBM bytes per launch of each 2D pass (SURVEY.md 8(d) pass
+    model, with the transform geometry of the embedding in use):
+      K1: read u (8 B per node-component), write the half spectrum
+          (16 B x Hx x Ny per component);
+      K3: read + write the half spectrum, read the real symbol once per launch
+          (n_pairs x Hx x Py doubles);
+      K5: read the half spectrum, write f.
+    Padded (P = 2N, the reference's PadTransform): Hx = N + 1, Py = 2N --
+    80 B/DOF/vector + 48N B symbol.  Periodic (P = N): Hx = N/2 + 1, Py = N --
+    48 B/DOF/vector + 12N B symbol."""
     n = n_side * n_side
-    return batch * 80 * DIM * n + 48 * n
+    hx = (n_side // 2 + 1) if periodic else (n_side + 1)
+    py = n_side if periodic else 2 * n_side
+    spec = DIM * hx * n_side * 16
+    return {"K1_rfft_x": batch * (8 * DIM * n + spec),
+            "K3_spectral": batch * 2 * spec + 3 * hx * py * 8,
+            "K5_irfft_x": batch * (spec + 8 * DIM * n)}
 
 
 # ------------------------------------------------------------------ CPU leg --
@@ -439,31 +445,44 @@ def main():
     assert torch.isfinite(f).all().item(), "non-finite K.u"
 
     peak, peak_src = measured_peaks()
-    k3_ms, k3_n = passes.get("K3_spectral", (0.0, 0))
-    k3_bytes = k3_algorithmic_bytes(N_SIDE, BATCH)
-    k3_avg_s = (k3_ms / max(k3_n, 1)) * 1e-3
-    k3_gbs = k3_bytes / k3_avg_s / 1e9 if k3_avg_s > 0 else None
-    mv_bytes = matvec_algorithmic_bytes(N_SIDE, BATCH)
+    periodic = ff.embedding() == 3
+    pbytes = pass_algorithmic_bytes(N_SIDE, BATCH, periodic)
+    kernels = {"K1_rfft_x": "k_rfft_rows_pipe (K1: R2C along x, transposed store)",
+               "K3_spectral": "k_spectral2d_duo (K3: y-FFT + symbol + inverse y-FFT)",
+               "K5_irfft_x": "k_irfft_rows (K5: gather + C2R along x + epilogue)"}
+    per_pass = {}
+    for k in kernels:
+        ms_k, n_k = passes.get(k, (0.0, 0))
+        avg_s = (ms_k / max(n_k, 1)) * 1e-3
+        gbs = pbytes[k] / avg_s / 1e9 if avg_s > 0 else None
+        per_pass[k] = {"algorithmic_bytes_per_launch": pbytes[k], "mean_launch_ms": avg_s * 1e3,
+                       "achieved_gbs": gbs, "frac": (gbs / peak) if gbs else None}
+    # dominant kernel = the pass with the largest share of the step
+    dom = max(per_pass, key=lambda k: per_pass[k]["mean_launch_ms"])
+    mv_bytes = sum(pbytes.values())
     mv_gbs = mv_bytes / (ms_step * 1e-3) / 1e9
     traffic = None
-    tr_path = os.path.join(ROOT, "profiles", "k3_dram_bytes.json")
+    tr_path = os.path.join(ROOT, "profiles", "dram_bytes.json")
     if os.path.exists(tr_path):
         try:
             with open(tr_path) as fh:
                 tj = json.load(fh)
-            if tj.get("n") == N_SIDE and tj.get("batch") == BATCH:
-                traffic = tj.get("dram_bytes_per_launch")
+            if tj.get("n") == N_SIDE and tj.get("batch") == BATCH and tj.get("periodic") == periodic:
+                traffic = tj.get("dram_bytes_per_launch", {}).get(dom)
         except Exception:
             pass
-    roofline = {"bound": "hbm", "kernel": "k_spectral2d_duo (K3: y-FFT + symbol + inverse y-FFT)",
-                "achieved": k3_gbs, "peak": peak, "unit": "GB/s", "frac": (k3_gbs / peak) if k3_gbs else None,
-                "traffic": traffic, "algorithmic_bytes_per_launch": k3_bytes, "mean_launch_ms": k3_avg_s * 1e3,
-                "peak_source": peak_src,
+    pd = per_pass[dom]
+    roofline = {"bound": "hbm", "kernel": kernels[dom],
+                "achieved": pd["achieved_gbs"], "peak": peak, "unit": "GB/s", "frac": pd["frac"],
+                "traffic": traffic, "algorithmic_bytes_per_launch": pd["algorithmic_bytes_per_launch"],
+                "mean_launch_ms": pd["mean_launch_ms"], "peak_source": peak_src,
+                "embedding": "periodic (P = N + wrap correction)" if periodic else "padded (P = 2N)",
+                "per_pass": per_pass,
                 "matvec": {"algorithmic_bytes_per_step": mv_bytes, "achieved_gbs": mv_gbs, "frac": mv_gbs / peak,
-                           "model": "SURVEY 8(d): 80 B/DOF/vector + 48N B symbol"},
+                           "model": ("48 B/DOF/vector + 12N B symbol (periodic)" if periodic
+                                     else "SURVEY 8(d): 80 B/DOF/vector + 48N B symbol (padded)")},
                 "passes_ms_per_step": {k: v[0] / args.steps for k, v in passes.items()},
-                "symbol_mode": ff.symbol_mode(),
-                "note": "path is fp64-pipe bound on B200 (DESIGN.md sec.3); HBM fraction per the contract"}
+                "symbol_mode": ff.symbol_mode()}
 
     # comparison point: the same apply by direct stencil summation
     direct = None
