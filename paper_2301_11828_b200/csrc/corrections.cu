@@ -14,6 +14,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "engine.h"
 
@@ -122,9 +123,11 @@ static void check(cudaError_t e, const char* what) {
 // f_a[p] -= scale * sum_o sum_b K_ab(o) u_b[wrap(p+o)] on rows not
 // constrained in a (K5 has zeroed those).
 template <int D>
-__global__ void k_wrap(const double* __restrict__ u, double* __restrict__ f, const double* __restrict__ K,
-                       int M, int64_t ss, int N0, int N1, int N2, int circ_mask, const uint8_t* __restrict__ cmask,
-                       int64_t nodes, int batch, double scale, int64_t band0, int64_t band1, int64_t band2) {
+__global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, double* __restrict__ f,
+                                              const int* __restrict__ wrows, const int* __restrict__ wo0,
+                                              const double* __restrict__ wK, int M, int N0, int N1, int N2,
+                                              int circ_mask, const uint8_t* __restrict__ cmask, int64_t nodes,
+                                              int batch, double scale, int64_t band0, int64_t band1, int64_t band2) {
     constexpr int NP = D * (D + 1) / 2;
     const int64_t per_vec = band0 + band1 + band2;
     const int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -141,14 +144,16 @@ __global__ void k_wrap(const double* __restrict__ u, double* __restrict__ f, con
             ax = 2;
         }
     }
-    // mixed radix (x fastest), the band axis taking 2M values
+    // mixed radix over the two other axes (lower axis fastest), the band
+    // layer (2M values) slowest: a warp shares one depth, so one trip count
     int c[3];
+#pragma unroll
     for (int d = 0; d < 3; ++d) {
-        const int n = d == ax ? 2 * M : N[d];
-        c[d] = (int)(r % n);
-        r /= n;
+        if (d == ax) continue;
+        c[d] = (int)(r % N[d]);
+        r /= N[d];
     }
-    c[ax] = c[ax] < M ? c[ax] : N[ax] - 2 * M + c[ax];
+    c[ax] = (int)r < M ? (int)r : N[ax] - 2 * M + (int)r;
     for (int d = 0; d < ax; ++d)  // already covered by an earlier periodic axis
         if (((circ_mask >> d) & 1) && (c[d] < M || c[d] >= N[d] - M)) return;
     const int64_t p = ((int64_t)c[2] * N1 + c[1]) * N0 + c[0];
@@ -157,50 +162,107 @@ __global__ void k_wrap(const double* __restrict__ u, double* __restrict__ f, con
     double acc[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) acc[a] = 0.0;
-    const int side = 2 * M + 1;
+    // in-lattice o0 range of this node; entries outside it along x alias when x is periodic
+    const int lo0 = -c[0], hi0 = N0 - 1 - c[0];
+    const bool cx = circ_mask & 1;
+    auto add = [&](int e, int64_t q) {
+        double uq[D];
+#pragma unroll
+        for (int bb = 0; bb < D; ++bb) uq[bb] = ub[(int64_t)bb * nodes + q];
+        constexpr int KS = (NP + 1) & ~1;  // entry stride: 16-byte aligned pairs
+        double kv[KS];
+        const double2* ke = reinterpret_cast<const double2*>(wK + (int64_t)e * KS);
+#pragma unroll
+        for (int k = 0; k < KS / 2; ++k) {
+            const double2 v2 = __ldg(ke + k);
+            kv[2 * k] = v2.x;
+            kv[2 * k + 1] = v2.y;
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a)
+#pragma unroll
+            for (int bb = 0; bb < D; ++bb) acc[a] += kv[pair_idx<D>(a, bb)] * uq[bb];
+    };
     const int m2 = D == 3 ? M : 0;
+    const int side = 2 * M + 1;
     for (int o2 = -m2; o2 <= m2; ++o2) {
-        int w2 = c[2] + o2, out2 = 0;
+        int w2 = c[2] + o2;
+        bool out2 = false;
         if (D == 3 && (w2 < 0 || w2 >= N2)) {
             if (!((circ_mask >> 2) & 1)) continue;
             w2 = w2 < 0 ? w2 + N2 : w2 - N2;
-            out2 = 1;
+            out2 = true;
         }
         for (int o1 = -M; o1 <= M; ++o1) {
-            int w1 = c[1] + o1, out1 = out2;
+            int w1 = c[1] + o1;
+            bool out1 = out2;
             if (w1 < 0 || w1 >= N1) {
                 if (!((circ_mask >> 1) & 1)) continue;
                 w1 = w1 < 0 ? w1 + N1 : w1 - N1;
-                out1 = 1;
+                out1 = true;
             }
-            const int64_t srow = ((int64_t)(o2 + m2) * side + (o1 + M)) * side + M;
+            const int row = (o2 + m2) * side + (o1 + M);
+            const int e0 = __ldg(wrows + 2 * row), e1 = __ldg(wrows + 2 * row + 1);
             const int64_t qrow = ((int64_t)w2 * N1 + w1) * N0;
-            for (int o0 = -M; o0 <= M; ++o0) {
-                int w0 = c[0] + o0, out = out1;
-                if (w0 < 0 || w0 >= N0) {
-                    if (!(circ_mask & 1)) continue;
-                    w0 = w0 < 0 ? w0 + N0 : w0 - N0;
-                    out = 1;
+            if (out1) {  // every entry of the row aliases (x in range) or is dropped (x out, padded)
+                for (int e = e0; e < e1; ++e) {
+                    int w0 = c[0] + __ldg(wo0 + e);
+                    if (w0 < 0 || w0 >= N0) {
+                        if (!cx) continue;
+                        w0 = w0 < 0 ? w0 + N0 : w0 - N0;
+                    }
+                    add(e, qrow + w0);
                 }
-                if (!out) continue;
-                const int64_t si = srow + o0;
-                const int64_t q = qrow + w0;
-                double uq[D];
-#pragma unroll
-                for (int bb = 0; bb < D; ++bb) uq[bb] = ub[(int64_t)bb * nodes + q];
-#pragma unroll
-                for (int a = 0; a < D; ++a)
-#pragma unroll
-                    for (int bb = 0; bb < D; ++bb) acc[a] += __ldg(K + pair_idx<D>(a, bb) * ss + si) * uq[bb];
+            } else if (cx) {  // only the entries leaving along x
+                for (int e = e0; e < e1; ++e) {
+                    const int o0 = __ldg(wo0 + e);
+                    if (o0 >= lo0) break;
+                    add(e, qrow + c[0] + o0 + N0);
+                }
+                for (int e = e1 - 1; e >= e0; --e) {
+                    const int o0 = __ldg(wo0 + e);
+                    if (o0 <= hi0) break;
+                    add(e, qrow + c[0] + o0 - N0);
+                }
             }
         }
     }
-    (void)NP;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
         if ((cm >> a) & 1u) continue;
         f[((int64_t)b * D + a) * nodes + p] -= scale * acc[a];
     }
+}
+
+void build_wrap_table(Engine& e) {
+    const int dim = e.dim, M = e.M, side = 2 * M + 1, np = e.np;
+    const int nrows = dim == 3 ? side * side : side;
+    std::vector<int> rows(2 * (size_t)nrows), o0s;
+    std::vector<double> kv;
+    for (int row = 0; row < nrows; ++row) {
+        rows[2 * row] = (int)o0s.size();
+        for (int i0 = 0; i0 < side; ++i0) {
+            const int64_t si = (int64_t)row * side + i0;  // KernelStack storage: axis 0 fastest (kernel.hpp:50-54)
+            bool any = false;
+            for (int pp = 0; pp < np; ++pp) any = any || e.stencils[(size_t)(pp * e.ss + si)] != 0.0;
+            if (!any) continue;
+            o0s.push_back(i0 - M);
+            for (int pp = 0; pp < np; ++pp) kv.push_back(e.stencils[(size_t)(pp * e.ss + si)]);
+            if (np & 1) kv.push_back(0.0);  // entry stride (np + 1) & ~1 (k_wrap's double2 loads)
+        }
+        rows[2 * row + 1] = (int)o0s.size();
+    }
+    if (o0s.empty()) {
+        o0s.push_back(0);
+        for (int pp = 0; pp < ((np + 1) & ~1); ++pp) kv.push_back(0.0);
+    }
+    auto up = [](void** dst, const void* src, size_t bytes) {
+        check(cudaMalloc(dst, bytes), "alloc wrap table");
+        check(cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice), "copy wrap table");
+    };
+    up((void**)&e.d_wrows, rows.data(), sizeof(int) * rows.size());
+    up((void**)&e.d_wo0, o0s.data(), sizeof(int) * o0s.size());
+    up((void**)&e.d_wK, kv.data(), sizeof(double) * kv.size());
 }
 
 void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
@@ -215,14 +277,15 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
     }
     const int64_t tot = (band[0] + band[1] + band[2]) * batch;
     if (tot == 0) return;
+    if (!e.d_wrows) build_wrap_table(e);
     const int th = 128;
     const unsigned blocks = (unsigned)((tot + th - 1) / th);
     if (pl.dim == 2)
-        k_wrap<2><<<blocks, th, 0, s>>>(u, f, e.d_K, e.M, e.ss, pl.N[0], pl.N[1], pl.N[2], pl.circ_mask, cmask,
-                                        pl.nodes, batch, scale, band[0], band[1], band[2]);
+        k_wrap<2><<<blocks, th, 0, s>>>(u, f, e.d_wrows, e.d_wo0, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],
+                                        pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2]);
     else
-        k_wrap<3><<<blocks, th, 0, s>>>(u, f, e.d_K, e.M, e.ss, pl.N[0], pl.N[1], pl.N[2], pl.circ_mask, cmask,
-                                        pl.nodes, batch, scale, band[0], band[1], band[2]);
+        k_wrap<3><<<blocks, th, 0, s>>>(u, f, e.d_wrows, e.d_wo0, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],
+                                        pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2]);
 }
 
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale) {

@@ -74,6 +74,12 @@ struct Engine {
     double2* d_tw = nullptr;        // exp(-2 pi i k / TWN)
     void* d_sym = nullptr;          // symbol: real double or double2, np * ncols * Pl
     double* d_K = nullptr;          // stencils on device (np * ss), then koff[nof][np]
+    // wrap correction (periodic embedding): nonzero stencil entries grouped in
+    // (o2, o1) rows, o0 ascending -- d_wrows[2*row] = first entry, [2*row+1] =
+    // end; d_wo0[entry] = o0; d_wK[entry*np + pair] = K
+    int* d_wrows = nullptr;
+    int* d_wo0 = nullptr;
+    double* d_wK = nullptr;
     double* d_kc = nullptr;         // centre coefficients (3D direct stencil)
     double* d_coltab = nullptr;     // separable symbol: per column n_pairs x (M+1) coefficients (2D)
     int coltab_oddmask = 0;         // bit p: pair p odd along the column axis (sin terms)
@@ -190,6 +196,7 @@ void set_kernel_attributes();
 void launch_direct_apply(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale);
 
 // corrections.cu
+void build_wrap_table(Engine& e);
 void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
                             const uint8_t* cmask);
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s,

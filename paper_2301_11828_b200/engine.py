@@ -176,7 +176,7 @@ class FastForce:
     def footprint_bytes(self) -> int:
         return self._lib.pdgpu_footprint_bytes(self._h)
 
-    PASSES = ("K1_rfft_x", "K2_fft_y", "K3_spectral", "K4_ifft_y", "K5_irfft_x", "K6_surface", "K6_bonds", "vec")
+    PASSES = ("K1_rfft_x", "K2_fft_y", "K3_spectral", "K4_ifft_y", "K5_irfft_x", "K6_surface_wrap", "K6_bonds", "vec")
 
     def timing(self, on: bool = True):
         _check(self._lib.pdgpu_timing_enable(self._h, 1 if on else 0))
