@@ -175,6 +175,15 @@ int pdgpu_sim_init(pdgpu_t h, double dt, const double* v0);
 /* n_steps of Simulation::step (timestepping.hpp:209-241); s0 < 0 disables
  * fracture; watch as in update_bonds.  *broken = bonds broken in these steps. */
 int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64_t* broken);
+/* Simulation<Dim> with Integrator::Adr (AdrIntegrator, timestepping.hpp:79-145;
+ * adr_mass :150-162): the reference's quasi-static solver.  Same state and
+ * constraints as sim_init (v0 = 0); fixed_damping NaN = adaptive Rayleigh-
+ * quotient damping (SolverOptions::fixed_damping = std::nullopt).
+ * pdgpu_sim_step then advances ADR steps (the stretch test runs after each
+ * step when s0 >= 0, as in Simulation::step). */
+int pdgpu_sim_init_adr(pdgpu_t h, double dt, double fixed_damping);
+/* Simulation::adr_damping() (timestepping.hpp:271): damping c of the last step. */
+int pdgpu_sim_adr_damping(pdgpu_t h, double* c);
 /* Copies of the state (host, dim x N each, any may be NULL). */
 int pdgpu_sim_get(pdgpu_t h, double* u, double* v, double* f, double* t);
 

@@ -21,7 +21,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path = [p for p in sys.path if os.path.abspath(p or ".") != HERE]
 sys.path.insert(0, os.path.dirname(HERE))
-from oracle.oracle import RefProblem, Rng, _d, i64p, ip, rlib  # noqa: E402
+from oracle.oracle import Oracle, RefProblem, Rng, _d, i64p, ip, rlib  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(HERE), "tests", "golden")
 STEEL_E = 2e11
@@ -279,11 +279,54 @@ def gen_snapshots():
             subprocess.run(args, check=True, capture_output=True)
 
 
+def adr_problem(dims, ref=True):
+    """Quasi-static plate/cube for the reference's ADR solver (timestepping.hpp:79-162):
+    bottom layer clamped, a downward load on the top layer."""
+    dim = len(dims)
+    h = 1.0 / dims[0]
+    d = 3.015 * h
+    P = RefProblem(dims, h=h, delta=d, M=3, E=1.0, thickness=1.0) if ref else \
+        Oracle(dims, h=h, delta=d, M=3, E=1.0, thickness=1.0)
+    lo, hi = [0.0] * dim, [1.0] * dim
+    hi[dim - 1] = d
+    P.add_constraint(lo, hi, (1 << dim) - 1)
+    llo, lhi = [0.0] * dim, [1.0] * dim
+    llo[dim - 1] = 1.0 - d
+    val = [0.0] * dim
+    val[dim - 1] = -1e-3
+    P.add_load(llo, lhi, val)
+    if ref:
+        P.finalize()
+    return P
+
+
+ADR_CASES = (("p2", (64, 64), None, 300), ("p2_fixed", (64, 64), 0.05, 200), ("p3", (16, 16, 16), None, 100))
+
+
+def gen_adr():
+    """ADR trajectories (adaptive and fixed damping): u, v_half-driven damping
+    trace every 25 steps."""
+    out = {}
+    for tag, dims, fixed, steps in ADR_CASES:
+        r = adr_problem(dims)
+        r.sim_init_adr(1.0, fixed_damping=fixed)
+        trace = []
+        for k in range(steps // 25):
+            r.sim_step(25)
+            trace.append(r.adr_damping())
+        u, v, f, t = r.sim_get()
+        out.update({tag + "_u": u, tag + "_f": f, tag + "_t": np.array(t), tag + "_damping": np.array(trace)})
+    np.savez_compressed(os.path.join(OUT, "adr.npz"), **out)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
-    for fn in (gen_conv, gen_corrections, gen_acceptance, gen_configs, gen_seeds, gen_vv, gen_snapshots):
-        fn()
-        print("wrote", fn.__name__)
+    fns = {"conv": gen_conv, "corrections": gen_corrections, "acceptance": gen_acceptance, "configs": gen_configs,
+           "seeds": gen_seeds, "vv": gen_vv, "snapshots": gen_snapshots, "adr": gen_adr}
+    pick = sys.argv[1:] or list(fns)
+    for name in pick:
+        fns[name]()
+        print("wrote", name)
 
 
 if __name__ == "__main__":

@@ -206,6 +206,12 @@ typedef struct {
     idx_t step;
     int force_ready;
     int* sorted_off;    /* offsets sorted by linear displacement (partner order) */
+    /* ADR state (AdrIntegrator, timestepping.hpp:79-145) */
+    int integrator;     /* 0 velocity Verlet, 1 ADR */
+    double* vh;         /* staggered velocity v_half (dim x n) */
+    double mass[3];     /* adr_mass, timestepping.hpp:150-162 */
+    int fixed;          /* fixed_damping given */
+    double fixed_c, last_c;
 } orc_t;
 
 static void pos_of(const orc_t* P, const int* c, double* x) {
@@ -295,7 +301,7 @@ void orc_free(orc_t* P) {
     if (!P) return;
     free(P->offs); free(P->K); free(P->near_surface); free(P->cmask); free(P->De);
     free(P->ledger); free(P->body); free(P->sorted_off);
-    free(P->u); free(P->v); free(P->f); free(P->f_prev);
+    free(P->u); free(P->v); free(P->f); free(P->f_prev); free(P->vh);
     free(P);
 }
 
@@ -894,7 +900,90 @@ void orc_sim_init(orc_t* P, double dt) {
     P->dt = dt;
     P->step = 0;
     P->force_ready = 0;
+    P->integrator = 0;
     enforce_constraints(P);
+}
+
+/* Simulation<Dim> with Integrator::Adr: adr_mass (timestepping.hpp:150-162)
+ * over the in-band offsets in for_each_offset order (kernel.hpp:71-89);
+ * fixed_damping NaN = adaptive (std::nullopt). */
+void orc_sim_init_adr(orc_t* P, double dt, double fixed_damping) {
+    orc_sim_init(P, dt);
+    free(P->vh);
+    P->vh = (double*)calloc((size_t)(P->dim * P->n), sizeof(double));
+    P->integrator = 1;
+    P->fixed = fixed_damping == fixed_damping;
+    P->fixed_c = P->fixed ? fixed_damping : 0.0;
+    P->last_c = 0.0;
+    const int side = 2 * P->M + 1;
+    for (int a = 0; a < P->dim; ++a) {
+        double row = 0.0;
+        for (int b = 0; b < P->dim; ++b) {
+            double off_abs = 0.0;
+            const int pr = orc_pair_index(P->dim, a, b);
+            for (int k = 0; k < P->nof; ++k) {
+                const int* o = &P->offs[3 * k];
+                idx_t si = 0;
+                for (int d = P->dim - 1; d >= 0; --d) si = si * side + (o[d] + P->M);
+                off_abs += fabs(P->K[pr * P->ss + si]);
+            }
+            row += 2.0 * off_abs;
+        }
+        P->mass[a] = 0.25 * dt * dt * row;
+    }
+}
+
+double orc_sim_adr_damping(const orc_t* P) { return P->last_c; }
+void orc_sim_adr_mass(const orc_t* P, double* m) { for (int a = 0; a < P->dim; ++a) m[a] = P->mass[a]; }
+
+/* AdrIntegrator::advance + estimate_damping, timestepping.hpp:86-139 */
+static void adr_advance(orc_t* P) {
+    const idx_t n = P->n;
+    const double dt = P->dt;
+    if (P->step == 0) {
+        for (int a = 0; a < P->dim; ++a) {
+            const double inv_m = 1.0 / P->mass[a];
+            for (idx_t p = 0; p < n; ++p) {
+                if ((P->cmask[p] >> a) & 1u) continue;
+                P->vh[a * n + p] = 0.5 * dt * P->f[a * n + p] * inv_m;
+            }
+        }
+    } else {
+        double c;
+        if (P->fixed) {
+            c = P->fixed_c;
+        } else {
+            double num = 0.0, den = 0.0;
+            for (int a = 0; a < P->dim; ++a)
+                for (idx_t p = 0; p < n; ++p) {
+                    if ((P->cmask[p] >> a) & 1u) continue;
+                    const double up = P->u[a * n + p], vh = P->vh[a * n + p];
+                    double k = 0.0;
+                    if (vh != 0.0) k = -(P->f[a * n + p] - P->f_prev[a * n + p]) / (P->mass[a] * dt * vh);
+                    if (k > 0.0) num += up * up * k;
+                    den += up * up;
+                }
+            if (den <= 0.0 || num <= 0.0) c = 0.0;
+            else {
+                c = 2.0 * sqrt(num / den);
+                if (1.9 / dt < c) c = 1.9 / dt;
+            }
+        }
+        P->last_c = c;
+        const double lead = 2.0 - c * dt, trail = 1.0 / (2.0 + c * dt);
+        for (int a = 0; a < P->dim; ++a) {
+            const double inv_m = 1.0 / P->mass[a];
+            for (idx_t p = 0; p < n; ++p) {
+                if ((P->cmask[p] >> a) & 1u) continue;
+                P->vh[a * n + p] = (lead * P->vh[a * n + p] + 2.0 * dt * P->f[a * n + p] * inv_m) * trail;
+            }
+        }
+    }
+    for (int a = 0; a < P->dim; ++a)
+        for (idx_t p = 0; p < n; ++p) {
+            if ((P->cmask[p] >> a) & 1u) continue;
+            P->u[a * n + p] += dt * P->vh[a * n + p];
+        }
 }
 
 void orc_sim_set_velocity(orc_t* P, const double* v) {
@@ -908,6 +997,17 @@ idx_t orc_sim_step(orc_t* P, double s0, const double* watch) {
     const int dim = P->dim;
     const double dt = P->dt, inv_rho = 1.0 / P->rho;
     if (!P->force_ready) { orc_evaluate_force(P, P->u, P->f); P->force_ready = 1; }
+    if (P->integrator == 1) {  /* ADR branch, timestepping.hpp:215-220 */
+        adr_advance(P);
+        P->t += dt;
+        enforce_constraints(P);
+        double* tmp = P->f_prev; P->f_prev = P->f; P->f = tmp;
+        orc_evaluate_force(P, P->u, P->f);
+        idx_t nb = 0;
+        if (s0 >= 0.0) nb = orc_update_bonds(P, P->u, s0, watch, NULL, 0);
+        P->step++;
+        return nb;
+    }
     for (int a = 0; a < dim; ++a)   /* vv_drift :312-322 */
         for (idx_t p = 0; p < n; ++p) {
             if ((P->cmask[p] >> a) & 1u) continue;

@@ -88,6 +88,9 @@ def olib():
             "orc_seed_notch": (C.c_int64, [C.c_void_p, dp]),
             "orc_sim_init": (None, [C.c_void_p, C.c_double]),
             "orc_sim_set_velocity": (None, [C.c_void_p, dp]),
+            "orc_sim_init_adr": (None, [C.c_void_p, C.c_double, C.c_double]),
+            "orc_sim_adr_damping": (C.c_double, [C.c_void_p]),
+            "orc_sim_adr_mass": (None, [C.c_void_p, dp]),
             "orc_sim_step": (C.c_int64, [C.c_void_p, C.c_double, dp]),
             "orc_sim_get": (None, [C.c_void_p, dp, dp, dp, dp]),
         }
@@ -134,6 +137,8 @@ def rlib():
             "ref_cg": (C.c_int, [C.c_void_p, dp, dp, C.c_double, C.c_int, ip, dp, dp, C.c_int]),
             "ref_sim_init": (C.c_int, [C.c_void_p, C.c_double, C.c_double, dp]),
             "ref_sim_step": (C.c_int64, [C.c_void_p, C.c_int]),
+            "ref_sim_init_adr": (C.c_int, [C.c_void_p, C.c_double, C.c_double, dp, C.c_double]),
+            "ref_sim_adr_damping": (C.c_double, [C.c_void_p]),
             "ref_sim_get": (None, [C.c_void_p, dp, dp, dp, dp]),
             "ref_bench": (C.c_double, [C.c_void_p, dp, C.c_int64, C.c_int]),
             "ref_random_kernel": (None, [C.c_void_p, C.c_int, C.c_int, C.c_double, dp]),
@@ -293,6 +298,18 @@ class Oracle:
         if v0 is not None:
             self.L.orc_sim_set_velocity(self.h, _d(_f64(v0)))
 
+    def sim_init_adr(self, dt, fixed_damping=None):
+        """Simulation with Integrator::Adr (timestepping.hpp:79-162)."""
+        self.L.orc_sim_init_adr(self.h, dt, float("nan") if fixed_damping is None else float(fixed_damping))
+
+    def adr_damping(self):
+        return self.L.orc_sim_adr_damping(self.h)
+
+    def adr_mass(self):
+        m = np.zeros(3)
+        self.L.orc_sim_adr_mass(self.h, _d(m))
+        return m[: self.dim]
+
     def sim_step(self, n=1, s0=-1.0, watch=None):
         w = None if watch is None else _box6(watch, self.dim)
         tot = 0
@@ -419,6 +436,14 @@ class RefProblem:
     def sim_init(self, dt, s0=-1.0, watch=None):
         w = None if watch is None else _f64(np.concatenate([watch[0], watch[1]]))
         self.L.ref_sim_init(self.h, dt, s0, None if w is None else _d(w))
+
+    def sim_init_adr(self, dt, s0=-1.0, watch=None, fixed_damping=None):
+        w = None if watch is None else _box6(watch, self.dim)
+        self.L.ref_sim_init_adr(self.h, dt, s0, None if w is None else _d(w),
+                                float("nan") if fixed_damping is None else float(fixed_damping))
+
+    def adr_damping(self):
+        return self.L.ref_sim_adr_damping(self.h)
 
     def sim_step(self, n=1):
         return self.L.ref_sim_step(self.h, n)

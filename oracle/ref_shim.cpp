@@ -454,6 +454,41 @@ int ref_sim_init(void* vp, double dt, double s0, const double* watch) {
     return 0;
 }
 
+// Simulation with Integrator::Adr (timestepping.hpp:79-162); fixed NaN = adaptive damping
+int ref_sim_init_adr(void* vp, double dt, double s0, const double* watch, double fixed) {
+    auto* P = static_cast<RefProblem*>(vp);
+    auto run = [&](auto* B, auto dimc) {
+        constexpr int Dim = decltype(dimc)::value;
+        Problem<Dim> prob;
+        prob.grid = B->grid;
+        prob.horizon = B->hz;
+        prob.material = B->mat;
+        prob.constraints = B->constraints;
+        prob.loads = B->loads;
+        prob.cracks = B->cracks;
+        if (s0 >= 0) prob.s0 = s0;
+        if (watch) {
+            Box<Dim> b;
+            for (int d = 0; d < Dim; ++d) {
+                b.lo[d] = watch[d];
+                b.hi[d] = watch[Dim + d];
+            }
+            prob.watch = b;
+        }
+        std::optional<double> fd;
+        if (fixed == fixed) fd = fixed;
+        B->sim = std::make_unique<Simulation<Dim>>(prob, SolverOptions{Method::Fast, Integrator::Adr, dt, fd});
+    };
+    if (P->dim == 2) run(get<2>(P), std::integral_constant<int, 2>{});
+    else run(get<3>(P), std::integral_constant<int, 3>{});
+    return 0;
+}
+
+double ref_sim_adr_damping(void* vp) {
+    auto* P = static_cast<RefProblem*>(vp);
+    return P->dim == 2 ? get<2>(P)->sim->adr_damping() : get<3>(P)->sim->adr_damping();
+}
+
 int64_t ref_sim_step(void* vp, int n) {
     auto* P = static_cast<RefProblem*>(vp);
     int64_t nb = 0;

@@ -63,6 +63,8 @@ SIGNATURES = {
                                       c_double_p, C.c_int]),
     "pdgpu_sim_init": (C.c_int, [C.c_void_p, C.c_double, c_double_p]),
     "pdgpu_sim_step": (C.c_int, [C.c_void_p, C.c_int, C.c_double, c_double_p, c_int64_p]),
+    "pdgpu_sim_init_adr": (C.c_int, [C.c_void_p, C.c_double, C.c_double]),
+    "pdgpu_sim_adr_damping": (C.c_int, [C.c_void_p, c_double_p]),
     "pdgpu_sim_get": (C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p, c_double_p]),
     "pdgpu_timing_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "pdgpu_timing_read": (C.c_int, [C.c_void_p, c_double_p, c_int64_p, C.c_int]),

@@ -481,7 +481,7 @@ void pdgpu_destroy(pdgpu_t h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    void* ptrs[] = {h->d_wrows, h->d_wo0, h->d_wK, h->d_tw, h->d_sym, h->d_K, h->d_offs, h->d_disp, h->d_S1, h->d_S2, h->d_u_stage, h->d_f_stage,
+    void* ptrs[] = {h->d_vh, h->d_wrows, h->d_wo0, h->d_wK, h->d_tw, h->d_sym, h->d_K, h->d_offs, h->d_disp, h->d_S1, h->d_S2, h->d_u_stage, h->d_f_stage,
                     h->d_cmask, h->d_surf_rows, h->d_surf_de, h->d_ledger, h->d_bond_rows, h->d_listed,
                     h->d_counters, h->d_new_pairs, h->d_body, h->d_cdofs, h->d_cval, h->d_ckind, h->d_u, h->d_v,
                     h->d_f, h->d_fprev, h->d_red, h->d_scal, h->d_ticket, h->d_cg, h->d_coltab,
@@ -1100,8 +1100,46 @@ int pdgpu_sim_init(pdgpu_t h, double dt, const double* v0) {
         h->t = 0.0;
         h->step = 0;
         h->force_ready = false;
+        h->integrator = 0;
         launch_enforce(h->d_u, h->d_v, h->d_cdofs, h->d_cval, h->d_ckind, h->n_cdofs, 0.0, h->stream);
         cuda_check(cudaStreamSynchronize(h->stream), "sim init");
+    });
+}
+
+int pdgpu_sim_init_adr(pdgpu_t h, double dt, double fixed_damping) {
+    const int rc = pdgpu_sim_init(h, dt, nullptr);
+    if (rc != PDGPU_OK) return rc;
+    return guarded([&] {
+        Engine& e = *h;
+        const int64_t m = (int64_t)e.dim * e.plan.nodes;
+        dalloc(e.d_vh, (size_t)m, "alloc v_half");
+        cuda_check(cudaMemset(e.d_vh, 0, sizeof(double) * m), "zero v_half");
+        // adr_mass (timestepping.hpp:150-162): 1/4 dt^2 sum_b 2 sum_off |K_ab(off)|,
+        // offsets in for_each_offset order (kernel.hpp:71-89)
+        for (int a = 0; a < e.dim; ++a) {
+            double row = 0.0;
+            for (int b = 0; b < e.dim; ++b) {
+                double off_abs = 0.0;
+                const int pr = assembly::pair_index(e.dim, a, b);
+                for (int k = 0; k < e.nof; ++k)
+                    off_abs += fabs(e.stencils[(size_t)(pr * e.ss + assembly::stencil_index(e.dim, e.M, &e.offs[3 * k]))]);
+                row += 2.0 * off_abs;
+            }
+            e.adr_mass[a] = 0.25 * dt * dt * row;
+        }
+        e.integrator = 1;
+        e.adr_fixed = fixed_damping == fixed_damping;  // NaN: adaptive (std::nullopt)
+        e.adr_fixed_c = e.adr_fixed ? fixed_damping : 0.0;
+        cuda_check(cudaMemset(e.d_scal + 8, 0, sizeof(double)), "zero damping");
+    });
+}
+
+int pdgpu_sim_adr_damping(pdgpu_t h, double* c) {
+    return guarded([&] {
+        if (!h || !c) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        cuda_check(cudaStreamSynchronize(h->stream), "sync");
+        cuda_check(cudaMemcpy(c, h->d_scal + 8, sizeof(double), cudaMemcpyDeviceToHost), "damping");
     });
 }
 
@@ -1121,6 +1159,16 @@ int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64
             if (!e.force_ready) {
                 evaluate_force_impl(e, e.d_u, e.d_f, e.stream);
                 e.force_ready = true;
+            }
+            if (e.integrator == 1) {  // ADR branch (timestepping.hpp:215-220)
+                launch_adr_step(e, e.step == 0, e.stream);
+                e.t += e.dt;
+                launch_enforce(e.d_u, e.d_v, e.d_cdofs, e.d_cval, e.d_ckind, e.n_cdofs, e.t, e.stream);
+                std::swap(e.d_f, e.d_fprev);
+                evaluate_force_impl(e, e.d_u, e.d_f, e.stream);
+                if (s0 >= 0) launch_update_bonds(e, e.d_u, s0, watch, e.stream, /*sync=*/false);
+                ++e.step;
+                continue;
             }
             launch_vv_drift(e.d_u, e.d_v, e.d_f, e.d_cmask, N, e.dim, e.dt, inv_rho, e.stream);
             e.t += e.dt;

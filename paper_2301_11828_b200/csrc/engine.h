@@ -124,6 +124,11 @@ struct Engine {
     int64_t n_cdofs = 0;
     double *d_u = nullptr, *d_v = nullptr, *d_f = nullptr, *d_fprev = nullptr;
     double t = 0.0, dt = 0.0;
+    int integrator = 0;                  // 0 velocity Verlet, 1 ADR (SolverOptions, timestepping.hpp:53)
+    double* d_vh = nullptr;              // ADR staggered velocity v_half
+    double adr_mass[3] = {1.0, 1.0, 1.0};  // adr_mass (timestepping.hpp:150-162)
+    bool adr_fixed = false;
+    double adr_fixed_c = 0.0;
     int64_t step = 0;
     bool force_ready = false;
     bool any_cmask = false;              // constraint mask set directly (set_regions)
@@ -218,6 +223,7 @@ void launch_vv_drift(double* u, const double* v, const double* f, const uint8_t*
                      int dim, double dt, double inv_rho, cudaStream_t s);
 void launch_vv_kick(double* v, const double* fprev, const double* f, const uint8_t* cmask,
                     int64_t N, int dim, double dt, double inv_rho, cudaStream_t s);
+void launch_adr_step(Engine& e, bool first, cudaStream_t s);
 void launch_enforce(double* u, double* v, const long long* dofs, const double* val, const int* kind,
                     int64_t n, double t, cudaStream_t s);
 void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s);

@@ -194,6 +194,92 @@ __global__ void k_vv_kick(double* v, const double* fprev, const double* f, const
     v[i] = __dadd_rn(v[i], t);
 }
 
+// ------------------------------------------------------------------ ADR --
+// AdrIntegrator (timestepping.hpp:79-145).  Damping estimate: num = sum u^2 k
+// (k > 0), den = sum u^2 over unconstrained DOFs, k = -(f - f_prev) /
+// (m_a dt v_half); deterministic two-value grid reduction (fixed grid, the
+// last block sums the partials in index order) that leaves c in *cout.
+__global__ void k_adr_damping(const double* __restrict__ u, const double* __restrict__ vh,
+                              const double* __restrict__ f, const double* __restrict__ fprev,
+                              const uint8_t* __restrict__ cmask, int64_t N, int dim, double m0, double m1, double m2,
+                              double dt, double* partial, unsigned int* ticket, double* cout) {
+    __shared__ double ws[2][32];
+    __shared__ bool last;
+    double num = 0.0, den = 0.0;
+    const int64_t tot = N * dim;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int a = (int)(i / N);
+        const int64_t p = i - (int64_t)a * N;
+        if ((cmask[p] >> a) & 1u) continue;
+        const double m = a == 0 ? m0 : (a == 1 ? m1 : m2);
+        const double up = u[i], v = vh[i];
+        double k = 0.0;
+        if (v != 0.0) k = -__ddiv_rn(__dadd_rn(f[i], -fprev[i]), __dmul_rn(__dmul_rn(m, dt), v));
+        const double u2 = __dmul_rn(up, up);
+        if (k > 0.0) num = __dadd_rn(num, __dmul_rn(u2, k));
+        den = __dadd_rn(den, u2);
+    }
+    num = warp_sum(num);
+    den = warp_sum(den);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) {
+        ws[0][wid] = num;
+        ws[1][wid] = den;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        double a = lane < (int)(blockDim.x >> 5) ? ws[0][lane] : 0.0;
+        double b = lane < (int)(blockDim.x >> 5) ? ws[1][lane] : 0.0;
+        a = warp_sum(a);
+        b = warp_sum(b);
+        if (lane == 0) {
+            partial[2 * blockIdx.x] = a;
+            partial[2 * blockIdx.x + 1] = b;
+            __threadfence();
+            last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        }
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double sn = 0.0, sd = 0.0;
+        for (int i = 0; i < (int)gridDim.x; ++i) {
+            sn += ((volatile double*)partial)[2 * i];
+            sd += ((volatile double*)partial)[2 * i + 1];
+        }
+        double c = 0.0;
+        if (!(sd <= 0.0 || sn <= 0.0)) c = fmin(2.0 * sqrt(sn / sd), 1.9 / dt);
+        *cout = c;
+        *ticket = 0u;
+    }
+}
+
+// first call: v_half = 0.5 dt f / m (unconstrained); else v_half = (lead v_half
+// + 2 dt f / m) * trail with c from *cdev (or the fixed damping); then u += dt v_half
+__global__ void k_adr_advance(double* __restrict__ u, double* __restrict__ vh, const double* __restrict__ f,
+                              const uint8_t* __restrict__ cmask, int64_t N, int dim, double m0, double m1, double m2,
+                              double dt, int first, const double* __restrict__ cdev) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N * dim) return;
+    const int a = (int)(i / N);
+    const int64_t p = i - (int64_t)a * N;
+    if ((cmask[p] >> a) & 1u) return;
+    const double inv_m = __ddiv_rn(1.0, a == 0 ? m0 : (a == 1 ? m1 : m2));
+    double v;
+    if (first) {
+        v = __dmul_rn(__dmul_rn(__dmul_rn(0.5, dt), f[i]), inv_m);
+    } else {
+        const double c = *cdev;
+        const double lead = __dadd_rn(2.0, -__dmul_rn(c, dt));
+        const double trail = __ddiv_rn(1.0, __dadd_rn(2.0, __dmul_rn(c, dt)));
+        v = __dmul_rn(__dadd_rn(__dmul_rn(lead, vh[i]), __dmul_rn(__dmul_rn(__dmul_rn(2.0, dt), f[i]), inv_m)), trail);
+    }
+    vh[i] = v;
+    u[i] = __dadd_rn(u[i], __dmul_rn(dt, v));
+}
+
+__global__ void k_set_scalar(double* dst, double v) { *dst = v; }
+
 __global__ void k_enforce(double* u, double* v, const long long* dofs, const double* val, const int* kind, int64_t n,
                           double t) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -266,6 +352,24 @@ void launch_vv_kick(double* v, const double* fprev, const double* f, const uint8
                     double dt, double inv_rho, cudaStream_t s) {
     k_vv_kick<<<blocks_for(N * dim, 256), 256, 0, s>>>(v, fprev, f, cmask, N, dim, dt, inv_rho);
     check(cudaGetLastError(), "vv_kick");
+}
+
+void launch_adr_step(Engine& e, bool first, cudaStream_t s) {
+    const int64_t N = e.plan.nodes, m = N * e.dim;
+    double* cdev = e.d_scal + 8;  // CG uses scal[0..5]
+    if (!first) {
+        if (e.adr_fixed)
+            k_set_scalar<<<1, 1, 0, s>>>(cdev, e.adr_fixed_c);
+        else
+            k_adr_damping<<<kRedBlocks, kRedThreads, 0, s>>>(e.d_u, e.d_vh, e.d_f, e.d_fprev, e.d_cmask, N, e.dim,
+                                                             e.adr_mass[0], e.adr_mass[1], e.adr_mass[2], e.dt,
+                                                             e.d_red, e.d_ticket, cdev);
+        e.launches += 1;
+    }
+    k_adr_advance<<<blocks_for(m, 256), 256, 0, s>>>(e.d_u, e.d_vh, e.d_f, e.d_cmask, N, e.dim, e.adr_mass[0],
+                                                     e.adr_mass[1], e.adr_mass[2], e.dt, first ? 1 : 0, cdev);
+    e.launches += 1;
+    check(cudaGetLastError(), "adr step");
 }
 
 void launch_enforce(double* u, double* v, const long long* dofs, const double* val, const int* kind, int64_t n,

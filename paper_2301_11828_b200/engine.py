@@ -319,6 +319,16 @@ class FastForce:
     def sim_init(self, dt: float, v0=None):
         _check(self._lib.pdgpu_sim_init(self._h, dt, None if v0 is None else _dp(_f64(v0))))
 
+    def sim_init_adr(self, dt: float, fixed_damping=None):
+        """Simulation with Integrator::Adr (timestepping.hpp:79-162); None = adaptive damping."""
+        _check(self._lib.pdgpu_sim_init_adr(self._h, dt, float("nan") if fixed_damping is None else float(fixed_damping)))
+
+    def adr_damping(self) -> float:
+        """Simulation::adr_damping(): damping of the last ADR step."""
+        c = C.c_double()
+        _check(self._lib.pdgpu_sim_adr_damping(self._h, C.byref(c)))
+        return c.value
+
     def sim_step(self, n_steps: int = 1, s0: float = -1.0, watch=None) -> int:
         w = None if watch is None else _f64(np.concatenate([np.asarray(watch[0]), np.asarray(watch[1])]))
         nb = C.c_int64()

@@ -256,3 +256,29 @@ def test_vv_golden(tag, s0):
     assert per == list(d[tag + "_broken_per_step"])
     assert np.array_equal(o.ledger_pairs(), d[tag + "_ledger"])
     assert np.abs(u - d[tag + "_u"]).max() <= 1e-8 * np.abs(d[tag + "_u"]).max()
+
+
+def _adr_oracle(dims):
+    from oracle.gen_golden import adr_problem
+    return adr_problem(dims, ref=False)
+
+
+@pytest.mark.parametrize("tag,dims,fixed,steps", [("p2", (64, 64), None, 300), ("p2_fixed", (64, 64), 0.05, 200),
+                                                  ("p3", (16, 16, 16), None, 100)])
+def test_adr_golden(tag, dims, fixed, steps):
+    """AdrIntegrator (timestepping.hpp:79-162) restated in oracle.c against the
+    reference's own ADR trajectory (oracle/gen_golden.py gen_adr): u and the
+    adaptive damping trace."""
+    d = np.load(os.path.join(G, "adr.npz"))
+    o = _adr_oracle(dims)
+    o.sim_init_adr(1.0, fixed_damping=fixed)
+    trace = []
+    for _ in range(steps // 25):
+        o.sim_step(25)
+        trace.append(o.adr_damping())
+    u, v, f, t = o.sim_get()
+    assert t == float(d[tag + "_t"])
+    # the reference's own FFT-vs-dense ADR criterion (tests/test_timestepping.cpp:168-176):
+    # max |du| <= 1e-8 max |u| after the run (adaptive damping amplifies round-off)
+    assert np.abs(u - d[tag + "_u"]).max() <= 1e-8 * np.abs(d[tag + "_u"]).max()
+    assert np.allclose(trace, d[tag + "_damping"], rtol=1e-6, atol=0)
