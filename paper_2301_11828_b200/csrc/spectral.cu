@@ -686,6 +686,123 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
     cp_async_wait_all();
 }
 
+// ------------------------------------------------- K1, two CTAs per SM ---
+// Same transform and store pattern as k_rfft_rows_pipe with two rows per
+// tile, sized for two co-resident CTAs per SM (256 threads, <= 128
+// registers, ~104 KB SMEM each): the FFT exchanges use 8-byte slots (split
+// real/imaginary), and one buffer per row serves first as the cp.async
+// staging area of the input row and then as the natural-order spectrum the
+// R2C post-processing reads.  The next tile's rows are fetched after the
+// post-processing; its latency is covered by the other CTA on the SM.
+template <int LOGQ, bool CIRC>
+__global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restrict__ u, double2* __restrict__ S,
+                                                          int Nx, int Nrow, int nslab, int Hx,
+                                                          const double2* __restrict__ tw, int logTWN) {
+    using Sh = FftShape<LOGQ, 4>;
+    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
+    constexpr int TR = 2;
+    static_assert(4 * T <= 256, "two rows of two transforms per 256-thread CTA");
+    extern __shared__ double2 sm[];
+    constexpr int rowlen = CIRC ? 4 * Q : 2 * Q;          // staged doubles per row (>= Nx)
+    constexpr int RS = (2 * 2 * XB > rowlen ? 2 * 2 * XB : rowlen);  // doubles per row buffer
+    double* rowbuf = reinterpret_cast<double*>(sm);        // TR x RS doubles
+    double* xd = rowbuf + TR * RS;                          // 2*TR transforms x XB doubles
+    const int gi = threadIdx.x >> Sh::LOGT;
+    const int t = threadIdx.x & (T - 1);
+    const int r = gi >> 1, eo = gi & 1;
+    const int shE = logTWN - (LOGQ + 1);
+    const int shX = logTWN - (LOGQ + 2);
+    constexpr int halfP = 2 * Q;
+    const int groups = (Nrow + TR - 1) / TR;
+    const int64_t ntiles = (int64_t)groups * nslab;
+    auto fetch = [&](int64_t tile) {
+        const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
+        const int nr = min(TR, Nrow - row0);
+        const double* src = u + ((int64_t)slab * Nrow + row0) * Nx;
+        constexpr int chunks_per_row = rowlen / 2;
+        for (int c = threadIdx.x; c < TR * chunks_per_row; c += blockDim.x) {
+            const int rr = c / chunks_per_row, i0 = 2 * (c - rr * chunks_per_row);
+            const bool p = rr < nr && i0 < Nx;
+            cp_async16(rowbuf + rr * RS + i0, p ? src + (int64_t)rr * Nx + i0 : u, p);
+        }
+        cp_async_commit();
+    };
+    constexpr int LA = (2 * T >= 8) ? 3 : 0;
+    const int rr = (threadIdx.x >> LA) & (TR - 1);
+    const int a0 = ((threadIdx.x >> (LA + 1)) << LA) + (threadIdx.x & ((1 << LA) - 1));
+    int64_t tile = blockIdx.x;
+    if (tile < ntiles) fetch(tile);
+    for (; tile < ntiles; tile += gridDim.x) {
+        const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
+        const int nr = min(TR, Nrow - row0);
+        double2 v[R];
+        cp_async_wait_all();
+        __syncthreads();
+        {
+            const double* st = rowbuf + r * RS;
+            const double2 wbase = __ldg(tw + (opaque(t) << shE));
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                const int n = t + j * T;
+                double2 z = *reinterpret_cast<const double2*>(st + 2 * n);
+                if (CIRC) {
+                    const double2 z2 = *reinterpret_cast<const double2*>(st + 2 * (n + Q));
+                    z = eo ? csub(z, z2) : cadd(z, z2);
+                }
+                v[j] = eo ? cmul(z, tw32r<-1>(j * (16 / R), wbase)) : z;
+            }
+        }
+        __syncthreads();  // row buffers free: they receive the spectra below
+        reg_fft<LOGQ, 4, -1, BlockBar, true>(v, t, reinterpret_cast<double2*>(xd + gi * XB),
+                                             make_fft_tw<LOGQ, 4>(opaque(t), tw, logTWN), BlockBar{});
+        double2* spec = reinterpret_cast<double2*>(rowbuf + r * RS) + eo * XB;
+#pragma unroll
+        for (int j = 0; j < R; ++j) spec[nat_slot<T>(t, j)] = v[j];
+        __syncthreads();
+        const double2* E = reinterpret_cast<const double2*>(rowbuf + rr * RS);
+        const double2* O = E + XB;
+        double2* dst = S + (int64_t)slab * Hx * Nrow + row0 + rr;
+        const bool live = rr < nr;
+        const double2 W0 = __ldg(tw + ((2 * opaque(a0)) << shX));
+        const double2 W1 = cmul(W0, __ldg(tw + (1 << shX)));
+#pragma unroll 4
+        for (int uu = 0; uu < R / 2; ++uu) {
+            const int a = a0 + 2 * T * uu;
+            const double2 Ae = E[spad(a)];
+            const double2 Be = cconj(E[spad((Q - a) & (Q - 1))]);
+            const double2 Ao = O[spad(a)];
+            const double2 Bo = cconj(O[spad(Q - 1 - a)]);
+            {
+                const double2 Fe = cscale(cadd(Ae, Be), 0.5);
+                const double2 D = csub(Ae, Be);
+                const double2 Fo = make_double2(0.5 * D.y, -0.5 * D.x);
+                if (live) dst[(int64_t)(2 * a) * Nrow] = cadd(Fe, cmul(tw32r<-1>(uu * (32 / R), W0), Fo));
+            }
+            {
+                const double2 Fe = cscale(cadd(Ao, Bo), 0.5);
+                const double2 D = csub(Ao, Bo);
+                const double2 Fo = make_double2(0.5 * D.y, -0.5 * D.x);
+                if (live) dst[(int64_t)(2 * a + 1) * Nrow] = cadd(Fe, cmul(tw32r<-1>(uu * (32 / R), W1), Fo));
+            }
+        }
+        if (a0 == 0 && live) {  // Nyquist: X[halfP] = Re Z0 - Im Z0
+            const double2 A = E[0];
+            dst[(int64_t)halfP * Nrow] = make_double2(A.x - A.y, 0.0);
+        }
+        __syncthreads();  // spectra read: the buffers take the next tile's rows
+        if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);
+    }
+    cp_async_wait_all();
+}
+
+static int k1_duo_smem(int logq, bool circ) {
+    const int Q = 1 << logq;
+    const int XB = xbuf_slots(logq);
+    const int rowlen = circ ? 4 * Q : 2 * Q;
+    const int RS = std::max(2 * 2 * XB, rowlen);
+    return (int)sizeof(double) * (2 * RS + 4 * XB);
+}
+
 constexpr int kPipeLogR = 4;  // 16 points per thread: 256 threads per 4096-point column
 constexpr int kPipeThreads = 256;
 
@@ -1248,6 +1365,7 @@ static void set_attrs_k1_l() {
     smem_attr((const void*)k_rfft_rows_pipe<L, 1, C>);
     smem_attr((const void*)k_rfft_rows_pipe<L, 2, C>);
     smem_attr((const void*)k_rfft_rows_pipe<L, 3, C>);
+    if constexpr (L == 10) smem_attr((const void*)k_rfft_rows_duo<L, C>);
 }
 template <int... Ls>
 static void set_attrs_k1_all(std::integer_sequence<int, Ls...>) {
@@ -1264,6 +1382,22 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
     const bool cx = pl.circ[0] != 0;
     int TR = pl.k1_rows;
     const int T = threads_per_transform(lqx, 4);
+    // two-CTA/SM variant: two rows of two transforms fill a 256-thread CTA
+    if ((Nx & 1) == 0 && 4 * T == 256 && !getenv("PDGPU_NO_K1_DUO")) {
+        const size_t dsm = (size_t)k1_duo_smem(lqx, cx);
+        if (2 * (dsm + 1024) <= 228 * 1024) {
+            const int64_t ntiles = (int64_t)((Ny + 1) / 2) * nslab;
+            const unsigned dgrid = (unsigned)std::min<int64_t>(ntiles, (int64_t)e.num_sms * 2);
+#define PDGPU_K1D(C) k_rfft_rows_duo<LQ, C><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, e.d_tw, pl.logTWN)
+            switch (lqx) {
+                PDGPU_CASE(10, (cx ? PDGPU_K1D(true) : PDGPU_K1D(false)))
+                default: goto no_duo;
+            }
+#undef PDGPU_K1D
+            return;
+        }
+    }
+no_duo:
     const size_t rowlen = (size_t)(cx ? 4 : 2) << lqx;  // staged reals per row
     auto smem_of = [&](int tr) { return sizeof(double2) * (size_t)2 * tr * xbuf_slots(lqx); };
     auto psmem_of = [&](int tr) { return smem_of(tr) + sizeof(double) * (size_t)tr * rowlen; };
