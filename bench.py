@@ -224,7 +224,8 @@ def clamp_boxes(dim, dl):
 
 
 def extra_configs(device, stream):
-    """CG solve times (configs 1, 3, 4) and the 3D K.u rate (config 4), device-resident."""
+    """CG solve times (configs 1, 3, 4), the 3D K.u rate (config 4, 128^3 and 256^3), the
+    config-2 sweep (512^2 .. 2048^2, batch 16) and the VV step (config 5), device-resident."""
     import torch
     from paper_2301_11828_b200 import FastForce, build_kernel
     out = {}
@@ -288,6 +289,36 @@ def extra_configs(device, stream):
     ms, (it, rel) = timed(lambda: ff.cg_solve_device(b, x, tol=1e-9, maxit=20000, stream=stream))
     out["config4_cg"] = {"grid": [n, n, n], "tol": 1e-9, "iterations": it, "relres": rel, "solve_ms": ms}
     ff.close()
+    del u, f, b, x
+    # config 4, 256^3 rung: K.u rate on one GPU
+    n = 256
+    dl = 3.015 / n
+    ff = engine((n, n, n), [(lo, hi, 7, 0.0) for lo, hi in clamp_boxes(3, dl)])
+    u = torch.empty((3, n ** 3), dtype=torch.float64, device="cuda").uniform_(-1, 1, generator=g.manual_seed(4002))
+    f = torch.empty_like(u)
+    for _ in range(3):
+        ff.matvec_device(u, f, 1, stream)
+    reps = 10
+    ms, _ = timed(lambda: [ff.matvec_device(u, f, 1, stream) for _ in range(reps)])
+    out["config4_matvec_256"] = {"grid": [n, n, n], "value": 3 * n ** 3 / (ms / reps * 1e-3), "unit": UNIT,
+                                 "ms_per_matvec": ms / reps}
+    ff.close()
+    del u, f
+    # config 2 sweep (512^2 .. 2048^2, batch 16, no constraints); 4096^2 is the headline line
+    sweep = {}
+    for n in (512, 1024, 2048):
+        ff = engine((n, n), [])
+        u = torch.empty((BATCH, 2, n * n), dtype=torch.float64, device="cuda").uniform_(
+            -1, 1, generator=g.manual_seed(2000 + n))
+        f = torch.empty_like(u)
+        for _ in range(3):
+            ff.matvec_device(u, f, BATCH, stream)
+        reps = 10
+        ms, _ = timed(lambda: [ff.matvec_device(u, f, BATCH, stream) for _ in range(reps)])
+        sweep[f"{n}x{n}"] = {"ms_per_step": ms / reps, "value": BATCH * 2 * n * n / (ms / reps * 1e-3), "unit": UNIT}
+        ff.close()
+        del u, f
+    out["config2_sweep_b16"] = sweep
     # config 5: 2048^2 notch, velocity-driven top/bottom layers, VV with bond breaking (s0 = 1e-3)
     import numpy as np
     n = 2048
