@@ -99,6 +99,16 @@ int pdgpu_set_regions(pdgpu_t h, const uint8_t* near_surface, const uint8_t* con
  * the global lattice are not surfaces.  The caller supplies M ghost rows on
  * each interior face and keeps only the owned rows of K.u. */
 int pdgpu_set_slab(pdgpu_t h, int global_rows, int row_offset);
+/* Halo slabs without ghost rows in the lattice: the engine's lattice is the
+ * owned rows only (a power-of-two count keeps the slowest axis on the
+ * periodic embedding), and the M rows beyond each interior face come from
+ * `ghosts`, device [batch][dim][2][M][plane] fp64 (side 0 = the M rows
+ * before the slab, side 1 = the M rows after it; plane = Nx (2D) or Nx*Ny
+ * (3D)), read by every following apply / mat-vec until reset with NULL.  The
+ * wrap correction adds their stencil terms to the rows within M of the face.
+ * Requires pdgpu_set_slab; the caller refreshes the buffer's contents before
+ * each mat-vec (stream-ordered). */
+int pdgpu_set_ghosts(pdgpu_t h, const double* ghosts);
 /* Constraint state as the CG driver uses it (timestepping.hpp:306-309,
  * corrections.hpp:142-160): mask[N] = constrained direction bits per node,
  * uc[dim*N] = prescribed displacement values (0 where free or velocity-driven).

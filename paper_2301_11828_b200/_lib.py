@@ -35,6 +35,7 @@ SIGNATURES = {
     "pdgpu_symbol_is_real": (C.c_int, [C.c_void_p]),
     "pdgpu_symbol_mode": (C.c_int, [C.c_void_p]),
     "pdgpu_embedding": (C.c_int, [C.c_void_p]),
+    "pdgpu_set_ghosts": (C.c_int, [C.c_void_p, C.c_void_p]),
     "pdgpu_set_regions": (C.c_int, [C.c_void_p, c_uint8_p, c_uint8_p]),
     "pdgpu_set_surface_diag": (C.c_int, [C.c_void_p, c_double_p]),
     "pdgpu_set_slab": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),

@@ -452,7 +452,7 @@ int pdgpu_create(int dim, const int* dims, int M, const double* stencils, int de
             build_twiddles(*e);
             build_symbol(*e);
             build_coltab(*e);
-            if (e->plan.circ_mask) build_wrap_table(*e);
+            build_wrap_table(*e);  // wrap correction and slab ghost rows (built before any graph capture)
             // regions + surface diagonal from the geometry (build_de)
             e->h_near = assembly::near_surface(dim, dims, M);
             std::vector<long long> rows;
@@ -594,6 +594,19 @@ int pdgpu_set_slab(pdgpu_t h, int global_rows, int row_offset) {
         std::vector<double> de;
         assembly::surface_diag(h->dim, h->plan.N, h->M, h->stencils.data(), h->h_near, rows, de, h->slab);
         upload_surface(*h, rows, de);
+    });
+}
+
+int pdgpu_set_ghosts(pdgpu_t h, const double* ghosts) {
+    return guarded([&] {
+        if (!h) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null handle");
+        if (ghosts && h->slab.global < 0) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "ghost rows need pdgpu_set_slab");
+        h->d_ghost = ghosts;
+        h->cg_graph_x = nullptr;  // a captured CG iteration holds the old pointer
+        if (h->cg_graph) {
+            cudaGraphExecDestroy(h->cg_graph);
+            h->cg_graph = nullptr;
+        }
     });
 }
 

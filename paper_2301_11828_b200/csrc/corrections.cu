@@ -127,7 +127,8 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
                                               const int* __restrict__ wrows, const int* __restrict__ wo0,
                                               const double* __restrict__ wK, int M, int N0, int N1, int N2,
                                               int circ_mask, const uint8_t* __restrict__ cmask, int64_t nodes,
-                                              int batch, double scale, int64_t band0, int64_t band1, int64_t band2) {
+                                              int batch, double scale, int64_t band0, int64_t band1, int64_t band2,
+                                              const double* __restrict__ ghost, int lo_int, int hi_int) {
     constexpr int NP = D * (D + 1) / 2;
     const int64_t per_vec = band0 + band1 + band2;
     const int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -159,18 +160,14 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
     const int64_t p = ((int64_t)c[2] * N1 + c[1]) * N0 + c[0];
     const uint8_t cm = cmask ? cmask[p] : 0;
     const double* ub = u + (int64_t)b * D * nodes;
-    double acc[D];
+    constexpr int KS = (NP + 1) & ~1;  // entry stride: 16-byte aligned pairs
+    double acc[D], gacc[D];
 #pragma unroll
-    for (int a = 0; a < D; ++a) acc[a] = 0.0;
+    for (int a = 0; a < D; ++a) acc[a] = gacc[a] = 0.0;
     // in-lattice o0 range of this node; entries outside it along x alias when x is periodic
     const int lo0 = -c[0], hi0 = N0 - 1 - c[0];
     const bool cx = circ_mask & 1;
-    auto add = [&](int e, int64_t q) {
-        double uq[D];
-#pragma unroll
-        for (int bb = 0; bb < D; ++bb) uq[bb] = ub[(int64_t)bb * nodes + q];
-        constexpr int KS = (NP + 1) & ~1;  // entry stride: 16-byte aligned pairs
-        double kv[KS];
+    auto load_k = [&](int e, double (&kv)[KS]) {
         const double2* ke = reinterpret_cast<const double2*>(wK + (int64_t)e * KS);
 #pragma unroll
         for (int k = 0; k < KS / 2; ++k) {
@@ -178,59 +175,108 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
             kv[2 * k] = v2.x;
             kv[2 * k + 1] = v2.y;
         }
+    };
+    auto add = [&](int e, int64_t q) {
+        double uq[D];
+#pragma unroll
+        for (int bb = 0; bb < D; ++bb) uq[bb] = ub[(int64_t)bb * nodes + q];
+        double kv[KS];
+        load_k(e, kv);
 #pragma unroll
         for (int a = 0; a < D; ++a)
 #pragma unroll
             for (int bb = 0; bb < D; ++bb) acc[a] += kv[pair_idx<D>(a, bb)] * uq[bb];
     };
+    // halo slabs (pdgpu_set_ghosts): rows beyond an interior face of the slowest
+    // axis come from the neighbour's ghost rows, ghost[b][c][side][layer][plane]
+    const int64_t plane = D == 3 ? (int64_t)N0 * N1 : N0;
+    const int SA = D - 1, NS = N[SA];
+    auto add_ghost = [&](int e, int side, int layer, int64_t pidx) {
+        double kv[KS];
+        load_k(e, kv);
+#pragma unroll
+        for (int bb = 0; bb < D; ++bb) {
+            const double g = ghost[(((int64_t)(b * D + bb) * 2 + side) * M + layer) * plane + pidx];
+#pragma unroll
+            for (int a = 0; a < D; ++a) gacc[a] += kv[pair_idx<D>(a, bb)] * g;
+        }
+    };
     const int m2 = D == 3 ? M : 0;
     const int side = 2 * M + 1;
     for (int o2 = -m2; o2 <= m2; ++o2) {
         int w2 = c[2] + o2;
-        bool out2 = false;
+        bool out2 = false, al2 = true, gh2 = false;
+        int gside = 0, glayer = 0;
         if (D == 3 && (w2 < 0 || w2 >= N2)) {
-            if (!((circ_mask >> 2) & 1)) continue;
-            w2 = w2 < 0 ? w2 + N2 : w2 - N2;
             out2 = true;
+            if (ghost && (w2 < 0 ? lo_int : hi_int)) {  // z is the slowest axis in 3D
+                gh2 = true;
+                gside = w2 < 0 ? 0 : 1;
+                glayer = w2 < 0 ? w2 + M : w2 - N2;
+            }
+            if ((circ_mask >> 2) & 1) w2 = w2 < 0 ? w2 + N2 : w2 - N2;
+            else al2 = false;
+            if (!al2 && !gh2) continue;
         }
         for (int o1 = -M; o1 <= M; ++o1) {
             int w1 = c[1] + o1;
-            bool out1 = out2;
+            bool out1 = out2, al1 = al2, gh1 = gh2;
+            int gs = gside, gl = glayer;
             if (w1 < 0 || w1 >= N1) {
-                if (!((circ_mask >> 1) & 1)) continue;
-                w1 = w1 < 0 ? w1 + N1 : w1 - N1;
                 out1 = true;
+                if (D == 2) {  // y is the slowest axis in 2D
+                    gh1 = ghost && (w1 < 0 ? lo_int : hi_int);
+                    gs = w1 < 0 ? 0 : 1;
+                    gl = w1 < 0 ? w1 + M : w1 - N1;
+                } else {
+                    gh1 = false;  // the neighbour slab has no nodes outside the y range either
+                }
+                if ((circ_mask >> 1) & 1) w1 = w1 < 0 ? w1 + N1 : w1 - N1;
+                else al1 = false;
             }
+            if (!al1 && !gh1) continue;
             const int row = (o2 + m2) * side + (o1 + M);
             const int e0 = __ldg(wrows + 2 * row), e1 = __ldg(wrows + 2 * row + 1);
             const int64_t qrow = ((int64_t)w2 * N1 + w1) * N0;
-            if (out1) {  // every entry of the row aliases (x in range) or is dropped (x out, padded)
-                for (int e = e0; e < e1; ++e) {
-                    int w0 = c[0] + __ldg(wo0 + e);
-                    if (w0 < 0 || w0 >= N0) {
-                        if (!cx) continue;
-                        w0 = w0 < 0 ? w0 + N0 : w0 - N0;
+            if (al1) {
+                if (out1) {  // every entry of the row aliases (x in range) or is dropped (x out, padded)
+                    for (int e = e0; e < e1; ++e) {
+                        int w0 = c[0] + __ldg(wo0 + e);
+                        if (w0 < 0 || w0 >= N0) {
+                            if (!cx) continue;
+                            w0 = w0 < 0 ? w0 + N0 : w0 - N0;
+                        }
+                        add(e, qrow + w0);
                     }
-                    add(e, qrow + w0);
+                } else if (cx) {  // only the entries leaving along x
+                    for (int e = e0; e < e1; ++e) {
+                        const int o0 = __ldg(wo0 + e);
+                        if (o0 >= lo0) break;
+                        add(e, qrow + c[0] + o0 + N0);
+                    }
+                    for (int e = e1 - 1; e >= e0; --e) {
+                        const int o0 = __ldg(wo0 + e);
+                        if (o0 <= hi0) break;
+                        add(e, qrow + c[0] + o0 - N0);
+                    }
                 }
-            } else if (cx) {  // only the entries leaving along x
+            }
+            if (gh1) {  // true neighbour values, x inside the lattice only
+                const int64_t prow = D == 3 ? (int64_t)(c[1] + o1) * N0 : 0;
                 for (int e = e0; e < e1; ++e) {
-                    const int o0 = __ldg(wo0 + e);
-                    if (o0 >= lo0) break;
-                    add(e, qrow + c[0] + o0 + N0);
-                }
-                for (int e = e1 - 1; e >= e0; --e) {
-                    const int o0 = __ldg(wo0 + e);
-                    if (o0 <= hi0) break;
-                    add(e, qrow + c[0] + o0 - N0);
+                    const int x = c[0] + __ldg(wo0 + e);
+                    if (x < 0 || x >= N0) continue;
+                    add_ghost(e, gs, gl, prow + x);
                 }
             }
         }
     }
+    (void)SA;
+    (void)NS;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
         if ((cm >> a) & 1u) continue;
-        f[((int64_t)b * D + a) * nodes + p] -= scale * acc[a];
+        f[((int64_t)b * D + a) * nodes + p] += scale * (gacc[a] - acc[a]);
     }
 }
 
@@ -268,9 +314,13 @@ void build_wrap_table(Engine& e) {
 void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
                             const uint8_t* cmask) {
     const Plan& pl = e.plan;
+    const int SA = pl.dim - 1;
+    const int lo_int = e.slab.global >= 0 && e.slab.off > 0;
+    const int hi_int = e.slab.global >= 0 && e.slab.off + pl.N[SA] < e.slab.global;
+    const double* ghost = e.d_ghost && (lo_int || hi_int) ? e.d_ghost : nullptr;
     int64_t band[3] = {0, 0, 0};
     for (int d = 0; d < pl.dim; ++d) {
-        if (!pl.circ[d]) continue;
+        if (!pl.circ[d] && !(d == SA && ghost)) continue;
         band[d] = 2 * e.M;
         for (int k = 0; k < 3; ++k)
             if (k != d) band[d] *= pl.N[k];
@@ -282,10 +332,12 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
     const unsigned blocks = (unsigned)((tot + th - 1) / th);
     if (pl.dim == 2)
         k_wrap<2><<<blocks, th, 0, s>>>(u, f, e.d_wrows, e.d_wo0, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],
-                                        pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2]);
+                                        pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2],
+                                        ghost, lo_int, hi_int);
     else
         k_wrap<3><<<blocks, th, 0, s>>>(u, f, e.d_wrows, e.d_wo0, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],
-                                        pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2]);
+                                        pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2],
+                                        ghost, lo_int, hi_int);
 }
 
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale) {

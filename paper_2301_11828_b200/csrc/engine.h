@@ -98,6 +98,7 @@ struct Engine {
     uint8_t* d_cmask = nullptr;        // N, constraint direction mask per node
     std::vector<uint8_t> h_cmask, h_near;
     assembly::SlabFrame slab;          // rows of a larger lattice (pdgpu_set_slab)
+    const double* d_ghost = nullptr;   // caller's ghost rows of the interior slab faces (pdgpu_set_ghosts)
     int64_t n_surf = 0;
     long long* d_surf_rows = nullptr;  // surface node ids
     double* d_surf_de = nullptr;       // n_surf * np

@@ -1745,7 +1745,7 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
         PassTimer pt(e, kPassK5, s);
         launch_k5(e, xin, f, batch, s, scale, cmask, body);
     }
-    if (pl.circ_mask) {  // K6w: the periodic embedding's wrap correction (timed with the corrections)
+    if (pl.circ_mask || e.d_ghost) {  // K6w: wrap correction / slab ghost rows (timed with the corrections)
         PassTimer pt(e, kPassCorr, s);
         launch_wrap_correction(e, u, f, batch, s, scale, cmask);
     }

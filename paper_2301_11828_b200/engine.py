@@ -215,6 +215,11 @@ class FastForce:
         near-surface flags and D^e follow the global faces."""
         _check(self._lib.pdgpu_set_slab(self._h, int(global_rows), int(row_offset)))
 
+    def set_ghosts(self, ghosts):
+        """Ghost rows of the interior slab faces (device tensor [batch][dim][2][M][plane]) or None."""
+        _check(self._lib.pdgpu_set_ghosts(self._h, None if ghosts is None else _ptr(ghosts)))
+        self._ghosts = ghosts  # keep the buffer alive while the engine may read it
+
     def constraint_values(self):
         """(mask[N] uint8 constrained-direction bits, uc[dim, N] prescribed
         displacements) -- what cg_solve masks with and shifts by."""

@@ -4,8 +4,13 @@ SURVEY.md sec.8e.  The FFT convolution couples every node, but the stencil
 reaches only M rows, so the operator on a block of rows needs the rows
 themselves plus M rows on either side.  Rank r owns rows [r0, r1) of the
 slowest axis (rows j in 2D, planes k in 3D; node p = (k*Ny + j)*Nx + i,
-grid.hpp:30-36) and runs its own zero-padded FFT convolution (one libpdgpu
-engine) over those rows plus M ghost rows on each interior face.  Before every
+grid.hpp:30-36) and runs its own FFT convolution (one libpdgpu engine).
+Two halo modes: "ghost" (default) -- the engine's lattice is exactly the owned
+rows (a power-of-two count keeps every axis on the periodic embedding, so a
+rank does 1/G of the single-GPU transform work) and the M rows beyond each
+interior face arrive in a side buffer whose stencil terms the engine's wrap
+correction adds (pdgpu_set_ghosts); "embedded" -- the ghost rows are part of
+the engine's lattice (R + 2M rows, zero-padded transforms).  Before every
 mat-vec each rank sends its first / last M owned rows to its neighbours
 (torch.distributed point-to-point: NCCL between GPUs, gloo in the CPU tests):
 2*M*plane*dim*8 bytes per rank per vector -- 393 KB at 4096^2 -- against the
@@ -44,7 +49,7 @@ class SlabForce:
     """
 
     def __init__(self, dims, M: int, stencils, rank: int = 0, world: int = 1, device=None, engine=None,
-                 group=None):
+                 group=None, halo: str = "ghost"):
         self.dims = tuple(int(d) for d in dims)
         self.dim = len(self.dims)
         self.M = int(M)
@@ -57,7 +62,16 @@ class SlabForce:
             raise ValueError(f"slab of {self.R} rows is thinner than the horizon M = {self.M}")
         self.gl = self.M if self.r0 > 0 else 0
         self.gh = self.M if self.r1 < self.rows else 0
-        self.L = self.R + self.gl + self.gh
+        if halo not in ("ghost", "embedded"):
+            raise ValueError("halo must be 'ghost' or 'embedded'")
+        # "ghost": the engine's lattice is the owned rows (periodic along the
+        # slowest axis when R is a power of two) and the neighbours' rows
+        # arrive in a side buffer read by the wrap correction
+        # (pdgpu_set_ghosts); "embedded": the ghost rows are part of the
+        # engine's lattice (zero-padded transforms of R + 2M rows).
+        self.halo = halo
+        self.L = self.R if halo == "ghost" else self.R + self.gl + self.gh
+        self.off = self.r0 if halo == "ghost" else self.r0 - self.gl
         self.ext_dims = self.dims[:-1] + (self.L,)
         self.device = torch.device(device) if device is not None else torch.device("cpu")
         if engine is None:
@@ -67,7 +81,7 @@ class SlabForce:
                 raise RuntimeError("SlabForce needs a CUDA device (libpdgpu engine)")
             engine = lambda ext: FastForce(ext, self.M, stencils, device=self.device.index or 0)  # noqa: E731
         self.eng = engine(self.ext_dims)
-        self.eng.set_slab(self.rows, self.r0 - self.gl)
+        self.eng.set_slab(self.rows, self.off)
         self._bufs = {}
 
     # ------------------------------------------------------------ set-up
@@ -75,7 +89,7 @@ class SlabForce:
         """Global geometry; the engine's origin moves to its first (ghost) row
         so node positions stay global (grid.hpp:53-57)."""
         org = np.zeros(self.dim) if origin is None else np.array(origin, dtype=np.float64)
-        org[-1] += (self.r0 - self.gl) * h
+        org[-1] += self.off * h
         self.eng.set_geometry(h, org, delta, rho)
 
     def add_constraint(self, lo, hi, dir_mask: int, kind: int = 0, value: float = 0.0):
@@ -94,8 +108,36 @@ class SlabForce:
         if batch not in self._bufs:
             z = lambda: torch.zeros((batch, self.dim, self.L * self.plane), dtype=torch.float64,  # noqa: E731
                                     device=self.device)
-            self._bufs[batch] = (z(), z())
+            g = torch.zeros((batch, self.dim, 2, self.M, self.plane), dtype=torch.float64, device=self.device)
+            self._bufs[batch] = (z(), z(), g)
         return self._bufs[batch]
+
+    def exchange_ghosts(self, u3, g):
+        """Ghost mode: g (batch, dim, 2, M, plane) <- the M rows before / after
+        this slab from the neighbours (zeros at global faces); u3 the owned
+        rows (batch, dim, R*plane)."""
+        if self.world == 1:
+            return
+        b = u3.shape[0]
+        e = u3.reshape(b, self.dim, self.R, self.plane)
+        M = self.M
+        ops, recvs = [], []
+        if self.gl:
+            peer = self.rank - 1
+            ops.append(dist.P2POp(dist.isend, e[:, :, :M].contiguous(), peer, self.group))
+            buf = torch.empty((b, self.dim, M, self.plane), dtype=u3.dtype, device=u3.device)
+            ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
+            recvs.append((buf, 0))
+        if self.gh:
+            peer = self.rank + 1
+            ops.append(dist.P2POp(dist.isend, e[:, :, self.R - M:].contiguous(), peer, self.group))
+            buf = torch.empty((b, self.dim, M, self.plane), dtype=u3.dtype, device=u3.device)
+            ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
+            recvs.append((buf, 1))
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+        for buf, side in recvs:
+            g[:, :, side].copy_(buf)
 
     def exchange(self, ext):
         """Fill the ghost rows of ext (batch, dim, L*plane) from the neighbours."""
@@ -132,12 +174,19 @@ class SlabForce:
         squeeze = u.dim() == 2
         u3 = u.unsqueeze(0) if squeeze else u
         b = u3.shape[0]
-        ext, fext = self._buf(b)
-        own = slice(self.gl * self.plane, (self.gl + self.R) * self.plane)
-        ext[:, :, own].copy_(u3)
-        self.exchange(ext)
-        self.eng.matvec_device(ext, fext, b, stream=self._stream())
-        out = fext[:, :, own]
+        ext, fext, g = self._buf(b)
+        if self.halo == "ghost":
+            ext.copy_(u3)
+            self.exchange_ghosts(ext, g)
+            self.eng.set_ghosts(g if self.world > 1 else None)
+            self.eng.matvec_device(ext, fext, b, stream=self._stream())
+            out = fext
+        else:
+            own = slice(self.gl * self.plane, (self.gl + self.R) * self.plane)
+            ext[:, :, own].copy_(u3)
+            self.exchange(ext)
+            self.eng.matvec_device(ext, fext, b, stream=self._stream())
+            out = fext[:, :, own]
         if f is None:
             f = out.clone()
         else:
@@ -157,7 +206,8 @@ class SlabForce:
     def constraint_values(self):
         """(free[dim, R*plane] fp64 0/1 mask, uc[dim, R*plane]) on the owned rows."""
         mask, uc = self.eng.constraint_values()
-        own = slice(self.gl * self.plane, (self.gl + self.R) * self.plane)
+        g0 = 0 if self.halo == "ghost" else self.gl
+        own = slice(g0 * self.plane, (g0 + self.R) * self.plane)
         mask = np.asarray(mask)[own]
         free = np.stack([((mask >> a) & 1) == 0 for a in range(self.dim)]).astype(np.float64)
         uc = np.asarray(uc).reshape(self.dim, -1)[:, own]

@@ -73,7 +73,28 @@ class OracleSlabEngine:
         return self._o
 
     def set_slab(self, rows, off):
+        self.rows, self.off = rows, off
         self.de = self.de_g[:, off * self.plane:off * self.plane + self.n]
+        self.ghosts = None
+
+    def set_ghosts(self, g):
+        """pdgpu_set_ghosts contract: g (batch, dim, 2, M, plane), side 0 = rows before the slab."""
+        self.ghosts = g
+
+    def _apply_with_ghosts(self, ub, g):
+        """The engine's ghost-mode result: the oracle on [ghost_lo; slab; ghost_hi], owned rows."""
+        from oracle.oracle import Oracle
+        lo_int, hi_int = self.off > 0, self.off + self.ext[-1] < self.rows
+        gl, gh = (M if lo_int else 0), (M if hi_int else 0)
+        parts = ([g[:, 0].numpy()] if gl else []) + [ub.reshape(self.dim, self.ext[-1], self.plane)] + \
+                ([g[:, 1].numpy()] if gh else [])
+        ue = np.concatenate(parts, axis=1).reshape(self.dim, -1)
+        org = self.origin.copy()
+        org[-1] -= gl * self.h
+        o = Oracle(self.ext[:-1] + (self.ext[-1] + gl + gh,), h=self.h, delta=3.015 * self.h, M=M, origin=org)
+        o.set_kernel(self.K)
+        fe = o.apply(ue).reshape(self.dim, -1, self.plane)
+        return np.ascontiguousarray(fe[:, gl:gl + self.ext[-1]].reshape(self.dim, -1))
 
     def set_geometry(self, h, origin, delta, rho):
         self.h, self.origin, self._o = h, np.array(origin, dtype=np.float64), None
@@ -93,7 +114,7 @@ class OracleSlabEngine:
         o = self._oracle()
         for b in range(batch):
             ub = u[b].numpy()
-            fb = o.apply(ub)
+            fb = o.apply(ub) if self.ghosts is None else self._apply_with_ghosts(ub, self.ghosts[b])
             for a in range(self.dim):
                 for c in range(self.dim):
                     fb[a] += self.de[pair_index(self.dim, a, c)] * ub[c]
@@ -109,7 +130,7 @@ def _global_oracle(n, clamp):
     return o
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, halo="ghost"):
     os.environ.update(RANK=str(rank), WORLD_SIZE=str(world), LOCAL_RANK=str(rank), MASTER_ADDR="127.0.0.1",
                       MASTER_PORT=str(port))
     from oracle.oracle import Rng, random_field
@@ -120,14 +141,14 @@ def _worker(rank, world, port, q):
     K, de = g.kernel(), g.de()
     h, delta = _geom(N)
     sf = SlabForce((N, N), M, K, rank=r, world=w,
-                   engine=lambda ext: OracleSlabEngine(ext, (N, N), K, de))
+                   engine=lambda ext: OracleSlabEngine(ext, (N, N), K, de), halo=halo)
     sf.set_geometry(h, None, delta, 1.0)
     u = random_field(Rng(4100), 2, N * N)
     ub = torch.from_numpy(np.stack([sf.owned(u), sf.owned(-0.5 * u)]))
     f = sf.matvec(ub)
     # CG on the clamped problem
     sfc = SlabForce((N, N), M, K, rank=r, world=w,
-                    engine=lambda ext: OracleSlabEngine(ext, (N, N), K, de))
+                    engine=lambda ext: OracleSlabEngine(ext, (N, N), K, de), halo=halo)
     sfc.set_geometry(h, None, delta, 1.0)
     _clamp(sfc.add_constraint, N)
     b = random_field(Rng(4101), 2, N * N)
@@ -141,13 +162,13 @@ def _worker(rank, world, port, q):
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("world", [2, 3])
-def test_slab_halo_gloo(world):
+@pytest.mark.parametrize("world,halo", [(2, "ghost"), (3, "ghost"), (2, "embedded"), (3, "embedded")])
+def test_slab_halo_gloo(world, halo):
     from oracle.oracle import Rng, random_field
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, halo)) for r in range(world)]
     for p in procs:
         p.start()
     parts = q.get(timeout=500)
@@ -182,7 +203,7 @@ def test_slab_rows_partition():
         assert all(spans[i][1] == spans[i + 1][0] for i in range(w - 1))
 
 
-def _emulated_slabs(dims, K, world, u, dev, constraints=()):
+def _emulated_slabs(dims, K, world, u, dev, constraints=(), halo="ghost"):
     """All slabs of one lattice on one GPU; ghost rows copied from the global
     field (what the P2P exchange delivers)."""
     from paper_2301_11828_b200.slab import SlabForce
@@ -190,7 +211,7 @@ def _emulated_slabs(dims, K, world, u, dev, constraints=()):
     h = 1.0 / dims[0]
     out = torch.zeros_like(u)
     for r in range(world):
-        sf = SlabForce(dims, M, K, rank=r, world=world, device=dev)
+        sf = SlabForce(dims, M, K, rank=r, world=world, device=dev, halo=halo)
         sf.set_geometry(h, None, 3.015 * h, 1.0)
         for c in constraints:
             sf.add_constraint(*c)
@@ -200,15 +221,24 @@ def _emulated_slabs(dims, K, world, u, dev, constraints=()):
         def fill(ext, lo=lo, hi=hi):
             ext.copy_(u[:, :, lo:hi])
 
+        def fill_ghosts(u3, g, sf=sf):
+            if sf.gl:
+                g[:, :, 0].copy_(u[:, :, (sf.r0 - M) * plane:sf.r0 * plane].reshape(g.shape[0], sf.dim, M, plane))
+            if sf.gh:
+                g[:, :, 1].copy_(u[:, :, sf.r1 * plane:(sf.r1 + M) * plane].reshape(g.shape[0], sf.dim, M, plane))
+
         sf.exchange = fill
+        sf.exchange_ghosts = fill_ghosts
         out[:, :, sf.r0 * plane:sf.r1 * plane] = sf.matvec(sf.owned(u).contiguous())
         sf.eng.close()
     return out
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("dims,world", [((256, 256), 4), ((96, 80), 3), ((24, 20, 32), 4)])
-def test_slab_engine_gpu(dims, world):
+@pytest.mark.parametrize("halo", ["ghost", "embedded"])
+@pytest.mark.parametrize("dims,world", [((256, 256), 4), ((96, 80), 3), ((24, 20, 32), 4), ((32, 32, 64), 2),
+                                        ((512, 512), 8)])
+def test_slab_engine_gpu(dims, world, halo):
     from oracle.oracle import Rng, random_field
     from paper_2301_11828_b200.engine import FastForce, build_kernel
     dev = torch.device("cuda:0")
@@ -222,7 +252,7 @@ def test_slab_engine_gpu(dims, world):
     f_ref = torch.zeros_like(u)
     full.matvec_device(u, f_ref, 2, stream=torch.cuda.current_stream())
     torch.cuda.synchronize()
-    f = _emulated_slabs(dims, K, world, u, dev)
+    f = _emulated_slabs(dims, K, world, u, dev, halo=halo)
     torch.cuda.synchronize()
     err = float(torch.linalg.norm(f - f_ref) / torch.linalg.norm(f_ref))
     assert err <= 1e-12, err
