@@ -128,14 +128,15 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
                                               const double* __restrict__ wK, int M, int N0, int N1, int N2,
                                               int circ_mask, const uint8_t* __restrict__ cmask, int64_t nodes,
                                               int batch, double scale, int64_t band0, int64_t band1, int64_t band2,
-                                              const double* __restrict__ ghost, int lo_int, int hi_int) {
+                                              const double* __restrict__ ghost, int lo_int, int hi_int,
+                                              const int* __restrict__ lidx, const int* __restrict__ loff,
+                                              const double* __restrict__ lK) {
     constexpr int NP = D * (D + 1) / 2;
     const int64_t per_vec = band0 + band1 + band2;
     const int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gidx >= per_vec * batch) return;
     const int b = (int)(gidx / per_vec);
     int64_t r = gidx - (int64_t)b * per_vec;
-    const int N[3] = {N0, N1, N2};
     int ax = 0;
     if (r >= band0) {
         r -= band0;
@@ -146,26 +147,102 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
         }
     }
     // mixed radix over the two other axes (lower axis fastest), the band
-    // layer (2M values) slowest: a warp shares one depth, so one trip count
-    int c[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        if (d == ax) continue;
-        c[d] = (int)(r % N[d]);
-        r /= N[d];
+    // layer (2M values) slowest: a warp shares one depth, so one trip count.
+    // Scalars, not arrays: a runtime-indexed array would live in local memory.
+    auto layer = [&](int64_t l, int n) { return (int)l < M ? (int)l : n - 2 * M + (int)l; };
+    int c0, c1, c2;
+    if (ax == 0) {
+        c1 = (int)(r % N1);
+        r /= N1;
+        c2 = (int)(r % N2);
+        r /= N2;
+        c0 = layer(r, N0);
+    } else if (ax == 1) {
+        c0 = (int)(r % N0);
+        r /= N0;
+        c2 = (int)(r % N2);
+        r /= N2;
+        c1 = layer(r, N1);
+    } else {
+        c0 = (int)(r % N0);
+        r /= N0;
+        c1 = (int)(r % N1);
+        r /= N1;
+        c2 = layer(r, N2);
     }
-    c[ax] = (int)r < M ? (int)r : N[ax] - 2 * M + (int)r;
-    for (int d = 0; d < ax; ++d)  // already covered by an earlier periodic axis
-        if (((circ_mask >> d) & 1) && (c[d] < M || c[d] >= N[d] - M)) return;
-    const int64_t p = ((int64_t)c[2] * N1 + c[1]) * N0 + c[0];
+    // already covered by an earlier periodic axis
+    if (ax >= 1 && (circ_mask & 1) && (c0 < M || c0 >= N0 - M)) return;
+    if (ax >= 2 && ((circ_mask >> 1) & 1) && (c1 < M || c1 >= N1 - M)) return;
+    const int64_t p = ((int64_t)c2 * N1 + c1) * N0 + c0;
     const uint8_t cm = cmask ? cmask[p] : 0;
     const double* ub = u + (int64_t)b * D * nodes;
     constexpr int KS = (NP + 1) & ~1;  // entry stride: 16-byte aligned pairs
     double acc[D], gacc[D];
 #pragma unroll
     for (int a = 0; a < D; ++a) acc[a] = gacc[a] = 0.0;
+    const int64_t plane = D == 3 ? (int64_t)N0 * N1 : N0;
+    // fast path: the node is M or more away from every face of the other axes,
+    // so the aliased entries are exactly the precomputed list of its layer
+    // (uniform across the warp: one depth per warp, no row bookkeeping)
+    {
+        const bool in0 = ax == 0 || (c0 >= M && c0 < N0 - M);
+        const bool in1 = ax == 1 || (c1 >= M && c1 < N1 - M);
+        const bool in2 = D == 2 || ax == 2 || (c2 >= M && c2 < N2 - M);
+        if (in0 && in1 && in2) {
+            const int cax = ax == 0 ? c0 : (ax == 1 ? c1 : c2);
+            const int nax = ax == 0 ? N0 : (ax == 1 ? N1 : N2);
+            const int sd = cax < M ? 0 : 1;
+            const int l = sd ? nax - 1 - cax : cax;
+            const bool per = (circ_mask >> ax) & 1;
+            const bool gface = ghost && ax == D - 1 && (sd ? hi_int : lo_int);
+            const int li = (ax * 2 + sd) * M + l;
+            const int e0 = __ldg(lidx + li), e1 = __ldg(lidx + li + 1);
+            const int wrapd = sd ? -nax : nax;
+#pragma unroll 2
+            for (int e = e0; e < e1; ++e) {
+                const int4 o = __ldg(reinterpret_cast<const int4*>(loff) + e);
+                const int q0 = c0 + o.x, q1 = c1 + o.y, q2 = c2 + o.z;
+                double kv[KS];
+                const double2* ke = reinterpret_cast<const double2*>(lK + (int64_t)e * KS);
+#pragma unroll
+                for (int k = 0; k < KS / 2; ++k) {
+                    const double2 v2 = __ldg(ke + k);
+                    kv[2 * k] = v2.x;
+                    kv[2 * k + 1] = v2.y;
+                }
+                if (per) {
+                    const int64_t q = ((int64_t)(q2 + (ax == 2 ? wrapd : 0)) * N1 + q1 + (ax == 1 ? wrapd : 0)) * N0 +
+                                      q0 + (ax == 0 ? wrapd : 0);
+                    double uq[D];
+#pragma unroll
+                    for (int bb = 0; bb < D; ++bb) uq[bb] = ub[(int64_t)bb * nodes + q];
+#pragma unroll
+                    for (int a = 0; a < D; ++a)
+#pragma unroll
+                        for (int bb = 0; bb < D; ++bb) acc[a] += kv[pair_idx<D>(a, bb)] * uq[bb];
+                }
+                if (gface) {
+                    const int qs = D == 3 ? q2 : q1;
+                    const int layer = sd ? qs - nax : qs + M;
+                    const int64_t pidx = D == 3 ? (int64_t)q1 * N0 + q0 : q0;
+#pragma unroll
+                    for (int bb = 0; bb < D; ++bb) {
+                        const double g = ghost[(((int64_t)(b * D + bb) * 2 + sd) * M + layer) * plane + pidx];
+#pragma unroll
+                        for (int a = 0; a < D; ++a) gacc[a] += kv[pair_idx<D>(a, bb)] * g;
+                    }
+                }
+            }
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                if ((cm >> a) & 1u) continue;
+                f[((int64_t)b * D + a) * nodes + p] += scale * (gacc[a] - acc[a]);
+            }
+            return;
+        }
+    }
     // in-lattice o0 range of this node; entries outside it along x alias when x is periodic
-    const int lo0 = -c[0], hi0 = N0 - 1 - c[0];
+    const int lo0 = -c0, hi0 = N0 - 1 - c0;
     const bool cx = circ_mask & 1;
     auto load_k = [&](int e, double (&kv)[KS]) {
         const double2* ke = reinterpret_cast<const double2*>(wK + (int64_t)e * KS);
@@ -189,8 +266,6 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
     };
     // halo slabs (pdgpu_set_ghosts): rows beyond an interior face of the slowest
     // axis come from the neighbour's ghost rows, ghost[b][c][side][layer][plane]
-    const int64_t plane = D == 3 ? (int64_t)N0 * N1 : N0;
-    const int SA = D - 1, NS = N[SA];
     auto add_ghost = [&](int e, int side, int layer, int64_t pidx) {
         double kv[KS];
         load_k(e, kv);
@@ -204,7 +279,7 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
     const int m2 = D == 3 ? M : 0;
     const int side = 2 * M + 1;
     for (int o2 = -m2; o2 <= m2; ++o2) {
-        int w2 = c[2] + o2;
+        int w2 = c2 + o2;
         bool out2 = false, al2 = true, gh2 = false;
         int gside = 0, glayer = 0;
         if (D == 3 && (w2 < 0 || w2 >= N2)) {
@@ -219,7 +294,7 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
             if (!al2 && !gh2) continue;
         }
         for (int o1 = -M; o1 <= M; ++o1) {
-            int w1 = c[1] + o1;
+            int w1 = c1 + o1;
             bool out1 = out2, al1 = al2, gh1 = gh2;
             int gs = gside, gl = glayer;
             if (w1 < 0 || w1 >= N1) {
@@ -241,7 +316,7 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
             if (al1) {
                 if (out1) {  // every entry of the row aliases (x in range) or is dropped (x out, padded)
                     for (int e = e0; e < e1; ++e) {
-                        int w0 = c[0] + __ldg(wo0 + e);
+                        int w0 = c0 + __ldg(wo0 + e);
                         if (w0 < 0 || w0 >= N0) {
                             if (!cx) continue;
                             w0 = w0 < 0 ? w0 + N0 : w0 - N0;
@@ -252,27 +327,25 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
                     for (int e = e0; e < e1; ++e) {
                         const int o0 = __ldg(wo0 + e);
                         if (o0 >= lo0) break;
-                        add(e, qrow + c[0] + o0 + N0);
+                        add(e, qrow + c0 + o0 + N0);
                     }
                     for (int e = e1 - 1; e >= e0; --e) {
                         const int o0 = __ldg(wo0 + e);
                         if (o0 <= hi0) break;
-                        add(e, qrow + c[0] + o0 - N0);
+                        add(e, qrow + c0 + o0 - N0);
                     }
                 }
             }
             if (gh1) {  // true neighbour values, x inside the lattice only
-                const int64_t prow = D == 3 ? (int64_t)(c[1] + o1) * N0 : 0;
+                const int64_t prow = D == 3 ? (int64_t)(c1 + o1) * N0 : 0;
                 for (int e = e0; e < e1; ++e) {
-                    const int x = c[0] + __ldg(wo0 + e);
+                    const int x = c0 + __ldg(wo0 + e);
                     if (x < 0 || x >= N0) continue;
                     add_ghost(e, gs, gl, prow + x);
                 }
             }
         }
     }
-    (void)SA;
-    (void)NS;
 #pragma unroll
     for (int a = 0; a < D; ++a) {
         if ((cm >> a) & 1u) continue;
@@ -309,6 +382,35 @@ void build_wrap_table(Engine& e) {
     up((void**)&e.d_wrows, rows.data(), sizeof(int) * rows.size());
     up((void**)&e.d_wo0, o0s.data(), sizeof(int) * o0s.size());
     up((void**)&e.d_wK, kv.data(), sizeof(double) * kv.size());
+    // layer lists (k_wrap fast path): for axis a, side s, depth l the entries
+    // with o_a < -l (s = 0) or o_a > l (s = 1), storage order
+    const int KSh = (np + 1) & ~1;
+    std::vector<int> lidx, loff;
+    std::vector<double> lk;
+    for (int a = 0; a < 3; ++a)
+        for (int sd = 0; sd < 2; ++sd)
+            for (int l = 0; l < M; ++l) {
+                lidx.push_back((int)(loff.size() / 4));
+                if (a >= dim) continue;
+                int64_t ent = 0;
+                for (int row = 0; row < nrows; ++row)
+                    for (int ei = rows[2 * row]; ei < rows[2 * row + 1]; ++ei, ++ent) {
+                        const int o[3] = {o0s[(size_t)ei], (dim == 3 ? row % side : row) - M,
+                                          dim == 3 ? row / side - M : 0};
+                        if (!(sd == 0 ? o[a] < -l : o[a] > l)) continue;
+                        loff.insert(loff.end(), {o[0], o[1], o[2], 0});
+                        for (int k = 0; k < KSh; ++k) lk.push_back(kv[(size_t)ei * KSh + k]);
+                    }
+                (void)ent;
+            }
+    lidx.push_back((int)(loff.size() / 4));
+    if (loff.empty()) {
+        loff.assign(4, 0);
+        lk.assign((size_t)KSh, 0.0);
+    }
+    up((void**)&e.d_lidx, lidx.data(), sizeof(int) * lidx.size());
+    up((void**)&e.d_loff, loff.data(), sizeof(int) * loff.size());
+    up((void**)&e.d_lK, lk.data(), sizeof(double) * lk.size());
 }
 
 void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
@@ -333,11 +435,11 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
     if (pl.dim == 2)
         k_wrap<2><<<blocks, th, 0, s>>>(u, f, e.d_wrows, e.d_wo0, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],
                                         pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2],
-                                        ghost, lo_int, hi_int);
+                                        ghost, lo_int, hi_int, e.d_lidx, e.d_loff, e.d_lK);
     else
         k_wrap<3><<<blocks, th, 0, s>>>(u, f, e.d_wrows, e.d_wo0, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],
                                         pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2],
-                                        ghost, lo_int, hi_int);
+                                        ghost, lo_int, hi_int, e.d_lidx, e.d_loff, e.d_lK);
 }
 
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale) {

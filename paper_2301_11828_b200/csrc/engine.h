@@ -80,6 +80,12 @@ struct Engine {
     int* d_wrows = nullptr;
     int* d_wo0 = nullptr;
     double* d_wK = nullptr;
+    // per (axis, side, depth) lists of the entries that leave the lattice for a
+    // node M or more away from the other faces: d_lidx[(axis*2+side)*M+depth]
+    // = first entry (one extra end slot), d_loff[4*entry] = o0, o1, o2, d_lK as d_wK
+    int* d_lidx = nullptr;
+    int* d_loff = nullptr;
+    double* d_lK = nullptr;
     double* d_kc = nullptr;         // centre coefficients (3D direct stencil)
     double* d_coltab = nullptr;     // separable symbol: per column n_pairs x (M+1) coefficients (2D)
     int coltab_oddmask = 0;         // bit p: pair p odd along the column axis (sin terms)
