@@ -367,17 +367,11 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
     const int z = slab % Nz;
     double* dst = f + ((int64_t)slab * Nrow + row0) * Nx;
     const bool vec = (Nx & 1) == 0;
-    constexpr int NOUT = CIRC ? 2 * Q : Q;  // complex outputs kept per row
-    constexpr int LOGNOUT = CIRC ? LOGQ + 1 : LOGQ;
-#pragma unroll 4
-    for (int u = 0; u < (CIRC ? R : R / 2); ++u) {  // nr*NOUT <= 2*TR*T * R/2 (x2) items
-        const int idx = threadIdx.x + u * 2 * TR * T;
-        const int rr = idx >> LOGNOUT, n = idx & (NOUT - 1);
+    // item (rr, m), m < Q: z[m] = E'[m] + O'[m] (and, periodic, z[m + Q] =
+    // E'[m] - O'[m] from the same two SMEM reads); x[2n] = Re z, x[2n+1] = Im z
+    auto emit = [&](int rr, int n, double2 zz) {
         const int i0 = 2 * n;
-        if (rr >= nr || i0 >= Nx) continue;
-        const int m = n & (Q - 1);
-        const double2 zo = sm[(2 * rr + 1) * XB + spad(m)];
-        const double2 zz = (CIRC && n >= Q) ? csub(sm[2 * rr * XB + spad(m)], zo) : cadd(sm[2 * rr * XB + spad(m)], zo);
+        if (i0 >= Nx) return;
         double v0 = zz.x * scale, v1 = zz.y * scale;
         const int64_t node = ((int64_t)z * Nrow + row0 + rr) * Nx + i0;
         const bool two = i0 + 1 < Nx;
@@ -396,6 +390,16 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
             o[0] = v0;
             if (two) o[1] = v1;
         }
+    };
+#pragma unroll 4
+    for (int u = 0; u < R / 2; ++u) {  // nr*Q <= 2*TR*T * R/2 items
+        const int idx = threadIdx.x + u * 2 * TR * T;
+        const int rr = idx >> LOGQ, m = idx & (Q - 1);
+        if (rr >= nr) continue;
+        const double2 ze = sm[2 * rr * XB + spad(m)];
+        const double2 zo = sm[(2 * rr + 1) * XB + spad(m)];
+        emit(rr, m, cadd(ze, zo));
+        if (CIRC) emit(rr, m + Q, csub(ze, zo));
     }
 }
 
