@@ -769,29 +769,31 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
         const bool live = rr < nr;
         const double2 W0 = __ldg(tw + ((2 * opaque(a0)) << shX));
         const double2 W1 = cmul(W0, __ldg(tw + (1 << shX)));
-#pragma unroll 4
-        for (int uu = 0; uu < R / 2; ++uu) {
-            const int a = a0 + 2 * T * uu;
-            const double2 Ae = E[spad(a)];
-            const double2 Be = cconj(E[spad((Q - a) & (Q - 1))]);
-            const double2 Ao = O[spad(a)];
-            const double2 Bo = cconj(O[spad(Q - 1 - a)]);
-            {
-                const double2 Fe = cscale(cadd(Ae, Be), 0.5);
-                const double2 D = csub(Ae, Be);
-                const double2 Fo = make_double2(0.5 * D.y, -0.5 * D.x);
-                if (live) dst[(int64_t)(2 * a) * Nrow] = cadd(Fe, cmul(tw32r<-1>(uu * (32 / R), W0), Fo));
-            }
-            {
-                const double2 Fe = cscale(cadd(Ao, Bo), 0.5);
-                const double2 D = csub(Ao, Bo);
-                const double2 Fo = make_double2(0.5 * D.y, -0.5 * D.x);
-                if (live) dst[(int64_t)(2 * a + 1) * Nrow] = cadd(Fe, cmul(tw32r<-1>(uu * (32 / R), W1), Fo));
+        // Mirrored pairs share their two SMEM reads: X[2a] and X[2Q-2a] both come
+        // from E[a], E[Q-a]; X[2a+1] and X[2Q-2a-1] from O[a], O[Q-1-a]; the
+        // mirrored twiddle is e^{-2 pi i (2Q-k)/Px} = -conj(e^{-2 pi i k/Px}).
+        auto post = [](double2 A, double2 B, double2 W) {
+            const double2 Fe = cscale(cadd(A, B), 0.5);
+            const double2 D = csub(A, B);
+            return cadd(Fe, cmul(W, make_double2(0.5 * D.y, -0.5 * D.x)));
+        };
+#pragma unroll 2
+        for (int uu = 0; uu < R / 4; ++uu) {
+            const int a = a0 + 2 * T * uu;  // a < Q/2
+            const double2 e1 = E[spad(a)], e2 = E[spad((Q - a) & (Q - 1))];
+            const double2 o1 = O[spad(a)], o2 = O[spad(Q - 1 - a)];
+            const double2 We = tw32r<-1>(uu * (32 / R), W0), Wo = tw32r<-1>(uu * (32 / R), W1);
+            const double2 Wem = make_double2(-We.x, We.y), Wom = make_double2(-Wo.x, Wo.y);
+            if (live) {
+                dst[(int64_t)(2 * a) * Nrow] = post(e1, cconj(e2), We);
+                dst[(int64_t)(2 * Q - 2 * a) * Nrow] = post(e2, cconj(e1), Wem);  // a = 0: Nyquist
+                dst[(int64_t)(2 * a + 1) * Nrow] = post(o1, cconj(o2), Wo);
+                dst[(int64_t)(2 * Q - 2 * a - 1) * Nrow] = post(o2, cconj(o1), Wom);
             }
         }
-        if (a0 == 0 && live) {  // Nyquist: X[halfP] = Re Z0 - Im Z0
-            const double2 A = E[0];
-            dst[(int64_t)halfP * Nrow] = make_double2(A.x - A.y, 0.0);
+        if (a0 == 0 && live) {  // kx = Q (a = Q/2, self-paired), W = e^{-i pi/2}
+            const double2 A = E[spad(Q / 2)];
+            dst[(int64_t)Q * Nrow] = post(A, cconj(A), make_double2(0.0, -1.0));
         }
         __syncthreads();  // spectra read: the buffers take the next tile's rows
         if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);

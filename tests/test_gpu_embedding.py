@@ -37,7 +37,7 @@ def test_embedding_choice(dims, M, bits, monkeypatch):
 
 @pytest.mark.parametrize("dims,M", [((64, 64), 3), ((32, 128), 2), ((128, 40), 4), ((40, 64), 3), ((16, 16), 7),
                                     ((16, 16, 16), 3), ((32, 16, 16), 2), ((16, 24, 32), 3), ((32, 32, 12), 2),
-                                    ((512, 37), 3), ((256, 20, 8), 2)])
+                                    ((512, 37), 3), ((256, 20, 8), 2), ((4096, 24), 3), ((2048, 20), 2)])
 def test_random_stencil_both_embeddings(dims, M, monkeypatch):
     rng = Rng(91 + M)
     o = Oracle(dims, h=0.5, M=M)
