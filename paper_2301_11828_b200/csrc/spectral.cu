@@ -704,8 +704,9 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
                                                           const double2* __restrict__ tw, int logTWN) {
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
-    constexpr int TR = 2;
-    static_assert(4 * T <= 256, "two rows of two transforms per 256-thread CTA");
+    constexpr int LOGTR = 11 - LOGQ;  // rows per tile: 2 * TR * T = 256 threads
+    constexpr int TR = 1 << LOGTR;
+    static_assert(LOGQ >= 4 && LOGQ <= 10, "2048/Q rows of two Q-point transforms per 256-thread CTA");
     extern __shared__ double2 sm[];
     constexpr int rowlen = CIRC ? 4 * Q : 2 * Q;          // staged doubles per row (>= Nx)
     constexpr int RS = (2 * 2 * XB > rowlen ? 2 * 2 * XB : rowlen);  // doubles per row buffer
@@ -733,7 +734,7 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
     };
     constexpr int LA = (2 * T >= 8) ? 3 : 0;
     const int rr = (threadIdx.x >> LA) & (TR - 1);
-    const int a0 = ((threadIdx.x >> (LA + 1)) << LA) + (threadIdx.x & ((1 << LA) - 1));
+    const int a0 = ((threadIdx.x >> (LA + LOGTR)) << LA) + (threadIdx.x & ((1 << LA) - 1));
     int64_t tile = blockIdx.x;
     if (tile < ntiles) fetch(tile);
     for (; tile < ntiles; tile += gridDim.x) {
@@ -803,10 +804,11 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
 
 static int k1_duo_smem(int logq, bool circ) {
     const int Q = 1 << logq;
+    const int TR = 2048 >> logq;
     const int XB = xbuf_slots(logq);
     const int rowlen = circ ? 4 * Q : 2 * Q;
     const int RS = std::max(2 * 2 * XB, rowlen);
-    return (int)sizeof(double) * (2 * RS + 4 * XB);
+    return (int)sizeof(double) * TR * (RS + 2 * XB);
 }
 
 constexpr int kPipeLogR = 4;  // 16 points per thread: 256 threads per 4096-point column
@@ -1371,7 +1373,7 @@ static void set_attrs_k1_l() {
     smem_attr((const void*)k_rfft_rows_pipe<L, 1, C>);
     smem_attr((const void*)k_rfft_rows_pipe<L, 2, C>);
     smem_attr((const void*)k_rfft_rows_pipe<L, 3, C>);
-    if constexpr (L == 10) smem_attr((const void*)k_rfft_rows_duo<L, C>);
+    if constexpr (L >= 6 && L <= 10) smem_attr((const void*)k_rfft_rows_duo<L, C>);
 }
 template <int... Ls>
 static void set_attrs_k1_all(std::integer_sequence<int, Ls...>) {
@@ -1389,13 +1391,18 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
     int TR = pl.k1_rows;
     const int T = threads_per_transform(lqx, 4);
     // two-CTA/SM variant: two rows of two transforms fill a 256-thread CTA
-    if ((Nx & 1) == 0 && 4 * T == 256 && !getenv("PDGPU_NO_K1_DUO")) {
+    if ((Nx & 1) == 0 && lqx >= 7 && lqx <= 10 && !getenv("PDGPU_NO_K1_DUO")) {  // lqx 6 (256-wide rows): the pipelined kernel measured faster
         const size_t dsm = (size_t)k1_duo_smem(lqx, cx);
+        const int DTR = 2048 >> lqx;
         if (2 * (dsm + 1024) <= 228 * 1024) {
-            const int64_t ntiles = (int64_t)((Ny + 1) / 2) * nslab;
+            const int64_t ntiles = (int64_t)((Ny + DTR - 1) / DTR) * nslab;
             const unsigned dgrid = (unsigned)std::min<int64_t>(ntiles, (int64_t)e.num_sms * 2);
 #define PDGPU_K1D(C) k_rfft_rows_duo<LQ, C><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, e.d_tw, pl.logTWN)
             switch (lqx) {
+                PDGPU_CASE(6, (cx ? PDGPU_K1D(true) : PDGPU_K1D(false)))
+                PDGPU_CASE(7, (cx ? PDGPU_K1D(true) : PDGPU_K1D(false)))
+                PDGPU_CASE(8, (cx ? PDGPU_K1D(true) : PDGPU_K1D(false)))
+                PDGPU_CASE(9, (cx ? PDGPU_K1D(true) : PDGPU_K1D(false)))
                 PDGPU_CASE(10, (cx ? PDGPU_K1D(true) : PDGPU_K1D(false)))
                 default: goto no_duo;
             }
