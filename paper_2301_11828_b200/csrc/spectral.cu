@@ -1468,9 +1468,11 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
     const bool cx = pl.circ[0] != 0;
     // padded rows: one row per CTA, two 256-thread CTAs co-reside per SM
     // (measured faster than two rows per CTA or a persistent double-buffered
-    // variant); periodic rows (half the length): two rows per 256-thread CTA
-    // (32-byte gather chunks), 2.87 vs 3.22 ms at 4096^2 x 16
-    int TR = pl.circ[0] ? std::min(2, pl.k1_rows) : 1;
+    // variant); periodic rows (half the length): several rows per CTA (wider
+    // gather chunks), 2.87 vs 3.22 ms at 4096^2 x 16
+    // periodic rows: up to 256 threads / 4 rows per CTA (measured at 1024..4096 x 16:
+    // 4096 -> 2 rows (2.73 ms), 2048 -> 4 rows (0.65 vs 0.68 ms with 2))
+    int TR = pl.circ[0] ? std::min(std::min(4, pl.k1_rows), std::max(1, 128 / threads_per_transform(pl.logQx, 4))) : 1;
     // short rows: at least 128 threads per CTA (up to the 8-row template limit)
     while (TR < pl.k1_rows && 2 * TR * threads_per_transform(pl.logQx, 4) < 128) TR *= 2;
     if (const char* env = getenv("PDGPU_K5_ROWS")) TR = std::max(1, std::min(pl.k1_rows, atoi(env)));
