@@ -370,6 +370,7 @@ def run_slab(args):
     for _ in range(args.warmup):
         sf.matvec(u, f)
     torch.cuda.synchronize()
+    launches0 = sf.eng.launch_count()
     clk = ClockSampler(local)
     clk.start()
     D.barrier()
@@ -384,6 +385,7 @@ def run_slab(args):
     D.barrier()
     clocks = clk.stop()
     ms_step = D.max_over_ranks(ev0.elapsed_time(ev1), "cuda") / args.steps
+    launches = sf.eng.launch_count() - launches0
     halo = 2 * M * N_SIDE * DIM * 8 * BATCH if world > 1 else 0
     if rank == 0:
         line = {"metric": METRIC, "value": BATCH * DIM * n / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
@@ -392,8 +394,9 @@ def run_slab(args):
                 "data": "synthetic (seeded uniform[-1,1], torch Philox)",
                 "config": {"workload": f"2D MSBFM K.u, {N_SIDE}x{N_SIDE} nodes, batch {BATCH}, row slabs",
                            "parallelism": f"{world} row slabs + {M}-row halo (NCCL send/recv)",
+                           "halo": sf.halo, "engine_rows": sf.L, "embedding_bits": sf.eng.embedding(),
                            "halo_bytes_per_rank_per_step": halo},
-                "clocks": clocks, "gpu_launches": None, "roofline": None, "cpu_baseline": None, "e2e": None}
+                "clocks": clocks, "gpu_launches": launches, "roofline": None, "cpu_baseline": None, "e2e": None}
         print(json.dumps(line))
     D.finalize()
     return 0

@@ -176,10 +176,16 @@ class SlabForce:
         b = u3.shape[0]
         ext, fext, g = self._buf(b)
         if self.halo == "ghost":
-            ext.copy_(u3)
-            self.exchange_ghosts(ext, g)
+            # the engine reads the owned rows in place and writes f directly
+            uc = u3 if u3.is_contiguous() else u3.contiguous()
+            self.exchange_ghosts(uc, g)
             self.eng.set_ghosts(g if self.world > 1 else None)
-            self.eng.matvec_device(ext, fext, b, stream=self._stream())
+            if f is not None:
+                f3 = f.unsqueeze(0) if squeeze else f
+                if f3.is_contiguous():
+                    self.eng.matvec_device(uc, f3, b, stream=self._stream())
+                    return f
+            self.eng.matvec_device(uc, fext, b, stream=self._stream())
             out = fext
         else:
             own = slice(self.gl * self.plane, (self.gl + self.R) * self.plane)
