@@ -387,6 +387,16 @@ int pdgpu_create(int dim, const int* dims, int M, const double* stencils, int de
         for (int d = 0; d < dim; ++d)
             if (dims[d] < M + 1)
                 throw PdError(PDGPU_ERR_HORIZON_TOO_LARGE, "need at least M+1 nodes per axis for the embedding");
+        {
+            // transform lengths the kernels are instantiated for (checked before touching the device):
+            // x rows up to 2 * 4096-point halves, columns up to 4096 points per transform (3D: 512)
+            Plan pl;
+            plan_init(pl, dim, dims, M);
+            const int lq = pl.logPl - (pl.nh == 2 ? 1 : 0);
+            const int lqy = dim == 3 ? pl.logP[1] - 1 : 0;
+            if (pl.logQx > 12 || lq > (dim == 2 ? 12 : 9) || lqy > 9)
+                throw PdError(PDGPU_ERR_NOT_SUPPORTED, "lattice too large for the single-CTA transform tiles");
+        }
         cuda_check(cudaSetDevice(device), "set device");
         auto* e = new pdgpu_engine();
         try {

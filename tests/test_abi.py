@@ -66,3 +66,17 @@ def test_band_offsets_order():
     assert o.L.orc_offsets(2, 3, offs.ctypes.data_as(C.POINTER(C.c_int))) == 28
     assert np.array_equal(band_offsets(2, 3), offs)
     assert len(band_offsets(3, 3)) == 122
+
+
+@pytest.mark.parametrize("dims", [(64, 8192), (32768, 16), (1024, 1024, 1024), (64, 64, 2048)])
+def test_lattice_too_large_is_refused_before_the_device(dims):
+    """Transform lengths beyond the instantiated kernels: a clean
+    PDGPU_ERR_NOT_SUPPORTED from pdgpu_create, without touching the device."""
+    from paper_2301_11828_b200 import _lib
+    lib = _lib.load()
+    out = C.c_void_p()
+    d = (C.c_int * len(dims))(*dims)
+    K = np.zeros(6 * 7 ** len(dims))
+    rc = lib.pdgpu_create(len(dims), d, 3, K.ctypes.data_as(_lib.c_double_p), 0, C.byref(out))
+    assert rc == 7  # PDGPU_ERR_NOT_SUPPORTED
+    assert b"too large" in lib.pdgpu_last_error()
