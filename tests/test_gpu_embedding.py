@@ -37,7 +37,8 @@ def test_embedding_choice(dims, M, bits, monkeypatch):
 
 @pytest.mark.parametrize("dims,M", [((64, 64), 3), ((32, 128), 2), ((128, 40), 4), ((40, 64), 3), ((16, 16), 7),
                                     ((16, 16, 16), 3), ((32, 16, 16), 2), ((16, 24, 32), 3), ((32, 32, 12), 2),
-                                    ((512, 37), 3), ((256, 20, 8), 2), ((4096, 24), 3), ((2048, 20), 2)])
+                                    ((512, 37), 3), ((256, 20, 8), 2), ((4096, 24), 3), ((2048, 20), 2),
+                                    ((8192, 16), 2)])
 def test_random_stencil_both_embeddings(dims, M, monkeypatch):
     rng = Rng(91 + M)
     o = Oracle(dims, h=0.5, M=M)
@@ -51,6 +52,23 @@ def test_random_stencil_both_embeddings(dims, M, monkeypatch):
     assert rel(got_p, want) <= TOL
     assert rel(got_z, want) <= TOL
     assert rel(got_p, got_z) <= TOL
+
+
+def test_longest_periodic_rows(monkeypatch):
+    """16384-node rows: the periodic embedding's longest x transform (2 x 4096-point
+    halves through the unpipelined K1, whose staging would not fit); the padded
+    embedding of the same lattice is refused (NOT_SUPPORTED) at create time."""
+    from paper_2301_11828_b200 import FastForce
+    rng = Rng(97)
+    o = Oracle((16384, 16), h=0.5, M=2)
+    o.random_kernel(rng)
+    u = random_field(rng, 2, o.n)
+    ff = make(o, "periodic", monkeypatch)
+    assert ff.embedding() == 3
+    assert rel(ff.apply(u), o.apply(u)) <= TOL
+    monkeypatch.setenv("PDGPU_EMBED", "padded")
+    with pytest.raises(NotImplementedError):
+        FastForce(o.dims, o.M, o.kernel())
 
 
 @pytest.mark.parametrize("dims", [(128, 128), (256, 64), (32, 32, 32)])
