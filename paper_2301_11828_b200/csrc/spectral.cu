@@ -21,6 +21,7 @@
 // for the physical (even) stencils, complex for arbitrary ones (the
 // reference's random-stencil tests).  Layout [col][half][k][pair] so each
 // thread reads its n_pairs coefficients contiguously.
+#include <cuda.h>  // CUtensorMap (encoded through the runtime's driver entry point, no libcuda link)
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdlib.h>
@@ -270,12 +271,24 @@ __global__ void __launch_bounds__(512) k_rfft_rows(const double* __restrict__ u,
 // h = Px/2; z = IFFT_{2Qx}(Z) on its first Qx outputs = E'[n] + e^{+2 pi i n/(2Qx)} O'[n];
 // x[2n] = Re z, x[2n+1] = Im z.  CIRC (Px = Nx): all 2Qx outputs are kept,
 // z[n + Qx] = E'[n] - e^{+2 pi i n/(2Qx)} O'[n].
-template <int LOGQ, int LOGTR, bool CIRC>
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* m, void* dst, uint64_t* bar, int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(m), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
+
+// TMAG: the tile's [kx][row] spectrum block lands in SMEM through TMA boxes
+// ({2*TR doubles, 256 kx} per box, the box tensor map tm over S) instead of
+// per-thread global gathers; the pre-processing then reads it from SMEM.
+template <int LOGQ, int LOGTR, bool CIRC, bool TMAG = false>
 __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ S, double* __restrict__ f, int Nx,
                                                     int Nrow, int Nz, int dim, int Hx,
                                                     const double2* __restrict__ tw, int logTWN, double scale,
                                                     const uint8_t* __restrict__ cmask,
-                                                    const double* __restrict__ body, int64_t nodes) {
+                                                    const double* __restrict__ body, int64_t nodes,
+                                                    const __grid_constant__ CUtensorMap tm) {
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
     constexpr int TR = 1 << LOGTR;
@@ -305,12 +318,36 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
         const double2 W0 = twiddle<1>(tw, (2 * j0) << shX);
         const double2 W1 = cmul(W0, twiddle<1>(tw, 1 << shX));
         double2 Xa[U], Xb[U];
+        double2 xq = make_double2(0.0, 0.0);
+        if constexpr (TMAG) {
+            __shared__ __align__(8) uint64_t bar;
+            double2* land = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(sm) + 127) & ~uintptr_t(127));
+            const int nbox = (Hx + 255) / 256;
+            if (threadIdx.x == 0) mbar_init(&bar, 1);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                mbar_expect_tx(&bar, (unsigned)(nbox * 256 * TR * 16));
+                for (int bx = 0; bx < nbox; ++bx) tma_load_3d(&tm, land + bx * 256 * TR, &bar, 2 * row0, bx * 256, slab);
+            }
+            mbar_wait(&bar, 0);
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int j = j0 + 2 * T * u;
-            const int k = j < Q / 2 ? 2 * j : 2 * (j - Q / 2) + 1;
-            Xa[u] = live ? src[(int64_t)k * Nrow + rr] : make_double2(0.0, 0.0);
-            Xb[u] = live ? src[(int64_t)(halfP - k) * Nrow + rr] : make_double2(0.0, 0.0);
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + 2 * T * u;
+                const int k = j < Q / 2 ? 2 * j : 2 * (j - Q / 2) + 1;
+                Xa[u] = land[k * TR + rr];
+                Xb[u] = land[(halfP - k) * TR + rr];
+            }
+            if (threadIdx.x < nr) xq = land[Q * TR + threadIdx.x];
+            __syncthreads();  // the landing area is about to be overwritten by E / O
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + 2 * T * u;
+                const int k = j < Q / 2 ? 2 * j : 2 * (j - Q / 2) + 1;
+                Xa[u] = live ? src[(int64_t)k * Nrow + rr] : make_double2(0.0, 0.0);
+                Xb[u] = live ? src[(int64_t)(halfP - k) * Nrow + rr] : make_double2(0.0, 0.0);
+            }
+            if (threadIdx.x < nr) xq = src[(int64_t)Q * Nrow + threadIdx.x];
         }
         double2* E = sm + 2 * rr * XB;
         double2* O = E + XB;
@@ -342,7 +379,6 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
         }
         // Nyquist k = Q (self-paired, W = e^{i pi/2} = i) -> E[Q/2]
         if (threadIdx.x < nr) {
-            const double2 xq = src[(int64_t)Q * Nrow + threadIdx.x];
             const double2 s1 = cadd(xq, cconj(xq));
             const double2 t1 = cmul(make_double2(0.0, 1.0), csub(xq, cconj(xq)));
             sm[2 * threadIdx.x * XB + (Q & 1) * XB + spad(Q >> 1)] = make_double2(s1.x - t1.y, s1.y + t1.x);
@@ -1324,7 +1360,11 @@ static void check(cudaError_t e, const char* what) {
 }
 
 static void smem_attr(const void* fn) {
-    check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448), "smem attr");
+    cudaFuncAttributes fa;
+    check(cudaFuncGetAttributes(&fa, fn), "func attributes");
+    // the 227 KB per-block limit covers static + dynamic shared memory
+    check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448 - (int)fa.sharedSizeBytes),
+          "smem attr");
 }
 
 
@@ -1445,12 +1485,38 @@ no_duo:
 #endif
 
 #if defined(PDGPU_ALL_PARTS) || PDGPU_PART == 2
+// box tensor map over S[slab][kx][row] (complex): dims {2*Nrow doubles, Hx, nslab},
+// box {2*TR doubles, 256 kx, 1}; cuTensorMapEncodeTiled through the runtime's
+// driver entry point
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static bool encode_k5_map(CUtensorMap& m, const double2* S, int Nrow, int Hx, int nslab, int TR) {
+    static EncodeTiledFn enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            enc = nullptr;
+            return false;
+        }
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)2 * Nrow, (cuuint64_t)Hx, (cuuint64_t)nslab};
+    cuuint64_t strides[2] = {(cuuint64_t)Nrow * 16, (cuuint64_t)Hx * Nrow * 16};
+    cuuint32_t box[3] = {(cuuint32_t)(2 * TR), 256, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)S, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int L, bool C>
 static void set_attrs_k5_l() {
     smem_attr((const void*)k_irfft_rows<L, 0, C>);
     smem_attr((const void*)k_irfft_rows<L, 1, C>);
     smem_attr((const void*)k_irfft_rows<L, 2, C>);
     smem_attr((const void*)k_irfft_rows<L, 3, C>);
+    if constexpr (C && L >= 8) smem_attr((const void*)k_irfft_rows<L, 1, C, true>);
 }
 template <int... Ls>
 static void set_attrs_k5_all(std::integer_sequence<int, Ls...>) {
@@ -1473,16 +1539,43 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
     // periodic rows: up to 256 threads / 4 rows per CTA (measured at 1024..4096 x 16:
     // 4096 -> 2 rows (2.73 ms), 2048 -> 4 rows (0.65 vs 0.68 ms with 2))
     int TR = pl.circ[0] ? std::min(std::min(4, pl.k1_rows), std::max(1, 128 / threads_per_transform(pl.logQx, 4))) : 1;
+    const char* tenv = getenv("PDGPU_K5_TMA");
+    const bool use_tma = !(tenv && tenv[0] == '0');
+    // TMA-landed gathers run two rows per CTA (1024..4096-wide rows: 0.146 -> 0.131,
+    // 0.673 -> 0.560, 2.74 -> 2.49 ms at batch 16)
+    const bool tma_rows = pl.circ[0] && pl.logQx >= 8 && use_tma && pl.k1_rows >= 2;
+    if (tma_rows) TR = 2;
     // short rows: at least 128 threads per CTA (up to the 8-row template limit)
-    while (TR < pl.k1_rows && 2 * TR * threads_per_transform(pl.logQx, 4) < 128) TR *= 2;
+    while (!tma_rows && TR < pl.k1_rows && 2 * TR * threads_per_transform(pl.logQx, 4) < 128) TR *= 2;
     if (const char* env = getenv("PDGPU_K5_ROWS")) TR = std::max(1, std::min(pl.k1_rows, atoi(env)));
     while (TR & (TR - 1)) TR &= TR - 1;  // power of two (template)
     const int ltr = TR == 8 ? 3 : TR == 4 ? 2 : TR == 2 ? 1 : 0;
     const int T = threads_per_transform(lqx, 4);
     dim3 grid((Ny + TR - 1) / TR, nslab);
     const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_slots(lqx);
+    CUtensorMap tm;
+    memset(&tm, 0, sizeof(tm));
+    // TMA-landed gathers (periodic rows, two per CTA; PDGPU_K5_TMA=0 disables)
+    if (cx && TR == 2 && lqx >= 8 && use_tma && encode_k5_map(tm, xin, Ny, pl.Hx, nslab, TR)) {
+        const int nbox = (pl.Hx + 255) / 256;
+        const size_t tsm = std::max(smem, sizeof(double2) * (size_t)nbox * 256 * TR) + 128;
+        switch (lqx) {
+            PDGPU_CASE(8, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm)))
+            PDGPU_CASE(9, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm)))
+            PDGPU_CASE(10, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm)))
+            PDGPU_CASE(11, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm)))
+            PDGPU_CASE(12, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm)))
+            default: break;
+        }
+        return;
+    }
 #define PDGPU_K5(LT, C) k_irfft_rows<LQ, LT, C><<<grid, 2 * TR * T, smem, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx, e.d_tw, \
-                                                                          pl.logTWN, scale, cmask, body, pl.nodes)
+                                                                          pl.logTWN, scale, cmask, body, pl.nodes, tm)
 #define PDGPU_K5C(C) (ltr == 3 ? PDGPU_K5(3, C) : ltr == 2 ? PDGPU_K5(2, C) : ltr == 1 ? PDGPU_K5(1, C) : PDGPU_K5(0, C))
     if (cx) PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(true))
     else PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(false))
