@@ -756,10 +756,27 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
     constexpr int halfP = 2 * Q;
     const int groups = (Nrow + TR - 1) / TR;
     const int64_t ntiles = (int64_t)groups * nslab;
+    // rows exactly fill the staging length (periodic, or padded power-of-two
+    // rows): one TMA bulk copy per row, else per-thread cp.async with zero fill
+    const bool bulk = Nx == rowlen;
+    __shared__ __align__(8) uint64_t bar;
+    if (bulk) {
+        if (threadIdx.x == 0) mbar_init(&bar, 1);
+        __syncthreads();
+    }
+    unsigned ph = 0;
     auto fetch = [&](int64_t tile) {
         const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
         const int nr = min(TR, Nrow - row0);
         const double* src = u + ((int64_t)slab * Nrow + row0) * Nx;
+        if (bulk) {
+            if (threadIdx.x == 0) {
+                fence_proxy_async();
+                mbar_expect_tx(&bar, (unsigned)(nr * rowlen * 8));
+                for (int rr = 0; rr < nr; ++rr) bulk_load(rowbuf + rr * RS, src + (int64_t)rr * Nx, rowlen * 8, &bar);
+            }
+            return;
+        }
         constexpr int chunks_per_row = rowlen / 2;
         for (int c = threadIdx.x; c < TR * chunks_per_row; c += blockDim.x) {
             const int rr = c / chunks_per_row, i0 = 2 * (c - rr * chunks_per_row);
@@ -777,7 +794,12 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
         const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
         const int nr = min(TR, Nrow - row0);
         double2 v[R];
-        cp_async_wait_all();
+        if (bulk) {
+            mbar_wait(&bar, ph);  // rows past the lattice (nr < TR) hold stale data: never stored
+            ph ^= 1;
+        } else {
+            cp_async_wait_all();
+        }
         __syncthreads();
         {
             const double* st = rowbuf + r * RS;
