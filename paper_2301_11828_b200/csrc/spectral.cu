@@ -118,6 +118,31 @@ constexpr int kSmemBudget = 210 * 1024;
 static int xbuf_slots(int logq) { return (1 << logq) + ((1 << logq) >> 4) + 1; }
 static int threads_per_transform(int logq, int logrmax) { return 1 << std::max(0, logq - logrmax); }
 
+// box tensor map over S[slab][kx][row] (complex): dims {2*Nrow doubles, Hx, nslab},
+// box {2*TR doubles, 256 kx, 1}; cuTensorMapEncodeTiled through the runtime's
+// driver entry point
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static bool encode_box_map(CUtensorMap& m, const double2* S, int Nrow, int Hx, int nslab, int TR) {
+    static EncodeTiledFn enc = nullptr;
+    if (!enc) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            enc = nullptr;
+            return false;
+        }
+    }
+    cuuint64_t dims[3] = {(cuuint64_t)2 * Nrow, (cuuint64_t)Hx, (cuuint64_t)nslab};
+    cuuint64_t strides[2] = {(cuuint64_t)Nrow * 16, (cuuint64_t)Hx * Nrow * 16};
+    cuuint32_t box[3] = {(cuuint32_t)(2 * TR), 256, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)S, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 #if defined(PDGPU_ALL_PARTS) || PDGPU_PART == 0
 void plan_init(Plan& pl, int dim, const int* dims, int M) {
     pl.dim = dim;
@@ -734,10 +759,21 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
 // staging area of the input row and then as the natural-order spectrum the
 // R2C post-processing reads.  The next tile's rows are fetched after the
 // post-processing; its latency is covered by the other CTA on the SM.
-template <int LOGQ, bool CIRC>
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* src, int x, int y, int z) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(m),
+                 "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z)
+                 : "memory");
+}
+
+// TSTORE: the tile's [kx][row] spectrum block is assembled in SMEM (over the
+// row buffers, after every spectrum value has been read into registers) and
+// written by TMA boxes ({2*TR doubles, 256 kx}, tensor map tm over S) instead of
+// per-thread scattered stores.
+template <int LOGQ, bool CIRC, bool TSTORE = false>
 __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restrict__ u, double2* __restrict__ S,
                                                           int Nx, int Nrow, int nslab, int Hx,
-                                                          const double2* __restrict__ tw, int logTWN) {
+                                                          const double2* __restrict__ tw, int logTWN,
+                                                          const __grid_constant__ CUtensorMap tm) {
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
     constexpr int LOGTR = 11 - LOGQ;  // rows per tile: 2 * TR * T = 256 threads
@@ -836,6 +872,44 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
             const double2 D = csub(A, B);
             return cadd(Fe, cmul(W, make_double2(0.5 * D.y, -0.5 * D.x)));
         };
+        if constexpr (TSTORE) {
+            constexpr int NU = R / 4;
+            double2 e1[NU], e2[NU], o1[NU], o2[NU];
+#pragma unroll
+            for (int uu = 0; uu < NU; ++uu) {
+                const int a = a0 + 2 * T * uu;
+                e1[uu] = E[spad(a)];
+                e2[uu] = E[spad((Q - a) & (Q - 1))];
+                o1[uu] = O[spad(a)];
+                o2[uu] = O[spad(Q - 1 - a)];
+            }
+            const double2 Aq = E[spad(Q / 2)];
+            __syncthreads();  // every spectrum value is in registers: the block overwrites them
+            double2* ob = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(sm) + 127) & ~uintptr_t(127));
+#pragma unroll
+            for (int uu = 0; uu < NU; ++uu) {
+                const int a = a0 + 2 * T * uu;
+                const double2 We = tw32r<-1>(uu * (32 / R), W0), Wo = tw32r<-1>(uu * (32 / R), W1);
+                const double2 Wem = make_double2(-We.x, We.y), Wom = make_double2(-Wo.x, Wo.y);
+                ob[(2 * a) * TR + rr] = post(e1[uu], cconj(e2[uu]), We);
+                ob[(2 * Q - 2 * a) * TR + rr] = post(e2[uu], cconj(e1[uu]), Wem);
+                ob[(2 * a + 1) * TR + rr] = post(o1[uu], cconj(o2[uu]), Wo);
+                ob[(2 * Q - 2 * a - 1) * TR + rr] = post(o2[uu], cconj(o1[uu]), Wom);
+            }
+            if (a0 == 0) ob[Q * TR + rr] = post(Aq, cconj(Aq), make_double2(0.0, -1.0));
+            fence_proxy_async();
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const int nbox = (Hx + 255) / 256;
+                for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm, ob + bx * 256 * TR, 2 * row0, bx * 256, slab);
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                // the block region takes the next tile's rows: wait until the stores have read it
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+            __syncthreads();
+            if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);
+            continue;
+        }
 #pragma unroll 2
         for (int uu = 0; uu < R / 4; ++uu) {
             const int a = a0 + 2 * T * uu;  // a < Q/2
@@ -858,6 +932,7 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
         if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);
     }
     cp_async_wait_all();
+    if (TSTORE && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 static int k1_duo_smem(int logq, bool circ) {
@@ -866,7 +941,9 @@ static int k1_duo_smem(int logq, bool circ) {
     const int XB = xbuf_slots(logq);
     const int rowlen = circ ? 4 * Q : 2 * Q;
     const int RS = std::max(2 * 2 * XB, rowlen);
-    return (int)sizeof(double) * TR * (RS + 2 * XB);
+    // + alignment slack for the TMA-store block (it may run past the row
+    // buffers into the exchange buffer, free at that point)
+    return (int)sizeof(double) * TR * (RS + 2 * XB) + 128;
 }
 
 constexpr int kPipeLogR = 4;  // 16 points per thread: 256 threads per 4096-point column
@@ -1436,6 +1513,7 @@ static void set_attrs_k1_l() {
     smem_attr((const void*)k_rfft_rows_pipe<L, 2, C>);
     smem_attr((const void*)k_rfft_rows_pipe<L, 3, C>);
     if constexpr (L >= 6 && L <= 10) smem_attr((const void*)k_rfft_rows_duo<L, C>);
+    if constexpr (C && L == 10) smem_attr((const void*)k_rfft_rows_duo<L, C, true>);
 }
 template <int... Ls>
 static void set_attrs_k1_all(std::integer_sequence<int, Ls...>) {
@@ -1459,7 +1537,18 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
         if (2 * (dsm + 1024) <= 228 * 1024) {
             const int64_t ntiles = (int64_t)((Ny + DTR - 1) / DTR) * nslab;
             const unsigned dgrid = (unsigned)std::min<int64_t>(ntiles, (int64_t)e.num_sms * 2);
-#define PDGPU_K1D(C) k_rfft_rows_duo<LQ, C><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, e.d_tw, pl.logTWN)
+            CUtensorMap tm;
+            memset(&tm, 0, sizeof(tm));
+            // TMA-stored spectrum blocks (periodic 4096-wide rows, two per tile:
+            // K1 2.71 -> 2.32 ms at 4096^2 x 16; neutral at 2048, slower at 1024):
+            // PDGPU_K1_TMA=0 disables
+            const char* tenv = getenv("PDGPU_K1_TMA");
+            const bool tst = cx && DTR <= 2 && !(tenv && tenv[0] == '0') && encode_box_map(tm, e.d_S1, Ny, pl.Hx, nslab, DTR) &&
+                             (size_t)(((pl.Hx + 255) / 256) * 256 * DTR * 16 + 128) <= dsm;
+#define PDGPU_K1D(C) (tst ? k_rfft_rows_duo<LQ, true, true><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, \
+                                                                      e.d_tw, pl.logTWN, tm)                    \
+                      : k_rfft_rows_duo<LQ, C><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, e.d_tw, \
+                                                                      pl.logTWN, tm))
             switch (lqx) {
                 PDGPU_CASE(6, (cx ? PDGPU_K1D(true) : PDGPU_K1D(false)))
                 PDGPU_CASE(7, (cx ? PDGPU_K1D(true) : PDGPU_K1D(false)))
@@ -1507,31 +1596,6 @@ no_duo:
 #endif
 
 #if defined(PDGPU_ALL_PARTS) || PDGPU_PART == 2
-// box tensor map over S[slab][kx][row] (complex): dims {2*Nrow doubles, Hx, nslab},
-// box {2*TR doubles, 256 kx, 1}; cuTensorMapEncodeTiled through the runtime's
-// driver entry point
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static bool encode_k5_map(CUtensorMap& m, const double2* S, int Nrow, int Hx, int nslab, int TR) {
-    static EncodeTiledFn enc = nullptr;
-    if (!enc) {
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q) != cudaSuccess ||
-            q != cudaDriverEntryPointSuccess) {
-            enc = nullptr;
-            return false;
-        }
-    }
-    cuuint64_t dims[3] = {(cuuint64_t)2 * Nrow, (cuuint64_t)Hx, (cuuint64_t)nslab};
-    cuuint64_t strides[2] = {(cuuint64_t)Nrow * 16, (cuuint64_t)Hx * Nrow * 16};
-    cuuint32_t box[3] = {(cuuint32_t)(2 * TR), 256, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)S, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
 template <int L, bool C>
 static void set_attrs_k5_l() {
     smem_attr((const void*)k_irfft_rows<L, 0, C>);
@@ -1578,7 +1642,7 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
     CUtensorMap tm;
     memset(&tm, 0, sizeof(tm));
     // TMA-landed gathers (periodic rows, two per CTA; PDGPU_K5_TMA=0 disables)
-    if (cx && TR == 2 && lqx >= 8 && use_tma && encode_k5_map(tm, xin, Ny, pl.Hx, nslab, TR)) {
+    if (cx && TR == 2 && lqx >= 8 && use_tma && encode_box_map(tm, xin, Ny, pl.Hx, nslab, TR)) {
         const int nbox = (pl.Hx + 255) / 256;
         const size_t tsm = std::max(smem, sizeof(double2) * (size_t)nbox * 256 * TR) + 128;
         switch (lqx) {
