@@ -555,7 +555,7 @@ size_t pdgpu_footprint_bytes(pdgpu_t h) {
     const Plan& pl = h->plan;
     const int64_t N = pl.nodes;
     size_t b = 0;
-    if (h->d_sym) b += (size_t)pl.ncols * pl.Pl * h->np * (h->real_symbol ? 8 : 16);
+    if (h->d_sym) b += (size_t)pl.ncols * pl.Pl * (h->dim == 2 && h->real_symbol ? 4 : h->np) * (h->real_symbol ? 8 : 16);
     if (h->d_coltab) b += (size_t)pl.ncols * h->np * (h->M + 1) * 8;
     b += (size_t)(16 * (1 << pl.logTWN));
     b += (size_t)h->cap_batch * 16 * (pl.S1_per_vec + ((pl.dim == 3 || pl.k3_halves == 1) ? pl.S2_per_vec : 0));

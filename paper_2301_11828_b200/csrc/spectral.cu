@@ -491,10 +491,18 @@ __device__ __forceinline__ void symbol_product(double2* F, const double2* U, con
                                                int64_t fidx) {
     constexpr int NP = D * (D + 1) / 2;
     if (REAL) {
-        const double* H = (const double*)sym + fidx * NP;
-        double g[NP];
+        double g[NP > 3 ? NP : 4];
+        if constexpr (D == 2) {
+            // 2D real symbol: 4 doubles per frequency (xx, xy, yy, 0), one 32-byte load
+            const double* H = (const double*)sym + fidx * 4;
+            asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                : "=d"(g[0]), "=d"(g[1]), "=d"(g[2]), "=d"(g[3])
+                : "l"(H));
+        } else {
+            const double* H = (const double*)sym + fidx * NP;
 #pragma unroll
-        for (int p = 0; p < NP; ++p) g[p] = __ldg(H + p);
+            for (int p = 0; p < NP; ++p) g[p] = __ldg(H + p);
+        }
 #pragma unroll
         for (int a = 0; a < D; ++a) {
             double2 acc = make_double2(0.0, 0.0);
@@ -1188,8 +1196,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
                         // x_1, this half's symbol rows, and z^0 for the half-1 update
                         l2_prefetch(x0 + cstride, xbytes);
                         if (SYM != 2)
-                            l2_prefetch((const char*)sym + (((int64_t)cc * NH + h) * Q) * 3 * (SYM == 1 ? 8 : 16),
-                                        (unsigned)Q * 3 * (SYM == 1 ? 8 : 16));
+                            l2_prefetch((const char*)sym + (((int64_t)cc * NH + h) * Q) * (SYM == 1 ? 4 * 8 : 3 * 16),
+                                        (unsigned)Q * (SYM == 1 ? 4 * 8 : 3 * 16));
                         if (NH == 2 && h) {
                             l2_prefetch(z0, xbytes);
                             l2_prefetch(z0 + cstride, xbytes);
@@ -1393,7 +1401,7 @@ __global__ void __launch_bounds__(512) k_cfft_y_inv(const double2* __restrict__ 
 // Output layout [col][h][k][pair], ky = 2k + h.
 #if defined(PDGPU_ALL_PARTS) || PDGPU_PART == 0
 __global__ void k_build_symbol(void* sym, const double* __restrict__ K, int dim, int M, int np, int64_t ss,
-                               int ncols, int Pl, int P0, int P1, int P2, int real, double scale, int NH) {
+                               int ncols, int Pl, int P0, int P1, int P2, int real, double scale, int NH, int ns) {
     const int64_t nfreq = (int64_t)ncols * Pl;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= nfreq) return;
@@ -1445,10 +1453,13 @@ __global__ void k_build_symbol(void* sym, const double* __restrict__ K, int dim,
             }
         }
     const int Ql = Pl / NH;
-    const int64_t o = (((int64_t)col * NH + (kl % NH)) * Ql + kl / NH) * np;
+    const int64_t o = (((int64_t)col * NH + (kl % NH)) * Ql + kl / NH) * ns;
     for (int p = 0; p < np; ++p) {
         if (real) ((double*)sym)[o + p] = acc[p].x * scale;
         else ((double2*)sym)[o + p] = make_double2(acc[p].x * scale, acc[p].y * scale);
+    }
+    for (int p = np; p < ns; ++p) {  // padding of the 2D real layout
+        if (real) ((double*)sym)[o + p] = 0.0;
     }
 }
 #endif
@@ -1884,13 +1895,15 @@ void build_symbol(Engine& e) {
     const Plan& pl = e.plan;
     const int64_t nfreq = (int64_t)pl.ncols * pl.Pl;
     const size_t elt = e.real_symbol ? sizeof(double) : sizeof(double2);
+    // 2D real symbols are stored 4 doubles per frequency (one 32-byte load, symbol_product)
+    const int ns = (e.dim == 2 && e.real_symbol) ? 4 : e.np;
     if (e.d_sym) cudaFree(e.d_sym);
-    check(cudaMalloc(&e.d_sym, elt * nfreq * e.np), "alloc symbol");
+    check(cudaMalloc(&e.d_sym, elt * nfreq * ns), "alloc symbol");
     const double scale = 1.0 / ((double)pl.P[0] * (double)pl.P[1] * (double)pl.P[2]);
     const int th = 128;
     const int64_t blocks = (nfreq + th - 1) / th;
     k_build_symbol<<<(unsigned)blocks, th, 0, e.stream>>>(e.d_sym, e.d_K, e.dim, e.M, e.np, e.ss, pl.ncols, pl.Pl,
-                                                         pl.P[0], pl.P[1], pl.P[2], e.real_symbol ? 1 : 0, scale, pl.nh);
+                                                         pl.P[0], pl.P[1], pl.P[2], e.real_symbol ? 1 : 0, scale, pl.nh, ns);
     check(cudaGetLastError(), "build_symbol launch");
     check(cudaStreamSynchronize(e.stream), "build_symbol");
 }
