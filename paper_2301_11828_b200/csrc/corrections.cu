@@ -122,6 +122,24 @@ static void check(cudaError_t e, const char* what) {
 // entries the symbol is built from, so arbitrary stencils stay exact).
 // f_a[p] -= scale * sum_o sum_b K_ab(o) u_b[wrap(p+o)] on rows not
 // constrained in a (K5 has zeroed those).
+// 3D: the x-face strips u[b][c][z][y][x in [0,2M) u [N0-2M,N0)] copied to
+// strip[b][c][slot][z][y] (slot = x for the low side, 2M + x - (N0-2M) for the
+// high side), so the x-band's aliased reads -- a warp spans consecutive y --
+// are unit-stride instead of one cache line per lane.
+__global__ void k_xstrip(const double* __restrict__ u, double* __restrict__ strip, int N0, int N1, int N2, int M,
+                         int64_t nrows) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // ((b*3 + c)*N2 + z)*N1 + y
+    if (i >= nrows) return;
+    const int64_t plane = (int64_t)N1 * N2;
+    const int64_t bc = i / plane, zy = i - bc * plane;
+    const double* row = u + i * N0;
+    double* dst = strip + bc * 4 * M * plane + zy;
+    for (int x = 0; x < 2 * M; ++x) {
+        dst[(int64_t)x * plane] = row[x];
+        dst[(int64_t)(2 * M + x) * plane] = row[N0 - 2 * M + x];
+    }
+}
+
 template <int D>
 __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, double* __restrict__ f,
                                               const int* __restrict__ wrows, const int* __restrict__ wo0,
@@ -130,7 +148,7 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
                                               int batch, double scale, int64_t band0, int64_t band1, int64_t band2,
                                               const double* __restrict__ ghost, int lo_int, int hi_int,
                                               const int* __restrict__ lidx, const int* __restrict__ loff,
-                                              const double* __restrict__ lK) {
+                                              const double* __restrict__ lK, const double* __restrict__ xstrip) {
     constexpr int NP = D * (D + 1) / 2;
     const int64_t per_vec = band0 + band1 + band2;
     const int64_t gidx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -211,11 +229,21 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
                     kv[2 * k + 1] = v2.y;
                 }
                 if (per) {
-                    const int64_t q = ((int64_t)(q2 + (ax == 2 ? wrapd : 0)) * N1 + q1 + (ax == 1 ? wrapd : 0)) * N0 +
-                                      q0 + (ax == 0 ? wrapd : 0);
                     double uq[D];
+                    if (D == 3 && ax == 0 && xstrip) {
+                        // x-face strip: slot of the wrapped x, [b][c][slot][z][y]
+                        const int slot = sd ? q0 - N0 : q0 + 4 * M;  // x = q0 - N0 (low strip) or q0 + N0 (high)
+                        const int64_t pl = (int64_t)N1 * N2;
+                        const double* sp = xstrip + (int64_t)b * D * 4 * M * pl + (int64_t)slot * pl +
+                                           (int64_t)q2 * N1 + q1;
 #pragma unroll
-                    for (int bb = 0; bb < D; ++bb) uq[bb] = ub[(int64_t)bb * nodes + q];
+                        for (int bb = 0; bb < D; ++bb) uq[bb] = sp[(int64_t)bb * 4 * M * pl];
+                    } else {
+                        const int64_t q = ((int64_t)(q2 + (ax == 2 ? wrapd : 0)) * N1 + q1 + (ax == 1 ? wrapd : 0)) * N0 +
+                                          q0 + (ax == 0 ? wrapd : 0);
+#pragma unroll
+                        for (int bb = 0; bb < D; ++bb) uq[bb] = ub[(int64_t)bb * nodes + q];
+                    }
 #pragma unroll
                     for (int a = 0; a < D; ++a)
 #pragma unroll
@@ -432,14 +460,21 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
     if (!e.d_wrows) build_wrap_table(e);
     const int th = 128;
     const unsigned blocks = (unsigned)((tot + th - 1) / th);
+    const double* xstrip = nullptr;
+    if (pl.dim == 3 && pl.circ[0] && e.d_xstrip && batch <= e.cap_batch && 4 * e.M <= pl.N[0]) {
+        const int64_t nrows = (int64_t)batch * 3 * pl.N[1] * pl.N[2];
+        k_xstrip<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(u, e.d_xstrip, pl.N[0], pl.N[1], pl.N[2], e.M, nrows);
+        xstrip = e.d_xstrip;
+        e.launches += 1;
+    }
     if (pl.dim == 2)
         k_wrap<2><<<blocks, th, 0, s>>>(u, f, e.d_wrows, e.d_wo0, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],
                                         pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2],
-                                        ghost, lo_int, hi_int, e.d_lidx, e.d_loff, e.d_lK);
+                                        ghost, lo_int, hi_int, e.d_lidx, e.d_loff, e.d_lK, nullptr);
     else
         k_wrap<3><<<blocks, th, 0, s>>>(u, f, e.d_wrows, e.d_wo0, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],
                                         pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2],
-                                        ghost, lo_int, hi_int, e.d_lidx, e.d_loff, e.d_lK);
+                                        ghost, lo_int, hi_int, e.d_lidx, e.d_loff, e.d_lK, xstrip);
 }
 
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale) {

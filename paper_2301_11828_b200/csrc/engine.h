@@ -96,6 +96,7 @@ struct Engine {
     int64_t cap_batch = 0;
     double2* d_S1 = nullptr;
     double2* d_S2 = nullptr;
+    double* d_xstrip = nullptr;     // 3D wrap correction: the 2M-wide x-face strips, [b][c][slot][z][y]
     double* d_u_stage = nullptr;    // host-API staging
     double* d_f_stage = nullptr;
     int64_t stage_cap = 0;

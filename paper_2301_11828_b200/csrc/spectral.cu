@@ -1916,6 +1916,10 @@ void engine_alloc_workspace(Engine& e, int64_t batch) {
     const Plan& pl = e.plan;
     check(cudaMalloc(&e.d_S1, sizeof(double2) * pl.S1_per_vec * batch), "alloc S1");
     if (pl.S2_per_vec) check(cudaMalloc(&e.d_S2, sizeof(double2) * pl.S2_per_vec * batch), "alloc S2");
+    if (e.d_xstrip) cudaFree(e.d_xstrip);
+    e.d_xstrip = nullptr;
+    if (pl.dim == 3 && pl.circ[0])  // 4M x-values per (y, z) row and component
+        check(cudaMalloc(&e.d_xstrip, sizeof(double) * (size_t)batch * 3 * 4 * e.M * pl.N[1] * pl.N[2]), "alloc strip");
     e.cap_batch = batch;
 }
 
