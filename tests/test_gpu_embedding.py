@@ -137,3 +137,25 @@ def test_separable_symbol_periodic(dims, monkeypatch):
     assert ff.symbol_mode() == "separable" and ff.embedding() == (1 << len(dims)) - 1
     u = random_field(Rng(31), len(dims), o.n)
     assert rel(ff.matvec(u), o.matvec(u)) <= TOL
+
+
+def test_cg_after_workspace_growth(monkeypatch):
+    """A CG solve, then a larger-batch mat-vec (the workspace is reallocated),
+    then CG again: the captured CG iteration must not keep the old buffers."""
+    torch = pytest.importorskip("torch")
+    n = 64
+    h = 1.0 / n
+    o = Oracle((n, n), h=h, delta=3.015 * h, M=3)
+    ff = make(o, "periodic", monkeypatch)
+    ff.set_geometry(h, [0.0, 0.0], 3.015 * h, 1.0)
+    for lo, hi in [((0, 0), (1, 3.015 * h)), ((0, 1 - 3.015 * h), (1, 1))]:
+        o.add_constraint(lo, hi, 3)
+        ff.add_constraint(lo, hi, 3)
+    b = random_field(Rng(5), 2, o.n)
+    x1, it1, rel1, _ = ff.cg_solve(b, tol=1e-10, maxit=5000)
+    u = np.stack([random_field(Rng(6 + i), 2, o.n) for i in range(8)])
+    fb = ff.matvec(u)  # batch 8 > the CG's batch-1 workspace
+    assert rel(fb[3], o.matvec(u[3])) <= TOL
+    x2, it2, rel2, _ = ff.cg_solve(b, tol=1e-10, maxit=5000)
+    assert it1 == it2 and rel2 <= 1e-10
+    assert np.array_equal(x1, x2)
