@@ -405,3 +405,36 @@ def _stream(s):
         return None
     h = s.cuda_stream if hasattr(s, "cuda_stream") else int(s)
     return h if h else _CUDA_STREAM_LEGACY
+
+
+class Convolver:
+    """Single-pair spectral convolution, the reference's Convolver<Dim>
+    (convolution.hpp:210-230): f = sum_o K_ab(o) u[p + o] over the lattice
+    (zero outside), one scalar field in and out.  Built on the same engine as
+    FastForce: a stencil stack holding only pair (a, b), the input placed in
+    component b, the result read from component a."""
+
+    def __init__(self, dims, M: int, stencils: np.ndarray, a: int = 0, b: int = 0, device: int = 0):
+        dims = tuple(int(d) for d in dims)
+        dim = len(dims)
+        npairs = dim * (dim + 1) // 2
+        side = 2 * M + 1
+        K = np.asarray(stencils, dtype=np.float64).reshape(npairs, side ** dim)
+        pr = pair_index(dim, a, b)
+        only = np.zeros_like(K)
+        only[pr] = K[pr]
+        self.dim, self.a, self.b = dim, int(a), int(b)
+        self.n = int(np.prod(dims))
+        self._ff = FastForce(dims, M, only, device=device)
+
+    def apply(self, u: np.ndarray) -> np.ndarray:
+        """Convolver::apply(u, f) (convolution.hpp:217-221); u, f: N-vectors."""
+        x = np.zeros((self.dim, self.n))
+        x[self.b] = np.asarray(u, dtype=np.float64).reshape(self.n)
+        return self._ff.apply(x)[self.a].copy()
+
+    def last_imag_residue(self) -> float:
+        return self._ff.last_imag_residue()
+
+    def close(self):
+        self._ff.close()

@@ -159,3 +159,33 @@ def test_cg_after_workspace_growth(monkeypatch):
     x2, it2, rel2, _ = ff.cg_solve(b, tol=1e-10, maxit=5000)
     assert it1 == it2 and rel2 <= 1e-10
     assert np.array_equal(x1, x2)
+
+
+@pytest.mark.parametrize("dims,M,a,b", [((64, 48), 3, 0, 0), ((64, 48), 3, 0, 1), ((33, 17), 2, 1, 1),
+                                        ((16, 12, 20), 2, 0, 2), ((16, 16, 16), 3, 1, 1)])
+def test_convolver_single_pair(dims, M, a, b):
+    """Convolver<Dim> (convolution.hpp:210-230): one stencil pair, one scalar
+    field, against a direct correlation f[p] = sum_o K_ab(o) u[p+o] (zero
+    outside the lattice), as tests/test_convolution.cpp:104-118 checks it."""
+    from paper_2301_11828_b200 import Convolver, pair_index
+    rng = Rng(211 + M)
+    o = Oracle(dims, h=0.5, M=M)
+    o.random_kernel(rng)
+    K = o.kernel()
+    dim = len(dims)
+    u = random_field(rng, 1, o.n)[0]
+    cv = Convolver(dims, M, K, a, b)
+    f = cv.apply(u)
+    side = 2 * M + 1
+    Kp = K.reshape(dim * (dim + 1) // 2, *([side] * dim))[pair_index(dim, a, b)]  # [o_{d-1}]...[o_0]
+    U = u.reshape(tuple(reversed(dims)))  # [.., y, x]
+    pad = np.pad(U, M)
+    want = np.zeros_like(U)
+    for idx in np.ndindex(*([side] * dim)):
+        kv = Kp[idx]
+        if kv == 0.0:
+            continue
+        sl = tuple(slice(i, i + n) for i, n in zip(idx, reversed(dims)))
+        want += kv * pad[sl]
+    assert rel(f, want.reshape(-1)) <= TOL
+    cv.close()
