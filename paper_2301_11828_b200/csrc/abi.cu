@@ -1024,12 +1024,15 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
             if (e.cg_graph) cudaGraphExecDestroy(e.cg_graph);
             e.cg_graph = nullptr;
             cudaGraph_t g;
+            const int64_t l0 = e.launches;
             cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
             launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
             launch_corrections(e, p, q, 1, s, -1.0);
             launch_dot(e, p, q, m, e.d_scal + 1, s);
             launch_cg_step_dev(e, x, r, p, q, m, e.d_scal, s);
             cuda_check(cudaStreamEndCapture(s, &g), "end capture");
+            e.cg_graph_launches = e.launches - l0;  // kernels per replay (capture itself launches none)
+            e.launches = l0;
             cuda_check(cudaGraphInstantiate(&e.cg_graph, g, 0), "instantiate");
             cudaGraphDestroy(g);
             e.cg_graph_x = x;
@@ -1045,7 +1048,7 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
             const int nl = std::min(chunk, maxit - launched);
             for (int i = 0; i < nl; ++i) cuda_check(cudaGraphLaunch(e.cg_graph, s), "graph launch");
             launched += nl;
-            e.launches += (int64_t)nl * 8;
+            e.launches += (int64_t)nl * e.cg_graph_launches;
             cuda_check(cudaMemcpyAsync(st, e.d_scal, sizeof(st), cudaMemcpyDeviceToHost, s), "read scal");
             cuda_check(cudaStreamSynchronize(s), "cg chunk");
             if (st[4] != 0.0) break;

@@ -145,6 +145,7 @@ struct Engine {
     cudaGraphExec_t cg_graph = nullptr;  // one captured CG iteration (keyed by x, stream)
     const double* cg_graph_x = nullptr;
     cudaStream_t cg_graph_stream = nullptr;
+    int64_t cg_graph_launches = 0;       // kernels in one captured CG iteration
     // reductions scratch
     double* d_red = nullptr;           // partial sums
     double* d_scal = nullptr;          // device scalars

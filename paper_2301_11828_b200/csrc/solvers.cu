@@ -92,7 +92,7 @@ __global__ void k_cg_direction(double* __restrict__ p, const double* __restrict_
 __global__ void k_rotate(double* scal) { scal[0] = scal[2]; }
 
 // ---- graph-replayable CG step with the convergence test on the device ----
-// scal = {rr, p.q, rr_new, tol^2 * rr_0, done, iterations}
+// scal = {rr, p.q, rr_new, tol^2 * rr_0, done, iterations, -, rr_old}
 template <class CB>
 __device__ void grid_reduce_cb(double v, double* partial, unsigned int* ticket, CB cb) {
     __shared__ double ws[32];
@@ -140,7 +140,12 @@ __global__ void k_cg_update_dev(double* __restrict__ x, double* __restrict__ r, 
         r[i] = ri;
         s += ri * ri;
     }
+    // the last block runs this after every block has read alpha (scal[0]):
+    // rotate rr in place (old -> scal[7], new -> scal[0] and scal[2]), so no
+    // separate rotation kernel is needed
     grid_reduce_cb(s, partial, ticket, [&](double tot) {
+        scal[7] = scal[0];
+        scal[0] = tot;
         scal[2] = tot;
         scal[5] += 1.0;
         if (tot <= scal[3]) scal[4] = 1.0;
@@ -150,13 +155,9 @@ __global__ void k_cg_update_dev(double* __restrict__ x, double* __restrict__ r, 
 __global__ void k_cg_direction_dev(double* __restrict__ p, const double* __restrict__ r, int64_t n,
                                    const double* scal) {
     if (scal[4] != 0.0) return;
-    const double beta = scal[2] / scal[0];
+    const double beta = scal[0] / scal[7];  // rr_new / rr_old, rotated by k_cg_update_dev
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         p[i] = r[i] + beta * p[i];
-}
-
-__global__ void k_rotate_dev(double* scal) {
-    if (scal[4] == 0.0) scal[0] = scal[2];
 }
 
 __global__ void k_mask_rhs(double* out, const double* b, const double* Auc, const uint8_t* cmask, int64_t N,
@@ -325,8 +326,7 @@ void launch_cg_step_dev(Engine& e, double* x, double* r, double* p, const double
                         cudaStream_t s) {
     k_cg_update_dev<<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, q, n, scal, e.d_red, e.d_ticket);
     k_cg_direction_dev<<<kRedBlocks, kRedThreads, 0, s>>>(p, r, n, scal);
-    k_rotate_dev<<<1, 1, 0, s>>>(scal);
-    e.launches += 3;
+    e.launches += 2;
     check(cudaGetLastError(), "cg_step_dev");
 }
 
