@@ -530,7 +530,7 @@ __device__ __forceinline__ void symbol_product(double2* F, const double2* U, con
 }
 
 template <int LOGQ, int D, bool REAL, int LOGR, bool ZSMEM, bool SEP = false, int NH = 2>
-__global__ void __launch_bounds__(256, 1) k_spectral(const double2* in, double2* out, const void* __restrict__ sym,
+__global__ void __launch_bounds__(256, NH == 1 ? 2 : 1) k_spectral(const double2* in, double2* out, const void* __restrict__ sym,
                                                      int ncols, int Nl, int NC, const double2* __restrict__ tw,
                                                      int logTWN, const double* __restrict__ coltab = nullptr,
                                                      int M = 0, int oddmask = 0) {
