@@ -25,11 +25,61 @@
  * rounding follow the reference (g++ x86-64 default target has no FMA).
  */
 #include <math.h>
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 typedef int64_t idx_t;
+
+/* ------------------------------------------------------- row threading --
+ * The row sweeps below (apply, corrections, dense force) compute every node
+ * independently with the serial operation order, so splitting the node range
+ * over threads is bit-identical to the serial sweep.  ORC_THREADS caps the
+ * thread count (default: online cores, at most 64). */
+typedef void (*orc_rows_fn)(void* ctx, idx_t p0, idx_t p1);
+typedef struct {
+    orc_rows_fn fn;
+    void* ctx;
+    idx_t p0, p1;
+} orc_rows_job;
+
+static void* orc_rows_thread(void* a) {
+    orc_rows_job* j = (orc_rows_job*)a;
+    j->fn(j->ctx, j->p0, j->p1);
+    return NULL;
+}
+
+static void orc_par_rows(idx_t n, orc_rows_fn fn, void* ctx) {
+    long t = sysconf(_SC_NPROCESSORS_ONLN);
+    const char* env = getenv("ORC_THREADS");
+    if (env && atoi(env) > 0) t = atoi(env);
+    if (t > 64) t = 64;
+    if (t < 1 || n < 65536) t = 1;
+    if (t == 1) {
+        fn(ctx, 0, n);
+        return;
+    }
+    pthread_t th[64];
+    orc_rows_job jobs[64];
+    for (long i = 0; i < t; ++i) {
+        jobs[i].fn = fn;
+        jobs[i].ctx = ctx;
+        jobs[i].p0 = n * i / t;
+        jobs[i].p1 = n * (i + 1) / t;
+    }
+    for (long i = 1; i < t; ++i) pthread_create(&th[i], NULL, orc_rows_thread, &jobs[i]);
+    orc_rows_thread(&jobs[0]);
+    for (long i = 1; i < t; ++i) pthread_join(th[i], NULL);
+}
+
+typedef struct orc_t orc_t;
+typedef struct {
+    const orc_t* P;
+    const double* u;
+    double* f;
+} orc_op_ctx;
 
 /* ------------------------------------------------------------------ RNG --
  * std::mt19937 (32-bit Mersenne twister, init_genrand seeding) and the
@@ -185,7 +235,7 @@ typedef struct {
     double value;
 } orc_constraint;
 
-typedef struct {
+struct orc_t {
     int dim, dims[3];
     double h, origin[3], thickness, delta, E, rho;
     int M, nof, np, lw;
@@ -212,7 +262,7 @@ typedef struct {
     double mass[3];     /* adr_mass, timestepping.hpp:150-162 */
     int fixed;          /* fixed_damping given */
     double fixed_c, last_c;
-} orc_t;
+};
 
 static void pos_of(const orc_t* P, const int* c, double* x) {
     for (int d = 0; d < P->dim; ++d) x[d] = P->origin[d] + (c[d] + 0.5) * P->h;
@@ -473,12 +523,16 @@ void orc_random_kernel(orc_t* P, orc_rng* r) {
 /* f = A_hat u, the translation-invariant operator generated by the stencils
  * with zero padding outside the lattice: FastForce::apply
  * (convolution.hpp:249-259) restated as oracles.hpp:72-96 tbt_apply_all. */
-void orc_apply_fast(const orc_t* P, const double* u, double* f) {
+static void apply_fast_rows(void* vc, idx_t p0, idx_t p1) {
+    const orc_op_ctx* X = (const orc_op_ctx*)vc;
+    const orc_t* P = X->P;
+    const double* u = X->u;
+    double* f = X->f;
     const int dim = P->dim;
     const idx_t n = P->n;
     int zero[3] = {0, 0, 0};
     const idx_t c0 = stencil_index(dim, P->M, zero);
-    for (idx_t p = 0; p < n; ++p) {
+    for (idx_t p = p0; p < p1; ++p) {
         int c[3];
         coords_of(P, p, c);
         double acc[3];
@@ -503,12 +557,21 @@ void orc_apply_fast(const orc_t* P, const double* u, double* f) {
     }
 }
 
+void orc_apply_fast(const orc_t* P, const double* u, double* f) {
+    orc_op_ctx X = {P, u, f};
+    orc_par_rows(P->n, apply_fast_rows, &X);
+}
+
 /* apply_corrections, corrections.hpp:76-110: surface diagonal then the
  * fracture gather (partners in ascending q, as BondLedger stores them). */
-void orc_apply_corrections(const orc_t* P, const double* u, double* f) {
+static void corrections_rows(void* vc, idx_t p0, idx_t p1) {
+    const orc_op_ctx* X = (const orc_op_ctx*)vc;
+    const orc_t* P = X->P;
+    const double* u = X->u;
+    double* f = X->f;
     const int dim = P->dim;
     const idx_t n = P->n;
-    for (idx_t p = 0; p < n; ++p) {
+    for (idx_t p = p0; p < p1; ++p) {
         if (!P->near_surface[p]) continue;
         for (int a = 0; a < dim; ++a) {
             if ((P->cmask[p] >> a) & 1u) continue;
@@ -518,7 +581,7 @@ void orc_apply_corrections(const orc_t* P, const double* u, double* f) {
         }
     }
     if (P->total_broken == 0) return;
-    for (idx_t p = 0; p < n; ++p) {
+    for (idx_t p = p0; p < p1; ++p) {
         for (int s = 0; s < P->nof; ++s) {
             const int k = P->sorted_off[s];
             if (!orc_is_broken_k(P, p, k)) continue;
@@ -536,6 +599,14 @@ void orc_apply_corrections(const orc_t* P, const double* u, double* f) {
     }
 }
 
+/* apply_corrections, corrections.hpp:76-110: per row, the surface diagonal
+ * first, then the fracture gather (partners in ascending q, as BondLedger
+ * stores them).  Rows are independent (each row only writes its own f). */
+void orc_apply_corrections(const orc_t* P, const double* u, double* f) {
+    orc_op_ctx X = {P, u, f};
+    orc_par_rows(P->n, corrections_rows, &X);
+}
+
 /* The corrected force the reference's tests compare:
  * FastForce::apply + apply_corrections (e.g. tests/test_corrections.cpp:107-110). */
 void orc_matvec(const orc_t* P, const double* u, double* f) {
@@ -544,13 +615,17 @@ void orc_matvec(const orc_t* P, const double* u, double* f) {
 }
 
 /* dense_force, reference.hpp:100-127 (meshfree sum over present unbroken bonds) */
-void orc_dense_force(const orc_t* P, const double* u, double* f) {
+static void dense_rows(void* vc, idx_t p0, idx_t p1) {
+    const orc_op_ctx* X = (const orc_op_ctx*)vc;
+    const orc_t* P = X->P;
+    const double* u = X->u;
+    double* f = X->f;
     const int dim = P->dim;
     const idx_t n = P->n;
     const double alpha = orc_alpha(P->E, P->delta, dim, P->thickness);
     const double vol = dim == 2 ? P->h * P->h * P->thickness : P->h * P->h * P->h;
     const double h = P->h;
-    for (idx_t p = 0; p < n; ++p) {
+    for (idx_t p = p0; p < p1; ++p) {
         int c[3];
         coords_of(P, p, c);
         double acc[3] = {0, 0, 0};
@@ -573,6 +648,11 @@ void orc_dense_force(const orc_t* P, const double* u, double* f) {
         }
         for (int a = 0; a < dim; ++a) f[a * n + p] = acc[a];
     }
+}
+
+void orc_dense_force(const orc_t* P, const double* u, double* f) {
+    orc_op_ctx X = {P, u, f};
+    orc_par_rows(P->n, dense_rows, &X);
 }
 
 /* Simulation::evaluate_force, timestepping.hpp:295-310 */

@@ -84,6 +84,7 @@ int find_offset(const Engine& e, const int* o) {
 
 void ensure_ledger(Engine& e) {
     if (e.d_ledger) return;
+    touch_state(e);
     const int64_t N = e.plan.nodes;
     dalloc(e.d_ledger, (size_t)(N * e.lw), "alloc ledger");
     dalloc(e.d_bond_rows, (size_t)N, "alloc bond rows");
@@ -99,6 +100,7 @@ void ensure_ledger(Engine& e) {
 }
 
 void upload_surface(Engine& e, const std::vector<long long>& rows, const std::vector<double>& de) {
+    touch_state(e);
     e.n_surf = (int64_t)rows.size();
     dalloc(e.d_surf_rows, rows.size(), "alloc surface rows");
     dalloc(e.d_surf_de, de.size(), "alloc surface de");
@@ -113,6 +115,7 @@ void upload_surface(Engine& e, const std::vector<long long>& rows, const std::ve
 // recompute the constraint mask and the constrained-dof list (last writer wins,
 // identical to applying the constraints in order, corrections.hpp:142-160)
 void rebuild_constraints(Engine& e) {
+    touch_state(e);
     const int64_t N = e.plan.nodes;
     const int dim = e.dim;
     e.h_cmask.assign((size_t)N, 0);
@@ -214,6 +217,7 @@ int64_t break_pairs(Engine& e, const int64_t* pairs, int64_t n) {
     }
     const int64_t m = (int64_t)quad.size() / 4;
     if (m == 0) return 0;
+    touch_state(e);
     long long* d_quad = nullptr;
     cuda_check(cudaMalloc(&d_quad, sizeof(long long) * quad.size()), "alloc quad");
     cuda_check(cudaMemcpy(d_quad, quad.data(), sizeof(long long) * quad.size(), cudaMemcpyHostToDevice), "copy quad");
@@ -548,7 +552,10 @@ int pdgpu_apply_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes, int
     });
 }
 
-double pdgpu_last_imag_residue(pdgpu_t h) { return h ? h->imag_residue : 0.0; }
+// The reference records max|Im|/max|Re| after each inverse C2C transform
+// (convolution.hpp:158-172).  The R2C/C2R pipeline here never forms an
+// imaginary part of the output field, so the residue is identically 0.
+double pdgpu_last_imag_residue(pdgpu_t) { return 0.0; }
 
 size_t pdgpu_footprint_bytes(pdgpu_t h) {
     if (!h) return 0;
@@ -612,11 +619,7 @@ int pdgpu_set_ghosts(pdgpu_t h, const double* ghosts) {
         if (!h) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null handle");
         if (ghosts && h->slab.global < 0) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "ghost rows need pdgpu_set_slab");
         h->d_ghost = ghosts;
-        h->cg_graph_x = nullptr;  // a captured CG iteration holds the old pointer
-        if (h->cg_graph) {
-            cudaGraphExecDestroy(h->cg_graph);
-            h->cg_graph = nullptr;
-        }
+        touch_state(*h);  // a captured CG iteration holds the old pointer
     });
 }
 
@@ -641,6 +644,7 @@ int pdgpu_set_ledger(pdgpu_t h, const int64_t* row_start, const int64_t* partner
         if (!h || !row_start) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
         cuda_check(cudaSetDevice(h->device), "set device");
         ensure_ledger(*h);
+        touch_state(*h);
         const int64_t N = h->plan.nodes;
         std::vector<uint32_t> bits((size_t)(N * h->lw), 0u);
         std::vector<long long> rows;
@@ -923,23 +927,48 @@ int pdgpu_update_bonds(pdgpu_t h, const double* u, double s0, const double* watc
         if (!h || !u) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
         cuda_check(cudaSetDevice(h->device), "set device");
         ensure_ledger(*h);
+        const bool want = out && cap > 0;
+        const int64_t N = h->plan.nodes;
+        const size_t lbytes = sizeof(uint32_t) * (size_t)(N * h->lw);
+        // ledger before the sweep: if one sweep breaks more bonds than the
+        // device pair buffer holds, the new pairs are recovered as the ledger
+        // difference instead of being truncated
+        uint32_t* d_prev = nullptr;
+        if (want) {
+            cuda_check(cudaMallocAsync((void**)&d_prev, lbytes, h->stream), "alloc ledger snapshot");
+            cuda_check(cudaMemcpyAsync(d_prev, h->d_ledger, lbytes, cudaMemcpyDeviceToDevice, h->stream), "snapshot");
+        }
         const int64_t n = launch_update_bonds(*h, u, s0, watch, h->stream);
         if (count) *count = n;
-        if (out && cap > 0 && n > 0) {
-            const int64_t m = std::min(n, h->new_pairs_cap);
-            std::vector<long long> raw((size_t)(2 * m));
+        std::vector<std::pair<long long, long long>> pk;  // (p, offset index)
+        if (want && n > 0 && n <= h->new_pairs_cap) {
+            std::vector<long long> raw((size_t)(2 * n));
             cuda_check(cudaMemcpy(raw.data(), h->d_new_pairs, sizeof(long long) * raw.size(), cudaMemcpyDeviceToHost),
                        "read pairs");
-            std::vector<std::pair<long long, long long>> pk;
-            for (int64_t i = 0; i < m; ++i) pk.push_back({raw[2 * i], raw[2 * i + 1]});
-            std::sort(pk.begin(), pk.end());
-            const int* N = h->plan.N;
-            for (int64_t i = 0; i < std::min(m, cap); ++i) {
-                const int* o = &h->offs[3 * pk[i].second];
-                out[2 * i] = pk[i].first;
-                out[2 * i + 1] = pk[i].first + (long long)o[2] * N[0] * N[1] + (long long)o[1] * N[0] + o[0];
-            }
+            for (int64_t i = 0; i < n; ++i) pk.push_back({raw[2 * i], raw[2 * i + 1]});
+        } else if (want && n > 0) {
+            std::vector<uint32_t> now((size_t)(N * h->lw)), before((size_t)(N * h->lw));
+            cuda_check(cudaMemcpy(now.data(), h->d_ledger, lbytes, cudaMemcpyDeviceToHost), "read ledger");
+            cuda_check(cudaMemcpy(before.data(), d_prev, lbytes, cudaMemcpyDeviceToHost), "read ledger snapshot");
+            for (int64_t p = 0; p < N; ++p)
+                for (int k = 0; k < h->nof; ++k) {
+                    const int* o = &h->offs[3 * k];
+                    const long long disp = (long long)o[2] * h->plan.N[0] * h->plan.N[1] + (long long)o[1] * h->plan.N[0] + o[0];
+                    if (disp <= 0) continue;  // q > p owns the pair (fracture.hpp:220)
+                    const size_t w = (size_t)(p * h->lw + (k >> 5));
+                    if (((now[w] & ~before[w]) >> (k & 31)) & 1u) pk.push_back({p, k});
+                }
         }
+        if (d_prev) cuda_check(cudaFreeAsync(d_prev, h->stream), "free ledger snapshot");
+        // the reference's visiting order: p ascending, then for_each_offset order
+        std::sort(pk.begin(), pk.end());
+        const int* Nd = h->plan.N;
+        for (int64_t i = 0; i < std::min<int64_t>((int64_t)pk.size(), want ? cap : 0); ++i) {
+            const int* o = &h->offs[3 * pk[i].second];
+            out[2 * i] = pk[i].first;
+            out[2 * i + 1] = pk[i].first + (long long)o[2] * Nd[0] * Nd[1] + (long long)o[1] * Nd[0] + o[0];
+        }
+        cuda_check(cudaStreamSynchronize(h->stream), "update_bonds");
     });
 }
 
@@ -1020,7 +1049,8 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
         engine_alloc_workspace(e, 1);
         const bool timing = e.timing;
         e.timing = false;
-        if (!e.cg_graph || e.cg_graph_x != x || e.cg_graph_stream != s || e.cg_cap != m) {
+        if (!e.cg_graph || e.cg_graph_x != x || e.cg_graph_stream != s || e.cg_cap != m ||
+            e.cg_graph_version != e.state_version) {
             if (e.cg_graph) cudaGraphExecDestroy(e.cg_graph);
             e.cg_graph = nullptr;
             cudaGraph_t g;
@@ -1037,6 +1067,7 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
             cudaGraphDestroy(g);
             e.cg_graph_x = x;
             e.cg_graph_stream = s;
+            e.cg_graph_version = e.state_version;
         }
         e.timing = timing;
         const double init[6] = {rr0, 0.0, rr0, tol * tol * rr0, 0.0, 0.0};

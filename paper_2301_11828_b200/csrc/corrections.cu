@@ -711,6 +711,7 @@ int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double*
         A.wlo[d] = watch && d < e.dim ? watch[d] : 0.0;
         A.whi[d] = watch && d < e.dim ? watch[e.dim + d] : 0.0;
     }
+    touch_state(e);  // the bond-row count changes under any captured launch sequence
     // reset the new-pair counter, keep the row counter
     check(cudaMemsetAsync(e.d_counters + 1, 0, sizeof(unsigned long long), s), "reset counter");
     const int th = 128;

@@ -142,15 +142,20 @@ struct Engine {
     bool any_cmask = false;              // constraint mask set directly (set_regions)
     double* d_cg = nullptr;              // CG work vectors r, p, q, u_c
     int64_t cg_cap = 0;
-    cudaGraphExec_t cg_graph = nullptr;  // one captured CG iteration (keyed by x, stream)
+    cudaGraphExec_t cg_graph = nullptr;  // one captured CG iteration (keyed by x, stream, state version)
     const double* cg_graph_x = nullptr;
     cudaStream_t cg_graph_stream = nullptr;
+    // Bumped by every change a captured launch sequence bakes in by value or
+    // by pointer: surface rows / D^e (re)uploads, bond-row count (breaks,
+    // ledger replacement), ghost buffer, slab frame, workspace growth.  A
+    // captured graph is valid only for the version it was recorded at.
+    uint64_t state_version = 0;
+    uint64_t cg_graph_version = ~0ull;
     int64_t cg_graph_launches = 0;       // kernels in one captured CG iteration
     // reductions scratch
     double* d_red = nullptr;           // partial sums
     double* d_scal = nullptr;          // device scalars
     unsigned int* d_ticket = nullptr;
-    double imag_residue = 0.0;
 
     // per-pass device timing (CUDA events on the launching stream) and the
     // number of kernels launched -- read by bench.py for the roofline
@@ -169,6 +174,16 @@ struct Engine {
         return ev_pool[ev_used++];
     }
 };
+
+// Invalidate every captured launch sequence (see Engine::state_version).
+inline void touch_state(Engine& e) {
+    ++e.state_version;
+    if (e.cg_graph) {
+        cudaGraphExecDestroy(e.cg_graph);
+        e.cg_graph = nullptr;
+    }
+    e.cg_graph_x = nullptr;
+}
 
 enum PassId { kPassK1 = 0, kPassK2 = 1, kPassK3 = 2, kPassK4 = 3, kPassK5 = 4, kPassCorr = 5, kPassBonds = 6,
               kPassVec = 7, kNumPass = 8 };

@@ -1911,11 +1911,7 @@ void build_symbol(Engine& e) {
 void engine_alloc_workspace(Engine& e, int64_t batch) {
     if (batch <= e.cap_batch) return;
     // a captured CG iteration holds the workspace pointers it was recorded with
-    if (e.cg_graph) {
-        cudaGraphExecDestroy(e.cg_graph);
-        e.cg_graph = nullptr;
-        e.cg_graph_x = nullptr;
-    }
+    touch_state(e);
     if (e.d_S1) cudaFree(e.d_S1);
     if (e.d_S2) cudaFree(e.d_S2);
     e.d_S1 = e.d_S2 = nullptr;

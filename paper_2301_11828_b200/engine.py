@@ -163,14 +163,16 @@ class FastForce:
 
     def apply_device(self, u, f, batch: int = 1, stream=None):
         """Device pointers / torch tensors, layout [batch][dim][N]."""
-        _check(self._lib.pdgpu_apply(self._h, _ptr(u), _ptr(f), batch, _stream(stream)))
+        _check(self._lib.pdgpu_apply(self._h, _ptr(u), _ptr(f), batch, _stream(stream, u, f)))
 
     def apply_direct_device(self, u, f, batch: int = 1, stream=None):
         """FastForce::apply by direct stencil summation on the device (cross-check
         of apply_device; the reference oracle's tbt_apply_all)."""
-        _check(self._lib.pdgpu_apply_direct(self._h, _ptr(u), _ptr(f), batch, _stream(stream)))
+        _check(self._lib.pdgpu_apply_direct(self._h, _ptr(u), _ptr(f), batch, _stream(stream, u, f)))
 
     def last_imag_residue(self) -> float:
+        """FastForce::last_imag_residue (convolution.hpp:261).  Always 0.0: the
+        R2C/C2R transforms never form an imaginary part of the output."""
         return self._lib.pdgpu_last_imag_residue(self._h)
 
     def footprint_bytes(self) -> int:
@@ -261,13 +263,13 @@ class FastForce:
         return f
 
     def matvec_device(self, u, f, batch: int = 1, stream=None):
-        _check(self._lib.pdgpu_matvec(self._h, _ptr(u), _ptr(f), batch, _stream(stream)))
+        _check(self._lib.pdgpu_matvec(self._h, _ptr(u), _ptr(f), batch, _stream(stream, u, f)))
 
     def apply_corrections_device(self, u, f, batch: int = 1, stream=None):
-        _check(self._lib.pdgpu_apply_corrections(self._h, _ptr(u), _ptr(f), batch, _stream(stream)))
+        _check(self._lib.pdgpu_apply_corrections(self._h, _ptr(u), _ptr(f), batch, _stream(stream, u, f)))
 
     def evaluate_force_device(self, u, f, stream=None):
-        _check(self._lib.pdgpu_evaluate_force(self._h, _ptr(u), _ptr(f), _stream(stream)))
+        _check(self._lib.pdgpu_evaluate_force(self._h, _ptr(u), _ptr(f), _stream(stream, u, f)))
 
     # ------------------------------------------------------------- problem
     def add_constraint(self, lo, hi, dir_mask: int, kind: int = 0, value: float = 0.0):
@@ -298,6 +300,9 @@ class FastForce:
         w = None if watch is None else _f64(np.concatenate([np.asarray(watch[0]), np.asarray(watch[1])]))
         out = np.zeros((cap, 2), dtype=np.int64)
         cnt = C.c_int64()
+        if getattr(u, "is_cuda", False):  # the sweep runs on the engine stream: order it after u's producers
+            import torch
+            torch.cuda.current_stream(u.device).synchronize()
         _check(self._lib.pdgpu_update_bonds(self._h, _ptr(u), float(s0), None if w is None else _dp(w),
                                             out.ctypes.data_as(_lib.c_int64_p), cap, C.byref(cnt)))
         return out[: min(cnt.value, cap)]
@@ -317,7 +322,7 @@ class FastForce:
         it = C.c_int()
         rel = C.c_double()
         _check(self._lib.pdgpu_cg_solve(self._h, _ptr(b), _ptr(x), tol, maxit, C.byref(it), C.byref(rel),
-                                        _stream(stream)))
+                                        _stream(stream, b, x)))
         return it.value, rel.value
 
     # ------------------------------------------------------------------ VV
@@ -396,13 +401,24 @@ def _ptr(x) -> int:
 _CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: the legacy default stream's explicit handle
 
 
-def _stream(s):
-    """None -> the engine's own stream; a torch stream (or raw handle) -> that
-    stream.  Torch's default stream has handle 0, which the C ABI reads as
-    "engine stream", so it is passed as cudaStreamLegacy to stay ordered with
-    the caller's torch work."""
+def _stream(s, *tensors):
+    """Stream for a device entry point.
+
+    s = None: when any argument is a torch CUDA tensor, the caller's current
+    torch stream on that tensor's device, so the engine is ordered after the
+    torch kernels that produced its inputs and before those that consume its
+    outputs; with raw pointers only, the engine's own stream.  A torch stream
+    (or raw handle) -> that stream.  Torch's default stream has handle 0, which
+    the C ABI reads as "engine stream", so it is passed as cudaStreamLegacy.
+
+    One engine must not be driven from two streams at once: its spectral
+    workspace and reduction scratch are shared by every entry point."""
     if s is None:
-        return None
+        dev = next((t.device for t in tensors if getattr(t, "is_cuda", False)), None)
+        if dev is None:
+            return None
+        import torch
+        s = torch.cuda.current_stream(dev)
     h = s.cuda_stream if hasattr(s, "cuda_stream") else int(s)
     return h if h else _CUDA_STREAM_LEGACY
 
