@@ -144,6 +144,22 @@ def pass_algorithmic_bytes(n_side: int, batch: int, periodic: bool):
             "K5_irfft_x": batch * (spec + 8 * DIM * n)}
 
 
+def pass_algorithmic_bytes_3d(n: int, batch: int, n_pairs: int = 6):
+    """3D periodic pass model (P = N on every axis, R2C along x: Hx = N/2 + 1):
+    K1 reads u (8 B per node-component) and writes S1 = d*Nz*Hx*Ny complex; K2
+    (y) reads S1 and writes S2 = d*Hx*Ny*Nz; K3 (z, symbol, inverse z) reads
+    and writes S2 plus the real symbol once per launch (n_pairs*Hx*Ny*Nz
+    doubles); K4 reads S2, writes S1; K5 reads S1 and writes f."""
+    d = 3
+    nodes = n ** 3
+    hx = n // 2 + 1
+    spec = d * hx * n * n * 16
+    field = d * nodes * 8
+    return {"K1_rfft_x": batch * (field + spec), "K2_fft_y": batch * 2 * spec,
+            "K3_spectral": batch * 2 * spec + n_pairs * hx * n * n * 8, "K4_ifft_y": batch * 2 * spec,
+            "K5_irfft_x": batch * (spec + field)}
+
+
 # ------------------------------------------------------------------ CPU leg --
 def _mem_available_bytes():
     try:
@@ -163,9 +179,26 @@ def cpu_threads_for(n_side):
     return max(1, min(cores, int(0.6 * _mem_available_bytes() // footprint))), cores
 
 
-def cpu_reference_sample(n_side, steps=1, budget_s=150.0):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+CPU_BUILD = ("reference headers (proj/include/pdfast, unmodified) compiled g++ -O3 -ffp-contract=off against "
+             "oracle/fftw_cpu (our radix-2/4 Stockham stand-in for the 10 FFTW3 symbols the reference calls; FFTW3 "
+             "is absent from the image and unpinned by the reference)")
+
+
+def cpu_reference_sample(n_side, steps=3, budget_s=150.0):
     """Time the reference path (oracle/_ref) on host cores: each step one
-    vector per thread, independent FastForce instances (convolution.hpp:53-54)."""
+    vector per thread, independent FastForce instances (convolution.hpp:53-54);
+    median over the steps that fit in the wall budget (at least one)."""
     import numpy as np
     from oracle import oracle as orc
     if not orc.ref_available():
@@ -184,10 +217,34 @@ def cpu_reference_sample(n_side, steps=1, budget_s=150.0):
             break
     per_step = statistics.median(times)
     value = threads * DIM * n_side * n_side / per_step
-    return {"value": value, "unit": UNIT, "cores": threads, "host_cores": cores, "kind": "reference",
-            "sample": f"{threads} of the {BATCH} vectors per step ({threads} threads x 1 vector, one FastForce each), "
-                      f"{len(times)} step(s), median {per_step:.2f} s; reference headers + oracle/fftw_cpu (FFTW3 "
-                      f"absent), g++ -O2", "steps_timed": len(times), "s_per_step": per_step}
+    return {"value": value, "unit": UNIT, "cores": threads, "host_cores": cores, "cpu_model": cpu_model(),
+            "kind": "reference",
+            "sample": f"{threads} of the {BATCH} vectors per step ({threads} threads x 1 vector, one FastForce each; "
+                      f"thread count capped by host memory, 7.5 GB per 4096^2 instance), {len(times)} step(s), "
+                      f"median {per_step:.2f} s (all: {', '.join(f'{t:.2f}' for t in times)})",
+            "build": CPU_BUILD, "steps_timed": len(times), "s_per_step": per_step}
+
+
+def cpu_reference_cg_config1():
+    """CG on BASELINE config 1 (128^2, clamped delta layers, tol 1e-10) over the
+    reference's own mat-vec (FastForce::apply + apply_corrections, oracle/_ref;
+    the CG loop itself is the restated Hestenes-Stiefel of SURVEY 8(c): the
+    reference has no CG), single host thread."""
+    import numpy as np
+    from oracle import oracle as orc
+    if not orc.ref_available():
+        return None
+    n = 128
+    h = 1.0 / n
+    r = orc.RefProblem((n, n), h=h, delta=3.015 * h, M=M, E=1.0, thickness=1.0)
+    for lo, hi in clamp_boxes(2, 3.015 * h):
+        r.add_constraint(lo, hi, 3)
+    r.finalize()
+    b = orc.random_field(orc.Rng(1001), 2, n * n)
+    t0 = time.perf_counter()
+    _, it, rel, _ = r.cg(b, tol=1e-10, maxit=20000)
+    return {"grid": [n, n], "tol": 1e-10, "iterations": it, "relres": rel,
+            "solve_s": time.perf_counter() - t0, "threads": 1, "kind": "reference mat-vec + restated CG"}
 
 
 def run_reference_arm(args):
@@ -203,7 +260,8 @@ def run_reference_arm(args):
             "warmup": 0, "ms_per_step": res["s_per_step"] * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": workload_config(1),
-            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "host_cores", "cpu_model", "kind", "sample",
+                                                 "build")},
             "e2e": {"value": res["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": "reference arm: the reference's own CPU path; warm-up steps skipped (no caches/JIT to warm), "
                     "timed steps capped by a wall budget"}
@@ -299,9 +357,30 @@ def extra_configs(device, stream):
     for _ in range(3):
         ff.matvec_device(u, f, 1, stream)
     reps = 10
+    ff.timing_read()
+    ff.timing(True)
     ms, _ = timed(lambda: [ff.matvec_device(u, f, 1, stream) for _ in range(reps)])
-    out["config4_matvec_256"] = {"grid": [n, n, n], "value": 3 * n ** 3 / (ms / reps * 1e-3), "unit": UNIT,
-                                 "ms_per_matvec": ms / reps}
+    passes = ff.timing_read()
+    ff.timing(False)
+    peak, peak_src = measured_peaks()
+    pb = pass_algorithmic_bytes_3d(n, 1)
+    per_pass = {}
+    for k, b in pb.items():
+        ms_k, n_k = passes.get(k, (0.0, 0))
+        avg = ms_k / max(n_k, 1)
+        per_pass[k] = {"algorithmic_bytes_per_launch": b, "mean_launch_ms": avg,
+                       "achieved_gbs": b / (avg * 1e-3) / 1e9 if avg else None,
+                       "frac": b / (avg * 1e-3) / 1e9 / peak if avg else None}
+    dom = max(per_pass, key=lambda k: per_pass[k]["mean_launch_ms"])
+    tot = sum(pb.values())
+    mv_gbs = tot / (ms / reps * 1e-3) / 1e9
+    out["config4_matvec_256"] = {
+        "grid": [n, n, n], "value": 3 * n ** 3 / (ms / reps * 1e-3), "unit": UNIT, "ms_per_matvec": ms / reps,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": per_pass[dom]["achieved_gbs"], "peak": peak,
+                     "unit": "GB/s", "frac": per_pass[dom]["frac"], "peak_source": peak_src, "per_pass": per_pass,
+                     "passes_ms_per_matvec": {k: v[0] / reps for k, v in passes.items()},
+                     "matvec": {"algorithmic_bytes": tot, "achieved_gbs": mv_gbs, "frac": mv_gbs / peak,
+                                "model": "periodic 3D pass model (bench.pass_algorithmic_bytes_3d), batch 1"}}}
     ff.close()
     del u, f
     # config 2 sweep (512^2 .. 2048^2, batch 16, no constraints); 4096^2 is the headline line
@@ -581,9 +660,13 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_reference_sample(N_SIDE, steps=1, budget_s=60.0)
+            cpu = cpu_reference_sample(N_SIDE, steps=3, budget_s=45.0)
             if cpu:
-                cpu = {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
+                cpu = {k: cpu[k] for k in ("value", "unit", "cores", "host_cores", "cpu_model", "kind", "sample",
+                                           "build")}
+                cg = cpu_reference_cg_config1()
+                if cg:
+                    cpu["config1_cg"] = cg
         except Exception as exc:  # the CPU leg must not kill the GPU number
             cpu = {"error": str(exc)[:200]}
 

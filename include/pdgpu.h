@@ -140,6 +140,8 @@ int pdgpu_matvec_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes, in
 /* Simulation::evaluate_force (timestepping.hpp:295-310): f = A u + body,
  * then zero every constrained (node, dir).  Device pointers, one field. */
 int pdgpu_evaluate_force(pdgpu_t h, const double* u, double* f, void* stream);
+/* Same on host fields (dim x N); n_nodes as in pdgpu_apply_host. */
+int pdgpu_evaluate_force_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes);
 
 /* --------------------------------------------------------------- problem --
  * Problem<Dim> setup (timestepping.hpp:40-52).  Boxes are closed, cell
@@ -163,6 +165,12 @@ int pdgpu_seed_notch(pdgpu_t h, const double* notch, int64_t* added);
  * visiting order (p ascending, then offset order); *count = total. */
 int pdgpu_update_bonds(pdgpu_t h, const double* u, double s0, const double* watch, int64_t* out_pairs, int64_t cap,
                        int64_t* count);
+/* Same with u a host field (dim x N, n_nodes = lattice size, else ShapeMismatch). */
+int pdgpu_update_bonds_host(pdgpu_t h, const double* u, int64_t n_nodes, double s0, const double* watch,
+                            int64_t* out_pairs, int64_t cap, int64_t* count);
+/* All (p, q) pairs of the last pdgpu_update_bonds[_host] sweep (visiting
+ * order), e.g. when that call's cap was smaller than its count. */
+int pdgpu_last_new_pairs(pdgpu_t h, int64_t* out_pairs, int64_t cap, int64_t* count);
 
 /* ------------------------------------------------------------ CG solver --
  * New static solver (the reference has ADR only): Hestenes-Stiefel CG on
@@ -196,6 +204,19 @@ int pdgpu_sim_init_adr(pdgpu_t h, double dt, double fixed_damping);
 int pdgpu_sim_adr_damping(pdgpu_t h, double* c);
 /* Copies of the state (host, dim x N each, any may be NULL). */
 int pdgpu_sim_get(pdgpu_t h, double* u, double* v, double* f, double* t);
+/* SimState::f_prev and ::v_half (timestepping.hpp:55-61), host, either may be NULL. */
+int pdgpu_sim_get_aux(pdgpu_t h, double* f_prev, double* v_half);
+/* InitialVelocity (timestepping.hpp:33-37, applied in the Simulation ctor
+ * :194-197): overwrite v (dim x N host) and re-apply the constraints at the
+ * current time (enforce_constraints, corrections.hpp:142-160). */
+int pdgpu_sim_set_velocity(pdgpu_t h, const double* v);
+/* Simulation::newly_broken() (timestepping.hpp:273): the (p, q) pairs broken
+ * by the stretch test of the last step of the last pdgpu_sim_step call, in
+ * the reference's visiting order; *count = 0 when that call had s0 < 0. */
+int pdgpu_sim_newly_broken(pdgpu_t h, int64_t* out_pairs, int64_t cap, int64_t* count);
+/* Simulation::finite() (timestepping.hpp:256-261): *ok = 1 iff every entry of
+ * u is finite (device reduction, no copy of u). */
+int pdgpu_sim_finite(pdgpu_t h, int* ok);
 
 /* ---------------------------------------------------------- diagnostics --
  * Per-pass device timing with CUDA events on the launching stream (pass ids:

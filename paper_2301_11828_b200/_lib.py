@@ -67,6 +67,14 @@ SIGNATURES = {
     "pdgpu_sim_init_adr": (C.c_int, [C.c_void_p, C.c_double, C.c_double]),
     "pdgpu_sim_adr_damping": (C.c_int, [C.c_void_p, c_double_p]),
     "pdgpu_sim_get": (C.c_int, [C.c_void_p, c_double_p, c_double_p, c_double_p, c_double_p]),
+    "pdgpu_sim_get_aux": (C.c_int, [C.c_void_p, c_double_p, c_double_p]),
+    "pdgpu_sim_set_velocity": (C.c_int, [C.c_void_p, c_double_p]),
+    "pdgpu_sim_newly_broken": (C.c_int, [C.c_void_p, c_int64_p, C.c_int64, c_int64_p]),
+    "pdgpu_sim_finite": (C.c_int, [C.c_void_p, c_int_p]),
+    "pdgpu_evaluate_force_host": (C.c_int, [C.c_void_p, c_double_p, c_double_p, C.c_int64]),
+    "pdgpu_update_bonds_host": (C.c_int, [C.c_void_p, c_double_p, C.c_int64, C.c_double, c_double_p, c_int64_p,
+                                          C.c_int64, c_int64_p]),
+    "pdgpu_last_new_pairs": (C.c_int, [C.c_void_p, c_int64_p, C.c_int64, c_int64_p]),
     "pdgpu_timing_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "pdgpu_timing_read": (C.c_int, [C.c_void_p, c_double_p, c_int64_p, C.c_int]),
     "pdgpu_launch_count": (C.c_int64, [C.c_void_p]),

@@ -804,6 +804,20 @@ int pdgpu_evaluate_force(pdgpu_t h, const double* u, double* f, void* stream) {
     });
 }
 
+int pdgpu_evaluate_force_host(pdgpu_t h, const double* u, double* f, int64_t n_nodes) {
+    return guarded([&] {
+        if (!h || !u || !f) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
+        if (n_nodes != h->plan.nodes) throw PdError(PDGPU_ERR_SHAPE_MISMATCH, "field length does not match the lattice");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const int64_t m = (int64_t)h->dim * n_nodes;
+        ensure_stage(*h, m);
+        cuda_check(cudaMemcpyAsync(h->d_u_stage, u, sizeof(double) * m, cudaMemcpyHostToDevice, h->stream), "H2D");
+        evaluate_force_impl(*h, h->d_u_stage, h->d_f_stage, h->stream);
+        cuda_check(cudaMemcpyAsync(f, h->d_f_stage, sizeof(double) * m, cudaMemcpyDeviceToHost, h->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(h->stream), "evaluate_force_host");
+    });
+}
+
 int pdgpu_add_constraint(pdgpu_t h, const double* lo, const double* hi, int dir_mask, int kind, double value) {
     return guarded([&] {
         if (!h || !lo || !hi) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
@@ -921,54 +935,88 @@ int pdgpu_seed_notch(pdgpu_t h, const double* notch, int64_t* added) {
     });
 }
 
+// one stretch sweep on device-resident u; the newly broken pairs are kept on
+// the host (e.last_pairs) in the reference's visiting order
+static int64_t update_bonds_impl(Engine& e, const double* u, double s0, const double* watch) {
+    ensure_ledger(e);
+    const int64_t N = e.plan.nodes;
+    const size_t lbytes = sizeof(uint32_t) * (size_t)(N * e.lw);
+    // ledger before the sweep: if one sweep breaks more bonds than the device
+    // pair buffer holds, the new pairs are recovered as the ledger difference
+    // instead of being truncated
+    uint32_t* d_prev = nullptr;
+    cuda_check(cudaMallocAsync((void**)&d_prev, lbytes, e.stream), "alloc ledger snapshot");
+    cuda_check(cudaMemcpyAsync(d_prev, e.d_ledger, lbytes, cudaMemcpyDeviceToDevice, e.stream), "snapshot");
+    const int64_t n = launch_update_bonds(e, u, s0, watch, e.stream);
+    std::vector<std::pair<long long, long long>> pk;  // (p, offset index)
+    if (n > 0 && n <= e.new_pairs_cap) {
+        std::vector<long long> raw((size_t)(2 * n));
+        cuda_check(cudaMemcpy(raw.data(), e.d_new_pairs, sizeof(long long) * raw.size(), cudaMemcpyDeviceToHost),
+                   "read pairs");
+        for (int64_t i = 0; i < n; ++i) pk.push_back({raw[2 * i], raw[2 * i + 1]});
+    } else if (n > 0) {
+        std::vector<uint32_t> now((size_t)(N * e.lw)), before((size_t)(N * e.lw));
+        cuda_check(cudaMemcpy(now.data(), e.d_ledger, lbytes, cudaMemcpyDeviceToHost), "read ledger");
+        cuda_check(cudaMemcpy(before.data(), d_prev, lbytes, cudaMemcpyDeviceToHost), "read ledger snapshot");
+        for (int64_t p = 0; p < N; ++p)
+            for (int k = 0; k < e.nof; ++k) {
+                const int* o = &e.offs[3 * k];
+                const long long disp = (long long)o[2] * e.plan.N[0] * e.plan.N[1] + (long long)o[1] * e.plan.N[0] + o[0];
+                if (disp <= 0) continue;  // q > p owns the pair (fracture.hpp:220)
+                const size_t w = (size_t)(p * e.lw + (k >> 5));
+                if (((now[w] & ~before[w]) >> (k & 31)) & 1u) pk.push_back({p, k});
+            }
+    }
+    cuda_check(cudaFreeAsync(d_prev, e.stream), "free ledger snapshot");
+    cuda_check(cudaStreamSynchronize(e.stream), "update_bonds");
+    // the reference's visiting order: p ascending, then for_each_offset order
+    std::sort(pk.begin(), pk.end());
+    const int* Nd = e.plan.N;
+    e.last_pairs.resize(2 * pk.size());
+    for (size_t i = 0; i < pk.size(); ++i) {
+        const int* o = &e.offs[3 * pk[i].second];
+        e.last_pairs[2 * i] = pk[i].first;
+        e.last_pairs[2 * i + 1] = pk[i].first + (long long)o[2] * Nd[0] * Nd[1] + (long long)o[1] * Nd[0] + o[0];
+    }
+    return n;
+}
+
+static void copy_pairs(const std::vector<int64_t>& pairs, int64_t* out, int64_t cap) {
+    const int64_t n = (int64_t)pairs.size() / 2;
+    if (out && cap > 0) std::copy(pairs.begin(), pairs.begin() + 2 * std::min(n, cap), out);
+}
+
 int pdgpu_update_bonds(pdgpu_t h, const double* u, double s0, const double* watch, int64_t* out, int64_t cap,
                        int64_t* count) {
     return guarded([&] {
         if (!h || !u) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
         cuda_check(cudaSetDevice(h->device), "set device");
-        ensure_ledger(*h);
-        const bool want = out && cap > 0;
-        const int64_t N = h->plan.nodes;
-        const size_t lbytes = sizeof(uint32_t) * (size_t)(N * h->lw);
-        // ledger before the sweep: if one sweep breaks more bonds than the
-        // device pair buffer holds, the new pairs are recovered as the ledger
-        // difference instead of being truncated
-        uint32_t* d_prev = nullptr;
-        if (want) {
-            cuda_check(cudaMallocAsync((void**)&d_prev, lbytes, h->stream), "alloc ledger snapshot");
-            cuda_check(cudaMemcpyAsync(d_prev, h->d_ledger, lbytes, cudaMemcpyDeviceToDevice, h->stream), "snapshot");
-        }
-        const int64_t n = launch_update_bonds(*h, u, s0, watch, h->stream);
+        const int64_t n = update_bonds_impl(*h, u, s0, watch);
         if (count) *count = n;
-        std::vector<std::pair<long long, long long>> pk;  // (p, offset index)
-        if (want && n > 0 && n <= h->new_pairs_cap) {
-            std::vector<long long> raw((size_t)(2 * n));
-            cuda_check(cudaMemcpy(raw.data(), h->d_new_pairs, sizeof(long long) * raw.size(), cudaMemcpyDeviceToHost),
-                       "read pairs");
-            for (int64_t i = 0; i < n; ++i) pk.push_back({raw[2 * i], raw[2 * i + 1]});
-        } else if (want && n > 0) {
-            std::vector<uint32_t> now((size_t)(N * h->lw)), before((size_t)(N * h->lw));
-            cuda_check(cudaMemcpy(now.data(), h->d_ledger, lbytes, cudaMemcpyDeviceToHost), "read ledger");
-            cuda_check(cudaMemcpy(before.data(), d_prev, lbytes, cudaMemcpyDeviceToHost), "read ledger snapshot");
-            for (int64_t p = 0; p < N; ++p)
-                for (int k = 0; k < h->nof; ++k) {
-                    const int* o = &h->offs[3 * k];
-                    const long long disp = (long long)o[2] * h->plan.N[0] * h->plan.N[1] + (long long)o[1] * h->plan.N[0] + o[0];
-                    if (disp <= 0) continue;  // q > p owns the pair (fracture.hpp:220)
-                    const size_t w = (size_t)(p * h->lw + (k >> 5));
-                    if (((now[w] & ~before[w]) >> (k & 31)) & 1u) pk.push_back({p, k});
-                }
-        }
-        if (d_prev) cuda_check(cudaFreeAsync(d_prev, h->stream), "free ledger snapshot");
-        // the reference's visiting order: p ascending, then for_each_offset order
-        std::sort(pk.begin(), pk.end());
-        const int* Nd = h->plan.N;
-        for (int64_t i = 0; i < std::min<int64_t>((int64_t)pk.size(), want ? cap : 0); ++i) {
-            const int* o = &h->offs[3 * pk[i].second];
-            out[2 * i] = pk[i].first;
-            out[2 * i + 1] = pk[i].first + (long long)o[2] * Nd[0] * Nd[1] + (long long)o[1] * Nd[0] + o[0];
-        }
-        cuda_check(cudaStreamSynchronize(h->stream), "update_bonds");
+        copy_pairs(h->last_pairs, out, cap);
+    });
+}
+
+int pdgpu_update_bonds_host(pdgpu_t h, const double* u, int64_t n_nodes, double s0, const double* watch,
+                            int64_t* out, int64_t cap, int64_t* count) {
+    return guarded([&] {
+        if (!h || !u) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        if (n_nodes != h->plan.nodes) throw PdError(PDGPU_ERR_SHAPE_MISMATCH, "field length does not match the lattice");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const int64_t m = (int64_t)h->dim * n_nodes;
+        ensure_stage(*h, m);
+        cuda_check(cudaMemcpyAsync(h->d_u_stage, u, sizeof(double) * m, cudaMemcpyHostToDevice, h->stream), "H2D");
+        const int64_t n = update_bonds_impl(*h, h->d_u_stage, s0, watch);
+        if (count) *count = n;
+        copy_pairs(h->last_pairs, out, cap);
+    });
+}
+
+int pdgpu_last_new_pairs(pdgpu_t h, int64_t* out, int64_t cap, int64_t* count) {
+    return guarded([&] {
+        if (!h || !count) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        *count = (int64_t)h->last_pairs.size() / 2;
+        copy_pairs(h->last_pairs, out, cap);
     });
 }
 
@@ -1208,6 +1256,7 @@ int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64
         const int64_t N = e.plan.nodes;
         const double inv_rho = 1.0 / e.rho;
         int64_t nb = 0;
+        e.sim_swept = s0 >= 0 && n_steps > 0;
         if (s0 >= 0) {
             ensure_ledger(e);
             cuda_check(cudaMemsetAsync(e.d_counters + 2, 0, sizeof(unsigned long long), e.stream), "reset breaks");
@@ -1262,6 +1311,72 @@ int pdgpu_sim_get(pdgpu_t h, double* u, double* v, double* f, double* t) {
         if (v) cuda_check(cudaMemcpy(v, h->d_v, m, cudaMemcpyDeviceToHost), "v");
         if (f) cuda_check(cudaMemcpy(f, h->d_f, m, cudaMemcpyDeviceToHost), "f");
         if (t) *t = h->t;
+    });
+}
+
+int pdgpu_sim_get_aux(pdgpu_t h, double* f_prev, double* v_half) {
+    return guarded([&] {
+        if (!h || !h->d_u) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "simulation not initialised");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const size_t m = sizeof(double) * h->dim * h->plan.nodes;
+        cuda_check(cudaStreamSynchronize(h->stream), "sync");
+        if (f_prev) cuda_check(cudaMemcpy(f_prev, h->d_fprev, m, cudaMemcpyDeviceToHost), "f_prev");
+        if (v_half) {
+            if (h->d_vh) cuda_check(cudaMemcpy(v_half, h->d_vh, m, cudaMemcpyDeviceToHost), "v_half");
+            else memset(v_half, 0, m);
+        }
+    });
+}
+
+int pdgpu_sim_set_velocity(pdgpu_t h, const double* v) {
+    return guarded([&] {
+        if (!h || !h->d_u || !v) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "simulation not initialised");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        const size_t m = sizeof(double) * h->dim * h->plan.nodes;
+        cuda_check(cudaMemcpyAsync(h->d_v, v, m, cudaMemcpyHostToDevice, h->stream), "copy v");
+        launch_enforce(h->d_u, h->d_v, h->d_cdofs, h->d_cval, h->d_ckind, h->n_cdofs, h->t, h->stream);
+        cuda_check(cudaStreamSynchronize(h->stream), "set velocity");
+    });
+}
+
+int pdgpu_sim_newly_broken(pdgpu_t h, int64_t* out, int64_t cap, int64_t* count) {
+    return guarded([&] {
+        if (!h || !count) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        *count = 0;
+        if (!h->sim_swept || !h->d_counters) return;
+        unsigned long long n = 0;
+        cuda_check(cudaStreamSynchronize(h->stream), "sync");
+        cuda_check(cudaMemcpy(&n, h->d_counters + 1, sizeof(n), cudaMemcpyDeviceToHost), "count");
+        *count = (int64_t)n;
+        if (!out || cap <= 0 || n == 0) return;
+        if ((int64_t)n > h->new_pairs_cap)
+            throw PdError(PDGPU_ERR_NOT_SUPPORTED, "the last step broke more bonds than the device pair buffer holds");
+        std::vector<long long> raw((size_t)(2 * n));
+        cuda_check(cudaMemcpy(raw.data(), h->d_new_pairs, sizeof(long long) * raw.size(), cudaMemcpyDeviceToHost),
+                   "read pairs");
+        std::vector<std::pair<long long, long long>> pk;
+        for (size_t i = 0; i < n; ++i) pk.push_back({raw[2 * i], raw[2 * i + 1]});
+        std::sort(pk.begin(), pk.end());
+        const int* Nd = h->plan.N;
+        for (int64_t i = 0; i < std::min<int64_t>((int64_t)n, cap); ++i) {
+            const int* o = &h->offs[3 * pk[(size_t)i].second];
+            out[2 * i] = pk[(size_t)i].first;
+            out[2 * i + 1] = pk[(size_t)i].first + (long long)o[2] * Nd[0] * Nd[1] + (long long)o[1] * Nd[0] + o[0];
+        }
+    });
+}
+
+int pdgpu_sim_finite(pdgpu_t h, int* ok) {
+    return guarded([&] {
+        if (!h || !h->d_u || !ok) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "simulation not initialised");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        int* d_ok = (int*)(h->d_ticket + 2);  // spare slots of the ticket allocation
+        const int one = 1;
+        cuda_check(cudaMemcpyAsync(d_ok, &one, sizeof(int), cudaMemcpyHostToDevice, h->stream), "finite init");
+        launch_finite(h->d_u, (int64_t)h->dim * h->plan.nodes, d_ok, h->stream);
+        cuda_check(cudaMemcpyAsync(ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream), "finite read");
+        cuda_check(cudaStreamSynchronize(h->stream), "finite");
     });
 }
 

@@ -118,6 +118,8 @@ struct Engine {
     int64_t total_broken = 0;
     long long* d_new_pairs = nullptr;  // update_bonds output buffer (p, k) pairs
     int64_t new_pairs_cap = 0;
+    std::vector<int64_t> last_pairs;   // (p, q) pairs of the last pdgpu_update_bonds sweep, visiting order
+    bool sim_swept = false;            // the last sim_step ran the stretch test (pdgpu_sim_newly_broken)
 
     // constraints / loads / simulation state
     std::vector<Constraint> constraints;
@@ -251,6 +253,7 @@ void launch_adr_step(Engine& e, bool first, cudaStream_t s);
 void launch_enforce(double* u, double* v, const long long* dofs, const double* val, const int* kind,
                     int64_t n, double t, cudaStream_t s);
 void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s);
+void launch_finite(const double* u, int64_t n, int* ok, cudaStream_t s);
 void launch_scatter(double* y, const long long* ids, const double* val, int64_t n, cudaStream_t s);
 
 }  // namespace pdgpu

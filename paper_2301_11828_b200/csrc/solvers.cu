@@ -385,6 +385,20 @@ void launch_scatter(double* y, const long long* ids, const double* val, int64_t 
     check(cudaGetLastError(), "scatter");
 }
 
+// Simulation::finite() (timestepping.hpp:256-261): *ok = 0 if any entry of u
+// is not finite (the caller sets *ok = 1 first)
+__global__ void k_finite(const double* __restrict__ u, int64_t n, int* ok) {
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        bad = bad || !isfinite(u[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *ok = 0;
+}
+
+void launch_finite(const double* u, int64_t n, int* ok, cudaStream_t s) {
+    k_finite<<<kRedBlocks, kRedThreads, 0, s>>>(u, n, ok);
+    check(cudaGetLastError(), "finite");
+}
+
 void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s) {
     k_axpy<<<blocks_for(n, 256), 256, 0, s>>>(y, x, a, n);
     check(cudaGetLastError(), "axpy");

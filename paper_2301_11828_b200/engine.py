@@ -345,6 +345,20 @@ class FastForce:
         _check(self._lib.pdgpu_sim_step(self._h, n_steps, s0, None if w is None else _dp(w), C.byref(nb)))
         return nb.value
 
+    def sim_newly_broken(self) -> np.ndarray:
+        """Simulation::newly_broken() (timestepping.hpp:273): pairs broken in the last step."""
+        cnt = C.c_int64()
+        _check(self._lib.pdgpu_sim_newly_broken(self._h, None, 0, C.byref(cnt)))
+        out = np.zeros((max(cnt.value, 1), 2), dtype=np.int64)
+        _check(self._lib.pdgpu_sim_newly_broken(self._h, out.ctypes.data_as(_lib.c_int64_p), cnt.value, C.byref(cnt)))
+        return out[: cnt.value]
+
+    def sim_finite(self) -> bool:
+        """Simulation::finite() (timestepping.hpp:256-261), evaluated on the device."""
+        ok = C.c_int()
+        _check(self._lib.pdgpu_sim_finite(self._h, C.byref(ok)))
+        return bool(ok.value)
+
     def write_snapshot(self, directory: str, u: np.ndarray, step: int, t: float, damage=None) -> str:
         """write_snapshot_dat (output.hpp:76-102) of host field u (dim, N) on this lattice/geometry."""
         return write_snapshot(directory, self.dims, self._geom[0], self._geom[1], u, step, t, damage)
