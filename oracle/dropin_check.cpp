@@ -22,8 +22,7 @@
 #include "pdfast/scenario.hpp"
 #include "pdfast/timestepping.hpp"
 #include "support/oracles.hpp"
-#define PDGPU_WITH_PDFAST
-#include "pdgpu.hpp"
+#include "pdgpu_sim.hpp"
 
 using namespace pdfast;
 

@@ -51,3 +51,14 @@ def test_dropin_header_compiles_and_links(tmp_path):
            f"-L{os.path.dirname(_lib.lib_path())}", "-lpdgpu", f"-Wl,-rpath,{os.path.dirname(_lib.lib_path())}"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="reference tree absent")
+def test_solver_level_dropin_compiles():
+    """pdgpu::Simulation<Dim> (include/pdgpu_sim.hpp) against the reference's
+    Problem / SolverOptions / SimState / BondLedger: the GPU test
+    tests/test_gpu_cpp_dropin.py runs the resulting oracle/_ref/dropin_check."""
+    cmd = ["g++", "-std=c++20", "-fsyntax-only", f"-I{REF}", f"-I{REF}/../tests", f"-I{ROOT}/include",
+           f"-I{ROOT}/oracle/fftw_cpu", os.path.join(ROOT, "oracle", "dropin_check.cpp")]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]
