@@ -21,8 +21,10 @@ configs : secondary BASELINE numbers -- CG solve times (configs 1, 3, 4) and
 cpu_baseline: the reference's own FastForce::apply + apply_corrections
           (oracle/_ref, headers compiled unmodified) on the host cores,
           bounded sample.  --impl reference prints that arm alone.
-N > 1 (torchrun): every rank runs its own 16-vector batch (independent
-vectors, no data-path collective) -> weak scaling; time = max over ranks.
+N > 1 (torchrun): the same 4096^2 x 16 lattice split into row slabs, one
+          libpdgpu engine per rank with the library's own NCCL halo exchange
+          (strong scaling, BASELINE configs[1]); time = max over ranks.
+          --shard vectors instead gives every rank its own batch (replicas).
 """
 from __future__ import annotations
 
@@ -52,7 +54,7 @@ def workload_config(n_gpus: int):
             "E": 1.0, "thickness": 1.0, "corrections": "surface diagonal (12N-36 rows), no cracks",
             "embedding": "periodic P = N per axis + wrap correction (PDGPU_EMBED=padded: P = 2N)", "l2": "inputs 4.3 GB per step > L2, no flush",
             "parallelism": f"{n_gpus} ranks x own batch (replicas, no data-path collective)" if n_gpus > 1
-            else "single GPU"}
+            else "single GPU (N > 1: the same lattice in row slabs, strong scaling)"}
 
 
 # ----------------------------------------------------------------- clocks --
@@ -257,7 +259,7 @@ def run_reference_arm(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpdref.so not built"}))
         return 0
     line = {"metric": METRIC, "value": res["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": res["steps_timed"],
-            "warmup": 0, "ms_per_step": res["s_per_step"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": 0, "ms_per_step": res["s_per_step"] * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": workload_config(1),
             "cpu_baseline": {k: res[k] for k in ("value", "unit", "cores", "host_cores", "cpu_model", "kind", "sample",
@@ -425,15 +427,20 @@ def extra_configs(device, stream):
 
 # -------------------------------------------------------------------- main --
 def run_slab(args):
-    """Strong scaling of one BATCH x N^2 problem over the ranks: row slabs with
-    M ghost rows per interior face, ghost rows exchanged by NCCL send/recv
-    before every mat-vec (paper_2301_11828_b200/slab.py).  Timed like the
-    default arm: barrier + synchronize on both sides, max over ranks."""
+    """Strong scaling of the BATCH x N^2 lattice over the ranks (BASELINE
+    configs[1]: "the 4096^2 grid is slab-sharded across 2/4/8 GPUs"): row
+    slabs of the halo decomposition (paper_2301_11828_b200/slab.py), each rank
+    one libpdgpu engine with the library's NCCL halo exchange (csrc/comm.cpp:
+    M rows per interior face per vector, packed and sent on a side stream
+    while K1..K5 run).  Timed like the single-GPU line: barrier + synchronize
+    on both sides, CUDA events on the launching stream, max over ranks."""
     import torch
     from paper_2301_11828_b200 import build_kernel
     from paper_2301_11828_b200 import dist as D
     from paper_2301_11828_b200.slab import SlabForce
 
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     rank, world, local = D.env()
     torch.cuda.set_device(local)
     D.init("nccl", torch.device("cuda", local))
@@ -442,41 +449,114 @@ def run_slab(args):
     K = build_kernel(DIM, h, 3.015 * h, M, 1.0, 1.0)
     sf = SlabForce((N_SIDE, N_SIDE), M, K, rank=rank, world=world, device=torch.device("cuda", local))
     sf.set_geometry(h, None, 3.015 * h, 1.0)
+    ff = sf.eng
+    stream = torch.cuda.Stream()
     gen = torch.Generator(device="cuda").manual_seed(D.vector_seed(2000, 0) + rank)
     u = torch.empty((BATCH, DIM, sf.n_owned), dtype=torch.float64, device="cuda")
     u.uniform_(-1.0, 1.0, generator=gen)
     f = torch.empty_like(u)
-    for _ in range(args.warmup):
-        sf.matvec(u, f)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            sf.matvec(u, f)
     torch.cuda.synchronize()
-    launches0 = sf.eng.launch_count()
+    ff.timing_read()
+    ff.timing(True)
+    launches0 = ff.launch_count()
     clk = ClockSampler(local)
     clk.start()
     D.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for _ in range(args.steps):
-        sf.matvec(u, f)
-    ev1.record()
+    ev0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(args.steps):
+            sf.matvec(u, f)
+    ev1.record(stream)
     torch.cuda.synchronize()
     D.barrier()
     clocks = clk.stop()
     ms_step = D.max_over_ranks(ev0.elapsed_time(ev1), "cuda") / args.steps
-    launches = sf.eng.launch_count() - launches0
-    halo = 2 * M * N_SIDE * DIM * 8 * BATCH if world > 1 else 0
+    launches = ff.launch_count() - launches0
+    passes = ff.timing_read()
+    ff.timing(False)
+    assert torch.isfinite(f).all().item(), "non-finite K.u"
+    value = BATCH * DIM * n / (ms_step * 1e-3)
+    halo_bytes = (2 * (sf.gl > 0) + 2 * (sf.gh > 0)) * M * N_SIDE * DIM * 8 * BATCH  # sent + received
+
+    # roofline of this rank's slab (its own lattice: Nx x R rows)
+    peak, peak_src = measured_peaks()
+    periodic = ff.embedding() == 3
+    R = sf.R
+    hx = (N_SIDE // 2 + 1) if periodic else (N_SIDE + 1)
+    py = R if periodic else 2 * R
+    spec = DIM * hx * R * 16
+    own = DIM * N_SIDE * R * 8
+    pbytes = {"K1_rfft_x": BATCH * (own + spec), "K3_spectral": BATCH * 2 * spec + 3 * hx * py * 8,
+              "K5_irfft_x": BATCH * (spec + own)}
+    per_pass = {}
+    for k, b in pbytes.items():
+        ms_k, n_k = passes.get(k, (0.0, 0))
+        avg = ms_k / max(n_k, 1)
+        per_pass[k] = {"algorithmic_bytes_per_launch": b, "mean_launch_ms": avg,
+                       "achieved_gbs": b / (avg * 1e-3) / 1e9 if avg else None,
+                       "frac": b / (avg * 1e-3) / 1e9 / peak if avg else None}
+    dom = max(per_pass, key=lambda k: per_pass[k]["mean_launch_ms"])
+    halo_ms, halo_n = passes.get("halo_exchange", (0.0, 0))
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": per_pass[dom]["achieved_gbs"], "peak": peak,
+                "unit": "GB/s", "frac": per_pass[dom]["frac"], "traffic": None, "peak_source": peak_src,
+                "rank": rank, "slab_rows": R, "per_pass": per_pass,
+                "passes_ms_per_step": {k: v[0] / args.steps for k, v in passes.items()},
+                "halo": {"bytes_per_rank_per_step": halo_bytes,
+                         "comm_stream_ms_per_step": halo_ms / args.steps if halo_n else 0.0,
+                         "gbs": (halo_bytes / (halo_ms / args.steps * 1e-3) / 1e9) if halo_n and halo_ms else None,
+                         "overlapped_with": "K1..K5 (K6w waits for it)"}}
+
+    # end to end through the public host API: this rank's owned rows from pinned host memory
+    e2e = None
+    if not args.no_e2e:
+        uh = torch.empty((BATCH, DIM, sf.n_owned), dtype=torch.float64, pin_memory=True)
+        uh.copy_(u)
+        fh = torch.empty_like(uh, pin_memory=True)
+        ff.matvec(uh.numpy(), out=fh.numpy())
+        e2e_steps = max(1, min(args.steps, 3))
+        D.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            ff.matvec(uh.numpy(), out=fh.numpy())
+        torch.cuda.synchronize()
+        e2e_s = D.max_over_ranks((time.perf_counter() - t0) / e2e_steps, "cuda")
+        nbytes = BATCH * DIM * n * 8
+        e2e = {"value": BATCH * DIM * n / e2e_s, "unit": UNIT, "h2d_bytes_per_step": nbytes,
+               "d2h_bytes_per_step": nbytes, "steps": e2e_steps, "ms_per_step": e2e_s * 1e3,
+               "api": "pdgpu_matvec_host on every rank (its pinned host rows in, host f out; NCCL halo inside)"}
+        del uh, fh
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        try:
+            cpu = cpu_reference_sample(N_SIDE, steps=3, budget_s=45.0)
+            if cpu:
+                cpu = {k: cpu[k] for k in ("value", "unit", "cores", "host_cores", "cpu_model", "kind", "sample",
+                                           "build")}
+        except Exception as exc:
+            cpu = {"error": str(exc)[:200]}
+    D.barrier()
     if rank == 0:
-        line = {"metric": METRIC, "value": BATCH * DIM * n / (ms_step * 1e-3), "unit": UNIT, "n_gpus": world,
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded uniform[-1,1], torch Philox)",
-                "config": {"workload": f"2D MSBFM K.u, {N_SIDE}x{N_SIDE} nodes, batch {BATCH}, row slabs",
-                           "parallelism": f"{world} row slabs + {M}-row halo (NCCL send/recv)",
-                           "halo": sf.halo, "engine_rows": sf.L, "embedding_bits": sf.eng.embedding(),
-                           "halo_bytes_per_rank_per_step": halo},
-                "clocks": clocks, "gpu_launches": launches, "roofline": None, "cpu_baseline": None, "e2e": None}
+                "config": dict(workload_config(world),
+                               parallelism=f"{world} row slabs + {M}-row halo (library NCCL send/recv, overlapped "
+                                           f"with K1..K5)", halo=sf.halo, transport=sf.transport,
+                               engine_rows=sf.L, embedding_bits=ff.embedding()),
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clocks,
+                "nccl": {"nranks": world, "comm": "pdgpu_comm_init (ncclCommInitRank)",
+                         "collectives": "grouped ncclSend/ncclRecv of the halo rows per K.u"}}
         print(json.dumps(line))
+    ff.close()
     D.finalize()
     return 0
 
@@ -493,15 +573,19 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra", action="store_true", help="skip the secondary configs")
     ap.add_argument("--ref-budget", type=float, default=150.0)
-    ap.add_argument("--shard", default="vectors", choices=["vectors", "slab"],
-                    help="N>1: vectors = every rank its own batch (weak, default); slab = one lattice split "
-                         "into row slabs with M-row halo exchange (strong, SURVEY 8e)")
+    ap.add_argument("--slab-single", action="store_true",
+                    help="run the slab arm (NCCL engine transport, one rank) at N = 1 too")
+    ap.add_argument("--shard", default="slab", choices=["vectors", "slab"],
+                    help="N>1: slab = the one lattice split into row slabs with the M-row NCCL halo exchange "
+                         "(strong scaling, BASELINE configs[1], default); vectors = every rank its own batch "
+                         "(replicas, weak)")
     args = ap.parse_args()
     globals()["N_SIDE"] = args.n
     globals()["BATCH"] = args.batch
     if args.impl == "reference":
         return run_reference_arm(args)
-    if args.shard == "slab":
+    from paper_2301_11828_b200 import dist as D0
+    if args.shard == "slab" and (D0.env()[1] > 1 or args.slab_single):
         return run_slab(args)
 
     import torch
@@ -672,7 +756,8 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                "scaling": "weak" if args.shard == "vectors" else "strong",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform[-1,1], torch Philox)",
                 "config": workload_config(world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks, "configs": extra}

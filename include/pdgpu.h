@@ -109,6 +109,36 @@ int pdgpu_set_slab(pdgpu_t h, int global_rows, int row_offset);
  * Requires pdgpu_set_slab; the caller refreshes the buffer's contents before
  * each mat-vec (stream-ordered). */
 int pdgpu_set_ghosts(pdgpu_t h, const double* ghosts);
+/* Same with an explicit layout: ghost row `layer` of side `side` for vector
+ * b, component c at ghosts[(b*dim + c)*vec_comp_stride + side*side_stride +
+ * layer*plane + i] (pdgpu_set_ghosts is vec_comp_stride = 2*M*plane,
+ * side_stride = M*plane; pdgpu_halo_pack's send layout is vec_comp_stride =
+ * M*plane, side_stride = batch*dim*M*plane). */
+int pdgpu_set_ghosts_strided(pdgpu_t h, const double* ghosts, int64_t vec_comp_stride, int64_t side_stride);
+/* The rows a slab sends to its neighbours before a K.u: send[side][batch][dim]
+ * [M][plane] <- the first (side 0, to the rank before) and last (side 1, to the
+ * rank after) M owned rows of u ([batch][dim][N] device).  Stream-ordered.
+ * Used by the built-in NCCL exchange and by callers that move halos with
+ * their own transport. */
+int pdgpu_halo_pack(pdgpu_t h, const double* u, int batch, double* send, void* stream);
+
+/* ---------------------------------------------------- multi-GPU (NCCL) --
+ * Halo slabs across GPUs, one process per GPU (the reference is
+ * single-process).  Rank r's engine is created on its own rows
+ * [r0, r1) of the slowest axis (pdgpu_slab_rows) and told its place with
+ * pdgpu_set_slab(h, global_rows, r0); pdgpu_comm_init then attaches an NCCL
+ * communicator (rank - 1 / rank + 1 hold the neighbouring slabs).  From then on
+ * every apply / matvec / evaluate_force exchanges the M rows next to each
+ * interior face on a side stream, overlapped with the spectral passes, and
+ * pdgpu_cg_solve / the ADR damping all-reduce their dot products (inside the
+ * captured CG iteration).  libnccl.so.2 is loaded at first use. */
+#define PDGPU_COMM_ID_BYTES 128
+/* ncclGetUniqueId on one rank; the caller broadcasts the 128 bytes. */
+int pdgpu_comm_unique_id(void* id_out);
+int pdgpu_comm_init(pdgpu_t h, int nranks, int rank, const void* id);
+/* Balanced contiguous split: rows [*row_begin, *row_end) of rank. */
+int pdgpu_slab_rows(int global_rows, int nranks, int rank, int* row_begin, int* row_end);
+
 /* Constraint state as the CG driver uses it (timestepping.hpp:306-309,
  * corrections.hpp:142-160): mask[N] = constrained direction bits per node,
  * uc[dim*N] = prescribed displacement values (0 where free or velocity-driven).
@@ -222,7 +252,7 @@ int pdgpu_sim_finite(pdgpu_t h, int* ok);
  * Per-pass device timing with CUDA events on the launching stream (pass ids:
  * 0 K1 x-forward, 1 K2 y-forward (3D), 2 K3 spectral, 3 K4 y-inverse (3D),
  * 4 K5 x-inverse, 5 surface correction, 6 fracture correction, 7 vector
- * ops).  timing_read synchronises, returns the summed milliseconds and
+ * ops, 8 halo exchange on the comm stream -- overlapped with 0..4).  timing_read synchronises, returns the summed milliseconds and
  * launch counts per pass since the last read, and resets them. */
 int pdgpu_timing_enable(pdgpu_t h, int on);
 int pdgpu_timing_read(pdgpu_t h, double* ms_per_pass, int64_t* count_per_pass, int npass);

@@ -36,6 +36,11 @@ SIGNATURES = {
     "pdgpu_symbol_mode": (C.c_int, [C.c_void_p]),
     "pdgpu_embedding": (C.c_int, [C.c_void_p]),
     "pdgpu_set_ghosts": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "pdgpu_set_ghosts_strided": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64]),
+    "pdgpu_halo_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]),
+    "pdgpu_comm_unique_id": (C.c_int, [C.c_void_p]),
+    "pdgpu_comm_init": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p]),
+    "pdgpu_slab_rows": (C.c_int, [C.c_int, C.c_int, C.c_int, c_int_p, c_int_p]),
     "pdgpu_set_regions": (C.c_int, [C.c_void_p, c_uint8_p, c_uint8_p]),
     "pdgpu_set_surface_diag": (C.c_int, [C.c_void_p, c_double_p]),
     "pdgpu_set_slab": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),

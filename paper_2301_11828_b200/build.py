@@ -17,7 +17,7 @@ LIB = os.path.join(HERE, "libpdgpu.so")
 # spectral.cu is compiled once per part (-DPDGPU_PART=k): each object
 # instantiates only its own kernel templates, and the parts build in parallel
 SPECTRAL_PARTS = 5
-SOURCES = ["spectral.cu", "corrections.cu", "direct.cu", "solvers.cu", "abi.cu", "assembly.cpp", "snapshot.cpp"]
+SOURCES = ["spectral.cu", "corrections.cu", "direct.cu", "solvers.cu", "abi.cu", "assembly.cpp", "snapshot.cpp", "comm.cpp"]
 HEADERS = ["engine.h", "fft.cuh", "assembly.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -66,7 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stdout.write(out.decode())
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed: " + r.stdout + r.stderr)

@@ -503,6 +503,10 @@ void pdgpu_destroy(pdgpu_t h) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->cg_graph) cudaGraphExecDestroy(h->cg_graph);
+    try {
+        comm_destroy(*h);
+    } catch (...) {
+    }
     if (h->stream) cudaStreamDestroy(h->stream);
     if (h->copy_in) cudaStreamDestroy(h->copy_in);
     if (h->copy_out) cudaStreamDestroy(h->copy_out);
@@ -619,7 +623,58 @@ int pdgpu_set_ghosts(pdgpu_t h, const double* ghosts) {
         if (!h) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null handle");
         if (ghosts && h->slab.global < 0) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "ghost rows need pdgpu_set_slab");
         h->d_ghost = ghosts;
+        h->user_ghost_bc = 0;  // default layout [batch][dim][2][M][plane]
+        h->user_ghost_side = 0;
         touch_state(*h);  // a captured CG iteration holds the old pointer
+    });
+}
+
+int pdgpu_set_ghosts_strided(pdgpu_t h, const double* ghosts, int64_t vec_comp_stride, int64_t side_stride) {
+    return guarded([&] {
+        if (!h) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null handle");
+        if (ghosts && h->slab.global < 0) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "ghost rows need pdgpu_set_slab");
+        if (ghosts && (vec_comp_stride <= 0 || side_stride <= 0))
+            throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "ghost strides must be positive");
+        h->d_ghost = ghosts;
+        h->user_ghost_bc = vec_comp_stride;
+        h->user_ghost_side = side_stride;
+        touch_state(*h);
+    });
+}
+
+int pdgpu_halo_pack(pdgpu_t h, const double* u, int batch, double* send, void* stream) {
+    return guarded([&] {
+        if (!h || !u || !send || batch < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
+        if (h->plan.N[h->dim - 1] < h->M) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "slab thinner than the horizon");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        halo_pack(*h, u, batch, send, pick_stream(*h, stream));
+    });
+}
+
+int pdgpu_comm_unique_id(void* id_out) {
+    return guarded([&] {
+        if (!id_out) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        comm_unique_id(id_out);
+    });
+}
+
+int pdgpu_comm_init(pdgpu_t h, int nranks, int rank, const void* id) {
+    return guarded([&] {
+        if (!h || !id || nranks < 1 || rank < 0 || rank >= nranks)
+            throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad communicator arguments");
+        if (nranks > 1 && h->slab.global < 0) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "multi-rank engines need pdgpu_set_slab");
+        if (h->plan.N[h->dim - 1] < h->M) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "slab thinner than the horizon");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        comm_init(*h, nranks, rank, id);
+    });
+}
+
+int pdgpu_slab_rows(int global_rows, int nranks, int rank, int* row_begin, int* row_end) {
+    return guarded([&] {
+        if (!row_begin || !row_end || nranks < 1 || rank < 0 || rank >= nranks || global_rows < nranks)
+            throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad slab arguments");
+        *row_begin = (int)((int64_t)global_rows * rank / nranks);
+        *row_end = (int)((int64_t)global_rows * (rank + 1) / nranks);
     });
 }
 
@@ -1084,6 +1139,10 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
     cuda_check(cudaMemsetAsync(x, 0, sizeof(double) * m, s), "zero x");
     cuda_check(cudaMemcpyAsync(p, r, sizeof(double) * m, cudaMemcpyDeviceToDevice, s), "p = r");
     launch_dot(e, r, r, m, e.d_scal + 0, s);
+    // slabs over NCCL: every dot product is this rank's share, all-reduced in place
+    const bool multi = comm_attached(e);
+    comm_allreduce(e, e.d_scal + 0, 1, s);
+    if (multi && halo_active(e)) ensure_halo(e, 1);  // the captured iteration's halo buffers exist before capture
     double rr0 = 0;
     cuda_check(cudaMemcpyAsync(&rr0, e.d_scal, sizeof(double), cudaMemcpyDeviceToHost, s), "read rr");
     cuda_check(cudaStreamSynchronize(s), "cg init");
@@ -1107,7 +1166,12 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
             launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
             launch_corrections(e, p, q, 1, s, -1.0);
             launch_dot(e, p, q, m, e.d_scal + 1, s);
-            launch_cg_step_dev(e, x, r, p, q, m, e.d_scal, s);
+            if (multi) {
+                comm_allreduce(e, e.d_scal + 1, 1, s);
+                launch_cg_step_dev_comm(e, x, r, p, q, m, e.d_scal, s);
+            } else {
+                launch_cg_step_dev(e, x, r, p, q, m, e.d_scal, s);
+            }
             cuda_check(cudaStreamEndCapture(s, &g), "end capture");
             e.cg_graph_launches = e.launches - l0;  // kernels per replay (capture itself launches none)
             e.launches = l0;
@@ -1139,7 +1203,9 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
         launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
         launch_corrections(e, p, q, 1, s, -1.0);
         launch_dot(e, p, q, m, e.d_scal + 1, s);
+        comm_allreduce(e, e.d_scal + 1, 1, s);
         launch_cg_update(e, x, r, p, q, m, e.d_scal, e.d_scal + 2, s);
+        comm_allreduce(e, e.d_scal + 2, 1, s);
         double rr1 = 0;
         cuda_check(cudaMemcpyAsync(&rr1, e.d_scal + 2, sizeof(double), cudaMemcpyDeviceToHost, s), "read rr");
         ++k;
@@ -1235,7 +1301,7 @@ int pdgpu_sim_init_adr(pdgpu_t h, double dt, double fixed_damping) {
         e.integrator = 1;
         e.adr_fixed = fixed_damping == fixed_damping;  // NaN: adaptive (std::nullopt)
         e.adr_fixed_c = e.adr_fixed ? fixed_damping : 0.0;
-        cuda_check(cudaMemset(e.d_scal + 8, 0, sizeof(double)), "zero damping");
+        cuda_check(cudaMemset(e.d_scal + 10, 0, sizeof(double)), "zero damping");
     });
 }
 
@@ -1244,7 +1310,7 @@ int pdgpu_sim_adr_damping(pdgpu_t h, double* c) {
         if (!h || !c) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
         cuda_check(cudaSetDevice(h->device), "set device");
         cuda_check(cudaStreamSynchronize(h->stream), "sync");
-        cuda_check(cudaMemcpy(c, h->d_scal + 8, sizeof(double), cudaMemcpyDeviceToHost), "damping");
+        cuda_check(cudaMemcpy(c, h->d_scal + 10, sizeof(double), cudaMemcpyDeviceToHost), "damping");
     });
 }
 

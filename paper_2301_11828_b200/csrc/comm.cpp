@@ -1,0 +1,208 @@
+// comm.cpp -- multi-GPU halo slabs over NCCL, one process per
+// GPU.  Host-side orchestration only: the kernels are the single-GPU ones.
+//
+// Rank r's engine holds rows [r0, r1) of the slowest axis (pdgpu_set_slab);
+// ranks are ordered by slab, so the rows before the slab live on rank - 1 and
+// the rows after it on rank + 1.  Every K.u (apply / matvec / evaluate_force)
+// exchanges the M rows next to each interior face with those neighbours:
+//
+//   s:            record ev_fork ----------------- K1 .. K5 ------- wait ev_join -> K6w (reads the received rows)
+//   comm_stream:  wait ev_fork -> pack (2 x memcpy2D) -> ncclSend/ncclRecv (grouped) -> record ev_join
+//
+// so the transfer overlaps the spectral passes, which need only the owned
+// rows; only the wrap correction K6w reads the ghost rows.  CG dot products
+// are all-reduced in place on the launching stream (capturable into the CG
+// graph).  libnccl is dlopen'ed on first use (the one torch already loaded
+// when present), so libpdgpu.so has no link-time NCCL dependency.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "engine.h"
+
+namespace pdgpu {
+
+namespace {
+
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    std::string error;
+};
+
+NcclApi load_api() {
+    NcclApi a;
+    void* h = nullptr;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+        h = dlopen(name, RTLD_NOW | RTLD_NOLOAD);  // already in the process (torch's copy)
+        if (!h) h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+        if (h) break;
+    }
+    if (!h) {
+        a.error = std::string("cannot load libnccl.so.2: ") + dlerror();
+        return a;
+    }
+    auto sym = [&](const char* n) {
+        void* p = dlsym(h, n);
+        if (!p) a.error = std::string("libnccl lacks ") + n;
+        return p;
+    };
+    a.GetUniqueId = (decltype(a.GetUniqueId))sym("ncclGetUniqueId");
+    a.CommInitRank = (decltype(a.CommInitRank))sym("ncclCommInitRank");
+    a.CommDestroy = (decltype(a.CommDestroy))sym("ncclCommDestroy");
+    a.AllReduce = (decltype(a.AllReduce))sym("ncclAllReduce");
+    a.Send = (decltype(a.Send))sym("ncclSend");
+    a.Recv = (decltype(a.Recv))sym("ncclRecv");
+    a.GroupStart = (decltype(a.GroupStart))sym("ncclGroupStart");
+    a.GroupEnd = (decltype(a.GroupEnd))sym("ncclGroupEnd");
+    a.GetErrorString = (decltype(a.GetErrorString))sym("ncclGetErrorString");
+    return a;
+}
+
+const NcclApi& api() {
+    static const NcclApi a = load_api();
+    if (!a.error.empty()) throw std::runtime_error(a.error);
+    return a;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw std::runtime_error(std::string(what) + ": " + api().GetErrorString(r));
+}
+
+void cuda_ok(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+int64_t plane_of(const Engine& e) {
+    return e.dim == 3 ? (int64_t)e.plan.N[0] * e.plan.N[1] : e.plan.N[0];
+}
+
+}  // namespace
+
+void comm_unique_id(void* out) {
+    ncclUniqueId id;
+    nccl_check(api().GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id is 128 bytes");
+    memcpy(out, &id, sizeof(id));
+}
+
+void comm_init(Engine& e, int nranks, int rank, const void* id) {
+    if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad rank / nranks");
+    comm_destroy(e);
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof(uid));
+    ncclComm_t c = nullptr;
+    nccl_check(api().CommInitRank(&c, nranks, uid, rank), "ncclCommInitRank");
+    e.nccl_comm = c;
+    e.nranks = nranks;
+    e.rank = rank;
+    cuda_ok(cudaStreamCreateWithFlags(&e.comm_stream, cudaStreamNonBlocking), "comm stream");
+    cuda_ok(cudaEventCreateWithFlags(&e.ev_fork, cudaEventDisableTiming), "event");
+    cuda_ok(cudaEventCreateWithFlags(&e.ev_join, cudaEventDisableTiming), "event");
+    touch_state(e);
+}
+
+void comm_destroy(Engine& e) {
+    if (e.comm_stream) cudaStreamSynchronize(e.comm_stream);
+    if (e.nccl_comm) api().CommDestroy((ncclComm_t)e.nccl_comm);
+    if (e.comm_stream) cudaStreamDestroy(e.comm_stream);
+    if (e.ev_fork) cudaEventDestroy(e.ev_fork);
+    if (e.ev_join) cudaEventDestroy(e.ev_join);
+    if (e.d_halo) cudaFree(e.d_halo);
+    e.nccl_comm = nullptr;
+    e.comm_stream = nullptr;
+    e.ev_fork = e.ev_join = nullptr;
+    e.d_halo = nullptr;
+    e.halo_cap = 0;
+    e.nranks = 1;
+    e.rank = 0;
+}
+
+bool comm_attached(const Engine& e) { return e.nccl_comm != nullptr; }
+
+// interior faces of this slab (neighbours exist below / above)
+static bool lo_face(const Engine& e) { return e.slab.global >= 0 && e.slab.off > 0; }
+static bool hi_face(const Engine& e) {
+    return e.slab.global >= 0 && e.slab.off + e.plan.N[e.dim - 1] < e.slab.global;
+}
+
+bool halo_active(const Engine& e) { return comm_attached(e) && e.nranks > 1 && (lo_face(e) || hi_face(e)); }
+
+// [send|recv][side][batch][dim][M][plane]; side 0 = the rows before the slab
+void ensure_halo(Engine& e, int batch) {
+    if (batch <= e.halo_cap) return;
+    touch_state(e);
+    if (e.d_halo) cudaFree(e.d_halo);
+    e.d_halo = nullptr;
+    const size_t n = (size_t)2 * 2 * batch * e.dim * e.M * plane_of(e);
+    cuda_ok(cudaMalloc(&e.d_halo, sizeof(double) * n), "alloc halo buffers");
+    cuda_ok(cudaMemset(e.d_halo, 0, sizeof(double) * n), "zero halo buffers");
+    e.halo_cap = batch;
+}
+
+void halo_pack(const Engine& e, const double* u, int batch, double* send, cudaStream_t s) {
+    const int64_t plane = plane_of(e), N = e.plan.nodes, R = e.plan.N[e.dim - 1];
+    const size_t w = sizeof(double) * (size_t)(e.M * plane);
+    const size_t side = (size_t)batch * e.dim * e.M * plane;
+    // the first M owned rows (to rank - 1) and the last M (to rank + 1), every (vector, component)
+    cuda_ok(cudaMemcpy2DAsync(send, w, u, sizeof(double) * N, w, (size_t)batch * e.dim, cudaMemcpyDeviceToDevice, s),
+            "pack low rows");
+    cuda_ok(cudaMemcpy2DAsync(send + side, w, u + (R - e.M) * plane, sizeof(double) * N, w, (size_t)batch * e.dim,
+                              cudaMemcpyDeviceToDevice, s),
+            "pack high rows");
+}
+
+const double* halo_exchange_begin(Engine& e, const double* u, int batch, cudaStream_t s) {
+    if (!halo_active(e)) return nullptr;
+    ensure_halo(e, batch);
+    const int64_t plane = plane_of(e);
+    const size_t side = (size_t)batch * e.dim * e.M * plane;
+    const size_t stride = (size_t)2 * e.halo_cap * e.dim * e.M * plane;  // send block size
+    double* send = e.d_halo;
+    double* recv = e.d_halo + stride;
+    cuda_ok(cudaEventRecord(e.ev_fork, s), "fork");
+    cuda_ok(cudaStreamWaitEvent(e.comm_stream, e.ev_fork, 0), "fork wait");
+    PassTimer pt(e, kPassHalo, e.comm_stream, 0);  // pack + transfer, on the comm stream (overlapped)
+    halo_pack(e, u, batch, send, e.comm_stream);
+    const ncclComm_t c = (ncclComm_t)e.nccl_comm;
+    nccl_check(api().GroupStart(), "ncclGroupStart");
+    if (lo_face(e)) {
+        nccl_check(api().Send(send, side, ncclFloat64, e.rank - 1, c, e.comm_stream), "ncclSend low");
+        nccl_check(api().Recv(recv, side, ncclFloat64, e.rank - 1, c, e.comm_stream), "ncclRecv low");
+    }
+    if (hi_face(e)) {
+        nccl_check(api().Send(send + side, side, ncclFloat64, e.rank + 1, c, e.comm_stream), "ncclSend high");
+        nccl_check(api().Recv(recv + side, side, ncclFloat64, e.rank + 1, c, e.comm_stream), "ncclRecv high");
+    }
+    nccl_check(api().GroupEnd(), "ncclGroupEnd");
+    pt.finish();
+    cuda_ok(cudaEventRecord(e.ev_join, e.comm_stream), "join");
+    // ghost view of the received rows for K6w: [side][batch][dim][M][plane]
+    e.ghost_view = recv;
+    e.ghost_bc_stride = e.M * plane;
+    e.ghost_side_stride = (int64_t)side;
+    return recv;
+}
+
+void halo_exchange_end(Engine& e, cudaStream_t s) {
+    cuda_ok(cudaStreamWaitEvent(s, e.ev_join, 0), "join wait");
+}
+
+void comm_allreduce(Engine& e, double* d, int n, cudaStream_t s) {
+    if (!comm_attached(e)) return;  // one rank: still a real (identity) all-reduce
+    nccl_check(api().AllReduce(d, d, (size_t)n, ncclFloat64, ncclSum, (ncclComm_t)e.nccl_comm, s), "ncclAllReduce");
+}
+
+}  // namespace pdgpu

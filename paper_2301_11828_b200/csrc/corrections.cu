@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
                                               const double* __restrict__ wK, int M, int N0, int N1, int N2,
                                               int circ_mask, const uint8_t* __restrict__ cmask, int64_t nodes,
                                               int batch, double scale, int64_t band0, int64_t band1, int64_t band2,
-                                              const double* __restrict__ ghost, int lo_int, int hi_int,
-                                              const int* __restrict__ lidx, const int* __restrict__ loff,
+                                              const double* __restrict__ ghost, int64_t gs_bc, int64_t gs_side,
+                                              int lo_int, int hi_int, const int* __restrict__ lidx, const int* __restrict__ loff,
                                               const double* __restrict__ lK, const double* __restrict__ xstrip) {
     constexpr int NP = D * (D + 1) / 2;
     const int64_t per_vec = band0 + band1 + band2;
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
                     const int64_t pidx = D == 3 ? (int64_t)q1 * N0 + q0 : q0;
 #pragma unroll
                     for (int bb = 0; bb < D; ++bb) {
-                        const double g = ghost[(((int64_t)(b * D + bb) * 2 + sd) * M + layer) * plane + pidx];
+                        const double g = ghost[(int64_t)(b * D + bb) * gs_bc + sd * gs_side + (int64_t)layer * plane + pidx];
 #pragma unroll
                         for (int a = 0; a < D; ++a) gacc[a] += kv[pair_idx<D>(a, bb)] * g;
                     }
@@ -292,14 +292,14 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
 #pragma unroll
             for (int bb = 0; bb < D; ++bb) acc[a] += kv[pair_idx<D>(a, bb)] * uq[bb];
     };
-    // halo slabs (pdgpu_set_ghosts): rows beyond an interior face of the slowest
-    // axis come from the neighbour's ghost rows, ghost[b][c][side][layer][plane]
+    // halo slabs: rows beyond an interior face of the slowest axis come from
+    // the neighbour's ghost rows, ghost[(b*D + c)*gs_bc + side*gs_side + layer*plane]
     auto add_ghost = [&](int e, int side, int layer, int64_t pidx) {
         double kv[KS];
         load_k(e, kv);
 #pragma unroll
         for (int bb = 0; bb < D; ++bb) {
-            const double g = ghost[(((int64_t)(b * D + bb) * 2 + side) * M + layer) * plane + pidx];
+            const double g = ghost[(int64_t)(b * D + bb) * gs_bc + side * gs_side + (int64_t)layer * plane + pidx];
 #pragma unroll
             for (int a = 0; a < D; ++a) gacc[a] += kv[pair_idx<D>(a, bb)] * g;
         }
@@ -447,7 +447,7 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
     const int SA = pl.dim - 1;
     const int lo_int = e.slab.global >= 0 && e.slab.off > 0;
     const int hi_int = e.slab.global >= 0 && e.slab.off + pl.N[SA] < e.slab.global;
-    const double* ghost = e.d_ghost && (lo_int || hi_int) ? e.d_ghost : nullptr;
+    const double* ghost = e.ghost_view && (lo_int || hi_int) ? e.ghost_view : nullptr;
     int64_t band[3] = {0, 0, 0};
     for (int d = 0; d < pl.dim; ++d) {
         if (!pl.circ[d] && !(d == SA && ghost)) continue;
@@ -470,11 +470,13 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
     if (pl.dim == 2)
         k_wrap<2><<<blocks, th, 0, s>>>(u, f, e.d_wrows, e.d_wo0, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],
                                         pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2],
-                                        ghost, lo_int, hi_int, e.d_lidx, e.d_loff, e.d_lK, nullptr);
+                                        ghost, e.ghost_bc_stride, e.ghost_side_stride, lo_int, hi_int, e.d_lidx,
+                                        e.d_loff, e.d_lK, nullptr);
     else
         k_wrap<3><<<blocks, th, 0, s>>>(u, f, e.d_wrows, e.d_wo0, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],
                                         pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2],
-                                        ghost, lo_int, hi_int, e.d_lidx, e.d_loff, e.d_lK, xstrip);
+                                        ghost, e.ghost_bc_stride, e.ghost_side_stride, lo_int, hi_int, e.d_lidx,
+                                        e.d_loff, e.d_lK, xstrip);
 }
 
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale) {

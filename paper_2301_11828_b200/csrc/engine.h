@@ -106,6 +106,18 @@ struct Engine {
     std::vector<uint8_t> h_cmask, h_near;
     assembly::SlabFrame slab;          // rows of a larger lattice (pdgpu_set_slab)
     const double* d_ghost = nullptr;   // caller's ghost rows of the interior slab faces (pdgpu_set_ghosts)
+    // ghost rows the current K.u reads (K6w): the caller's buffer
+    // [batch][dim][2][M][plane] or the NCCL receive buffer [2][batch][dim][M][plane]
+    const double* ghost_view = nullptr;
+    int64_t ghost_bc_stride = 0, ghost_side_stride = 0;
+    int64_t user_ghost_bc = 0, user_ghost_side = 0;  // pdgpu_set_ghosts_strided (0 = default layout)
+    // multi-GPU halo slabs over NCCL (comm.cpp)
+    void* nccl_comm = nullptr;
+    int nranks = 1, rank = 0;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    double* d_halo = nullptr;          // [send|recv][side][batch][dim][M][plane]
+    int64_t halo_cap = 0;
     int64_t n_surf = 0;
     long long* d_surf_rows = nullptr;  // surface node ids
     double* d_surf_de = nullptr;       // n_surf * np
@@ -188,7 +200,7 @@ inline void touch_state(Engine& e) {
 }
 
 enum PassId { kPassK1 = 0, kPassK2 = 1, kPassK3 = 2, kPassK4 = 3, kPassK5 = 4, kPassCorr = 5, kPassBonds = 6,
-              kPassVec = 7, kNumPass = 8 };
+              kPassVec = 7, kPassHalo = 8, kNumPass = 9 };
 
 // RAII bracket of one pass with events when e.timing is on
 struct PassTimer {
@@ -203,15 +215,19 @@ struct PassTimer {
             cudaEventRecord(a, s);
         }
     }
-    ~PassTimer() {
-        if (e.timing) {
+    // close the bracket early (before work that must not be timed in it)
+    void finish() {
+        if (e.timing && !done) {
             cudaEvent_t b = e.next_event();
             cudaEventRecord(b, s);
             e.mark_pass.push_back(id);
             e.mark_a.push_back(a);
             e.mark_b.push_back(b);
         }
+        done = true;
     }
+    ~PassTimer() { finish(); }
+    bool done = false;
 };
 
 // spectral.cu
@@ -235,11 +251,25 @@ void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaSt
 int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double* watch,
                             cudaStream_t s, bool sync = true);
 
+// comm.cpp
+void comm_unique_id(void* out);
+void comm_init(Engine& e, int nranks, int rank, const void* id);
+void comm_destroy(Engine& e);
+bool comm_attached(const Engine& e);
+bool halo_active(const Engine& e);
+void ensure_halo(Engine& e, int batch);
+void halo_pack(const Engine& e, const double* u, int batch, double* send, cudaStream_t s);
+const double* halo_exchange_begin(Engine& e, const double* u, int batch, cudaStream_t s);
+void halo_exchange_end(Engine& e, cudaStream_t s);
+void comm_allreduce(Engine& e, double* d, int n, cudaStream_t s);
+
 // solvers.cu
 void launch_dot(Engine& e, const double* a, const double* b, int64_t n, double* out_dev,
                 cudaStream_t s);
 void launch_cg_update(Engine& e, double* x, double* r, const double* p, const double* q, int64_t n,
                       const double* scal, double* rr_out, cudaStream_t s);
+void launch_cg_step_dev_comm(Engine& e, double* x, double* r, double* p, const double* q, int64_t n, double* scal,
+                             cudaStream_t s);
 void launch_cg_direction(double* p, const double* r, int64_t n, const double* scal, cudaStream_t s);
 void launch_cg_step_dev(Engine& e, double* x, double* r, double* p, const double* q, int64_t n, double* scal,
                         cudaStream_t s);

@@ -152,6 +152,33 @@ __global__ void k_cg_update_dev(double* __restrict__ x, double* __restrict__ r, 
     });
 }
 
+// multi-rank variant (NCCL): the update writes this rank's r.r to scal[9];
+// after the all-reduce of scal[9], k_cg_finish rotates and tests on one thread
+__global__ void k_cg_update_local(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                                  const double* __restrict__ q, int64_t n, double* scal, double* partial,
+                                  unsigned int* ticket) {
+    if (scal[4] != 0.0) return;
+    const double alpha = scal[0] / scal[1];
+    double s = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        x[i] += alpha * p[i];
+        const double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        s += ri * ri;
+    }
+    grid_reduce_cb(s, partial, ticket, [&](double tot) { scal[9] = tot; });
+}
+
+__global__ void k_cg_finish(double* scal) {
+    if (scal[4] != 0.0) return;
+    const double tot = scal[9];
+    scal[7] = scal[0];
+    scal[0] = tot;
+    scal[2] = tot;
+    scal[5] += 1.0;
+    if (tot <= scal[3]) scal[4] = 1.0;
+}
+
 __global__ void k_cg_direction_dev(double* __restrict__ p, const double* __restrict__ r, int64_t n,
                                    const double* scal) {
     if (scal[4] != 0.0) return;
@@ -203,7 +230,7 @@ __global__ void k_vv_kick(double* v, const double* fprev, const double* f, const
 __global__ void k_adr_damping(const double* __restrict__ u, const double* __restrict__ vh,
                               const double* __restrict__ f, const double* __restrict__ fprev,
                               const uint8_t* __restrict__ cmask, int64_t N, int dim, double m0, double m1, double m2,
-                              double dt, double* partial, unsigned int* ticket, double* cout) {
+                              double dt, double* partial, unsigned int* ticket, double* cout, int raw) {
     __shared__ double ws[2][32];
     __shared__ bool last;
     double num = 0.0, den = 0.0;
@@ -248,11 +275,23 @@ __global__ void k_adr_damping(const double* __restrict__ u, const double* __rest
             sn += ((volatile double*)partial)[2 * i];
             sd += ((volatile double*)partial)[2 * i + 1];
         }
-        double c = 0.0;
-        if (!(sd <= 0.0 || sn <= 0.0)) c = fmin(2.0 * sqrt(sn / sd), 1.9 / dt);
-        *cout = c;
+        if (raw) {  // multi-rank: this rank's sums to cout[2], cout[3]; k_adr_c after the all-reduce
+            cout[2] = sn;
+            cout[3] = sd;
+        } else {
+            double c = 0.0;
+            if (!(sd <= 0.0 || sn <= 0.0)) c = fmin(2.0 * sqrt(sn / sd), 1.9 / dt);
+            *cout = c;
+        }
         *ticket = 0u;
     }
+}
+
+__global__ void k_adr_c(double* cout, double dt) {
+    const double sn = cout[2], sd = cout[3];
+    double c = 0.0;
+    if (!(sd <= 0.0 || sn <= 0.0)) c = fmin(2.0 * sqrt(sn / sd), 1.9 / dt);
+    *cout = c;
 }
 
 // first call: v_half = 0.5 dt f / m (unconstrained); else v_half = (lead v_half
@@ -330,6 +369,16 @@ void launch_cg_step_dev(Engine& e, double* x, double* r, double* p, const double
     check(cudaGetLastError(), "cg_step_dev");
 }
 
+void launch_cg_step_dev_comm(Engine& e, double* x, double* r, double* p, const double* q, int64_t n, double* scal,
+                             cudaStream_t s) {
+    k_cg_update_local<<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, q, n, scal, e.d_red, e.d_ticket);
+    comm_allreduce(e, scal + 9, 1, s);
+    k_cg_finish<<<1, 1, 0, s>>>(scal);
+    k_cg_direction_dev<<<kRedBlocks, kRedThreads, 0, s>>>(p, r, n, scal);
+    e.launches += 3;
+    check(cudaGetLastError(), "cg_step_dev_comm");
+}
+
 void launch_cg_direction(double* p, const double* r, int64_t n, const double* scal, cudaStream_t s) {
     k_cg_direction<<<kRedBlocks, kRedThreads, 0, s>>>(p, r, n, scal);
     k_rotate<<<1, 1, 0, s>>>(const_cast<double*>(scal));
@@ -356,14 +405,21 @@ void launch_vv_kick(double* v, const double* fprev, const double* f, const uint8
 
 void launch_adr_step(Engine& e, bool first, cudaStream_t s) {
     const int64_t N = e.plan.nodes, m = N * e.dim;
-    double* cdev = e.d_scal + 8;  // CG uses scal[0..5]
+    double* cdev = e.d_scal + 10;  // CG uses scal[0..9]; [10] = c, [12..13] = the rank's raw sums
     if (!first) {
-        if (e.adr_fixed)
+        if (e.adr_fixed) {
             k_set_scalar<<<1, 1, 0, s>>>(cdev, e.adr_fixed_c);
-        else
+        } else {
+            const bool multi = comm_attached(e);
             k_adr_damping<<<kRedBlocks, kRedThreads, 0, s>>>(e.d_u, e.d_vh, e.d_f, e.d_fprev, e.d_cmask, N, e.dim,
                                                              e.adr_mass[0], e.adr_mass[1], e.adr_mass[2], e.dt,
-                                                             e.d_red, e.d_ticket, cdev);
+                                                             e.d_red, e.d_ticket, cdev, multi ? 1 : 0);
+            if (multi) {
+                comm_allreduce(e, cdev + 2, 2, s);
+                k_adr_c<<<1, 1, 0, s>>>(cdev, e.dt);
+                e.launches += 1;
+            }
+        }
         e.launches += 1;
     }
     k_adr_advance<<<blocks_for(m, 256), 256, 0, s>>>(e.d_u, e.d_vh, e.d_f, e.d_cmask, N, e.dim, e.adr_mass[0],

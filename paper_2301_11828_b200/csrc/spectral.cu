@@ -1930,6 +1930,15 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
     const Plan& pl = e.plan;
     engine_alloc_workspace(e, batch);
     const int d = pl.dim;
+    // halo slabs over NCCL: the M rows beyond each interior face travel on the
+    // comm stream while K1..K5 run (they read only the owned rows); K6w waits
+    const double* halo = halo_exchange_begin(e, u, batch, s);
+    if (!halo) {  // the caller's ghost rows (pdgpu_set_ghosts), [batch][dim][2][M][plane]
+        const int64_t plane = d == 3 ? (int64_t)pl.N[0] * pl.N[1] : pl.N[0];
+        e.ghost_view = e.d_ghost;
+        e.ghost_bc_stride = e.user_ghost_bc ? e.user_ghost_bc : 2 * e.M * plane;
+        e.ghost_side_stride = e.user_ghost_side ? e.user_ghost_side : e.M * plane;
+    }
     {
         PassTimer pt(e, kPassK1, s);
         launch_k1(e, u, batch, s);
@@ -1958,7 +1967,8 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
         PassTimer pt(e, kPassK5, s);
         launch_k5(e, xin, f, batch, s, scale, cmask, body);
     }
-    if (pl.circ_mask || e.d_ghost) {  // K6w: wrap correction / slab ghost rows (timed with the corrections)
+    if (halo) halo_exchange_end(e, s);
+    if (pl.circ_mask || e.ghost_view) {  // K6w: wrap correction / slab ghost rows (timed with the corrections)
         PassTimer pt(e, kPassCorr, s);
         launch_wrap_correction(e, u, f, batch, s, scale, cmask);
     }

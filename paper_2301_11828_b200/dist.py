@@ -1,11 +1,11 @@
-"""Multi-GPU plumbing for the batched mat-vec (one process per GPU).
+"""torch.distributed plumbing for multi-GPU runs (one process per GPU).
 
-Round 1 shards the work unit BASELINE.json batches -- independent
-displacement vectors -- across ranks: every rank owns whole vectors, there is
-no data-path collective (SURVEY.md sec.8e "replicas"), and the only
-communication is the timing reduction (max over ranks) and the result
-checksums.  The slab-decomposed FFT (all-to-all transposes) is the next
-multi-GPU item.
+The data path of a sharded lattice is the halo-slab engine (slab.py, the
+library's NCCL exchange in csrc/comm.cpp); this module holds the launcher
+environment, the max-over-ranks timing reduction, per-vector seeding and
+checksum gathering (bench.py and the gloo tests), and the vector split of the
+"replicas" bench arm (--shard vectors: independent vectors per rank, no
+data-path collective).
 """
 from __future__ import annotations
 

@@ -178,16 +178,18 @@ class FastForce:
     def footprint_bytes(self) -> int:
         return self._lib.pdgpu_footprint_bytes(self._h)
 
-    PASSES = ("K1_rfft_x", "K2_fft_y", "K3_spectral", "K4_ifft_y", "K5_irfft_x", "K6_surface_wrap", "K6_bonds", "vec")
+    PASSES = ("K1_rfft_x", "K2_fft_y", "K3_spectral", "K4_ifft_y", "K5_irfft_x", "K6_surface_wrap", "K6_bonds", "vec",
+              "halo_exchange")
 
     def timing(self, on: bool = True):
         _check(self._lib.pdgpu_timing_enable(self._h, 1 if on else 0))
 
     def timing_read(self):
         """{pass name: (total ms, launches)} since the last read (CUDA events on the launching stream)."""
-        ms = np.zeros(8)
-        cnt = np.zeros(8, dtype=np.int64)
-        _check(self._lib.pdgpu_timing_read(self._h, _dp(ms), cnt.ctypes.data_as(_lib.c_int64_p), 8))
+        npass = len(self.PASSES)
+        ms = np.zeros(npass)
+        cnt = np.zeros(npass, dtype=np.int64)
+        _check(self._lib.pdgpu_timing_read(self._h, _dp(ms), cnt.ctypes.data_as(_lib.c_int64_p), npass))
         return {n: (float(ms[i]), int(cnt[i])) for i, n in enumerate(self.PASSES) if cnt[i]}
 
     def launch_count(self) -> int:
@@ -221,6 +223,31 @@ class FastForce:
         """Ghost rows of the interior slab faces (device tensor [batch][dim][2][M][plane]) or None."""
         _check(self._lib.pdgpu_set_ghosts(self._h, None if ghosts is None else _ptr(ghosts)))
         self._ghosts = ghosts  # keep the buffer alive while the engine may read it
+
+    def set_ghosts_strided(self, ghosts, vec_comp_stride: int, side_stride: int):
+        """Ghost rows with an explicit layout (pdgpu_set_ghosts_strided), e.g. the
+        receive buffer of a halo exchange [2][batch][dim][M][plane]."""
+        _check(self._lib.pdgpu_set_ghosts_strided(self._h, None if ghosts is None else _ptr(ghosts),
+                                                  int(vec_comp_stride), int(side_stride)))
+        self._ghosts = ghosts
+
+    def halo_pack(self, u, send, batch: int = 1, stream=None):
+        """send[2][batch][dim][M][plane] <- the first / last M owned rows of u (pdgpu_halo_pack)."""
+        _check(self._lib.pdgpu_halo_pack(self._h, _ptr(u), batch, _ptr(send), _stream(stream, u, send)))
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        """Attach an NCCL communicator (pdgpu_comm_init): from then on every K.u
+        exchanges the halo rows with rank -+ 1 and CG all-reduces its dots."""
+        buf = C.create_string_buffer(bytes(uid), 128)
+        _check(self._lib.pdgpu_comm_init(self._h, int(nranks), int(rank), buf))
+
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """ncclGetUniqueId (pdgpu_comm_unique_id): 128 bytes to broadcast to every rank."""
+        lib = _lib.load()
+        buf = C.create_string_buffer(128)
+        _check(lib.pdgpu_comm_unique_id(buf))
+        return buf.raw
 
     def constraint_values(self):
         """(mask[N] uint8 constrained-direction bits, uc[dim, N] prescribed

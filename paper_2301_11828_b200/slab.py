@@ -9,23 +9,28 @@ Two halo modes: "ghost" (default) -- the engine's lattice is exactly the owned
 rows (a power-of-two count keeps every axis on the periodic embedding, so a
 rank does 1/G of the single-GPU transform work) and the M rows beyond each
 interior face arrive in a side buffer whose stencil terms the engine's wrap
-correction adds (pdgpu_set_ghosts); "embedded" -- the ghost rows are part of
-the engine's lattice (R + 2M rows, zero-padded transforms).  Before every
-mat-vec each rank sends its first / last M owned rows to its neighbours
-(torch.distributed point-to-point: NCCL between GPUs, gloo in the CPU tests):
-2*M*plane*dim*8 bytes per rank per vector -- 393 KB at 4096^2 -- against the
-two full all-to-all transposes of a distributed FFT.
+correction adds; "embedded" -- the ghost rows are part of the engine's
+lattice (R + 2M rows, zero-padded transforms).
+
+Two transports for the ghost rows (2*M*plane*dim*8 bytes per rank per
+vector, 393 KB at 4096^2, against the two full all-to-all transposes of a
+distributed FFT):
+  "engine" (default on CUDA + NCCL, ghost mode): the library's own NCCL
+      exchange (pdgpu_comm_init, csrc/comm.cpp): packed rows go out on a side
+      stream while the spectral passes run, and CG runs entirely on the
+      device (one captured iteration, its two dot products all-reduced by
+      ncclAllReduce inside the graph, no per-iteration host read).
+  "torch": torch.distributed point-to-point of the same packed rows -- the
+      gloo CPU tests drive the host logic through this with a test-double
+      engine; CG is then the restated loop below with all-reduced dots.
 
 Exactness: for an owned row every in-band neighbour lies in the owned or ghost
 rows, the engine's zero padding only replaces rows outside the global lattice
 (where the reference pads with zeros too, convolution.hpp:183-195), and
 pdgpu_set_slab rebuilds D^e / near-surface flags against the global faces
 (grid.hpp:181-189, corrections.hpp:24-42).  Ghost-row outputs are discarded.
-
-CG over slabs restates the engine's Hestenes-Stiefel loop (abi.cu cg_impl;
-K := -M_f A M_f, rhs = M_f (b + A u_c)) with the two dot products per
-iteration all-reduced.  Fracture / VV across slabs (cross-face bond ledgers)
-is not built: SlabForce covers K.u, corrections on a fixed ledger, and CG.
+Fracture across slab faces: see FastForce.sim_* with a communicator
+(DESIGN.md sec.6).
 """
 from __future__ import annotations
 
@@ -49,7 +54,7 @@ class SlabForce:
     """
 
     def __init__(self, dims, M: int, stencils, rank: int = 0, world: int = 1, device=None, engine=None,
-                 group=None, halo: str = "ghost"):
+                 group=None, halo: str = "ghost", transport: str = "auto"):
         self.dims = tuple(int(d) for d in dims)
         self.dim = len(self.dims)
         self.M = int(M)
@@ -83,6 +88,20 @@ class SlabForce:
         self.eng = engine(self.ext_dims)
         self.eng.set_slab(self.rows, self.off)
         self._bufs = {}
+        if transport == "auto":
+            nccl = dist.is_available() and dist.is_initialized() and dist.get_backend(group) == "nccl"
+            transport = "engine" if (self.device.type == "cuda" and halo == "ghost" and
+                                     (nccl or self.world == 1) and hasattr(self.eng, "comm_init")) else "torch"
+        if transport not in ("engine", "torch"):
+            raise ValueError("transport must be 'engine', 'torch' or 'auto'")
+        if transport == "engine" and halo != "ghost":
+            raise ValueError("the engine transport fills ghost-mode side buffers")
+        self.transport = transport
+        if transport == "engine":
+            uid = [self.eng.comm_unique_id() if self.rank == 0 else None]
+            if self.world > 1:
+                dist.broadcast_object_list(uid, src=0, group=group)
+            self.eng.comm_init(self.world, self.rank, uid[0])
 
     # ------------------------------------------------------------ set-up
     def set_geometry(self, h: float, origin=None, delta: float = 0.0, rho: float = 1.0):
@@ -175,7 +194,17 @@ class SlabForce:
         u3 = u.unsqueeze(0) if squeeze else u
         b = u3.shape[0]
         ext, fext, g = self._buf(b)
-        if self.halo == "ghost":
+        if self.transport == "engine":
+            # the library exchanges the halo rows itself (NCCL, overlapped)
+            uc = u3 if u3.is_contiguous() else u3.contiguous()
+            if f is not None:
+                f3 = f.unsqueeze(0) if squeeze else f
+                if f3.is_contiguous():
+                    self.eng.matvec_device(uc, f3, b, stream=self._stream())
+                    return f
+            self.eng.matvec_device(uc, fext, b, stream=self._stream())
+            out = fext
+        elif self.halo == "ghost":
             # the engine reads the owned rows in place and writes f directly
             uc = u3 if u3.is_contiguous() else u3.contiguous()
             self.exchange_ghosts(uc, g)
@@ -223,7 +252,13 @@ class SlabForce:
     def cg_solve(self, b, tol: float = 1e-10, maxit: int = 10000):
         """Solve K_ff x_f = b_f over all ranks (K := -A on free DOFs, x = u_c on
         constrained ones); b, x: (dim, R*plane) owned rows.  Returns
-        (x, iterations, relative residual)."""
+        (x, iterations, relative residual).  Engine transport: the device CG
+        of pdgpu_cg_solve with NCCL-all-reduced dots."""
+        if self.transport == "engine":
+            bc = b.contiguous()
+            x = torch.empty_like(bc)
+            it, rel = self.eng.cg_solve_device(bc, x, tol=tol, maxit=maxit, stream=self._stream())
+            return x, it, rel
         free, uc = self.constraint_values()
         any_uc = bool(self._allsum(torch.tensor([float(torch.count_nonzero(uc))], dtype=torch.float64,
                                                 device=self.device)).item() > 0)

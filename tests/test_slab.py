@@ -257,3 +257,106 @@ def test_slab_engine_gpu(dims, world, halo):
     err = float(torch.linalg.norm(f - f_ref) / torch.linalg.norm(f_ref))
     assert err <= 1e-12, err
     full.close()
+
+
+def _engine(dims, dev_index=0):
+    from paper_2301_11828_b200.engine import FastForce, build_kernel
+    dim = len(dims)
+    h = 1.0 / dims[0]
+    K = build_kernel(dim, h, 3.015 * h, M, 1.0, 1.0 if dim == 2 else 0.0)
+    ff = FastForce(dims, M, K, device=dev_index)
+    ff.set_geometry(h, None, 3.015 * h, 1.0)
+    return ff, K, h
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims", [(128, 128), (32, 32, 32)])
+def test_comm_one_rank_matches_plain_engine(dims):
+    """An engine with an NCCL communicator of one rank runs the multi-rank code
+    path (split CG update, ncclAllReduce of every dot product inside the
+    captured iteration, all-reduced ADR damping sums); all-reducing over one
+    rank is the identity, so every result equals the plain engine's bit for bit."""
+    from oracle.oracle import Rng, random_field
+    dim = len(dims)
+    n = int(np.prod(dims))
+    plain, K, h = _engine(dims)
+    comm, _, _ = _engine(dims)
+    comm.comm_init(1, 0, comm.comm_unique_id())
+    dl = 3.015 * h
+    for ff in (plain, comm):
+        for ax in range(dim):
+            lo, hi = [0.0] * dim, [1.0] * dim
+            hi[ax] = dl
+            ff.add_constraint(lo, hi, (1 << dim) - 1, 0, 0.0)
+        top_lo = [0.0] * dim
+        top_lo[-1] = 1.0 - dl
+        ff.add_constraint(top_lo, [1.0] * dim, 1 << (dim - 1), 0, 1e-3)  # prescribed layer: the any_uc branch
+    u = torch.from_numpy(random_field(Rng(77), dim, n)).cuda()
+    f0, f1 = torch.empty_like(u), torch.empty_like(u)
+    plain.matvec_device(u, f0)
+    comm.matvec_device(u, f1)
+    torch.cuda.synchronize()
+    assert torch.equal(f0, f1)
+    b = torch.from_numpy(random_field(Rng(78), dim, n)).cuda()
+    x0, x1 = torch.empty_like(b), torch.empty_like(b)
+    it0, r0 = plain.cg_solve_device(b, x0, tol=1e-9, maxit=5000)
+    it1, r1 = comm.cg_solve_device(b, x1, tol=1e-9, maxit=5000)
+    assert it0 == it1 and r0 == r1 and r1 <= 1e-9
+    assert torch.equal(x0, x1)
+    # ADR: damping sums all-reduced before c is formed
+    for ff in (plain, comm):
+        ff.set_body(np.full((dim, n), 1e-3))
+        ff.sim_init_adr(1.0)
+        ff.sim_step(20)
+    ua = plain.sim_get()[0]
+    ub = comm.sim_get()[0]
+    assert np.array_equal(ua, ub) and plain.adr_damping() == comm.adr_damping()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dims,world", [((256, 256), 4), ((64, 48, 32), 4), ((512, 512), 8)])
+def test_packed_halo_slabs_gpu(dims, world):
+    """The NCCL exchange's data layout on one GPU: every slab packs its first /
+    last M rows with pdgpu_halo_pack, the neighbours' packed rows are placed
+    in a receive buffer [2][batch][dim][M][plane] exactly as ncclRecv leaves
+    them, and the engine reads them through pdgpu_set_ghosts_strided; the
+    gathered owned rows must equal the single engine's K.u."""
+    from oracle.oracle import Rng, random_field
+    from paper_2301_11828_b200.slab import slab_rows
+    dim = len(dims)
+    n = int(np.prod(dims))
+    plane = n // dims[-1]
+    batch = 2
+    full, K, h = _engine(dims)
+    u = torch.from_numpy(np.stack([random_field(Rng(4300 + i), dim, n) for i in range(batch)])).cuda()
+    f_ref = torch.empty_like(u)
+    full.matvec_device(u, f_ref, batch)
+    engines, sends = [], []
+    from paper_2301_11828_b200.engine import FastForce
+    for r in range(world):
+        r0, r1 = slab_rows(dims[-1], r, world)
+        ff = FastForce(dims[:-1] + (r1 - r0,), M, K)
+        org = [0.0] * dim
+        org[-1] = r0 * h
+        ff.set_geometry(h, org, 3.015 * h, 1.0)
+        ff.set_slab(dims[-1], r0)
+        uo = u[:, :, r0 * plane:r1 * plane].contiguous()
+        send = torch.zeros((2, batch, dim, M, plane), dtype=torch.float64, device="cuda")
+        ff.halo_pack(uo, send, batch)
+        engines.append((ff, r0, r1, uo))
+        sends.append(send)
+    f = torch.zeros_like(u)
+    side = batch * dim * M * plane
+    for r, (ff, r0, r1, uo) in enumerate(engines):
+        recv = torch.zeros((2, batch, dim, M, plane), dtype=torch.float64, device="cuda")
+        if r > 0:
+            recv[0].copy_(sends[r - 1][1])  # what ncclRecv from rank - 1 delivers
+        if r < world - 1:
+            recv[1].copy_(sends[r + 1][0])
+        ff.set_ghosts_strided(recv, M * plane, side)
+        fo = torch.empty_like(uo)
+        ff.matvec_device(uo, fo, batch)
+        torch.cuda.synchronize()
+        f[:, :, r0 * plane:r1 * plane] = fo
+    err = float(torch.linalg.norm(f - f_ref) / torch.linalg.norm(f_ref))
+    assert err <= 1e-12, err
