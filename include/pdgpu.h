@@ -53,7 +53,9 @@ void pdgpu_destroy(pdgpu_t h);
 
 /* Grid::h / Grid::origin (grid.hpp:15-20), Horizon::delta (grid.hpp:114-116),
  * Material::rho (material.hpp:33-37): needed by positions (update_bonds,
- * crack seeding, constraints) and by the VV step. */
+ * crack seeding, constraints) and by the VV step.  For a slab engine
+ * (pdgpu_set_slab) the origin is the global lattice's: positions are
+ * computed from global node coordinates, as the reference does. */
 int pdgpu_set_geometry(pdgpu_t h, double spacing, const double* origin, double delta, double rho);
 
 /* FastForce::apply(u, f)   convolution.hpp:249-259 -- f = A_hat u, the
@@ -155,7 +157,9 @@ int pdgpu_set_surface_diag(pdgpu_t h, const double* de);
 int pdgpu_set_ledger(pdgpu_t h, const int64_t* row_start, const int64_t* partners);
 /* BondLedger::break_bond for n pairs (p,q) (ledger.hpp:21-26). */
 int pdgpu_break_bonds(pdgpu_t h, const int64_t* pairs, int64_t n);
-/* Broken bonds as sorted (p,q) pairs, p < q; *count = total (may exceed cap). */
+/* Broken bonds as sorted (p,q) pairs, p < q; *count = total (may exceed cap).
+ * Global node ids: a slab engine lists the pairs whose lower node it holds
+ * (q may lie in the next slab), so the ranks' lists together are the ledger. */
 int pdgpu_ledger_pairs(pdgpu_t h, int64_t* out_pairs, int64_t cap, int64_t* count);
 /* apply_corrections(f, u, de, regions, ledger, K, grid)  corrections.hpp:76-110
  * f += De u (surface rows) + sum_q K(q-p)(u_p - u_q) (fracture rows), rows
@@ -223,6 +227,13 @@ int pdgpu_sim_init(pdgpu_t h, double dt, const double* v0);
 /* n_steps of Simulation::step (timestepping.hpp:209-241); s0 < 0 disables
  * fracture; watch as in update_bonds.  *broken = bonds broken in these steps. */
 int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64_t* broken);
+/* Halo slabs in one process: n engines holding consecutive row slabs of one
+ * lattice (each with pdgpu_set_slab, no communicator; one or several
+ * devices) advanced together by n_steps of Simulation::step.  Halo rows and
+ * the ledger words of bonds broken across a face move by device-to-device
+ * copies between the phases of each step (the NCCL path does the same
+ * inside pdgpu_sim_step).  *broken = bonds broken over all slabs. */
+int pdgpu_group_sim_step(pdgpu_t* engines, int n, int n_steps, double s0, const double* watch, int64_t* broken);
 /* Simulation<Dim> with Integrator::Adr (AdrIntegrator, timestepping.hpp:79-145;
  * adr_mass :150-162): the reference's quasi-static solver.  Same state and
  * constraints as sim_init (v0 = 0); fixed_damping NaN = adaptive Rayleigh-

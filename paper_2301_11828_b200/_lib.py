@@ -76,6 +76,7 @@ SIGNATURES = {
     "pdgpu_sim_set_velocity": (C.c_int, [C.c_void_p, c_double_p]),
     "pdgpu_sim_newly_broken": (C.c_int, [C.c_void_p, c_int64_p, C.c_int64, c_int64_p]),
     "pdgpu_sim_finite": (C.c_int, [C.c_void_p, c_int_p]),
+    "pdgpu_group_sim_step": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_double, c_double_p, c_int64_p]),
     "pdgpu_evaluate_force_host": (C.c_int, [C.c_void_p, c_double_p, c_double_p, C.c_int64]),
     "pdgpu_update_bonds_host": (C.c_int, [C.c_void_p, c_double_p, C.c_int64, C.c_double, c_double_p, c_int64_p,
                                           C.c_int64, c_int64_p]),

@@ -76,6 +76,20 @@ void coords_of(const Engine& e, int64_t p, int* c) {
     c[2] = (int)(p / ((int64_t)e.plan.N[0] * e.plan.N[1]));
 }
 
+// node position in GLOBAL coordinates (grid.hpp:53-57): a slab engine's rows
+// are rows [slab.off, ...) of the global lattice; origin is the global origin
+void pos_of(const Engine& e, int64_t p, double* x) {
+    int c[3];
+    coords_of(e, p, c);
+    if (e.slab.global >= 0) c[e.dim - 1] += e.slab.off;
+    for (int d = 0; d < e.dim; ++d) x[d] = e.origin[d] + (c[d] + 0.5) * e.h;
+}
+
+int64_t global_offset(const Engine& e) {
+    const int64_t plane = e.dim == 3 ? (int64_t)e.plan.N[0] * e.plan.N[1] : e.plan.N[0];
+    return e.slab.global >= 0 ? (int64_t)e.slab.off * plane : 0;
+}
+
 int find_offset(const Engine& e, const int* o) {
     for (int k = 0; k < e.nof; ++k)
         if (e.offs[3 * k] == o[0] && e.offs[3 * k + 1] == o[1] && e.offs[3 * k + 2] == o[2]) return k;
@@ -124,7 +138,7 @@ void rebuild_constraints(Engine& e) {
     for (const auto& cs : e.constraints) {
         for (int64_t p = 0; p < N; ++p) {
             double x[3];
-            assembly::node_pos(dim, e.plan.N, e.h, e.origin, p, x);
+            pos_of(e, p, x);
             if (!assembly::box_contains(dim, cs.lo, cs.hi, x)) continue;
             e.h_cmask[(size_t)p] |= cs.dir_mask;
             for (int d = 0; d < dim; ++d)
@@ -229,6 +243,40 @@ int64_t break_pairs(Engine& e, const int64_t* pairs, int64_t n) {
     cuda_check(cudaMemcpyAsync(cnt, e.d_counters, sizeof(cnt), cudaMemcpyDeviceToHost, e.stream), "counters");
     cuda_check(cudaStreamSynchronize(e.stream), "break pairs sync");
     cudaFree(d_quad);
+    e.n_bond_rows = (int64_t)cnt[0];
+    e.total_broken += (int64_t)cnt[1];
+    return (int64_t)cnt[1];
+}
+
+// one-sided breaks of bonds whose partner lives in another slab: (p, k,
+// counted) triples; counted = this slab owns the pair (its node is the lower)
+__global__ void k_break_halves(uint32_t* ledger, int lw, const long long* tri, int64_t n, long long* bond_rows,
+                               int* listed, unsigned long long* counters) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const long long p = tri[3 * i], k = tri[3 * i + 1];
+    const unsigned old = atomicOr(&ledger[p * lw + (k >> 5)], 1u << (k & 31));
+    if ((old >> (k & 31)) & 1u) return;
+    if (tri[3 * i + 2]) atomicAdd(&counters[1], 1ull);
+    if (atomicExch(&listed[p], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = p;
+}
+
+int64_t break_halves(Engine& e, const std::vector<long long>& tri) {
+    const int64_t m = (int64_t)tri.size() / 3;
+    if (m == 0) return 0;
+    ensure_ledger(e);
+    touch_state(e);
+    long long* d_tri = nullptr;
+    cuda_check(cudaMalloc(&d_tri, sizeof(long long) * tri.size()), "alloc halves");
+    cuda_check(cudaMemcpy(d_tri, tri.data(), sizeof(long long) * tri.size(), cudaMemcpyHostToDevice), "copy halves");
+    cuda_check(cudaMemsetAsync(e.d_counters + 1, 0, sizeof(unsigned long long), e.stream), "reset");
+    k_break_halves<<<(unsigned)((m + 127) / 128), 128, 0, e.stream>>>(e.d_ledger, e.lw, d_tri, m, e.d_bond_rows,
+                                                                      e.d_listed, e.d_counters);
+    cuda_check(cudaGetLastError(), "break halves");
+    unsigned long long cnt[2];
+    cuda_check(cudaMemcpyAsync(cnt, e.d_counters, sizeof(cnt), cudaMemcpyDeviceToHost, e.stream), "counters");
+    cuda_check(cudaStreamSynchronize(e.stream), "break halves sync");
+    cudaFree(d_tri);
     e.n_bond_rows = (int64_t)cnt[0];
     e.total_broken += (int64_t)cnt[1];
     return (int64_t)cnt[1];
@@ -499,10 +547,12 @@ void pdgpu_destroy(pdgpu_t h) {
                     h->d_cmask, h->d_surf_rows, h->d_surf_de, h->d_ledger, h->d_bond_rows, h->d_listed,
                     h->d_counters, h->d_new_pairs, h->d_body, h->d_cdofs, h->d_cval, h->d_ckind, h->d_u, h->d_v,
                     h->d_f, h->d_fprev, h->d_red, h->d_scal, h->d_ticket, h->d_cg, h->d_coltab,
-                    h->d_scratch, h->d_kc, h->d_uc_ids, h->d_uc_val};
+                    h->d_scratch, h->d_kc, h->d_uc_ids, h->d_uc_val, h->d_face_recv, h->d_halo};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->cg_graph) cudaGraphExecDestroy(h->cg_graph);
+    h->d_face_recv = nullptr;  // freed with the other buffers above
+    h->d_halo = nullptr;
     try {
         comm_destroy(*h);
     } catch (...) {
@@ -765,14 +815,18 @@ int pdgpu_ledger_pairs(pdgpu_t h, int64_t* out, int64_t cap, int64_t* count) {
             disp[k] = (long long)o[2] * h->plan.N[0] * h->plan.N[1] + (long long)o[1] * h->plan.N[0] + o[0];
         }
         std::sort(order.begin(), order.end(), [&](int a, int b) { return disp[a] < disp[b]; });
+        // global node ids: a slab engine reports the pairs whose lower node it
+        // holds (partners may lie in the next slab), so the union over ranks is
+        // the global ledger
+        const int64_t goff = global_offset(*h);
         int64_t c = 0;
         for (int64_t p = 0; p < N; ++p)
             for (int k : order) {
                 if (disp[k] <= 0) continue;
                 if (!((bits[(size_t)(p * h->lw + (k >> 5))] >> (k & 31)) & 1u)) continue;
                 if (out && c < cap) {
-                    out[2 * c] = p;
-                    out[2 * c + 1] = p + disp[k];
+                    out[2 * c] = goff + p;
+                    out[2 * c + 1] = goff + p + disp[k];
                 }
                 ++c;
             }
@@ -899,7 +953,7 @@ int pdgpu_add_load(pdgpu_t h, const double* lo, const double* hi, const double* 
         if (h->h_body.empty()) h->h_body.assign((size_t)(h->dim * N), 0.0);
         for (int64_t p = 0; p < N; ++p) {
             double x[3];
-            assembly::node_pos(h->dim, h->plan.N, h->h, h->origin, p, x);
+            pos_of(*h, p, x);
             if (!assembly::box_contains(h->dim, lo, hi, x)) continue;
             for (int d = 0; d < h->dim; ++d) h->h_body[(size_t)(d * N + p)] += value[d];
         }
@@ -936,39 +990,66 @@ static void seed_impl(Engine& e, const double* geom, bool notch, int64_t* added)
             hi[d] = d == axis ? geom[1] + geom[2] : geom[6 + d];
         }
     }
+    // visit the nodes within delta + h of the crack hull (fracture.hpp:164-198),
+    // in global lattice coordinates; a slab engine visits its own rows and
+    // also sees partners in the neighbouring slabs (the bond's lower node owns
+    // it, q > p as in fracture.hpp:189, and each side keeps its own half)
+    const int SA = dim - 1;
+    const int zoff = e.slab.global >= 0 ? e.slab.off : 0;
+    int G[3] = {e.plan.N[0], e.plan.N[1], e.plan.N[2]};
+    if (e.slab.global >= 0) G[SA] = e.slab.global;
     int clo[3] = {0, 0, 0}, chi[3] = {0, 0, 0};
     const double pad = e.delta + e.h;
     for (int d = 0; d < dim; ++d) {
         clo[d] = std::max(0, (int)floor((lo[d] - pad - e.origin[d]) / e.h));
-        chi[d] = std::min(e.plan.N[d] - 1, (int)ceil((hi[d] + pad - e.origin[d]) / e.h));
+        chi[d] = std::min(G[d] - 1, (int)ceil((hi[d] + pad - e.origin[d]) / e.h));
     }
+    clo[SA] = std::max(clo[SA], zoff);
+    chi[SA] = std::min(chi[SA], zoff + e.plan.N[SA] - 1);
+    auto gpos = [&](const int* cg, double* x) {
+        for (int d = 0; d < dim; ++d) x[d] = e.origin[d] + (cg[d] + 0.5) * e.h;
+    };
+    auto glin = [&](const int* cg) { return ((int64_t)cg[2] * G[1] + cg[1]) * G[0] + cg[0]; };
     std::vector<int64_t> pairs;
+    std::vector<long long> halves;  // (p, k, counted): the partner lives in another slab
     const int* N = e.plan.N;
     int c[3];
     for (c[2] = clo[2]; c[2] <= chi[2]; ++c[2])
         for (c[1] = clo[1]; c[1] <= chi[1]; ++c[1])
             for (c[0] = clo[0]; c[0] <= chi[0]; ++c[0]) {
-                const int64_t p = ((int64_t)c[2] * N[1] + c[1]) * N[0] + c[0];
+                int cl[3] = {c[0], c[1], c[2]};
+                cl[SA] -= zoff;
+                const int64_t p = ((int64_t)cl[2] * N[1] + cl[1]) * N[0] + cl[0];
+                const int64_t gp = glin(c);
                 double xp[3];
-                assembly::node_pos(dim, N, e.h, e.origin, p, xp);
+                gpos(c, xp);
                 for (int k = 0; k < e.nof; ++k) {
                     const int* o = &e.offs[3 * k];
                     int qc[3] = {c[0] + o[0], c[1] + o[1], c[2] + o[2]};
                     bool in = true;
-                    for (int d = 0; d < dim; ++d) in = in && qc[d] >= 0 && qc[d] < N[d];
+                    for (int d = 0; d < dim; ++d) in = in && qc[d] >= 0 && qc[d] < G[d];
                     if (!in) continue;
-                    const int64_t q = ((int64_t)qc[2] * N[1] + qc[1]) * N[0] + qc[0];
-                    if (q < p) continue;
+                    const bool local = qc[SA] >= zoff && qc[SA] < zoff + N[SA];
+                    const int64_t gq = glin(qc);
+                    if (gq < gp && local) continue;  // visited from q
                     double xq[3];
-                    assembly::node_pos(dim, N, e.h, e.origin, q, xq);
-                    const bool cross = notch ? assembly::notch_crosses(geom, xp, xq) : assembly::segment_crosses(geom, xp, xq);
-                    if (cross) {
+                    gpos(qc, xq);
+                    const double* a = gq > gp ? xp : xq;  // lower node first, as the reference visits it
+                    const double* b = gq > gp ? xq : xp;
+                    const bool cross = notch ? assembly::notch_crosses(geom, a, b) : assembly::segment_crosses(geom, a, b);
+                    if (!cross) continue;
+                    if (local) {
+                        int ql[3] = {qc[0], qc[1], qc[2]};
+                        ql[SA] -= zoff;
                         pairs.push_back(p);
-                        pairs.push_back(q);
+                        pairs.push_back(((int64_t)ql[2] * N[1] + ql[1]) * N[0] + ql[0]);
+                    } else {
+                        halves.insert(halves.end(), {(long long)p, (long long)k, gq > gp ? 1LL : 0LL});
                     }
                 }
             }
-    const int64_t n = break_pairs(e, pairs.data(), (int64_t)pairs.size() / 2);
+    int64_t n = break_pairs(e, pairs.data(), (int64_t)pairs.size() / 2);
+    n += break_halves(e, halves);
     if (added) *added = n;
 }
 
@@ -994,6 +1075,7 @@ int pdgpu_seed_notch(pdgpu_t h, const double* notch, int64_t* added) {
 // the host (e.last_pairs) in the reference's visiting order
 static int64_t update_bonds_impl(Engine& e, const double* u, double s0, const double* watch) {
     ensure_ledger(e);
+    halo_exchange_now(e, u, e.stream);  // slabs: the rows beyond the upper face, for the bonds this slab owns
     const int64_t N = e.plan.nodes;
     const size_t lbytes = sizeof(uint32_t) * (size_t)(N * e.lw);
     // ledger before the sweep: if one sweep breaks more bonds than the device
@@ -1003,6 +1085,13 @@ static int64_t update_bonds_impl(Engine& e, const double* u, double s0, const do
     cuda_check(cudaMallocAsync((void**)&d_prev, lbytes, e.stream), "alloc ledger snapshot");
     cuda_check(cudaMemcpyAsync(d_prev, e.d_ledger, lbytes, cudaMemcpyDeviceToDevice, e.stream), "snapshot");
     const int64_t n = launch_update_bonds(e, u, s0, watch, e.stream);
+    if (halo_active(e)) {
+        ledger_exchange(e, e.stream);  // slabs: mirror the bits of bonds broken across the face below
+        unsigned long long rows = 0;
+        cuda_check(cudaMemcpyAsync(&rows, e.d_counters, sizeof(rows), cudaMemcpyDeviceToHost, e.stream), "rows");
+        cuda_check(cudaStreamSynchronize(e.stream), "merge");
+        e.n_bond_rows = (int64_t)rows;
+    }
     std::vector<std::pair<long long, long long>> pk;  // (p, offset index)
     if (n > 0 && n <= e.new_pairs_cap) {
         std::vector<long long> raw((size_t)(2 * n));
@@ -1027,11 +1116,12 @@ static int64_t update_bonds_impl(Engine& e, const double* u, double s0, const do
     // the reference's visiting order: p ascending, then for_each_offset order
     std::sort(pk.begin(), pk.end());
     const int* Nd = e.plan.N;
+    const int64_t goff = global_offset(e);
     e.last_pairs.resize(2 * pk.size());
     for (size_t i = 0; i < pk.size(); ++i) {
         const int* o = &e.offs[3 * pk[i].second];
-        e.last_pairs[2 * i] = pk[i].first;
-        e.last_pairs[2 * i + 1] = pk[i].first + (long long)o[2] * Nd[0] * Nd[1] + (long long)o[1] * Nd[0] + o[0];
+        e.last_pairs[2 * i] = goff + pk[i].first;
+        e.last_pairs[2 * i + 1] = goff + pk[i].first + (long long)o[2] * Nd[0] * Nd[1] + (long long)o[1] * Nd[0] + o[0];
     }
     return n;
 }
@@ -1084,7 +1174,7 @@ static bool prescribed_values(const Engine& e, std::vector<double>& huc) {
         if (cs.kind != 0) continue;
         for (int64_t pn = 0; pn < N; ++pn) {
             double xx[3];
-            assembly::node_pos(e.dim, e.plan.N, e.h, e.origin, pn, xx);
+            pos_of(e, pn, xx);
             if (!assembly::box_contains(e.dim, cs.lo, cs.hi, xx)) continue;
             for (int d = 0; d < e.dim; ++d)
                 if ((cs.dir_mask >> d) & 1u) huc[(size_t)(d * N + pn)] = cs.value;
@@ -1314,55 +1404,177 @@ int pdgpu_sim_adr_damping(pdgpu_t h, double* c) {
     });
 }
 
+// ---- one Simulation::step (timestepping.hpp:209-241) in phases, so the
+// single-process slab group (pdgpu_group_sim_step) can exchange halo rows and
+// face ledgers between them; pdgpu_sim_step runs them back to back (the NCCL
+// exchanges happen inside the force and after the sweep).
+static void sim_initial_force(Engine& e) {
+    if (e.force_ready) return;
+    evaluate_force_impl(e, e.d_u, e.d_f, e.stream);
+    e.force_ready = true;
+}
+
+static void sim_pre(Engine& e) {
+    const int64_t N = e.plan.nodes;
+    if (e.integrator == 1) {  // ADR branch (timestepping.hpp:215-220)
+        launch_adr_step(e, e.step == 0, e.stream);
+    } else {
+        launch_vv_drift(e.d_u, e.d_v, e.d_f, e.d_cmask, N, e.dim, e.dt, 1.0 / e.rho, e.stream);
+    }
+    e.t += e.dt;
+    launch_enforce(e.d_u, e.d_v, e.d_cdofs, e.d_cval, e.d_ckind, e.n_cdofs, e.t, e.stream);
+    std::swap(e.d_f, e.d_fprev);
+}
+
+static void sim_force(Engine& e) { evaluate_force_impl(e, e.d_u, e.d_f, e.stream); }
+
+static void sim_post(Engine& e, double s0, const double* watch) {
+    const int64_t N = e.plan.nodes;
+    if (e.integrator != 1) {
+        launch_vv_kick(e.d_v, e.d_fprev, e.d_f, e.d_cmask, N, e.dim, e.dt, 1.0 / e.rho, e.stream);
+        launch_enforce(e.d_u, e.d_v, e.d_cdofs, e.d_cval, e.d_ckind, e.n_cdofs, e.t, e.stream);
+    }
+    // the stretch test reads u's halo rows from this step's force exchange
+    if (s0 >= 0) launch_update_bonds(e, e.d_u, s0, watch, e.stream, /*sync=*/false);
+    ++e.step;
+}
+
+static void sim_begin(Engine& e, int n_steps, double s0) {
+    if (!e.d_u) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "simulation not initialised");
+    e.sim_swept = s0 >= 0 && n_steps > 0;
+    if (s0 >= 0) {
+        ensure_ledger(e);
+        cuda_check(cudaMemsetAsync(e.d_counters + 2, 0, sizeof(unsigned long long), e.stream), "reset breaks");
+    }
+}
+
+static int64_t sim_end(Engine& e, double s0) {
+    int64_t nb = 0;
+    if (s0 >= 0) {
+        // one read-back per call: row count and breaks of all steps
+        unsigned long long cnt[3];
+        cuda_check(cudaMemcpyAsync(cnt, e.d_counters, sizeof(cnt), cudaMemcpyDeviceToHost, e.stream), "counters");
+        cuda_check(cudaStreamSynchronize(e.stream), "sim step");
+        e.n_bond_rows = (int64_t)cnt[0];
+        e.bond_rows_on_device = false;
+        nb = (int64_t)cnt[2];
+        e.total_broken += nb;
+    }
+    cuda_check(cudaStreamSynchronize(e.stream), "sim step");
+    return nb;
+}
+
 int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64_t* broken) {
     return guarded([&] {
         if (!h || !h->d_u) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "simulation not initialised");
         cuda_check(cudaSetDevice(h->device), "set device");
         Engine& e = *h;
-        const int64_t N = e.plan.nodes;
-        const double inv_rho = 1.0 / e.rho;
-        int64_t nb = 0;
-        e.sim_swept = s0 >= 0 && n_steps > 0;
-        if (s0 >= 0) {
-            ensure_ledger(e);
-            cuda_check(cudaMemsetAsync(e.d_counters + 2, 0, sizeof(unsigned long long), e.stream), "reset breaks");
-        }
+        sim_begin(e, n_steps, s0);
         for (int i = 0; i < n_steps; ++i) {
-            if (!e.force_ready) {
-                evaluate_force_impl(e, e.d_u, e.d_f, e.stream);
-                e.force_ready = true;
-            }
-            if (e.integrator == 1) {  // ADR branch (timestepping.hpp:215-220)
-                launch_adr_step(e, e.step == 0, e.stream);
-                e.t += e.dt;
-                launch_enforce(e.d_u, e.d_v, e.d_cdofs, e.d_cval, e.d_ckind, e.n_cdofs, e.t, e.stream);
-                std::swap(e.d_f, e.d_fprev);
-                evaluate_force_impl(e, e.d_u, e.d_f, e.stream);
-                if (s0 >= 0) launch_update_bonds(e, e.d_u, s0, watch, e.stream, /*sync=*/false);
-                ++e.step;
-                continue;
-            }
-            launch_vv_drift(e.d_u, e.d_v, e.d_f, e.d_cmask, N, e.dim, e.dt, inv_rho, e.stream);
-            e.t += e.dt;
-            launch_enforce(e.d_u, e.d_v, e.d_cdofs, e.d_cval, e.d_ckind, e.n_cdofs, e.t, e.stream);
-            std::swap(e.d_f, e.d_fprev);
-            evaluate_force_impl(e, e.d_u, e.d_f, e.stream);
-            launch_vv_kick(e.d_v, e.d_fprev, e.d_f, e.d_cmask, N, e.dim, e.dt, inv_rho, e.stream);
-            launch_enforce(e.d_u, e.d_v, e.d_cdofs, e.d_cval, e.d_ckind, e.n_cdofs, e.t, e.stream);
-            if (s0 >= 0) launch_update_bonds(e, e.d_u, s0, watch, e.stream, /*sync=*/false);
-            ++e.step;
+            sim_initial_force(e);
+            sim_pre(e);
+            sim_force(e);
+            sim_post(e, s0, watch);
+            if (s0 >= 0) ledger_exchange(e, e.stream);  // NCCL slabs: mirror bonds broken across the face below
         }
-        if (s0 >= 0) {
-            // one read-back per call: row count and breaks of all steps
-            unsigned long long cnt[3];
-            cuda_check(cudaMemcpyAsync(cnt, e.d_counters, sizeof(cnt), cudaMemcpyDeviceToHost, e.stream), "counters");
-            cuda_check(cudaStreamSynchronize(e.stream), "sim step");
-            e.n_bond_rows = (int64_t)cnt[0];
-            e.bond_rows_on_device = false;
-            nb = (int64_t)cnt[2];
-            e.total_broken += nb;
+        const int64_t nb = sim_end(e, s0);
+        if (broken) *broken = nb;
+    });
+}
+
+// ---- single-process slab group: n engines holding consecutive row slabs of
+// one lattice (pdgpu_set_slab), on one or several devices, stepped together;
+// halo rows and face ledgers move by device copies instead of NCCL.
+static void group_halo(pdgpu_t* hs, int n) {
+    for (int r = 0; r < n; ++r) {
+        Engine& e = *hs[r];
+        cuda_check(cudaSetDevice(e.device), "set device");
+        ensure_halo(e, 1);
+        halo_pack(e, e.d_u, 1, e.d_halo, e.stream);
+        if (!e.ev_fork) cuda_check(cudaEventCreateWithFlags(&e.ev_fork, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventRecord(e.ev_fork, e.stream), "pack done");
+    }
+    for (int r = 0; r < n; ++r) {
+        Engine& e = *hs[r];
+        cuda_check(cudaSetDevice(e.device), "set device");
+        const int64_t plane = e.dim == 3 ? (int64_t)e.plan.N[0] * e.plan.N[1] : e.plan.N[0];
+        const size_t side = (size_t)e.dim * e.M * plane;  // batch 1
+        double* recv = e.d_halo + (size_t)2 * e.halo_cap * e.dim * e.M * plane;
+        for (int sd = 0; sd < 2; ++sd) {
+            const int nb = sd == 0 ? r - 1 : r + 1;
+            if (nb < 0 || nb >= n) continue;
+            Engine& o = *hs[nb];
+            cuda_check(cudaStreamWaitEvent(e.stream, o.ev_fork, 0), "wait pack");
+            // the neighbour's high rows arrive as side 0, its low rows as side 1
+            const double* src = o.d_halo + (sd == 0 ? side : 0);
+            cuda_check(cudaMemcpyPeerAsync(recv + sd * side, e.device, src, o.device, sizeof(double) * side, e.stream),
+                       "halo copy");
         }
-        cuda_check(cudaStreamSynchronize(e.stream), "sim step");
+        e.ghost_view = recv;
+        e.ghost_bc_stride = e.M * plane;
+        e.ghost_side_stride = (int64_t)side;
+        e.halo_external = true;
+    }
+}
+
+static void group_faces(pdgpu_t* hs, int n) {
+    for (int r = 0; r < n; ++r) {
+        Engine& e = *hs[r];
+        cuda_check(cudaSetDevice(e.device), "set device");
+        cuda_check(cudaEventRecord(e.ev_fork, e.stream), "sweep done");
+    }
+    for (int r = 1; r < n; ++r) {
+        Engine& e = *hs[r];
+        Engine& o = *hs[r - 1];
+        cuda_check(cudaSetDevice(e.device), "set device");
+        ledger_face_buffer(e);
+        const int64_t plane = e.dim == 3 ? (int64_t)e.plan.N[0] * e.plan.N[1] : e.plan.N[0];
+        const size_t bytes = sizeof(uint32_t) * (size_t)e.M * plane * e.lw;
+        cuda_check(cudaStreamWaitEvent(e.stream, o.ev_fork, 0), "wait sweep");
+        cuda_check(cudaMemcpyPeerAsync(e.d_face_recv, e.device, ledger_face_send(o), o.device, bytes, e.stream),
+                   "face copy");
+        launch_merge_face(e, e.d_face_recv, e.stream);
+    }
+}
+
+int pdgpu_group_sim_step(pdgpu_t* hs, int n, int n_steps, double s0, const double* watch, int64_t* broken) {
+    return guarded([&] {
+        if (!hs || n < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "empty group");
+        for (int r = 0; r < n; ++r) {
+            if (!hs[r] || !hs[r]->d_u) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "simulation not initialised");
+            if (n > 1 && hs[r]->slab.global < 0) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "group engines need pdgpu_set_slab");
+            if (comm_attached(*hs[r])) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "group engines carry no communicator");
+        }
+        struct Reset {
+            pdgpu_t* hs;
+            int n;
+            ~Reset() {
+                for (int r = 0; r < n; ++r) hs[r]->halo_external = false;
+            }
+        } reset{hs, n};
+        for (int r = 0; r < n; ++r) {
+            cuda_check(cudaSetDevice(hs[r]->device), "set device");
+            sim_begin(*hs[r], n_steps, s0);
+        }
+        auto each = [&](auto&& fn) {
+            for (int r = 0; r < n; ++r) {
+                cuda_check(cudaSetDevice(hs[r]->device), "set device");
+                fn(*hs[r]);
+            }
+        };
+        for (int i = 0; i < n_steps; ++i) {
+            if (!hs[0]->force_ready) {
+                group_halo(hs, n);
+                each([](Engine& e) { sim_initial_force(e); });
+            }
+            each([](Engine& e) { sim_pre(e); });
+            group_halo(hs, n);
+            each([](Engine& e) { sim_force(e); });
+            each([&](Engine& e) { sim_post(e, s0, watch); });
+            if (s0 >= 0) group_faces(hs, n);
+        }
+        int64_t nb = 0;
+        each([&](Engine& e) { nb += sim_end(e, s0); });
         if (broken) *broken = nb;
     });
 }
@@ -1425,10 +1637,11 @@ int pdgpu_sim_newly_broken(pdgpu_t h, int64_t* out, int64_t cap, int64_t* count)
         for (size_t i = 0; i < n; ++i) pk.push_back({raw[2 * i], raw[2 * i + 1]});
         std::sort(pk.begin(), pk.end());
         const int* Nd = h->plan.N;
+        const int64_t goff = global_offset(*h);
         for (int64_t i = 0; i < std::min<int64_t>((int64_t)n, cap); ++i) {
             const int* o = &h->offs[3 * pk[(size_t)i].second];
-            out[2 * i] = pk[(size_t)i].first;
-            out[2 * i + 1] = pk[(size_t)i].first + (long long)o[2] * Nd[0] * Nd[1] + (long long)o[1] * Nd[0] + o[0];
+            out[2 * i] = goff + pk[(size_t)i].first;
+            out[2 * i + 1] = goff + pk[(size_t)i].first + (long long)o[2] * Nd[0] * Nd[1] + (long long)o[1] * Nd[0] + o[0];
         }
     });
 }

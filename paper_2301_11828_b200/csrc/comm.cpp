@@ -121,6 +121,8 @@ void comm_destroy(Engine& e) {
     if (e.ev_fork) cudaEventDestroy(e.ev_fork);
     if (e.ev_join) cudaEventDestroy(e.ev_join);
     if (e.d_halo) cudaFree(e.d_halo);
+    if (e.d_face_recv) cudaFree(e.d_face_recv);
+    e.d_face_recv = nullptr;
     e.nccl_comm = nullptr;
     e.comm_stream = nullptr;
     e.ev_fork = e.ev_join = nullptr;
@@ -132,13 +134,10 @@ void comm_destroy(Engine& e) {
 
 bool comm_attached(const Engine& e) { return e.nccl_comm != nullptr; }
 
-// interior faces of this slab (neighbours exist below / above)
-static bool lo_face(const Engine& e) { return e.slab.global >= 0 && e.slab.off > 0; }
-static bool hi_face(const Engine& e) {
-    return e.slab.global >= 0 && e.slab.off + e.plan.N[e.dim - 1] < e.slab.global;
-}
+static bool lo_face(const Engine& e) { return slab_lo_face(e); }
+static bool hi_face(const Engine& e) { return slab_hi_face(e); }
 
-bool halo_active(const Engine& e) { return comm_attached(e) && e.nranks > 1 && (lo_face(e) || hi_face(e)); }
+bool halo_active(const Engine& e) { return comm_attached(e) && e.nranks > 1 && slab_has_faces(e); }
 
 // [send|recv][side][batch][dim][M][plane]; side 0 = the rows before the slab
 void ensure_halo(Engine& e, int batch) {
@@ -165,6 +164,7 @@ void halo_pack(const Engine& e, const double* u, int batch, double* send, cudaSt
 }
 
 const double* halo_exchange_begin(Engine& e, const double* u, int batch, cudaStream_t s) {
+    if (e.halo_external) return e.ghost_view;  // a group driver placed this call's ghost rows already
     if (!halo_active(e)) return nullptr;
     ensure_halo(e, batch);
     const int64_t plane = plane_of(e);
@@ -197,7 +197,39 @@ const double* halo_exchange_begin(Engine& e, const double* u, int batch, cudaStr
 }
 
 void halo_exchange_end(Engine& e, cudaStream_t s) {
+    if (e.halo_external) return;
     cuda_ok(cudaStreamWaitEvent(s, e.ev_join, 0), "join wait");
+}
+
+// the u halo of one field now (stream-ordered), for kernels outside a K.u
+void halo_exchange_now(Engine& e, const double* u, cudaStream_t s) {
+    if (halo_exchange_begin(e, u, 1, s)) halo_exchange_end(e, s);
+}
+
+// the ledger words of the last M rows (rank -> rank + 1) after a stretch sweep:
+// the lower slab decided every bond crossing the face between them
+void ledger_face_buffer(Engine& e) {
+    if (e.d_face_recv) return;
+    const size_t words = (size_t)e.M * plane_of(e) * e.lw;
+    cuda_ok(cudaMalloc(&e.d_face_recv, sizeof(uint32_t) * words), "alloc face ledger");
+    cuda_ok(cudaMemset(e.d_face_recv, 0, sizeof(uint32_t) * words), "zero face ledger");
+}
+
+const uint32_t* ledger_face_send(const Engine& e) {
+    const int64_t R = e.plan.N[e.dim - 1];
+    return e.d_ledger + (size_t)(R - e.M) * plane_of(e) * e.lw;
+}
+
+void ledger_exchange(Engine& e, cudaStream_t s) {
+    if (!halo_active(e) || !e.d_ledger) return;
+    ledger_face_buffer(e);
+    const size_t words = (size_t)e.M * plane_of(e) * e.lw;
+    const ncclComm_t c = (ncclComm_t)e.nccl_comm;
+    nccl_check(api().GroupStart(), "ncclGroupStart");
+    if (hi_face(e)) nccl_check(api().Send(ledger_face_send(e), words, ncclUint32, e.rank + 1, c, s), "ncclSend ledger");
+    if (lo_face(e)) nccl_check(api().Recv(e.d_face_recv, words, ncclUint32, e.rank - 1, c, s), "ncclRecv ledger");
+    nccl_check(api().GroupEnd(), "ncclGroupEnd");
+    if (lo_face(e)) launch_merge_face(e, e.d_face_recv, s);
 }
 
 void comm_allreduce(Engine& e, double* d, int n, cudaStream_t s) {

@@ -58,7 +58,8 @@ __global__ void k_bonds(const double* __restrict__ u, double* __restrict__ f, co
                         int64_t nrows, const unsigned long long* __restrict__ nrows_dev,
                         const uint32_t* __restrict__ ledger, int lw, const long long* __restrict__ disp,
                         const double* __restrict__ koff, int nof, const uint8_t* __restrict__ cmask, int64_t nodes,
-                        int batch, double scale) {
+                        int batch, double scale, const double* __restrict__ ghost, int64_t gs_bc, int64_t gs_side,
+                        int64_t plane, int R, int M) {
     constexpr int NP = D * (D + 1) / 2;
     // row count from the device when bonds broke since the host last looked
     // (sim_step does not synchronise per step); grid-stride over warps
@@ -82,8 +83,19 @@ __global__ void k_bonds(const double* __restrict__ u, double* __restrict__ f, co
             if (k < nof && ((word >> lane) & 1u)) {
                 const int64_t q = p + disp[k];
                 double du[D];
+                if (ghost && (q < 0 || q >= nodes)) {
+                    // partner beyond an interior slab face: the neighbour's halo rows
+                    const int64_t qrow = q >= 0 ? q / plane : -((-q + plane - 1) / plane);
+                    const int64_t qin = q - qrow * plane;
+                    const int side = qrow < 0 ? 0 : 1;
+                    const int64_t layer = side ? qrow - R : qrow + M;
 #pragma unroll
-                for (int c = 0; c < D; ++c) du[c] = up[c] - ub[(int64_t)c * nodes + q];
+                    for (int c = 0; c < D; ++c)
+                        du[c] = up[c] - ghost[(int64_t)(b * D + c) * gs_bc + side * gs_side + layer * plane + qin];
+                } else {
+#pragma unroll
+                    for (int c = 0; c < D; ++c) du[c] = up[c] - ub[(int64_t)c * nodes + q];
+                }
 #pragma unroll
                 for (int a = 0; a < D; ++a) {
                     double sacc = 0.0;
@@ -501,12 +513,19 @@ void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaSt
         const unsigned long long* nd = e.bond_rows_on_device ? e.d_counters : nullptr;
         // koff is stored right after the stencils in d_K (see abi.cu)
         const double* koff = e.d_K + e.np * e.ss;
+        const int SA = e.dim - 1;
+        const int64_t plane = e.dim == 3 ? (int64_t)e.plan.N[0] * e.plan.N[1] : e.plan.N[0];
+        const double* gh = slab_has_faces(e) ? e.ghost_view : nullptr;
         if (e.dim == 2)
             k_bonds<2><<<(unsigned)blocks, th, 0, s>>>(u, f, e.d_bond_rows, e.n_bond_rows, nd, e.d_ledger, e.lw,
-                                                      e.d_disp, koff, e.nof, e.d_cmask, N, batch, scale);
+                                                      e.d_disp, koff, e.nof, e.d_cmask, N, batch, scale, gh,
+                                                      e.ghost_bc_stride, e.ghost_side_stride, plane, e.plan.N[SA],
+                                                      e.M);
         else
             k_bonds<3><<<(unsigned)blocks, th, 0, s>>>(u, f, e.d_bond_rows, e.n_bond_rows, nd, e.d_ledger, e.lw,
-                                                      e.d_disp, koff, e.nof, e.d_cmask, N, batch, scale);
+                                                      e.d_disp, koff, e.nof, e.d_cmask, N, batch, scale, gh,
+                                                      e.ghost_bc_stride, e.ghost_side_stride, plane, e.plan.N[SA],
+                                                      e.M);
     }
     check(cudaGetLastError(), "corrections launch");
 }
@@ -520,6 +539,12 @@ struct BondArgs {
     int fast;     // squared-length pre-test enabled (s0 > -1)
     int has_watch;
     double wlo[3], whi[3];
+    // halo slabs: global row offset of the slowest axis (positions are global,
+    // grid.hpp:53-57), and the rows beyond the upper interior face (ghost side
+    // 1, read for bonds the lower slab owns: q > p, fracture.hpp:220)
+    int zoff, ghi;
+    const double* ghost;
+    int64_t gs_bc, gs_side, plane;
 };
 
 // counters[2] += counters[1] (breaks of this sweep, for a later host read)
@@ -541,8 +566,9 @@ __global__ void k_update_bonds(const double* __restrict__ u, uint32_t* ledger, c
     c[1] = (int)(t % A.Ny);
     c[2] = (int)(t / A.Ny);
     const double org[3] = {A.o0, A.o1, A.o2};
+    const int SA = A.dim - 1;
     double xp[3], up[3];
-    for (int d = 0; d < A.dim; ++d) xp[d] = pos_rn(org[d], c[d], A.h);
+    for (int d = 0; d < A.dim; ++d) xp[d] = pos_rn(org[d], c[d] + (d == SA ? A.zoff : 0), A.h);
     if (A.has_watch)
         for (int d = 0; d < A.dim; ++d)
             if (xp[d] < A.wlo[d] || xp[d] > A.whi[d]) return;
@@ -554,11 +580,12 @@ __global__ void k_update_bonds(const double* __restrict__ u, uint32_t* ledger, c
         bool inside = true;
         for (int d = 0; d < A.dim; ++d) {
             cq[d] = c[d] + offs[3 * k + d];
-            inside = inside && cq[d] >= 0 && cq[d] < dims[d];
+            inside = inside && cq[d] >= 0 && cq[d] < dims[d] + (d == SA ? A.ghi : 0);
         }
         if (!inside) continue;
+        const bool remote = cq[SA] >= dims[SA];  // in the next slab (ghost side 1)
         double xq[3];
-        for (int d = 0; d < A.dim; ++d) xq[d] = pos_rn(org[d], cq[d], A.h);
+        for (int d = 0; d < A.dim; ++d) xq[d] = pos_rn(org[d], cq[d] + (d == SA ? A.zoff : 0), A.h);
         if (A.has_watch) {
             bool in = true;
             for (int d = 0; d < A.dim; ++d) in = in && !(xq[d] < A.wlo[d] || xq[d] > A.whi[d]);
@@ -569,7 +596,9 @@ __global__ void k_update_bonds(const double* __restrict__ u, uint32_t* ledger, c
         double len0 = 0.0, len1 = 0.0;
         for (int d = 0; d < A.dim; ++d) {
             const double r = __dsub_rn(xq[d], xp[d]);
-            const double ev = __dsub_rn(__dadd_rn(r, u[(int64_t)d * nodes + q]), up[d]);
+            // ghost side 1, vector 0: layer * plane + in-plane index == q - nodes
+            const double uq = remote ? A.ghost[(int64_t)d * A.gs_bc + A.gs_side + (q - nodes)] : u[(int64_t)d * nodes + q];
+            const double ev = __dsub_rn(__dadd_rn(r, uq), up[d]);
             len0 = __dadd_rn(len0, __dmul_rn(r, r));
             len1 = __dadd_rn(len1, __dmul_rn(ev, ev));
         }
@@ -593,14 +622,14 @@ __global__ void k_update_bonds(const double* __restrict__ u, uint32_t* ledger, c
         if (brk) {
             atomicOr(&ledger[p * A.lw + (k >> 5)], 1u << (k & 31));
             const int kn = negk[k];
-            atomicOr(&ledger[q * A.lw + (kn >> 5)], 1u << (kn & 31));
+            if (!remote) atomicOr(&ledger[q * A.lw + (kn >> 5)], 1u << (kn & 31));  // remote: the face merge
             const unsigned long long slot = atomicAdd(&counters[1], 1ull);
             if ((int64_t)slot < cap) {
                 new_pairs[2 * slot] = p;
                 new_pairs[2 * slot + 1] = k;
             }
             if (atomicExch(&listed[p], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = p;
-            if (atomicExch(&listed[q], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = q;
+            if (!remote && atomicExch(&listed[q], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = q;
         }
     }
 }
@@ -632,6 +661,11 @@ __global__ void __launch_bounds__(256) k_update_bonds_tile2d(const double* __res
         const int gx = x0 + xx - M, gy = y0 + yy;
         const bool in = gx >= 0 && gx < A.Nx && gy < A.Ny;
         const int64_t q = (int64_t)gy * A.Nx + gx;
+        if (!in && gx >= 0 && gx < A.Nx && gy < A.Ny + A.ghi) {  // rows of the next slab (ghost side 1)
+            su[0][yy][xx] = A.ghost[A.gs_side + (q - nodes)];
+            su[1][yy][xx] = A.ghost[A.gs_bc + A.gs_side + (q - nodes)];
+            continue;
+        }
         su[0][yy][xx] = in ? u[q] : 0.0;
         su[1][yy][xx] = in ? u[nodes + q] : 0.0;
     }
@@ -640,7 +674,7 @@ __global__ void __launch_bounds__(256) k_update_bonds_tile2d(const double* __res
     const int cx = x0 + tx, cy = y0 + ty;
     if (cx >= A.Nx || cy >= A.Ny) return;
     const int64_t p = (int64_t)cy * A.Nx + cx;
-    const double xp0 = pos_rn(A.o0, cx, A.h), xp1 = pos_rn(A.o1, cy, A.h);
+    const double xp0 = pos_rn(A.o0, cx, A.h), xp1 = pos_rn(A.o1, cy + A.zoff, A.h);
     const double up0 = su[0][ty][tx + M], up1 = su[1][ty][tx + M];
     const uint32_t word = ledger[p];  // lw == 1 (<= 32 in-band offsets)
     uint32_t newbits = 0;
@@ -651,10 +685,10 @@ __global__ void __launch_bounds__(256) k_update_bonds_tile2d(const double* __res
             if (ox * ox + oy * oy > M * M || (oy == 0 && ox <= 0)) continue;
             const int k = band_index2d(M, ox, oy);
             const int qx = cx + ox, qy = cy + oy;
-            if (qx < 0 || qx >= A.Nx || qy >= A.Ny) continue;
+            if (qx < 0 || qx >= A.Nx || qy >= A.Ny + A.ghi) continue;
             if ((word >> k) & 1u) continue;
             const double r0 = __dsub_rn(pos_rn(A.o0, qx, A.h), xp0);
-            const double r1 = __dsub_rn(pos_rn(A.o1, qy, A.h), xp1);
+            const double r1 = __dsub_rn(pos_rn(A.o1, qy + A.zoff, A.h), xp1);
             const double e0 = __dsub_rn(__dadd_rn(r0, su[0][ty + oy][tx + M + ox]), up0);
             const double e1 = __dsub_rn(__dadd_rn(r1, su[1][ty + oy][tx + M + ox]), up1);
             double len0 = __dadd_rn(__dadd_rn(0.0, __dmul_rn(r0, r0)), __dmul_rn(r1, r1));
@@ -673,19 +707,59 @@ __global__ void __launch_bounds__(256) k_update_bonds_tile2d(const double* __res
             if (!brk) continue;
             newbits |= 1u << k;
             const int64_t q = p + (int64_t)oy * A.Nx + ox;
-            atomicOr(&ledger[q], 1u << band_index2d(M, -ox, -oy));
+            const bool local = qy < A.Ny;  // else the next slab's node: its bit arrives by the face merge
+            if (local) atomicOr(&ledger[q], 1u << band_index2d(M, -ox, -oy));
             const unsigned long long slot = atomicAdd(&counters[1], 1ull);
             if ((int64_t)slot < cap) {
                 new_pairs[2 * slot] = p;
                 new_pairs[2 * slot + 1] = k;
             }
-            if (atomicExch(&listed[q], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = q;
+            if (local && atomicExch(&listed[q], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = q;
         }
     }
     if (newbits) {
         atomicOr(&ledger[p], newbits);
         if (atomicExch(&listed[p], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = p;
     }
+}
+
+// Halo slabs: the lower slab decides the bonds crossing its upper face (q > p,
+// fracture.hpp:220) and sets only its own half; the ledger words of its last M
+// rows reach this slab (recv, [M][plane][lw]) and every bit whose partner lies
+// in this slab's rows becomes the mirrored bit here (ledger.hpp:21-26), the
+// row listed for the correction SpMV.  Idempotent (the ledger is monotone).
+__global__ void k_merge_face(uint32_t* ledger, int lw, const uint32_t* __restrict__ recv, const int* __restrict__ offs,
+                             const int* __restrict__ negk, int nof, int dim, int N0, int N1, int M, int64_t plane,
+                             long long* bond_rows, int* listed, unsigned long long* counters) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // (layer, in-plane node)
+    if (i >= (int64_t)M * plane) return;
+    const int layer = (int)(i / plane);
+    const int64_t pin = i - (int64_t)layer * plane;
+    const int c0 = (int)(pin % N0), c1 = dim == 3 ? (int)(pin / N0) : 0;
+    const int SA = dim - 1;
+    for (int k = 0; k < nof; ++k) {
+        if (!((recv[i * lw + (k >> 5)] >> (k & 31)) & 1u)) continue;
+        const int* o = offs + 3 * k;
+        const int row = layer - M + o[SA];  // local row of the partner
+        if (row < 0) continue;              // a bond inside the lower slab
+        const int q0 = c0 + o[0], q1 = dim == 3 ? c1 + o[1] : 0;
+        const int64_t q = (int64_t)row * plane + (dim == 3 ? (int64_t)q1 * N0 : 0) + q0;
+        (void)N1;
+        const int kn = negk[k];
+        const unsigned old = atomicOr(&ledger[q * lw + (kn >> 5)], 1u << (kn & 31));
+        if (!((old >> (kn & 31)) & 1u) && atomicExch(&listed[q], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = q;
+    }
+}
+
+void launch_merge_face(Engine& e, const uint32_t* recv, cudaStream_t s) {
+    const int64_t plane = e.dim == 3 ? (int64_t)e.plan.N[0] * e.plan.N[1] : e.plan.N[0];
+    const int64_t n = (int64_t)e.M * plane;
+    const int* negk = (const int*)(e.d_offs + 3 * e.nof);
+    k_merge_face<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(e.d_ledger, e.lw, recv, e.d_offs, negk, e.nof, e.dim,
+                                                           e.plan.N[0], e.plan.N[1], e.M, plane, e.d_bond_rows,
+                                                           e.d_listed, e.d_counters);
+    e.launches += 1;
+    check(cudaGetLastError(), "merge face");
 }
 
 // Returns the number of newly broken bonds (sync = true); new pairs are left
@@ -713,6 +787,13 @@ int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double*
         A.wlo[d] = watch && d < e.dim ? watch[d] : 0.0;
         A.whi[d] = watch && d < e.dim ? watch[e.dim + d] : 0.0;
     }
+    A.zoff = e.slab.global >= 0 ? e.slab.off : 0;
+    const bool hi_ghost = slab_hi_face(e) && e.ghost_view;
+    A.ghi = hi_ghost ? e.M : 0;
+    A.ghost = hi_ghost ? e.ghost_view : nullptr;
+    A.gs_bc = e.ghost_bc_stride;
+    A.gs_side = e.ghost_side_stride;
+    A.plane = e.dim == 3 ? (int64_t)pl.N[0] * pl.N[1] : pl.N[0];
     touch_state(e);  // the bond-row count changes under any captured launch sequence
     // reset the new-pair counter, keep the row counter
     check(cudaMemsetAsync(e.d_counters + 1, 0, sizeof(unsigned long long), s), "reset counter");

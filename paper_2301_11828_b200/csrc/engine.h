@@ -118,6 +118,8 @@ struct Engine {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     double* d_halo = nullptr;          // [send|recv][side][batch][dim][M][plane]
     int64_t halo_cap = 0;
+    bool halo_external = false;        // ghost rows placed by a single-process group driver (abi.cu)
+    uint32_t* d_face_recv = nullptr;   // ledger words of the lower neighbour's last M rows
     int64_t n_surf = 0;
     long long* d_surf_rows = nullptr;  // surface node ids
     double* d_surf_de = nullptr;       // n_surf * np
@@ -189,6 +191,13 @@ struct Engine {
     }
 };
 
+// halo slabs: this engine's lattice has an interior face below / above
+inline bool slab_lo_face(const Engine& e) { return e.slab.global >= 0 && e.slab.off > 0; }
+inline bool slab_hi_face(const Engine& e) {
+    return e.slab.global >= 0 && e.slab.off + e.plan.N[e.dim - 1] < e.slab.global;
+}
+inline bool slab_has_faces(const Engine& e) { return slab_lo_face(e) || slab_hi_face(e); }
+
 // Invalidate every captured launch sequence (see Engine::state_version).
 inline void touch_state(Engine& e) {
     ++e.state_version;
@@ -248,6 +257,7 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
                             const uint8_t* cmask);
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s,
                         double scale);
+void launch_merge_face(Engine& e, const uint32_t* recv, cudaStream_t s);
 int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double* watch,
                             cudaStream_t s, bool sync = true);
 
@@ -261,6 +271,10 @@ void ensure_halo(Engine& e, int batch);
 void halo_pack(const Engine& e, const double* u, int batch, double* send, cudaStream_t s);
 const double* halo_exchange_begin(Engine& e, const double* u, int batch, cudaStream_t s);
 void halo_exchange_end(Engine& e, cudaStream_t s);
+void halo_exchange_now(Engine& e, const double* u, cudaStream_t s);
+void ledger_face_buffer(Engine& e);
+const uint32_t* ledger_face_send(const Engine& e);
+void ledger_exchange(Engine& e, cudaStream_t s);
 void comm_allreduce(Engine& e, double* d, int n, cudaStream_t s);
 
 // solvers.cu

@@ -399,6 +399,22 @@ class FastForce:
         return u, v, f, t.value
 
 
+def group_sim_step(engines, n_steps: int = 1, s0: float = -1.0, watch=None) -> int:
+    """pdgpu_group_sim_step: n engines holding consecutive row slabs of one
+    lattice (set_slab), stepped together in one process -- halo rows and the
+    face ledgers move by device copies (the single-process counterpart of the
+    NCCL slab path).  Returns the bonds broken over all slabs."""
+    lib = _lib.load()
+    hs = (C.c_void_p * len(engines))(*[e.handle for e in engines])
+    dim = engines[0].dim
+    w = None if watch is None else _f64(np.concatenate([np.asarray(watch[0]), np.asarray(watch[1])]))
+    nb = C.c_int64()
+    _check(lib.pdgpu_group_sim_step(hs, len(engines), int(n_steps), float(s0), None if w is None else _dp(w),
+                                    C.byref(nb)))
+    del dim
+    return nb.value
+
+
 def write_snapshot(directory: str, dims, h: float, origin, u: np.ndarray, step: int, t: float, damage=None) -> str:
     """write_snapshot_dat (output.hpp:76-102): directory/snap_%07d.dat, %.17g values; returns the path."""
     lib = _lib.load()

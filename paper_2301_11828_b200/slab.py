@@ -105,10 +105,10 @@ class SlabForce:
 
     # ------------------------------------------------------------ set-up
     def set_geometry(self, h: float, origin=None, delta: float = 0.0, rho: float = 1.0):
-        """Global geometry; the engine's origin moves to its first (ghost) row
-        so node positions stay global (grid.hpp:53-57)."""
+        """Global geometry: the engine keeps the global origin and places its
+        rows at [off, off + L) of the global lattice (pdgpu_set_slab), so node
+        positions are the reference's own (grid.hpp:53-57) bit for bit."""
         org = np.zeros(self.dim) if origin is None else np.array(origin, dtype=np.float64)
-        org[-1] += self.off * h
         self.eng.set_geometry(h, org, delta, rho)
 
     def add_constraint(self, lo, hi, dir_mask: int, kind: int = 0, value: float = 0.0):

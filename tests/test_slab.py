@@ -97,7 +97,11 @@ class OracleSlabEngine:
         return np.ascontiguousarray(fe[:, gl:gl + self.ext[-1]].reshape(self.dim, -1))
 
     def set_geometry(self, h, origin, delta, rho):
-        self.h, self.origin, self._o = h, np.array(origin, dtype=np.float64), None
+        """pdgpu_set_geometry contract for slabs: the global origin; this engine's
+        first row sits at row `off` of the global lattice."""
+        org = np.array(origin, dtype=np.float64)
+        org[-1] += self.off * h
+        self.h, self.origin, self._o = h, org, None
 
     def add_constraint(self, lo, hi, mask, kind=0, value=0.0):
         self.cons.append((lo, hi, mask, kind, value))
@@ -360,3 +364,75 @@ def test_packed_halo_slabs_gpu(dims, world):
         f[:, :, r0 * plane:r1 * plane] = fo
     err = float(torch.linalg.norm(f - f_ref) / torch.linalg.norm(f_ref))
     assert err <= 1e-12, err
+
+
+def _vv_engines(dims, world, dt_scale=0.8, rate_per_step=1e-4):
+    """Config-5 geometry (notch (0,0.5)-(0.25,0.5), velocity-driven top/bottom
+    delta-layers) on the whole lattice and on `world` row slabs."""
+    from paper_2301_11828_b200.engine import FastForce, build_kernel
+    from paper_2301_11828_b200.slab import slab_rows
+    n = dims[0]
+    h = 1.0 / n
+    dl = 3.015 * h
+    K = build_kernel(2, h, dl, M, 1.0, 1.0)
+    lam = max(sum(2.0 * np.abs(K[0 if (a, b) == (0, 0) else (1 if a != b else 2)]).sum() for b in range(2))
+              for a in range(2))
+    dt = dt_scale * 2.0 * (1.0 / lam) ** 0.5
+    rate = rate_per_step / dt
+
+    def setup(ff):
+        ff.set_geometry(h, [0.0, 0.0], dl, 1.0)
+        ff.add_constraint((0.0, 1.0 - dl), (1.0, 1.0), 0b10, 1, rate)
+        ff.add_constraint((0.0, 0.0), (1.0, dl), 0b10, 1, -rate)
+
+    full = FastForce(dims, M, K)
+    setup(full)
+    slabs = []
+    for r in range(world):
+        r0, r1 = slab_rows(dims[1], r, world)
+        ff = FastForce((dims[0], r1 - r0), M, K)
+        ff.set_slab(dims[1], r0)
+        setup(ff)
+        slabs.append(ff)
+    return full, slabs, dt
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_fracture_across_slabs_gpu(world):
+    """Velocity Verlet with bond breaking over row slabs (pdgpu_group_sim_step,
+    the single-process form of the NCCL slab path): the notch and the torn
+    layers' bonds cross slab faces; per-step breaks, the ledger (union of the
+    slabs' pairs, global ids) and u must equal the single engine's."""
+    from paper_2301_11828_b200.engine import group_sim_step
+    dims = (256, 256)
+    full, slabs, dt = _vv_engines(dims, world)
+    a = full.seed_segment((0.0, 0.5), (0.25, 0.5))
+    b = sum(s.seed_segment((0.0, 0.5), (0.25, 0.5)) for s in slabs)
+    assert a == b > 0
+
+    def union():
+        return np.concatenate([s.ledger_pairs() for s in slabs])
+
+    def rows(x):
+        return x[np.lexsort((x[:, 1], x[:, 0]))]
+
+    assert np.array_equal(rows(union()), full.ledger_pairs())
+    full.sim_init(dt)
+    for s in slabs:
+        s.sim_init(dt)
+    total = 0
+    for blk in range(8):
+        pf = [full.sim_step(1, s0=1e-3) for _ in range(10)]
+        pg = [group_sim_step(slabs, 1, s0=1e-3) for _ in range(10)]
+        assert pf == pg, blk
+        total += sum(pf)
+        assert np.array_equal(rows(union()), full.ledger_pairs()), blk
+    assert total > 100
+    uf = full.sim_get()[0]
+    plane = dims[0]
+    ug = np.concatenate([s.sim_get()[0] for s in slabs], axis=1)
+    assert np.linalg.norm(ug - uf) / np.linalg.norm(uf) <= 1e-10
+    for s in slabs:
+        s.close()
+    full.close()
