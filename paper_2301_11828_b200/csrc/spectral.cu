@@ -804,10 +804,10 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
     // rows): one TMA bulk copy per row, else per-thread cp.async with zero fill
     const bool bulk = Nx == rowlen;
     __shared__ __align__(8) uint64_t bar;
-    if (bulk) {
-        if (threadIdx.x == 0) mbar_init(&bar, 1);
-        __syncthreads();
-    }
+    __shared__ double2 stw[FftTwTable<LOGQ, 4>::SIZE];
+    fill_fft_tw_table<LOGQ, 4>(stw, tw, logTWN);
+    if (bulk && threadIdx.x == 0) mbar_init(&bar, 1);
+    __syncthreads();
     unsigned ph = 0;
     auto fetch = [&](int64_t tile) {
         const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
@@ -861,7 +861,7 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
         }
         __syncthreads();  // row buffers free: they receive the spectra below
         reg_fft<LOGQ, 4, -1, BlockBar, true>(v, t, reinterpret_cast<double2*>(xd + gi * XB),
-                                             make_fft_tw<LOGQ, 4>(opaque(t), tw, logTWN), BlockBar{});
+                                             make_fft_tw_s<LOGQ, 4>(opaque(t), stw), BlockBar{});
         double2* spec = reinterpret_cast<double2*>(rowbuf + r * RS) + eo * XB;
 #pragma unroll
         for (int j = 0; j < R; ++j) spec[nat_slot<T>(t, j)] = v[j];
@@ -1168,6 +1168,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
             bulk_load(park, src, xbytes, &bars[gi]);
         }
     };
+    __shared__ double2 stw[FftTwTable<LOGQ, kPipeLogR>::SIZE];
+    fill_fft_tw_table<LOGQ, kPipeLogR>(stw, tw, logTWN);
     if (t == 0) mbar_init(&bars[gi], 1);
     __syncthreads();
     unsigned ph = 0;
@@ -1227,7 +1229,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
 #pragma unroll
                     for (int j = 0; j < RR; ++j) v[j] = cmul(v[j], tw32r<-1>(j * (16 / RR), w));
                 }
-                reg_fft<LOGQ, kPipeLogR, -1, BlockBar, true>(v, t, xb, make_fft_tw<LOGQ, kPipeLogR>(opaque(t), tw, logTWN),
+                reg_fft<LOGQ, kPipeLogR, -1, BlockBar, true>(v, t, xb, make_fft_tw_s<LOGQ, kPipeLogR>(opaque(t), stw),
                                                              BlockBar{});
                 if (c == 0) {
 #pragma unroll
@@ -1276,7 +1278,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
                         prefetch(x, ok);
                     }
                 }
-                reg_fft<LOGQ, kPipeLogR, 1, BlockBar, true>(v, t, xb, make_fft_tw<LOGQ, kPipeLogR>(opaque(t), tw, logTWN),
+                reg_fft<LOGQ, kPipeLogR, 1, BlockBar, true>(v, t, xb, make_fft_tw_s<LOGQ, kPipeLogR>(opaque(t), stw),
                                                             BlockBar{});
                 double2* dst = z0 + a * cstride;
                 if (NH == 1) {
