@@ -116,6 +116,11 @@ static inline int ilog2(int64_t v) {
 constexpr int kSmemBudget = 210 * 1024;
 
 static int xbuf_slots(int logq) { return (1 << logq) + ((1 << logq) >> 4) + 1; }
+// TMA-gather / TMA-store row kernels (two rows per CTA): per-transform buffer
+// stride with 2*stride = 4 (mod 8) 16-byte slots, so the two rows' buffers sit
+// 64 bytes apart (mod 128): a quarter-warp spanning both rows hits all 32 banks
+__host__ __device__ constexpr int xbuf_stride_rows(int xb) { return xb + ((2 - (xb & 3)) & 3); }
+static int xbuf_stride_rows_h(int logq) { return xbuf_stride_rows(xbuf_slots(logq)); }
 static int threads_per_transform(int logq, int logrmax) { return 1 << std::max(0, logq - logrmax); }
 
 // box tensor map over S[slab][kx][row] (complex): dims {2*Nrow doubles, Hx, nslab},
@@ -315,7 +320,8 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
                                                     const double* __restrict__ body, int64_t nodes,
                                                     const __grid_constant__ CUtensorMap tm) {
     using Sh = FftShape<LOGQ, 4>;
-    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
+    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R;
+    constexpr int XB = TMAG ? xbuf_stride_rows(Sh::XBUF) : Sh::XBUF;  // per-transform buffer stride
     constexpr int TR = 1 << LOGTR;
     extern __shared__ double2 sm[];
     const int gi = threadIdx.x >> Sh::LOGT;
@@ -335,7 +341,11 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
     // item loads are issued together (the gather is latency bound).
     // e^{+2 pi i k/Px} = e^{2 pi i 2 j0/Px} e^{2 pi i u/R} (x e^{2 pi i/Px} e^{-i pi/2} for odd k).
     {
-        constexpr int LA = (2 * T >= 8) ? 3 : 0;
+        // TMAG: quarter-warp = 4 consecutive j x the 2 rows (LA = 2), and the
+        // even / odd k of the same j swapped on (j >> 1) & 1 -- the landed
+        // [k][row] block is then read conflict-free (8 distinct 16-byte bank
+        // groups per quarter-warp instead of 2 or 4)
+        constexpr int LA = TMAG ? 2 : ((2 * T >= 8) ? 3 : 0);
         constexpr int U = R / 2;
         const int rr = (threadIdx.x >> LA) & (TR - 1);
         const int j0 = ((threadIdx.x >> (LA + LOGTR)) << LA) + (threadIdx.x & ((1 << LA) - 1));
@@ -355,12 +365,19 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
                 for (int bx = 0; bx < nbox; ++bx) tma_load_3d(&tm, land + bx * 256 * TR, &bar, 2 * row0, bx * 256, slab);
             }
             mbar_wait(&bar, 0);
+            static_assert(U % 2 == 0, "even / odd k halves");
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
+            for (int u = 0; u < U / 2; ++u) {
+                // items u (k = 2j) and u + U/2 (k = 2j + 1) of the same j
                 const int j = j0 + 2 * T * u;
-                const int k = j < Q / 2 ? 2 * j : 2 * (j - Q / 2) + 1;
-                Xa[u] = land[k * TR + rr];
-                Xb[u] = land[(halfP - k) * TR + rr];
+                const int ke = 2 * j, ko = 2 * j + 1;
+                const bool sw = (j >> 1) & 1;
+                const double2 a1 = land[(sw ? ko : ke) * TR + rr], a2 = land[(sw ? ke : ko) * TR + rr];
+                const double2 b1 = land[(halfP - (sw ? ko : ke)) * TR + rr], b2 = land[(halfP - (sw ? ke : ko)) * TR + rr];
+                Xa[u] = sw ? a2 : a1;
+                Xa[u + U / 2] = sw ? a1 : a2;
+                Xb[u] = sw ? b2 : b1;
+                Xb[u + U / 2] = sw ? b1 : b2;
             }
             if (threadIdx.x < nr) xq = land[Q * TR + threadIdx.x];
             __syncthreads();  // the landing area is about to be overwritten by E / O
@@ -899,10 +916,12 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
                 const int a = a0 + 2 * T * uu;
                 const double2 We = tw32r<-1>(uu * (32 / R), W0), Wo = tw32r<-1>(uu * (32 / R), W1);
                 const double2 Wem = make_double2(-We.x, We.y), Wom = make_double2(-Wo.x, Wo.y);
-                ob[(2 * a) * TR + rr] = post(e1[uu], cconj(e2[uu]), We);
-                ob[(2 * Q - 2 * a) * TR + rr] = post(e2[uu], cconj(e1[uu]), Wem);
-                ob[(2 * a + 1) * TR + rr] = post(o1[uu], cconj(o2[uu]), Wo);
-                ob[(2 * Q - 2 * a - 1) * TR + rr] = post(o2[uu], cconj(o1[uu]), Wom);
+                const double2 xe = post(e1[uu], cconj(e2[uu]), We), xem = post(e2[uu], cconj(e1[uu]), Wem);
+                const double2 xo = post(o1[uu], cconj(o2[uu]), Wo), xom = post(o2[uu], cconj(o1[uu]), Wom);
+                ob[(2 * a) * TR + rr] = xe;
+                ob[(2 * Q - 2 * a) * TR + rr] = xem;
+                ob[(2 * a + 1) * TR + rr] = xo;
+                ob[(2 * Q - 2 * a - 1) * TR + rr] = xom;
             }
             if (a0 == 0) ob[Q * TR + rr] = post(Aq, cconj(Aq), make_double2(0.0, -1.0));
             fence_proxy_async();
@@ -1657,7 +1676,8 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
     // TMA-landed gathers (periodic rows, two per CTA; PDGPU_K5_TMA=0 disables)
     if (cx && TR == 2 && lqx >= 8 && use_tma && encode_box_map(tm, xin, Ny, pl.Hx, nslab, TR)) {
         const int nbox = (pl.Hx + 255) / 256;
-        const size_t tsm = std::max(smem, sizeof(double2) * (size_t)nbox * 256 * TR) + 128;
+        const size_t tsm = std::max(sizeof(double2) * (size_t)2 * TR * xbuf_stride_rows_h(lqx),
+                                    sizeof(double2) * (size_t)nbox * 256 * TR) + 128;
         switch (lqx) {
             PDGPU_CASE(8, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
                                                       e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm)))
