@@ -710,6 +710,9 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
     // (distinct banks for the 16-byte loads) and each warp store still fills
     // whole 32-byte sectors along rr.  W(2a) = e^{-2 pi i 2a/Px} =
     // W(2a0) e^{-2 pi i u/R}: two table reads per thread, hoisted.
+    // post-processing thread map: a quarter-warp covers 8 consecutive kx of one
+    // row; with TSTORE (two rows) 4 consecutive kx of both rows, so that its
+    // [kx][row] block writes land on 8 distinct 16-byte bank groups (below)
     constexpr int LA = (2 * T >= 8) ? 3 : 0;  // tiny transforms: rr fastest
     const int rr = (threadIdx.x >> LA) & (TR - 1);
     const int a0 = ((threadIdx.x >> (LA + LOGTR)) << LA) + (threadIdx.x & ((1 << LA) - 1));
@@ -790,11 +793,20 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* m, const void* s
                  : "memory");
 }
 
+// K1 duo row buffers: max(two exchange buffers, staged row) doubles, rounded
+// up to 8 mod 16 doubles so consecutive rows sit 64 bytes apart in the banks
+// CFM (TSTORE tiles): 0 the plain stride; 1 rounded to 8 mod 16 doubles
+// (rows 64 B apart in the banks) for the conflict-free thread map below.
+__host__ __device__ constexpr int k1_duo_row_stride(int XB, int rowlen, int cfm = 0) {
+    return (2 * 2 * XB > rowlen ? 2 * 2 * XB : rowlen) +
+           (cfm ? ((24 - (2 * 2 * XB > rowlen ? 2 * 2 * XB : rowlen) % 16) % 16) : 0);
+}
+
 // TSTORE: the tile's [kx][row] spectrum block is assembled in SMEM (over the
 // row buffers, after every spectrum value has been read into registers) and
 // written by TMA boxes ({2*TR doubles, 256 kx}, tensor map tm over S) instead of
 // per-thread scattered stores.
-template <int LOGQ, bool CIRC, bool TSTORE = false>
+template <int LOGQ, bool CIRC, bool TSTORE = false, int CFM = 0>
 __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restrict__ u, double2* __restrict__ S,
                                                           int Nx, int Nrow, int nslab, int Hx,
                                                           const double2* __restrict__ tw, int logTWN,
@@ -806,7 +818,8 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
     static_assert(LOGQ >= 4 && LOGQ <= 10, "2048/Q rows of two Q-point transforms per 256-thread CTA");
     extern __shared__ double2 sm[];
     constexpr int rowlen = CIRC ? 4 * Q : 2 * Q;          // staged doubles per row (>= Nx)
-    constexpr int RS = (2 * 2 * XB > rowlen ? 2 * 2 * XB : rowlen);  // doubles per row buffer
+    constexpr int RS = k1_duo_row_stride(XB, rowlen, CFM);  // doubles per row buffer
+    constexpr bool CF = TSTORE && CFM == 1;  // conflict-free [kx][row] block writes
     double* rowbuf = reinterpret_cast<double*>(sm);        // TR x RS doubles
     double* xd = rowbuf + TR * RS;                          // 2*TR transforms x XB doubles
     const int gi = threadIdx.x >> Sh::LOGT;
@@ -846,7 +859,10 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
         }
         cp_async_commit();
     };
-    constexpr int LA = (2 * T >= 8) ? 3 : 0;
+    // post-processing thread map: a quarter-warp covers 8 consecutive kx of one
+    // row; with TSTORE (two rows) 4 consecutive kx of both rows, so that its
+    // [kx][row] block writes land on 8 distinct 16-byte bank groups (below)
+    constexpr int LA = CF ? 2 : (2 * T >= 8) ? 3 : 0;
     const int rr = (threadIdx.x >> LA) & (TR - 1);
     const int a0 = ((threadIdx.x >> (LA + LOGTR)) << LA) + (threadIdx.x & ((1 << LA) - 1));
     int64_t tile = blockIdx.x;
@@ -918,10 +934,15 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
                 const double2 Wem = make_double2(-We.x, We.y), Wom = make_double2(-Wo.x, Wo.y);
                 const double2 xe = post(e1[uu], cconj(e2[uu]), We), xem = post(e2[uu], cconj(e1[uu]), Wem);
                 const double2 xo = post(o1[uu], cconj(o2[uu]), Wo), xom = post(o2[uu], cconj(o1[uu]), Wom);
-                ob[(2 * a) * TR + rr] = xe;
-                ob[(2 * Q - 2 * a) * TR + rr] = xem;
-                ob[(2 * a + 1) * TR + rr] = xo;
-                ob[(2 * Q - 2 * a - 1) * TR + rr] = xom;
+                // kx pairs (2a, 2a+1) and (2Q-2a, 2Q-2a-1) are 64 contiguous bytes
+                // of the block; threads with a bit 1 set store them in the other
+                // order, so each store instruction of a quarter-warp (a..a+3, two
+                // rows) covers all eight 16-byte slots of a 128-byte bank line
+                const bool sw = CF && ((a >> 1) & 1);
+                ob[(2 * a + sw) * TR + rr] = sw ? xo : xe;
+                ob[(2 * a + 1 - sw) * TR + rr] = sw ? xe : xo;
+                ob[(2 * Q - 2 * a - sw) * TR + rr] = sw ? xom : xem;
+                ob[(2 * Q - 2 * a - 1 + sw) * TR + rr] = sw ? xem : xom;
             }
             if (a0 == 0) ob[Q * TR + rr] = post(Aq, cconj(Aq), make_double2(0.0, -1.0));
             fence_proxy_async();
@@ -962,12 +983,12 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
     if (TSTORE && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-static int k1_duo_smem(int logq, bool circ) {
+static int k1_duo_smem(int logq, bool circ, int cfm = 0) {
     const int Q = 1 << logq;
     const int TR = 2048 >> logq;
     const int XB = xbuf_slots(logq);
     const int rowlen = circ ? 4 * Q : 2 * Q;
-    const int RS = std::max(2 * 2 * XB, rowlen);
+    const int RS = k1_duo_row_stride(XB, rowlen, cfm);
     // + alignment slack for the TMA-store block (it may run past the row
     // buffers into the exchange buffer, free at that point)
     return (int)sizeof(double) * TR * (RS + 2 * XB) + 128;
@@ -1330,6 +1351,236 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
     }
 }
 
+// ---------------------------------------------- K3, TMEM-parked variant ---
+// Tensor memory as thread-private parking space.  A thread owns the 16
+// frequencies t + j*T of its column; the other component's spectrum (X0 while
+// FFT(x1) runs, then F0 while IFFT(F1) runs) waits in the thread's own TMEM
+// lane (32x32b shape: warp w reaches lanes 32*(w%4).., 64 columns of 32 bits
+// hold 16 complex values; warps w and w+4 take columns 0 / 64 of the CTA's
+// 128-column allocation).  That takes the 64 KB park out of shared memory,
+// so the FFT exchanges can use 16-byte slots (half the LDS/STS instructions
+// and barriers of the split 8-byte exchange) and two CTAs still fit per SM
+// (~74 KB each).  Operands come straight from global memory into registers,
+// L2-prefetched one item ahead.  Periodic columns (NH = 1) of 2048 / 4096
+// points; same data flow and numerics as k_spectral2d_duo<LOGQ, SYM, 1>.
+__device__ __forceinline__ uint32_t dlo(double d) { return (uint32_t)__double2loint(d); }
+__device__ __forceinline__ uint32_t dhi(double d) { return (uint32_t)__double2hiint(d); }
+
+// 4 complex values <-> 16 TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_st4(uint32_t ta, const double2* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15, %16};" ::"r"(ta),
+        "r"(dlo(v[0].x)), "r"(dhi(v[0].x)), "r"(dlo(v[0].y)), "r"(dhi(v[0].y)), "r"(dlo(v[1].x)), "r"(dhi(v[1].x)),
+        "r"(dlo(v[1].y)), "r"(dhi(v[1].y)), "r"(dlo(v[2].x)), "r"(dhi(v[2].x)), "r"(dlo(v[2].y)), "r"(dhi(v[2].y)),
+        "r"(dlo(v[3].x)), "r"(dhi(v[3].x)), "r"(dlo(v[3].y)), "r"(dhi(v[3].y))
+        : "memory");
+}
+
+struct TmemQuad {
+    uint32_t r[16];
+};
+
+__device__ __forceinline__ void tmem_ld4(uint32_t ta, TmemQuad& q) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(q.r[0]), "=r"(q.r[1]), "=r"(q.r[2]), "=r"(q.r[3]), "=r"(q.r[4]), "=r"(q.r[5]), "=r"(q.r[6]),
+          "=r"(q.r[7]), "=r"(q.r[8]), "=r"(q.r[9]), "=r"(q.r[10]), "=r"(q.r[11]), "=r"(q.r[12]), "=r"(q.r[13]),
+          "=r"(q.r[14]), "=r"(q.r[15])
+        : "r"(ta)
+        : "memory");
+}
+
+// wait for every tcgen05.ld of this thread; the registers of q pass through
+// the wait so no use of them is scheduled before it
+__device__ __forceinline__ void tmem_wait_ld(TmemQuad& q) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(q.r[0]), "+r"(q.r[1]), "+r"(q.r[2]), "+r"(q.r[3]), "+r"(q.r[4]), "+r"(q.r[5]), "+r"(q.r[6]),
+                   "+r"(q.r[7]), "+r"(q.r[8]), "+r"(q.r[9]), "+r"(q.r[10]), "+r"(q.r[11]), "+r"(q.r[12]),
+                   "+r"(q.r[13]), "+r"(q.r[14]), "+r"(q.r[15])
+                 :
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_unpack4(const TmemQuad& q, double2* v) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        v[i] = make_double2(__hiloint2double((int)q.r[4 * i + 1], (int)q.r[4 * i]),
+                            __hiloint2double((int)q.r[4 * i + 3], (int)q.r[4 * i + 2]));
+}
+
+// 2 complex values <-> 8 TMEM columns
+__device__ __forceinline__ void tmem_st2(uint32_t ta, double2 a, double2 b) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(ta),
+                 "r"(dlo(a.x)), "r"(dhi(a.x)), "r"(dlo(a.y)), "r"(dhi(a.y)), "r"(dlo(b.x)), "r"(dhi(b.x)),
+                 "r"(dlo(b.y)), "r"(dhi(b.y))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld2_wait(uint32_t ta, double2& a, double2& b) {
+    uint32_t r[8];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(ta)
+                 : "memory");
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7])
+                 :
+                 : "memory");
+    a = make_double2(__hiloint2double((int)r[1], (int)r[0]), __hiloint2double((int)r[3], (int)r[2]));
+    b = make_double2(__hiloint2double((int)r[5], (int)r[4]), __hiloint2double((int)r[7], (int)r[6]));
+}
+
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// LAND = false: 16-byte exchange slots (XB * 16 bytes per column), operands
+// loaded straight into registers.  LAND = true: x_0 lands by one TMA bulk copy
+// in a Q * 16-byte buffer that is free again as soon as the thread has read
+// it (the park is in TMEM), so the next item's x_0 is requested a whole item
+// ahead; the exchange then uses 8-byte slots (split real/imaginary) to keep
+// two CTAs per SM.
+template <int LOGQ, int SYM, bool LAND>
+__global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_tm(const double2* __restrict__ in, double2* out,
+                                                                  const void* __restrict__ sym, int ncols, int NC,
+                                                                  int batch, const double2* __restrict__ tw,
+                                                                  int logTWN) {
+    using Sh = FftShape<LOGQ, kPipeLogR>;
+    constexpr int Q = Sh::Q, T = Sh::T, XB = Sh::XBUF, RR = Sh::R;
+    static_assert(RR == 16 && T % 128 == 0, "16 points per thread, whole TMEM lane quadrants per column");
+    extern __shared__ double2 sm[];
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bars[kPipeThreads / 128];
+    __shared__ double2 stw[FftTwTable<LOGQ, kPipeLogR>::SIZE];
+    const int gi = threadIdx.x >> Sh::LOGT;
+    const int t = threadIdx.x & (T - 1);
+    const int NCc = kPipeThreads / T;
+    double2* land = sm + gi * Q;                                                       // LAND only
+    double2* xb = LAND ? reinterpret_cast<double2*>(reinterpret_cast<double*>(sm + NCc * Q) + gi * XB)
+                       : sm + gi * XB;
+    const int warp = threadIdx.x >> 5;
+    fill_fft_tw_table<LOGQ, kPipeLogR>(stw, tw, logTWN);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tbase)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (LAND && t == 0) mbar_init(&bars[gi], 1);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t ta = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+    const int ngroups = (ncols + NC - 1) / NC;
+    const int64_t nitems = (int64_t)ngroups * batch;
+    const int64_t cstride = (int64_t)ncols * Q;
+    const uint64_t pol = l2_policy_evict_first();
+    constexpr unsigned xbytes = (unsigned)Q * 16u;
+    constexpr unsigned sbytes = (unsigned)Q * (SYM == 1 ? 4 * 8 : 3 * 16);
+    auto item_col = [&](int64_t item, int& b, int& col) {
+        b = (int)(item % batch);
+        col = (int)(item / batch) * NC + gi;
+        return col < ncols;
+    };
+    auto x0_of = [&](int b, int col) { return in + ((int64_t)(b * 2) * ncols + col) * Q; };
+    // LAND: x_0 of an item into this column's landing buffer (one thread)
+    auto land_x0 = [&](int64_t item) {
+        int b, col;
+        if (t == 0 && item < nitems && item_col(item, b, col)) {
+            fence_proxy_async();
+            mbar_expect_tx(&bars[gi], xbytes);
+            bulk_load(land, x0_of(b, col), xbytes, &bars[gi]);
+        }
+    };
+    if (LAND) land_x0(blockIdx.x);
+    unsigned ph = 0;
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        int b, col;
+        const bool valid = item_col(it, b, col);
+        const int cc = valid ? col : 0;
+        const double2* x0 = x0_of(b, cc);
+        double2* z0 = out + ((int64_t)(b * 2) * ncols + cc) * Q;
+        if (valid && t == 0) {
+            // x_1 and the symbol rows into L2 behind FFT(x_0)
+            l2_prefetch(x0 + cstride, xbytes);
+            l2_prefetch((const char*)sym + (int64_t)cc * sbytes, sbytes);
+        }
+        double2 v[RR];
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+            if (LAND && c == 0) {
+                if (valid) {
+                    mbar_wait(&bars[gi], ph);
+                    ph ^= 1;
+                }
+#pragma unroll
+                for (int j = 0; j < RR; ++j) v[j] = valid ? land[t + j * T] : make_double2(0.0, 0.0);
+                __syncthreads();  // landing buffer read by every thread: take the next item's x_0
+                land_x0(it + gridDim.x);
+            } else {
+                const double2* src = x0 + c * cstride;
+#pragma unroll
+                for (int j = 0; j < RR; ++j) v[j] = valid ? ld_hint(src + t + j * T, pol) : make_double2(0.0, 0.0);
+            }
+            reg_fft<LOGQ, kPipeLogR, -1, BlockBar, LAND>(v, t, xb, make_fft_tw_s<LOGQ, kPipeLogR>(opaque(t), stw),
+                                                         BlockBar{});
+            if (c == 0) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tmem_st4(ta + 16 * q, v + 4 * q);
+                tmem_wait_st();
+            }
+        }
+        // 2 x 2 product, two frequencies per TMEM round trip; F0 replaces X0
+        const int64_t sbase = (int64_t)cc * Q;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            double2 x0v[2], f0[2];
+            tmem_ld2_wait(ta + 8 * q, x0v[0], x0v[1]);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int j = 2 * q + i;
+                double2 U[2], F[2];
+                U[0] = x0v[i];
+                U[1] = v[j];
+                symbol_product<2, SYM == 1>(F, U, sym, sbase + t + j * T);
+                f0[i] = F[0];
+                v[j] = F[1];
+            }
+            tmem_st2(ta + 8 * q, f0[0], f0[1]);
+        }
+        if (!LAND && t == 0) {
+            // the next item's x_0 into L2 behind the two inverse transforms (a
+            // whole item ahead, 19 MB in flight over the GPU, it was partly
+            // evicted again before use: DRAM reads +9 %)
+            int b2, col2;
+            if (it + gridDim.x < nitems && item_col(it + gridDim.x, b2, col2)) l2_prefetch(x0_of(b2, col2), xbytes);
+        }
+#pragma unroll 1
+        for (int ai = 0; ai < 2; ++ai) {
+            const int a = 1 - ai;
+            if (ai == 1) {
+                tmem_wait_st();
+                TmemQuad tq[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tmem_ld4(ta + 16 * q, tq[q]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    tmem_wait_ld(tq[q]);
+                    tmem_unpack4(tq[q], v + 4 * q);
+                }
+            }
+            reg_fft<LOGQ, kPipeLogR, 1, BlockBar, LAND>(v, t, xb, make_fft_tw_s<LOGQ, kPipeLogR>(opaque(t), stw),
+                                                        BlockBar{});
+            double2* dst = z0 + a * cstride;
+            if (valid) {
+#pragma unroll
+                for (int j = 0; j < RR; ++j) st_hint(dst + t + j * T, v[j], pol);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tbase));
+}
+
 // ------------------------------------------------------- K2 / K4 (3D) ---
 // CIRC (periodic y, Py = Ny = 2Q): even/odd outputs by a decimation-in-
 // frequency stage (as in k_rfft_rows); K4 keeps all 2Q outputs.
@@ -1545,7 +1796,10 @@ static void set_attrs_k1_l() {
     smem_attr((const void*)k_rfft_rows_pipe<L, 2, C>);
     smem_attr((const void*)k_rfft_rows_pipe<L, 3, C>);
     if constexpr (L >= 6 && L <= 10) smem_attr((const void*)k_rfft_rows_duo<L, C>);
-    if constexpr (C && L == 10) smem_attr((const void*)k_rfft_rows_duo<L, C, true>);
+    if constexpr (C && L == 10) {
+        smem_attr((const void*)k_rfft_rows_duo<L, C, true, 0>);
+        smem_attr((const void*)k_rfft_rows_duo<L, C, true, 1>);
+    }
 }
 template <int... Ls>
 static void set_attrs_k1_all(std::integer_sequence<int, Ls...>) {
@@ -1564,7 +1818,13 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
     const int T = threads_per_transform(lqx, 4);
     // two-CTA/SM variant: two rows of two transforms fill a 256-thread CTA
     if ((Nx & 1) == 0 && lqx >= 7 && lqx <= 10 && !getenv("PDGPU_NO_K1_DUO")) {  // lqx 6 (256-wide rows): the pipelined kernel measured faster
-        const size_t dsm = (size_t)k1_duo_smem(lqx, cx);
+        // PDGPU_K1_CF=1: conflict-free [kx][row] block writes (4 kx x 2 rows per
+        // quarter-warp).  SMEM bank conflicts 129M -> 18M per launch, and 6 %
+        // faster at batch 2, but 22 % slower at batch 16 (long-scoreboard
+        // stalls 23 -> 38 %, same DRAM bytes): off by default
+        const char* cfenv = getenv("PDGPU_K1_CF");
+        const int cfm = (cx && lqx == 10 && cfenv && cfenv[0] == '1') ? 1 : 0;
+        const size_t dsm = (size_t)k1_duo_smem(lqx, cx, cfm);
         const int DTR = 2048 >> lqx;
         if (2 * (dsm + 1024) <= 228 * 1024) {
             const int64_t ntiles = (int64_t)((Ny + DTR - 1) / DTR) * nslab;
@@ -1577,8 +1837,9 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
             const char* tenv = getenv("PDGPU_K1_TMA");
             const bool tst = cx && DTR <= 2 && !(tenv && tenv[0] == '0') && encode_box_map(tm, e.d_S1, Ny, pl.Hx, nslab, DTR) &&
                              (size_t)(((pl.Hx + 255) / 256) * 256 * DTR * 16 + 128) <= dsm;
-#define PDGPU_K1D(C) (tst ? k_rfft_rows_duo<LQ, true, true><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, \
-                                                                      e.d_tw, pl.logTWN, tm)                    \
+#define PDGPU_K1T(CF) k_rfft_rows_duo<LQ, true, true, CF><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, \
+                                                                                e.d_tw, pl.logTWN, tm)
+#define PDGPU_K1D(C) (tst ? (cfm == 1 ? PDGPU_K1T(1) : PDGPU_K1T(0))                                     \
                       : k_rfft_rows_duo<LQ, C><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, e.d_tw, \
                                                                       pl.logTWN, tm))
             switch (lqx) {
@@ -1590,6 +1851,7 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
                 default: goto no_duo;
             }
 #undef PDGPU_K1D
+#undef PDGPU_K1T
             return;
         }
     }
@@ -1714,6 +1976,12 @@ static void set_attrs_k3_l() {
         smem_attr((const void*)k_spectral2d_duo<L, 1, 2>);
         smem_attr((const void*)k_spectral2d_duo<L, 2, 2>);
     }
+    if constexpr (L == 11 || L == 12) {
+        smem_attr((const void*)k_spectral2d_tm<L, 0, false>);
+        smem_attr((const void*)k_spectral2d_tm<L, 1, false>);
+        smem_attr((const void*)k_spectral2d_tm<L, 0, true>);
+        smem_attr((const void*)k_spectral2d_tm<L, 1, true>);
+    }
     smem_attr((const void*)k_spectral2d_pipe<L, 0>);
     smem_attr((const void*)k_spectral2d_pipe<L, 1>);
     smem_attr((const void*)k_spectral2d_pipe<L, 2>);
@@ -1745,6 +2013,32 @@ void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s) {
     // two-CTA/SM split-exchange kernel (default) unless PDGPU_K3=pipe
     // (the pipe variant handles padded columns only)
     const char* k3env = getenv("PDGPU_K3");
+    // periodic 2048/4096-point columns: TMEM-parked kernel, operands by
+    // register loads, 16-byte exchange (PDGPU_K3=tmland: x_0 TMA-landed with
+    // the split exchange; PDGPU_K3=split: the SMEM-parked k_spectral2d_duo)
+    const bool k3split = k3env && std::string(k3env) == "split";
+    if (nh == 1 && (lq == 11 || lq == 12) && mode != 2 && !k3split) {
+        const bool land = k3env && std::string(k3env) == "tmland";
+        const int NCt = kPipeThreads / Tp;
+        const size_t tsmem = land ? (size_t)NCt * (sizeof(double2) * ((size_t)1 << lq) + sizeof(double) * xbuf_slots(lq))
+                                  : (size_t)NCt * sizeof(double2) * xbuf_slots(lq);
+        const int64_t nitems = (int64_t)((pl.ncols + NCt - 1) / NCt) * batch;
+        const unsigned tgrid = (unsigned)std::min<int64_t>(nitems, (int64_t)e.num_sms * 2);
+#define TM_ARGS spec, e.d_S2, e.d_sym, pl.ncols, NCt, batch, e.d_tw, pl.logTWN
+#define TM_L(LQV, LANDV)                                                                          \
+    (mode == 1 ? k_spectral2d_tm<LQV, 1, LANDV><<<tgrid, kPipeThreads, tsmem, s>>>(TM_ARGS)       \
+               : k_spectral2d_tm<LQV, 0, LANDV><<<tgrid, kPipeThreads, tsmem, s>>>(TM_ARGS))
+        if (lq == 12) {
+            if (land) TM_L(12, true);
+            else TM_L(12, false);
+        } else {
+            if (land) TM_L(11, true);
+            else TM_L(11, false);
+        }
+#undef TM_L
+#undef TM_ARGS
+        return;
+    }
     if ((nh == 1 || !(k3env && std::string(k3env) == "pipe")) && lq >= 4) {
         const int NCd = kPipeThreads / Tp;
         const size_t dsmem = (size_t)NCd * (sizeof(double2) * (1 << lq) + sizeof(double) * xbuf_slots(lq) +
