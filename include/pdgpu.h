@@ -35,6 +35,7 @@ extern "C" {
 #define PDGPU_ERR_CUDA 5
 #define PDGPU_ERR_OUT_OF_MEMORY 6
 #define PDGPU_ERR_NOT_SUPPORTED 7
+#define PDGPU_ERR_IO 8                /* pdfast::IoError, errors.hpp:33-35 */
 
 typedef struct pdgpu_engine* pdgpu_t;
 
@@ -289,6 +290,30 @@ int pdgpu_write_snapshot(int dim, const int* dims, double spacing, const double*
                          const double* damage, int64_t step, double t, const char* dir, char* path_out, int path_cap);
 int pdgpu_read_snapshot(const char* path, int dim, int* dims, double* spacing, double* origin, int64_t* step,
                         double* t, double* u, double* damage);
+
+/* ------------------------------------------------------------- monitors --
+ * MonitorWriter (output.hpp:45-72) and nearest_node (output.hpp:33-41): the
+ * reference's tab-separated monitor file ("# step\tt\tnode\tu_x\tu_y[\tu_z]",
+ * then one row per point and append: step, %.17g t, node id from 1, %.17g
+ * components), flushed after every append.  pdgpu_monitor_open with path ""
+ * or NULL only resolves nodes; an unwritable path fails with PDGPU_ERR_IO
+ * (the reference throws IoError).  pdgpu_monitor_append takes one row of
+ * values [point][component].
+ * pdgpu_sim_monitor registers nodes with an engine: after every step of
+ * pdgpu_sim_step u at those nodes is gathered on the device (one tiny kernel,
+ * no field download); pdgpu_sim_monitor_read drains the recorded rows
+ * (steps[count], t[count], values[count][n][dim]); pass NULL buffers to learn
+ * count.  This is the CLI's per-step monitor.append (tools/pdfast_cli.cpp:76)
+ * without a per-step host round trip. */
+typedef struct pdgpu_monitor* pdgpu_monitor_t;
+int pdgpu_monitor_open(const char* path, int dim, const int* dims, double spacing, const double* origin,
+                       const double* points, int npts, pdgpu_monitor_t* out);
+int pdgpu_monitor_nodes(int dim, const int* dims, double spacing, const double* origin, const double* points, int npts,
+                        int64_t* nodes);
+int pdgpu_monitor_append(pdgpu_monitor_t m, int64_t step, double t, const double* values);
+void pdgpu_monitor_close(pdgpu_monitor_t m);
+int pdgpu_sim_monitor(pdgpu_t h, const int64_t* nodes, int n);
+int pdgpu_sim_monitor_read(pdgpu_t h, int64_t* steps, double* t, double* values, int64_t cap, int64_t* count);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,7 @@
 // BondLedger, ...) and its host-side assembly (build_kernel,
 // classify_regions); everything per step runs through libpdgpu.so.
 #pragma once
+#include "pdfast/output.hpp"
 #include "pdfast/timestepping.hpp"
 #ifndef PDGPU_WITH_PDFAST
 #define PDGPU_WITH_PDFAST
@@ -214,6 +215,66 @@ class Simulation {
     mutable pdfast::SimState<Dim> state_;
     mutable pdfast::BondLedger ledger_;
     mutable std::vector<std::pair<pdfast::index_t, pdfast::index_t>> newly_broken_;
+};
+
+// MonitorWriter<Dim> (output.hpp:45-72) on libpdgpu's writer: the same
+// constructor, nodes() and append(step, t, u) (host field), byte-identical
+// rows; append_recorded(sim) writes the rows a Simulation recorded on the
+// device since the last call (Simulation::monitor), i.e. the CLI's per-step
+// monitor.append (tools/pdfast_cli.cpp:76) without a field download per step.
+template <int Dim>
+class MonitorWriter {
+  public:
+    MonitorWriter() = default;
+    MonitorWriter(const std::string& path, const pdfast::Grid<Dim>& grid, const std::vector<pdfast::Vec<Dim>>& points) {
+        std::vector<double> pts;
+        for (const auto& x : points) pts.insert(pts.end(), x.begin(), x.end());
+        int dims[Dim];
+        for (int d = 0; d < Dim; ++d) dims[d] = grid.dims[d];
+        nodes64_.resize(points.size());
+        check(pdgpu_monitor_nodes(Dim, dims, grid.h, grid.origin.data(), pts.data(), (int)points.size(),
+                                  nodes64_.data()));
+        nodes_.assign(nodes64_.begin(), nodes64_.end());
+        const int rc = pdgpu_monitor_open(path.c_str(), Dim, dims, grid.h, grid.origin.data(), pts.data(),
+                                          (int)points.size(), &m_);
+        if (rc == PDGPU_ERR_IO) throw pdfast::IoError(pdgpu_last_error());
+        check(rc);
+    }
+    MonitorWriter(const MonitorWriter&) = delete;
+    MonitorWriter& operator=(const MonitorWriter&) = delete;
+    ~MonitorWriter() { pdgpu_monitor_close(m_); }
+
+    const std::vector<pdfast::index_t>& nodes() const { return nodes_; }
+
+    void append(pdfast::index_t step, double t, const pdfast::VecField<Dim>& u) {
+        std::vector<double> row;
+        for (pdfast::index_t p : nodes_)
+            for (int d = 0; d < Dim; ++d) row.push_back(u.c[d][p]);
+        if (!m_) return;
+        check(pdgpu_monitor_append(m_, step, t, row.data()));
+    }
+
+    // rows recorded on the device by sim (after sim.engine() monitors nodes())
+    int64_t append_recorded(Simulation<Dim>& sim) {
+        const pdgpu_t h = sim.engine().handle();
+        int64_t cnt = 0;
+        check(pdgpu_sim_monitor_read(h, nullptr, nullptr, nullptr, 0, &cnt));
+        std::vector<int64_t> steps((size_t)cnt + 1);
+        std::vector<double> t((size_t)cnt + 1), vals((size_t)(cnt * nodes_.size() * Dim) + 1);
+        check(pdgpu_sim_monitor_read(h, steps.data(), t.data(), vals.data(), cnt, &cnt));
+        for (int64_t r = 0; r < cnt && m_; ++r)
+            check(pdgpu_monitor_append(m_, steps[(size_t)r], t[(size_t)r], vals.data() + (size_t)r * nodes_.size() * Dim));
+        return cnt;
+    }
+    // register this writer's nodes with the simulation's per-step device record
+    void watch(Simulation<Dim>& sim) const {
+        check(pdgpu_sim_monitor(sim.engine().handle(), nodes64_.data(), (int)nodes64_.size()));
+    }
+
+  private:
+    pdgpu_monitor_t m_ = nullptr;
+    std::vector<int64_t> nodes64_;
+    std::vector<pdfast::index_t> nodes_;
 };
 
 }  // namespace pdgpu

@@ -16,6 +16,8 @@
 
 #include <cmath>
 #include <cstdio>
+#include <fstream>
+#include <sstream>
 #include <random>
 #include <string>
 
@@ -306,6 +308,73 @@ void check_errors() {
 
 }  // namespace
 
+// MonitorWriter (output.hpp:45-72): the reference writer fed every step from
+// the reference Simulation vs pdgpu::MonitorWriter fed from the rows the GPU
+// Simulation recorded on the device; same nodes, steps and times, values to the
+// trajectory tolerance; IoError on an unwritable path from both
+void check_monitor() {
+    auto cfg = preset("precracked_plate", 0.05 / 100.0);
+    auto prob = make_problem<2>(cfg);
+    const SolverOptions opts{Method::Fast, Integrator::Vv, cfg.dt, std::nullopt};
+    Simulation<2> ref(prob, opts);
+    pdgpu::Simulation<2> gpu(prob, opts);
+    const std::vector<Vec<2>> pts = {{0.0255, 0.0125}, {0.01, 0.04}, {-1.0, 9.0}};
+    const std::string pr = "/tmp/pdgpu_mon_ref.tsv", pg = "/tmp/pdgpu_mon_gpu.tsv";
+    bool ok = true;
+    {
+        MonitorWriter<2> mref(pr, prob.grid, pts);
+        pdgpu::MonitorWriter<2> mgpu(pg, prob.grid, pts);
+        ok = ok && mref.nodes() == mgpu.nodes();
+        mgpu.watch(gpu);
+        for (int n = 0; n < 60; ++n) {
+            ref.step();
+            mref.append(ref.state().step, ref.state().t, ref.state().u);
+        }
+        gpu.run(60);
+        ok = ok && mgpu.append_recorded(gpu) == 60;
+    }
+    auto rows = [](const std::string& path) {
+        std::ifstream in(path);
+        std::string line;
+        std::vector<std::vector<double>> out;
+        std::getline(in, line);
+        while (std::getline(in, line)) {
+            std::istringstream ss(line);
+            std::vector<double> v;
+            double x;
+            while (ss >> x) v.push_back(x);
+            out.push_back(v);
+        }
+        return out;
+    };
+    const auto a = rows(pr), b = rows(pg);
+    double worst = 0.0, scale = 0.0;
+    ok = ok && a.size() == b.size() && a.size() == 60 * pts.size();
+    for (size_t r = 0; ok && r < a.size(); ++r) {
+        ok = ok && a[r][0] == b[r][0] && a[r][1] == b[r][1] && a[r][2] == b[r][2];
+        for (int d = 3; d < 5; ++d) {
+            worst = std::max(worst, std::abs(a[r][d] - b[r][d]));
+            scale = std::max(scale, std::abs(a[r][d]));
+        }
+    }
+    const double rel = scale > 0 ? worst / scale : worst;
+    bool ioerr_ref = false, ioerr_gpu = false;
+    try {
+        MonitorWriter<2>("/nonexistent_dir/m.tsv", prob.grid, pts);
+    } catch (const IoError&) {
+        ioerr_ref = true;
+    }
+    try {
+        pdgpu::MonitorWriter<2>("/nonexistent_dir/m.tsv", prob.grid, pts);
+    } catch (const IoError&) {
+        ioerr_gpu = true;
+    }
+    char buf[200];
+    std::snprintf(buf, sizeof buf, "\"rows\": %zu, \"max_rel_u\": %.3e, \"tol\": 1e-8, \"io_error\": %s", b.size(), rel,
+                  ioerr_ref && ioerr_gpu ? "true" : "false");
+    report("monitor", ok && rel <= 1e-8 && ioerr_ref && ioerr_gpu, buf);
+}
+
 int main() {
     check_matvec<2>({128, 96}, "matvec_2d");
     check_matvec<3>({24, 20, 16}, "matvec_3d");
@@ -314,5 +383,6 @@ int main() {
     check_simulation_adr();
     check_static_solve();
     check_errors();
+    check_monitor();
     return g_fail;
 }

@@ -279,6 +279,51 @@ def gen_snapshots():
             subprocess.run(args, check=True, capture_output=True)
 
 
+def monitor_case(dim):
+    """Inputs of the monitor goldens: a small lattice, monitor points inside,
+    on node coordinates, between nodes and outside the domain (clamped), and
+    rows whose fields hold edge values (+-0, subnormal, huge) at those nodes."""
+    dims = (10, 10) if dim == 2 else (4, 3, 2)
+    h = 0.01 if dim == 2 else 0.1
+    origin = np.array([0.0, 0.0, 0.0][:dim]) if dim == 2 else np.array([0.125, -2.0 / 3.0, 1e-17])
+    if dim == 2:
+        pts = np.array([[0.055, 0.025], [0.0, 0.0], [0.1, 0.1], [-1.0, 0.05], [0.0999999, 2.0], [0.03, 0.07]])
+    else:
+        pts = origin + np.array([[0.05, 0.05, 0.05], [0.3, 0.2, 0.1], [-5.0, 9.0, 0.15], [0.1, 0.1, 0.0999999999]])
+    n = int(np.prod(dims))
+    rng = Rng(7000 + dim, ref=True)
+    steps = [0, 12, 9999999]
+    ts = [0.0, 12 * 2e-8, 1.0 / 3.0]
+    rows = []
+    for r in range(3):
+        u = rng.uniform(dim * n).reshape(dim, n) * 10.0 ** np.linspace(-200, 200, dim * n).reshape(dim, n)
+        u[:, :4] = [[0.0, -0.0, 5e-324, 1.7976931348623157e308]] * dim
+        u[0, n - 1] = 3.5e-5
+        rows.append((steps[r], ts[r], u))
+    return dims, h, origin, pts, rows
+
+
+def gen_monitors():
+    """Monitor files written by the reference's MonitorWriter (output.hpp:45-72)
+    through oracle/_ref/snap_writer, plus the inputs and the nodes it chose."""
+    import subprocess
+    import tempfile
+    exe = os.path.join(HERE, "_ref", "snap_writer")
+    out = {}
+    for dim in (2, 3):
+        dims, h, origin, pts, rows = monitor_case(dim)
+        path = os.path.join(OUT, f"monitor{dim}d.tsv")
+        with tempfile.TemporaryDirectory() as tmp:
+            fp, fr = os.path.join(tmp, "p.raw"), os.path.join(tmp, "r.raw")
+            np.ascontiguousarray(pts, dtype=np.float64).tofile(fp)
+            np.concatenate([np.concatenate([[s, t], u.ravel()]) for s, t, u in rows]).tofile(fr)
+            args = [exe, "mon", str(dim), *map(str, dims), repr(h), *map(repr, origin.tolist()), path, fp,
+                    str(len(pts)), fr, str(len(rows))]
+            res = subprocess.run(args, check=True, capture_output=True, text=True)
+        out[f"nodes{dim}d"] = np.array([int(x) for x in res.stdout.split()], dtype=np.int64)
+    np.savez_compressed(os.path.join(OUT, "monitor_nodes.npz"), **out)
+
+
 def adr_problem(dims, ref=True):
     """Quasi-static plate/cube for the reference's ADR solver (timestepping.hpp:79-162):
     bottom layer clamped, a downward load on the top layer."""
@@ -322,7 +367,7 @@ def gen_adr():
 def main():
     os.makedirs(OUT, exist_ok=True)
     fns = {"conv": gen_conv, "corrections": gen_corrections, "acceptance": gen_acceptance, "configs": gen_configs,
-           "seeds": gen_seeds, "vv": gen_vv, "snapshots": gen_snapshots, "adr": gen_adr}
+           "seeds": gen_seeds, "vv": gen_vv, "snapshots": gen_snapshots, "monitors": gen_monitors, "adr": gen_adr}
     pick = sys.argv[1:] or list(fns)
     for name in pick:
         fns[name]()

@@ -21,6 +21,12 @@ std::string write(const std::string& dir, int dim, const int* dims, double h, co
                   const double* u, const double* damage, int64_t step, double t);
 bool read(const std::string& path, int dim, int* dims, double* h, double* origin, int64_t* step, double* t,
           double* u, double* damage, std::string& err);
+struct Monitor;
+int64_t nearest_node(int dim, const int* dims, double h, const double* origin, const double* x);
+Monitor* monitor_open(const char* path, int dim, const int* dims, double h, const double* origin, const double* pts,
+                      int npts, std::string& err);
+void monitor_append(Monitor* m, int64_t step, double t, const double* vals);
+void monitor_close(Monitor* m);
 }  // namespace snapshot
 }  // namespace pdgpu
 
@@ -547,7 +553,8 @@ void pdgpu_destroy(pdgpu_t h) {
                     h->d_cmask, h->d_surf_rows, h->d_surf_de, h->d_ledger, h->d_bond_rows, h->d_listed,
                     h->d_counters, h->d_new_pairs, h->d_body, h->d_cdofs, h->d_cval, h->d_ckind, h->d_u, h->d_v,
                     h->d_f, h->d_fprev, h->d_red, h->d_scal, h->d_ticket, h->d_cg, h->d_coltab,
-                    h->d_scratch, h->d_kc, h->d_uc_ids, h->d_uc_val, h->d_face_recv, h->d_halo};
+                    h->d_scratch, h->d_kc, h->d_uc_ids, h->d_uc_val, h->d_face_recv, h->d_halo,
+                    h->d_mon_nodes, h->d_mon_rows};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->cg_graph) cudaGraphExecDestroy(h->cg_graph);
@@ -1439,6 +1446,30 @@ static void sim_post(Engine& e, double s0, const double* watch) {
     ++e.step;
 }
 
+// one MonitorWriter row per step: u at the monitored nodes, gathered on the
+// device (no field download); a full device buffer moves to the host spill
+static void monitor_spill(Engine& e) {
+    if (!e.mon_dev_rows) return;
+    const size_t cnt = (size_t)e.mon_dev_rows * e.n_mon * e.dim;
+    const size_t off = e.mon_spill.size();
+    e.mon_spill.resize(off + cnt);
+    cuda_check(cudaMemcpyAsync(e.mon_spill.data() + off, e.d_mon_rows, sizeof(double) * cnt, cudaMemcpyDeviceToHost,
+                               e.stream), "monitor rows");
+    cuda_check(cudaStreamSynchronize(e.stream), "monitor rows");
+    e.mon_dev_rows = 0;
+}
+
+static void monitor_record(Engine& e) {
+    if (!e.n_mon) return;
+    if (e.mon_dev_rows == e.mon_cap) monitor_spill(e);
+    launch_monitor_gather(e.d_u, e.d_mon_nodes, e.n_mon, e.dim, e.plan.nodes,
+                          e.d_mon_rows + (size_t)e.mon_dev_rows * e.n_mon * e.dim, e.stream);
+    e.launches += 1;
+    ++e.mon_dev_rows;
+    e.mon_step.push_back(e.step);
+    e.mon_t.push_back(e.t);
+}
+
 static void sim_begin(Engine& e, int n_steps, double s0) {
     if (!e.d_u) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "simulation not initialised");
     e.sim_swept = s0 >= 0 && n_steps > 0;
@@ -1476,6 +1507,7 @@ int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64
             sim_force(e);
             sim_post(e, s0, watch);
             if (s0 >= 0) ledger_exchange(e, e.stream);  // NCCL slabs: mirror bonds broken across the face below
+            monitor_record(e);
         }
         const int64_t nb = sim_end(e, s0);
         if (broken) *broken = nb;
@@ -1714,6 +1746,79 @@ int pdgpu_near_surface(int dim, const int* dims, int M, uint8_t* out) {
 }  // extern "C"
 
 /* ------------------------------------------------------------ snapshots -- */
+int pdgpu_sim_monitor(pdgpu_t h, const int64_t* nodes, int n) {
+    return guarded([&] {
+        if (!h || n < 0 || (n > 0 && !nodes)) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad monitor nodes");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        Engine& e = *h;
+        for (int k = 0; k < n; ++k)
+            if (nodes[k] < 0 || nodes[k] >= e.plan.nodes) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "monitor node out of range");
+        cuda_check(cudaStreamSynchronize(e.stream), "sync");
+        e.n_mon = n;
+        e.mon_dev_rows = 0;
+        e.mon_step.clear();
+        e.mon_t.clear();
+        e.mon_spill.clear();
+        if (!n) return;
+        dalloc(e.d_mon_nodes, (size_t)n, "alloc monitor nodes");
+        cuda_check(cudaMemcpy(e.d_mon_nodes, nodes, sizeof(long long) * n, cudaMemcpyHostToDevice), "copy monitor nodes");
+        e.mon_cap = (int)std::max<int64_t>(64, std::min<int64_t>(4096, (1 << 22) / ((int64_t)n * e.dim)));
+        dalloc(e.d_mon_rows, (size_t)e.mon_cap * n * e.dim, "alloc monitor rows");
+    });
+}
+
+int pdgpu_sim_monitor_read(pdgpu_t h, int64_t* steps, double* t, double* values, int64_t cap, int64_t* count) {
+    return guarded([&] {
+        if (!h || !count) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        Engine& e = *h;
+        const int64_t rows = (int64_t)e.mon_step.size();
+        *count = rows;
+        if (!steps || !t || !values) return;
+        if (cap < rows) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "monitor buffer too small");
+        monitor_spill(e);
+        const size_t per = (size_t)e.n_mon * e.dim;
+        std::copy(e.mon_step.begin(), e.mon_step.end(), steps);
+        std::copy(e.mon_t.begin(), e.mon_t.end(), t);
+        std::copy(e.mon_spill.begin(), e.mon_spill.begin() + (size_t)rows * per, values);
+        e.mon_step.clear();
+        e.mon_t.clear();
+        e.mon_spill.clear();
+    });
+}
+
+int pdgpu_monitor_open(const char* path, int dim, const int* dims, double spacing, const double* origin,
+                       const double* points, int npts, pdgpu_monitor_t* out) {
+    return guarded([&] {
+        if (!out || !dims || !origin || (npts > 0 && !points) || npts < 0 || dim < 2 || dim > 3 || !(spacing > 0))
+            throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad monitor arguments");
+        std::string err;
+        snapshot::Monitor* m = snapshot::monitor_open(path, dim, dims, spacing, origin, points, npts, err);
+        if (!m) throw PdError(PDGPU_ERR_IO, err);
+        *out = reinterpret_cast<pdgpu_monitor_t>(m);
+    });
+}
+
+int pdgpu_monitor_nodes(int dim, const int* dims, double spacing, const double* origin, const double* points, int npts,
+                        int64_t* nodes) {
+    return guarded([&] {
+        if (!dims || !origin || !nodes || (npts > 0 && !points) || dim < 2 || dim > 3)
+            throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad arguments");
+        for (int k = 0; k < npts; ++k) nodes[k] = snapshot::nearest_node(dim, dims, spacing, origin, points + (size_t)k * dim);
+    });
+}
+
+int pdgpu_monitor_append(pdgpu_monitor_t m, int64_t step, double t, const double* values) {
+    return guarded([&] {
+        if (!m || !values) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        snapshot::monitor_append(reinterpret_cast<snapshot::Monitor*>(m), step, t, values);
+    });
+}
+
+void pdgpu_monitor_close(pdgpu_monitor_t m) {
+    if (m) snapshot::monitor_close(reinterpret_cast<snapshot::Monitor*>(m));
+}
+
 int pdgpu_write_snapshot(int dim, const int* dims, double spacing, const double* origin, const double* u,
                          const double* damage, int64_t step, double t, const char* dir, char* path_out, int path_cap) {
     return guarded([&] {

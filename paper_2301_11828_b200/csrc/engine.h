@@ -155,6 +155,15 @@ struct Engine {
     double adr_fixed_c = 0.0;
     int64_t step = 0;
     bool force_ready = false;
+    // MonitorWriter nodes (output.hpp:45-72): u at these nodes is gathered on
+    // the device after every step into rows [row][node][dim]; the host keeps
+    // (step, t) per row and drains them with pdgpu_sim_monitor_read
+    long long* d_mon_nodes = nullptr;
+    int n_mon = 0;
+    double* d_mon_rows = nullptr;
+    int mon_cap = 0, mon_dev_rows = 0;
+    std::vector<int64_t> mon_step;
+    std::vector<double> mon_t, mon_spill;  // spill: rows moved off the device when its buffer filled
     bool any_cmask = false;              // constraint mask set directly (set_regions)
     double* d_cg = nullptr;              // CG work vectors r, p, q, u_c
     int64_t cg_cap = 0;
@@ -299,5 +308,7 @@ void launch_enforce(double* u, double* v, const long long* dofs, const double* v
 void launch_axpy(double* y, const double* x, double a, int64_t n, cudaStream_t s);
 void launch_finite(const double* u, int64_t n, int* ok, cudaStream_t s);
 void launch_scatter(double* y, const long long* ids, const double* val, int64_t n, cudaStream_t s);
+void launch_monitor_gather(const double* u, const long long* nodes, int n, int dim, int64_t N, double* dst,
+                           cudaStream_t s);
 
 }  // namespace pdgpu

@@ -9,6 +9,8 @@
 #include <string.h>
 #include <sys/stat.h>
 
+#include <algorithm>
+#include <cmath>
 #include <fstream>
 #include <sstream>
 #include <string>
@@ -124,6 +126,62 @@ bool read(const std::string& path, int dim, int* dims, double* h, double* origin
         }
     }
     return true;
+}
+
+// ---- MonitorWriter (output.hpp:45-72): tab-separated rows "step t node u..."
+// with node ids from 1 and %.17g values, one header line, flushed per append.
+// nearest_node (output.hpp:33-41): floor((x - origin) / h) clamped per axis.
+int64_t nearest_node(int dim, const int* dims, double h, const double* origin, const double* x) {
+    int64_t p = 0, stride = 1;
+    for (int d = 0; d < dim; ++d) {
+        int i = (int)std::floor((x[d] - origin[d]) / h);
+        i = std::min(std::max(i, 0), dims[d] - 1);
+        p += stride * i;
+        stride *= dims[d];
+    }
+    return p;
+}
+
+struct Monitor {
+    FILE* fp = nullptr;
+    int dim = 0;
+    std::vector<int64_t> nodes;
+};
+
+Monitor* monitor_open(const char* path, int dim, const int* dims, double h, const double* origin, const double* pts,
+                      int npts, std::string& err) {
+    Monitor* m = new Monitor();
+    m->dim = dim;
+    for (int k = 0; k < npts; ++k) m->nodes.push_back(nearest_node(dim, dims, h, origin, pts + (size_t)k * dim));
+    if (path && path[0]) {
+        m->fp = fopen(path, "w");
+        if (!m->fp) {
+            err = std::string("cannot open monitor file: ") + path;
+            delete m;
+            return nullptr;
+        }
+        fputs(dim == 3 ? "# step\tt\tnode\tu_x\tu_y\tu_z\n" : "# step\tt\tnode\tu_x\tu_y\n", m->fp);
+    }
+    return m;
+}
+
+// vals: this row's monitored values [node][component]
+void monitor_append(Monitor* m, int64_t step, double t, const double* vals) {
+    if (!m->fp) return;
+    std::string out;
+    const std::string ts = g17(t);
+    for (size_t k = 0; k < m->nodes.size(); ++k) {
+        out += std::to_string((long long)step) + "\t" + ts + "\t" + std::to_string((long long)(m->nodes[k] + 1));
+        for (int d = 0; d < m->dim; ++d) out += "\t" + g17(vals[k * m->dim + d]);
+        out += "\n";
+    }
+    fputs(out.c_str(), m->fp);
+    fflush(m->fp);
+}
+
+void monitor_close(Monitor* m) {
+    if (m->fp) fclose(m->fp);
+    delete m;
 }
 
 }  // namespace snapshot

@@ -435,6 +435,21 @@ void launch_enforce(double* u, double* v, const long long* dofs, const double* v
     check(cudaGetLastError(), "enforce");
 }
 
+// MonitorWriter row: dst[k * dim + d] = u[d * N + nodes[k]]
+__global__ void k_monitor_gather(const double* __restrict__ u, const long long* __restrict__ nodes, int n, int dim,
+                                 int64_t N, double* __restrict__ dst) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * dim) return;
+    const int k = i / dim, d = i - k * dim;
+    dst[i] = u[(int64_t)d * N + nodes[k]];
+}
+
+void launch_monitor_gather(const double* u, const long long* nodes, int n, int dim, int64_t N, double* dst,
+                           cudaStream_t s) {
+    if (n <= 0) return;
+    k_monitor_gather<<<(n * dim + 127) / 128, 128, 0, s>>>(u, nodes, n, dim, N, dst);
+}
+
 void launch_scatter(double* y, const long long* ids, const double* val, int64_t n, cudaStream_t s) {
     if (n == 0) return;
     k_scatter<<<blocks_for(n, 256), 256, 0, s>>>(y, ids, val, n);

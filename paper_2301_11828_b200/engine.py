@@ -36,8 +36,12 @@ class CudaError(Error):
     pass
 
 
+class IoError(Error):
+    """pdfast::IoError (errors.hpp:33-35)"""
+
+
 _CODES = {1: HorizonTooLargeForGrid, 2: ShapeMismatch, 3: LedgerOutOfBand, 4: ValueError, 5: CudaError,
-          6: MemoryError, 7: NotImplementedError}
+          6: MemoryError, 7: NotImplementedError, 8: IoError}
 
 
 def _check(rc: int):
@@ -386,6 +390,24 @@ class FastForce:
         _check(self._lib.pdgpu_sim_finite(self._h, C.byref(ok)))
         return bool(ok.value)
 
+    def sim_monitor(self, nodes):
+        """Record u at `nodes` after every sim_step step on the device (MonitorWriter rows)."""
+        nodes = np.ascontiguousarray(nodes, dtype=np.int64)
+        _check(self._lib.pdgpu_sim_monitor(self._h, nodes.ctypes.data_as(_lib.c_int64_p), len(nodes)))
+        self._mon_n = len(nodes)
+
+    def sim_monitor_read(self):
+        """Drain the recorded rows: (steps[k], t[k], values[k, node, dim])."""
+        cnt = C.c_int64()
+        _check(self._lib.pdgpu_sim_monitor_read(self._h, None, None, None, 0, C.byref(cnt)))
+        k = cnt.value
+        steps = np.zeros(max(k, 1), dtype=np.int64)
+        t = np.zeros(max(k, 1))
+        vals = np.zeros((max(k, 1), getattr(self, "_mon_n", 0), self.dim))
+        _check(self._lib.pdgpu_sim_monitor_read(self._h, steps.ctypes.data_as(_lib.c_int64_p), _dp(t), _dp(vals), k,
+                                                C.byref(cnt)))
+        return steps[:k], t[:k], vals[:k]
+
     def write_snapshot(self, directory: str, u: np.ndarray, step: int, t: float, damage=None) -> str:
         """write_snapshot_dat (output.hpp:76-102) of host field u (dim, N) on this lattice/geometry."""
         return write_snapshot(directory, self.dims, self._geom[0], self._geom[1], u, step, t, damage)
@@ -427,6 +449,49 @@ def write_snapshot(directory: str, dims, h: float, origin, u: np.ndarray, step: 
     _check(lib.pdgpu_write_snapshot(dim, (C.c_int * dim)(*dims), float(h), _dp(org), _dp(u),
                                     None if d is None else _dp(d), int(step), float(t), directory.encode(), buf, 4096))
     return buf.value.decode()
+
+
+class MonitorWriter:
+    """pdfast::MonitorWriter<Dim> (output.hpp:45-72) on the library's host writer:
+    MonitorWriter(path, dims, h, origin, points); .nodes; .append(step, t, u)
+    with a host field u (dim, N); .append_sim(engine) writes the rows an engine
+    recorded on the device since the last call (FastForce.sim_monitor)."""
+
+    def __init__(self, path: str, dims, h: float, origin, points):
+        self.dims = tuple(int(d) for d in dims)
+        self.dim = len(self.dims)
+        pts = _f64(points).reshape(-1, self.dim)
+        d = (C.c_int * self.dim)(*self.dims)
+        self.nodes = np.zeros(len(pts), dtype=np.int64)
+        lib = _lib.load()
+        _check(lib.pdgpu_monitor_nodes(self.dim, d, float(h), _dp(_f64(origin)), _dp(pts), len(pts),
+                                       self.nodes.ctypes.data_as(_lib.c_int64_p)))
+        self._h = C.c_void_p()
+        _check(lib.pdgpu_monitor_open(path.encode() if path else None, self.dim, d, float(h), _dp(_f64(origin)),
+                                      _dp(pts), len(pts), C.byref(self._h)))
+        self._lib = lib
+
+    def append(self, step: int, t: float, u: np.ndarray):
+        u = np.asarray(u).reshape(self.dim, -1)
+        vals = _f64(u[:, self.nodes].T)
+        _check(self._lib.pdgpu_monitor_append(self._h, int(step), float(t), _dp(vals)))
+
+    def append_sim(self, engine: "FastForce") -> int:
+        steps, ts, vals = engine.sim_monitor_read()
+        for s_, t_, v_ in zip(steps, ts, vals):
+            _check(self._lib.pdgpu_monitor_append(self._h, int(s_), float(t_), _dp(_f64(v_))))
+        return len(steps)
+
+    def close(self):
+        if self._h:
+            self._lib.pdgpu_monitor_close(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def read_snapshot(path: str, dim: int):

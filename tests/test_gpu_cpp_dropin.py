@@ -15,6 +15,8 @@ here on the reference's own types:
   evaluate_force_and_cg   Simulation::evaluate_force <= 1e-11; solve_static's
                           solution meets 1e-10 through the reference's operator
   exceptions              HorizonTooLargeForGrid, ShapeMismatch, LedgerOutOfBand
+  monitor                 pdgpu::MonitorWriter on device-recorded rows vs the reference
+                          MonitorWriter fed every step: nodes, steps, t equal, u <= 1e-8
 """
 import json
 import os
@@ -26,7 +28,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 EXE = os.path.join(ROOT, "oracle", "_ref", "dropin_check")
 CHECKS = {"matvec_2d", "matvec_3d", "update_bonds", "simulation_vv_fracture", "simulation_adr",
-          "evaluate_force_and_cg", "exceptions"}
+          "evaluate_force_and_cg", "exceptions", "monitor"}
 
 
 @pytest.fixture(scope="module")

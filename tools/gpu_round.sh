@@ -1,11 +1,14 @@
 #!/bin/bash
-# One GPU call: tests, bench line, launch list, ncu full capture of the top kernels.
+# One GPU call: tests, bench line, sanitizers, launch list, ncu full capture of the top kernels.
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/smi.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/t.log 2>&1; echo "pytest rc=$?" >> gpurun_out/t.log
-timeout 600 python bench.py > gpurun_out/b.json 2> gpurun_out/b.err
+timeout 900 python bench.py > gpurun_out/b.json 2> gpurun_out/b.err
+for tool in memcheck racecheck synccheck; do
+  timeout 1200 compute-sanitizer --tool $tool --error-exitcode 9 python tools/sanitize.py > gpurun_out/san_$tool.log 2>&1; echo "rc=$?" >> gpurun_out/san_$tool.log
+done
 B="python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-extra"
 timeout 300 $B > gpurun_out/plain.log 2>&1 && timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv $B > gpurun_out/ncu1.log 2>&1
 B2="python bench.py --batch 2 --steps 1 --warmup 1 --no-cpu --no-e2e --no-extra"
-timeout 300 $B2 > gpurun_out/plain2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_rfft_rows|k_spectral2d_duo|k_irfft_rows|k_wrap" -s 4 -c 4 -o gpurun_out/prof $B2 > gpurun_out/ncu2.log 2>&1
+timeout 300 $B2 > gpurun_out/plain2.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_rfft_rows|k_spectral2d|k_irfft_rows|k_wrap" -s 4 -c 4 -o gpurun_out/prof $B2 > gpurun_out/ncu2.log 2>&1
 echo done
