@@ -549,7 +549,7 @@ void pdgpu_destroy(pdgpu_t h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    void* ptrs[] = {h->d_xstrip, h->d_lidx, h->d_loff, h->d_lK, h->d_vh, h->d_wrows, h->d_wo0, h->d_wK, h->d_tw, h->d_sym, h->d_K, h->d_offs, h->d_disp, h->d_S1, h->d_S2, h->d_u_stage, h->d_f_stage,
+    void* ptrs[] = {h->d_xstrip, h->d_lidx, h->d_loff, h->d_lK, h->d_sidx, h->d_stab, h->d_vh, h->d_wrows, h->d_wo0, h->d_wK, h->d_tw, h->d_sym, h->d_K, h->d_offs, h->d_disp, h->d_S1, h->d_S2, h->d_u_stage, h->d_f_stage,
                     h->d_cmask, h->d_surf_rows, h->d_surf_de, h->d_ledger, h->d_bond_rows, h->d_listed,
                     h->d_counters, h->d_new_pairs, h->d_body, h->d_cdofs, h->d_cval, h->d_ckind, h->d_u, h->d_v,
                     h->d_f, h->d_fprev, h->d_red, h->d_scal, h->d_ticket, h->d_cg, h->d_coltab,
@@ -1262,11 +1262,12 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
             cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
             launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
             launch_corrections(e, p, q, 1, s, -1.0);
-            launch_dot(e, p, q, m, e.d_scal + 1, s);
             if (multi) {
+                launch_dot(e, p, q, m, e.d_scal + 1, s);
                 comm_allreduce(e, e.d_scal + 1, 1, s);
                 launch_cg_step_dev_comm(e, x, r, p, q, m, e.d_scal, s);
-            } else {
+            } else if (!launch_cg_fused(e, x, r, p, q, m, e.d_scal, s)) {  // one cooperative kernel
+                launch_dot(e, p, q, m, e.d_scal + 1, s);
                 launch_cg_step_dev(e, x, r, p, q, m, e.d_scal, s);
             }
             cuda_check(cudaStreamEndCapture(s, &g), "end capture");

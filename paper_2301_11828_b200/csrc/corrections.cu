@@ -393,6 +393,205 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
     }
 }
 
+// K6w with per-state entry lists (the general form of k_wrap's fast path):
+// every band node, including edges and corners, loops over one precomputed
+// list of the entries that leave the lattice from its position class, with
+// the wrapped displacement stored -- no per-row bookkeeping, independent loads
+// (unrolled), and the ghost-row terms of halo slabs in the same pass.
+template <int D, int LPN>
+__global__ void __launch_bounds__(128) k_wrap_tab(const double* __restrict__ u, double* __restrict__ f,
+                                                  const int* __restrict__ sidx, const int4* __restrict__ stab,
+                                                  const double* __restrict__ wK, int M, int N0, int N1, int N2,
+                                                  int circ_mask, const uint8_t* __restrict__ cmask, int64_t nodes,
+                                                  int batch, double scale, int64_t band0, int64_t band1,
+                                                  int64_t band2, const double* __restrict__ ghost, int64_t gs_bc,
+                                                  int64_t gs_side, int lo_int, int hi_int,
+                                                  const double* __restrict__ xstrip) {
+    constexpr int NP = D * (D + 1) / 2;
+    constexpr int KS = (NP + 1) & ~1;
+    // LPN lanes per node (a quad of consecutive lanes), entries strided over them
+    const int64_t per_vec = band0 + band1 + band2;
+    const int64_t gidx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPN;
+    const int sub = threadIdx.x % LPN;
+    if (gidx >= per_vec * batch) return;
+    const int b = (int)(gidx / per_vec);
+    int64_t r = gidx - (int64_t)b * per_vec;
+    int ax = 0;
+    if (r >= band0) {
+        r -= band0;
+        ax = 1;
+        if (r >= band1) {
+            r -= band1;
+            ax = 2;
+        }
+    }
+    auto layer = [&](int64_t l, int n) { return (int)l < M ? (int)l : n - 2 * M + (int)l; };
+    int c0, c1, c2;
+    if (ax == 0) {
+        c1 = (int)(r % N1);
+        r /= N1;
+        c2 = (int)(r % N2);
+        r /= N2;
+        c0 = layer(r, N0);
+    } else if (ax == 1) {
+        c0 = (int)(r % N0);
+        r /= N0;
+        c2 = (int)(r % N2);
+        r /= N2;
+        c1 = layer(r, N1);
+    } else {
+        c0 = (int)(r % N0);
+        r /= N0;
+        c1 = (int)(r % N1);
+        r /= N1;
+        c2 = layer(r, N2);
+    }
+    if (ax >= 1 && (circ_mask & 1) && (c0 < M || c0 >= N0 - M)) return;
+    if (ax >= 2 && ((circ_mask >> 1) & 1) && (c1 < M || c1 >= N1 - M)) return;
+    auto st = [&](int c, int n) { return c < M ? 1 + c : (c >= n - M ? M + n - c : 0); };
+    const int S = 2 * M + 1;
+    const int state = st(c0, N0) + S * (st(c1, N1) + (D == 3 ? S * st(c2, N2) : 0));
+    const int64_t p = ((int64_t)c2 * N1 + c1) * N0 + c0;
+    const uint8_t cm = cmask ? cmask[p] : 0;
+    const double* ub = u + (int64_t)b * D * nodes + p;
+    // 3D x band: every read has x within 2M of the node's x face, i.e. in the
+    // compact strip [b][c][slot][z][y] (a warp spans y: unit stride)
+    const bool strip = D == 3 && ax == 0 && xstrip;
+    const int64_t spl = (int64_t)N1 * N2;
+    const double* sb = strip ? xstrip + (int64_t)b * D * 4 * M * spl : nullptr;
+    const int64_t plane = D == 3 ? (int64_t)N0 * N1 : N0;
+    const int64_t pin = D == 3 ? (int64_t)c1 * N0 + c0 : c0;  // in-plane index of p
+    double acc[D], gacc[D];
+#pragma unroll
+    for (int a = 0; a < D; ++a) acc[a] = gacc[a] = 0.0;
+    const int e0 = __ldg(sidx + state), e1 = __ldg(sidx + state + 1);
+#pragma unroll 4
+    for (int e = e0 + sub; e < e1; e += LPN) {
+        const int4 rec = __ldg(stab + e);
+        const int w0 = (int)(short)(rec.x & 0xffff), w1 = rec.x >> 16, w2 = rec.y;  // wrapped displacement
+        const int fl = rec.w;
+        double kv[KS];
+        const double2* ke = reinterpret_cast<const double2*>(wK + (int64_t)rec.z * KS);
+#pragma unroll
+        for (int k = 0; k < KS / 2; ++k) {
+            const double2 v2 = __ldg(ke + k);
+            kv[2 * k] = v2.x;
+            kv[2 * k + 1] = v2.y;
+        }
+        if (fl & 1) {
+            double uq[D];
+            if (strip) {
+                const int q0 = c0 + w0;
+                const int slot = q0 < 2 * M ? q0 : q0 - N0 + 4 * M;
+                const double* sp = sb + (int64_t)slot * spl + (int64_t)(c2 + w2) * N1 + (c1 + w1);
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) uq[bb] = sp[(int64_t)bb * 4 * M * spl];
+            } else {
+                const int64_t lin = (int64_t)w0 + (int64_t)N0 * (w1 + (int64_t)N1 * w2);
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) uq[bb] = ub[(int64_t)bb * nodes + lin];
+            }
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) acc[a] += kv[pair_idx<D>(a, bb)] * uq[bb];
+        }
+        if ((fl & 2) && ghost) {
+            const int sd = (fl >> 2) & 1;
+            if (sd ? hi_int : lo_int) {
+                const int gl = (fl >> 3) & 31;
+                const int64_t pidx = pin + (fl >> 8);
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) {
+                    const double g = ghost[(int64_t)(b * D + bb) * gs_bc + sd * gs_side + (int64_t)gl * plane + pidx];
+#pragma unroll
+                    for (int a = 0; a < D; ++a) gacc[a] += kv[pair_idx<D>(a, bb)] * g;
+                }
+            }
+        }
+    }
+    if (LPN > 1) {  // the node's lanes: consecutive, all alive (the early returns are per node)
+        const unsigned qm = ((1u << LPN) - 1u) << ((threadIdx.x & 31) & ~(LPN - 1));
+#pragma unroll
+        for (int o = 1; o < LPN; o <<= 1)
+#pragma unroll
+            for (int a = 0; a < D; ++a) {
+                acc[a] += __shfl_xor_sync(qm, acc[a], o);
+                gacc[a] += __shfl_xor_sync(qm, gacc[a], o);
+            }
+        if (sub) return;
+    }
+#pragma unroll
+    for (int a = 0; a < D; ++a) {
+        if ((cm >> a) & 1u) continue;
+        f[((int64_t)b * D + a) * nodes + p] += scale * (gacc[a] - acc[a]);
+    }
+}
+
+// per-state lists for k_wrap_tab (engine.h d_sidx / d_stab); entry ids index
+// the d_wK table built below (same storage order)
+static void build_state_table(Engine& e, const std::vector<int>& rows, const std::vector<int>& o0s) {
+    const Plan& pl = e.plan;
+    const int dim = e.dim, M = e.M, S = 2 * M + 1;
+    for (int a = 0; a < dim; ++a)
+        if (pl.N[a] < S || (a < 2 && pl.N[a] > 32767)) return;  // k_wrap's general path
+    const int SA = dim - 1;
+    const int nrows = dim == 3 ? S * S : S;
+    int nstates = 1;
+    for (int a = 0; a < dim; ++a) nstates *= S;
+    std::vector<int> sidx;
+    std::vector<int4> tab;
+    for (int state = 0; state < nstates; ++state) {
+        sidx.push_back((int)tab.size());
+        int sa[3] = {0, 0, 0};
+        int rem = state;
+        for (int a = 0; a < dim; ++a) {
+            sa[a] = rem % S;
+            rem /= S;
+        }
+        for (int row = 0; row < nrows; ++row)
+            for (int ei = rows[2 * row]; ei < rows[2 * row + 1]; ++ei) {
+                const int o[3] = {o0s[(size_t)ei], (dim == 3 ? row % S : row) - M, dim == 3 ? row / S - M : 0};
+                bool out[3] = {false, false, false};
+                int shift[3] = {0, 0, 0};
+                bool any = false, alias = true;
+                for (int a = 0; a < dim; ++a) {
+                    const int s_ = sa[a];
+                    if (s_ >= 1 && s_ <= M) out[a] = o[a] < -(s_ - 1);          // low face, depth s-1
+                    else if (s_ > M) out[a] = o[a] > (s_ - M - 1);              // high face, depth s-M-1
+                    if (!out[a]) continue;
+                    any = true;
+                    if (pl.circ[a]) shift[a] = s_ <= M ? pl.N[a] : -pl.N[a];
+                    else alias = false;
+                }
+                if (!any) continue;
+                // ghost rows: out along the slowest axis only
+                bool gh = out[SA];
+                for (int a = 0; a < SA; ++a) gh = gh && !out[a];
+                if (!alias && !gh) continue;
+                int fl = alias ? 1 : 0;
+                if (gh) {
+                    const int side = sa[SA] <= M ? 0 : 1;
+                    const int depth = side == 0 ? sa[SA] - 1 : sa[SA] - M - 1;
+                    const int c = side == 0 ? depth : pl.N[SA] - 1 - depth;  // coordinate of p along SA
+                    const int w = c + o[SA];
+                    const int gl = side == 0 ? w + M : w - pl.N[SA];
+                    const int goff = dim == 3 ? o[0] + pl.N[0] * o[1] : o[0];
+                    fl |= 2 | (side << 2) | (gl << 3) | (goff << 8);
+                }
+                // wrapped displacement: x and y in 16 bits each, z in 32
+                const int w0 = o[0] + shift[0], w1 = o[1] + shift[1], w2 = o[2] + shift[2];
+                tab.push_back(make_int4((int)(((uint32_t)w0 & 0xffffu) | ((uint32_t)w1 << 16)), w2, ei, fl));
+            }
+    }
+    sidx.push_back((int)tab.size());
+    if (tab.empty()) tab.push_back(make_int4(0, 0, 0, 0));
+    check(cudaMalloc((void**)&e.d_sidx, sizeof(int) * sidx.size()), "alloc state index");
+    check(cudaMemcpy(e.d_sidx, sidx.data(), sizeof(int) * sidx.size(), cudaMemcpyHostToDevice), "copy state index");
+    check(cudaMalloc((void**)&e.d_stab, sizeof(int4) * tab.size()), "alloc state table");
+    check(cudaMemcpy(e.d_stab, tab.data(), sizeof(int4) * tab.size(), cudaMemcpyHostToDevice), "copy state table");
+}
+
 void build_wrap_table(Engine& e) {
     const int dim = e.dim, M = e.M, side = 2 * M + 1, np = e.np;
     const int nrows = dim == 3 ? side * side : side;
@@ -451,6 +650,7 @@ void build_wrap_table(Engine& e) {
     up((void**)&e.d_lidx, lidx.data(), sizeof(int) * lidx.size());
     up((void**)&e.d_loff, loff.data(), sizeof(int) * loff.size());
     up((void**)&e.d_lK, lk.data(), sizeof(double) * lk.size());
+    if (!getenv("PDGPU_WRAP_GENERIC")) build_state_table(e, rows, o0s);
 }
 
 void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
@@ -478,6 +678,24 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
         k_xstrip<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(u, e.d_xstrip, pl.N[0], pl.N[1], pl.N[2], e.M, nrows);
         xstrip = e.d_xstrip;
         e.launches += 1;
+    }
+    if (e.d_stab) {  // per-state lists (every band node)
+        // few band nodes (small lattices, latency-bound): four lanes per node
+        const bool quad = tot < (int64_t)e.num_sms * 256;
+        const unsigned tb = (unsigned)((tot * (quad ? 4 : 1) + th - 1) / th);
+#define PDGPU_WT(D, L, XS)                                                                                       \
+    k_wrap_tab<D, L><<<tb, th, 0, s>>>(u, f, e.d_sidx, e.d_stab, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2], pl.circ_mask, \
+                                       cmask, pl.nodes, batch, scale, band[0], band[1], band[2], ghost,              \
+                                       e.ghost_bc_stride, e.ghost_side_stride, lo_int, hi_int, XS)
+        if (pl.dim == 2) {
+            if (quad) PDGPU_WT(2, 4, nullptr);
+            else PDGPU_WT(2, 1, nullptr);
+        } else {
+            if (quad) PDGPU_WT(3, 4, xstrip);
+            else PDGPU_WT(3, 1, xstrip);
+        }
+#undef PDGPU_WT
+        return;
     }
     if (pl.dim == 2)
         k_wrap<2><<<blocks, th, 0, s>>>(u, f, e.d_wrows, e.d_wo0, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],

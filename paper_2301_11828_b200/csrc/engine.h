@@ -86,6 +86,15 @@ struct Engine {
     int* d_lidx = nullptr;
     int* d_loff = nullptr;
     double* d_lK = nullptr;
+    // per-state entry lists (k_wrap_tab): a band node's state is its position
+    // class on every axis (interior, depth l from the low face, depth l from
+    // the high face: (2M+1)^dim states); d_sidx[state] = first record (one
+    // extra end slot); a record {lin (int64), box entry (int32), flags (int32)}
+    // says: subtract K(box) u[p + lin] (flag 1, lin already wrapped) and/or add
+    // the ghost-row term (flag 2, side bit 2, layer bits 3-7, in-plane offset
+    // bits 8-31).  Empty (d_stab null) when an axis is shorter than 2M + 1.
+    int* d_sidx = nullptr;
+    int4* d_stab = nullptr;
     double* d_kc = nullptr;         // centre coefficients (3D direct stencil)
     double* d_coltab = nullptr;     // separable symbol: per column n_pairs x (M+1) coefficients (2D)
     int coltab_oddmask = 0;         // bit p: pair p odd along the column axis (sin terms)
@@ -296,6 +305,8 @@ void launch_cg_step_dev_comm(Engine& e, double* x, double* r, double* p, const d
 void launch_cg_direction(double* p, const double* r, int64_t n, const double* scal, cudaStream_t s);
 void launch_cg_step_dev(Engine& e, double* x, double* r, double* p, const double* q, int64_t n, double* scal,
                         cudaStream_t s);
+bool launch_cg_fused(Engine& e, double* x, double* r, double* p, const double* q, int64_t n, double* scal,
+                     cudaStream_t s);
 void launch_mask_rhs(double* out, const double* b, const double* Auc, const uint8_t* cmask,
                      int64_t N, int dim, cudaStream_t s);
 void launch_vv_drift(double* u, const double* v, const double* f, const uint8_t* cmask, int64_t N,

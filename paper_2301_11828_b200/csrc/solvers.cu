@@ -4,6 +4,7 @@
 // CG is new work (the reference has only ADR, timestepping.hpp:79-145);
 // VV drift/kick/constraints follow timestepping.hpp:312-334 and
 // corrections.hpp:142-160.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <stdexcept>
@@ -12,6 +13,8 @@
 #include "engine.h"
 
 namespace pdgpu {
+
+static void check(cudaError_t e, const char* what);
 
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs, fixed => deterministic order
 constexpr int kRedThreads = 256;
@@ -185,6 +188,106 @@ __global__ void k_cg_direction_dev(double* __restrict__ p, const double* __restr
     const double beta = scal[0] / scal[7];  // rr_new / rr_old, rotated by k_cg_update_dev
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         p[i] = r[i] + beta * p[i];
+}
+
+// ---- one CG step in one cooperative kernel (graph-captured single-GPU CG):
+// p.q, the x / r update with r.r, and the new direction, separated by two grid
+// barriers instead of three launches.  Every block forms the totals itself from
+// the per-block partials in the same fixed order as grid_reduce's last block,
+// so the iterates are bit-identical to k_dot + k_cg_update_dev +
+// k_cg_direction_dev.
+__device__ __forceinline__ void block_partial(double v, double* partial, double* ws) {
+    v = warp_sum(v);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) ws[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double s = lane < (blockDim.x >> 5) ? ws[lane] : 0.0;
+        s = warp_sum(s);
+        if (lane == 0) partial[blockIdx.x] = s;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ double block_total(const double* partial, double* ws, double* tot) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) s += __ldcg(partial + i);  // not L1: other SMs wrote it
+    s = warp_sum(s);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) ws[wid] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+        *tot = t;
+    }
+    __syncthreads();
+    return *tot;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_cg_fused(double* __restrict__ x, double* __restrict__ r,
+                                                         double* __restrict__ p, const double* __restrict__ q,
+                                                         int64_t n, double* scal, double* partA, double* partB) {
+    namespace cg = cooperative_groups;
+    __shared__ double ws[32];
+    __shared__ double tot;
+    if (scal[4] != 0.0) return;  // converged: every block leaves before any barrier
+    const double rr = scal[0], thr = scal[3];
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, st = (int64_t)gridDim.x * blockDim.x;
+    double s = 0.0;
+    for (int64_t i = i0; i < n; i += st) s += p[i] * q[i];
+    block_partial(s, partA, ws);
+    cg::this_grid().sync();
+    const double pq = block_total(partA, ws, &tot);
+    const double alpha = rr / pq;
+    s = 0.0;
+    for (int64_t i = i0; i < n; i += st) {
+        x[i] += alpha * p[i];
+        const double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        s += ri * ri;
+    }
+    block_partial(s, partB, ws);
+    cg::this_grid().sync();
+    const double rrn = block_total(partB, ws, &tot);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        scal[1] = pq;
+        scal[7] = rr;
+        scal[0] = rrn;
+        scal[2] = rrn;
+        scal[5] += 1.0;
+        if (rrn <= thr) scal[4] = 1.0;
+    }
+    if (rrn <= thr) return;
+    const double beta = rrn / rr;
+    for (int64_t i = i0; i < n; i += st) p[i] = r[i] + beta * p[i];
+}
+
+// true when the fused step can run (all kRedBlocks co-resident); launches it
+bool launch_cg_fused(Engine& e, double* x, double* r, double* p, const double* q, int64_t n, double* scal,
+                     cudaStream_t s) {
+    static int ok = -1;
+    if (ok < 0) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_fused, kRedThreads, 0);
+        int coop = 0;
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, e.device);
+        const char* env = getenv("PDGPU_CG_FUSED");
+        ok = coop && per_sm * e.num_sms >= kRedBlocks && !(env && env[0] == '0');
+    }
+    if (!ok) return false;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kRedBlocks);
+    cfg.blockDim = dim3(kRedThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    check(cudaLaunchKernelEx(&cfg, k_cg_fused, x, r, p, q, n, scal, e.d_red, e.d_red + 1024), "cg fused");
+    e.launches += 1;
+    return true;
 }
 
 __global__ void k_mask_rhs(double* out, const double* b, const double* Auc, const uint8_t* cmask, int64_t N,

@@ -1861,6 +1861,8 @@ no_duo:
     auto psmem_of = [&](int tr) { return smem_of(tr) + sizeof(double) * (size_t)tr * rowlen; };
     int PTR = TR;  // pipelined kernel: shrink the tile until the staging buffer fits
     while (PTR > 1 && psmem_of(PTR) > 227 * 1024) PTR /= 2;
+    // small lattices: down until the grid covers the SMs twice
+    while (PTR > 1 && (int64_t)((Ny + PTR - 1) / PTR) * nslab < 2 * e.num_sms) PTR /= 2;
     if ((Nx & 1) == 0 && psmem_of(PTR) <= 227 * 1024 && !getenv("PDGPU_NO_K1_PIPE")) {
         const size_t psmem = psmem_of(PTR);
         const int64_t ntiles = (int64_t)((Ny + PTR - 1) / PTR) * nslab;
@@ -1927,6 +1929,9 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
     if (tma_rows) TR = 2;
     // short rows: at least 128 threads per CTA (up to the 8-row template limit)
     while (!tma_rows && TR < pl.k1_rows && 2 * TR * threads_per_transform(pl.logQx, 4) < 128) TR *= 2;
+    // small lattices (latency-bound: CG on 128^2): rows per CTA down until the
+    // grid covers the SMs twice
+    while (!tma_rows && TR > 1 && (int64_t)((Ny + TR - 1) / TR) * nslab < 2 * e.num_sms) TR /= 2;
     if (const char* env = getenv("PDGPU_K5_ROWS")) TR = std::max(1, std::min(pl.k1_rows, atoi(env)));
     while (TR & (TR - 1)) TR &= TR - 1;  // power of two (template)
     const int ltr = TR == 8 ? 3 : TR == 4 ? 2 : TR == 2 ? 1 : 0;
@@ -2040,7 +2045,9 @@ void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s) {
         return;
     }
     if ((nh == 1 || !(k3env && std::string(k3env) == "pipe")) && lq >= 4) {
-        const int NCd = kPipeThreads / Tp;
+        int NCd = kPipeThreads / Tp;
+        // small lattices: fewer columns per CTA until the grid covers the SMs twice
+        while (NCd > 1 && (int64_t)((pl.ncols + NCd - 1) / NCd) * batch < 2 * e.num_sms) NCd /= 2;
         const size_t dsmem = (size_t)NCd * (sizeof(double2) * (1 << lq) + sizeof(double) * xbuf_slots(lq) +
                                             (mode == 2 ? sizeof(double) * ND : 0) + sizeof(uint64_t));
         const int per_sm = std::max(1, std::min(2, (int)(228 * 1024 / (dsmem + 1024))));
