@@ -309,6 +309,11 @@ __device__ __forceinline__ void tma_load_3d(const CUtensorMap* m, void* dst, uin
         : "memory");
 }
 
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* m, int x, int y, int z) {
+    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(m), "r"(x), "r"(y), "r"(z)
+                 : "memory");
+}
+
 // TMAG: the tile's [kx][row] spectrum block lands in SMEM through TMA boxes
 // ({2*TR doubles, 256 kx} per box, the box tensor map tm over S) instead of
 // per-thread global gathers; the pre-processing then reads it from SMEM.
@@ -318,7 +323,7 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
                                                     const double2* __restrict__ tw, int logTWN, double scale,
                                                     const uint8_t* __restrict__ cmask,
                                                     const double* __restrict__ body, int64_t nodes,
-                                                    const __grid_constant__ CUtensorMap tm) {
+                                                    const __grid_constant__ CUtensorMap tm, int pf) {
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R;
     constexpr int XB = TMAG ? xbuf_stride_rows(Sh::XBUF) : Sh::XBUF;  // per-transform buffer stride
@@ -363,6 +368,14 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
             if (threadIdx.x == 0) {
                 mbar_expect_tx(&bar, (unsigned)(nbox * 256 * TR * 16));
                 for (int bx = 0; bx < nbox; ++bx) tma_load_3d(&tm, land + bx * 256 * TR, &bar, 2 * row0, bx * 256, slab);
+                // the block of the CTA that starts pf CTAs later (launch order:
+                // x fastest) into L2, so its landing is an L2 hit
+                if (pf) {
+                    const int64_t nxt = (int64_t)blockIdx.y * gridDim.x + blockIdx.x + pf;
+                    const int by = (int)(nxt / gridDim.x), bxx = (int)(nxt % gridDim.x);
+                    if (by < (int)gridDim.y)
+                        for (int bx = 0; bx < nbox; ++bx) tma_prefetch_3d(&tm, 2 * bxx * TR, bx * 256, by);
+                }
             }
             mbar_wait(&bar, 0);
             static_assert(U % 2 == 0, "even / odd k halves");
@@ -810,7 +823,7 @@ template <int LOGQ, bool CIRC, bool TSTORE = false, int CFM = 0>
 __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restrict__ u, double2* __restrict__ S,
                                                           int Nx, int Nrow, int nslab, int Hx,
                                                           const double2* __restrict__ tw, int logTWN,
-                                                          const __grid_constant__ CUtensorMap tm) {
+                                                          const __grid_constant__ CUtensorMap tm, int pf) {
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
     constexpr int LOGTR = 11 - LOGQ;  // rows per tile: 2 * TR * T = 256 threads
@@ -870,6 +883,14 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
     for (; tile < ntiles; tile += gridDim.x) {
         const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
         const int nr = min(TR, Nrow - row0);
+        if (pf && bulk && threadIdx.x == 0 && tile + (int64_t)pf * gridDim.x < ntiles) {
+            // the rows this CTA fetches pf tiles later, into L2 now
+            const int64_t nt = tile + (int64_t)pf * gridDim.x;
+            const int ns = (int)(nt / groups), nr0 = (int)(nt % groups) * TR;
+            const int nn = min(TR, Nrow - nr0);
+            for (int rr2 = 0; rr2 < nn; ++rr2)
+                l2_prefetch(u + ((int64_t)ns * Nrow + nr0 + rr2) * Nx, rowlen * 8);
+        }
         double2 v[R];
         if (bulk) {
             mbar_wait(&bar, ph);  // rows past the lattice (nr < TR) hold stale data: never stored
@@ -1822,6 +1843,10 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
         // quarter-warp).  SMEM bank conflicts 129M -> 18M per launch, and 6 %
         // faster at batch 2, but 22 % slower at batch 16 (long-scoreboard
         // stalls 23 -> 38 %, same DRAM bytes): off by default
+        // L2 prefetch of the rows this CTA loads PDGPU_K1_PF tiles later: off
+        // (measured 2.21 -> 2.7 / 3.1 ms at 4096^2 x 16 with 1 / 2 tiles ahead)
+        const char* pfenv = getenv("PDGPU_K1_PF");
+        const int k1pf = pfenv ? atoi(pfenv) : 0;
         const char* cfenv = getenv("PDGPU_K1_CF");
         const int cfm = (cx && lqx == 10 && cfenv && cfenv[0] == '1') ? 1 : 0;
         const size_t dsm = (size_t)k1_duo_smem(lqx, cx, cfm);
@@ -1838,10 +1863,10 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
             const bool tst = cx && DTR <= 2 && !(tenv && tenv[0] == '0') && encode_box_map(tm, e.d_S1, Ny, pl.Hx, nslab, DTR) &&
                              (size_t)(((pl.Hx + 255) / 256) * 256 * DTR * 16 + 128) <= dsm;
 #define PDGPU_K1T(CF) k_rfft_rows_duo<LQ, true, true, CF><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, \
-                                                                                e.d_tw, pl.logTWN, tm)
+                                                                                e.d_tw, pl.logTWN, tm, k1pf)
 #define PDGPU_K1D(C) (tst ? (cfm == 1 ? PDGPU_K1T(1) : PDGPU_K1T(0))                                     \
                       : k_rfft_rows_duo<LQ, C><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, e.d_tw, \
-                                                                      pl.logTWN, tm))
+                                                                      pl.logTWN, tm, k1pf))
             switch (lqx) {
                 PDGPU_CASE(6, (cx ? PDGPU_K1D(true) : PDGPU_K1D(false)))
                 PDGPU_CASE(7, (cx ? PDGPU_K1D(true) : PDGPU_K1D(false)))
@@ -1940,6 +1965,12 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
     const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_slots(lqx);
     CUtensorMap tm;
     memset(&tm, 0, sizeof(tm));
+    // L2 prefetch of the TMA-landed block of the CTA launched num_sms later
+    // (its landing then hits L2: the block is 2049 32-byte pieces 64 KB apart):
+    // K5 2.22 -> 1.97 ms at 4096^2 x 16, 0.479 -> 0.465 at 2048^2, but
+    // 0.113 -> 0.136 at 1024^2, so from 2048-wide rows up (PDGPU_K5_PF = distance)
+    const char* pfenv = getenv("PDGPU_K5_PF");
+    const int k5pf = pfenv ? atoi(pfenv) : (lqx >= 9 ? e.num_sms : 0);
     // TMA-landed gathers (periodic rows, two per CTA; PDGPU_K5_TMA=0 disables)
     if (cx && TR == 2 && lqx >= 8 && use_tma && encode_box_map(tm, xin, Ny, pl.Hx, nslab, TR)) {
         const int nbox = (pl.Hx + 255) / 256;
@@ -1947,21 +1978,21 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
                                     sizeof(double2) * (size_t)nbox * 256 * TR) + 128;
         switch (lqx) {
             PDGPU_CASE(8, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf)))
             PDGPU_CASE(9, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf)))
             PDGPU_CASE(10, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf)))
             PDGPU_CASE(11, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf)))
             PDGPU_CASE(12, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf)))
             default: break;
         }
         return;
     }
 #define PDGPU_K5(LT, C) k_irfft_rows<LQ, LT, C><<<grid, 2 * TR * T, smem, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx, e.d_tw, \
-                                                                          pl.logTWN, scale, cmask, body, pl.nodes, tm)
+                                                                          pl.logTWN, scale, cmask, body, pl.nodes, tm, 0)
 #define PDGPU_K5C(C) (ltr == 3 ? PDGPU_K5(3, C) : ltr == 2 ? PDGPU_K5(2, C) : ltr == 1 ? PDGPU_K5(1, C) : PDGPU_K5(0, C))
     if (cx) PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(true))
     else PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(false))
