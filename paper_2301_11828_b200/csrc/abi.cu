@@ -207,6 +207,174 @@ __global__ void k_break_pairs(uint32_t* ledger, int lw, const long long* quad, i
     if (atomicExch(&listed[q], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = q;
 }
 
+// ---- on-device assembly (set-up) --------------------------------------
+// Crack seeding (seed_cracks, fracture.hpp:164-198) with the predicates of
+// fracture.hpp:38-55 / 75-92 / 122-146 in explicitly rounded fp64 (no FMA
+// contraction: bit-identical to the host restatement and the reference),
+// thread per node of the crack's bounding box; the lower node of each bond
+// tests it (q > p) and sets both ledger bits as k_break_pairs does.
+struct SeedGeom {
+    double g[9];
+};
+
+__device__ int d_orient2_sign(const double* a, const double* b, const double* c) {
+    const double t1 = __dmul_rn(__dsub_rn(b[0], a[0]), __dsub_rn(c[1], a[1]));
+    const double t2 = __dmul_rn(__dsub_rn(b[1], a[1]), __dsub_rn(c[0], a[0]));
+    const double det = __dsub_rn(t1, t2);
+    const double tol = __dmul_rn(1e-10, __dadd_rn(fabs(t1), fabs(t2)));
+    if (fabs(det) <= tol) return 0;
+    return det > 0.0 ? 1 : -1;
+}
+
+__device__ bool d_segments_cross(const double* a, const double* b, const double* p, const double* q) {
+    const int o1 = d_orient2_sign(a, b, p), o2 = d_orient2_sign(a, b, q);
+    const int o3 = d_orient2_sign(p, q, a), o4 = d_orient2_sign(p, q, b);
+    return o1 * o2 < 0 && o3 * o4 < 0;
+}
+
+__device__ bool d_segment_crosses(const double* seg, const double* p, const double* q) {
+    const double a[2] = {seg[0], seg[1]}, b[2] = {seg[2], seg[3]};
+    const double width = seg[4];
+    if (width <= 0.0) return d_segments_cross(a, b, p, q);
+    const double t[2] = {__dsub_rn(b[0], a[0]), __dsub_rn(b[1], a[1])};
+    const double len = __dsqrt_rn(__dadd_rn(__dmul_rn(t[0], t[0]), __dmul_rn(t[1], t[1])));
+    if (len == 0.0) return false;
+    const double nrm[2] = {__ddiv_rn(-t[1], len), __ddiv_rn(t[0], len)};
+    for (int si = 0; si < 2; ++si) {
+        const double side = si == 0 ? __dmul_rn(0.5, width) : __dmul_rn(-0.5, width);
+        const double fa[2] = {__dadd_rn(a[0], __dmul_rn(side, nrm[0])), __dadd_rn(a[1], __dmul_rn(side, nrm[1]))};
+        const double fb[2] = {__dadd_rn(b[0], __dmul_rn(side, nrm[0])), __dadd_rn(b[1], __dmul_rn(side, nrm[1]))};
+        if (d_segments_cross(fa, fb, p, q)) return true;
+    }
+    return false;
+}
+
+__device__ bool d_notch_crosses(const double* nt, const double* p, const double* q) {
+    const int axis = (int)nt[0];
+    const double plane = nt[1], width = nt[2];
+    const int n_faces = width > 0.0 ? 2 : 1;
+    for (int fi = 0; fi < n_faces; ++fi) {
+        const double face = width > 0.0 ? (fi == 0 ? __dsub_rn(plane, __dmul_rn(0.5, width))
+                                                   : __dadd_rn(plane, __dmul_rn(0.5, width)))
+                                         : plane;
+        const double dp = __dsub_rn(p[axis], face), dq = __dsub_rn(q[axis], face);
+        const double tol = __dmul_rn(1e-12, __dadd_rn(__dadd_rn(fabs(p[axis]), fabs(q[axis])), fabs(face)));
+        if (fabs(dp) <= tol || fabs(dq) <= tol) continue;
+        if (!((dp > 0.0 && dq < 0.0) || (dp < 0.0 && dq > 0.0))) continue;
+        const double t = __ddiv_rn(dp, __dsub_rn(dp, dq));
+        bool inside = true;
+        for (int d = 0; d < 3; ++d) {
+            if (d == axis) continue;
+            const double x = __dadd_rn(p[d], __dmul_rn(t, __dsub_rn(q[d], p[d])));
+            inside = inside && x >= nt[3 + d] && x <= nt[6 + d];
+        }
+        if (inside) return true;
+    }
+    return false;
+}
+
+template <bool NOTCH>
+__global__ void k_seed(SeedGeom geom, int dim, int N0, int N1, int N2, int lo0, int lo1, int lo2, int n0, int n1,
+                       int64_t total, double h, double o0, double o1, double o2, const int* __restrict__ offs, int nof,
+                       uint32_t* ledger, int lw, long long* bond_rows, int* listed, unsigned long long* counters) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= total) return;
+    const int c[3] = {lo0 + (int)(i % n0), lo1 + (int)((i / n0) % n1), lo2 + (int)(i / ((int64_t)n0 * n1))};
+    const double org[3] = {o0, o1, o2};
+    double xp[3] = {0, 0, 0};
+    for (int d = 0; d < dim; ++d) xp[d] = __dadd_rn(org[d], __dmul_rn(__dadd_rn((double)c[d], 0.5), h));
+    const int Nd[3] = {N0, N1, N2};
+    const int64_t p = ((int64_t)c[2] * N1 + c[1]) * N0 + c[0];
+    for (int k = 0; k < nof; ++k) {
+        const int qc[3] = {c[0] + offs[3 * k], c[1] + offs[3 * k + 1], c[2] + offs[3 * k + 2]};
+        bool in = true;
+        for (int d = 0; d < dim; ++d) in = in && qc[d] >= 0 && qc[d] < Nd[d];
+        if (!in) continue;
+        const int64_t q = ((int64_t)qc[2] * N1 + qc[1]) * N0 + qc[0];
+        if (q < p) continue;  // visited from q
+        double xq[3] = {0, 0, 0};
+        for (int d = 0; d < dim; ++d) xq[d] = __dadd_rn(org[d], __dmul_rn(__dadd_rn((double)qc[d], 0.5), h));
+        const bool cross = NOTCH ? d_notch_crosses(geom.g, xp, xq) : d_segment_crosses(geom.g, xp, xq);
+        if (!cross) continue;
+        const int kn = offs[3 * nof + k];  // index of -offset
+        const unsigned old = atomicOr(&ledger[p * lw + (k >> 5)], 1u << (k & 31));
+        if ((old >> (k & 31)) & 1u) continue;
+        atomicOr(&ledger[q * lw + (kn >> 5)], 1u << (kn & 31));
+        atomicAdd(&counters[1], 1ull);
+        if (atomicExch(&listed[p], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = p;
+        if (atomicExch(&listed[q], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = q;
+    }
+}
+
+// SurfaceDiag (corrections.hpp:24-42) on the device for the engine's own
+// lattice: near-surface rows enumerated row by row (a whole x row when y / z
+// is within M of a face, else its 2M end nodes), so rows come out ascending
+// like the host scan; D^e sums the kernel entries of the offsets that leave
+// the lattice in for_each_offset order (koff), i.e. the same sums.
+__global__ void k_surface_rows(int dim, int M, int N0, int N1, int N2, const long long* __restrict__ rowoff,
+                               int64_t nrows, const int* __restrict__ offs, int nof,
+                               const double* __restrict__ koff, int np, long long* out_rows, double* out_de) {
+    const int64_t r = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;  // (z, y) row
+    if (r >= nrows) return;
+    const long long b0 = rowoff[r], cnt = rowoff[r + 1] - b0;
+    const int y = (int)(r % N1), z = (int)(r / N1);
+    for (long long i = threadIdx.x; i < cnt; i += blockDim.x) {
+        const int x = cnt == N0 ? (int)i : (i < M ? (int)i : N0 - 2 * M + (int)i);
+        const int c[3] = {x, y, z};
+        const int Nd[3] = {N0, N1, N2};
+        double acc[6] = {0, 0, 0, 0, 0, 0};
+        for (int k = 0; k < nof; ++k) {
+            bool inside = true;
+            for (int d = 0; d < dim; ++d) {
+                const int q = c[d] + offs[3 * k + d];
+                inside = inside && q >= 0 && q < Nd[d];
+            }
+            if (inside) continue;
+            for (int pp = 0; pp < np; ++pp) acc[pp] = __dadd_rn(acc[pp], koff[(int64_t)k * np + pp]);
+        }
+        out_rows[b0 + i] = ((long long)z * N1 + y) * N0 + x;
+        for (int pp = 0; pp < np; ++pp) out_de[(b0 + i) * np + pp] = acc[pp];
+    }
+}
+
+// engine's own lattice (no slab frame): D^e and the near-surface row list on
+// the device; the host near flags are filled lazily (ensure_h_near)
+void build_surface_device(Engine& e) {
+    const int dim = e.dim, M = e.M;
+    const int* N = e.plan.N;
+    const int nz = dim == 3 ? N[2] : 1;
+    const int64_t nrows = (int64_t)N[1] * nz;
+    std::vector<long long> rowoff((size_t)nrows + 1, 0);
+    for (int64_t r = 0; r < nrows; ++r) {
+        const int y = (int)(r % N[1]), z = (int)(r / N[1]);
+        bool full = y < M || y >= N[1] - M;
+        if (dim == 3) full = full || z < M || z >= N[2] - M;
+        const long long cnt = full || N[0] <= 2 * M ? N[0] : 2 * M;
+        rowoff[(size_t)r + 1] = rowoff[(size_t)r] + cnt;
+    }
+    const int64_t n = rowoff[(size_t)nrows];
+    touch_state(e);
+    e.n_surf = n;
+    dalloc(e.d_surf_rows, (size_t)n, "alloc surface rows");
+    dalloc(e.d_surf_de, (size_t)(n * e.np), "alloc surface de");
+    long long* d_rowoff = nullptr;
+    cuda_check(cudaMalloc(&d_rowoff, sizeof(long long) * rowoff.size()), "alloc row offsets");
+    cuda_check(cudaMemcpy(d_rowoff, rowoff.data(), sizeof(long long) * rowoff.size(), cudaMemcpyHostToDevice), "rowoff");
+    const unsigned gx = (unsigned)std::min<int64_t>(nrows, 65535);
+    const unsigned gy = (unsigned)((nrows + gx - 1) / gx);
+    k_surface_rows<<<dim3(gx, gy), 128, 0, e.stream>>>(dim, M, N[0], N[1], nz, d_rowoff, nrows, e.d_offs, e.nof,
+                                                       e.d_K + e.np * e.ss, e.np, e.d_surf_rows, e.d_surf_de);
+    cuda_check(cudaGetLastError(), "surface rows");
+    cuda_check(cudaStreamSynchronize(e.stream), "surface rows");
+    cudaFree(d_rowoff);
+    e.h_near.clear();
+}
+
+void ensure_h_near(Engine& e) {
+    if ((int64_t)e.h_near.size() == e.plan.nodes) return;
+    e.h_near = assembly::near_surface(e.dim, e.plan.N, e.M, e.slab);
+}
+
 // host (p,q) pairs -> device bits; dedups within the call by sequential
 // semantics of break_bond (a pair listed twice breaks once).
 int64_t break_pairs(Engine& e, const int64_t* pairs, int64_t n) {
@@ -522,11 +690,15 @@ int pdgpu_create(int dim, const int* dims, int M, const double* stencils, int de
             build_coltab(*e);
             build_wrap_table(*e);  // wrap correction and slab ghost rows (built before any graph capture)
             // regions + surface diagonal from the geometry (build_de)
-            e->h_near = assembly::near_surface(dim, dims, M);
-            std::vector<long long> rows;
-            std::vector<double> de;
-            assembly::surface_diag(dim, dims, M, e->stencils.data(), e->h_near, rows, de);
-            upload_surface(*e, rows, de);
+            if (getenv("PDGPU_HOST_ASSEMBLY")) {
+                e->h_near = assembly::near_surface(dim, dims, M);
+                std::vector<long long> rows;
+                std::vector<double> de;
+                assembly::surface_diag(dim, dims, M, e->stencils.data(), e->h_near, rows, de);
+                upload_surface(*e, rows, de);
+            } else {
+                build_surface_device(*e);  // D^e and the near-surface rows on the device
+            }
             dalloc(e->d_cmask, (size_t)N, "alloc cmask");
             cuda_check(cudaMemset(e->d_cmask, 0, (size_t)N), "zero cmask");
             e->h_cmask.assign((size_t)N, 0);
@@ -740,6 +912,7 @@ int pdgpu_set_surface_diag(pdgpu_t h, const double* de) {
         if (!h || !de) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
         cuda_check(cudaSetDevice(h->device), "set device");
         const int64_t N = h->plan.nodes;
+        ensure_h_near(*h);
         std::vector<long long> rows;
         std::vector<double> vals;
         for (int64_t p = 0; p < N; ++p) {
@@ -1013,6 +1186,40 @@ static void seed_impl(Engine& e, const double* geom, bool notch, int64_t* added)
     }
     clo[SA] = std::max(clo[SA], zoff);
     chi[SA] = std::min(chi[SA], zoff + e.plan.N[SA] - 1);
+    if (e.slab.global < 0 && !getenv("PDGPU_HOST_ASSEMBLY")) {
+        // the engine's own lattice: the box sweep runs on the device (k_seed)
+        for (int d = 0; d < dim; ++d)
+            if (chi[d] < clo[d]) {
+                if (added) *added = 0;
+                return;
+            }
+        ensure_ledger(e);
+        touch_state(e);
+        SeedGeom sg;
+        for (int i = 0; i < 9; ++i) sg.g[i] = i < (notch ? 9 : 5) ? geom[i] : 0.0;
+        const int n0 = chi[0] - clo[0] + 1, n1 = dim >= 2 ? chi[1] - clo[1] + 1 : 1, n2 = dim == 3 ? chi[2] - clo[2] + 1 : 1;
+        const int64_t total = (int64_t)n0 * n1 * n2;
+        cuda_check(cudaMemsetAsync(e.d_counters + 1, 0, sizeof(unsigned long long), e.stream), "reset");
+        const unsigned blocks = (unsigned)((total + 127) / 128);
+        if (notch)
+            k_seed<true><<<blocks, 128, 0, e.stream>>>(sg, dim, e.plan.N[0], e.plan.N[1], e.plan.N[2], clo[0], clo[1],
+                                                       clo[2], n0, n1, total, e.h, e.origin[0], e.origin[1], e.origin[2],
+                                                       e.d_offs, e.nof, e.d_ledger, e.lw, e.d_bond_rows, e.d_listed,
+                                                       e.d_counters);
+        else
+            k_seed<false><<<blocks, 128, 0, e.stream>>>(sg, dim, e.plan.N[0], e.plan.N[1], e.plan.N[2], clo[0], clo[1],
+                                                        clo[2], n0, n1, total, e.h, e.origin[0], e.origin[1],
+                                                        e.origin[2], e.d_offs, e.nof, e.d_ledger, e.lw, e.d_bond_rows,
+                                                        e.d_listed, e.d_counters);
+        cuda_check(cudaGetLastError(), "seed");
+        unsigned long long cnt[2];
+        cuda_check(cudaMemcpyAsync(cnt, e.d_counters, sizeof(cnt), cudaMemcpyDeviceToHost, e.stream), "counters");
+        cuda_check(cudaStreamSynchronize(e.stream), "seed sync");
+        e.n_bond_rows = (int64_t)cnt[0];
+        e.total_broken += (int64_t)cnt[1];
+        if (added) *added = (int64_t)cnt[1];
+        return;
+    }
     auto gpos = [&](const int* cg, double* x) {
         for (int d = 0; d < dim; ++d) x[d] = e.origin[d] + (cg[d] + 0.5) * e.h;
     };
