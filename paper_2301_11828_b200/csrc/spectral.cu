@@ -395,6 +395,17 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
             if (threadIdx.x < nr) xq = land[Q * TR + threadIdx.x];
             __syncthreads();  // the landing area is about to be overwritten by E / O
         } else {
+            if (pf) {
+                // the gather region of the CTA launched pf later into L2: its
+                // Hx + 1 row chunks (TR rows x 16 B each, Nrow apart), one per thread
+                const int64_t nxt = (int64_t)blockIdx.y * gridDim.x + blockIdx.x + pf;
+                const int by = (int)(nxt / gridDim.x), bxx = (int)(nxt % gridDim.x);
+                if (by < (int)gridDim.y) {
+                    const double2* nsrc = S + (int64_t)by * Hx * Nrow + bxx * TR;
+                    for (int c = threadIdx.x; c < Hx; c += blockDim.x)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(nsrc + (int64_t)c * Nrow));
+                }
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int j = j0 + 2 * T * u;
@@ -1662,9 +1673,26 @@ __global__ void __launch_bounds__(512) k_cfft_y_inv(const double2* __restrict__ 
     const int kx = blockIdx.y;
     const int bd = blockIdx.z;
     const int shP = logTWN - (LOGQ + 1);
-    for (int idx = threadIdx.x; idx < Py * nz; idx += blockDim.x) {
-        const int ky = idx / nz, z = idx - ky * nz;
-        sm[(2 * z + (ky & 1)) * XB + spad(ky >> 1)] = S2[(((int64_t)bd * Hx + kx) * Py + ky) * Nz + z0 + z];
+    // the strided gather (runs of nz values per ky): every load of the thread
+    // in flight before the SMEM stores (a full tile is exactly R per thread)
+    {
+        const int tot = Py * nz;
+        const double2* base = S2 + ((int64_t)bd * Hx + kx) * Py * Nz + z0;
+        for (int i0 = 0; i0 < tot; i0 += R * (int)blockDim.x) {
+            double2 g[R];
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+                const int idx = i0 + threadIdx.x + u * (int)blockDim.x;
+                const int ky = idx / nz, z = idx - ky * nz;
+                g[u] = idx < tot ? base[(int64_t)ky * Nz + z] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+                const int idx = i0 + threadIdx.x + u * (int)blockDim.x;
+                const int ky = idx / nz, z = idx - ky * nz;
+                if (idx < tot) sm[(2 * z + (ky & 1)) * XB + spad(ky >> 1)] = g[u];
+            }
+        }
     }
     __syncthreads();
     double2* xb = sm + gi * XB;
@@ -1991,8 +2019,11 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
         }
         return;
     }
+    // gathers (short rows, 3D): prefetch distance PDGPU_K5_GPF (CTAs)
+    const char* gpfenv = getenv("PDGPU_K5_GPF");
+    const int gpf = gpfenv ? atoi(gpfenv) : 0;
 #define PDGPU_K5(LT, C) k_irfft_rows<LQ, LT, C><<<grid, 2 * TR * T, smem, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx, e.d_tw, \
-                                                                          pl.logTWN, scale, cmask, body, pl.nodes, tm, 0)
+                                                                          pl.logTWN, scale, cmask, body, pl.nodes, tm, gpf)
 #define PDGPU_K5C(C) (ltr == 3 ? PDGPU_K5(3, C) : ltr == 2 ? PDGPU_K5(2, C) : ltr == 1 ? PDGPU_K5(1, C) : PDGPU_K5(0, C))
     if (cx) PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(true))
     else PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(false))
