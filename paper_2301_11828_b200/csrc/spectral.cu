@@ -116,12 +116,17 @@ static inline int ilog2(int64_t v) {
 constexpr int kSmemBudget = 210 * 1024;
 
 static int xbuf_slots(int logq) { return (1 << logq) + ((1 << logq) >> 4) + 1; }
+static int threads_per_transform(int logq, int logrmax) { return 1 << std::max(0, logq - logrmax); }
 // TMA-gather / TMA-store row kernels (two rows per CTA): per-transform buffer
 // stride with 2*stride = 4 (mod 8) 16-byte slots, so the two rows' buffers sit
 // 64 bytes apart (mod 128): a quarter-warp spanning both rows hits all 32 banks
 __host__ __device__ constexpr int xbuf_stride_rows(int xb) { return xb + ((2 - (xb & 3)) & 3); }
 static int xbuf_stride_rows_h(int logq) { return xbuf_stride_rows(xbuf_slots(logq)); }
-static int threads_per_transform(int logq, int logrmax) { return 1 << std::max(0, logq - logrmax); }
+// row kernels with T < 8 threads per transform: 8/T transforms share a
+// quarter-warp; per-transform buffers T (mod 8) 16-byte slots apart put them
+// on distinct bank groups (T = 4: the two halves of a quarter-warp 64 B apart)
+__host__ __device__ constexpr int xbuf_stride_t(int xb, int T) { return T >= 8 ? xb : xb + ((T - (xb & 7)) & 7); }
+static int xbuf_stride_t_h(int logq) { return xbuf_stride_t(xbuf_slots(logq), threads_per_transform(logq, 4)); }
 
 // box tensor map over S[slab][kx][row] (complex): dims {2*Nrow doubles, Hx, nslab},
 // box {2*TR doubles, 256 kx, 1}; cuTensorMapEncodeTiled through the runtime's
@@ -239,7 +244,7 @@ __global__ void __launch_bounds__(512) k_rfft_rows(const double* __restrict__ u,
                                                    int Nrow, int Hx, int TR, const double2* __restrict__ tw,
                                                    int logTWN) {
     using Sh = FftShape<LOGQ, 4>;
-    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
+    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = xbuf_stride_t(Sh::XBUF, Sh::T);
     extern __shared__ double2 sm[];
     const int gi = threadIdx.x >> Sh::LOGT;
     const int t = threadIdx.x & (T - 1);
@@ -326,7 +331,7 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
                                                     const __grid_constant__ CUtensorMap tm, int pf) {
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R;
-    constexpr int XB = TMAG ? xbuf_stride_rows(Sh::XBUF) : Sh::XBUF;  // per-transform buffer stride
+    constexpr int XB = TMAG ? xbuf_stride_rows(Sh::XBUF) : xbuf_stride_t(Sh::XBUF, Sh::T);  // per-transform stride
     constexpr int TR = 1 << LOGTR;
     extern __shared__ double2 sm[];
     const int gi = threadIdx.x >> Sh::LOGT;
@@ -700,7 +705,7 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
                                                            int Nx, int Nrow, int nslab, int Hx,
                                                            const double2* __restrict__ tw, int logTWN) {
     using Sh = FftShape<LOGQ, 4>;
-    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
+    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = xbuf_stride_t(Sh::XBUF, Sh::T);
     constexpr int TR = 1 << LOGTR;
     extern __shared__ double2 sm[];
     double* stage = reinterpret_cast<double*>(sm + 2 * TR * XB);  // TR rows x rowlen reals
@@ -1910,7 +1915,7 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
     }
 no_duo:
     const size_t rowlen = (size_t)(cx ? 4 : 2) << lqx;  // staged reals per row
-    auto smem_of = [&](int tr) { return sizeof(double2) * (size_t)2 * tr * xbuf_slots(lqx); };
+    auto smem_of = [&](int tr) { return sizeof(double2) * (size_t)2 * tr * xbuf_stride_t_h(lqx); };
     auto psmem_of = [&](int tr) { return smem_of(tr) + sizeof(double) * (size_t)tr * rowlen; };
     int PTR = TR;  // pipelined kernel: shrink the tile until the staging buffer fits
     while (PTR > 1 && psmem_of(PTR) > 227 * 1024) PTR /= 2;
@@ -1990,7 +1995,7 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
     const int ltr = TR == 8 ? 3 : TR == 4 ? 2 : TR == 2 ? 1 : 0;
     const int T = threads_per_transform(lqx, 4);
     dim3 grid((Ny + TR - 1) / TR, nslab);
-    const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_slots(lqx);
+    const size_t smem = sizeof(double2) * (size_t)2 * TR * xbuf_stride_t_h(lqx);
     CUtensorMap tm;
     memset(&tm, 0, sizeof(tm));
     // L2 prefetch of the TMA-landed block of the CTA launched num_sms later

@@ -1,6 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-for g in 0 148 296 592 1184; do echo "GPF=$g $(PDGPU_K5_GPF=$g timeout 300 python profiles/pass_times.py 256 256 256 --reps 10 2>&1 | tail -1)" >> gpurun_out/ab_passes.txt; done
-for g in 0 592; do echo "GPF=$g $(PDGPU_K5_GPF=$g timeout 300 python profiles/pass_times.py 512 512 --batch 16 --reps 10 2>&1 | tail -1)" >> gpurun_out/ab_passes.txt; done
-for g in 0 592; do echo "GPF=$g $(PDGPU_K5_GPF=$g timeout 300 python profiles/pass_times.py 128 128 128 --reps 10 2>&1 | tail -1)" >> gpurun_out/ab_passes.txt; done
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/ab_t.log 2>&1; echo "rc=$?" >> gpurun_out/ab_t.log
+for d in "256 256 256" "128 128 128" "128 128" "1024 1024"; do timeout 300 python profiles/pass_times.py $d --reps 10 2>&1 | tail -1 >> gpurun_out/ab_passes.txt; done
+timeout 300 python profiles/pass_times.py 512 512 --batch 16 --reps 10 2>&1 | tail -1 >> gpurun_out/ab_passes.txt
+timeout 300 python tools/cg_iter.py >> gpurun_out/ab_passes.txt 2>&1
 echo done
