@@ -121,6 +121,7 @@ void ensure_ledger(Engine& e) {
 
 void upload_surface(Engine& e, const std::vector<long long>& rows, const std::vector<double>& de) {
     touch_state(e);
+    e.surf_default = false;
     e.n_surf = (int64_t)rows.size();
     dalloc(e.d_surf_rows, rows.size(), "alloc surface rows");
     dalloc(e.d_surf_de, de.size(), "alloc surface de");
@@ -368,6 +369,7 @@ void build_surface_device(Engine& e) {
     cuda_check(cudaStreamSynchronize(e.stream), "surface rows");
     cudaFree(d_rowoff);
     e.h_near.clear();
+    e.surf_default = true;
 }
 
 void ensure_h_near(Engine& e) {
@@ -580,12 +582,14 @@ void build_coltab(Engine& e) {
 }
 
 void matvec_impl(Engine& e, const double* u, double* f, int batch, cudaStream_t s) {
+    e.fold_surface_next = true;  // the corrections follow: the 3D face passes may take D^e
     launch_fast_apply(e, u, f, batch, s, 1.0, nullptr, nullptr);
     launch_corrections(e, u, f, batch, s, 1.0);
 }
 
 void evaluate_force_impl(Engine& e, const double* u, double* f, cudaStream_t s) {
     const bool cons = has_constraints(e);
+    e.fold_surface_next = true;
     launch_fast_apply(e, u, f, 1, s, 1.0, cons ? e.d_cmask : nullptr, e.d_body);
     launch_corrections(e, u, f, 1, s, 1.0);
 }
@@ -696,6 +700,7 @@ int pdgpu_create(int dim, const int* dims, int M, const double* stencils, int de
                 std::vector<double> de;
                 assembly::surface_diag(dim, dims, M, e->stencils.data(), e->h_near, rows, de);
                 upload_surface(*e, rows, de);
+                e->surf_default = true;
             } else {
                 build_surface_device(*e);  // D^e and the near-surface rows on the device
             }
@@ -721,7 +726,7 @@ void pdgpu_destroy(pdgpu_t h) {
     if (!h) return;
     cudaSetDevice(h->device);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    void* ptrs[] = {h->d_xstrip, h->d_lidx, h->d_loff, h->d_lK, h->d_sidx, h->d_stab, h->d_vh, h->d_wrows, h->d_wo0, h->d_wK, h->d_tw, h->d_sym, h->d_K, h->d_offs, h->d_disp, h->d_S1, h->d_S2, h->d_u_stage, h->d_f_stage,
+    void* ptrs[] = {h->d_xstrip, h->d_lidx, h->d_loff, h->d_lK, h->d_sidx, h->d_stab, h->d_fidx, h->d_ftab, h->d_vh, h->d_wrows, h->d_wo0, h->d_wK, h->d_tw, h->d_sym, h->d_K, h->d_offs, h->d_disp, h->d_S1, h->d_S2, h->d_u_stage, h->d_f_stage,
                     h->d_cmask, h->d_surf_rows, h->d_surf_de, h->d_ledger, h->d_bond_rows, h->d_listed,
                     h->d_counters, h->d_new_pairs, h->d_body, h->d_cdofs, h->d_cval, h->d_ckind, h->d_u, h->d_v,
                     h->d_f, h->d_fprev, h->d_red, h->d_scal, h->d_ticket, h->d_cg, h->d_coltab,
@@ -1467,6 +1472,7 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
             cudaGraph_t g;
             const int64_t l0 = e.launches;
             cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+            e.fold_surface_next = true;
             launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
             launch_corrections(e, p, q, 1, s, -1.0);
             if (multi) {

@@ -528,6 +528,206 @@ __global__ void __launch_bounds__(128) k_wrap_tab(const double* __restrict__ u, 
     }
 }
 
+// ---- 3D wrap correction as three tiled face passes (every axis periodic,
+// no ghost rows).  Each aliased (node, entry) term is taken by exactly one
+// pass: the x pass takes entries leaving along x, the y pass those leaving
+// along y but not x, the z pass those leaving along z only.  A CTA covers a
+// 32 x 8 tile of the face's node columns (tile axes B fast, C slow) on one
+// side, for the M depths; the M layers of u beyond the opposite face (with an
+// M halo in B and C, wrapped where that axis may wrap in this pass) are staged
+// in SMEM once, so the ~70 entries per column read SMEM instead of L2.  The x
+// pass stages from the x-face strip copy (unit stride along y).  Passes run
+// back to back, each node's row updated by one thread per pass.
+constexpr int kFaceTB = 32, kFaceTC = 8;
+
+template <int A, bool FOLD>
+__global__ void __launch_bounds__(kFaceTB * kFaceTC) k_wrap_face(
+    const double* __restrict__ u, double* __restrict__ f, const int* __restrict__ fidx,
+    const int4* __restrict__ ftab, const double* __restrict__ wK, int M, int N0, int N1, int N2,
+    const uint8_t* __restrict__ cmask, const uint8_t* __restrict__ smask, int64_t nodes, double scale,
+    int nrec_max, const double* __restrict__ xstrip, double* __restrict__ fx) {
+    constexpr int D = 3, KS = 6;
+    extern __shared__ double tile[];  // [layer][comp][c'][b'] (b' fastest), then the records and their K
+    const int NA = A == 0 ? N0 : (A == 1 ? N1 : N2);
+    const int NB = A == 0 ? N1 : N0;
+    const int NC = A == 2 ? N1 : N2;
+    const int side = blockIdx.z & 1, b = blockIdx.z >> 1;
+    const int b0 = blockIdx.x * kFaceTB, c0 = blockIdx.y * kFaceTC;
+    const int WB = kFaceTB + 2 * M, WC = kFaceTC + 2 * M;
+    const int layer_sz = WB * WC;
+    const int tot = M * D * layer_sz;
+    // this pass's entry records (the M depths of one side) and their stencil
+    // values, staged once: every thread of the CTA walks the same list
+    const int r0 = __ldg(fidx + (A * 2 + side) * M), r1 = __ldg(fidx + (A * 2 + side) * M + M);
+    int4* srec = reinterpret_cast<int4*>(tile + tot);
+    double* sK = reinterpret_cast<double*>(srec + nrec_max);
+    for (int e = threadIdx.x; e < r1 - r0; e += blockDim.x) {
+        const int4 r = __ldg(ftab + r0 + e);
+        srec[e] = r;
+#pragma unroll
+        for (int k = 0; k < KS; ++k) sK[e * KS + k] = __ldg(wK + (int64_t)r.w * KS + k);
+    }
+    // the M layers beyond the opposite face, eight loads of a thread in flight
+    // before its SMEM stores; the x pass walks the layers fastest (24
+    // contiguous bytes of a row end), the others the B axis (x)
+    const double* ub = u + (int64_t)b * D * nodes;
+    const int64_t spl = (int64_t)N1 * N2;
+    auto coords = [&](int idx, int& i, int& comp, int& cc, int& bb) {
+        if (A == 0 && !xstrip) {
+            i = idx % M;
+            const int rest = idx / M;
+            bb = rest % WB;
+            const int rest2 = rest / WB;
+            cc = rest2 % WC;
+            comp = rest2 / WC;
+        } else {
+            bb = idx % WB;
+            const int rest = idx / WB;
+            cc = rest % WC;
+            const int rest2 = rest / WC;
+            comp = rest2 % D;
+            i = rest2 / D;
+        }
+    };
+    auto fetch = [&](int i, int comp, int cc, int bb) -> double {
+        int gb = b0 + bb - M, gc = c0 + cc - M;
+        const int ga = side == 0 ? NA - M + i : i;
+        // B wraps in the x pass only (y pass: x stays in range; z pass: x and y do)
+        if (gb < 0 || gb >= NB) {
+            if (A != 0) return 0.0;
+            gb = gb < 0 ? gb + NB : gb - NB;
+        }
+        // C wraps in the x and y passes
+        if (gc < 0 || gc >= NC) {
+            if (A == 2) return 0.0;
+            gc = gc < 0 ? gc + NC : gc - NC;
+        }
+        if (A == 0 && xstrip) {  // the strip K1 wrote: [b][c][slot][z][y], unit stride along y
+            const int slot = ga < 2 * M ? ga : ga - N0 + 4 * M;
+            return xstrip[((int64_t)(b * D + comp) * 4 * M + slot) * spl + (int64_t)gc * N1 + gb];
+        }
+        if (A == 0) return ub[(int64_t)comp * nodes + ((int64_t)gc * N1 + gb) * N0 + ga];
+        if (A == 1) return ub[(int64_t)comp * nodes + ((int64_t)gc * N1 + ga) * N0 + gb];
+        return ub[(int64_t)comp * nodes + ((int64_t)ga * N1 + gc) * N0 + gb];
+    };
+    for (int i0 = threadIdx.x; i0 < tot; i0 += 8 * (int)blockDim.x) {
+        double v[8];
+        int dst[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int idx = i0 + k * (int)blockDim.x;
+            int i = 0, comp = 0, cc = 0, bb = 0;
+            if (idx < tot) coords(idx, i, comp, cc, bb);
+            dst[k] = idx < tot ? ((i * D + comp) * WC + cc) * WB + bb : -1;
+            v[k] = idx < tot ? fetch(i, comp, cc, bb) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (dst[k] >= 0) tile[dst[k]] = v[k];
+    }
+    __syncthreads();
+    const int tb = threadIdx.x % kFaceTB, tc = threadIdx.x / kFaceTB;
+    const int gb = b0 + tb, gc = c0 + tc;
+    if (gb >= NB || gc >= NC) return;
+    for (int l = 0; l < M; ++l) {
+        const int ga = side == 0 ? l : NA - 1 - l;
+        const int x = A == 0 ? ga : gb, y = A == 0 ? gb : (A == 1 ? ga : gc), z = A == 2 ? ga : gc;
+        const int64_t p = ((int64_t)z * N1 + y) * N0 + x;
+        const int e0 = __ldg(fidx + (A * 2 + side) * M + l) - r0, e1 = __ldg(fidx + (A * 2 + side) * M + l + 1) - r0;
+        // FOLD: the surface diagonal D^e (corrections.hpp:24-42) is the sum of
+        // exactly these entries (each taken by one pass), so the passes add
+        // (sum K) u_p in place of k_surface, under the engine's constraint mask
+        double acc[D] = {0.0, 0.0, 0.0};
+        double ds[KS] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
+        for (int e = e0; e < e1; ++e) {
+            const int4 r = srec[e];  // {oB, oC, oA, box}
+            if (A != 0 && (gb + r.x < 0 || gb + r.x >= NB)) continue;  // leaves along x: the x pass's
+            if (A == 2 && (gc + r.y < 0 || gc + r.y >= NC)) continue;  // leaves along y: the y pass's
+            const int i = side == 0 ? l + r.z + M : r.z - l - 1;
+            const double* tp = tile + ((i * D) * WC + (tc + r.y + M)) * WB + (tb + r.x + M);
+            const double2* k2 = reinterpret_cast<const double2*>(sK + e * KS);
+            const double2 ka = k2[0], kb = k2[1], kc = k2[2];
+            const double kv[KS] = {ka.x, ka.y, kb.x, kb.y, kc.x, kc.y};
+            const double uq[3] = {tp[0], tp[layer_sz], tp[2 * layer_sz]};
+            if (FOLD) {
+#pragma unroll
+                for (int k = 0; k < KS; ++k) ds[k] += kv[k];
+            }
+#pragma unroll
+            for (int a = 0; a < D; ++a)
+#pragma unroll
+                for (int bb = 0; bb < D; ++bb) acc[a] += kv[pair_idx<D>(a, bb)] * uq[bb];
+        }
+        const uint8_t cm = cmask ? cmask[p] : 0;
+        const uint8_t sm_ = FOLD && smask ? smask[p] : 0;
+        double up[D] = {0.0, 0.0, 0.0};
+        if (FOLD) {
+            if (A == 0 && xstrip) {  // the node's own values are in the strip too (slot l / 4M-1-l)
+                const int slot = side == 0 ? l : 4 * M - 1 - l;
+#pragma unroll
+                for (int c = 0; c < D; ++c)
+                    up[c] = xstrip[((int64_t)(b * D + c) * 4 * M + slot) * spl + (int64_t)gc * N1 + gb];
+            } else {
+#pragma unroll
+                for (int c = 0; c < D; ++c) up[c] = ub[(int64_t)c * nodes + p];
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < D; ++a) {
+            double dv = 0.0;
+            if ((cm >> a) & 1u) dv = 0.0;
+            else dv = -acc[a];
+            if (FOLD && !((sm_ >> a) & 1u)) {
+                double sa = 0.0;
+#pragma unroll
+                for (int c = 0; c < D; ++c) sa += ds[pair_idx<D>(a, c)] * up[c];
+                dv += sa;
+            }
+            if (A == 0 && fx)  // K5 adds it when it writes the row end: [b][a][z][y][slot 2M]
+                fx[(((int64_t)(b * D + a) * N2 + gc) * N1 + gb) * 2 * M + (side == 0 ? l : 2 * M - 1 - l)] = scale * dv;
+            else
+                f[((int64_t)b * D + a) * nodes + p] += scale * dv;
+        }
+    }
+}
+
+static void build_face_table(Engine& e, const std::vector<int>& rows, const std::vector<int>& o0s) {
+    const Plan& pl = e.plan;
+    const int M = e.M, S = 2 * M + 1;
+    if (e.dim != 3) return;
+    // measured: 256^3 wrap + D^e 0.237 -> 0.161 ms; at 128^3 the per-state
+    // kernel is as fast (0.081 vs 0.083 ms), so the passes start at 192
+    for (int a = 0; a < 3; ++a)
+        if (!pl.circ[a] || pl.N[a] < std::max(S, 192)) return;
+    std::vector<int> fidx;
+    std::vector<int4> ftab;
+    for (int A = 0; A < 3; ++A)
+        for (int side = 0; side < 2; ++side)
+            for (int l = 0; l < M; ++l) {
+                fidx.push_back((int)ftab.size());
+                for (int row = 0; row < S * S; ++row)
+                    for (int ei = rows[2 * row]; ei < rows[2 * row + 1]; ++ei) {
+                        const int o[3] = {o0s[(size_t)ei], row % S - M, row / S - M};
+                        if (!(side == 0 ? o[A] < -l : o[A] > l)) continue;
+                        const int oB = A == 0 ? o[1] : o[0];
+                        const int oC = A == 2 ? o[1] : o[2];
+                        ftab.push_back(make_int4(oB, oC, o[A], ei));
+                    }
+            }
+    fidx.push_back((int)ftab.size());
+    e.face_rec_max = 0;
+    for (int k = 0; k < 6; ++k) e.face_rec_max = std::max(e.face_rec_max, fidx[(size_t)(k + 1) * M] - fidx[(size_t)k * M]);
+    check(cudaMalloc((void**)&e.d_fidx, sizeof(int) * fidx.size()), "alloc face index");
+    check(cudaMemcpy(e.d_fidx, fidx.data(), sizeof(int) * fidx.size(), cudaMemcpyHostToDevice), "copy face index");
+    check(cudaMalloc((void**)&e.d_ftab, sizeof(int4) * ftab.size()), "alloc face table");
+    check(cudaMemcpy(e.d_ftab, ftab.data(), sizeof(int4) * ftab.size(), cudaMemcpyHostToDevice), "copy face table");
+    for (const void* fn : {(const void*)k_wrap_face<0, false>, (const void*)k_wrap_face<1, false>,
+                           (const void*)k_wrap_face<2, false>, (const void*)k_wrap_face<0, true>,
+                           (const void*)k_wrap_face<1, true>, (const void*)k_wrap_face<2, true>})
+        check(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024), "face smem");
+}
+
 // per-state lists for k_wrap_tab (engine.h d_sidx / d_stab); entry ids index
 // the d_wK table built below (same storage order)
 static void build_state_table(Engine& e, const std::vector<int>& rows, const std::vector<int>& o0s) {
@@ -651,6 +851,7 @@ void build_wrap_table(Engine& e) {
     up((void**)&e.d_loff, loff.data(), sizeof(int) * loff.size());
     up((void**)&e.d_lK, lk.data(), sizeof(double) * lk.size());
     if (!getenv("PDGPU_WRAP_GENERIC")) build_state_table(e, rows, o0s);
+    if (!getenv("PDGPU_WRAP_GENERIC") && !getenv("PDGPU_WRAP_NOFACE")) build_face_table(e, rows, o0s);
 }
 
 void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
@@ -673,11 +874,45 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
     const int th = 128;
     const unsigned blocks = (unsigned)((tot + th - 1) / th);
     const double* xstrip = nullptr;
-    if (pl.dim == 3 && pl.circ[0] && e.d_xstrip && batch <= e.cap_batch && 4 * e.M <= pl.N[0]) {
+    if (pl.dim == 3 && pl.circ[0] && e.d_xstrip && batch <= e.cap_batch && 4 * e.M <= pl.N[0] &&
+        !(e.d_ftab && !ghost && e.slab.global < 0)) {
         const int64_t nrows = (int64_t)batch * 3 * pl.N[1] * pl.N[2];
         k_xstrip<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(u, e.d_xstrip, pl.N[0], pl.N[1], pl.N[2], e.M, nrows);
         xstrip = e.d_xstrip;
         e.launches += 1;
+    }
+    if (e.d_ftab && !ghost && e.slab.global < 0) {  // 3D, every axis periodic: three tiled face passes
+        const int M = e.M;
+        const size_t smem = sizeof(double) * (size_t)M * 3 * (kFaceTB + 2 * M) * (kFaceTC + 2 * M) +
+                            (sizeof(int4) + 6 * sizeof(double)) * (size_t)e.face_rec_max;
+        const int* N = pl.N;
+        const dim3 g0((N[1] + kFaceTB - 1) / kFaceTB, (N[2] + kFaceTC - 1) / kFaceTC, 2 * batch);
+        const dim3 g1((N[0] + kFaceTB - 1) / kFaceTB, (N[2] + kFaceTC - 1) / kFaceTC, 2 * batch);
+        const dim3 g2((N[0] + kFaceTB - 1) / kFaceTB, (N[1] + kFaceTC - 1) / kFaceTC, 2 * batch);
+        const int th = kFaceTB * kFaceTC;
+        // the surface diagonal folds in when the caller adds the corrections
+        // right after (matvec / evaluate_force / CG) and D^e is the lattice's own
+        const bool fold = e.fold_surface_next && e.surf_default;
+        if (fold) e.surface_folded = true;
+        const double* xs = e.xstrip_ready ? e.d_xstrip : nullptr;  // written by this K.u's K1
+        e.xstrip_ready = false;
+#define PDGPU_WF(AX, G, FD)                                                                                         \
+    k_wrap_face<AX, FD><<<G, th, smem, s>>>(u, f, e.d_fidx, e.d_ftab, e.d_wK, M, N[0], N[1], N[2], cmask, e.d_cmask, \
+                                            pl.nodes, scale, e.face_rec_max, AX == 0 ? xs : nullptr, nullptr)
+        const bool xdone = e.xpass_done;  // the x pass ran before K5 (launch_wrap_xpass)
+        e.xpass_done = false;
+        if (fold) {
+            if (!xdone) PDGPU_WF(0, g0, true);
+            PDGPU_WF(1, g1, true);
+            PDGPU_WF(2, g2, true);
+        } else {
+            if (!xdone) PDGPU_WF(0, g0, false);
+            PDGPU_WF(1, g1, false);
+            PDGPU_WF(2, g2, false);
+        }
+#undef PDGPU_WF
+        e.launches += xdone ? 1 : 2;  // the caller counts one
+        return;
     }
     if (e.d_stab) {  // per-state lists (every band node)
         // few band nodes (small lattices, latency-bound): four lanes per node
@@ -709,9 +944,43 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
                                         e.d_loff, e.d_lK, xstrip);
 }
 
+// 3D face path, before K5: the x pass into d_fx (needs the strip K1 wrote);
+// returns true when it ran (K5 then adds d_fx at the row ends)
+bool launch_wrap_xpass(Engine& e, const double* u, int batch, cudaStream_t s, double scale, const uint8_t* cmask) {
+    const Plan& pl = e.plan;
+    e.xpass_done = false;
+    // opt-in (PDGPU_XFOLD=1): the x pass's f writes leave the wrap, but K5's
+    // row-end reads of d_fx put a dependent load at the end of every K5 CTA:
+    // measured 256^3 x pass 70 -> 46 us, K5 0.211 -> 0.250 ms, net slower
+    const char* xf = getenv("PDGPU_XFOLD");
+    if (!(xf && xf[0] == '1') ||
+        !(e.d_ftab && e.d_fx && e.xstrip_ready && e.slab.global < 0 && !e.ghost_view && batch <= e.cap_batch))
+        return false;
+    const int M = e.M;
+    const size_t smem = sizeof(double) * (size_t)M * 3 * (kFaceTB + 2 * M) * (kFaceTC + 2 * M) +
+                        (sizeof(int4) + 6 * sizeof(double)) * (size_t)e.face_rec_max;
+    const int* N = pl.N;
+    const dim3 g0((N[1] + kFaceTB - 1) / kFaceTB, (N[2] + kFaceTC - 1) / kFaceTC, 2 * batch);
+    const bool fold = e.fold_surface_next && e.surf_default;
+    if (fold)
+        k_wrap_face<0, true><<<g0, kFaceTB * kFaceTC, smem, s>>>(u, nullptr, e.d_fidx, e.d_ftab, e.d_wK, M, N[0], N[1],
+                                                                 N[2], cmask, e.d_cmask, pl.nodes, scale,
+                                                                 e.face_rec_max, e.d_xstrip, e.d_fx);
+    else
+        k_wrap_face<0, false><<<g0, kFaceTB * kFaceTC, smem, s>>>(u, nullptr, e.d_fidx, e.d_ftab, e.d_wK, M, N[0],
+                                                                  N[1], N[2], cmask, e.d_cmask, pl.nodes, scale,
+                                                                  e.face_rec_max, e.d_xstrip, e.d_fx);
+    e.launches += 1;
+    e.xpass_done = true;
+    return true;
+}
+
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale) {
     const int64_t N = e.plan.nodes;
-    if (e.n_surf > 0) {
+    const bool folded = e.surface_folded;  // D^e already added by the face passes of this K.u
+    e.surface_folded = false;
+    e.fold_surface_next = false;
+    if (e.n_surf > 0 && !folded) {
         PassTimer pt(e, kPassCorr, s);
         const int64_t tot = e.n_surf * batch;
         const int th = 256;

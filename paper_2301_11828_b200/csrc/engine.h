@@ -95,6 +95,22 @@ struct Engine {
     // bits 8-31).  Empty (d_stab null) when an axis is shorter than 2M + 1.
     int* d_sidx = nullptr;
     int4* d_stab = nullptr;
+    // 3D face passes (k_wrap_face, every axis periodic, no ghost rows): per
+    // (axis, side, depth) the entries whose offset along that axis leaves the
+    // lattice, {o_B, o_C, o_A, box entry} with (B, C) the tile axes of the
+    // pass; d_fidx[(axis*2+side)*M+depth] = first record (one end slot)
+    int* d_fidx = nullptr;
+    int4* d_ftab = nullptr;
+    int face_rec_max = 0;
+    // D^e is the lattice's own (no set_surface_diag / set_regions / slab);
+    // fold_surface_next: the caller adds the corrections right after this
+    // K.u, so the face passes may take D^e (surface_folded: they did)
+    bool surf_default = false, fold_surface_next = false, surface_folded = false;
+    bool xstrip_ready = false;  // K1 of this K.u wrote d_xstrip (3D face passes read it)
+    // 3D face passes: the x pass runs before K5 and leaves its per-node result
+    // in d_fx ([b][c][slot 2M][z][y]); K5 adds it at the row ends it writes
+    double* d_fx = nullptr;
+    bool xpass_done = false;
     double* d_kc = nullptr;         // centre coefficients (3D direct stencil)
     double* d_coltab = nullptr;     // separable symbol: per column n_pairs x (M+1) coefficients (2D)
     int coltab_oddmask = 0;         // bit p: pair p odd along the column axis (sin terms)
@@ -273,6 +289,7 @@ void launch_direct_apply(Engine& e, const double* u, double* f, int batch, cudaS
 void build_wrap_table(Engine& e);
 void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
                             const uint8_t* cmask);
+bool launch_wrap_xpass(Engine& e, const double* u, int batch, cudaStream_t s, double scale, const uint8_t* cmask);
 void launch_corrections(Engine& e, const double* u, double* f, int batch, cudaStream_t s,
                         double scale);
 void launch_merge_face(Engine& e, const uint32_t* recv, cudaStream_t s);

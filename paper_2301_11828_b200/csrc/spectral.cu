@@ -328,7 +328,8 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
                                                     const double2* __restrict__ tw, int logTWN, double scale,
                                                     const uint8_t* __restrict__ cmask,
                                                     const double* __restrict__ body, int64_t nodes,
-                                                    const __grid_constant__ CUtensorMap tm, int pf) {
+                                                    const __grid_constant__ CUtensorMap tm, int pf,
+                                                    const double* __restrict__ fx, int Mfx) {
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R;
     constexpr int XB = TMAG ? xbuf_stride_rows(Sh::XBUF) : xbuf_stride_t(Sh::XBUF, Sh::T);  // per-transform stride
@@ -489,6 +490,16 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
         if (cmask) {
             if ((cmask[node] >> a) & 1u) v0 = 0.0;
             if (two && ((cmask[node + 1] >> a) & 1u)) v1 = 0.0;
+        }
+        if (fx && (i0 < Mfx || i0 + 1 >= Nx - Mfx)) {  // 3D: the wrap x pass's result at the row ends
+            // fx[b][a][z][y][slot 2M]: the row's 2M values are contiguous
+            const double* fr = fx + ((int64_t)(slab / Nz) * Nz * Nrow + (int64_t)z * Nrow + row0 + rr) * 2 * Mfx;
+            if (i0 < Mfx) v0 += fr[i0];
+            else if (i0 >= Nx - Mfx) v0 += fr[Mfx + i0 - (Nx - Mfx)];
+            if (two) {
+                if (i0 + 1 < Mfx) v1 += fr[i0 + 1];
+                else if (i0 + 1 >= Nx - Mfx) v1 += fr[Mfx + i0 + 1 - (Nx - Mfx)];
+            }
         }
         double* o = dst + (int64_t)rr * Nx + i0;
         if (vec) {
@@ -703,7 +714,8 @@ __global__ void __launch_bounds__(256, NH == 1 ? 2 : 1) k_spectral(const double2
 template <int LOGQ, int LOGTR, bool CIRC>
 __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restrict__ u, double2* __restrict__ S,
                                                            int Nx, int Nrow, int nslab, int Hx,
-                                                           const double2* __restrict__ tw, int logTWN) {
+                                                           const double2* __restrict__ tw, int logTWN,
+                                                           double* __restrict__ xstrip, int M, int Nz) {
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = xbuf_stride_t(Sh::XBUF, Sh::T);
     constexpr int TR = 1 << LOGTR;
@@ -739,9 +751,6 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
     // (distinct banks for the 16-byte loads) and each warp store still fills
     // whole 32-byte sectors along rr.  W(2a) = e^{-2 pi i 2a/Px} =
     // W(2a0) e^{-2 pi i u/R}: two table reads per thread, hoisted.
-    // post-processing thread map: a quarter-warp covers 8 consecutive kx of one
-    // row; with TSTORE (two rows) 4 consecutive kx of both rows, so that its
-    // [kx][row] block writes land on 8 distinct 16-byte bank groups (below)
     constexpr int LA = (2 * T >= 8) ? 3 : 0;  // tiny transforms: rr fastest
     const int rr = (threadIdx.x >> LA) & (TR - 1);
     const int a0 = ((threadIdx.x >> (LA + LOGTR)) << LA) + (threadIdx.x & ((1 << LA) - 1));
@@ -756,6 +765,16 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
         double2 v[R];
         cp_async_wait_all();
         __syncthreads();
+        if (xstrip) {
+            // 3D: the 2M-wide row ends into the x-face strip [b][c][slot][z][y]
+            // (slot x, or 2M + x - (Nx - 2M)) for the wrap correction's x pass
+            const int S4 = 4 * M, bc = slab / Nz, z = slab - bc * Nz;
+            for (int idx = threadIdx.x; idx < nr * S4; idx += blockDim.x) {
+                const int rr2 = idx / S4, sl = idx - rr2 * S4;
+                const int x = sl < 2 * M ? sl : Nx - 4 * M + sl;
+                xstrip[(((int64_t)bc * S4 + sl) * Nz + z) * Nrow + row0 + rr2] = stage[rr2 * rowlen + x];
+            }
+        }
 #pragma unroll
         for (int j = 0; j < R; ++j) {
             const int n = t + j * T;
@@ -1864,6 +1883,7 @@ void set_attrs_k1() { set_attrs_k1_all(std::make_integer_sequence<int, 12>{}); }
 
 void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
     const Plan& pl = e.plan;
+    e.xstrip_ready = false;  // set below when this pass writes the x-face strip
     const int Nx = pl.N[0], Ny = pl.N[1], Nz = pl.N[2];
     const int nslab = batch * pl.dim * Nz;
     const int lqx = pl.logQx;
@@ -1928,8 +1948,14 @@ no_duo:
         const int per_sm = std::max(1, std::min((int)(228 * 1024 / (psmem + 1024)), 65536 / (2 * PTR * T * 128)));
         const unsigned pgrid = (unsigned)std::min<int64_t>(ntiles, (int64_t)e.num_sms * per_sm);
         const int ltr = PTR == 8 ? 3 : PTR == 4 ? 2 : PTR == 2 ? 1 : 0;
+        // 3D with the tiled wrap passes: the x-face strip comes out of this pass
+        double* xs = (pl.dim == 3 && e.d_ftab && pl.circ[0] && e.d_xstrip && batch <= e.cap_batch &&
+                      e.slab.global < 0 && 4 * e.M <= Nx)
+                         ? e.d_xstrip
+                         : nullptr;
+        e.xstrip_ready = xs != nullptr;
 #define PDGPU_K1P(LT, C) k_rfft_rows_pipe<LQ, LT, C><<<pgrid, 2 * PTR * T, psmem, s>>>(u, e.d_S1, Nx, Ny, nslab, \
-                                                                                pl.Hx, e.d_tw, pl.logTWN)
+                                                                                pl.Hx, e.d_tw, pl.logTWN, xs, e.M, Nz)
 #define PDGPU_K1PC(C) (ltr == 3 ? PDGPU_K1P(3, C) : ltr == 2 ? PDGPU_K1P(2, C) : ltr == 1 ? PDGPU_K1P(1, C) \
                                                                                  : PDGPU_K1P(0, C))
         if (cx) PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K1PC(true))
@@ -1967,6 +1993,7 @@ void set_attrs_k5() { set_attrs_k5_all(std::make_integer_sequence<int, 12>{}); }
 
 void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t s, double scale,
                const uint8_t* cmask, const double* body) {
+    const double* fxs = e.xpass_done ? e.d_fx : nullptr;  // the wrap x pass ran before this pass
     const Plan& pl = e.plan;
     const int Nx = pl.N[0], Ny = pl.N[1], Nz = pl.N[2], d = pl.dim;
     const int nslab = batch * d * Nz;
@@ -2011,15 +2038,15 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
                                     sizeof(double2) * (size_t)nbox * 256 * TR) + 128;
         switch (lqx) {
             PDGPU_CASE(8, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M)))
             PDGPU_CASE(9, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M)))
             PDGPU_CASE(10, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M)))
             PDGPU_CASE(11, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M)))
             PDGPU_CASE(12, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M)))
             default: break;
         }
         return;
@@ -2028,7 +2055,8 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
     const char* gpfenv = getenv("PDGPU_K5_GPF");
     const int gpf = gpfenv ? atoi(gpfenv) : 0;
 #define PDGPU_K5(LT, C) k_irfft_rows<LQ, LT, C><<<grid, 2 * TR * T, smem, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx, e.d_tw, \
-                                                                          pl.logTWN, scale, cmask, body, pl.nodes, tm, gpf)
+                                                                          pl.logTWN, scale, cmask, body, pl.nodes, tm, gpf, \
+                                                                          fxs, e.M)
 #define PDGPU_K5C(C) (ltr == 3 ? PDGPU_K5(3, C) : ltr == 2 ? PDGPU_K5(2, C) : ltr == 1 ? PDGPU_K5(1, C) : PDGPU_K5(0, C))
     if (cx) PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(true))
     else PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(false))
@@ -2309,9 +2337,13 @@ void engine_alloc_workspace(Engine& e, int64_t batch) {
     check(cudaMalloc(&e.d_S1, sizeof(double2) * pl.S1_per_vec * batch), "alloc S1");
     if (pl.S2_per_vec) check(cudaMalloc(&e.d_S2, sizeof(double2) * pl.S2_per_vec * batch), "alloc S2");
     if (e.d_xstrip) cudaFree(e.d_xstrip);
+    if (e.d_fx) cudaFree(e.d_fx);
     e.d_xstrip = nullptr;
-    if (pl.dim == 3 && pl.circ[0])  // 4M x-values per (y, z) row and component
+    e.d_fx = nullptr;
+    if (pl.dim == 3 && pl.circ[0]) {  // 4M x-values per (y, z) row and component; 2M x-pass results
         check(cudaMalloc(&e.d_xstrip, sizeof(double) * (size_t)batch * 3 * 4 * e.M * pl.N[1] * pl.N[2]), "alloc strip");
+        check(cudaMalloc(&e.d_fx, sizeof(double) * (size_t)batch * 3 * 2 * e.M * pl.N[1] * pl.N[2]), "alloc fx");
+    }
     e.cap_batch = batch;
 }
 
@@ -2352,6 +2384,10 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
     if (d == 3) {
         PassTimer pt(e, kPassK4, s);
         launch_k4_3d(e, batch, s);
+    }
+    if (d == 3 && (pl.circ_mask || e.ghost_view)) {  // 3D face path: the wrap x pass feeds K5's epilogue
+        PassTimer pt(e, kPassCorr, s);
+        launch_wrap_xpass(e, u, batch, s, scale, cmask);
     }
     {
         PassTimer pt(e, kPassK5, s);
