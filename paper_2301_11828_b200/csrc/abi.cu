@@ -1421,6 +1421,15 @@ int pdgpu_constraint_values(pdgpu_t h, uint8_t* mask, double* uc) {
 }
 
 // ------------------------------------------------------------------ CG ---
+// CG iterations per captured graph: small systems replay several per launch
+// (the host's graph-launch cadence would otherwise bound the iteration rate);
+// iterations past convergence find the done flag and update nothing.  The
+// slab (NCCL) path keeps one.
+static int cg_iters_per_graph(const Engine& e, int64_t m) {
+    if (const char* env = getenv("PDGPU_CG_IPG")) return std::max(1, atoi(env));
+    return (m <= (1 << 21) && !comm_attached(e)) ? 8 : 1;
+}
+
 static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit, int* iters, double* relres,
                     cudaStream_t s, double* hist_host, int nhist) {
     const int64_t N = e.plan.nodes, m = (int64_t)e.dim * N;
@@ -1472,16 +1481,18 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
             cudaGraph_t g;
             const int64_t l0 = e.launches;
             cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
-            e.fold_surface_next = true;
-            launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
-            launch_corrections(e, p, q, 1, s, -1.0);
-            if (multi) {
-                launch_dot(e, p, q, m, e.d_scal + 1, s);
-                comm_allreduce(e, e.d_scal + 1, 1, s);
-                launch_cg_step_dev_comm(e, x, r, p, q, m, e.d_scal, s);
-            } else if (!launch_cg_fused(e, x, r, p, q, m, e.d_scal, s)) {  // one cooperative kernel
-                launch_dot(e, p, q, m, e.d_scal + 1, s);
-                launch_cg_step_dev(e, x, r, p, q, m, e.d_scal, s);
+            for (int rep = 0; rep < cg_iters_per_graph(e, m); ++rep) {
+                e.fold_surface_next = true;
+                launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
+                launch_corrections(e, p, q, 1, s, -1.0);
+                if (multi) {
+                    launch_dot(e, p, q, m, e.d_scal + 1, s);
+                    comm_allreduce(e, e.d_scal + 1, 1, s);
+                    launch_cg_step_dev_comm(e, x, r, p, q, m, e.d_scal, s);
+                } else if (!launch_cg_fused(e, x, r, p, q, m, e.d_scal, s)) {  // one cooperative kernel
+                    launch_dot(e, p, q, m, e.d_scal + 1, s);
+                    launch_cg_step_dev(e, x, r, p, q, m, e.d_scal, s);
+                }
             }
             cuda_check(cudaStreamEndCapture(s, &g), "end capture");
             e.cg_graph_launches = e.launches - l0;  // kernels per replay (capture itself launches none)
@@ -1493,15 +1504,16 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
             e.cg_graph_version = e.state_version;
         }
         e.timing = timing;
-        const double init[6] = {rr0, 0.0, rr0, tol * tol * rr0, 0.0, 0.0};
+        const double init[7] = {rr0, 0.0, rr0, tol * tol * rr0, 0.0, 0.0, (double)maxit};  // [6]: iteration cap
         cuda_check(cudaMemcpyAsync(e.d_scal, init, sizeof(init), cudaMemcpyHostToDevice, s), "scal init");
         double st[6] = {0, 0, 0, 0, 0, 0};
         int launched = 0;
+        const int ipg = cg_iters_per_graph(e, m);
         const int chunk = m > (1 << 22) ? 4 : 16;
         while (launched < maxit) {
-            const int nl = std::min(chunk, maxit - launched);
+            const int nl = std::min(chunk, (maxit - launched + ipg - 1) / ipg);
             for (int i = 0; i < nl; ++i) cuda_check(cudaGraphLaunch(e.cg_graph, s), "graph launch");
-            launched += nl;
+            launched += nl * ipg;
             e.launches += (int64_t)nl * e.cg_graph_launches;
             cuda_check(cudaMemcpyAsync(st, e.d_scal, sizeof(st), cudaMemcpyDeviceToHost, s), "read scal");
             cuda_check(cudaStreamSynchronize(s), "cg chunk");

@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(128) k_wrap(const double* __restrict__ u, doub
 // list of the entries that leave the lattice from its position class, with
 // the wrapped displacement stored -- no per-row bookkeeping, independent loads
 // (unrolled), and the ghost-row terms of halo slabs in the same pass.
-template <int D, int LPN>
+template <int D, int LPN, bool FOLD = false>
 __global__ void __launch_bounds__(128) k_wrap_tab(const double* __restrict__ u, double* __restrict__ f,
                                                   const int* __restrict__ sidx, const int4* __restrict__ stab,
                                                   const double* __restrict__ wK, int M, int N0, int N1, int N2,
@@ -406,9 +406,14 @@ __global__ void __launch_bounds__(128) k_wrap_tab(const double* __restrict__ u, 
                                                   int batch, double scale, int64_t band0, int64_t band1,
                                                   int64_t band2, const double* __restrict__ ghost, int64_t gs_bc,
                                                   int64_t gs_side, int lo_int, int hi_int,
-                                                  const double* __restrict__ xstrip) {
+                                                  const double* __restrict__ xstrip,
+                                                  const uint8_t* __restrict__ smask) {
     constexpr int NP = D * (D + 1) / 2;
     constexpr int KS = (NP + 1) & ~1;
+    // FOLD (every axis periodic, the lattice's own D^e, corrections follow):
+    // the node's aliased entries are exactly the offsets that leave the
+    // lattice, whose kernel sum is D^e (corrections.hpp:24-42), so this pass
+    // also adds D^e u_p under the surface mask and k_surface is skipped
     // LPN lanes per node (a quad of consecutive lanes), entries strided over them
     const int64_t per_vec = band0 + band1 + band2;
     const int64_t gidx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / LPN;
@@ -461,9 +466,11 @@ __global__ void __launch_bounds__(128) k_wrap_tab(const double* __restrict__ u, 
     const double* sb = strip ? xstrip + (int64_t)b * D * 4 * M * spl : nullptr;
     const int64_t plane = D == 3 ? (int64_t)N0 * N1 : N0;
     const int64_t pin = D == 3 ? (int64_t)c1 * N0 + c0 : c0;  // in-plane index of p
-    double acc[D], gacc[D];
+    double acc[D], gacc[D], ds[NP];
 #pragma unroll
     for (int a = 0; a < D; ++a) acc[a] = gacc[a] = 0.0;
+#pragma unroll
+    for (int k = 0; k < NP; ++k) ds[k] = 0.0;
     const int e0 = __ldg(sidx + state), e1 = __ldg(sidx + state + 1);
 #pragma unroll 4
     for (int e = e0 + sub; e < e1; e += LPN) {
@@ -495,6 +502,10 @@ __global__ void __launch_bounds__(128) k_wrap_tab(const double* __restrict__ u, 
             for (int a = 0; a < D; ++a)
 #pragma unroll
                 for (int bb = 0; bb < D; ++bb) acc[a] += kv[pair_idx<D>(a, bb)] * uq[bb];
+            if (FOLD) {
+#pragma unroll
+                for (int k = 0; k < NP; ++k) ds[k] += kv[k];
+            }
         }
         if ((fl & 2) && ghost) {
             const int sd = (fl >> 2) & 1;
@@ -513,18 +524,35 @@ __global__ void __launch_bounds__(128) k_wrap_tab(const double* __restrict__ u, 
     if (LPN > 1) {  // the node's lanes: consecutive, all alive (the early returns are per node)
         const unsigned qm = ((1u << LPN) - 1u) << ((threadIdx.x & 31) & ~(LPN - 1));
 #pragma unroll
-        for (int o = 1; o < LPN; o <<= 1)
+        for (int o = 1; o < LPN; o <<= 1) {
 #pragma unroll
             for (int a = 0; a < D; ++a) {
                 acc[a] += __shfl_xor_sync(qm, acc[a], o);
                 gacc[a] += __shfl_xor_sync(qm, gacc[a], o);
             }
+            if (FOLD) {
+#pragma unroll
+                for (int k = 0; k < NP; ++k) ds[k] += __shfl_xor_sync(qm, ds[k], o);
+            }
+        }
         if (sub) return;
+    }
+    const uint8_t smk = FOLD && smask ? smask[p] : 0;
+    double up[D];
+    if (FOLD) {
+#pragma unroll
+        for (int c = 0; c < D; ++c) up[c] = ub[(int64_t)c * nodes];
     }
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-        if ((cm >> a) & 1u) continue;
-        f[((int64_t)b * D + a) * nodes + p] += scale * (gacc[a] - acc[a]);
+        double dv = ((cm >> a) & 1u) ? 0.0 : gacc[a] - acc[a];
+        if (FOLD && !((smk >> a) & 1u)) {
+            double sa = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) sa += ds[pair_idx<D>(a, c)] * up[c];
+            dv += sa;
+        }
+        f[((int64_t)b * D + a) * nodes + p] += scale * dv;
     }
 }
 
@@ -918,16 +946,31 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
         // few band nodes (small lattices, latency-bound): four lanes per node
         const bool quad = tot < (int64_t)e.num_sms * 256;
         const unsigned tb = (unsigned)((tot * (quad ? 4 : 1) + th - 1) / th);
-#define PDGPU_WT(D, L, XS)                                                                                       \
-    k_wrap_tab<D, L><<<tb, th, 0, s>>>(u, f, e.d_sidx, e.d_stab, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2], pl.circ_mask, \
-                                       cmask, pl.nodes, batch, scale, band[0], band[1], band[2], ghost,              \
-                                       e.ghost_bc_stride, e.ghost_side_stride, lo_int, hi_int, XS)
+        // D^e folds in when every axis is periodic (the band is then exactly
+        // the near-surface set) and the corrections follow this K.u
+        const bool fold = e.fold_surface_next && e.surf_default && !ghost && e.slab.global < 0 &&
+                          pl.circ_mask == (1 << pl.dim) - 1;
+        if (fold) e.surface_folded = true;
+#define PDGPU_WT(D, L, FD, XS)                                                                                        \
+    k_wrap_tab<D, L, FD><<<tb, th, 0, s>>>(u, f, e.d_sidx, e.d_stab, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],          \
+                                           pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2],    \
+                                           ghost, e.ghost_bc_stride, e.ghost_side_stride, lo_int, hi_int, XS, e.d_cmask)
         if (pl.dim == 2) {
-            if (quad) PDGPU_WT(2, 4, nullptr);
-            else PDGPU_WT(2, 1, nullptr);
+            if (quad) {
+                if (fold) PDGPU_WT(2, 4, true, nullptr);
+                else PDGPU_WT(2, 4, false, nullptr);
+            } else {
+                if (fold) PDGPU_WT(2, 1, true, nullptr);
+                else PDGPU_WT(2, 1, false, nullptr);
+            }
         } else {
-            if (quad) PDGPU_WT(3, 4, xstrip);
-            else PDGPU_WT(3, 1, xstrip);
+            if (quad) {
+                if (fold) PDGPU_WT(3, 4, true, xstrip);
+                else PDGPU_WT(3, 4, false, xstrip);
+            } else {
+                if (fold) PDGPU_WT(3, 1, true, xstrip);
+                else PDGPU_WT(3, 1, false, xstrip);
+            }
         }
 #undef PDGPU_WT
         return;

@@ -7,6 +7,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
@@ -151,7 +153,7 @@ __global__ void k_cg_update_dev(double* __restrict__ x, double* __restrict__ r, 
         scal[0] = tot;
         scal[2] = tot;
         scal[5] += 1.0;
-        if (tot <= scal[3]) scal[4] = 1.0;
+        if (tot <= scal[3] || scal[5] >= scal[6]) scal[4] = 1.0;  // converged, or the iteration cap
     });
 }
 
@@ -256,7 +258,7 @@ __global__ void __launch_bounds__(kRedThreads) k_cg_fused(double* __restrict__ x
         scal[0] = rrn;
         scal[2] = rrn;
         scal[5] += 1.0;
-        if (rrn <= thr) scal[4] = 1.0;
+        if (rrn <= thr || scal[5] >= scal[6]) scal[4] = 1.0;  // converged, or the iteration cap
     }
     if (rrn <= thr) return;
     const double beta = rrn / rr;
@@ -277,7 +279,12 @@ bool launch_cg_fused(Engine& e, double* x, double* r, double* p, const double* q
     }
     if (!ok) return false;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kRedBlocks);
+    // small systems: one block per SM (cheaper grid barriers and totals);
+    // the reduction order is fixed by the grid, so results are deterministic
+    const char* genv = getenv("PDGPU_CG_GRID");
+    const int grid = genv ? std::max(1, std::min(kRedBlocks, atoi(genv)))
+                          : (n <= (int64_t)e.num_sms * kRedThreads * 16 ? e.num_sms : kRedBlocks);
+    cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kRedThreads);
     cfg.stream = s;
     cudaLaunchAttribute at[1];
