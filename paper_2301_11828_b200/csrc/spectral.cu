@@ -1496,8 +1496,8 @@ __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.
 // it (the park is in TMEM), so the next item's x_0 is requested a whole item
 // ahead; the exchange then uses 8-byte slots (split real/imaginary) to keep
 // two CTAs per SM.
-template <int LOGQ, int SYM, bool LAND>
-__global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_tm(const double2* __restrict__ in, double2* out,
+template <int LOGQ, int SYM, bool LAND, int CPS = 2>
+__global__ void __launch_bounds__(kPipeThreads, CPS) k_spectral2d_tm(const double2* __restrict__ in, double2* out,
                                                                   const void* __restrict__ sym, int ncols, int NC,
                                                                   int batch, const double2* __restrict__ tw,
                                                                   int logTWN) {
@@ -2079,6 +2079,7 @@ static void set_attrs_k3_l() {
     if constexpr (L == 11 || L == 12) {
         smem_attr((const void*)k_spectral2d_tm<L, 0, false>);
         smem_attr((const void*)k_spectral2d_tm<L, 1, false>);
+        smem_attr((const void*)k_spectral2d_tm<L, 1, false, 3>);
         smem_attr((const void*)k_spectral2d_tm<L, 0, true>);
         smem_attr((const void*)k_spectral2d_tm<L, 1, true>);
     }
@@ -2128,7 +2129,11 @@ void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s) {
 #define TM_L(LQV, LANDV)                                                                          \
     (mode == 1 ? k_spectral2d_tm<LQV, 1, LANDV><<<tgrid, kPipeThreads, tsmem, s>>>(TM_ARGS)       \
                : k_spectral2d_tm<LQV, 0, LANDV><<<tgrid, kPipeThreads, tsmem, s>>>(TM_ARGS))
-        if (lq == 12) {
+        const char* t3 = getenv("PDGPU_K3_TM3");  // three CTAs per SM (80 registers, spills)
+        if (lq == 12 && mode == 1 && !land && t3 && t3[0] == '1') {
+            const unsigned g3 = (unsigned)std::min<int64_t>(nitems, (int64_t)e.num_sms * 3);
+            k_spectral2d_tm<12, 1, false, 3><<<g3, kPipeThreads, tsmem, s>>>(TM_ARGS);
+        } else if (lq == 12) {
             if (land) TM_L(12, true);
             else TM_L(12, false);
         } else {
