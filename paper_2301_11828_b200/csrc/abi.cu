@@ -1481,6 +1481,9 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
             cudaGraph_t g;
             const int64_t l0 = e.launches;
             cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+            // small systems: programmatic dependent launch between the latency-bound kernels
+            const char* pdlenv = getenv("PDGPU_PDL");
+            e.pdl = pdlenv && pdlenv[0] == '1';  // opt-in: measured neutral (32.1 vs 32.5 us at 128^2)
             for (int rep = 0; rep < cg_iters_per_graph(e, m); ++rep) {
                 e.fold_surface_next = true;
                 launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
@@ -1494,6 +1497,7 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
                     launch_cg_step_dev(e, x, r, p, q, m, e.d_scal, s);
                 }
             }
+            e.pdl = false;
             cuda_check(cudaStreamEndCapture(s, &g), "end capture");
             e.cg_graph_launches = e.launches - l0;  // kernels per replay (capture itself launches none)
             e.launches = l0;

@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(128) k_wrap_tab(const double* __restrict__ u, 
                                                   int64_t gs_side, int lo_int, int hi_int,
                                                   const double* __restrict__ xstrip,
                                                   const uint8_t* __restrict__ smask) {
+    pdl_entry();
     constexpr int NP = D * (D + 1) / 2;
     constexpr int KS = (NP + 1) & ~1;
     // FOLD (every axis periodic, the lattice's own D^e, corrections follow):
@@ -952,9 +953,9 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
                           pl.circ_mask == (1 << pl.dim) - 1;
         if (fold) e.surface_folded = true;
 #define PDGPU_WT(D, L, FD, XS)                                                                                        \
-    k_wrap_tab<D, L, FD><<<tb, th, 0, s>>>(u, f, e.d_sidx, e.d_stab, e.d_wK, e.M, pl.N[0], pl.N[1], pl.N[2],          \
-                                           pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1], band[2],    \
-                                           ghost, e.ghost_bc_stride, e.ghost_side_stride, lo_int, hi_int, XS, e.d_cmask)
+    launch_maybe_pdl(e.pdl, k_wrap_tab<D, L, FD>, dim3(tb), dim3(th), 0, s, u, f, e.d_sidx, e.d_stab, e.d_wK, e.M,    \
+                     pl.N[0], pl.N[1], pl.N[2], pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1],       \
+                     band[2], ghost, e.ghost_bc_stride, e.ghost_side_stride, lo_int, hi_int, XS, e.d_cmask)
         if (pl.dim == 2) {
             if (quad) {
                 if (fold) PDGPU_WT(2, 4, true, nullptr);

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "assembly.h"
@@ -106,6 +107,7 @@ struct Engine {
     // fold_surface_next: the caller adds the corrections right after this
     // K.u, so the face passes may take D^e (surface_folded: they did)
     bool surf_default = false, fold_surface_next = false, surface_folded = false;
+    bool pdl = false;           // launches of the current capture use programmatic dependent launch
     bool xstrip_ready = false;  // K1 of this K.u wrote d_xstrip (3D face passes read it)
     // 3D face passes: the x pass runs before K5 and leaves its per-node result
     // in d_fx ([b][c][slot 2M][z][y]); K5 adds it at the row ends it writes
@@ -224,6 +226,39 @@ struct Engine {
         return ev_pool[ev_used++];
     }
 };
+
+// Programmatic dependent launch (CUDA graphs of small CG iterations): the
+// kernel is launched with programmatic stream serialization, so its CTAs are
+// scheduled while the previous kernel drains; pdl_entry() at the top of the
+// kernels that take part waits for the previous grid's results
+// (griddepcontrol.wait) and lets the next kernel be scheduled
+// (griddepcontrol.launch_dependents).  Both are no-ops in plain launches.
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_maybe_pdl(bool pdl, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                    cudaStream_t s, Args&&... args) {
+    if (!pdl) {
+        kern<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+#endif
 
 // halo slabs: this engine's lattice has an interior face below / above
 inline bool slab_lo_face(const Engine& e) { return e.slab.global >= 0 && e.slab.off > 0; }

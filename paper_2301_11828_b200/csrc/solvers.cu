@@ -19,7 +19,17 @@ namespace pdgpu {
 static void check(cudaError_t e, const char* what);
 
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs, fixed => deterministic order
+
 constexpr int kRedThreads = 256;
+
+// CG reduction grid: one block per SM for small systems (cheaper totals and
+// grid barriers), kRedBlocks otherwise.  Every CG kernel of a solve uses the
+// same grid, so the fused and the split (multi-rank) steps sum in the same
+// order (bit-identical iterates).
+static int cg_red_grid(const Engine& e, int64_t n) {
+    if (const char* genv = getenv("PDGPU_CG_GRID")) return std::max(1, std::min(kRedBlocks, atoi(genv)));
+    return n <= (int64_t)e.num_sms * kRedThreads * 16 ? std::min(e.num_sms, kRedBlocks) : kRedBlocks;
+}
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -281,9 +291,7 @@ bool launch_cg_fused(Engine& e, double* x, double* r, double* p, const double* q
     cudaLaunchConfig_t cfg = {};
     // small systems: one block per SM (cheaper grid barriers and totals);
     // the reduction order is fixed by the grid, so results are deterministic
-    const char* genv = getenv("PDGPU_CG_GRID");
-    const int grid = genv ? std::max(1, std::min(kRedBlocks, atoi(genv)))
-                          : (n <= (int64_t)e.num_sms * kRedThreads * 16 ? e.num_sms : kRedBlocks);
+    const int grid = cg_red_grid(e, n);
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kRedThreads);
     cfg.stream = s;
@@ -461,30 +469,30 @@ static void check(cudaError_t e, const char* what) {
 static unsigned blocks_for(int64_t n, int th) { return (unsigned)((n + th - 1) / th); }
 
 void launch_dot(Engine& e, const double* a, const double* b, int64_t n, double* out_dev, cudaStream_t s) {
-    k_dot<<<kRedBlocks, kRedThreads, 0, s>>>(a, b, n, e.d_red, e.d_ticket, out_dev);
+    k_dot<<<cg_red_grid(e, n), kRedThreads, 0, s>>>(a, b, n, e.d_red, e.d_ticket, out_dev);
     check(cudaGetLastError(), "dot");
 }
 
 void launch_cg_update(Engine& e, double* x, double* r, const double* p, const double* q, int64_t n,
                       const double* scal, double* rr_out, cudaStream_t s) {
-    k_cg_update<<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, q, n, scal, e.d_red, e.d_ticket, rr_out);
+    k_cg_update<<<cg_red_grid(e, n), kRedThreads, 0, s>>>(x, r, p, q, n, scal, e.d_red, e.d_ticket, rr_out);
     check(cudaGetLastError(), "cg_update");
 }
 
 void launch_cg_step_dev(Engine& e, double* x, double* r, double* p, const double* q, int64_t n, double* scal,
                         cudaStream_t s) {
-    k_cg_update_dev<<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, q, n, scal, e.d_red, e.d_ticket);
-    k_cg_direction_dev<<<kRedBlocks, kRedThreads, 0, s>>>(p, r, n, scal);
+    k_cg_update_dev<<<cg_red_grid(e, n), kRedThreads, 0, s>>>(x, r, p, q, n, scal, e.d_red, e.d_ticket);
+    k_cg_direction_dev<<<cg_red_grid(e, n), kRedThreads, 0, s>>>(p, r, n, scal);
     e.launches += 2;
     check(cudaGetLastError(), "cg_step_dev");
 }
 
 void launch_cg_step_dev_comm(Engine& e, double* x, double* r, double* p, const double* q, int64_t n, double* scal,
                              cudaStream_t s) {
-    k_cg_update_local<<<kRedBlocks, kRedThreads, 0, s>>>(x, r, p, q, n, scal, e.d_red, e.d_ticket);
+    k_cg_update_local<<<cg_red_grid(e, n), kRedThreads, 0, s>>>(x, r, p, q, n, scal, e.d_red, e.d_ticket);
     comm_allreduce(e, scal + 9, 1, s);
     k_cg_finish<<<1, 1, 0, s>>>(scal);
-    k_cg_direction_dev<<<kRedBlocks, kRedThreads, 0, s>>>(p, r, n, scal);
+    k_cg_direction_dev<<<cg_red_grid(e, n), kRedThreads, 0, s>>>(p, r, n, scal);
     e.launches += 3;
     check(cudaGetLastError(), "cg_step_dev_comm");
 }

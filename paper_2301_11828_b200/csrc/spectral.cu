@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
                                                     const double* __restrict__ body, int64_t nodes,
                                                     const __grid_constant__ CUtensorMap tm, int pf,
                                                     const double* __restrict__ fx, int Mfx) {
+    pdl_entry();
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R;
     constexpr int XB = TMAG ? xbuf_stride_rows(Sh::XBUF) : xbuf_stride_t(Sh::XBUF, Sh::T);  // per-transform stride
@@ -716,6 +717,7 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_pipe(const double* __restr
                                                            int Nx, int Nrow, int nslab, int Hx,
                                                            const double2* __restrict__ tw, int logTWN,
                                                            double* __restrict__ xstrip, int M, int Nz) {
+    pdl_entry();
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = xbuf_stride_t(Sh::XBUF, Sh::T);
     constexpr int TR = 1 << LOGTR;
@@ -1230,6 +1232,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_duo(const double
                                                                    const double* __restrict__ coltab, int M,
                                                                    int ncols, int Nl, int NC, int batch,
                                                                    const double2* __restrict__ tw, int logTWN) {
+    pdl_entry();
     using Sh = FftShape<LOGQ, kPipeLogR>;
     constexpr int Q = Sh::Q, T = Sh::T, XB = Sh::XBUF, RR = Sh::R;
     extern __shared__ double2 sm[];
@@ -1954,8 +1957,8 @@ no_duo:
                          ? e.d_xstrip
                          : nullptr;
         e.xstrip_ready = xs != nullptr;
-#define PDGPU_K1P(LT, C) k_rfft_rows_pipe<LQ, LT, C><<<pgrid, 2 * PTR * T, psmem, s>>>(u, e.d_S1, Nx, Ny, nslab, \
-                                                                                pl.Hx, e.d_tw, pl.logTWN, xs, e.M, Nz)
+#define PDGPU_K1P(LT, C) launch_maybe_pdl(e.pdl, k_rfft_rows_pipe<LQ, LT, C>, dim3(pgrid), dim3(2 * PTR * T), psmem, s, \
+                                          u, e.d_S1, Nx, Ny, nslab, pl.Hx, e.d_tw, pl.logTWN, xs, e.M, Nz)
 #define PDGPU_K1PC(C) (ltr == 3 ? PDGPU_K1P(3, C) : ltr == 2 ? PDGPU_K1P(2, C) : ltr == 1 ? PDGPU_K1P(1, C) \
                                                                                  : PDGPU_K1P(0, C))
         if (cx) PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K1PC(true))
@@ -2054,9 +2057,8 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
     // gathers (short rows, 3D): prefetch distance PDGPU_K5_GPF (CTAs)
     const char* gpfenv = getenv("PDGPU_K5_GPF");
     const int gpf = gpfenv ? atoi(gpfenv) : 0;
-#define PDGPU_K5(LT, C) k_irfft_rows<LQ, LT, C><<<grid, 2 * TR * T, smem, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx, e.d_tw, \
-                                                                          pl.logTWN, scale, cmask, body, pl.nodes, tm, gpf, \
-                                                                          fxs, e.M)
+#define PDGPU_K5(LT, C) launch_maybe_pdl(e.pdl, k_irfft_rows<LQ, LT, C>, grid, dim3(2 * TR * T), smem, s, xin, f, Nx, Ny, \
+                                         Nz, d, pl.Hx, e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, gpf, fxs, e.M)
 #define PDGPU_K5C(C) (ltr == 3 ? PDGPU_K5(3, C) : ltr == 2 ? PDGPU_K5(2, C) : ltr == 1 ? PDGPU_K5(1, C) : PDGPU_K5(0, C))
     if (cx) PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(true))
     else PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(false))
@@ -2156,11 +2158,11 @@ void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s) {
 #define DUO_ARGS spec, e.d_S2, e.d_sym, e.d_coltab, e.M, pl.ncols, pl.Nl, NCd, batch, e.d_tw, pl.logTWN
 #define DUO_NH(NHV)                                                                                           \
     if (mode == 2)                                                                                            \
-        PDGPU_DISPATCH_LOGQ_4_12(lq, (k_spectral2d_duo<LQ, 2, NHV><<<dgrid, NCd * Tp, dsmem, s>>>(DUO_ARGS))) \
+        PDGPU_DISPATCH_LOGQ_4_12(lq, (launch_maybe_pdl(e.pdl, k_spectral2d_duo<LQ, 2, NHV>, dim3(dgrid), dim3(NCd * Tp), dsmem, s, DUO_ARGS))) \
     else if (mode == 1)                                                                                       \
-        PDGPU_DISPATCH_LOGQ_4_12(lq, (k_spectral2d_duo<LQ, 1, NHV><<<dgrid, NCd * Tp, dsmem, s>>>(DUO_ARGS))) \
+        PDGPU_DISPATCH_LOGQ_4_12(lq, (launch_maybe_pdl(e.pdl, k_spectral2d_duo<LQ, 1, NHV>, dim3(dgrid), dim3(NCd * Tp), dsmem, s, DUO_ARGS))) \
     else                                                                                                      \
-        PDGPU_DISPATCH_LOGQ_4_12(lq, (k_spectral2d_duo<LQ, 0, NHV><<<dgrid, NCd * Tp, dsmem, s>>>(DUO_ARGS)))
+        PDGPU_DISPATCH_LOGQ_4_12(lq, (launch_maybe_pdl(e.pdl, k_spectral2d_duo<LQ, 0, NHV>, dim3(dgrid), dim3(NCd * Tp), dsmem, s, DUO_ARGS)))
         if (nh == 1) {
             DUO_NH(1)
         } else {
