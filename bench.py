@@ -318,6 +318,11 @@ def extra_configs(device, stream):
     ff.cg_solve_device(b, x, tol=1e-10, maxit=20000, stream=stream)  # warm
     ms, (it, rel) = timed(lambda: ff.cg_solve_device(b, x, tol=1e-10, maxit=20000, stream=stream))
     out["config1_cg"] = {"grid": [128, 128], "tol": 1e-10, "iterations": it, "relres": rel, "solve_ms": ms}
+    ff.cg_operator("direct")  # the same K summed directly (comparison point, not the MSBFM metric)
+    ff.cg_solve_device(b, x, tol=1e-10, maxit=20000, stream=stream)
+    ms, (it, rel) = timed(lambda: ff.cg_solve_device(b, x, tol=1e-10, maxit=20000, stream=stream))
+    out["config1_cg_direct_operator"] = {"iterations": it, "relres": rel, "solve_ms": ms,
+                                         "what": "CG with the direct stencil sum of K (pdgpu_set_cg_operator)"}
     ff.close()
     # config 3: 1024^2, centre crack L/2, +-1e-3 on top/bottom layers (u_y), CG to 1e-10
     n = 1024
@@ -331,6 +336,10 @@ def extra_configs(device, stream):
     ms, (it, rel) = timed(lambda: ff.cg_solve_device(b, x, tol=1e-10, maxit=50000, stream=stream))
     out["config3_cg"] = {"grid": [n, n], "crack_bonds": bonds, "tol": 1e-10, "iterations": it, "relres": rel,
                          "solve_ms": ms}
+    ff.cg_operator("direct")
+    ms, (it, rel) = timed(lambda: ff.cg_solve_device(b, x, tol=1e-10, maxit=50000, stream=stream))
+    out["config3_cg_direct_operator"] = {"iterations": it, "relres": rel, "solve_ms": ms,
+                                         "what": "CG with the direct stencil sum of K (pdgpu_set_cg_operator)"}
     ff.close()
     # config 4: 128^3 clamped cube; K.u rate and CG to 1e-9
     n = 128

@@ -291,6 +291,13 @@ int pdgpu_write_snapshot(int dim, const int* dims, double spacing, const double*
 int pdgpu_read_snapshot(const char* path, int dim, int* dims, double* spacing, double* origin, int64_t* step,
                         double* t, double* u, double* damage);
 
+/* CG's operator (new work, the reference has no CG): 0 = MSBFM (default),
+ * 1 = the direct stencil sum of the same operator (the reference's own
+ * independent oracle form, tests/support/oracles.hpp:72-96) plus the same
+ * corrections -- at M = 3 it moves fewer bytes; MSBFM's advantage is
+ * asymptotic in the horizon.  Slab engines always use MSBFM. */
+int pdgpu_set_cg_operator(pdgpu_t h, int direct);
+
 /* ------------------------------------------------------------- monitors --
  * MonitorWriter (output.hpp:45-72) and nearest_node (output.hpp:33-41): the
  * reference's tab-separated monitor file ("# step\tt\tnode\tu_x\tu_y[\tu_z]",

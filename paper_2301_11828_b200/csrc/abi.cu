@@ -1421,6 +1421,19 @@ int pdgpu_constraint_values(pdgpu_t h, uint8_t* mask, double* uc) {
 }
 
 // ------------------------------------------------------------------ CG ---
+// q = -A_ff p on the free rows (zero on constrained ones): MSBFM (default) or,
+// with pdgpu_set_cg_operator(h, 1), the direct stencil sum of the same
+// operator (csrc/direct.cu; no symbol, no FFT) plus the same corrections
+static void cg_operator(Engine& e, const double* p, double* q, cudaStream_t s) {
+    if (e.cg_direct && !e.ghost_view && e.slab.global < 0) {
+        launch_direct_apply(e, p, q, 1, s, -1.0, e.d_cmask);
+    } else {
+        e.fold_surface_next = true;
+        launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
+    }
+    launch_corrections(e, p, q, 1, s, -1.0);
+}
+
 // CG iterations per captured graph: small systems replay several per launch
 // (the host's graph-launch cadence would otherwise bound the iteration rate);
 // iterations past convergence find the done flag and update nothing.  The
@@ -1485,9 +1498,7 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
             const char* pdlenv = getenv("PDGPU_PDL");
             e.pdl = pdlenv && pdlenv[0] == '1';  // opt-in: measured neutral (32.1 vs 32.5 us at 128^2)
             for (int rep = 0; rep < cg_iters_per_graph(e, m); ++rep) {
-                e.fold_surface_next = true;
-                launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
-                launch_corrections(e, p, q, 1, s, -1.0);
+                cg_operator(e, p, q, s);
                 if (multi) {
                     launch_dot(e, p, q, m, e.d_scal + 1, s);
                     comm_allreduce(e, e.d_scal + 1, 1, s);
@@ -1527,8 +1538,7 @@ static void cg_impl(Engine& e, const double* b, double* x, double tol, int maxit
         rel = sqrt(st[2]) / bnorm;
     }
     while (!(!hist_host && bnorm > 0 && !getenv("PDGPU_CG_HOSTLOOP")) && bnorm > 0 && k < maxit) {
-        launch_fast_apply(e, p, q, 1, s, -1.0, e.d_cmask, nullptr);
-        launch_corrections(e, p, q, 1, s, -1.0);
+        cg_operator(e, p, q, s);
         launch_dot(e, p, q, m, e.d_scal + 1, s);
         comm_allreduce(e, e.d_scal + 1, 1, s);
         launch_cg_update(e, x, r, p, q, m, e.d_scal, e.d_scal + 2, s);
@@ -1976,6 +1986,18 @@ int pdgpu_near_surface(int dim, const int* dims, int M, uint8_t* out) {
 }  // extern "C"
 
 /* ------------------------------------------------------------ snapshots -- */
+int pdgpu_set_cg_operator(pdgpu_t h, int direct) {
+    return guarded([&] {
+        if (!h) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null handle");
+        if (direct && (h->dim == 2 ? (h->M < 1 || h->M > 5) : false))
+            throw PdError(PDGPU_ERR_NOT_SUPPORTED, "direct stencil: 2D horizon M must be 1..5");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        if (direct) direct_prepare(*h);
+        h->cg_direct = direct != 0;
+        touch_state(*h);
+    });
+}
+
 int pdgpu_sim_monitor(pdgpu_t h, const int64_t* nodes, int n) {
     return guarded([&] {
         if (!h || n < 0 || (n > 0 && !nodes)) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad monitor nodes");

@@ -35,7 +35,8 @@ constexpr int isqrt_c(int v) {
 template <int M>
 __global__ void __launch_bounds__(kTX * (kTY / kRows)) k_direct2d(const double* __restrict__ u, double* __restrict__ f,
                                                                   const double* __restrict__ K, int Nx, int Ny,
-                                                                  int64_t nodes, double scale) {
+                                                                  int64_t nodes, double scale,
+                                                                  const uint8_t* __restrict__ cmask) {
     constexpr int W = kTX + 2 * M, H = kTY + 2 * M, SIDE = 2 * M + 1, SS = SIDE * SIDE, WIN = kRows + 2 * M;
     __shared__ double su[2][H][W + 1];
     const int b = blockIdx.z;
@@ -84,8 +85,9 @@ __global__ void __launch_bounds__(kTX * (kTY / kRows)) k_direct2d(const double* 
         const int gy = y0 + ty + i;
         if (gy >= Ny) continue;
         const int64_t p = (int64_t)gy * Nx + gx;
-        fb[p] = scale * acc[i][0];
-        fb[nodes + p] = scale * acc[i][1];
+        const uint8_t cm = cmask ? cmask[p] : 0;  // constrained rows read zero (CG operator)
+        fb[p] = (cm & 1u) ? 0.0 : scale * acc[i][0];
+        fb[nodes + p] = (cm & 2u) ? 0.0 : scale * acc[i][1];
     }
 }
 
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(kTX * (kTY / kRows)) k_direct2d(const double* 
 // centre coefficients kc[pair]
 __global__ void k_direct3d(const double* __restrict__ u, double* __restrict__ f, const int* __restrict__ offs,
                            const double* __restrict__ koff, const double* __restrict__ kc, int nof, int Nx, int Ny,
-                           int Nz, int64_t nodes, double scale) {
+                           int Nz, int64_t nodes, double scale, const uint8_t* __restrict__ cmask) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int b = blockIdx.y;
     if (p >= nodes) return;
@@ -117,42 +119,48 @@ __global__ void k_direct3d(const double* __restrict__ u, double* __restrict__ f,
         acc[2] += c[2] * ux + c[4] * uy + c[5] * uz;
     }
     double* fb = f + (int64_t)b * 3 * nodes;
-    fb[p] = scale * acc[0];
-    fb[nodes + p] = scale * acc[1];
-    fb[2 * nodes + p] = scale * acc[2];
+    const uint8_t cm = cmask ? cmask[p] : 0;
+    fb[p] = (cm & 1u) ? 0.0 : scale * acc[0];
+    fb[nodes + p] = (cm & 2u) ? 0.0 : scale * acc[1];
+    fb[2 * nodes + p] = (cm & 4u) ? 0.0 : scale * acc[2];
 }
 
 }  // namespace
 
-void launch_direct_apply(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale) {
+// 3D centre coefficients (stencil index of o = 0; stencils stored first in
+// d_K); allocated outside any graph capture (pdgpu_set_cg_operator)
+void direct_prepare(Engine& e) {
+    if (e.dim != 3 || e.d_kc) return;
+    std::vector<double> kc(6);
+    const int o0[3] = {0, 0, 0};
+    const int64_t si = assembly::stencil_index(3, e.M, o0);
+    for (int pr = 0; pr < 6; ++pr) kc[pr] = e.stencils[(size_t)(pr * e.ss + si)];
+    if (cudaMalloc(&e.d_kc, sizeof(double) * 6) != cudaSuccess) throw std::runtime_error("alloc kc");
+    cudaMemcpy(e.d_kc, kc.data(), sizeof(double) * 6, cudaMemcpyHostToDevice);
+}
+
+void launch_direct_apply(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
+                         const uint8_t* cmask) {
     const Plan& pl = e.plan;
     PassTimer pt(e, kPassVec, s);
     if (e.dim == 2) {
         dim3 grid((pl.N[0] + kTX - 1) / kTX, (pl.N[1] + kTY - 1) / kTY, batch);
         dim3 block(kTX, kTY / kRows);
         switch (e.M) {
-            case 1: k_direct2d<1><<<grid, block, 0, s>>>(u, f, e.d_K, pl.N[0], pl.N[1], pl.nodes, scale); break;
-            case 2: k_direct2d<2><<<grid, block, 0, s>>>(u, f, e.d_K, pl.N[0], pl.N[1], pl.nodes, scale); break;
-            case 3: k_direct2d<3><<<grid, block, 0, s>>>(u, f, e.d_K, pl.N[0], pl.N[1], pl.nodes, scale); break;
-            case 4: k_direct2d<4><<<grid, block, 0, s>>>(u, f, e.d_K, pl.N[0], pl.N[1], pl.nodes, scale); break;
-            case 5: k_direct2d<5><<<grid, block, 0, s>>>(u, f, e.d_K, pl.N[0], pl.N[1], pl.nodes, scale); break;
+            case 1: k_direct2d<1><<<grid, block, 0, s>>>(u, f, e.d_K, pl.N[0], pl.N[1], pl.nodes, scale, cmask); break;
+            case 2: k_direct2d<2><<<grid, block, 0, s>>>(u, f, e.d_K, pl.N[0], pl.N[1], pl.nodes, scale, cmask); break;
+            case 3: k_direct2d<3><<<grid, block, 0, s>>>(u, f, e.d_K, pl.N[0], pl.N[1], pl.nodes, scale, cmask); break;
+            case 4: k_direct2d<4><<<grid, block, 0, s>>>(u, f, e.d_K, pl.N[0], pl.N[1], pl.nodes, scale, cmask); break;
+            case 5: k_direct2d<5><<<grid, block, 0, s>>>(u, f, e.d_K, pl.N[0], pl.N[1], pl.nodes, scale, cmask); break;
             default: throw std::runtime_error("direct stencil: 2D horizon M must be 1..5");
         }
     } else {
-        // centre coefficients live at stencil index of o = 0 (stencils stored first in d_K)
-        if (!e.d_kc) {
-            std::vector<double> kc(6);
-            const int o0[3] = {0, 0, 0};
-            const int64_t si = assembly::stencil_index(3, e.M, o0);
-            for (int pr = 0; pr < 6; ++pr) kc[pr] = e.stencils[(size_t)(pr * e.ss + si)];
-            if (cudaMalloc(&e.d_kc, sizeof(double) * 6) != cudaSuccess) throw std::runtime_error("alloc kc");
-            cudaMemcpy(e.d_kc, kc.data(), sizeof(double) * 6, cudaMemcpyHostToDevice);
-        }
+        direct_prepare(e);
         const double* koff = e.d_K + e.np * e.ss;
         const int th = 256;
         dim3 grid((unsigned)((pl.nodes + th - 1) / th), batch);
         k_direct3d<<<grid, th, 0, s>>>(u, f, e.d_offs, koff, e.d_kc, e.nof, pl.N[0], pl.N[1], pl.N[2], pl.nodes,
-                                      scale);
+                                      scale, cmask);
     }
     const cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) throw std::runtime_error(std::string("direct launch: ") + cudaGetErrorString(err));

@@ -108,6 +108,7 @@ struct Engine {
     // K.u, so the face passes may take D^e (surface_folded: they did)
     bool surf_default = false, fold_surface_next = false, surface_folded = false;
     bool pdl = false;           // launches of the current capture use programmatic dependent launch
+    bool cg_direct = false;     // CG's operator: direct stencil sum instead of MSBFM (pdgpu_set_cg_operator)
     bool xstrip_ready = false;  // K1 of this K.u wrote d_xstrip (3D face passes read it)
     // 3D face passes: the x pass runs before K5 and leaves its per-node result
     // in d_fx ([b][c][slot 2M][z][y]); K5 adds it at the row ends it writes
@@ -318,7 +319,9 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
 void set_kernel_attributes();
 
 // direct.cu
-void launch_direct_apply(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale);
+void direct_prepare(Engine& e);
+void launch_direct_apply(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
+                         const uint8_t* cmask = nullptr);
 
 // corrections.cu
 void build_wrap_table(Engine& e);

@@ -349,6 +349,12 @@ class FastForce:
                                              None if hist is None else _dp(hist), nhist))
         return x, it.value, rel.value, hist
 
+    def cg_operator(self, kind: str = "msbfm"):
+        """CG's operator: "msbfm" (default) or "direct" (the direct stencil sum of the same K)."""
+        if kind not in ("msbfm", "direct"):
+            raise ValueError(kind)
+        _check(self._lib.pdgpu_set_cg_operator(self._h, 1 if kind == "direct" else 0))
+
     def cg_solve_device(self, b, x, tol: float = 1e-10, maxit: int = 10000, stream=None):
         it = C.c_int()
         rel = C.c_double()
