@@ -468,6 +468,80 @@ def extra_configs(device, stream):
 
 
 # -------------------------------------------------------------------- main --
+def run_transpose(args):
+    """The all-to-all distributed-FFT arm (SURVEY.md 8e comparison, opt-in:
+    --shard transpose): rank r holds rows and half-spectrum columns of the
+    BATCH x N^2 lattice (pdgpu_set_transpose), two NCCL all-to-all transposes
+    of the spectrum and the ring halo per K.u (csrc/transpose.cu, comm.cpp).
+    Timed like the slab arm: barrier + synchronize, CUDA events, max over ranks."""
+    import torch
+    import torch.distributed as tdist
+    from paper_2301_11828_b200 import FastForce, build_kernel
+    from paper_2301_11828_b200 import dist as D
+    from paper_2301_11828_b200.engine import transpose_splits
+
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    rank, world, local = D.env()
+    torch.cuda.set_device(local)
+    D.init("nccl", torch.device("cuda", local))
+    h = 1.0 / N_SIDE
+    K = build_kernel(DIM, h, 3.015 * h, M, 1.0, 1.0)
+    rb, cb = transpose_splits(N_SIDE, N_SIDE, world)
+    R = rb[rank + 1] - rb[rank]
+    ff = FastForce((N_SIDE, R), M, K, device=local)
+    ff.set_geometry(h, [0.0, rb[rank] * h], 3.015 * h, 1.0)
+    ff.set_transpose(world, rank, N_SIDE, rb, cb)
+    if world > 1:
+        uid = [ff.comm_unique_id() if rank == 0 else None]
+        if tdist.is_initialized():
+            tdist.broadcast_object_list(uid, src=0)
+        ff.comm_init(world, rank, uid[0])
+    stream = torch.cuda.Stream()
+    gen = torch.Generator(device="cuda").manual_seed(D.vector_seed(2000, 0) + rank)
+    u = torch.empty((BATCH, DIM, R * N_SIDE), dtype=torch.float64, device="cuda")
+    u.uniform_(-1.0, 1.0, generator=gen)
+    f = torch.empty_like(u)
+    for _ in range(args.warmup):
+        ff.matvec_device(u, f, BATCH, stream)
+    torch.cuda.synchronize()
+    ff.timing_read()
+    ff.timing(True)
+    launches0 = ff.launch_count()
+    clk = ClockSampler(local)
+    clk.start()
+    D.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        ff.matvec_device(u, f, BATCH, stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    D.barrier()
+    clocks = clk.stop()
+    ms_step = D.max_over_ranks(ev0.elapsed_time(ev1), "cuda") / args.steps
+    passes = ff.timing_read()
+    ff.timing(False)
+    assert torch.isfinite(f).all().item(), "non-finite K.u"
+    hx = N_SIDE // 2 + 1
+    share = BATCH * DIM * hx * (N_SIDE // world) * 16
+    line = {"metric": METRIC, "value": BATCH * DIM * N_SIDE * N_SIDE / (ms_step * 1e-3), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded uniform[-1,1], torch Philox)",
+            "config": dict(workload_config(world), parallelism=f"{world} ranks: all-to-all distributed FFT "
+                                                               "(two spectrum transposes + ring halo per K.u)"),
+            "transpose": {"bytes_sent_per_rank_per_step": 2 * share * (world - 1) / world,
+                          "passes_ms_per_step": {k: v[0] / args.steps for k, v in passes.items()}},
+            "gpu_launches": ff.launch_count() - launches0, "clocks": clocks}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ff.close()
+    D.finalize()
+
+
 def run_slab(args):
     """Strong scaling of the BATCH x N^2 lattice over the ranks (BASELINE
     configs[1]: "the 4096^2 grid is slab-sharded across 2/4/8 GPUs"): row
@@ -617,7 +691,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=150.0)
     ap.add_argument("--slab-single", action="store_true",
                     help="run the slab arm (NCCL engine transport, one rank) at N = 1 too")
-    ap.add_argument("--shard", default="slab", choices=["vectors", "slab"],
+    ap.add_argument("--shard", default="slab", choices=["vectors", "slab", "transpose"],
                     help="N>1: slab = the one lattice split into row slabs with the M-row NCCL halo exchange "
                          "(strong scaling, BASELINE configs[1], default); vectors = every rank its own batch "
                          "(replicas, weak)")
@@ -627,6 +701,8 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args)
     from paper_2301_11828_b200 import dist as D0
+    if args.shard == "transpose":
+        return run_transpose(args)
     if args.shard == "slab" and (D0.env()[1] > 1 or args.slab_single):
         return run_slab(args)
 

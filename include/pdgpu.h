@@ -235,6 +235,25 @@ int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64
  * copies between the phases of each step (the NCCL path does the same
  * inside pdgpu_sim_step).  *broken = bonds broken over all slabs. */
 int pdgpu_group_sim_step(pdgpu_t* engines, int n, int n_steps, double s0, const double* watch, int64_t* broken);
+
+/* ----------------------------------------------- distributed FFT (2D) --
+ * The all-to-all transpose arm of SURVEY §8e (north_star's distributed FFT;
+ * the halo slabs above are the default multi-GPU path).  Engine `rank` of
+ * `nranks` is created on its rows [row_bounds[rank], row_bounds[rank+1]) of
+ * an Nx x global_rows lattice (global_rows a power of two, Nx periodic) and
+ * also owns the half-spectrum columns [col_bounds[rank], col_bounds[rank+1])
+ * (col_bounds[nranks] = Nx/2 + 1).  Every K.u then runs K1 on its rows, an
+ * all-to-all transpose (NCCL grouped send/recv of equal padded blocks after
+ * pdgpu_comm_init; a copy for one rank), the y pass over the global columns
+ * with this rank's symbol, the reverse transpose and K5; the wrap correction
+ * takes the x aliases locally and the y aliases at the global faces from the
+ * opposite end's M rows.  D^e and the near-surface flags follow the global
+ * lattice.  Cross-face broken bonds are not supported in this arm.
+ * pdgpu_group_matvec_transpose: the same K.u for n engines of one process
+ * (rank r = engines[r]) with device copies for the transposes. */
+int pdgpu_set_transpose(pdgpu_t h, int nranks, int rank, int global_rows, const int* row_bounds,
+                        const int* col_bounds);
+int pdgpu_group_matvec_transpose(pdgpu_t* engines, int n, const double* const* u, double* const* f, int batch);
 /* Simulation<Dim> with Integrator::Adr (AdrIntegrator, timestepping.hpp:79-145;
  * adr_mass :150-162): the reference's quasi-static solver.  Same state and
  * constraints as sim_init (v0 = 0); fixed_damping NaN = adaptive Rayleigh-

@@ -54,6 +54,9 @@ SIGNATURES = {
     "pdgpu_monitor_close": (None, [C.c_void_p]),
     "pdgpu_sim_monitor": (C.c_int, [C.c_void_p, c_int64_p, C.c_int]),
     "pdgpu_set_cg_operator": (C.c_int, [C.c_void_p, C.c_int]),
+    "pdgpu_set_transpose": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, c_int_p, c_int_p]),
+    "pdgpu_group_matvec_transpose": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_void_p),
+                                              C.POINTER(C.c_void_p), C.c_int]),
     "pdgpu_sim_monitor_read": (C.c_int, [C.c_void_p, c_int64_p, c_double_p, c_double_p, C.c_int64, c_int64_p]),
     "pdgpu_read_snapshot": (C.c_int, [C.c_char_p, C.c_int, C.POINTER(C.c_int), c_double_p, c_double_p,
                                       C.POINTER(C.c_int64), c_double_p, c_double_p, c_double_p]),

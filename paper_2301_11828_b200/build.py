@@ -17,7 +17,8 @@ LIB = os.path.join(HERE, "libpdgpu.so")
 # spectral.cu is compiled once per part (-DPDGPU_PART=k): each object
 # instantiates only its own kernel templates, and the parts build in parallel
 SPECTRAL_PARTS = 5
-SOURCES = ["spectral.cu", "corrections.cu", "direct.cu", "solvers.cu", "abi.cu", "assembly.cpp", "snapshot.cpp", "comm.cpp"]
+SOURCES = ["spectral.cu", "corrections.cu", "direct.cu", "solvers.cu", "abi.cu", "transpose.cu", "assembly.cpp",
+           "snapshot.cpp", "comm.cpp"]
 HEADERS = ["engine.h", "fft.cuh", "assembly.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

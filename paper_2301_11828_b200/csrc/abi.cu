@@ -735,6 +735,7 @@ void pdgpu_destroy(pdgpu_t h) {
     for (void* p : ptrs)
         if (p) cudaFree(p);
     if (h->cg_graph) cudaGraphExecDestroy(h->cg_graph);
+    a2a_free(*h);
     h->d_face_recv = nullptr;  // freed with the other buffers above
     h->d_halo = nullptr;
     try {
@@ -1807,6 +1808,121 @@ static void group_faces(pdgpu_t* hs, int n) {
                    "face copy");
         launch_merge_face(e, e.d_face_recv, e.stream);
     }
+}
+
+// ---- distributed FFT (transpose.cu) ------------------------------------
+int pdgpu_set_transpose(pdgpu_t h, int nranks, int rank, int global_rows, const int* row_bounds,
+                        const int* col_bounds) {
+    return guarded([&] {
+        if (!h || !row_bounds || !col_bounds) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "null argument");
+        cuda_check(cudaSetDevice(h->device), "set device");
+        try {
+            a2a_setup(*h, nranks, rank, global_rows, row_bounds, col_bounds);
+        } catch (const std::runtime_error& ex) {
+            throw PdError(PDGPU_ERR_INVALID_ARGUMENT, ex.what());
+        }
+        // D^e, near-surface flags, positions and ids of the global lattice
+        Engine& e = *h;
+        e.h_near = assembly::near_surface(e.dim, e.plan.N, e.M, e.slab);
+        std::vector<long long> rows;
+        std::vector<double> de;
+        assembly::surface_diag(e.dim, e.plan.N, e.M, e.stencils.data(), e.h_near, rows, de, e.slab);
+        upload_surface(e, rows, de);
+    });
+}
+
+// One K.u (apply + corrections) of a lattice split over the n engines of one
+// process (pdgpu_set_transpose on each, rank r = engine r), the all-to-all
+// transposes done by device copies: the single-process stand-in for the NCCL
+// path, for tests on one GPU.
+int pdgpu_group_matvec_transpose(pdgpu_t* hs, int n, const double* const* us, double* const* fs, int batch) {
+    return guarded([&] {
+        if (!hs || !us || !fs || n < 1 || batch < 1) throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "bad group");
+        for (int r = 0; r < n; ++r)
+            if (!hs[r] || hs[r]->a2a.G != n || hs[r]->a2a.rank != r)
+                throw PdError(PDGPU_ERR_INVALID_ARGUMENT, "group engine without the matching pdgpu_set_transpose");
+        struct Reset {
+            pdgpu_t* hs;
+            int n;
+            ~Reset() {
+                for (int r = 0; r < n; ++r) hs[r]->a2a_external = false;
+            }
+        } reset{hs, n};
+        std::vector<cudaEvent_t> ev(n);
+        for (int r = 0; r < n; ++r) {
+            cuda_check(cudaSetDevice(hs[r]->device), "set device");
+            cuda_check(cudaEventCreateWithFlags(&ev[r], cudaEventDisableTiming), "event");
+            hs[r]->a2a_external = true;
+        }
+        auto each = [&](auto&& fn) {
+            for (int r = 0; r < n; ++r) {
+                cuda_check(cudaSetDevice(hs[r]->device), "set device");
+                fn(r, *hs[r]);
+                cuda_check(cudaEventRecord(ev[r], hs[r]->stream), "record");
+            }
+        };
+        // every engine's block g of d_send -> engine g's d_recv block r
+        auto exchange = [&]() {
+            const int64_t blk = a2a_block(*hs[0], batch);
+            for (int r = 0; r < n; ++r) {
+                Engine& e = *hs[r];
+                cuda_check(cudaSetDevice(e.device), "set device");
+                for (int g = 0; g < n; ++g) {
+                    Engine& o = *hs[g];
+                    cuda_check(cudaStreamWaitEvent(e.stream, ev[g], 0), "wait peer");
+                    cuda_check(cudaMemcpyPeerAsync(e.a2a.d_recv + (size_t)g * blk, e.device, o.a2a.d_send + (size_t)r * blk,
+                                                   o.device, sizeof(double2) * blk, e.stream),
+                               "a2a copy");
+                }
+            }
+            for (int r = 0; r < n; ++r) {
+                cuda_check(cudaSetDevice(hs[r]->device), "set device");
+                cuda_check(cudaEventRecord(ev[r], hs[r]->stream), "record");
+            }
+            for (int r = 0; r < n; ++r) {  // senders wait for their readers before reusing d_send
+                cuda_check(cudaSetDevice(hs[r]->device), "set device");
+                for (int g = 0; g < n; ++g) cuda_check(cudaStreamWaitEvent(hs[r]->stream, ev[g], 0), "wait readers");
+            }
+        };
+        each([&](int r, Engine& e) { a2a_phase1(e, us[r], batch, e.stream); });
+        exchange();
+        each([&](int, Engine& e) { a2a_phase2(e, batch, e.stream); });
+        exchange();
+        each([&](int r, Engine& e) {
+            a2a_phase3(e, fs[r], batch, e.stream, 1.0, nullptr, nullptr);
+            halo_pack(e, us[r], batch, e.a2a.d_alias, e.stream);  // [side][batch][dim][M][Nx]
+        });
+        // the ring halo: engine r's side 0 <- engine r-1's last M rows, side 1 <-
+        // engine r+1's first M rows (mod n)
+        for (int r = 0; r < n; ++r) {
+            Engine& e = *hs[r];
+            Engine& lo = *hs[(r + n - 1) % n];
+            Engine& hi = *hs[(r + 1) % n];
+            const size_t side = (size_t)batch * e.dim * e.M * e.plan.N[0];
+            cuda_check(cudaSetDevice(e.device), "set device");
+            cuda_check(cudaStreamWaitEvent(e.stream, ev[(r + n - 1) % n], 0), "wait");
+            cuda_check(cudaStreamWaitEvent(e.stream, ev[(r + 1) % n], 0), "wait");
+            cuda_check(cudaMemcpyPeerAsync(a2a_alias_recv(e, batch), e.device, lo.a2a.d_alias + side, lo.device,
+                                           sizeof(double) * side, e.stream),
+                       "ring low");
+            cuda_check(cudaMemcpyPeerAsync(a2a_alias_recv(e, batch) + side, e.device, hi.a2a.d_alias, hi.device,
+                                           sizeof(double) * side, e.stream),
+                       "ring high");
+        }
+        each([&](int r, Engine& e) {
+            const size_t side = (size_t)batch * e.dim * e.M * e.plan.N[0];
+            e.ghost_bc_stride = (int64_t)e.M * e.plan.N[0];
+            e.ghost_side_stride = (int64_t)side;
+            e.ghost_view = a2a_alias_recv(e, batch);
+            launch_wrap_correction(e, us[r], fs[r], batch, e.stream, 1.0, nullptr);
+            launch_corrections(e, us[r], fs[r], batch, e.stream, 1.0);
+        });
+        for (int r = 0; r < n; ++r) {
+            cuda_check(cudaSetDevice(hs[r]->device), "set device");
+            cuda_check(cudaStreamSynchronize(hs[r]->stream), "group matvec");
+            cudaEventDestroy(ev[r]);
+        }
+    });
 }
 
 int pdgpu_group_sim_step(pdgpu_t* hs, int n, int n_steps, double s0, const double* watch, int64_t* broken) {

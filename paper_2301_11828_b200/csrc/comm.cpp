@@ -137,7 +137,11 @@ bool comm_attached(const Engine& e) { return e.nccl_comm != nullptr; }
 static bool lo_face(const Engine& e) { return slab_lo_face(e); }
 static bool hi_face(const Engine& e) { return slab_hi_face(e); }
 
-bool halo_active(const Engine& e) { return comm_attached(e) && e.nranks > 1 && slab_has_faces(e); }
+// the halo exchange belongs to the halo slabs; the distributed FFT moves
+// the spectrum instead (a2a_nccl_exchange) and only the global faces' rows
+bool halo_active(const Engine& e) {
+    return comm_attached(e) && e.nranks > 1 && slab_has_faces(e) && e.a2a.G == 0;
+}
 
 // [send|recv][side][batch][dim][M][plane]; side 0 = the rows before the slab
 void ensure_halo(Engine& e, int batch) {
@@ -230,6 +234,47 @@ void ledger_exchange(Engine& e, cudaStream_t s) {
     if (lo_face(e)) nccl_check(api().Recv(e.d_face_recv, words, ncclUint32, e.rank - 1, c, s), "ncclRecv ledger");
     nccl_check(api().GroupEnd(), "ncclGroupEnd");
     if (lo_face(e)) launch_merge_face(e, e.d_face_recv, s);
+}
+
+// distributed FFT: the all-to-all of equal blocks d_send[g] -> rank g's
+// d_recv[rank] (grouped send/recv; the own block is a device copy)
+void a2a_nccl_exchange(Engine& e, int batch, cudaStream_t s) {
+    if (!comm_attached(e) || e.nranks != e.a2a.G || e.rank != e.a2a.rank)
+        throw std::runtime_error("distributed FFT: the NCCL communicator does not match the rank layout");
+    const int64_t blk = a2a_block(e, batch);
+    const size_t n = (size_t)blk * 2;  // doubles
+    double* send = reinterpret_cast<double*>(e.a2a.d_send);
+    double* recv = reinterpret_cast<double*>(e.a2a.d_recv);
+    const ncclComm_t c = (ncclComm_t)e.nccl_comm;
+    cuda_ok(cudaMemcpyAsync(recv + (size_t)e.rank * n, send + (size_t)e.rank * n, sizeof(double) * n,
+                            cudaMemcpyDeviceToDevice, s),
+            "a2a own block");
+    nccl_check(api().GroupStart(), "ncclGroupStart");
+    for (int g = 0; g < e.a2a.G; ++g) {
+        if (g == e.rank) continue;
+        nccl_check(api().Send(send + (size_t)g * n, n, ncclFloat64, g, c, s), "ncclSend a2a");
+        nccl_check(api().Recv(recv + (size_t)g * n, n, ncclFloat64, g, c, s), "ncclRecv a2a");
+    }
+    nccl_check(api().GroupEnd(), "ncclGroupEnd");
+}
+
+// the ring halo of the distributed FFT (G > 1): my first M rows to rank - 1,
+// my last M to rank + 1 (mod G); d_alias holds them packed
+// [side][batch][dim][M][Nx], the received rows land in a2a_alias_recv
+// (side 0 from rank - 1, side 1 from rank + 1)
+void a2a_nccl_alias(Engine& e, int batch, cudaStream_t s) {
+    const int G = e.a2a.G;
+    const size_t side = (size_t)batch * e.dim * e.M * e.plan.N[0];
+    double* send = e.a2a.d_alias;
+    double* recv = a2a_alias_recv(e, batch);
+    const int lo = (e.rank + G - 1) % G, hi = (e.rank + 1) % G;
+    const ncclComm_t c = (ncclComm_t)e.nccl_comm;
+    nccl_check(api().GroupStart(), "ncclGroupStart");
+    nccl_check(api().Send(send, side, ncclFloat64, lo, c, s), "ncclSend ring low");
+    nccl_check(api().Recv(recv + side, side, ncclFloat64, hi, c, s), "ncclRecv ring high");
+    nccl_check(api().Send(send + side, side, ncclFloat64, hi, c, s), "ncclSend ring high");
+    nccl_check(api().Recv(recv, side, ncclFloat64, lo, c, s), "ncclRecv ring low");
+    nccl_check(api().GroupEnd(), "ncclGroupEnd");
 }
 
 void comm_allreduce(Engine& e, double* d, int n, cudaStream_t s) {

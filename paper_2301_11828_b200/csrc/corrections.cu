@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(128) k_wrap_tab(const double* __restrict__ u, 
                                                   int64_t band2, const double* __restrict__ ghost, int64_t gs_bc,
                                                   int64_t gs_side, int lo_int, int hi_int,
                                                   const double* __restrict__ xstrip,
-                                                  const uint8_t* __restrict__ smask) {
+                                                  const uint8_t* __restrict__ smask, double gsign, int glob) {
     pdl_entry();
     constexpr int NP = D * (D + 1) / 2;
     constexpr int KS = (NP + 1) & ~1;
@@ -510,8 +510,12 @@ __global__ void __launch_bounds__(128) k_wrap_tab(const double* __restrict__ u, 
         }
         if ((fl & 2) && ghost) {
             const int sd = (fl >> 2) & 1;
-            if (sd ? hi_int : lo_int) {
-                const int gl = (fl >> 3) & 31;
+            // distributed FFT (gsign < 0): across a global face every such entry
+            // is aliased; across an interior face only those that also leave
+            // along x (the FFT wrapped them circularly there)
+            const bool use = gsign > 0.0 || ((glob >> sd) & 1) || (fl & 128);
+            if ((sd ? hi_int : lo_int) && use) {
+                const int gl = (fl >> 3) & 15;
                 const int64_t pidx = pin + (fl >> 8);
 #pragma unroll
                 for (int bb = 0; bb < D; ++bb) {
@@ -546,7 +550,9 @@ __global__ void __launch_bounds__(128) k_wrap_tab(const double* __restrict__ u, 
     }
 #pragma unroll
     for (int a = 0; a < D; ++a) {
-        double dv = ((cm >> a) & 1u) ? 0.0 : gacc[a] - acc[a];
+        // gsign: +1 halo slabs (true neighbour rows), -1 distributed FFT (aliases
+        // of the opposite global end, subtracted like the local ones)
+        double dv = ((cm >> a) & 1u) ? 0.0 : gsign * gacc[a] - acc[a];
         if (FOLD && !((smk >> a) & 1u)) {
             double sa = 0.0;
 #pragma unroll
@@ -761,6 +767,11 @@ static void build_face_table(Engine& e, const std::vector<int>& rows, const std:
 // the d_wK table built below (same storage order)
 static void build_state_table(Engine& e, const std::vector<int>& rows, const std::vector<int>& o0s) {
     const Plan& pl = e.plan;
+    // distributed FFT: along the slowest axis (global, periodic over Nyg) an
+    // entry leaving the slab aliases only at the global faces, onto the
+    // opposite end's rows -- every such entry becomes a ghost entry (with the
+    // wrapped x offset when it also leaves along x), none a local alias
+    const bool a2a = e.a2a.G > 0;
     const int dim = e.dim, M = e.M, S = 2 * M + 1;
     for (int a = 0; a < dim; ++a)
         if (pl.N[a] < S || (a < 2 && pl.N[a] > 32767)) return;  // k_wrap's general path
@@ -790,13 +801,17 @@ static void build_state_table(Engine& e, const std::vector<int>& rows, const std
                     else if (s_ > M) out[a] = o[a] > (s_ - M - 1);              // high face, depth s-M-1
                     if (!out[a]) continue;
                     any = true;
-                    if (pl.circ[a]) shift[a] = s_ <= M ? pl.N[a] : -pl.N[a];
+                    if (pl.circ[a] && !(a2a && a == SA)) shift[a] = s_ <= M ? pl.N[a] : -pl.N[a];
                     else alias = false;
                 }
                 if (!any) continue;
-                // ghost rows: out along the slowest axis only
+                // ghost rows: out along the slowest axis only (distributed FFT:
+                // out along it at all, other axes wrapped where they alias)
                 bool gh = out[SA];
-                for (int a = 0; a < SA; ++a) gh = gh && !out[a];
+                if (!a2a)
+                    for (int a = 0; a < SA; ++a) gh = gh && !out[a];
+                else
+                    for (int a = 0; a < SA; ++a) gh = gh && (!out[a] || pl.circ[a]);
                 if (!alias && !gh) continue;
                 int fl = alias ? 1 : 0;
                 if (gh) {
@@ -805,8 +820,14 @@ static void build_state_table(Engine& e, const std::vector<int>& rows, const std
                     const int c = side == 0 ? depth : pl.N[SA] - 1 - depth;  // coordinate of p along SA
                     const int w = c + o[SA];
                     const int gl = side == 0 ? w + M : w - pl.N[SA];
-                    const int goff = dim == 3 ? o[0] + pl.N[0] * o[1] : o[0];
-                    fl |= 2 | (side << 2) | (gl << 3) | (goff << 8);
+                    int ow[3] = {o[0], o[1], o[2]};
+                    if (a2a)
+                        for (int a = 0; a < SA; ++a)
+                            if (out[a]) ow[a] += sa[a] <= M ? pl.N[a] : -pl.N[a];
+                    const int goff = dim == 3 ? ow[0] + pl.N[0] * ow[1] : ow[0];
+                    bool xo = false;  // also leaves along a faster axis (distributed FFT: aliased there too)
+                    for (int a = 0; a < SA; ++a) xo = xo || out[a];
+                    fl |= 2 | (side << 2) | (gl << 3) | (xo ? 128 : 0) | (goff << 8);
                 }
                 // wrapped displacement: x and y in 16 bits each, z in 32
                 const int w0 = o[0] + shift[0], w1 = o[1] + shift[1], w2 = o[2] + shift[2];
@@ -815,6 +836,8 @@ static void build_state_table(Engine& e, const std::vector<int>& rows, const std
     }
     sidx.push_back((int)tab.size());
     if (tab.empty()) tab.push_back(make_int4(0, 0, 0, 0));
+    if (e.d_sidx) cudaFree(e.d_sidx);
+    if (e.d_stab) cudaFree(e.d_stab);
     check(cudaMalloc((void**)&e.d_sidx, sizeof(int) * sidx.size()), "alloc state index");
     check(cudaMemcpy(e.d_sidx, sidx.data(), sizeof(int) * sidx.size(), cudaMemcpyHostToDevice), "copy state index");
     check(cudaMalloc((void**)&e.d_stab, sizeof(int4) * tab.size()), "alloc state table");
@@ -887,8 +910,13 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
                             const uint8_t* cmask) {
     const Plan& pl = e.plan;
     const int SA = pl.dim - 1;
-    const int lo_int = e.slab.global >= 0 && e.slab.off > 0;
-    const int hi_int = e.slab.global >= 0 && e.slab.off + pl.N[SA] < e.slab.global;
+    // ghost faces: halo slabs add the true neighbour rows at interior faces;
+    // the distributed FFT subtracts the opposite end's rows at the global faces
+    const bool a2a = e.a2a.G > 0;
+    const int lo_int = a2a ? 1 : (e.slab.global >= 0 && e.slab.off > 0);
+    const int hi_int = a2a ? 1 : (e.slab.global >= 0 && e.slab.off + pl.N[SA] < e.slab.global);
+    const double gsign = a2a ? -1.0 : 1.0;
+    const int glob = a2a ? ((e.a2a.rank == 0 ? 1 : 0) | (e.a2a.rank == e.a2a.G - 1 ? 2 : 0)) : 0;
     const double* ghost = e.ghost_view && (lo_int || hi_int) ? e.ghost_view : nullptr;
     int64_t band[3] = {0, 0, 0};
     for (int d = 0; d < pl.dim; ++d) {
@@ -955,7 +983,8 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
 #define PDGPU_WT(D, L, FD, XS)                                                                                        \
     launch_maybe_pdl(e.pdl, k_wrap_tab<D, L, FD>, dim3(tb), dim3(th), 0, s, u, f, e.d_sidx, e.d_stab, e.d_wK, e.M,    \
                      pl.N[0], pl.N[1], pl.N[2], pl.circ_mask, cmask, pl.nodes, batch, scale, band[0], band[1],       \
-                     band[2], ghost, e.ghost_bc_stride, e.ghost_side_stride, lo_int, hi_int, XS, e.d_cmask)
+                     band[2], ghost, e.ghost_bc_stride, e.ghost_side_stride, lo_int, hi_int, XS, e.d_cmask,   \
+                     gsign, glob)
         if (pl.dim == 2) {
             if (quad) {
                 if (fold) PDGPU_WT(2, 4, true, nullptr);

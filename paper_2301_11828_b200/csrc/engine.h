@@ -57,6 +57,25 @@ struct Constraint {
     double value;
 };
 
+// All-to-all distributed FFT (north_star's transpose scheme; the
+// halo slabs are the default multi-GPU path).  Rank `rank` of G owns rows
+// [r0[rank], r0[rank+1]) of an Nx x Nyg lattice for the x passes and the
+// half-spectrum columns [k0[rank], k0[rank+1]) for the y pass; two all-to-all
+// transposes move the spectrum between the layouts (blocks padded to
+// Kmax x Rmax so every peer block has one size).  Global y faces: the wrap
+// correction subtracts the aliased terms from the opposite end's M rows.
+struct A2A {
+    int G = 0, rank = 0, Nyg = 0;       // G > 0: on
+    std::vector<int> r0, k0;            // G + 1 boundaries each
+    int Rmax = 0, Kmax = 0;
+    Plan col;                           // this rank's columns: ncols = k0[rank+1]-k0[rank], Nl = Pl = Nyg
+    void* d_sym = nullptr;              // symbol of those columns
+    double2 *d_c1 = nullptr, *d_c2 = nullptr, *d_send = nullptr, *d_recv = nullptr;
+    int64_t cap = 0;                    // batch capacity of the buffers
+    int* d_bounds = nullptr;            // r0 (G+1) then k0 (G+1) on the device
+    double* d_alias = nullptr;          // [send|recv][side][batch][dim][M][Nx]: opposite-end rows
+};
+
 struct Engine {
     int device = 0;
     int num_sms = 148;
@@ -107,6 +126,8 @@ struct Engine {
     // fold_surface_next: the caller adds the corrections right after this
     // K.u, so the face passes may take D^e (surface_folded: they did)
     bool surf_default = false, fold_surface_next = false, surface_folded = false;
+    A2A a2a;
+    bool a2a_external = false;  // a single-process group driver runs the distributed-FFT phases
     bool pdl = false;           // launches of the current capture use programmatic dependent launch
     bool cg_direct = false;     // CG's operator: direct stencil sum instead of MSBFM (pdgpu_set_cg_operator)
     bool xstrip_ready = false;  // K1 of this K.u wrote d_xstrip (3D face passes read it)
@@ -322,6 +343,21 @@ void set_kernel_attributes();
 void direct_prepare(Engine& e);
 void launch_direct_apply(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
                          const uint8_t* cmask = nullptr);
+
+// transpose.cu (all-to-all distributed FFT)
+void a2a_setup(Engine& e, int G, int rank, int Nyg, const int* r0, const int* k0);
+void a2a_free(Engine& e);
+void a2a_ensure(Engine& e, int batch);
+int64_t a2a_block(const Engine& e, int batch);  // complex elements per peer block
+void a2a_phase1(Engine& e, const double* u, int batch, cudaStream_t s);  // K1 + pack -> d_send
+void a2a_phase2(Engine& e, int batch, cudaStream_t s);                   // unpack + K3 + pack -> d_send
+void a2a_phase3(Engine& e, double* f, int batch, cudaStream_t s, double scale, const uint8_t* cmask,
+                const double* body);                                       // unpack + K5
+void a2a_exchange(Engine& e, int batch, cudaStream_t s);                 // d_send -> d_recv (NCCL, or G = 1)
+void a2a_alias(Engine& e, const double* u, int batch, cudaStream_t s);   // opposite-end rows -> ghost_view
+double* a2a_alias_recv(Engine& e, int batch);                            // where the opposite-end rows land
+void a2a_nccl_exchange(Engine& e, int batch, cudaStream_t s);
+void a2a_nccl_alias(Engine& e, int batch, cudaStream_t s);
 
 // corrections.cu
 void build_wrap_table(Engine& e);

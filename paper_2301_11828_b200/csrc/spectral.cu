@@ -1749,14 +1749,15 @@ __global__ void __launch_bounds__(512) k_cfft_y_inv(const double2* __restrict__ 
 // Output layout [col][h][k][pair], ky = 2k + h.
 #if defined(PDGPU_ALL_PARTS) || PDGPU_PART == 0
 __global__ void k_build_symbol(void* sym, const double* __restrict__ K, int dim, int M, int np, int64_t ss,
-                               int ncols, int Pl, int P0, int P1, int P2, int real, double scale, int NH, int ns) {
+                               int ncols, int Pl, int P0, int P1, int P2, int real, double scale, int NH, int ns,
+                               int col0) {
     const int64_t nfreq = (int64_t)ncols * Pl;
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= nfreq) return;
     const int col = (int)(idx / Pl), kl = (int)(idx % Pl);
     int k0, k1, k2;
     if (dim == 2) {
-        k0 = col;
+        k0 = col + col0;  // col0: first column of a distributed-FFT rank's share
         k1 = kl;
         k2 = 0;
     } else {
@@ -2328,9 +2329,57 @@ void build_symbol(Engine& e) {
     const int th = 128;
     const int64_t blocks = (nfreq + th - 1) / th;
     k_build_symbol<<<(unsigned)blocks, th, 0, e.stream>>>(e.d_sym, e.d_K, e.dim, e.M, e.np, e.ss, pl.ncols, pl.Pl,
-                                                         pl.P[0], pl.P[1], pl.P[2], e.real_symbol ? 1 : 0, scale, pl.nh, ns);
+                                                         pl.P[0], pl.P[1], pl.P[2], e.real_symbol ? 1 : 0, scale, pl.nh, ns,
+                                                         0);
     check(cudaGetLastError(), "build_symbol launch");
     check(cudaStreamSynchronize(e.stream), "build_symbol");
+}
+
+// symbol of columns [col0, col0 + pl.ncols) of plan pl (2D distributed FFT)
+void build_symbol_cols(Engine& e, const Plan& pl, int col0, void** out) {
+    const int64_t nfreq = (int64_t)pl.ncols * pl.Pl;
+    const size_t elt = e.real_symbol ? sizeof(double) : sizeof(double2);
+    const int ns = e.real_symbol ? 4 : e.np;
+    if (*out) cudaFree(*out);
+    *out = nullptr;
+    check(cudaMalloc(out, elt * std::max<int64_t>(nfreq, 1) * ns), "alloc column symbol");
+    const double scale = 1.0 / ((double)pl.P[0] * (double)pl.P[1]);
+    const int th = 128;
+    k_build_symbol<<<(unsigned)((nfreq + th - 1) / th), th, 0, e.stream>>>(*out, e.d_K, 2, e.M, e.np, e.ss, pl.ncols,
+                                                                           pl.Pl, pl.P[0], pl.P[1], 1,
+                                                                           e.real_symbol ? 1 : 0, scale, 1, ns, col0);
+    check(cudaGetLastError(), "column symbol launch");
+    check(cudaStreamSynchronize(e.stream), "column symbol");
+}
+
+// K3 of a distributed-FFT rank: its columns (plan col, symbol sym) from in to out
+void launch_k3_2d_cols(Engine& e, const Plan& col, void* sym, const double2* in, double2* out, int batch,
+                       cudaStream_t s) {
+    Plan saved = e.plan;
+    void* ssym = e.d_sym;
+    double2* sS2 = e.d_S2;
+    double* sct = e.d_coltab;
+    e.plan.ncols = col.ncols;
+    e.plan.Nl = col.Nl;
+    e.plan.Pl = col.Pl;
+    e.plan.logPl = col.logPl;
+    e.plan.nh = 1;
+    e.d_sym = sym;
+    e.d_S2 = out;
+    e.d_coltab = nullptr;
+    try {
+        launch_k3_2d(e, in, batch, s);
+    } catch (...) {
+        e.plan = saved;
+        e.d_sym = ssym;
+        e.d_S2 = sS2;
+        e.d_coltab = sct;
+        throw;
+    }
+    e.plan = saved;
+    e.d_sym = ssym;
+    e.d_S2 = sS2;
+    e.d_coltab = sct;
 }
 
 void engine_alloc_workspace(Engine& e, int64_t batch) {
@@ -2357,6 +2406,18 @@ void engine_alloc_workspace(Engine& e, int64_t batch) {
 void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStream_t s, double scale,
                        const uint8_t* cmask, const double* body) {
     const Plan& pl = e.plan;
+    if (e.a2a.G > 0 && !e.a2a_external) {  // distributed FFT arm (transpose.cu), NCCL or one rank
+        a2a_phase1(e, u, batch, s);
+        a2a_exchange(e, batch, s);
+        a2a_phase2(e, batch, s);
+        a2a_exchange(e, batch, s);
+        a2a_phase3(e, f, batch, s, scale, cmask, body);
+        a2a_alias(e, u, batch, s);
+        PassTimer pt(e, kPassCorr, s);
+        launch_wrap_correction(e, u, f, batch, s, scale, cmask);
+        check(cudaGetLastError(), "fast_apply launch");
+        return;
+    }
     engine_alloc_workspace(e, batch);
     const int d = pl.dim;
     // halo slabs over NCCL: the M rows beyond each interior face travel on the

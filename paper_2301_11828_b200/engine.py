@@ -349,6 +349,16 @@ class FastForce:
                                              None if hist is None else _dp(hist), nhist))
         return x, it.value, rel.value, hist
 
+    def set_transpose(self, nranks: int, rank: int, global_rows: int, row_bounds=None, col_bounds=None):
+        """Distributed-FFT arm (pdgpu_set_transpose): this engine holds rows
+        row_bounds[rank]..row_bounds[rank+1] of an Nx x global_rows lattice and
+        the half-spectrum columns col_bounds[rank]..; balanced splits by default."""
+        rb, cb = transpose_splits(self.dims[0], global_rows, nranks)
+        rb = rb if row_bounds is None else [int(x) for x in row_bounds]
+        cb = cb if col_bounds is None else [int(x) for x in col_bounds]
+        _check(self._lib.pdgpu_set_transpose(self._h, int(nranks), int(rank), int(global_rows),
+                                             (C.c_int * len(rb))(*rb), (C.c_int * len(cb))(*cb)))
+
     def cg_operator(self, kind: str = "msbfm"):
         """CG's operator: "msbfm" (default) or "direct" (the direct stencil sum of the same K)."""
         if kind not in ("msbfm", "direct"):
@@ -425,6 +435,23 @@ class FastForce:
         t = C.c_double()
         _check(self._lib.pdgpu_sim_get(self._h, _dp(u), _dp(v), _dp(f), C.byref(t)))
         return u, v, f, t.value
+
+
+def transpose_splits(nx: int, global_rows: int, nranks: int):
+    """Balanced row and half-spectrum column splits of the distributed-FFT arm."""
+    hx = nx // 2 + 1
+    return ([global_rows * g // nranks for g in range(nranks + 1)], [hx * g // nranks for g in range(nranks + 1)])
+
+
+def group_matvec_transpose(engines, us, fs, batch: int = 1):
+    """One K.u over n engines of one process (pdgpu_group_matvec_transpose);
+    us / fs: per-engine device tensors [batch][dim][own rows * Nx]."""
+    lib = _lib.load()
+    n = len(engines)
+    hs = (C.c_void_p * n)(*[e.handle for e in engines])
+    up = (C.c_void_p * n)(*[_ptr(u) for u in us])
+    fp = (C.c_void_p * n)(*[_ptr(f) for f in fs])
+    _check(lib.pdgpu_group_matvec_transpose(hs, n, up, fp, int(batch)))
 
 
 def group_sim_step(engines, n_steps: int = 1, s0: float = -1.0, watch=None) -> int:
