@@ -1678,9 +1678,26 @@ __global__ void __launch_bounds__(512) k_cfft_y_fwd(const double2* __restrict__ 
 #pragma unroll
     for (int j = 0; j < R; ++j) xb[spad(t + j * T)] = v[j];
     __syncthreads();
-    for (int idx = threadIdx.x; idx < Py * nz; idx += blockDim.x) {
-        const int ky = idx / nz, z = idx - ky * nz;
-        S2[(((int64_t)bd * Hx + kx) * Py + ky) * Nz + z0 + z] = sm[(2 * z + (ky & 1)) * XB + spad(ky >> 1)];
+    // transposed store (runs of nz values per ky): a thread's SMEM reads first,
+    // then its global stores (a full tile is exactly R per thread)
+    {
+        const int tot = Py * nz;
+        double2* base = S2 + ((int64_t)bd * Hx + kx) * Py * Nz + z0;
+        for (int i0 = 0; i0 < tot; i0 += R * (int)blockDim.x) {
+            double2 g[R];
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+                const int idx = i0 + threadIdx.x + u * (int)blockDim.x;
+                const int ky = idx / nz, z = idx - ky * nz;
+                g[u] = idx < tot ? sm[(2 * z + (ky & 1)) * XB + spad(ky >> 1)] : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int u = 0; u < R; ++u) {
+                const int idx = i0 + threadIdx.x + u * (int)blockDim.x;
+                const int ky = idx / nz, z = idx - ky * nz;
+                if (idx < tot) base[(int64_t)ky * Nz + z] = g[u];
+            }
+        }
     }
 }
 
