@@ -729,7 +729,7 @@ void pdgpu_destroy(pdgpu_t h) {
     void* ptrs[] = {h->d_xstrip, h->d_lidx, h->d_loff, h->d_lK, h->d_sidx, h->d_stab, h->d_fidx, h->d_ftab, h->d_vh, h->d_wrows, h->d_wo0, h->d_wK, h->d_tw, h->d_sym, h->d_K, h->d_offs, h->d_disp, h->d_S1, h->d_S2, h->d_u_stage, h->d_f_stage,
                     h->d_cmask, h->d_surf_rows, h->d_surf_de, h->d_ledger, h->d_bond_rows, h->d_listed,
                     h->d_counters, h->d_new_pairs, h->d_body, h->d_cdofs, h->d_cval, h->d_ckind, h->d_u, h->d_v,
-                    h->d_f, h->d_fprev, h->d_red, h->d_scal, h->d_ticket, h->d_cg, h->d_coltab,
+                    h->d_f, h->d_fprev, h->d_red, h->d_scal, h->d_ticket, h->d_cg, h->d_coltab, h->d_symh,
                     h->d_scratch, h->d_kc, h->d_uc_ids, h->d_uc_val, h->d_face_recv, h->d_halo,
                     h->d_mon_nodes, h->d_mon_rows};
     for (void* p : ptrs)

@@ -138,6 +138,11 @@ struct Engine {
     double* d_kc = nullptr;         // centre coefficients (3D direct stencil)
     double* d_coltab = nullptr;     // separable symbol: per column n_pairs x (M+1) coefficients (2D)
     int coltab_oddmask = 0;         // bit p: pair p odd along the column axis (sin terms)
+    double* d_symh = nullptr;       // 2D real symbol mirrored along the column axis: per column the planes
+                                    // xx, xy, yy over ky in [0, Pl/2] (symh_stride doubles each); K3 lands a
+                                    // column's planes in shared memory by one bulk copy
+    const void* symh_for = nullptr;  // the d_sym these planes were cut from
+    int symh_stride = 0;
     double2* d_scratch = nullptr;   // per-CTA component park of the two-CTA/SM spectral kernel
     int64_t scratch_cap = 0;
     int* d_offs = nullptr;          // nof*3
@@ -335,6 +340,7 @@ void plan_init(Plan& pl, int dim, const int* dims, int M);
 void engine_alloc_workspace(Engine& e, int64_t batch);
 void build_twiddles(Engine& e);
 void build_symbol(Engine& e);
+void build_symbol_half(Engine& e);
 void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStream_t s,
                        double scale, const uint8_t* cmask, const double* body);
 void set_kernel_attributes();

@@ -425,8 +425,16 @@ __device__ __forceinline__ int nat_slot(int t, int j) {
     else return spad(t + j * T);
 }
 
-template <int LOGQ, int LOGR, int S, int P, int LOGNS, bool SPLIT, class Bar>
-__device__ __forceinline__ void fft_passes(double2 (&v)[1 << LOGR], int t, double2* xb, const FftTw& tws, Bar bar) {
+// Hook: called once, behind the last exchange's closing barrier -- from there
+// on the exchange buffer is free while the last pass runs in registers (the
+// caller may start an asynchronous copy into it).
+struct NoHook {
+    __device__ __forceinline__ void operator()() const {}
+};
+
+template <int LOGQ, int LOGR, int S, int P, int LOGNS, bool SPLIT, class Bar, class Hook>
+__device__ __forceinline__ void fft_passes(double2 (&v)[1 << LOGR], int t, double2* xb, const FftTw& tws, Bar bar,
+                                           Hook hook) {
     using Sh = FftShape<LOGQ, LOGR>;
     if constexpr (P < Sh::NPASS) {
         constexpr int LR = (P == Sh::NPASS - 1 && Sh::LOGREM) ? Sh::LOGREM : LOGR;
@@ -434,7 +442,8 @@ __device__ __forceinline__ void fft_passes(double2 (&v)[1 << LOGR], int t, doubl
         if constexpr (P + 1 < Sh::NPASS) {
             if constexpr (SPLIT) fft_exchange_split<LOGQ, LOGR, LR, LOGNS>(v, t, reinterpret_cast<double*>(xb), bar);
             else fft_exchange<LOGQ, LOGR, LR, LOGNS>(v, t, xb, bar);
-            fft_passes<LOGQ, LOGR, S, P + 1, LOGNS + LR, SPLIT>(v, t, xb, tws, bar);
+            if constexpr (P + 2 == Sh::NPASS) hook();
+            fft_passes<LOGQ, LOGR, S, P + 1, LOGNS + LR, SPLIT>(v, t, xb, tws, bar, hook);
         }
     }
 }
@@ -445,12 +454,12 @@ __device__ __forceinline__ void fft_passes(double2 (&v)[1 << LOGR], int t, doubl
 // a barrier covering every thread of the transform (all groups of a CTA in
 // lockstep use __syncthreads).  SPLIT: xb holds XBUF 8-byte slots instead
 // (fft_exchange_split).
-template <int LOGQ, int LOGRMAX, int S, class Bar, bool SPLIT = false>
+template <int LOGQ, int LOGRMAX, int S, class Bar, bool SPLIT = false, class Hook = NoHook>
 __device__ __forceinline__ void reg_fft(double2 (&v)[1 << FftShape<LOGQ, LOGRMAX>::LOGR], int t, double2* xb,
-                                        const FftTw& tws, Bar bar) {
+                                        const FftTw& tws, Bar bar, Hook hook = Hook{}) {
     using Sh = FftShape<LOGQ, LOGRMAX>;
     static_assert(Sh::NPASS <= 4, "at most three twiddled passes");
-    fft_passes<LOGQ, Sh::LOGR, S, 0, 0, SPLIT>(v, t, xb, tws, bar);
+    fft_passes<LOGQ, Sh::LOGR, S, 0, 0, SPLIT>(v, t, xb, tws, bar, hook);
 }
 
 struct BlockBar {

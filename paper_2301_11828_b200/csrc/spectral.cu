@@ -860,7 +860,8 @@ template <int LOGQ, bool CIRC, bool TSTORE = false, int CFM = 0>
 __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restrict__ u, double2* __restrict__ S,
                                                           int Nx, int Nrow, int nslab, int Hx,
                                                           const double2* __restrict__ tw, int logTWN,
-                                                          const __grid_constant__ CUtensorMap tm, int pf) {
+                                                          const __grid_constant__ CUtensorMap tm, int pf,
+                                                          int early) {
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
     constexpr int LOGTR = 11 - LOGQ;  // rows per tile: 2 * TR * T = 256 threads
@@ -883,12 +884,39 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
     // rows exactly fill the staging length (periodic, or padded power-of-two
     // rows): one TMA bulk copy per row, else per-thread cp.async with zero fill
     const bool bulk = Nx == rowlen;
-    __shared__ __align__(8) uint64_t bar;
+    __shared__ __align__(8) uint64_t bar, bar0;
     __shared__ double2 stw[FftTwTable<LOGQ, 4>::SIZE];
     fill_fft_tw_table<LOGQ, 4>(stw, tw, logTWN);
-    if (bulk && threadIdx.x == 0) mbar_init(&bar, 1);
+    if (bulk && threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        mbar_init(&bar0, 1);
+    }
     __syncthreads();
-    unsigned ph = 0;
+    unsigned ph = 0, ph0 = 0;
+    // TSTORE tiles with `early`: row 0 of the next tile lands in the exchange
+    // buffer (free from the end of the transforms to the next tile's first
+    // exchange, and large enough for one row) while this tile is post-processed
+    // and stored; only the remaining rows wait for the store to release the row
+    // buffers.
+    const bool split = TSTORE && early && bulk && rowlen <= 2 * TR * XB;
+    auto fetch_row0 = [&](int64_t tile) {
+        if (threadIdx.x == 0) {
+            const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
+            fence_proxy_async();
+            mbar_expect_tx(&bar0, (unsigned)(rowlen * 8));
+            bulk_load(xd, u + ((int64_t)slab * Nrow + row0) * Nx, rowlen * 8, &bar0);
+        }
+    };
+    auto fetch_rest = [&](int64_t tile) {
+        const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
+        const int nr = min(TR, Nrow - row0);
+        if (threadIdx.x == 0 && nr > 1) {
+            const double* src = u + ((int64_t)slab * Nrow + row0) * Nx;
+            fence_proxy_async();
+            mbar_expect_tx(&bar, (unsigned)((nr - 1) * rowlen * 8));
+            for (int rr = 1; rr < nr; ++rr) bulk_load(rowbuf + rr * RS, src + (int64_t)rr * Nx, rowlen * 8, &bar);
+        }
+    };
     auto fetch = [&](int64_t tile) {
         const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
         const int nr = min(TR, Nrow - row0);
@@ -916,7 +944,14 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
     const int rr = (threadIdx.x >> LA) & (TR - 1);
     const int a0 = ((threadIdx.x >> (LA + LOGTR)) << LA) + (threadIdx.x & ((1 << LA) - 1));
     int64_t tile = blockIdx.x;
-    if (tile < ntiles) fetch(tile);
+    if (tile < ntiles) {
+        if (split) {
+            fetch_row0(tile);
+            fetch_rest(tile);
+        } else {
+            fetch(tile);
+        }
+    }
     for (; tile < ntiles; tile += gridDim.x) {
         const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
         const int nr = min(TR, Nrow - row0);
@@ -929,7 +964,14 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
                 l2_prefetch(u + ((int64_t)ns * Nrow + nr0 + rr2) * Nx, rowlen * 8);
         }
         double2 v[R];
-        if (bulk) {
+        if (split) {
+            mbar_wait(&bar0, ph0);
+            ph0 ^= 1;
+            if (nr > 1) {
+                mbar_wait(&bar, ph);
+                ph ^= 1;
+            }
+        } else if (bulk) {
             mbar_wait(&bar, ph);  // rows past the lattice (nr < TR) hold stale data: never stored
             ph ^= 1;
         } else {
@@ -937,7 +979,7 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
         }
         __syncthreads();
         {
-            const double* st = rowbuf + r * RS;
+            const double* st = (split && r == 0) ? xd : rowbuf + r * RS;
             const double2 wbase = __ldg(tw + (opaque(t) << shE));
 #pragma unroll
             for (int j = 0; j < R; ++j) {
@@ -957,6 +999,7 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
 #pragma unroll
         for (int j = 0; j < R; ++j) spec[nat_slot<T>(t, j)] = v[j];
         __syncthreads();
+        if (split && tile + gridDim.x < ntiles) fetch_row0(tile + gridDim.x);
         const double2* E = reinterpret_cast<const double2*>(rowbuf + rr * RS);
         const double2* O = E + XB;
         double2* dst = S + (int64_t)slab * Hx * Nrow + row0 + rr;
@@ -1013,7 +1056,10 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
             }
             __syncthreads();
-            if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);
+            if (tile + gridDim.x < ntiles) {
+                if (split) fetch_rest(tile + gridDim.x);
+                else fetch(tile + gridDim.x);
+            }
             continue;
         }
 #pragma unroll 2
@@ -1640,6 +1686,178 @@ __global__ void __launch_bounds__(kPipeThreads, CPS) k_spectral2d_tm(const doubl
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tbase));
 }
 
+// ---------------------------------- K3, TMEM park + landed operands ---
+// k_spectral2d_tm<LOGQ, SYM, false> with the operands landed by TMA bulk
+// copies in the exchange buffer itself.  Behind the closing barrier of a
+// transform's last exchange the buffer is idle while the last pass runs in
+// registers: that is when the next operand column is requested (x_1 during
+// FFT(x_0), the next item's x_0 during the last inverse transform; XL = 2 also
+// the first half of the column's symbol rows during FFT(x_1); XL = 3 the
+// column's mirror planes, build_symbol_half, which carry every frequency), so
+// its latency sits behind the last pass, the TMEM park and the stores instead
+// of in front of a transform.  Costs one SMEM read of the column and one extra
+// barrier.
+template <int LOGQ, int SYM, int XL>
+__global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_tx(const double2* __restrict__ in, double2* out,
+                                                                 const void* __restrict__ sym, int ncols, int NC,
+                                                                 int batch, const double2* __restrict__ tw,
+                                                                 int logTWN, const double* __restrict__ symh,
+                                                                 int HP) {
+    using Sh = FftShape<LOGQ, kPipeLogR>;
+    constexpr int Q = Sh::Q, T = Sh::T, XB = Sh::XBUF, RR = Sh::R;
+    static_assert(RR == 16 && T % 128 == 0, "16 points per thread, whole TMEM lane quadrants per column");
+    static_assert(XL == 1 || SYM == 1, "symbol landing: real table only");
+    extern __shared__ double2 sm[];
+    __shared__ uint32_t tbase;
+    __shared__ __align__(8) uint64_t bars[kPipeThreads / 128];
+    __shared__ double2 stw[FftTwTable<LOGQ, kPipeLogR>::SIZE];
+    const int gi = threadIdx.x >> Sh::LOGT;
+    const int t = threadIdx.x & (T - 1);
+    double2* xb = sm + gi * XB;
+    const int warp = threadIdx.x >> 5;
+    fill_fft_tw_table<LOGQ, kPipeLogR>(stw, tw, logTWN);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(&tbase)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (t == 0) mbar_init(&bars[gi], 1);
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t ta = tbase + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(64 * (warp >> 2));
+    const int ngroups = (ncols + NC - 1) / NC;
+    const int64_t nitems = (int64_t)ngroups * batch;
+    const int64_t cstride = (int64_t)ncols * Q;
+    const uint64_t pol = l2_policy_evict_first();
+    constexpr unsigned xbytes = (unsigned)Q * 16u;
+    constexpr unsigned sbytes = (unsigned)Q * (SYM == 1 ? 4 * 8 : 3 * 16);
+    auto item_col = [&](int64_t item, int& b, int& col) {
+        b = (int)(item % batch);
+        col = (int)(item / batch) * NC + gi;
+        return col < ncols;
+    };
+    auto x0_of = [&](int b, int col) { return in + ((int64_t)(b * 2) * ncols + col) * Q; };
+    // one column-sized block into this column's exchange buffer (one thread)
+    auto land = [&](const void* src, unsigned bytes) {
+        if (t == 0) {
+            fence_proxy_async();
+            mbar_expect_tx(&bars[gi], bytes);
+            bulk_load(xb, src, bytes, &bars[gi]);
+        }
+    };
+    unsigned ph = 0;
+    auto landed = [&]() {
+        mbar_wait(&bars[gi], ph);
+        ph ^= 1;
+    };
+    {
+        int b, col;
+        if ((int64_t)blockIdx.x < nitems && item_col(blockIdx.x, b, col)) land(x0_of(b, col), xbytes);
+    }
+    for (int64_t it = blockIdx.x; it < nitems; it += gridDim.x) {
+        int b, col;
+        const bool valid = item_col(it, b, col);
+        const int cc = valid ? col : 0;
+        const double2* x0 = x0_of(b, cc);
+        double2* z0 = out + ((int64_t)(b * 2) * ncols + cc) * Q;
+        int b2, col2;
+        const bool nvalid = it + gridDim.x < nitems && item_col(it + gridDim.x, b2, col2);
+        if (valid && t == 0) {
+            // x_1 and the symbol rows into L2 behind FFT(x_0)
+            l2_prefetch(x0 + cstride, xbytes);
+            if (XL == 3) l2_prefetch(symh + (int64_t)cc * 3 * HP, (unsigned)(3 * HP * 8));
+            else l2_prefetch((const char*)sym + (int64_t)cc * sbytes, sbytes);
+        }
+        double2 v[RR];
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+            if (valid) landed();
+#pragma unroll
+            for (int j = 0; j < RR; ++j) v[j] = valid ? xb[t + j * T] : make_double2(0.0, 0.0);
+            __syncthreads();  // the column is in registers: the buffer takes the exchanges
+            reg_fft<LOGQ, kPipeLogR, -1, BlockBar, false>(
+                v, t, xb, make_fft_tw_s<LOGQ, kPipeLogR>(opaque(t), stw), BlockBar{}, [&]() {
+                    if (!valid) return;
+                    if (c == 0) land(x0 + cstride, xbytes);
+                    else if (XL == 2) land((const char*)sym + (int64_t)cc * sbytes, sbytes / 2);
+                    else if (XL == 3) land(symh + (int64_t)cc * 3 * HP, (unsigned)(3 * HP * 8));
+                });
+            if (c == 0) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tmem_st4(ta + 16 * q, v + 4 * q);
+                tmem_wait_st();
+            }
+        }
+        // 2 x 2 product, two frequencies per TMEM round trip; F0 replaces X0
+        const int64_t sbase = (int64_t)cc * Q;
+        if (XL >= 2 && valid) landed();
+        const double* hp = reinterpret_cast<const double*>(xb);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            double2 x0v[2], f0[2];
+            tmem_ld2_wait(ta + 8 * q, x0v[0], x0v[1]);
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int j = 2 * q + i;
+                double2 U[2], F[2];
+                U[0] = x0v[i];
+                U[1] = v[j];
+                if (XL == 3) {
+                    // frequency k = t + j*T from the planes over [0, Q/2]: the upper
+                    // half mirrored, xy odd
+                    const int k = t + j * T;
+                    const int kk = j < RR / 2 ? k : Q - k;
+                    const double gxx = valid ? hp[kk] : 0.0;
+                    const double gxy = valid ? (j < RR / 2 ? hp[HP + kk] : -hp[HP + kk]) : 0.0;
+                    const double gyy = valid ? hp[2 * HP + kk] : 0.0;
+                    F[0] = make_double2(gxx * U[0].x + gxy * U[1].x, gxx * U[0].y + gxy * U[1].y);
+                    F[1] = make_double2(gxy * U[0].x + gyy * U[1].x, gxy * U[0].y + gyy * U[1].y);
+                } else if (XL == 2 && j < RR / 2) {
+                    // symbol rows t + j*T, j < 8: the landed first half of the column's table
+                    const double2 g01 = valid ? xb[2 * (t + j * T)] : make_double2(0.0, 0.0);
+                    const double2 g23 = valid ? xb[2 * (t + j * T) + 1] : make_double2(0.0, 0.0);
+                    F[0] = make_double2(g01.x * U[0].x + g01.y * U[1].x, g01.x * U[0].y + g01.y * U[1].y);
+                    F[1] = make_double2(g01.y * U[0].x + g23.x * U[1].x, g01.y * U[0].y + g23.x * U[1].y);
+                } else {
+                    symbol_product<2, SYM == 1>(F, U, sym, sbase + t + j * T);
+                }
+                f0[i] = F[0];
+                v[j] = F[1];
+            }
+            tmem_st2(ta + 8 * q, f0[0], f0[1]);
+        }
+        if (XL >= 2) __syncthreads();  // symbol rows read: the buffer takes the exchanges
+        if (nvalid && t == 0) l2_prefetch(x0_of(b2, col2), xbytes);
+#pragma unroll 1
+        for (int ai = 0; ai < 2; ++ai) {
+            const int a = 1 - ai;
+            if (ai == 1) {
+                tmem_wait_st();
+                TmemQuad tq[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) tmem_ld4(ta + 16 * q, tq[q]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    tmem_wait_ld(tq[q]);
+                    tmem_unpack4(tq[q], v + 4 * q);
+                }
+            }
+            reg_fft<LOGQ, kPipeLogR, 1, BlockBar, false>(v, t, xb, make_fft_tw_s<LOGQ, kPipeLogR>(opaque(t), stw),
+                                                         BlockBar{}, [&]() {
+                                                             if (ai == 1 && nvalid) land(x0_of(b2, col2), xbytes);
+                                                         });
+            double2* dst = z0 + a * cstride;
+            if (valid) {
+#pragma unroll
+                for (int j = 0; j < RR; ++j) st_hint(dst + t + j * T, v[j], pol);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tbase));
+}
+
 // ------------------------------------------------------- K2 / K4 (3D) ---
 // CIRC (periodic y, Py = Ny = 2Q): even/odd outputs by a decimation-in-
 // frequency stage (as in k_rfft_rows); K4 keeps all 2Q outputs.
@@ -1921,6 +2139,11 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
         // (measured 2.21 -> 2.7 / 3.1 ms at 4096^2 x 16 with 1 / 2 tiles ahead)
         const char* pfenv = getenv("PDGPU_K1_PF");
         const int k1pf = pfenv ? atoi(pfenv) : 0;
+        // PDGPU_K1_EARLY=1: row 0 of the next tile is requested into the
+        // exchange buffer before the post-processing, the rest after the TMA
+        // store has read its block (measured slower: K1 2.25 -> 2.30 ms; off)
+        const char* eenv = getenv("PDGPU_K1_EARLY");
+        const int k1early = (eenv && eenv[0] == '1') ? 1 : 0;
         const char* cfenv = getenv("PDGPU_K1_CF");
         const int cfm = (cx && lqx == 10 && cfenv && cfenv[0] == '1') ? 1 : 0;
         const size_t dsm = (size_t)k1_duo_smem(lqx, cx, cfm);
@@ -1937,10 +2160,10 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
             const bool tst = cx && DTR <= 2 && !(tenv && tenv[0] == '0') && encode_box_map(tm, e.d_S1, Ny, pl.Hx, nslab, DTR) &&
                              (size_t)(((pl.Hx + 255) / 256) * 256 * DTR * 16 + 128) <= dsm;
 #define PDGPU_K1T(CF) k_rfft_rows_duo<LQ, true, true, CF><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, \
-                                                                                e.d_tw, pl.logTWN, tm, k1pf)
+                                                                                e.d_tw, pl.logTWN, tm, k1pf, k1early)
 #define PDGPU_K1D(C) (tst ? (cfm == 1 ? PDGPU_K1T(1) : PDGPU_K1T(0))                                     \
                       : k_rfft_rows_duo<LQ, C><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, e.d_tw, \
-                                                                      pl.logTWN, tm, k1pf))
+                                                                      pl.logTWN, tm, k1pf, k1early))
             switch (lqx) {
                 PDGPU_CASE(6, (cx ? PDGPU_K1D(true) : PDGPU_K1D(false)))
                 PDGPU_CASE(7, (cx ? PDGPU_K1D(true) : PDGPU_K1D(false)))
@@ -2102,6 +2325,10 @@ static void set_attrs_k3_l() {
         smem_attr((const void*)k_spectral2d_tm<L, 1, false, 3>);
         smem_attr((const void*)k_spectral2d_tm<L, 0, true>);
         smem_attr((const void*)k_spectral2d_tm<L, 1, true>);
+        smem_attr((const void*)k_spectral2d_tx<L, 0, 1>);
+        smem_attr((const void*)k_spectral2d_tx<L, 1, 1>);
+        smem_attr((const void*)k_spectral2d_tx<L, 1, 2>);
+        smem_attr((const void*)k_spectral2d_tx<L, 1, 3>);
     }
     smem_attr((const void*)k_spectral2d_pipe<L, 0>);
     smem_attr((const void*)k_spectral2d_pipe<L, 1>);
@@ -2149,8 +2376,32 @@ void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s) {
 #define TM_L(LQV, LANDV)                                                                          \
     (mode == 1 ? k_spectral2d_tm<LQV, 1, LANDV><<<tgrid, kPipeThreads, tsmem, s>>>(TM_ARGS)       \
                : k_spectral2d_tm<LQV, 0, LANDV><<<tgrid, kPipeThreads, tsmem, s>>>(TM_ARGS))
+        // PDGPU_K3=tx / tx2: operands (tx2: and half the symbol rows) landed in
+        // the exchange buffer behind each transform's last exchange
+        // (4096-point columns, measured on one B200 at 4096^2 x 16: 2.68 -> 2.51 ms;
+        // tx2 2.55 ms -- the 32-byte symbol rows read at a two-way bank conflict;
+        // 2048-point columns 0.636 -> 0.646 ms, so those keep the register loads).
+        // PDGPU_K3=tm: the register-load kernel at every length.
+        const std::string k3s = k3env ? k3env : "";
+        // tx3: the symbol from the column's mirror planes, landed the same way
+        // (no symbol load left in the product; needs build_symbol_half's table)
+        const bool symh_ok = e.d_symh && e.symh_for == e.d_sym && lq == 12 && mode == 1;
+        int xl = k3s == "tx2" ? 2 : k3s == "tx" ? 1 : ((k3s == "tx3" || k3s.empty()) && lq == 12) ? 3 : 0;
+        if (xl == 3 && !symh_ok) xl = 1;
+        if (xl == 2 && mode != 1) xl = 1;
         const char* t3 = getenv("PDGPU_K3_TM3");  // three CTAs per SM (80 registers, spills)
-        if (lq == 12 && mode == 1 && !land && t3 && t3[0] == '1') {
+        if (xl) {
+#define TX_ARGS TM_ARGS, e.d_symh, e.symh_stride
+#define TX_L(LQV)                                                                                          \
+    (mode == 1 ? (xl == 3   ? k_spectral2d_tx<LQV, 1, 3><<<tgrid, kPipeThreads, tsmem, s>>>(TX_ARGS)        \
+                  : xl == 2 ? k_spectral2d_tx<LQV, 1, 2><<<tgrid, kPipeThreads, tsmem, s>>>(TX_ARGS)        \
+                            : k_spectral2d_tx<LQV, 1, 1><<<tgrid, kPipeThreads, tsmem, s>>>(TX_ARGS))       \
+               : k_spectral2d_tx<LQV, 0, 1><<<tgrid, kPipeThreads, tsmem, s>>>(TX_ARGS))
+            if (lq == 12) TX_L(12);
+            else TX_L(11);
+#undef TX_L
+#undef TX_ARGS
+        } else if (lq == 12 && mode == 1 && !land && t3 && t3[0] == '1') {
             const unsigned g3 = (unsigned)std::min<int64_t>(nitems, (int64_t)e.num_sms * 3);
             k_spectral2d_tm<12, 1, false, 3><<<g3, kPipeThreads, tsmem, s>>>(TM_ARGS);
         } else if (lq == 12) {
@@ -2350,6 +2601,67 @@ void build_symbol(Engine& e) {
                                                          0);
     check(cudaGetLastError(), "build_symbol launch");
     check(cudaStreamSynchronize(e.stream), "build_symbol");
+    build_symbol_half(e);
+}
+
+// Mirror planes of the 2D real symbol for 4096-point periodic columns.  A
+// stencil of definite parity along y (the physical kernels: xx and yy even, xy
+// odd, kernel.hpp:109-116) has H(kx, Pl - ky) = +-H(kx, ky), so the planes over
+// ky in [0, Pl/2] carry the whole column: 24 bytes per two frequencies instead
+// of 64, small enough to land in K3's exchange buffer.  The identity is
+// checked on the table itself; any other stencil keeps the full table.
+__global__ void k_symbol_half(const double* __restrict__ sym, double* __restrict__ symh, int ncols, int Q, int HP,
+                              unsigned long long* __restrict__ stat) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int nk = Q / 2 + 1;
+    double dmax = 0.0, hmax = 0.0;
+    if (i < (int64_t)ncols * nk) {
+        const int col = (int)(i / nk), k = (int)(i % nk);
+        const double* a = sym + ((int64_t)col * Q + k) * 4;
+        const double* m = sym + ((int64_t)col * Q + ((Q - k) & (Q - 1))) * 4;
+#pragma unroll
+        for (int p = 0; p < 3; ++p) {
+            const double v = a[p];
+            symh[((int64_t)col * 3 + p) * HP + k] = v;
+            dmax = fmax(dmax, fabs(m[p] - (p == 1 ? -v : v)));
+            hmax = fmax(hmax, fabs(v));
+        }
+    }
+    // non-negative doubles order like their bit patterns
+    atomicMax(stat, (unsigned long long)__double_as_longlong(dmax));
+    atomicMax(stat + 1, (unsigned long long)__double_as_longlong(hmax));
+}
+
+void build_symbol_half(Engine& e) {
+    const Plan& pl = e.plan;
+    if (e.d_symh) cudaFree(e.d_symh);
+    e.d_symh = nullptr;
+    e.symh_for = nullptr;
+    if (e.dim != 2 || !e.real_symbol || pl.nh != 1 || pl.logPl != 12 || getenv("PDGPU_NO_SYMH")) return;
+    const int Q = pl.Pl, HP = Q / 2 + 8;
+    unsigned long long* d_stat = nullptr;
+    check(cudaMalloc(&e.d_symh, sizeof(double) * (size_t)pl.ncols * 3 * HP), "alloc symbol planes");
+    check(cudaMalloc(&d_stat, 2 * sizeof(unsigned long long)), "alloc symbol stat");
+    check(cudaMemsetAsync(e.d_symh, 0, sizeof(double) * (size_t)pl.ncols * 3 * HP, e.stream), "symbol planes");
+    check(cudaMemsetAsync(d_stat, 0, 2 * sizeof(unsigned long long), e.stream), "symbol stat");
+    const int64_t n = (int64_t)pl.ncols * (Q / 2 + 1);
+    k_symbol_half<<<(unsigned)((n + 255) / 256), 256, 0, e.stream>>>((const double*)e.d_sym, e.d_symh, pl.ncols, Q, HP,
+                                                                   d_stat);
+    check(cudaGetLastError(), "symbol planes launch");
+    unsigned long long h[2];
+    check(cudaMemcpyAsync(h, d_stat, sizeof(h), cudaMemcpyDeviceToHost, e.stream), "symbol stat copy");
+    check(cudaStreamSynchronize(e.stream), "symbol planes");
+    cudaFree(d_stat);
+    double dmax, hmax;
+    memcpy(&dmax, &h[0], 8);
+    memcpy(&hmax, &h[1], 8);
+    if (dmax <= 1e-14 * hmax) {
+        e.symh_for = e.d_sym;
+        e.symh_stride = HP;
+    } else {
+        cudaFree(e.d_symh);
+        e.d_symh = nullptr;
+    }
 }
 
 // symbol of columns [col0, col0 + pl.ncols) of plan pl (2D distributed FFT)
