@@ -142,6 +142,7 @@ struct Engine {
                                     // xx, xy, yy over ky in [0, Pl/2] (symh_stride doubles each); K3 lands a
                                     // column's planes in shared memory by one bulk copy
     const void* symh_for = nullptr;  // the d_sym these planes were cut from
+    bool s2_blocked = false;         // 2D: K3 wrote S2 row-blocked, [slab][row / 8][kx][row % 8] (K5 reads it so)
     int symh_stride = 0;
     double2* d_scratch = nullptr;   // per-CTA component park of the two-CTA/SM spectral kernel
     int64_t scratch_cap = 0;

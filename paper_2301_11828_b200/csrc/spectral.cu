@@ -134,7 +134,10 @@ static int xbuf_stride_t_h(int logq) { return xbuf_stride_t(xbuf_slots(logq), th
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-static bool encode_box_map(CUtensorMap& m, const double2* S, int Nrow, int Hx, int nslab, int TR) {
+// blocked: the row-blocked spectrum [slab][row / 8][kx][row % 8] (2D S2 between
+// K3 and K5, launch_k3_2d) -- x = 2 * (row % 8), z = slab * (Nrow / 8) + row / 8
+static bool encode_box_map(CUtensorMap& m, const double2* S, int Nrow, int Hx, int nslab, int TR,
+                           bool blocked = false) {
     static EncodeTiledFn enc = nullptr;
     if (!enc) {
         cudaDriverEntryPointQueryResult q;
@@ -146,6 +149,12 @@ static bool encode_box_map(CUtensorMap& m, const double2* S, int Nrow, int Hx, i
     }
     cuuint64_t dims[3] = {(cuuint64_t)2 * Nrow, (cuuint64_t)Hx, (cuuint64_t)nslab};
     cuuint64_t strides[2] = {(cuuint64_t)Nrow * 16, (cuuint64_t)Hx * Nrow * 16};
+    if (blocked) {
+        dims[0] = 16;
+        dims[2] = (cuuint64_t)nslab * (Nrow / 8);
+        strides[0] = 128;
+        strides[1] = (cuuint64_t)Hx * 128;
+    }
     cuuint32_t box[3] = {(cuuint32_t)(2 * TR), 256, 1};
     cuuint32_t es[3] = {1, 1, 1};
     return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)S, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -329,7 +338,7 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
                                                     const uint8_t* __restrict__ cmask,
                                                     const double* __restrict__ body, int64_t nodes,
                                                     const __grid_constant__ CUtensorMap tm, int pf,
-                                                    const double* __restrict__ fx, int Mfx) {
+                                                    const double* __restrict__ fx, int Mfx, int blk = 0) {
     pdl_entry();
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R;
@@ -374,14 +383,21 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
             __syncthreads();
             if (threadIdx.x == 0) {
                 mbar_expect_tx(&bar, (unsigned)(nbox * 256 * TR * 16));
-                for (int bx = 0; bx < nbox; ++bx) tma_load_3d(&tm, land + bx * 256 * TR, &bar, 2 * row0, bx * 256, slab);
+                // blk: S is row-blocked, [slab][row / 8][kx][row % 8] (see encode_box_map)
+                const int cx0 = blk ? 2 * (row0 & 7) : 2 * row0;
+                const int cz0 = blk ? slab * (Nrow >> 3) + (row0 >> 3) : slab;
+                for (int bx = 0; bx < nbox; ++bx) tma_load_3d(&tm, land + bx * 256 * TR, &bar, cx0, bx * 256, cz0);
                 // the block of the CTA that starts pf CTAs later (launch order:
                 // x fastest) into L2, so its landing is an L2 hit
                 if (pf) {
                     const int64_t nxt = (int64_t)blockIdx.y * gridDim.x + blockIdx.x + pf;
                     const int by = (int)(nxt / gridDim.x), bxx = (int)(nxt % gridDim.x);
-                    if (by < (int)gridDim.y)
-                        for (int bx = 0; bx < nbox; ++bx) tma_prefetch_3d(&tm, 2 * bxx * TR, bx * 256, by);
+                    if (by < (int)gridDim.y) {
+                        const int r1 = bxx * TR;
+                        const int cx1 = blk ? 2 * (r1 & 7) : 2 * r1;
+                        const int cz1 = blk ? by * (Nrow >> 3) + (r1 >> 3) : by;
+                        for (int bx = 0; bx < nbox; ++bx) tma_prefetch_3d(&tm, cx1, bx * 256, cz1);
+                    }
                 }
             }
             mbar_wait(&bar, 0);
@@ -519,6 +535,175 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
         const double2 zo = sm[(2 * rr + 1) * XB + spad(m)];
         emit(rr, m, cadd(ze, zo));
         if (CIRC) emit(rr, m + Q, csub(ze, zo));
+    }
+}
+
+// ------------------------------------- K5, persistent, two row groups ---
+// k_irfft_rows<10, 1, true, true> (periodic 4096-wide rows, two rows per tile,
+// TMA-landed [kx][2 rows] blocks) as one persistent 512-thread CTA per SM made
+// of two 256-thread groups.  Each group has its own work area (E / O spectra
+// and FFT exchange) and its own named barrier; the landing buffer is shared:
+// the moment a group has its block in registers it requests the next tile's
+// block -- the other group's -- so a landing is always in flight behind the
+// two groups' transforms, where the one-tile CTA waits for its block with
+// nothing to do (20 % of its stall samples).  Same arithmetic and thread map
+// per tile as the one-tile kernel.
+struct GroupBar {
+    int id;
+    __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
+};
+
+template <int LOGQ>
+__global__ void __launch_bounds__(512, 1) k_irfft_rows_p2(double* __restrict__ f, int Nx, int Nrow, int Nz, int dim,
+                                                         int Hx, const double2* __restrict__ tw, int logTWN,
+                                                         double scale, const uint8_t* __restrict__ cmask,
+                                                         const double* __restrict__ body, int64_t nodes,
+                                                         const __grid_constant__ CUtensorMap tm, int pf, int blk,
+                                                         int64_t ntiles) {
+    using Sh = FftShape<LOGQ, 4>;
+    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R;
+    constexpr int XB = xbuf_stride_rows(Sh::XBUF);
+    constexpr int TR = 2, LOGTR = 1;
+    static_assert(2 * TR * T == 256, "a 256-thread group per two-row tile");
+    constexpr int halfP = 2 * Q;
+    extern __shared__ double2 smraw[];
+    __shared__ __align__(8) uint64_t full[2];
+    const int g = threadIdx.x >> 8;
+    const int tid = threadIdx.x & 255;
+    const GroupBar gbar{1 + g};
+    const int nbox = (Hx + 255) / 256;
+    double2* land = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+    double2* sm = land + (size_t)nbox * 256 * TR + (size_t)g * 2 * TR * XB;  // this group's work area
+    const int gi = tid >> Sh::LOGT;
+    const int t = tid & (T - 1);
+    const int eo = gi & 1;
+    const int shX = logTWN - (LOGQ + 2);
+    const int shE = logTWN - (LOGQ + 1);
+    const int groups = Nrow / TR;
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+    }
+    __syncthreads();
+    // tile i of this CTA: blockIdx.x + i * gridDim.x; group g takes i = g, g + 2, ...
+    auto request = [&](int64_t tile, int gdst) {
+        const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
+        const int cx0 = blk ? 2 * (row0 & 7) : 2 * row0;
+        const int cz0 = blk ? slab * (Nrow >> 3) + (row0 >> 3) : slab;
+        mbar_expect_tx(&full[gdst], (unsigned)(nbox * 256 * TR * 16));
+        for (int bx = 0; bx < nbox; ++bx) tma_load_3d(&tm, land + bx * 256 * TR, &full[gdst], cx0, bx * 256, cz0);
+    };
+    auto prefetch = [&](int64_t tile) {
+        const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
+        const int cx0 = blk ? 2 * (row0 & 7) : 2 * row0;
+        const int cz0 = blk ? slab * (Nrow >> 3) + (row0 >> 3) : slab;
+        for (int bx = 0; bx < nbox; ++bx) tma_prefetch_3d(&tm, cx0, bx * 256, cz0);
+    };
+    if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntiles) request(blockIdx.x, 0);
+    constexpr int LA = 2;
+    constexpr int U = R / 2;
+    const int rr = (tid >> LA) & (TR - 1);
+    const int j0 = ((tid >> (LA + LOGTR)) << LA) + (tid & ((1 << LA) - 1));
+    const double2 W0 = twiddle<1>(tw, (2 * j0) << shX);
+    const double2 W1 = cmul(W0, twiddle<1>(tw, 1 << shX));
+    const double2 wbase = twiddle<1>(tw, t << shE);  // e^{+2 pi i t/(2Qx)}
+    unsigned ph = 0;
+    for (int64_t tile = (int64_t)blockIdx.x + (int64_t)g * gridDim.x; tile < ntiles; tile += 2 * (int64_t)gridDim.x) {
+        const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
+        {
+            double2 Xa[U], Xb[U];
+            double2 xq = make_double2(0.0, 0.0);
+            mbar_wait(&full[g], ph);
+            ph ^= 1;
+#pragma unroll
+            for (int u = 0; u < U / 2; ++u) {
+                const int j = j0 + 2 * T * u;
+                const int ke = 2 * j, ko = 2 * j + 1;
+                const bool sw = (j >> 1) & 1;
+                const double2 a1 = land[(sw ? ko : ke) * TR + rr], a2 = land[(sw ? ke : ko) * TR + rr];
+                const double2 b1 = land[(halfP - (sw ? ko : ke)) * TR + rr], b2 = land[(halfP - (sw ? ke : ko)) * TR + rr];
+                Xa[u] = sw ? a2 : a1;
+                Xa[u + U / 2] = sw ? a1 : a2;
+                Xb[u] = sw ? b2 : b1;
+                Xb[u + U / 2] = sw ? b1 : b2;
+            }
+            if (tid < TR) xq = land[Q * TR + tid];
+            gbar();  // the block is in this group's registers: the buffer takes the other group's tile
+            if (tid == 0) {
+                const int64_t nxt = tile + gridDim.x;
+                if (nxt < ntiles) request(nxt, 1 - g);
+                if (pf && nxt + (int64_t)pf * gridDim.x < ntiles) prefetch(nxt + (int64_t)pf * gridDim.x);
+            }
+            double2* E = sm + 2 * rr * XB;
+            double2* O = E + XB;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + 2 * T * u;
+                const bool even = j < Q / 2;
+                const double2 W = 2 * T * u < Q / 2 ? tw32r<1>(u * (32 / R), W0) : tw32r<1>(u * (32 / R) - 8, W1);
+                const double2 a = Xa[u], bb = Xb[u];
+                const double2 s1 = cadd(a, cconj(bb));
+                const double2 t1 = cmul(W, csub(a, cconj(bb)));
+                const double2 W2 = make_double2(-W.x, W.y);  // e^{+2 pi i (halfP-k)/Px}
+                const double2 s2 = cadd(bb, cconj(a));
+                const double2 t2 = cmul(W2, csub(bb, cconj(a)));
+                const double2 Zk = make_double2(s1.x - t1.y, s1.y + t1.x);
+                const double2 Zm = make_double2(s2.x - t2.y, s2.y + t2.x);
+                if (even) {
+                    E[spad(j)] = Zk;
+                    if (j != 0) E[spad(Q - j)] = Zm;
+                } else {
+                    const int jo = j - Q / 2;
+                    O[spad(jo)] = Zk;
+                    O[spad(Q - 1 - jo)] = Zm;
+                }
+            }
+            if (tid < TR) {  // Nyquist k = Q (self-paired, W = i) -> E[Q/2]
+                const double2 s1 = cadd(xq, cconj(xq));
+                const double2 t1 = cmul(make_double2(0.0, 1.0), csub(xq, cconj(xq)));
+                sm[2 * tid * XB + (Q & 1) * XB + spad(Q >> 1)] = make_double2(s1.x - t1.y, s1.y + t1.x);
+            }
+        }
+        gbar();
+        double2* xb = sm + gi * XB;
+        double2 v[R];
+#pragma unroll
+        for (int j = 0; j < R; ++j) v[j] = xb[spad(t + j * T)];
+        gbar();
+        reg_fft<LOGQ, 4, 1>(v, t, xb, make_fft_tw<LOGQ, 4>(t, tw, logTWN), gbar);
+#pragma unroll
+        for (int j = 0; j < R; ++j) {
+            const int n = t + j * T;
+            xb[spad(n)] = eo ? cmul(tw32r<1>(j * (16 / R), wbase), v[j]) : v[j];
+        }
+        gbar();
+        const int a = (slab / Nz) % dim;
+        const int z = slab % Nz;
+        double* dst = f + ((int64_t)slab * Nrow + row0) * Nx;
+        auto emit = [&](int r2, int n, double2 zz) {
+            const int i0 = 2 * n;
+            double v0 = zz.x * scale, v1 = zz.y * scale;
+            const int64_t node = ((int64_t)z * Nrow + row0 + r2) * Nx + i0;
+            if (body) {
+                v0 += body[(int64_t)a * nodes + node];
+                v1 += body[(int64_t)a * nodes + node + 1];
+            }
+            if (cmask) {
+                if ((cmask[node] >> a) & 1u) v0 = 0.0;
+                if ((cmask[node + 1] >> a) & 1u) v1 = 0.0;
+            }
+            *reinterpret_cast<double2*>(dst + (int64_t)r2 * Nx + i0) = make_double2(v0, v1);
+        };
+#pragma unroll 4
+        for (int u = 0; u < R / 2; ++u) {
+            const int idx = tid + u * 2 * TR * T;
+            const int r2 = idx >> LOGQ, m = idx & (Q - 1);
+            const double2 ze = sm[2 * r2 * XB + spad(m)];
+            const double2 zo = sm[(2 * r2 + 1) * XB + spad(m)];
+            emit(r2, m, cadd(ze, zo));
+            emit(r2, m + Q, csub(ze, zo));
+        }
+        gbar();  // the work area is read: the next tile's spectra may overwrite it
     }
 }
 
@@ -1702,7 +1887,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_tx(const double2
                                                                  const void* __restrict__ sym, int ncols, int NC,
                                                                  int batch, const double2* __restrict__ tw,
                                                                  int logTWN, const double* __restrict__ symh,
-                                                                 int HP) {
+                                                                 int HP, int blk) {
     using Sh = FftShape<LOGQ, kPipeLogR>;
     constexpr int Q = Sh::Q, T = Sh::T, XB = Sh::XBUF, RR = Sh::R;
     static_assert(RR == 16 && T % 128 == 0, "16 points per thread, whole TMEM lane quadrants per column");
@@ -1846,10 +2031,15 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_tx(const double2
                                                          BlockBar{}, [&]() {
                                                              if (ai == 1 && nvalid) land(x0_of(b2, col2), xbytes);
                                                          });
-            double2* dst = z0 + a * cstride;
+            // blk: the row-blocked layout [slab][n / 8][col][n % 8] -- eight
+            // consecutive threads fill one 128-byte line, and K5's two-row gather
+            // then reads 32-byte pieces 128 bytes apart instead of a column apart
+            double2* dst = blk ? out + (int64_t)(b * 2 + a) * cstride + ((int64_t)(t >> 3) * ncols + cc) * 8 + (t & 7)
+                               : z0 + a * cstride + t;
+            const int64_t dj = blk ? (int64_t)T * ncols : T;
             if (valid) {
 #pragma unroll
-                for (int j = 0; j < RR; ++j) st_hint(dst + t + j * T, v[j], pol);
+                for (int j = 0; j < RR; ++j) st_hint(dst + j * dj, v[j], pol);
             }
         }
     }
@@ -2073,7 +2263,7 @@ void set_attrs_3d();
 void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s);
 void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t s, double scale,
                const uint8_t* cmask, const double* body);
-void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s);
+void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s, bool blocked_ok = false);
 void launch_k2_3d(Engine& e, int batch, cudaStream_t s);
 void launch_k3_3d(Engine& e, double2* spec, int batch, cudaStream_t s);
 void launch_k4_3d(Engine& e, int batch, cudaStream_t s);
@@ -2233,7 +2423,10 @@ static void set_attrs_k5_all(std::integer_sequence<int, Ls...>) {
     (set_attrs_k5_l<Ls + 1, false>(), ...);
     (set_attrs_k5_l<Ls + 1, true>(), ...);
 }
-void set_attrs_k5() { set_attrs_k5_all(std::make_integer_sequence<int, 12>{}); }
+void set_attrs_k5() {
+    set_attrs_k5_all(std::make_integer_sequence<int, 12>{});
+    smem_attr((const void*)k_irfft_rows_p2<10>);
+}
 
 void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t s, double scale,
                const uint8_t* cmask, const double* body) {
@@ -2276,30 +2469,48 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
     const char* pfenv = getenv("PDGPU_K5_PF");
     const int k5pf = pfenv ? atoi(pfenv) : (lqx >= 9 ? e.num_sms : 0);
     // TMA-landed gathers (periodic rows, two per CTA; PDGPU_K5_TMA=0 disables)
-    if (cx && TR == 2 && lqx >= 8 && use_tma && encode_box_map(tm, xin, Ny, pl.Hx, nslab, TR)) {
+    const bool blk = e.s2_blocked;  // set by launch_k3_2d for the spectrum it just wrote
+    e.s2_blocked = false;
+    if (blk && !(cx && TR == 2 && lqx >= 8 && use_tma && d == 2))
+        throw std::runtime_error("K5: row-blocked spectrum without the TMA row gather");
+    if (cx && TR == 2 && lqx >= 8 && use_tma && encode_box_map(tm, xin, Ny, pl.Hx, nslab, TR, blk)) {
         const int nbox = (pl.Hx + 255) / 256;
         const size_t tsm = std::max(sizeof(double2) * (size_t)2 * TR * xbuf_stride_rows_h(lqx),
                                     sizeof(double2) * (size_t)nbox * 256 * TR) + 128;
+        // 4096-wide rows of a 2D lattice: the persistent two-group kernel
+        // (PDGPU_K5_P2=0 keeps the one-tile CTAs; PDGPU_K5_P2PF = L2 prefetch distance in tiles)
+        const char* p2env = getenv("PDGPU_K5_P2");
+        if (lqx == 10 && d == 2 && Nz == 1 && !fxs && (Nx & 1) == 0 && Ny % TR == 0 && !(p2env && p2env[0] == '0')) {
+            const size_t psm = sizeof(double2) * ((size_t)nbox * 256 * TR + (size_t)2 * 2 * TR * xbuf_stride_rows_h(lqx)) + 128;
+            const int64_t ntiles = (int64_t)(Ny / TR) * nslab;
+            const char* ppf = getenv("PDGPU_K5_P2PF");
+            const int p2pf = ppf ? atoi(ppf) : 0;
+            const unsigned pgrid = (unsigned)std::min<int64_t>((ntiles + 1) / 2, (int64_t)e.num_sms);
+            k_irfft_rows_p2<10><<<pgrid, 512, psm, s>>>(f, Nx, Ny, Nz, d, pl.Hx, e.d_tw, pl.logTWN, scale, cmask, body,
+                                                       pl.nodes, tm, p2pf, blk ? 1 : 0, ntiles);
+            return;
+        }
         switch (lqx) {
             PDGPU_CASE(8, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M, blk ? 1 : 0)))
             PDGPU_CASE(9, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M, blk ? 1 : 0)))
             PDGPU_CASE(10, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M, blk ? 1 : 0)))
             PDGPU_CASE(11, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M, blk ? 1 : 0)))
             PDGPU_CASE(12, (k_irfft_rows<LQ, 1, true, true><<<grid, 2 * TR * T, tsm, s>>>(xin, f, Nx, Ny, Nz, d, pl.Hx,
-                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M)))
+                                                      e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, k5pf, fxs, e.M, blk ? 1 : 0)))
             default: break;
         }
         return;
     }
+    if (blk) throw std::runtime_error("K5: row-blocked spectrum but no tensor map");
     // gathers (short rows, 3D): prefetch distance PDGPU_K5_GPF (CTAs)
     const char* gpfenv = getenv("PDGPU_K5_GPF");
     const int gpf = gpfenv ? atoi(gpfenv) : 0;
 #define PDGPU_K5(LT, C) launch_maybe_pdl(e.pdl, k_irfft_rows<LQ, LT, C>, grid, dim3(2 * TR * T), smem, s, xin, f, Nx, Ny, \
-                                         Nz, d, pl.Hx, e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, gpf, fxs, e.M)
+                                         Nz, d, pl.Hx, e.d_tw, pl.logTWN, scale, cmask, body, pl.nodes, tm, gpf, fxs, e.M, 0)
 #define PDGPU_K5C(C) (ltr == 3 ? PDGPU_K5(3, C) : ltr == 2 ? PDGPU_K5(2, C) : ltr == 1 ? PDGPU_K5(1, C) : PDGPU_K5(0, C))
     if (cx) PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(true))
     else PDGPU_DISPATCH_LOGQ(lqx, PDGPU_K5C(false))
@@ -2348,8 +2559,11 @@ void set_attrs_k3_2d() { set_attrs_k3_all(std::make_integer_sequence<int, 12>{})
     }
 
 // 2D K3: out of place S1 -> S2 (padded: z^0 parked in S2)
-void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s) {
+// blocked_ok: the caller hands e.d_S2 straight to launch_k5, so the spectrum
+// may be written row-blocked (e.s2_blocked tells K5)
+void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s, bool blocked_ok) {
     const Plan& pl = e.plan;
+    e.s2_blocked = false;
     const int nh = pl.nh;
     const int lq = pl.logPl - (nh == 2 ? 1 : 0);
     // persistent, cp.async-pipelined variant: NC*(XB + 2Q) slots
@@ -2390,8 +2604,18 @@ void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s) {
         if (xl == 3 && !symh_ok) xl = 1;
         if (xl == 2 && mode != 1) xl = 1;
         const char* t3 = getenv("PDGPU_K3_TM3");  // three CTAs per SM (80 registers, spills)
+        // row-blocked S2 (landed-operand kernel only; opt-in, PDGPU_S2_BLOCKED=1):
+        // K5's TMA row gather must be the one that reads it (same conditions as
+        // launch_k5).  Measured neutral to slightly slower at 4096^2 x 16 (K3 2.39
+        // -> 2.42 ms, K5 2.13 -> 2.14 ms): K5 is not bound by its gather pattern.
+        const char* k5t = getenv("PDGPU_K5_TMA");
+        const char* sbe = getenv("PDGPU_S2_BLOCKED");
+        const bool blk = blocked_ok && xl && lq == 12 && pl.dim == 2 && pl.circ[0] && pl.logQx >= 8 && pl.k1_rows >= 2 &&
+                         !(k5t && k5t[0] == '0') && !getenv("PDGPU_K5_ROWS") && pl.Nl % 8 == 0 &&
+                         (sbe && sbe[0] == '1');
+        e.s2_blocked = blk;
         if (xl) {
-#define TX_ARGS TM_ARGS, e.d_symh, e.symh_stride
+#define TX_ARGS TM_ARGS, e.d_symh, e.symh_stride, blk ? 1 : 0
 #define TX_L(LQV)                                                                                          \
     (mode == 1 ? (xl == 3   ? k_spectral2d_tx<LQV, 1, 3><<<tgrid, kPipeThreads, tsmem, s>>>(TX_ARGS)        \
                   : xl == 2 ? k_spectral2d_tx<LQV, 1, 2><<<tgrid, kPipeThreads, tsmem, s>>>(TX_ARGS)        \
@@ -2772,7 +2996,7 @@ void launch_fast_apply(Engine& e, const double* u, double* f, int batch, cudaStr
     {
         PassTimer pt(e, kPassK3, s);
         if (d == 2) {
-            launch_k3_2d(e, spec, batch, s);
+            launch_k3_2d(e, spec, batch, s, /*blocked_ok=*/true);
             xin = e.d_S2;
         } else {
             launch_k3_3d(e, spec, batch, s);
