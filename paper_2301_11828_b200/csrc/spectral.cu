@@ -1272,6 +1272,147 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
     if (TSTORE && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ------------------------------------- K1, persistent, two row groups ---
+// k_rfft_rows_duo<10, true, true> (periodic 4096-wide rows, two rows per tile,
+// TMA-stored [kx][2 rows] blocks) as one persistent 512-thread CTA per SM made
+// of two 256-thread groups (k_irfft_rows_p2 is the inverse pass built the same
+// way).  The two rows of a tile land in a buffer the groups share; a group
+// has them in registers within a few hundred cycles and then requests the
+// other group's next tile, so a landing is always in flight behind the
+// transforms.  Each group's work area serves in turn as FFT exchange buffer,
+// natural-order spectra and the [kx][row] block the TMA store reads; the wait
+// for that store's read sits at the top of the group's next tile, behind the
+// other group's work.  Same arithmetic and thread map per tile as the duo kernel.
+// CF: the conflict-free [kx][row] block-write map of k_rfft_rows_duo<.., CFM = 1>
+template <int LOGQ, bool CF>
+__global__ void __launch_bounds__(512, 1) k_rfft_rows_p2(const double* __restrict__ u, int Nx, int Nrow, int Hx,
+                                                        const double2* __restrict__ tw, int logTWN,
+                                                        const __grid_constant__ CUtensorMap tm, int64_t ntiles) {
+    using Sh = FftShape<LOGQ, 4>;
+    constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
+    constexpr int TR = 2, LOGTR = 1;
+    static_assert(2 * TR * T == 256, "a 256-thread group per two-row tile");
+    constexpr int rowlen = 4 * Q;                       // doubles per row (= Nx)
+    constexpr int RS = k1_duo_row_stride(XB, rowlen, CF ? 1 : 0);   // doubles per row of spectra (E | O)
+    constexpr int WK = (TR * RS * 8 > 9 * 256 * TR * 16 ? TR * RS * 8 : 9 * 256 * TR * 16);  // bytes per work area
+    static_assert(2 * TR * XB * 16 <= WK, "four 16-byte-slot exchange buffers per work area");
+    extern __shared__ double2 smraw[];
+    __shared__ __align__(8) uint64_t full[2];
+    __shared__ double2 stw[FftTwTable<LOGQ, 4>::SIZE];
+    const int g = threadIdx.x >> 8;
+    const int tid = threadIdx.x & 255;
+    const GroupBar gbar{1 + g};
+    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
+    const double* land = reinterpret_cast<const double*>(base);                      // TR x rowlen doubles
+    double* wk = reinterpret_cast<double*>(base + TR * rowlen * 8 + (size_t)g * WK);   // this group's work area
+    const int gi = tid >> Sh::LOGT;
+    const int t = tid & (T - 1);
+    const int r = gi >> 1, eo = gi & 1;
+    const int shE = logTWN - (LOGQ + 1);
+    const int shX = logTWN - (LOGQ + 2);
+    const int groups = Nrow / TR;
+    fill_fft_tw_table<LOGQ, 4>(stw, tw, logTWN);
+    if (threadIdx.x == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+    }
+    __syncthreads();
+    auto request = [&](int64_t tile, int gdst) {
+        const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
+        const double* src = u + ((int64_t)slab * Nrow + row0) * Nx;
+        mbar_expect_tx(&full[gdst], (unsigned)(TR * rowlen * 8));
+        for (int rr = 0; rr < TR; ++rr)
+            bulk_load(const_cast<double*>(land) + rr * rowlen, src + (int64_t)rr * Nx, rowlen * 8, &full[gdst]);
+    };
+    if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntiles) request(blockIdx.x, 0);
+    constexpr int LA = CF ? 2 : 3;
+    const int rr = (tid >> LA) & (TR - 1);
+    const int a0 = ((tid >> (LA + LOGTR)) << LA) + (tid & ((1 << LA) - 1));
+    const double2 wbase = __ldg(tw + (opaque(t) << shE));
+    auto post = [](double2 A, double2 B, double2 W) {
+        const double2 Fe = cscale(cadd(A, B), 0.5);
+        const double2 D = csub(A, B);
+        return cadd(Fe, cmul(W, make_double2(0.5 * D.y, -0.5 * D.x)));
+    };
+    unsigned ph = 0;
+    for (int64_t tile = (int64_t)blockIdx.x + (int64_t)g * gridDim.x; tile < ntiles; tile += 2 * (int64_t)gridDim.x) {
+        const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
+        double2 v[R];
+        mbar_wait(&full[g], ph);
+        ph ^= 1;
+        {
+            const double* st = land + r * rowlen;
+#pragma unroll
+            for (int j = 0; j < R; ++j) {
+                const int n = t + j * T;
+                const double2 z = *reinterpret_cast<const double2*>(st + 2 * n);
+                const double2 z2 = *reinterpret_cast<const double2*>(st + 2 * (n + Q));
+                const double2 zz = eo ? csub(z, z2) : cadd(z, z2);
+                v[j] = eo ? cmul(zz, tw32r<-1>(j * (16 / R), wbase)) : zz;
+            }
+        }
+        // this group's previous block has been read by its TMA store: the work area is free
+        if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        gbar();  // the rows are in this group's registers: the landing buffer takes the other group's tile
+        if (tid == 0 && tile + gridDim.x < ntiles) request(tile + gridDim.x, 1 - g);
+        // 16-byte exchange slots: the work area holds all four transforms' buffers
+        // (the duo kernel needs the split 8-byte exchange to fit two CTAs per SM)
+        reg_fft<LOGQ, 4, -1, GroupBar, false>(v, t, reinterpret_cast<double2*>(wk) + gi * XB,
+                                              make_fft_tw_s<LOGQ, 4>(opaque(t), stw), gbar);
+        double2* spec = reinterpret_cast<double2*>(wk + r * RS) + eo * XB;
+#pragma unroll
+        for (int j = 0; j < R; ++j) spec[nat_slot<T>(t, j)] = v[j];
+        gbar();
+        const double2* E = reinterpret_cast<const double2*>(wk + rr * RS);
+        const double2* O = E + XB;
+        const double2 W0 = __ldg(tw + ((2 * opaque(a0)) << shX));
+        const double2 W1 = cmul(W0, __ldg(tw + (1 << shX)));
+        constexpr int NU = R / 4;
+        double2 e1[NU], e2[NU], o1[NU], o2[NU];
+#pragma unroll
+        for (int uu = 0; uu < NU; ++uu) {
+            const int a = a0 + 2 * T * uu;
+            e1[uu] = E[spad(a)];
+            e2[uu] = E[spad((Q - a) & (Q - 1))];
+            o1[uu] = O[spad(a)];
+            o2[uu] = O[spad(Q - 1 - a)];
+        }
+        const double2 Aq = E[spad(Q / 2)];
+        gbar();  // every spectrum value is in registers: the block overwrites them
+        double2* ob = reinterpret_cast<double2*>(wk);
+#pragma unroll
+        for (int uu = 0; uu < NU; ++uu) {
+            const int a = a0 + 2 * T * uu;
+            const double2 We = tw32r<-1>(uu * (32 / R), W0), Wo = tw32r<-1>(uu * (32 / R), W1);
+            const double2 Wem = make_double2(-We.x, We.y), Wom = make_double2(-Wo.x, Wo.y);
+            const double2 xe = post(e1[uu], cconj(e2[uu]), We), xem = post(e2[uu], cconj(e1[uu]), Wem);
+            const double2 xo = post(o1[uu], cconj(o2[uu]), Wo), xom = post(o2[uu], cconj(o1[uu]), Wom);
+            const bool sw = CF && ((a >> 1) & 1);  // see k_rfft_rows_duo
+            ob[(2 * a + sw) * TR + rr] = sw ? xo : xe;
+            ob[(2 * a + 1 - sw) * TR + rr] = sw ? xe : xo;
+            ob[(2 * Q - 2 * a - sw) * TR + rr] = sw ? xom : xem;
+            ob[(2 * Q - 2 * a - 1 + sw) * TR + rr] = sw ? xem : xom;
+        }
+        if (a0 == 0) ob[Q * TR + rr] = post(Aq, cconj(Aq), make_double2(0.0, -1.0));
+        fence_proxy_async();
+        gbar();
+        if (tid == 0) {
+            const int nbox = (Hx + 255) / 256;
+            for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm, ob + bx * 256 * TR, 2 * row0, bx * 256, slab);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+static int k1_p2_smem(int logq, int cfm) {
+    const int Q = 1 << logq;
+    const int XB = xbuf_slots(logq);
+    const int RS = k1_duo_row_stride(XB, 4 * Q, cfm);
+    const int wk = std::max(2 * RS * 8, 9 * 256 * 2 * 16);
+    return 2 * 4 * Q * 8 + 2 * wk + 128;
+}
+
 static int k1_duo_smem(int logq, bool circ, int cfm = 0) {
     const int Q = 1 << logq;
     const int TR = 2048 >> logq;
@@ -2301,6 +2442,10 @@ static void set_attrs_k1_l() {
     if constexpr (C && L == 10) {
         smem_attr((const void*)k_rfft_rows_duo<L, C, true, 0>);
         smem_attr((const void*)k_rfft_rows_duo<L, C, true, 1>);
+        if constexpr (L == 10 && C) {
+            smem_attr((const void*)k_rfft_rows_p2<10, false>);
+            smem_attr((const void*)k_rfft_rows_p2<10, true>);
+        }
     }
 }
 template <int... Ls>
@@ -2335,7 +2480,12 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
         const char* eenv = getenv("PDGPU_K1_EARLY");
         const int k1early = (eenv && eenv[0] == '1') ? 1 : 0;
         const char* cfenv = getenv("PDGPU_K1_CF");
-        const int cfm = (cx && lqx == 10 && cfenv && cfenv[0] == '1') ? 1 : 0;
+        // (with the persistent two-group kernel below the landing latency is off
+        // the critical path and the conflict-free map wins, 2.24 -> 2.15 ms: it is
+        // the default there, PDGPU_K1_CF=0 disables)
+        const char* p2e = getenv("PDGPU_K1_P2");
+        const bool p2on = !(p2e && p2e[0] == '0');
+        const int cfm = (cx && lqx == 10 && (cfenv ? cfenv[0] == '1' : p2on)) ? 1 : 0;
         const size_t dsm = (size_t)k1_duo_smem(lqx, cx, cfm);
         const int DTR = 2048 >> lqx;
         if (2 * (dsm + 1024) <= 228 * 1024) {
@@ -2349,6 +2499,20 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
             const char* tenv = getenv("PDGPU_K1_TMA");
             const bool tst = cx && DTR <= 2 && !(tenv && tenv[0] == '0') && encode_box_map(tm, e.d_S1, Ny, pl.Hx, nslab, DTR) &&
                              (size_t)(((pl.Hx + 255) / 256) * 256 * DTR * 16 + 128) <= dsm;
+            // 4096-wide periodic rows: the persistent two-group kernel (PDGPU_K1_P2=0:
+            // the two-CTA duo kernel)
+            const char* p2env = getenv("PDGPU_K1_P2");
+            if (tst && lqx == 10 && Nx == (4 << lqx) && Ny % 2 == 0 && pl.Hx <= 9 * 256 &&
+                !(p2env && p2env[0] == '0')) {
+                const unsigned pgrid = (unsigned)std::min<int64_t>((ntiles + 1) / 2, (int64_t)e.num_sms);
+                if (cfm)
+                    k_rfft_rows_p2<10, true><<<pgrid, 512, k1_p2_smem(10, 1), s>>>(u, Nx, Ny, pl.Hx, e.d_tw, pl.logTWN, tm,
+                                                                                 ntiles);
+                else
+                    k_rfft_rows_p2<10, false><<<pgrid, 512, k1_p2_smem(10, 0), s>>>(u, Nx, Ny, pl.Hx, e.d_tw, pl.logTWN,
+                                                                                  tm, ntiles);
+                return;
+            }
 #define PDGPU_K1T(CF) k_rfft_rows_duo<LQ, true, true, CF><<<dgrid, 256, dsm, s>>>(u, e.d_S1, Nx, Ny, nslab, pl.Hx, \
                                                                                 e.d_tw, pl.logTWN, tm, k1pf, k1early)
 #define PDGPU_K1D(C) (tst ? (cfm == 1 ? PDGPU_K1T(1) : PDGPU_K1T(0))                                     \
