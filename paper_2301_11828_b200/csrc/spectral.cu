@@ -377,7 +377,9 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
         double2 xq = make_double2(0.0, 0.0);
         if constexpr (TMAG) {
             __shared__ __align__(8) uint64_t bar;
-            double2* land = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(sm) + 127) & ~uintptr_t(127));
+            // (an element offset from sm, not a pointer rounded through an integer:
+            // the accesses stay in the shared window instead of becoming generic)
+            double2* land = sm + ((128u - (smem_u32(sm) & 127u)) & 127u) / 16u;
             const int nbox = (Hx + 255) / 256;
             if (threadIdx.x == 0) mbar_init(&bar, 1);
             __syncthreads();
@@ -566,14 +568,17 @@ __global__ void __launch_bounds__(512, 1) k_irfft_rows_p2(double* __restrict__ f
     constexpr int TR = 2, LOGTR = 1;
     static_assert(2 * TR * T == 256, "a 256-thread group per two-row tile");
     constexpr int halfP = 2 * Q;
-    extern __shared__ double2 smraw[];
+    // plain offsets from the array keep the accesses in the shared window (a
+    // pointer rounded up through an integer compiles to generic loads / stores)
+    extern __shared__ __align__(128) double2 smraw[];
     __shared__ __align__(8) uint64_t full[2];
     const int g = threadIdx.x >> 8;
     const int tid = threadIdx.x & 255;
     const GroupBar gbar{1 + g};
     const int nbox = (Hx + 255) / 256;
-    double2* land = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
-    double2* sm = land + (size_t)nbox * 256 * TR + (size_t)g * 2 * TR * XB;  // this group's work area
+    if (smem_u32(smraw) & 127u) __trap();  // TMA tensor boxes land on 128-byte boundaries
+    double2* land = smraw;
+    double2* sm = smraw + nbox * 256 * TR + g * 2 * TR * XB;  // this group's work area
     const int gi = tid >> Sh::LOGT;
     const int t = tid & (T - 1);
     const int eo = gi & 1;
@@ -1212,7 +1217,7 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
             }
             const double2 Aq = E[spad(Q / 2)];
             __syncthreads();  // every spectrum value is in registers: the block overwrites them
-            double2* ob = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(sm) + 127) & ~uintptr_t(127));
+            double2* ob = sm + ((128u - (smem_u32(sm) & 127u)) & 127u) / 16u;  // shared-window offset, 128-byte aligned
 #pragma unroll
             for (int uu = 0; uu < NU; ++uu) {
                 const int a = a0 + 2 * T * uu;
@@ -1296,15 +1301,17 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_p2(const double* __restric
     constexpr int RS = k1_duo_row_stride(XB, rowlen, CF ? 1 : 0);   // doubles per row of spectra (E | O)
     constexpr int WK = (TR * RS * 8 > 9 * 256 * TR * 16 ? TR * RS * 8 : 9 * 256 * TR * 16);  // bytes per work area
     static_assert(2 * TR * XB * 16 <= WK, "four 16-byte-slot exchange buffers per work area");
-    extern __shared__ double2 smraw[];
+    // plain offsets from the array keep the accesses in the shared window (a
+    // pointer rounded up through an integer compiles to generic loads / stores)
+    extern __shared__ __align__(128) double2 smraw[];
     __shared__ __align__(8) uint64_t full[2];
     __shared__ double2 stw[FftTwTable<LOGQ, 4>::SIZE];
     const int g = threadIdx.x >> 8;
     const int tid = threadIdx.x & 255;
     const GroupBar gbar{1 + g};
-    char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(smraw) + 127) & ~uintptr_t(127));
-    const double* land = reinterpret_cast<const double*>(base);                      // TR x rowlen doubles
-    double* wk = reinterpret_cast<double*>(base + TR * rowlen * 8 + (size_t)g * WK);   // this group's work area
+    if (smem_u32(smraw) & 127u) __trap();  // the TMA store reads its boxes from 128-byte boundaries
+    const double* land = reinterpret_cast<const double*>(smraw);                   // TR x rowlen doubles
+    double* wk = reinterpret_cast<double*>(smraw) + TR * rowlen + g * (WK / 8);    // this group's work area
     const int gi = tid >> Sh::LOGT;
     const int t = tid & (T - 1);
     const int r = gi >> 1, eo = gi & 1;
