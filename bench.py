@@ -762,9 +762,18 @@ def main():
     peak, peak_src = measured_peaks()
     periodic = ff.embedding() == 3
     pbytes = pass_algorithmic_bytes(N_SIDE, BATCH, periodic)
-    kernels = {"K1_rfft_x": "k_rfft_rows_pipe (K1: R2C along x, transposed store)",
-               "K3_spectral": "k_spectral2d_duo (K3: y-FFT + symbol + inverse y-FFT)",
-               "K5_irfft_x": "k_irfft_rows (K5: gather + C2R along x + epilogue)"}
+    # the symbol bytes K3 actually streams (the model's 3 doubles per frequency of
+    # the full table, or the mirror planes over ky in [0, Pl/2]: about half)
+    sym_model = 3 * ((N_SIDE // 2 + 1) if periodic else (N_SIDE + 1)) * (N_SIDE if periodic else 2 * N_SIDE) * 8
+    sym_stream = min(sym_model, ff.symbol_stream_bytes())
+    pbytes["K3_spectral"] += sym_stream - sym_model
+    p2 = periodic and N_SIDE == 4096 and not any(os.environ.get(k) for k in ("PDGPU_K1_P2", "PDGPU_K5_P2", "PDGPU_K3"))
+    kernels = {"K1_rfft_x": ("k_rfft_rows_p2 (K1: R2C along x, persistent two-group CTA, TMA-landed rows, TMA-stored "
+                             "transposed blocks)" if p2 else "k_rfft_rows_duo/pipe (K1: R2C along x, transposed store)"),
+               "K3_spectral": ("k_spectral2d_tx (K3: y-FFT + symbol + inverse y-FFT, TMEM park, TMA-landed operands "
+                               "and symbol planes)" if p2 else "k_spectral2d_tm/duo (K3: y-FFT + symbol + inverse y-FFT)"),
+               "K5_irfft_x": ("k_irfft_rows_p2 (K5: TMA gather + C2R along x + epilogue, persistent two-group CTA)"
+                              if p2 else "k_irfft_rows (K5: gather + C2R along x + epilogue)")}
     per_pass = {}
     for k in kernels:
         ms_k, n_k = passes.get(k, (0.0, 0))
@@ -794,7 +803,9 @@ def main():
                 "embedding": "periodic (P = N + wrap correction)" if periodic else "padded (P = 2N)",
                 "per_pass": per_pass,
                 "matvec": {"algorithmic_bytes_per_step": mv_bytes, "achieved_gbs": mv_gbs, "frac": mv_gbs / peak,
-                           "model": ("48 B/DOF/vector + 12N B symbol (periodic)" if periodic
+                           "symbol_bytes_per_launch": sym_stream,
+                           "model": ("48 B/DOF/vector + the symbol K3 streams (12N B full table, 6N B mirror planes) "
+                                     "(periodic)" if periodic
                                      else "SURVEY 8(d): 80 B/DOF/vector + 48N B symbol (padded)")},
                 "passes_ms_per_step": {k: v[0] / args.steps for k, v in passes.items()},
                 "symbol_mode": ff.symbol_mode()}

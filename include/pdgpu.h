@@ -83,6 +83,10 @@ int pdgpu_symbol_is_real(pdgpu_t h);
 /* 0 complex symbol table, 1 real symbol table, 2 separable per-column
  * symbol (physical stencils of definite parity per axis). */
 int pdgpu_symbol_mode(pdgpu_t h);
+/* Bytes of symbol table the 2D spectral pass streams per launch: the full
+ * table, or -- 4096-point periodic columns of a stencil with definite parity
+ * along y -- its mirror planes over ky in [0, Pl/2] (build_symbol_half). */
+size_t pdgpu_symbol_stream_bytes(pdgpu_t h);
 /* Transform embedding per axis, bit d set = periodic (P_d = N_d, aliased
  * boundary terms removed by the wrap correction), clear = zero-padded to
  * P_d = 2 pow2ceil(N_d) like PadTransform (convolution.hpp:58-71).  Both give

@@ -34,6 +34,7 @@ SIGNATURES = {
     "pdgpu_n_nodes": (C.c_int64, [C.c_void_p]),
     "pdgpu_symbol_is_real": (C.c_int, [C.c_void_p]),
     "pdgpu_symbol_mode": (C.c_int, [C.c_void_p]),
+    "pdgpu_symbol_stream_bytes": (C.c_size_t, [C.c_void_p]),
     "pdgpu_embedding": (C.c_int, [C.c_void_p]),
     "pdgpu_set_ghosts": (C.c_int, [C.c_void_p, C.c_void_p]),
     "pdgpu_set_ghosts_strided": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64]),

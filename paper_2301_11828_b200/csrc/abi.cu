@@ -812,6 +812,14 @@ size_t pdgpu_footprint_bytes(pdgpu_t h) {
 
 int64_t pdgpu_n_nodes(pdgpu_t h) { return h ? h->plan.nodes : 0; }
 int pdgpu_symbol_is_real(pdgpu_t h) { return h && h->real_symbol ? 1 : 0; }
+size_t pdgpu_symbol_stream_bytes(pdgpu_t h) {
+    if (!h) return 0;
+    const Plan& pl = h->plan;
+    if (h->d_symh && h->symh_for == h->d_sym && !getenv("PDGPU_K3"))
+        return (size_t)pl.ncols * 3 * h->symh_stride * 8;
+    if (h->d_coltab) return (size_t)pl.ncols * h->np * (h->M + 1) * 8;
+    return (size_t)pl.ncols * pl.Pl * (h->dim == 2 && h->real_symbol ? 4 : h->np) * (h->real_symbol ? 8 : 16);
+}
 int pdgpu_symbol_mode(pdgpu_t h) { return !h ? -1 : (h->d_coltab ? 2 : (h->real_symbol ? 1 : 0)); }
 int pdgpu_embedding(pdgpu_t h) { return !h ? -1 : h->plan.circ_mask; }
 

@@ -210,6 +210,11 @@ class FastForce:
         """'complex-table' | 'real-table' | 'separable' (per-column coefficients)."""
         return ("complex-table", "real-table", "separable")[self._lib.pdgpu_symbol_mode(self._h)]
 
+    def symbol_stream_bytes(self) -> int:
+        """Bytes of symbol table the 2D spectral pass reads per launch (the full
+        table, or the mirror planes over ky in [0, Pl/2])."""
+        return int(self._lib.pdgpu_symbol_stream_bytes(self._h))
+
     # --------------------------------------------------------- corrections
     def set_regions(self, near_surface=None, constraint_mask=None):
         ns = None if near_surface is None else np.ascontiguousarray(near_surface, dtype=np.uint8)

@@ -1,9 +1,9 @@
 """GPU parity against the CPU oracle at BASELINE.json's own sizes.
 
 The headline bench line runs the 4096^2 periodic instantiation of the
-spectral kernels (k_rfft_rows_duo<10>, k_spectral2d_duo<12>,
-k_irfft_rows<10>); these tests run exactly those instantiations (and the
-padded 8192-point-column ones) against oracle/oracle.c, plus configs 3, 4
+spectral kernels (k_rfft_rows_p2<10>, k_spectral2d_tx<12>,
+k_irfft_rows_p2<10>); these tests run exactly those instantiations (their
+opt-out predecessors and the padded 8192-point-column ones too) against oracle/oracle.c, plus configs 3, 4
 and 5 at the BASELINE lattice sizes:
 
   config 2   4096^2, batch 2, physical stencil: K.u rel L2 <= 1e-11
@@ -55,6 +55,48 @@ def test_config2_4096_matvec(embed, monkeypatch):
     f = ff.matvec(u)
     for b in range(2):
         assert rel(f[b], o.matvec(u[b])) <= TOL, b
+    ff.close()
+
+
+@pytest.mark.parametrize("ny,batch", [(16, 1), (64, 3), (256, 5)])
+def test_4096_wide_rows_short_lattices(ny, batch):
+    """The persistent two-group row kernels (k_rfft_rows_p2 / k_irfft_rows_p2,
+    4096-wide periodic rows) on lattices with few tiles: fewer tiles than CTAs,
+    an odd number of tiles per CTA, a group without work; constraint masks and
+    a body force in the K5 epilogue (evaluate_force, timestepping.hpp:295-310)."""
+    o, ff, h = pair((4096, ny))
+    assert ff.embedding() == 3
+    dl = 3.015 * h
+    o.add_constraint((0.0, 0.0), (dl, ny * h), 0b11, 0, 0.0)
+    ff.add_constraint((0.0, 0.0), (dl, ny * h), 0b11, 0, 0.0)
+    rng = Rng(2100 + ny)
+    u = np.stack([random_field(rng, 2, o.n) for _ in range(batch)])
+    f = ff.matvec(u)
+    for b in range(batch):
+        assert rel(f[b], o.matvec(u[b])) <= TOL, b
+    body = random_field(rng, 2, o.n)
+    o.set_body(body)
+    ff.set_body(body)
+    import torch
+    ud = torch.tensor(u[0], device="cuda")
+    fd = torch.empty_like(ud)
+    ff.evaluate_force_device(ud, fd)
+    torch.cuda.synchronize()
+    assert rel(fd.cpu().numpy(), o.evaluate_force(u[0])) <= TOL
+    ff.close()
+
+
+@pytest.mark.parametrize("env", [{"PDGPU_K1_P2": "0"}, {"PDGPU_K5_P2": "0"}, {"PDGPU_K1_CF": "0"},
+                                 {"PDGPU_K3": "tm"}, {"PDGPU_K3": "tx"}, {"PDGPU_K3": "tx2"},
+                                 {"PDGPU_S2_BLOCKED": "1"}, {"PDGPU_NO_SYMH": "1"}, {"PDGPU_K1_EARLY": "1", "PDGPU_K1_P2": "0"}])
+def test_4096_kernel_variants(env, monkeypatch):
+    """Every opt-in / opt-out variant of the 4096^2 row and column kernels (the
+    A/B knobs DESIGN.md quotes) against the oracle."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    o, ff, _ = pair((4096, 4096))
+    u = random_field(Rng(2200), 2, o.n)
+    assert rel(ff.matvec(u), o.matvec(u)) <= TOL
     ff.close()
 
 
