@@ -815,7 +815,8 @@ int pdgpu_symbol_is_real(pdgpu_t h) { return h && h->real_symbol ? 1 : 0; }
 size_t pdgpu_symbol_stream_bytes(pdgpu_t h) {
     if (!h) return 0;
     const Plan& pl = h->plan;
-    if (h->d_symh && h->symh_for == h->d_sym && !getenv("PDGPU_K3"))
+    const char* k3 = getenv("PDGPU_K3");
+    if (h->d_symh && h->symh_for == h->d_sym && (k3 ? std::string(k3) == "tx3" : true))
         return (size_t)pl.ncols * 3 * h->symh_stride * 8;
     if (h->d_coltab) return (size_t)pl.ncols * h->np * (h->M + 1) * 8;
     return (size_t)pl.ncols * pl.Pl * (h->dim == 2 && h->real_symbol ? 4 : h->np) * (h->real_symbol ? 8 : 16);

@@ -2765,14 +2765,15 @@ void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s, boo
         // the exchange buffer behind each transform's last exchange
         // (4096-point columns, measured on one B200 at 4096^2 x 16: 2.68 -> 2.51 ms;
         // tx2 2.55 ms -- the 32-byte symbol rows read at a two-way bank conflict;
-        // 2048-point columns 0.636 -> 0.646 ms, so those keep the register loads).
+        // tx3 2.39 ms; 2048-point columns: tm 0.640, tx 0.636, tx3 0.607 ms).
         // PDGPU_K3=tm: the register-load kernel at every length.
         const std::string k3s = k3env ? k3env : "";
         // tx3: the symbol from the column's mirror planes, landed the same way
         // (no symbol load left in the product; needs build_symbol_half's table)
-        const bool symh_ok = e.d_symh && e.symh_for == e.d_sym && lq == 12 && mode == 1;
-        int xl = k3s == "tx2" ? 2 : k3s == "tx" ? 1 : ((k3s == "tx3" || k3s.empty()) && lq == 12) ? 3 : 0;
-        if (xl == 3 && !symh_ok) xl = 1;
+        const bool symh_ok = e.d_symh && e.symh_for == e.d_sym && mode == 1;
+        int xl = k3s == "tx2" ? 2 : k3s == "tx" ? 1 : (k3s == "tx3" || k3s.empty()) ? 3 : 0;
+        // without the planes: landed operands at 4096 points, register loads at 2048
+        if (xl == 3 && !symh_ok) xl = (lq == 12 || k3s == "tx3") ? 1 : 0;
         if (xl == 2 && mode != 1) xl = 1;
         const char* t3 = getenv("PDGPU_K3_TM3");  // three CTAs per SM (80 registers, spills)
         // row-blocked S2 (landed-operand kernel only; opt-in, PDGPU_S2_BLOCKED=1):
@@ -3032,7 +3033,7 @@ void build_symbol_half(Engine& e) {
     if (e.d_symh) cudaFree(e.d_symh);
     e.d_symh = nullptr;
     e.symh_for = nullptr;
-    if (e.dim != 2 || !e.real_symbol || pl.nh != 1 || pl.logPl != 12 || getenv("PDGPU_NO_SYMH")) return;
+    if (e.dim != 2 || !e.real_symbol || pl.nh != 1 || (pl.logPl != 12 && pl.logPl != 11) || getenv("PDGPU_NO_SYMH")) return;
     const int Q = pl.Pl, HP = Q / 2 + 8;
     unsigned long long* d_stat = nullptr;
     check(cudaMalloc(&e.d_symh, sizeof(double) * (size_t)pl.ncols * 3 * HP), "alloc symbol planes");
