@@ -137,7 +137,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 // blocked: the row-blocked spectrum [slab][row / 8][kx][row % 8] (2D S2 between
 // K3 and K5, launch_k3_2d) -- x = 2 * (row % 8), z = slab * (Nrow / 8) + row / 8
 static bool encode_box_map(CUtensorMap& m, const double2* S, int Nrow, int Hx, int nslab, int TR,
-                           bool blocked = false) {
+                           bool blocked = false, int boxk = 256) {
     static EncodeTiledFn enc = nullptr;
     if (!enc) {
         cudaDriverEntryPointQueryResult q;
@@ -155,7 +155,7 @@ static bool encode_box_map(CUtensorMap& m, const double2* S, int Nrow, int Hx, i
         strides[0] = 128;
         strides[1] = (cuuint64_t)Hx * 128;
     }
-    cuuint32_t box[3] = {(cuuint32_t)(2 * TR), 256, 1};
+    cuuint32_t box[3] = {(cuuint32_t)(2 * TR), (cuuint32_t)boxk, 1};
     cuuint32_t es[3] = {1, 1, 1};
     return enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)S, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -551,11 +551,17 @@ __global__ void __launch_bounds__(512) k_irfft_rows(const double2* __restrict__ 
 // nothing to do (20 % of its stall samples).  Same arithmetic and thread map
 // per tile as the one-tile kernel.
 struct GroupBar {
-    int id;
-    __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, 256;" ::"r"(id) : "memory"); }
+    int id, n;
+    __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 };
 
-template <int LOGQ>
+// NG groups of 4T threads (512 threads in all) and NL landing buffers, NG % NL
+// == 0: tile i of the CTA belongs to group i % NG and lands in buffer i % NL;
+// the group that has just read buffer i % NL requests tile i + NL into it (for
+// group (i + NL) % NG), so NL landings are in flight.  4096-wide rows: two
+// 256-thread groups and one buffer; 2048-wide rows: four 128-thread groups and
+// two buffers.
+template <int LOGQ, int NG, int NL>
 __global__ void __launch_bounds__(512, 1) k_irfft_rows_p2(double* __restrict__ f, int Nx, int Nrow, int Nz, int dim,
                                                          int Hx, const double2* __restrict__ tw, int logTWN,
                                                          double scale, const uint8_t* __restrict__ cmask,
@@ -566,32 +572,31 @@ __global__ void __launch_bounds__(512, 1) k_irfft_rows_p2(double* __restrict__ f
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R;
     constexpr int XB = xbuf_stride_rows(Sh::XBUF);
     constexpr int TR = 2, LOGTR = 1;
-    static_assert(2 * TR * T == 256, "a 256-thread group per two-row tile");
+    constexpr int GS = 2 * TR * T, LOGGS = Sh::LOGT + 2;  // threads per group (one two-row tile)
+    static_assert(GS * NG == 512 && NG % NL == 0, "512 threads in NG groups, NL | NG landing buffers");
     constexpr int halfP = 2 * Q;
     // plain offsets from the array keep the accesses in the shared window (a
     // pointer rounded up through an integer compiles to generic loads / stores)
     extern __shared__ __align__(128) double2 smraw[];
-    __shared__ __align__(8) uint64_t full[2];
-    const int g = threadIdx.x >> 8;
-    const int tid = threadIdx.x & 255;
-    const GroupBar gbar{1 + g};
+    __shared__ __align__(8) uint64_t full[NG];
+    const int g = threadIdx.x >> LOGGS;
+    const int tid = threadIdx.x & (GS - 1);
+    const GroupBar gbar{1 + g, GS};
     const int nbox = (Hx + 255) / 256;
     if (smem_u32(smraw) & 127u) __trap();  // TMA tensor boxes land on 128-byte boundaries
-    double2* land = smraw;
-    double2* sm = smraw + nbox * 256 * TR + g * 2 * TR * XB;  // this group's work area
+    const int lsz = nbox * 256 * TR;                          // double2 per landing buffer
+    double2* sm = smraw + NL * lsz + g * 2 * TR * XB;         // this group's work area
     const int gi = tid >> Sh::LOGT;
     const int t = tid & (T - 1);
     const int eo = gi & 1;
     const int shX = logTWN - (LOGQ + 2);
     const int shE = logTWN - (LOGQ + 1);
     const int groups = Nrow / TR;
-    if (threadIdx.x == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-    }
+    if (threadIdx.x == 0)
+        for (int i = 0; i < NG; ++i) mbar_init(&full[i], 1);
     __syncthreads();
-    // tile i of this CTA: blockIdx.x + i * gridDim.x; group g takes i = g, g + 2, ...
-    auto request = [&](int64_t tile, int gdst) {
+    // tile i of this CTA: blockIdx.x + i * gridDim.x; group g takes i = g, g + NG, ...
+    auto request = [&](int64_t tile, int gdst, double2* land) {
         const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
         const int cx0 = blk ? 2 * (row0 & 7) : 2 * row0;
         const int cz0 = blk ? slab * (Nrow >> 3) + (row0 >> 3) : slab;
@@ -604,7 +609,10 @@ __global__ void __launch_bounds__(512, 1) k_irfft_rows_p2(double* __restrict__ f
         const int cz0 = blk ? slab * (Nrow >> 3) + (row0 >> 3) : slab;
         for (int bx = 0; bx < nbox; ++bx) tma_prefetch_3d(&tm, cx0, bx * 256, cz0);
     };
-    if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntiles) request(blockIdx.x, 0);
+    if (threadIdx.x == 0)
+        for (int i = 0; i < NL; ++i)
+            if ((int64_t)blockIdx.x + (int64_t)i * gridDim.x < ntiles)
+                request((int64_t)blockIdx.x + (int64_t)i * gridDim.x, i % NG, smraw + i * lsz);
     constexpr int LA = 2;
     constexpr int U = R / 2;
     const int rr = (tid >> LA) & (TR - 1);
@@ -613,9 +621,11 @@ __global__ void __launch_bounds__(512, 1) k_irfft_rows_p2(double* __restrict__ f
     const double2 W1 = cmul(W0, twiddle<1>(tw, 1 << shX));
     const double2 wbase = twiddle<1>(tw, t << shE);  // e^{+2 pi i t/(2Qx)}
     unsigned ph = 0;
-    for (int64_t tile = (int64_t)blockIdx.x + (int64_t)g * gridDim.x; tile < ntiles; tile += 2 * (int64_t)gridDim.x) {
+    const int li = g % NL;  // this group's landing buffer: (g + k * NG) % NL
+    for (int64_t tile = (int64_t)blockIdx.x + (int64_t)g * gridDim.x; tile < ntiles; tile += NG * (int64_t)gridDim.x) {
         const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
         {
+            double2* land = smraw + li * lsz;
             double2 Xa[U], Xb[U];
             double2 xq = make_double2(0.0, 0.0);
             mbar_wait(&full[g], ph);
@@ -633,10 +643,10 @@ __global__ void __launch_bounds__(512, 1) k_irfft_rows_p2(double* __restrict__ f
                 Xb[u + U / 2] = sw ? b1 : b2;
             }
             if (tid < TR) xq = land[Q * TR + tid];
-            gbar();  // the block is in this group's registers: the buffer takes the other group's tile
+            gbar();  // the block is in this group's registers: the buffer takes the tile NL further on
             if (tid == 0) {
-                const int64_t nxt = tile + gridDim.x;
-                if (nxt < ntiles) request(nxt, 1 - g);
+                const int64_t nxt = tile + NL * (int64_t)gridDim.x;
+                if (nxt < ntiles) request(nxt, (g + NL) % NG, land);
                 if (pf && nxt + (int64_t)pf * gridDim.x < ntiles) prefetch(nxt + (int64_t)pf * gridDim.x);
             }
             double2* E = sm + 2 * rr * XB;
@@ -1288,30 +1298,38 @@ __global__ void __launch_bounds__(256, 2) k_rfft_rows_duo(const double* __restri
 // natural-order spectra and the [kx][row] block the TMA store reads; the wait
 // for that store's read sits at the top of the group's next tile, behind the
 // other group's work.  Same arithmetic and thread map per tile as the duo kernel.
-// CF: the conflict-free [kx][row] block-write map of k_rfft_rows_duo<.., CFM = 1>
-template <int LOGQ, bool CF>
-__global__ void __launch_bounds__(512, 1) k_rfft_rows_p2(const double* __restrict__ u, int Nx, int Nrow, int Hx,
+// CF: the conflict-free [kx][row] block-write map of k_rfft_rows_duo<.., CFM = 1>.
+// NG groups of 4T threads and NL landing buffers as in k_irfft_rows_p2 (4096-
+// wide rows: 2 x 256 threads, one buffer; 2048-wide: 4 x 128 threads, two
+// buffers); the block leaves in NBOX TMA boxes of BOXK kx (2049 = 9 boxes of
+// 256, the last one clipped by the tensor map; 1025 = 4 boxes of 256 and the
+// Nyquist kx by plain stores).
+template <int LOGQ, bool CF, int NG, int NL, int BOXK, int NBOX>
+__global__ void __launch_bounds__(512, 1) k_rfft_rows_p2(const double* __restrict__ u, double2* __restrict__ S, int Nx,
+                                                        int Nrow, int Hx,
                                                         const double2* __restrict__ tw, int logTWN,
                                                         const __grid_constant__ CUtensorMap tm, int64_t ntiles) {
     using Sh = FftShape<LOGQ, 4>;
     constexpr int Q = Sh::Q, T = Sh::T, R = Sh::R, XB = Sh::XBUF;
     constexpr int TR = 2, LOGTR = 1;
-    static_assert(2 * TR * T == 256, "a 256-thread group per two-row tile");
+    constexpr int GS = 2 * TR * T, LOGGS = Sh::LOGT + 2;  // threads per group (one two-row tile)
+    static_assert(GS * NG == 512 && NG % NL == 0, "512 threads in NG groups, NL | NG landing buffers");
     constexpr int rowlen = 4 * Q;                       // doubles per row (= Nx)
     constexpr int RS = k1_duo_row_stride(XB, rowlen, CF ? 1 : 0);   // doubles per row of spectra (E | O)
-    constexpr int WK = (TR * RS * 8 > 9 * 256 * TR * 16 ? TR * RS * 8 : 9 * 256 * TR * 16);  // bytes per work area
+    constexpr int WK = ((TR * RS * 8 > NBOX * BOXK * TR * 16 ? TR * RS * 8 : NBOX * BOXK * TR * 16) + 127) / 128 * 128;
     static_assert(2 * TR * XB * 16 <= WK, "four 16-byte-slot exchange buffers per work area");
+    static_assert((TR * rowlen * 8) % 128 == 0, "landing buffers keep the work areas 128-byte aligned");
     // plain offsets from the array keep the accesses in the shared window (a
     // pointer rounded up through an integer compiles to generic loads / stores)
     extern __shared__ __align__(128) double2 smraw[];
-    __shared__ __align__(8) uint64_t full[2];
+    __shared__ __align__(8) uint64_t full[NG];
     __shared__ double2 stw[FftTwTable<LOGQ, 4>::SIZE];
-    const int g = threadIdx.x >> 8;
-    const int tid = threadIdx.x & 255;
-    const GroupBar gbar{1 + g};
+    const int g = threadIdx.x >> LOGGS;
+    const int tid = threadIdx.x & (GS - 1);
+    const GroupBar gbar{1 + g, GS};
     if (smem_u32(smraw) & 127u) __trap();  // the TMA store reads its boxes from 128-byte boundaries
-    const double* land = reinterpret_cast<const double*>(smraw);                   // TR x rowlen doubles
-    double* wk = reinterpret_cast<double*>(smraw) + TR * rowlen + g * (WK / 8);    // this group's work area
+    double* lands = reinterpret_cast<double*>(smraw);                                   // NL x TR x rowlen doubles
+    double* wk = reinterpret_cast<double*>(smraw) + NL * TR * rowlen + g * (WK / 8);    // this group's work area
     const int gi = tid >> Sh::LOGT;
     const int t = tid & (T - 1);
     const int r = gi >> 1, eo = gi & 1;
@@ -1319,19 +1337,20 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_p2(const double* __restric
     const int shX = logTWN - (LOGQ + 2);
     const int groups = Nrow / TR;
     fill_fft_tw_table<LOGQ, 4>(stw, tw, logTWN);
-    if (threadIdx.x == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
-    }
+    if (threadIdx.x == 0)
+        for (int i = 0; i < NG; ++i) mbar_init(&full[i], 1);
     __syncthreads();
-    auto request = [&](int64_t tile, int gdst) {
+    auto request = [&](int64_t tile, int gdst, double* land) {
         const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
         const double* src = u + ((int64_t)slab * Nrow + row0) * Nx;
         mbar_expect_tx(&full[gdst], (unsigned)(TR * rowlen * 8));
         for (int rr = 0; rr < TR; ++rr)
-            bulk_load(const_cast<double*>(land) + rr * rowlen, src + (int64_t)rr * Nx, rowlen * 8, &full[gdst]);
+            bulk_load(land + rr * rowlen, src + (int64_t)rr * Nx, rowlen * 8, &full[gdst]);
     };
-    if (threadIdx.x == 0 && (int64_t)blockIdx.x < ntiles) request(blockIdx.x, 0);
+    if (threadIdx.x == 0)
+        for (int i = 0; i < NL; ++i)
+            if ((int64_t)blockIdx.x + (int64_t)i * gridDim.x < ntiles)
+                request((int64_t)blockIdx.x + (int64_t)i * gridDim.x, i % NG, lands + i * TR * rowlen);
     constexpr int LA = CF ? 2 : 3;
     const int rr = (tid >> LA) & (TR - 1);
     const int a0 = ((tid >> (LA + LOGTR)) << LA) + (tid & ((1 << LA) - 1));
@@ -1342,7 +1361,8 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_p2(const double* __restric
         return cadd(Fe, cmul(W, make_double2(0.5 * D.y, -0.5 * D.x)));
     };
     unsigned ph = 0;
-    for (int64_t tile = (int64_t)blockIdx.x + (int64_t)g * gridDim.x; tile < ntiles; tile += 2 * (int64_t)gridDim.x) {
+    double* land = lands + (g % NL) * TR * rowlen;  // this group's landing buffer: (g + k * NG) % NL
+    for (int64_t tile = (int64_t)blockIdx.x + (int64_t)g * gridDim.x; tile < ntiles; tile += NG * (int64_t)gridDim.x) {
         const int slab = (int)(tile / groups), row0 = (int)(tile % groups) * TR;
         double2 v[R];
         mbar_wait(&full[g], ph);
@@ -1360,8 +1380,8 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_p2(const double* __restric
         }
         // this group's previous block has been read by its TMA store: the work area is free
         if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        gbar();  // the rows are in this group's registers: the landing buffer takes the other group's tile
-        if (tid == 0 && tile + gridDim.x < ntiles) request(tile + gridDim.x, 1 - g);
+        gbar();  // the rows are in this group's registers: the landing buffer takes the tile NL further on
+        if (tid == 0 && tile + NL * (int64_t)gridDim.x < ntiles) request(tile + NL * (int64_t)gridDim.x, (g + NL) % NG, land);
         // 16-byte exchange slots: the work area holds all four transforms' buffers
         // (the duo kernel needs the split 8-byte exchange to fit two CTAs per SM)
         reg_fft<LOGQ, 4, -1, GroupBar, false>(v, t, reinterpret_cast<double2*>(wk) + gi * XB,
@@ -1404,20 +1424,24 @@ __global__ void __launch_bounds__(512, 1) k_rfft_rows_p2(const double* __restric
         fence_proxy_async();
         gbar();
         if (tid == 0) {
-            const int nbox = (Hx + 255) / 256;
-            for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm, ob + bx * 256 * TR, 2 * row0, bx * 256, slab);
+            const int nbox = min(NBOX, (Hx + BOXK - 1) / BOXK);
+            for (int bx = 0; bx < nbox; ++bx) tma_store_3d(&tm, ob + bx * BOXK * TR, 2 * row0, bx * BOXK, slab);
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
+        // kx beyond the boxes (a box must start on a 128-byte boundary of the
+        // block, so 1025 kx leave as 4 boxes of 256 and this one)
+        for (int i = NBOX * BOXK * TR + tid; i < Hx * TR; i += GS)
+            S[((int64_t)slab * Hx + i / TR) * Nrow + row0 + (i & (TR - 1))] = ob[i];
     }
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-static int k1_p2_smem(int logq, int cfm) {
+static int k1_p2_smem(int logq, int cfm, int nl, int ng, int boxk, int nbox) {
     const int Q = 1 << logq;
     const int XB = xbuf_slots(logq);
     const int RS = k1_duo_row_stride(XB, 4 * Q, cfm);
-    const int wk = std::max(2 * RS * 8, 9 * 256 * 2 * 16);
-    return 2 * 4 * Q * 8 + 2 * wk + 128;
+    const int wk = (std::max(2 * RS * 8, nbox * boxk * 2 * 16) + 127) / 128 * 128;
+    return nl * 2 * 4 * Q * 8 + ng * wk + 128;
 }
 
 static int k1_duo_smem(int logq, bool circ, int cfm = 0) {
@@ -2450,8 +2474,10 @@ static void set_attrs_k1_l() {
         smem_attr((const void*)k_rfft_rows_duo<L, C, true, 0>);
         smem_attr((const void*)k_rfft_rows_duo<L, C, true, 1>);
         if constexpr (L == 10 && C) {
-            smem_attr((const void*)k_rfft_rows_p2<10, false>);
-            smem_attr((const void*)k_rfft_rows_p2<10, true>);
+            smem_attr((const void*)k_rfft_rows_p2<10, false, 2, 1, 256, 9>);
+            smem_attr((const void*)k_rfft_rows_p2<10, true, 2, 1, 256, 9>);
+            smem_attr((const void*)k_rfft_rows_p2<9, true, 4, 2, 256, 4>);
+            smem_attr((const void*)k_rfft_rows_p2<8, true, 8, 2, 256, 2>);
         }
     }
 }
@@ -2509,14 +2535,32 @@ void launch_k1(Engine& e, const double* u, int batch, cudaStream_t s) {
             // 4096-wide periodic rows: the persistent two-group kernel (PDGPU_K1_P2=0:
             // the two-CTA duo kernel)
             const char* p2env = getenv("PDGPU_K1_P2");
+            // 2048- / 1024-wide periodic rows: four 128-thread (eight 64-thread) groups, two
+            // landing buffers, two rows per tile stored as 4 (2) TMA boxes of 256 kx + the
+            // Nyquist kx: K1 0.626 -> 0.409 ms at 2048^2 x 16, 0.146 -> 0.137 ms at 1024^2 x 16
+            // (PDGPU_K1_P2=0 disables)
+            if (cx && (lqx == 9 || lqx == 8) && Nx == (4 << lqx) && Ny % 2 == 0 && pl.Hx == (2 << lqx) + 1 &&
+                !(p2env && p2env[0] == '0') && !(tenv && tenv[0] == '0') && encode_box_map(tm, e.d_S1, Ny, pl.Hx, nslab, 2)) {
+                const int64_t nt2 = (int64_t)(Ny / 2) * nslab;
+                const int ng = lqx == 9 ? 4 : 8;
+                const unsigned pgrid = (unsigned)std::min<int64_t>((nt2 + ng - 1) / ng, (int64_t)e.num_sms);
+                if (lqx == 9)
+                    k_rfft_rows_p2<9, true, 4, 2, 256, 4><<<pgrid, 512, k1_p2_smem(9, 1, 2, 4, 256, 4), s>>>(
+                        u, e.d_S1, Nx, Ny, pl.Hx, e.d_tw, pl.logTWN, tm, nt2);
+                else
+                    k_rfft_rows_p2<8, true, 8, 2, 256, 2><<<pgrid, 512, k1_p2_smem(8, 1, 2, 8, 256, 2), s>>>(
+                        u, e.d_S1, Nx, Ny, pl.Hx, e.d_tw, pl.logTWN, tm, nt2);
+                return;
+            }
             if (tst && lqx == 10 && Nx == (4 << lqx) && Ny % 2 == 0 && pl.Hx <= 9 * 256 &&
                 !(p2env && p2env[0] == '0')) {
                 const unsigned pgrid = (unsigned)std::min<int64_t>((ntiles + 1) / 2, (int64_t)e.num_sms);
+                const int psm = k1_p2_smem(10, cfm, 1, 2, 256, 9);
                 if (cfm)
-                    k_rfft_rows_p2<10, true><<<pgrid, 512, k1_p2_smem(10, 1), s>>>(u, Nx, Ny, pl.Hx, e.d_tw, pl.logTWN, tm,
-                                                                                 ntiles);
+                    k_rfft_rows_p2<10, true, 2, 1, 256, 9><<<pgrid, 512, psm, s>>>(u, e.d_S1, Nx, Ny, pl.Hx, e.d_tw, pl.logTWN,
+                                                                                 tm, ntiles);
                 else
-                    k_rfft_rows_p2<10, false><<<pgrid, 512, k1_p2_smem(10, 0), s>>>(u, Nx, Ny, pl.Hx, e.d_tw, pl.logTWN,
+                    k_rfft_rows_p2<10, false, 2, 1, 256, 9><<<pgrid, 512, psm, s>>>(u, e.d_S1, Nx, Ny, pl.Hx, e.d_tw, pl.logTWN,
                                                                                   tm, ntiles);
                 return;
             }
@@ -2596,7 +2640,9 @@ static void set_attrs_k5_all(std::integer_sequence<int, Ls...>) {
 }
 void set_attrs_k5() {
     set_attrs_k5_all(std::make_integer_sequence<int, 12>{});
-    smem_attr((const void*)k_irfft_rows_p2<10>);
+    smem_attr((const void*)k_irfft_rows_p2<10, 2, 1>);
+    smem_attr((const void*)k_irfft_rows_p2<9, 4, 2>);
+    smem_attr((const void*)k_irfft_rows_p2<8, 8, 2>);
 }
 
 void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t s, double scale,
@@ -2651,14 +2697,24 @@ void launch_k5(Engine& e, const double2* xin, double* f, int batch, cudaStream_t
         // 4096-wide rows of a 2D lattice: the persistent two-group kernel
         // (PDGPU_K5_P2=0 keeps the one-tile CTAs; PDGPU_K5_P2PF = L2 prefetch distance in tiles)
         const char* p2env = getenv("PDGPU_K5_P2");
-        if (lqx == 10 && d == 2 && Nz == 1 && !fxs && (Nx & 1) == 0 && Ny % TR == 0 && !(p2env && p2env[0] == '0')) {
-            const size_t psm = sizeof(double2) * ((size_t)nbox * 256 * TR + (size_t)2 * 2 * TR * xbuf_stride_rows_h(lqx)) + 128;
+        // (2048-wide rows: four 128-thread groups and two landing buffers, 0.523 -> 0.456 ms
+        // at 2048^2 x 16; 1024-wide rows: eight 64-thread groups, measured slower, 0.128 ->
+        // 0.146 ms at 1024^2 x 16, opt-in PDGPU_K5_P2=1)
+        const bool p2ok = d == 2 && Nz == 1 && !fxs && (Nx & 1) == 0 && Ny % TR == 0;
+        if (p2ok && (((lqx == 10 || lqx == 9) && !(p2env && p2env[0] == '0')) || (lqx == 8 && p2env && p2env[0] == '1'))) {
+            const int ng = lqx == 10 ? 2 : lqx == 9 ? 4 : 8, nl = lqx == 10 ? 1 : 2;
+            const size_t psm = sizeof(double2) * ((size_t)nl * nbox * 256 * TR + (size_t)ng * 2 * TR * xbuf_stride_rows_h(lqx)) + 128;
             const int64_t ntiles = (int64_t)(Ny / TR) * nslab;
             const char* ppf = getenv("PDGPU_K5_P2PF");
             const int p2pf = ppf ? atoi(ppf) : 0;
-            const unsigned pgrid = (unsigned)std::min<int64_t>((ntiles + 1) / 2, (int64_t)e.num_sms);
-            k_irfft_rows_p2<10><<<pgrid, 512, psm, s>>>(f, Nx, Ny, Nz, d, pl.Hx, e.d_tw, pl.logTWN, scale, cmask, body,
-                                                       pl.nodes, tm, p2pf, blk ? 1 : 0, ntiles);
+            const unsigned pgrid = (unsigned)std::min<int64_t>((ntiles + ng - 1) / ng, (int64_t)e.num_sms);
+#define PDGPU_K5P2(LQV, NGV, NLV)                                                                                       \
+    k_irfft_rows_p2<LQV, NGV, NLV><<<pgrid, 512, psm, s>>>(f, Nx, Ny, Nz, d, pl.Hx, e.d_tw, pl.logTWN, scale, cmask, body, \
+                                                          pl.nodes, tm, p2pf, blk ? 1 : 0, ntiles)
+            if (lqx == 10) PDGPU_K5P2(10, 2, 1);
+            else if (lqx == 9) PDGPU_K5P2(9, 4, 2);
+            else PDGPU_K5P2(8, 8, 2);
+#undef PDGPU_K5P2
             return;
         }
         switch (lqx) {

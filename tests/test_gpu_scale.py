@@ -58,13 +58,14 @@ def test_config2_4096_matvec(embed, monkeypatch):
     ff.close()
 
 
-@pytest.mark.parametrize("ny,batch", [(16, 1), (64, 3), (256, 5)])
-def test_4096_wide_rows_short_lattices(ny, batch):
-    """The persistent two-group row kernels (k_rfft_rows_p2 / k_irfft_rows_p2,
-    4096-wide periodic rows) on lattices with few tiles: fewer tiles than CTAs,
+@pytest.mark.parametrize("nx,ny,batch", [(4096, 16, 1), (4096, 64, 3), (4096, 256, 5), (2048, 16, 1), (2048, 64, 3),
+                                         (2048, 256, 5), (2048, 2048, 2), (1024, 16, 1), (1024, 64, 3), (1024, 1024, 2)])
+def test_wide_rows_short_lattices(nx, ny, batch):
+    """The persistent multi-group row kernels (k_rfft_rows_p2 / k_irfft_rows_p2,
+    4096-, 2048- and 1024-wide periodic rows) on lattices with few tiles: fewer tiles than CTAs,
     an odd number of tiles per CTA, a group without work; constraint masks and
     a body force in the K5 epilogue (evaluate_force, timestepping.hpp:295-310)."""
-    o, ff, h = pair((4096, ny))
+    o, ff, h = pair((nx, ny))
     assert ff.embedding() == 3
     dl = 3.015 * h
     o.add_constraint((0.0, 0.0), (dl, ny * h), 0b11, 0, 0.0)
