@@ -815,6 +815,8 @@ int pdgpu_symbol_is_real(pdgpu_t h) { return h && h->real_symbol ? 1 : 0; }
 size_t pdgpu_symbol_stream_bytes(pdgpu_t h) {
     if (!h) return 0;
     const Plan& pl = h->plan;
+    // (512/1024-point columns fall back to the full table on batches too small to
+    // fill the SMs, launch_k3_2d; this reports the large-batch figure)
     const char* k3 = getenv("PDGPU_K3");
     if (h->d_symh && h->symh_for == h->d_sym && (k3 ? std::string(k3) == "tx3" : true))
         return (size_t)pl.ncols * 3 * h->symh_stride * 8;

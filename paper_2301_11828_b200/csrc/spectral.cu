@@ -2062,11 +2062,11 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_tx(const double2
                                                                  int HP, int blk) {
     using Sh = FftShape<LOGQ, kPipeLogR>;
     constexpr int Q = Sh::Q, T = Sh::T, XB = Sh::XBUF, RR = Sh::R;
-    static_assert(RR == 16 && T % 128 == 0, "16 points per thread, whole TMEM lane quadrants per column");
+    static_assert(RR == 16 && T % 32 == 0, "16 points per thread, whole warps (TMEM lane quadrants) per column");
     static_assert(XL == 1 || SYM == 1, "symbol landing: real table only");
     extern __shared__ double2 sm[];
     __shared__ uint32_t tbase;
-    __shared__ __align__(8) uint64_t bars[kPipeThreads / 128];
+    __shared__ __align__(8) uint64_t bars[kPipeThreads / 32];
     __shared__ double2 stw[FftTwTable<LOGQ, kPipeLogR>::SIZE];
     const int gi = threadIdx.x >> Sh::LOGT;
     const int t = threadIdx.x & (T - 1);
@@ -2091,7 +2091,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) k_spectral2d_tx(const double2
     auto item_col = [&](int64_t item, int& b, int& col) {
         b = (int)(item % batch);
         col = (int)(item / batch) * NC + gi;
-        return col < ncols;
+        return col < ncols && gi < NC;  // NC below the CTA's column slots: small lattices, more CTAs
     };
     auto x0_of = [&](int b, int col) { return in + ((int64_t)(b * 2) * ncols + col) * Q; };
     // one column-sized block into this column's exchange buffer (one thread)
@@ -2768,6 +2768,7 @@ static void set_attrs_k3_l() {
         smem_attr((const void*)k_spectral2d_tx<L, 1, 2>);
         smem_attr((const void*)k_spectral2d_tx<L, 1, 3>);
     }
+    if constexpr (L == 9 || L == 10) smem_attr((const void*)k_spectral2d_tx<L, 1, 3>);
     smem_attr((const void*)k_spectral2d_pipe<L, 0>);
     smem_attr((const void*)k_spectral2d_pipe<L, 1>);
     smem_attr((const void*)k_spectral2d_pipe<L, 2>);
@@ -2806,6 +2807,29 @@ void launch_k3_2d(Engine& e, const double2* spec, int batch, cudaStream_t s, boo
     // register loads, 16-byte exchange (PDGPU_K3=tmland: x_0 TMA-landed with
     // the split exchange; PDGPU_K3=split: the SMEM-parked k_spectral2d_duo)
     const bool k3split = k3env && std::string(k3env) == "split";
+    // 512/1024-point periodic columns with symbol mirror planes: the landed-operand
+    // TMEM kernel with eight / four columns per CTA (K3 0.188 -> 0.156 ms at 1024^2 x 16,
+    // 0.056 -> 0.050 ms at 512^2 x 16; any other PDGPU_K3 value: k_spectral2d_duo)
+    // batches too small to cover the SMs twice with full CTAs (CG on 1024^2: 191 ->
+    // 225 ms per solve) stay on k_spectral2d_duo unless PDGPU_K3=tx3 forces it
+    const bool tx3_forced = k3env && std::string(k3env) == "tx3";
+    const bool tx3_fits = (int64_t)((pl.ncols + kPipeThreads / Tp - 1) / (kPipeThreads / Tp)) * batch >= 2 * e.num_sms;
+    if (nh == 1 && (lq == 9 || lq == 10) && mode == 1 && e.d_symh && e.symh_for == e.d_sym &&
+        (tx3_forced || (!k3env && tx3_fits))) {
+        int NCt = kPipeThreads / Tp;
+        const size_t tsmem = (size_t)NCt * sizeof(double2) * xbuf_slots(lq);
+        // forced on a small batch: fewer columns per CTA until the grid covers the SMs twice
+        while (NCt > 1 && (int64_t)((pl.ncols + NCt - 1) / NCt) * batch < 2 * e.num_sms) NCt /= 2;
+        const int64_t nitems = (int64_t)((pl.ncols + NCt - 1) / NCt) * batch;
+        const unsigned tgrid = (unsigned)std::min<int64_t>(nitems, (int64_t)e.num_sms * 2);
+        if (lq == 10)
+            k_spectral2d_tx<10, 1, 3><<<tgrid, kPipeThreads, tsmem, s>>>(spec, e.d_S2, e.d_sym, pl.ncols, NCt, batch, e.d_tw,
+                                                                        pl.logTWN, e.d_symh, e.symh_stride, 0);
+        else
+            k_spectral2d_tx<9, 1, 3><<<tgrid, kPipeThreads, tsmem, s>>>(spec, e.d_S2, e.d_sym, pl.ncols, NCt, batch, e.d_tw,
+                                                                       pl.logTWN, e.d_symh, e.symh_stride, 0);
+        return;
+    }
     if (nh == 1 && (lq == 11 || lq == 12) && mode != 2 && !k3split) {
         const bool land = k3env && std::string(k3env) == "tmland";
         const int NCt = kPipeThreads / Tp;
@@ -3089,7 +3113,7 @@ void build_symbol_half(Engine& e) {
     if (e.d_symh) cudaFree(e.d_symh);
     e.d_symh = nullptr;
     e.symh_for = nullptr;
-    if (e.dim != 2 || !e.real_symbol || pl.nh != 1 || (pl.logPl != 12 && pl.logPl != 11) || getenv("PDGPU_NO_SYMH")) return;
+    if (e.dim != 2 || !e.real_symbol || pl.nh != 1 || pl.logPl < 9 || pl.logPl > 12 || getenv("PDGPU_NO_SYMH")) return;
     const int Q = pl.Pl, HP = Q / 2 + 8;
     unsigned long long* d_stat = nullptr;
     check(cudaMalloc(&e.d_symh, sizeof(double) * (size_t)pl.ncols * 3 * HP), "alloc symbol planes");
