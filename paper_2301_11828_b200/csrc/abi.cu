@@ -861,6 +861,17 @@ int pdgpu_set_slab(pdgpu_t h, int global_rows, int row_offset) {
         std::vector<double> de;
         assembly::surface_diag(h->dim, h->plan.N, h->M, h->stencils.data(), h->h_near, rows, de, h->slab);
         upload_surface(*h, rows, de);
+        if (h->dim == 3) {
+            // the tiled wrap face passes serve a slab whose own axis is short (their z
+            // pass takes the ghost planes): rebuild the tables for the slab frame
+            touch_state(*h);
+            for (void** p : {(void**)&h->d_wrows, (void**)&h->d_wo0, (void**)&h->d_wK, (void**)&h->d_lidx, (void**)&h->d_loff,
+                             (void**)&h->d_lK, (void**)&h->d_sidx, (void**)&h->d_stab, (void**)&h->d_fidx, (void**)&h->d_ftab}) {
+                if (*p) cudaFree(*p);
+                *p = nullptr;
+            }
+            build_wrap_table(*h);
+        }
     });
 }
 

@@ -580,7 +580,9 @@ __global__ void __launch_bounds__(kFaceTB * kFaceTC) k_wrap_face(
     const double* __restrict__ u, double* __restrict__ f, const int* __restrict__ fidx,
     const int4* __restrict__ ftab, const double* __restrict__ wK, int M, int N0, int N1, int N2,
     const uint8_t* __restrict__ cmask, const uint8_t* __restrict__ smask, int64_t nodes, double scale,
-    int nrec_max, const double* __restrict__ xstrip, double* __restrict__ fx) {
+    int nrec_max, const double* __restrict__ xstrip, double* __restrict__ fx,
+    const double* __restrict__ ghost = nullptr, int64_t gs_bc = 0, int64_t gs_side = 0, int lo_int = 0,
+    int hi_int = 0) {
     constexpr int D = 3, KS = 6;
     extern __shared__ double tile[];  // [layer][comp][c'][b'] (b' fastest), then the records and their K
     const int NA = A == 0 ? N0 : (A == 1 ? N1 : N2);
@@ -643,7 +645,13 @@ __global__ void __launch_bounds__(kFaceTB * kFaceTC) k_wrap_face(
         }
         if (A == 0) return ub[(int64_t)comp * nodes + ((int64_t)gc * N1 + gb) * N0 + ga];
         if (A == 1) return ub[(int64_t)comp * nodes + ((int64_t)gc * N1 + ga) * N0 + gb];
-        return ub[(int64_t)comp * nodes + ((int64_t)ga * N1 + gc) * N0 + gb];
+        // z pass of a halo slab: across an interior face the entry's true
+        // neighbour is ghost plane i of that side (k_wrap_tab's layer order), so
+        // the staged value is alias - ghost and the pass subtracts both at once
+        double v = ub[(int64_t)comp * nodes + ((int64_t)ga * N1 + gc) * N0 + gb];
+        if (ghost && (side == 0 ? lo_int : hi_int))
+            v -= ghost[(int64_t)(b * D + comp) * gs_bc + side * gs_side + (int64_t)i * N0 * N1 + (int64_t)gc * N0 + gb];
+        return v;
     };
     for (int i0 = threadIdx.x; i0 < tot; i0 += 8 * (int)blockDim.x) {
         double v[8];
@@ -733,8 +741,9 @@ static void build_face_table(Engine& e, const std::vector<int>& rows, const std:
     if (e.dim != 3) return;
     // measured: 256^3 wrap + D^e 0.237 -> 0.161 ms; at 128^3 the per-state
     // kernel is as fast (0.081 vs 0.083 ms), so the passes start at 192
+    // (a halo slab's own axis may be short: its z pass covers the full ghost faces)
     for (int a = 0; a < 3; ++a)
-        if (!pl.circ[a] || pl.N[a] < std::max(S, 192)) return;
+        if (!pl.circ[a] || pl.N[a] < (a == 2 && e.slab.global >= 0 ? std::max(S, 2 * M) : std::max(S, 192))) return;
     std::vector<int> fidx;
     std::vector<int4> ftab;
     for (int A = 0; A < 3; ++A)
@@ -932,13 +941,13 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
     const unsigned blocks = (unsigned)((tot + th - 1) / th);
     const double* xstrip = nullptr;
     if (pl.dim == 3 && pl.circ[0] && e.d_xstrip && batch <= e.cap_batch && 4 * e.M <= pl.N[0] &&
-        !(e.d_ftab && !ghost && e.slab.global < 0)) {
+        !(e.d_ftab && !a2a)) {
         const int64_t nrows = (int64_t)batch * 3 * pl.N[1] * pl.N[2];
         k_xstrip<<<(unsigned)((nrows + 255) / 256), 256, 0, s>>>(u, e.d_xstrip, pl.N[0], pl.N[1], pl.N[2], e.M, nrows);
         xstrip = e.d_xstrip;
         e.launches += 1;
     }
-    if (e.d_ftab && !ghost && e.slab.global < 0) {  // 3D, every axis periodic: three tiled face passes
+    if (e.d_ftab && !a2a) {  // 3D, every axis periodic (halo slabs: ghost planes in the z pass): three tiled face passes
         const int M = e.M;
         const size_t smem = sizeof(double) * (size_t)M * 3 * (kFaceTB + 2 * M) * (kFaceTC + 2 * M) +
                             (sizeof(int4) + 6 * sizeof(double)) * (size_t)e.face_rec_max;
@@ -949,13 +958,14 @@ void launch_wrap_correction(Engine& e, const double* u, double* f, int batch, cu
         const int th = kFaceTB * kFaceTC;
         // the surface diagonal folds in when the caller adds the corrections
         // right after (matvec / evaluate_force / CG) and D^e is the lattice's own
-        const bool fold = e.fold_surface_next && e.surf_default;
+        const bool fold = e.fold_surface_next && e.surf_default && !ghost && e.slab.global < 0;
         if (fold) e.surface_folded = true;
         const double* xs = e.xstrip_ready ? e.d_xstrip : nullptr;  // written by this K.u's K1
         e.xstrip_ready = false;
 #define PDGPU_WF(AX, G, FD)                                                                                         \
     k_wrap_face<AX, FD><<<G, th, smem, s>>>(u, f, e.d_fidx, e.d_ftab, e.d_wK, M, N[0], N[1], N[2], cmask, e.d_cmask, \
-                                            pl.nodes, scale, e.face_rec_max, AX == 0 ? xs : nullptr, nullptr)
+                                            pl.nodes, scale, e.face_rec_max, AX == 0 ? xs : nullptr, nullptr,        \
+                                            AX == 2 ? ghost : nullptr, e.ghost_bc_stride, e.ghost_side_stride, lo_int, hi_int)
         const bool xdone = e.xpass_done;  // the x pass ran before K5 (launch_wrap_xpass)
         e.xpass_done = false;
         if (fold) {

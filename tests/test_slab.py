@@ -241,8 +241,10 @@ def _emulated_slabs(dims, K, world, u, dev, constraints=(), halo="ghost"):
 @pytest.mark.gpu
 @pytest.mark.parametrize("halo", ["ghost", "embedded"])
 @pytest.mark.parametrize("dims,world", [((256, 256), 4), ((96, 80), 3), ((24, 20, 32), 4), ((32, 32, 64), 2),
-                                        ((512, 512), 8)])
+                                        ((512, 512), 8), ((256, 256, 64), 4), ((256, 192, 32), 2)])
 def test_slab_engine_gpu(dims, world, halo):
+    # (256, 256, 64) / 4 and (256, 192, 32) / 2: 16-plane slabs of 256-wide planes -- the
+    # first runs the tiled wrap face passes with ghost planes in the z pass
     from oracle.oracle import Rng, random_field
     from paper_2301_11828_b200.engine import FastForce, build_kernel
     dev = torch.device("cuda:0")
