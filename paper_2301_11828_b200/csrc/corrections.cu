@@ -1106,6 +1106,9 @@ struct BondArgs {
     double h, o0, o1, o2;
     double s0;
     double s1sq;  // (1 + s0)^2
+    // tiled 2D test: (1 + s0)^2 h^2 (1 -+ 1e-9), times the offset's integer |o|^2 the
+    // squared-length thresholds of the unambiguous decisions (below)
+    double thr_lo, thr_hi;
     int fast;     // squared-length pre-test enabled (s0 > -1)
     int has_watch;
     double wlo[3], whi[3];
@@ -1261,16 +1264,21 @@ __global__ void __launch_bounds__(256) k_update_bonds_tile2d(const double* __res
             const double r1 = __dsub_rn(pos_rn(A.o1, qy + A.zoff, A.h), xp1);
             const double e0 = __dsub_rn(__dadd_rn(r0, su[0][ty + oy][tx + M + ox]), up0);
             const double e1 = __dsub_rn(__dadd_rn(r1, su[1][ty + oy][tx + M + ox]), up1);
-            double len0 = __dadd_rn(__dadd_rn(0.0, __dmul_rn(r0, r0)), __dmul_rn(r1, r1));
             double len1 = __dadd_rn(__dadd_rn(0.0, __dmul_rn(e0, e0)), __dmul_rn(e1, e1));
+            // Unambiguous decisions against the nominal reference length |o|^2 h^2:
+            // the rounded node positions move |xi|^2 by a few ulp of the largest
+            // coordinate over h (~1e-11 relative on a unit plate at 4096^2), the
+            // reference's own s by a few ulp, so outside the band (1e-9 plus that
+            // bound, launch_update_bonds) the reference decides the same way;
+            // inside it the reference's exact sequence runs (fracture.hpp:17-29, 224).
+            const double n2 = (double)(ox * ox + oy * oy);  // a constant once unrolled
             bool brk;
-            const double thr = A.s1sq * len0;
-            if (A.fast && len1 < thr * (1.0 - 1e-12)) {
+            if (A.fast && len1 < A.thr_lo * n2) {
                 brk = false;
-            } else if (A.fast && len1 > thr * (1.0 + 1e-12)) {
+            } else if (A.fast && len1 > A.thr_hi * n2) {
                 brk = true;
             } else {
-                len0 = __dsqrt_rn(len0);
+                const double len0 = __dsqrt_rn(__dadd_rn(__dadd_rn(0.0, __dmul_rn(r0, r0)), __dmul_rn(r1, r1)));
                 len1 = __dsqrt_rn(len1);
                 brk = __ddiv_rn(__dsub_rn(len1, len0), len0) >= A.s0;
             }
@@ -1351,6 +1359,16 @@ int64_t launch_update_bonds(Engine& e, const double* u, double s0, const double*
     A.o2 = e.origin[2];
     A.s0 = s0;
     A.s1sq = (1.0 + s0) * (1.0 + s0);
+    {
+        // band of the nominal-length decisions: the rounded positions move a bond
+        // component (>= h) by a few ulp of the largest coordinate
+        double xmax = 0.0;
+        for (int d = 0; d < e.dim; ++d)
+            xmax = std::max(xmax, std::fabs(e.origin[d]) + (pl.N[d] + (e.slab.global >= 0 && d == e.dim - 1 ? e.slab.global : 0)) * e.h);
+        const double band = 1e-9 + 32.0 * 2.2204460492503131e-16 * xmax / e.h;
+        A.thr_lo = A.s1sq * A.h * A.h * (1.0 - band);
+        A.thr_hi = A.s1sq * A.h * A.h * (1.0 + band);
+    }
     A.fast = s0 > -1.0 + 1e-6 && !getenv("PDGPU_EXACT_STRETCH");
     A.has_watch = watch != nullptr;
     for (int d = 0; d < 3; ++d) {
