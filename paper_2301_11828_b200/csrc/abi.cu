@@ -1688,6 +1688,8 @@ static void sim_pre(Engine& e) {
     const int64_t N = e.plan.nodes;
     if (e.integrator == 1) {  // ADR branch (timestepping.hpp:215-220)
         launch_adr_step(e, e.step == 0, e.stream);
+    } else if (e.drift_done) {
+        e.drift_done = false;  // done with the previous step's kick (sim_post)
     } else {
         launch_vv_drift(e.d_u, e.d_v, e.d_f, e.d_cmask, N, e.dim, e.dt, 1.0 / e.rho, e.stream);
     }
@@ -1698,8 +1700,20 @@ static void sim_pre(Engine& e) {
 
 static void sim_force(Engine& e) { evaluate_force_impl(e, e.d_u, e.d_f, e.stream); }
 
-static void sim_post(Engine& e, double s0, const double* watch) {
+// fuse_next: another VV step follows in this call and nothing reads the state
+// in between -- the stretch test moves in front (it reads u only), then the
+// kick and the next step's drift run as one kernel (both skip constrained
+// DOFs, which launch_enforce owns)
+static void sim_post(Engine& e, double s0, const double* watch, bool fuse_next = false) {
     const int64_t N = e.plan.nodes;
+    if (e.integrator != 1 && fuse_next) {
+        if (s0 >= 0) launch_update_bonds(e, e.d_u, s0, watch, e.stream, /*sync=*/false);
+        launch_vv_kick_drift(e.d_u, e.d_v, e.d_fprev, e.d_f, e.d_cmask, N, e.dim, e.dt, 1.0 / e.rho, e.stream);
+        launch_enforce(e.d_u, e.d_v, e.d_cdofs, e.d_cval, e.d_ckind, e.n_cdofs, e.t, e.stream);
+        e.drift_done = true;
+        ++e.step;
+        return;
+    }
     if (e.integrator != 1) {
         launch_vv_kick(e.d_v, e.d_fprev, e.d_f, e.d_cmask, N, e.dim, e.dt, 1.0 / e.rho, e.stream);
         launch_enforce(e.d_u, e.d_v, e.d_cdofs, e.d_cval, e.d_ckind, e.n_cdofs, e.t, e.stream);
@@ -1764,11 +1778,13 @@ int pdgpu_sim_step(pdgpu_t h, int n_steps, double s0, const double* watch, int64
         cuda_check(cudaSetDevice(h->device), "set device");
         Engine& e = *h;
         sim_begin(e, n_steps, s0);
+        // single lattice, no monitor: kick + next drift fused (PDGPU_VV_NOFUSE=1: separate kernels)
+        const bool can_fuse = e.integrator != 1 && !e.n_mon && e.slab.global < 0 && !e.nccl_comm && !getenv("PDGPU_VV_NOFUSE");
         for (int i = 0; i < n_steps; ++i) {
             sim_initial_force(e);
             sim_pre(e);
             sim_force(e);
-            sim_post(e, s0, watch);
+            sim_post(e, s0, watch, can_fuse && i + 1 < n_steps);
             if (s0 >= 0) ledger_exchange(e, e.stream);  // NCCL slabs: mirror bonds broken across the face below
             monitor_record(e);
         }

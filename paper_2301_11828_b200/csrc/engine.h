@@ -210,6 +210,7 @@ struct Engine {
     double adr_fixed_c = 0.0;
     int64_t step = 0;
     bool force_ready = false;
+    bool drift_done = false;  // VV: the next step's drift ran fused with this step's kick (k_vv_kick_drift)
     // MonitorWriter nodes (output.hpp:45-72): u at these nodes is gathered on
     // the device after every step into rows [row][node][dim]; the host keeps
     // (step, t) per row and drains them with pdgpu_sim_monitor_read
@@ -409,6 +410,8 @@ void launch_mask_rhs(double* out, const double* b, const double* Auc, const uint
                      int64_t N, int dim, cudaStream_t s);
 void launch_vv_drift(double* u, const double* v, const double* f, const uint8_t* cmask, int64_t N,
                      int dim, double dt, double inv_rho, cudaStream_t s);
+void launch_vv_kick_drift(double* u, double* v, const double* fprev, const double* f, const uint8_t* cmask, int64_t N,
+                          int dim, double dt, double inv_rho, cudaStream_t s);
 void launch_vv_kick(double* v, const double* fprev, const double* f, const uint8_t* cmask,
                     int64_t N, int dim, double dt, double inv_rho, cudaStream_t s);
 void launch_adr_step(Engine& e, bool first, cudaStream_t s);

@@ -515,6 +515,32 @@ void launch_vv_drift(double* u, const double* v, const double* f, const uint8_t*
     check(cudaGetLastError(), "vv_drift");
 }
 
+// kick of step n and drift of step n + 1 in one pass (timestepping.hpp:330-331
+// then :318-319 of the next step): the same operations in the same order, so
+// v and u are bit-identical to k_vv_kick followed by k_vv_drift; six array
+// passes instead of eight
+__global__ void k_vv_kick_drift(double* u, double* v, const double* fprev, const double* f, const uint8_t* cmask,
+                                int64_t N, int dim, double dt, double inv_rho) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N * dim) return;
+    const int a = (int)(i / N);
+    const int64_t p = i - (int64_t)a * N;
+    if ((cmask[p] >> a) & 1u) return;
+    const double fi = f[i];
+    const double t = __dmul_rn(__dmul_rn(__dmul_rn(0.5, dt), __dadd_rn(fprev[i], fi)), inv_rho);
+    const double vn = __dadd_rn(v[i], t);
+    v[i] = vn;
+    const double t1 = __dmul_rn(dt, vn);
+    const double t2 = __dmul_rn(__dmul_rn(__dmul_rn(__dmul_rn(0.5, dt), dt), fi), inv_rho);
+    u[i] = __dadd_rn(u[i], __dadd_rn(t1, t2));
+}
+
+void launch_vv_kick_drift(double* u, double* v, const double* fprev, const double* f, const uint8_t* cmask, int64_t N,
+                          int dim, double dt, double inv_rho, cudaStream_t s) {
+    k_vv_kick_drift<<<blocks_for(N * dim, 256), 256, 0, s>>>(u, v, fprev, f, cmask, N, dim, dt, inv_rho);
+    check(cudaGetLastError(), "vv_kick_drift");
+}
+
 void launch_vv_kick(double* v, const double* fprev, const double* f, const uint8_t* cmask, int64_t N, int dim,
                     double dt, double inv_rho, cudaStream_t s) {
     k_vv_kick<<<blocks_for(N * dim, 256), 256, 0, s>>>(v, fprev, f, cmask, N, dim, dt, inv_rho);
