@@ -14,6 +14,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "engine.h"
@@ -1251,50 +1252,58 @@ __global__ void __launch_bounds__(256) k_update_bonds_tile2d(const double* __res
     const double up0 = su[0][ty][tx + M], up1 = su[1][ty][tx + M];
     const uint32_t word = ledger[p];  // lw == 1 (<= 32 in-band offsets)
     uint32_t newbits = 0;
+    // tiles whose forward halo lies inside the lattice skip the per-bond range
+    // tests (uniform per CTA); a bond is looked at again only if it is live and
+    // not clearly below the threshold, so the common case is branch-free
+    const bool interior = x0 >= M && x0 + TX + M <= A.Nx && y0 + TY + M <= A.Ny;
+    auto sweep = [&](auto interior_c) {
+        constexpr bool INTERIOR = decltype(interior_c)::value;
 #pragma unroll
-    for (int oy = 0; oy <= M; ++oy) {
+        for (int oy = 0; oy <= M; ++oy) {
 #pragma unroll
-        for (int ox = -M; ox <= M; ++ox) {
-            if (ox * ox + oy * oy > M * M || (oy == 0 && ox <= 0)) continue;
-            const int k = band_index2d(M, ox, oy);
-            const int qx = cx + ox, qy = cy + oy;
-            if (qx < 0 || qx >= A.Nx || qy >= A.Ny + A.ghi) continue;
-            if ((word >> k) & 1u) continue;
-            const double r0 = __dsub_rn(pos_rn(A.o0, qx, A.h), xp0);
-            const double r1 = __dsub_rn(pos_rn(A.o1, qy + A.zoff, A.h), xp1);
-            const double e0 = __dsub_rn(__dadd_rn(r0, su[0][ty + oy][tx + M + ox]), up0);
-            const double e1 = __dsub_rn(__dadd_rn(r1, su[1][ty + oy][tx + M + ox]), up1);
-            double len1 = __dadd_rn(__dadd_rn(0.0, __dmul_rn(e0, e0)), __dmul_rn(e1, e1));
-            // Unambiguous decisions against the nominal reference length |o|^2 h^2:
-            // the rounded node positions move |xi|^2 by a few ulp of the largest
-            // coordinate over h (~1e-11 relative on a unit plate at 4096^2), the
-            // reference's own s by a few ulp, so outside the band (1e-9 plus that
-            // bound, launch_update_bonds) the reference decides the same way;
-            // inside it the reference's exact sequence runs (fracture.hpp:17-29, 224).
-            const double n2 = (double)(ox * ox + oy * oy);  // a constant once unrolled
-            bool brk;
-            if (A.fast && len1 < A.thr_lo * n2) {
-                brk = false;
-            } else if (A.fast && len1 > A.thr_hi * n2) {
-                brk = true;
-            } else {
-                const double len0 = __dsqrt_rn(__dadd_rn(__dadd_rn(0.0, __dmul_rn(r0, r0)), __dmul_rn(r1, r1)));
-                len1 = __dsqrt_rn(len1);
-                brk = __ddiv_rn(__dsub_rn(len1, len0), len0) >= A.s0;
+            for (int ox = -M; ox <= M; ++ox) {
+                if (ox * ox + oy * oy > M * M || (oy == 0 && ox <= 0)) continue;
+                const int k = band_index2d(M, ox, oy);
+                const int qx = cx + ox, qy = cy + oy;
+                const bool inb = INTERIOR || (qx >= 0 && qx < A.Nx && qy < A.Ny + A.ghi);
+                const bool live = inb && !((word >> k) & 1u);
+                const double r0 = __dsub_rn(pos_rn(A.o0, qx, A.h), xp0);
+                const double r1 = __dsub_rn(pos_rn(A.o1, qy + A.zoff, A.h), xp1);
+                const double e0 = __dsub_rn(__dadd_rn(r0, su[0][ty + oy][tx + M + ox]), up0);
+                const double e1 = __dsub_rn(__dadd_rn(r1, su[1][ty + oy][tx + M + ox]), up1);
+                double len1 = __dadd_rn(__dadd_rn(0.0, __dmul_rn(e0, e0)), __dmul_rn(e1, e1));
+                // Unambiguous decisions against the nominal reference length |o|^2 h^2:
+                // the rounded node positions move |xi|^2 by a few ulp of the largest
+                // coordinate over h (~1e-11 relative on a unit plate at 4096^2), the
+                // reference's own s by a few ulp, so outside the band (1e-9 plus that
+                // bound, launch_update_bonds) the reference decides the same way;
+                // inside it the reference's exact sequence runs (fracture.hpp:17-29, 224).
+                const double n2 = (double)(ox * ox + oy * oy);  // a constant once unrolled
+                if (!live || (A.fast && len1 < A.thr_lo * n2)) continue;
+                bool brk;
+                if (A.fast && len1 > A.thr_hi * n2) {
+                    brk = true;
+                } else {
+                    const double len0 = __dsqrt_rn(__dadd_rn(__dadd_rn(0.0, __dmul_rn(r0, r0)), __dmul_rn(r1, r1)));
+                    len1 = __dsqrt_rn(len1);
+                    brk = __ddiv_rn(__dsub_rn(len1, len0), len0) >= A.s0;
+                }
+                if (!brk) continue;
+                newbits |= 1u << k;
+                const int64_t q = p + (int64_t)oy * A.Nx + ox;
+                const bool local = qy < A.Ny;  // else the next slab's node: its bit arrives by the face merge
+                if (local) atomicOr(&ledger[q], 1u << band_index2d(M, -ox, -oy));
+                const unsigned long long slot = atomicAdd(&counters[1], 1ull);
+                if ((int64_t)slot < cap) {
+                    new_pairs[2 * slot] = p;
+                    new_pairs[2 * slot + 1] = k;
+                }
+                if (local && atomicExch(&listed[q], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = q;
             }
-            if (!brk) continue;
-            newbits |= 1u << k;
-            const int64_t q = p + (int64_t)oy * A.Nx + ox;
-            const bool local = qy < A.Ny;  // else the next slab's node: its bit arrives by the face merge
-            if (local) atomicOr(&ledger[q], 1u << band_index2d(M, -ox, -oy));
-            const unsigned long long slot = atomicAdd(&counters[1], 1ull);
-            if ((int64_t)slot < cap) {
-                new_pairs[2 * slot] = p;
-                new_pairs[2 * slot + 1] = k;
-            }
-            if (local && atomicExch(&listed[q], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = q;
         }
-    }
+    };
+    if (interior) sweep(std::true_type{});
+    else sweep(std::false_type{});
     if (newbits) {
         atomicOr(&ledger[p], newbits);
         if (atomicExch(&listed[p], 1) == 0) bond_rows[atomicAdd(&counters[0], 1ull)] = p;
