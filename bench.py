@@ -608,7 +608,8 @@ def run_slab(args):
     py = R if periodic else 2 * R
     spec = DIM * hx * R * 16
     own = DIM * N_SIDE * R * 8
-    pbytes = {"K1_rfft_x": BATCH * (own + spec), "K3_spectral": BATCH * 2 * spec + 3 * hx * py * 8,
+    sym = min(3 * hx * py * 8, ff.symbol_stream_bytes())  # the symbol bytes K3 streams (full table or mirror planes)
+    pbytes = {"K1_rfft_x": BATCH * (own + spec), "K3_spectral": BATCH * 2 * spec + sym,
               "K5_irfft_x": BATCH * (spec + own)}
     per_pass = {}
     for k, b in pbytes.items():
