@@ -271,23 +271,38 @@ __device__ __forceinline__ FftTw make_fft_tw(int t, const double2* __restrict__ 
     return r;
 }
 
-// The same bases from a shared-memory copy of the only table entries the
-// passes use: base of pass p = tw[k << (logTWN - logns - lr)], k < 2^logns,
-// which are all multiples of the last pass's stride, so a table of
-// Q / r_last entries (stw[i] = tw[i << (logTWN - LOGQ)]) serves every pass.
+// The same bases from shared memory: one compact table per twiddled pass
+// (pass p: 2^logns entries, entry k = tw[k << (logTWN - logns - lr)]), laid
+// out back to back, so a warp's loads are consecutive 16-byte entries.  (A
+// single table of Q / r_last entries read at the pass's stride put pass 1's
+// sixteen entries 256 bytes apart -- an eight-way bank conflict per load.)
 // Persistent kernels re-derive the bases per transform (registers); reading
 // them from SMEM instead of the global table keeps an L2 round trip (the L1
 // is mostly carved out for shared memory) off the start of every transform.
 template <int LOGQ, int LOGRMAX>
 struct FftTwTable {
     using Sh = FftShape<LOGQ, LOGRMAX>;
-    static constexpr int LR_LAST = Sh::LOGREM ? Sh::LOGREM : Sh::LOGR;
-    static constexpr int SIZE = Sh::NPASS > 1 ? (1 << (LOGQ - LR_LAST)) : 1;
+    // entries of passes 1 .. p-1
+    static constexpr int offset(int p) {
+        int o = 0;
+        for (int q = 1; q < p; ++q) o += 1 << (q * Sh::LOGR);
+        return o;
+    }
+    static constexpr int SIZE = Sh::NPASS > 1 ? offset(Sh::NPASS) : 1;
 };
 
 template <int LOGQ, int LOGRMAX>
 __device__ __forceinline__ void fill_fft_tw_table(double2* stw, const double2* __restrict__ tw, int logTWN) {
-    for (int i = threadIdx.x; i < FftTwTable<LOGQ, LOGRMAX>::SIZE; i += blockDim.x) stw[i] = __ldg(tw + (i << (logTWN - LOGQ)));
+    using Sh = FftShape<LOGQ, LOGRMAX>;
+#pragma unroll
+    for (int p = 1; p < 4; ++p) {
+        if (p < Sh::NPASS) {
+            const int logns = p * Sh::LOGR;
+            const int lr = (p == Sh::NPASS - 1 && Sh::LOGREM) ? Sh::LOGREM : Sh::LOGR;
+            for (int k = threadIdx.x; k < (1 << logns); k += blockDim.x)
+                stw[FftTwTable<LOGQ, LOGRMAX>::offset(p) + k] = __ldg(tw + (k << (logTWN - logns - lr)));
+        }
+    }
 }
 
 template <int LOGQ, int LOGRMAX>
@@ -299,9 +314,8 @@ __device__ __forceinline__ FftTw make_fft_tw_s(int t, const double2* stw) {
         r.w[p - 1] = make_double2(1.0, 0.0);
         if (p < Sh::NPASS) {
             const int logns = p * Sh::LOGR;
-            const int lr = (p == Sh::NPASS - 1 && Sh::LOGREM) ? Sh::LOGREM : Sh::LOGR;
             const int k = t & ((1 << logns) - 1);
-            r.w[p - 1] = stw[k << (LOGQ - logns - lr)];
+            r.w[p - 1] = stw[FftTwTable<LOGQ, LOGRMAX>::offset(p) + k];
         }
     }
     return r;
