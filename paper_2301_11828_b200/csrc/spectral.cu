@@ -756,6 +756,15 @@ __device__ __forceinline__ void symbol_product(double2* F, const double2* U, con
             asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
                 : "=d"(g[0]), "=d"(g[1]), "=d"(g[2]), "=d"(g[3])
                 : "l"(H));
+        } else if constexpr (NP % 2 == 0) {
+            // 3D: six doubles per frequency, 48 bytes: three 16-byte loads
+            const double2* H2 = reinterpret_cast<const double2*>((const double*)sym + fidx * NP);
+#pragma unroll
+            for (int p = 0; p < NP / 2; ++p) {
+                const double2 h2 = __ldg(H2 + p);
+                g[2 * p] = h2.x;
+                g[2 * p + 1] = h2.y;
+            }
         } else {
             const double* H = (const double*)sym + fidx * NP;
 #pragma unroll
