@@ -2955,6 +2955,7 @@ static void set_attrs_3d_l() {
         smem_attr((const void*)k_spectral<L, 3, true, 3, false, false, 1>);
         smem_attr((const void*)k_spectral<L, 3, false, 3, false, false, 1>);
         smem_attr((const void*)k_spectral<L, 3, true, 3, false, true, 1>);
+        if constexpr (L == 7 || L == 8) smem_attr((const void*)k_spectral<L, 3, true, 4, false, false, 1>);
     }
 }
 template <int... Ls>
@@ -3022,7 +3023,17 @@ void launch_k3_3d(Engine& e, double2* spec, int batch, cudaStream_t s) {
             PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, true, 3, true, true><<<sgrid, NCs * T, per_col * NCs, s>>>(
                                          spec, spec, e.d_sym, pl.ncols, pl.Nl, NCs, e.d_tw, pl.logTWN, ct, M, om)))
     } else if (e.real_symbol) {
-        if (nh == 1)
+        // 128/256-point periodic columns: 16 points per thread (256 = 16 x 16: one exchange
+        // per transform instead of the two of 8 x 8 x 4); PDGPU_K3_3D_R8=1: 8 points per thread
+        if (nh == 1 && (lq == 8 || lq == 7) && !getenv("PDGPU_K3_3D_R8")) {
+            const int T16 = threads_per_transform(lq, 4);
+            if (lq == 8)
+                k_spectral<8, 3, true, 4, false, false, 1><<<grid, NC * T16, smem, s>>>(spec, spec, e.d_sym, pl.ncols, pl.Nl,
+                                                                                       NC, e.d_tw, pl.logTWN);
+            else
+                k_spectral<7, 3, true, 4, false, false, 1><<<grid, NC * T16, smem, s>>>(spec, spec, e.d_sym, pl.ncols, pl.Nl,
+                                                                                       NC, e.d_tw, pl.logTWN);
+        } else if (nh == 1)
             PDGPU_DISPATCH_LOGQ9(lq, (k_spectral<LQ, 3, true, 3, false, false, 1><<<grid, NC * T, smem, s>>>(
                                          spec, spec, e.d_sym, pl.ncols, pl.Nl, NC, e.d_tw, pl.logTWN)))
         else
